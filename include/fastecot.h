@@ -1,0 +1,102 @@
+/*
+ * fastecot.h -- C ABI of the B200 Fast-ECoT engine (libfastecot.so).
+ *
+ * The reference has no FFI: its hot path crosses one Python protocol,
+ * `GenerationBackend` (pkg/src/ecot_sched/backends.py:98-110), whose
+ * `begin_step(context, prefix, step, prev_content)` the runners call through
+ * `_generate_step` (schedulers.py:217-225).  These entry points are what a
+ * backend implementing that protocol binds (ctypes in
+ * paper_2506_07639_b200/engine.py; a cgo/JNI/N-API stub would bind the same
+ * symbols):
+ *
+ *   encode(instruction, observation)     -> fe_prefill of the context trunk
+ *                                           (backends.py:102, :113-117)
+ *   begin_step(ctx, prefix, step, prev)  -> fe_seq_fork + fe_prefill of the
+ *                                           uncached prefix + fe_submit +
+ *                                           fe_run + fe_request_tokens
+ *                                           (backends.py:104-110)
+ *   StepGenerator.drain()                -> fe_request_tokens (backends.py:93-95)
+ *   runner-level batching                -> fe_submit / fe_run: continuous
+ *     (_MicroEngine, schedulers.py:244-299;  batcher with the reference's
+ *      ParallelSync fan-out :399-420)        action-first admission
+ *
+ * Conventions: every function returns 0 on success and a non-zero status on
+ * failure, with a message retrievable through fe_last_error() (thread-local).
+ * No C++ exceptions cross the ABI.  Host pointers are caller-owned; the
+ * engine owns weights, the paged KV pool and its work buffers.  All device
+ * work is ordered on the engine's CUDA stream; only fe_request_tokens,
+ * fe_request_logits and fe_synchronize block the host.
+ */
+#ifndef FASTECOT_H
+#define FASTECOT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct fe_engine fe_engine;
+
+enum { FE_F32 = 0, FE_BF16 = 1 };
+enum { FE_PRIO_ACTION = 0, FE_PRIO_REASONING = 1 };  /* batching.py:21-22 */
+
+typedef struct fe_config {
+  int32_t d_model, n_layers, n_heads, head_dim, d_ffn;
+  int32_t vocab;        /* rows of embed / lm_head */
+  int32_t n_text;       /* greedy argmax range [0, n_text) */
+  int32_t max_pos;      /* rows of the RoPE table */
+  float rms_eps;
+  float attn_scale;     /* 1/sqrt(head_dim) as fp32 */
+  int32_t dtype;        /* FE_F32 (canonical, bit-exact) or FE_BF16 */
+  int32_t max_rows;     /* rows per forward pass (prefill chunk) */
+  int32_t kv_pages;     /* 64-token pages in the KV pool; 0 = size from free memory */
+  int32_t max_slots;    /* capacity of the continuous batcher */
+} fe_config;
+
+/* engine lifetime; `rope` = host [max_pos][2][head_dim/2] fp32 (cos, sin) */
+int fe_engine_create(const fe_config* cfg, int32_t device, const float* rope, fe_engine** out);
+int fe_engine_destroy(fe_engine* e);
+int fe_weights_init_random(fe_engine* e, uint64_t seed);
+const char* fe_last_error(void);
+
+/* paged KV sequences (64-token pages, refcounted, copy-on-write at forks) */
+int fe_seq_create(fe_engine* e, int32_t* seq);
+int fe_seq_fork(fe_engine* e, int32_t parent, int32_t len, int32_t* child);
+int fe_seq_free(fe_engine* e, int32_t seq);
+int fe_seq_len(fe_engine* e, int32_t seq, int32_t* len);
+
+/* append n input ids to `seq` (positions len .. len+n-1); ids equal to
+ * `vis_id` take row (pos-1) of the vision embedding seeded by `vision_seed` */
+int fe_prefill(fe_engine* e, int32_t seq, const int32_t* ids, int32_t n, uint64_t vision_seed, int32_t vis_id);
+
+/* continuous batcher: a request decodes `length` greedy tokens on `seq`,
+ * the first iteration consuming `first_id` */
+int fe_set_slots(fe_engine* e, int32_t slots);
+int fe_submit(fe_engine* e, int32_t seq, int32_t first_id, int32_t length, int32_t priority, int32_t* req);
+/* run decode iterations until request `stop_req` completes (-1: until idle);
+ * per tick: occupancy[t]; completions in order: completed[i] at tick
+ * completed_tick[i].  Arrays need room for `cap` entries. */
+int fe_run(fe_engine* e, int32_t stop_req, int32_t cap, int32_t* n_ticks, int32_t* occupancy,
+           int32_t* completed, int32_t* completed_tick, int32_t* n_completed);
+int fe_request_tokens(fe_engine* e, int32_t req, int32_t* out, int32_t cap);
+int fe_request_release(fe_engine* e, int32_t req);
+int fe_request_capture_logits(fe_engine* e, int32_t req);  /* parity mode: keep fp32 logits */
+int fe_request_logits(fe_engine* e, int32_t req, float* out, int32_t rows);
+int fe_in_flight(fe_engine* e, int32_t* n);
+
+int fe_synchronize(fe_engine* e);
+int fe_stream(fe_engine* e, void** stream);
+int fe_stats(fe_engine* e, int64_t* out, int32_t n);  /* ticks, forwards, launches, pages used, ... */
+
+/* kernel-level entry points (device pointers, engine stream), for parity tests */
+int fe_weight_ptr(fe_engine* e, int32_t tensor, int32_t layer, void** ptr, size_t* bytes);
+int fe_memcpy(fe_engine* e, void* dst, const void* src, size_t bytes);  /* any direction, synchronous */
+int fe_op_gemv(fe_engine* e, const void* w, int32_t N, int32_t K, const void* x, int32_t rows, float* y);
+int fe_op_rmsnorm(fe_engine* e, const float* x, const float* w, void* out, int32_t rows, int32_t d);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FASTECOT_H */

@@ -1,0 +1,764 @@
+// Host side of the Fast-ECoT B200 engine: weights, paged KV pool, forward
+// passes, the continuous batcher and the C ABI (include/fastecot.h).
+//
+// Reference anchors: the batcher's admission policy restates the simulated
+// `_MicroEngine.tick` (pkg/src/ecot_sched/schedulers.py:277-299: admit
+// waiting requests into free slots, action class first then FIFO by seqno;
+// every occupied slot emits one token per tick; a slot freed at tick k is
+// reusable at k+1).  Token generation itself has no reference counterpart
+// (SPEC.md:166, :250): it is the decoder of DESIGN.md.
+#include "common.cuh"
+#include "engine_internal.h"
+#include "../../include/fastecot.h"
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct Error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define CK(x)                                                                              \
+  do {                                                                                     \
+    cudaError_t _e = (x);                                                                  \
+    if (_e != cudaSuccess)                                                                 \
+      throw Error(std::string(#x) + ": " + cudaGetErrorString(_e) + " @" + std::to_string(__LINE__)); \
+  } while (0)
+
+constexpr int kRequestCap = 1024;   // tokens per request (out_tokens arena slot)
+constexpr int kMetaRing = 4;
+constexpr int kItemRows = 16;       // query rows per cascade work item
+constexpr int kLogitRows = 256;
+
+struct Seq {
+  std::vector<int> pages;
+  int len = 0;
+  bool live = false;
+};
+
+struct Request {
+  int seq = -1;
+  int first_id = 0;
+  int length = 0;
+  int produced = 0;
+  int priority = 1;
+  uint64_t seqno = 0;
+  int arena = -1;
+  int state = 0;      // 0 waiting, 1 running, 2 done, 3 released
+  bool capture = false;
+  bool live = false;
+};
+
+struct RowIn {
+  int seq, pos, tok, tok_src, vis_row, out_idx, logit_row;
+  bool head;
+};
+
+}  // namespace
+
+struct fe_engine {
+  fe::ModelDims m{};
+  int dtype = 0;
+  int device = 0;
+  size_t elem = 4;
+  int max_rows = 0;
+  int max_slots = 0;
+  int slots = 8;
+  cudaStream_t stream = nullptr;
+  std::mutex mu;
+
+  // weights
+  std::vector<void*> allocs;
+  fe::Weights w{};
+  std::vector<fe::Weights::Layer> layers;
+  float* rope = nullptr;
+
+  // KV pool
+  void* kv_pool = nullptr;
+  int n_pages = 0;
+  size_t page_elems = 0;
+  std::vector<int> page_ref;
+  std::vector<int> free_pages;
+  std::vector<Seq> seqs;
+  std::vector<int> free_seqs;
+
+  // work buffers
+  fe::Workspace ws{};
+  int max_partials = 0;
+  int max_items = 0;
+  size_t meta_bytes = 0;
+  unsigned char* meta_host[kMetaRing] = {};
+  cudaEvent_t meta_ev[kMetaRing] = {};
+  int meta_next = 0;
+
+  // batcher
+  std::vector<Request> reqs;
+  std::vector<int> free_reqs;
+  std::vector<int> slot_req;
+  std::vector<int> waiting;
+  uint64_t seqno = 0;
+  std::vector<int> free_arena;
+  int capture_req = -1;
+
+  // stats
+  int64_t n_ticks = 0, n_forwards = 0, n_rows_total = 0;
+
+  void* dalloc(size_t bytes) {
+    void* p = nullptr;
+    CK(cudaMalloc(&p, bytes));
+    allocs.push_back(p);
+    return p;
+  }
+};
+
+namespace {
+
+int alloc_page(fe_engine* e) {
+  if (e->free_pages.empty()) throw Error("KV pool exhausted (" + std::to_string(e->n_pages) + " pages)");
+  int p = e->free_pages.back();
+  e->free_pages.pop_back();
+  e->page_ref[p] = 1;
+  return p;
+}
+
+void release_page(fe_engine* e, int p) {
+  if (--e->page_ref[p] == 0) e->free_pages.push_back(p);
+}
+
+Seq& seq_at(fe_engine* e, int s) {
+  if (s < 0 || s >= (int)e->seqs.size() || !e->seqs[s].live) throw Error("invalid sequence " + std::to_string(s));
+  return e->seqs[s];
+}
+
+int new_seq(fe_engine* e) {
+  int s;
+  if (!e->free_seqs.empty()) {
+    s = e->free_seqs.back();
+    e->free_seqs.pop_back();
+  } else {
+    s = (int)e->seqs.size();
+    e->seqs.emplace_back();
+  }
+  e->seqs[s] = Seq();
+  e->seqs[s].live = true;
+  return s;
+}
+
+// Pinned staging buffer for one forward's metadata; waits for the buffer's
+// previous H2D copy to finish before reuse.
+unsigned char* next_meta(fe_engine* e, int* idx) {
+  int i = e->meta_next;
+  e->meta_next = (i + 1) % kMetaRing;
+  CK(cudaEventSynchronize(e->meta_ev[i]));
+  *idx = i;
+  return e->meta_host[i];
+}
+
+// One forward pass over `rows` (all positions must already be < seq.len+1 in
+// order).  Builds row metadata, the cascade work list and launches the layer
+// stack.  Host-side sequence lengths advance as rows are written.
+void forward(fe_engine* e, const std::vector<RowIn>& rows, uint64_t vision_seed) {
+  const fe::ModelDims& m = e->m;
+  const int n = (int)rows.size();
+  if (n == 0) return;
+  if (n > e->max_rows) throw Error("forward: too many rows");
+
+  std::vector<fe::RowMeta> meta(n);
+  std::vector<int32_t> head_rows;
+  int chunk_total = 0;
+  for (int i = 0; i < n; i++) {
+    const RowIn& r = rows[i];
+    Seq& s = seq_at(e, r.seq);
+    if (r.pos != s.len) throw Error("forward: non-contiguous append");
+    if (r.pos >= m.max_pos) throw Error("forward: position beyond max_pos");
+    const int pg = r.pos / FE_PAGE;
+    if (pg == (int)s.pages.size()) s.pages.push_back(alloc_page(e));
+    if (e->page_ref[s.pages[pg]] != 1) throw Error("forward: write into a shared page");
+    s.len = r.pos + 1;
+    fe::RowMeta& mm = meta[i];
+    mm.pos = r.pos;
+    mm.tok = r.tok;
+    mm.tok_src = r.tok_src;
+    mm.vis_row = r.vis_row;
+    mm.kv_page = s.pages[pg];
+    mm.kv_slot = r.pos % FE_PAGE;
+    mm.out_idx = r.out_idx;
+    mm.chunk_base = chunk_total;
+    mm.n_chunks = pg + 1;
+    mm.logit_row = r.logit_row;
+    mm.head_row = -1;
+    chunk_total += pg + 1;
+    if (r.head) {
+      mm.head_row = (int)head_rows.size();
+      head_rows.push_back(i);
+    }
+  }
+  if (chunk_total > e->max_partials) throw Error("forward: partial workspace too small");
+
+  // cascade work list: group rows by the physical page their chunk maps to.
+  // Rows sharing a trunk point at the same pages, so each shared page is
+  // staged once per (page, head) CTA and serves all of them.
+  std::map<int, std::vector<std::pair<int, int>>> by_page;  // page -> (row, valid)
+  std::unordered_map<int, int> page_chunk;
+  for (int i = 0; i < n; i++) {
+    const Seq& s = e->seqs[rows[i].seq];
+    const int pos = rows[i].pos;
+    for (int c = 0; c <= pos / FE_PAGE; c++) {
+      const int pg = s.pages[c];
+      by_page[pg].push_back({i, std::min(FE_PAGE, pos + 1 - c * FE_PAGE)});
+      page_chunk[pg] = c;
+    }
+  }
+  std::vector<fe::AttnItem> items;
+  std::vector<fe::ItemRow> irows;
+  for (auto& kv : by_page) {
+    const auto& lst = kv.second;
+    for (size_t b = 0; b < lst.size(); b += kItemRows) {
+      fe::AttnItem it;
+      it.page = kv.first;
+      it.chunk = page_chunk[kv.first];
+      it.row_begin = (int)irows.size();
+      it.row_count = (int)std::min<size_t>(kItemRows, lst.size() - b);
+      for (int j = 0; j < it.row_count; j++) irows.push_back({lst[b + j].first, lst[b + j].second});
+      items.push_back(it);
+    }
+  }
+  if ((int)items.size() > e->max_items) throw Error("forward: too many attention items");
+
+  // pack metadata into one pinned buffer -> one H2D copy
+  const size_t o_rows = 0;
+  const size_t o_items = o_rows + sizeof(fe::RowMeta) * n;
+  const size_t o_irows = o_items + sizeof(fe::AttnItem) * items.size();
+  const size_t o_heads = o_irows + sizeof(fe::ItemRow) * irows.size();
+  const size_t total = o_heads + sizeof(int32_t) * head_rows.size();
+  if (total > e->meta_bytes) throw Error("forward: metadata buffer too small");
+  int mi;
+  unsigned char* hbuf = next_meta(e, &mi);
+  std::memcpy(hbuf + o_rows, meta.data(), sizeof(fe::RowMeta) * n);
+  if (!items.empty()) std::memcpy(hbuf + o_items, items.data(), sizeof(fe::AttnItem) * items.size());
+  if (!irows.empty()) std::memcpy(hbuf + o_irows, irows.data(), sizeof(fe::ItemRow) * irows.size());
+  if (!head_rows.empty()) std::memcpy(hbuf + o_heads, head_rows.data(), sizeof(int32_t) * head_rows.size());
+  unsigned char* dbuf = (unsigned char*)e->ws.meta;
+  CK(cudaMemcpyAsync(dbuf, hbuf, total, cudaMemcpyHostToDevice, e->stream));
+  CK(cudaEventRecord(e->meta_ev[mi], e->stream));
+
+  fe::Fwd f{};
+  f.rows = (const fe::RowMeta*)(dbuf + o_rows);
+  f.n_rows = n;
+  f.items = (const fe::AttnItem*)(dbuf + o_items);
+  f.n_items = (int)items.size();
+  f.item_rows = (const fe::ItemRow*)(dbuf + o_irows);
+  f.n_head_rows = (int)head_rows.size();
+  f.head_rows = (const int32_t*)(dbuf + o_heads);
+  f.vision_key = fe::tensor_key(vision_seed, 4 /* T_VISION */);
+
+  cudaStream_t st = e->stream;
+  const int dt = e->dtype;
+  fe::launch_embed(dt, f, m, e->w.embed, e->ws.out_tokens, e->ws.x, st);
+  for (int l = 0; l < m.L; l++) {
+    const fe::Weights::Layer& ly = e->layers[l];
+    fe::launch_rmsnorm(dt, e->ws.x, ly.attn_norm, e->ws.xn, n, m.d, m.d, m.eps, nullptr, st);
+    fe::launch_qkv(dt, f, m, ly.wqkv, e->ws.xn, e->ws.q, e->kv_pool, l, e->rope, st);
+    fe::launch_attention(dt, f, m, e->ws.q, e->kv_pool, l, e->ws.partial, e->ws.attn, st);
+    fe::launch_resid(dt, f, m.d, m.d, ly.wo, e->ws.attn, e->ws.x, st);
+    fe::launch_rmsnorm(dt, e->ws.x, ly.ffn_norm, e->ws.xn, n, m.d, m.d, m.eps, nullptr, st);
+    fe::launch_swiglu(dt, f, m.F, m.d, ly.wgu, e->ws.xn, e->ws.attn /* reused as the SwiGLU activation */, st);
+    fe::launch_resid(dt, f, m.d, m.F, ly.wdown, e->ws.attn, e->ws.x, st);
+  }
+  if (f.n_head_rows > 0) {
+    fe::launch_rmsnorm(dt, e->ws.x, e->w.final_norm, e->ws.xn, f.n_head_rows, m.d, m.d, m.eps, f.head_rows, st);
+    fe::launch_lm_head(dt, f, m, e->w.lm_head, e->ws.xn, e->ws.part_keys, e->ws.logits, e->ws.out_tokens, st);
+  }
+  CK(cudaGetLastError());
+  e->n_forwards++;
+  e->n_rows_total += n;
+}
+
+void prefill(fe_engine* e, int seq, const int32_t* ids, int n, uint64_t vseed, int vis_id) {
+  Seq& s = seq_at(e, seq);
+  int pos = s.len;
+  int i = 0;
+  while (i < n) {
+    std::vector<RowIn> rows;
+    int chunks = 0;
+    while (i < n && (int)rows.size() < e->max_rows) {
+      const int c = pos / FE_PAGE + 1;
+      if (chunks + c > e->max_partials && !rows.empty()) break;
+      RowIn r{};
+      r.seq = seq;
+      r.pos = pos;
+      r.tok = ids[i] == vis_id ? -1 : ids[i];
+      r.tok_src = -1;
+      r.vis_row = ids[i] == vis_id ? pos - 1 : -1;
+      if (ids[i] == vis_id && pos < 1) throw Error("prefill: vision placeholder at position 0");
+      if (ids[i] != vis_id && (ids[i] < 0 || ids[i] >= e->m.V)) throw Error("prefill: token id out of range");
+      r.out_idx = -1;
+      r.logit_row = -1;
+      r.head = false;
+      rows.push_back(r);
+      chunks += c;
+      pos++;
+      i++;
+    }
+    forward(e, rows, vseed);
+  }
+}
+
+int new_request_slot(fe_engine* e) {
+  int r;
+  if (!e->free_reqs.empty()) {
+    r = e->free_reqs.back();
+    e->free_reqs.pop_back();
+  } else {
+    r = (int)e->reqs.size();
+    e->reqs.emplace_back();
+  }
+  return r;
+}
+
+Request& req_at(fe_engine* e, int r) {
+  if (r < 0 || r >= (int)e->reqs.size() || !e->reqs[r].live) throw Error("invalid request " + std::to_string(r));
+  return e->reqs[r];
+}
+
+// One decode iteration (= one tick of the reference _MicroEngine).
+int tick(fe_engine* e, std::vector<int>* completed) {
+  // admission: action class first, then FIFO by seqno (schedulers.py:279-285)
+  if (!e->waiting.empty()) {
+    std::stable_sort(e->waiting.begin(), e->waiting.end(), [&](int a, int b) {
+      const Request &ra = e->reqs[a], &rb = e->reqs[b];
+      if (ra.priority != rb.priority) return ra.priority < rb.priority;
+      return ra.seqno < rb.seqno;
+    });
+    for (int s = 0; s < e->slots && !e->waiting.empty(); s++) {
+      if (e->slot_req[s] < 0) {
+        e->slot_req[s] = e->waiting.front();
+        e->reqs[e->waiting.front()].state = 1;
+        e->waiting.erase(e->waiting.begin());
+      }
+    }
+  }
+  std::vector<RowIn> rows;
+  for (int s = 0; s < e->slots; s++) {
+    const int ri = e->slot_req[s];
+    if (ri < 0) continue;
+    Request& q = e->reqs[ri];
+    RowIn r{};
+    r.seq = q.seq;
+    r.pos = e->seqs[q.seq].len;
+    r.tok = q.produced == 0 ? q.first_id : -1;
+    r.tok_src = q.produced == 0 ? -1 : q.arena * kRequestCap + q.produced - 1;
+    r.vis_row = -1;
+    r.out_idx = q.arena * kRequestCap + q.produced;
+    r.logit_row = (q.capture && q.produced < kLogitRows) ? q.produced : -1;
+    r.head = true;
+    rows.push_back(r);
+  }
+  const int occupied = (int)rows.size();
+  forward(e, rows, 0);
+  for (int s = 0; s < e->slots; s++) {
+    const int ri = e->slot_req[s];
+    if (ri < 0) continue;
+    Request& q = e->reqs[ri];
+    if (++q.produced == q.length) {
+      q.state = 2;
+      e->slot_req[s] = -1;
+      completed->push_back(ri);
+    }
+  }
+  e->n_ticks++;
+  return occupied;
+}
+
+void init_weights(fe_engine* e, uint64_t seed) {
+  const fe::ModelDims& m = e->m;
+  cudaStream_t st = e->stream;
+  const size_t d = m.d, F = m.F, V = m.V;
+  auto key = [&](uint64_t tid) { return fe::tensor_key(seed, tid); };
+  fe::launch_init_linear(e->dtype, e->w.embed, key(1), V * d, st);
+  fe::launch_init_linear(e->dtype, e->w.lm_head, key(2), V * d, st);
+  fe::launch_init_norm(e->w.final_norm, key(3), d, st);
+  for (int l = 0; l < m.L; l++) {
+    const uint64_t b = 16 + 16 * (uint64_t)l;
+    fe::Weights::Layer& ly = e->layers[l];
+    char* qkv = (char*)ly.wqkv;
+    char* gu = (char*)ly.wgu;
+    fe::launch_init_norm(ly.attn_norm, key(b + 0), d, st);
+    fe::launch_init_linear(e->dtype, qkv, key(b + 1), d * d, st);
+    fe::launch_init_linear(e->dtype, qkv + d * d * e->elem, key(b + 2), d * d, st);
+    fe::launch_init_linear(e->dtype, qkv + 2 * d * d * e->elem, key(b + 3), d * d, st);
+    fe::launch_init_linear(e->dtype, ly.wo, key(b + 4), d * d, st);
+    fe::launch_init_norm(ly.ffn_norm, key(b + 5), d, st);
+    fe::launch_init_linear(e->dtype, gu, key(b + 6), F * d, st);
+    fe::launch_init_linear(e->dtype, gu + F * d * e->elem, key(b + 7), F * d, st);
+    fe::launch_init_linear(e->dtype, ly.wdown, key(b + 8), d * F, st);
+  }
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(st));
+}
+
+fe_engine* create(const fe_config* c, int device, const float* rope_host) {
+  if (c->head_dim != 64 && c->head_dim != 128) throw Error("head_dim must be 64 or 128");
+  if (c->n_heads * c->head_dim != c->d_model) throw Error("n_heads * head_dim != d_model");
+  if (c->d_model % 8 || c->d_ffn % 8 || c->vocab % 4) throw Error("dimensions must be multiples of 8");
+  if (c->dtype != FE_F32 && c->dtype != FE_BF16) throw Error("dtype must be FE_F32 or FE_BF16");
+  auto* e = new fe_engine();
+  try {
+    e->device = device;
+    CK(cudaSetDevice(device));
+    e->m = {c->d_model, c->n_layers, c->n_heads, c->head_dim, c->d_ffn, c->vocab, c->n_text, c->max_pos,
+            c->rms_eps, c->attn_scale};
+    e->dtype = c->dtype;
+    e->elem = c->dtype == FE_F32 ? 4 : 2;
+    e->max_rows = c->max_rows > 0 ? c->max_rows : 512;
+    e->max_slots = c->max_slots > 0 ? c->max_slots : 64;
+    e->slots = std::min(8, e->max_slots);
+    CK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+    const fe::ModelDims& m = e->m;
+    const size_t d = m.d, F = m.F, V = m.V, el = e->elem;
+
+    e->w.embed = e->dalloc(V * d * el);
+    e->w.lm_head = e->dalloc(V * d * el);
+    e->w.final_norm = (float*)e->dalloc(d * 4);
+    e->layers.resize(m.L);
+    for (int l = 0; l < m.L; l++) {
+      auto& ly = e->layers[l];
+      ly.attn_norm = (float*)e->dalloc(d * 4);
+      ly.ffn_norm = (float*)e->dalloc(d * 4);
+      ly.wqkv = e->dalloc(3 * d * d * el);
+      ly.wo = e->dalloc(d * d * el);
+      ly.wgu = e->dalloc(2 * F * d * el);
+      ly.wdown = e->dalloc(d * F * el);
+    }
+    e->w.layers = e->layers.data();
+    e->rope = (float*)e->dalloc(sizeof(float) * (size_t)m.max_pos * m.hd);
+    CK(cudaMemcpy(e->rope, rope_host, sizeof(float) * (size_t)m.max_pos * m.hd, cudaMemcpyHostToDevice));
+
+    // work buffers
+    const size_t R = e->max_rows;
+    e->ws.x = (float*)e->dalloc(R * d * 4);
+    e->ws.xn = e->dalloc(R * std::max(d, F) * el);
+    e->ws.q = (float*)e->dalloc(R * d * 4);
+    e->ws.attn = e->dalloc(R * std::max(d, F) * el);
+    e->max_partials = (int)std::min<size_t>(R * (size_t)(m.max_pos / FE_PAGE), 65536);
+    e->max_items = e->max_partials;
+    e->ws.partial = (float*)e->dalloc((size_t)e->max_partials * m.H * (m.hd + 2) * 4);
+    e->ws.part_keys = (unsigned long long*)e->dalloc(R * (size_t)fe::lm_head_ctas(m) * 8);
+    e->ws.logits = (float*)e->dalloc((size_t)kLogitRows * V * 4);
+    const int n_arena = std::max(4 * e->max_slots, 256);
+    e->ws.out_tokens = (int32_t*)e->dalloc((size_t)n_arena * kRequestCap * 4);
+    CK(cudaMemset(e->ws.out_tokens, 0, (size_t)n_arena * kRequestCap * 4));
+    for (int i = n_arena - 1; i >= 0; i--) e->free_arena.push_back(i);
+    e->meta_bytes = R * sizeof(fe::RowMeta) + (size_t)e->max_items * sizeof(fe::AttnItem) +
+                    (size_t)e->max_partials * sizeof(fe::ItemRow) + R * 4 + 4096;
+    e->ws.meta = e->dalloc(e->meta_bytes);
+    for (int i = 0; i < kMetaRing; i++) {
+      CK(cudaMallocHost((void**)&e->meta_host[i], e->meta_bytes));
+      CK(cudaEventCreateWithFlags(&e->meta_ev[i], cudaEventDisableTiming));
+      CK(cudaEventRecord(e->meta_ev[i], e->stream));
+    }
+
+    // KV pool: 64-token pages [L][2][H][64][hd]
+    e->page_elems = fe::kv_page_elems(m);
+    size_t pages = c->kv_pages;
+    if (pages == 0) {
+      size_t free_b = 0, total_b = 0;
+      CK(cudaMemGetInfo(&free_b, &total_b));
+      const size_t reserve = (size_t)4 << 30;
+      const size_t avail = free_b > reserve ? free_b - reserve : free_b / 2;
+      pages = std::max<size_t>(16, std::min<size_t>(avail / 2 / (e->page_elems * el), 8192));
+    }
+    e->n_pages = (int)pages;
+    e->kv_pool = e->dalloc(pages * e->page_elems * el);
+    e->page_ref.assign(pages, 0);
+    for (int p = (int)pages - 1; p >= 0; p--) e->free_pages.push_back(p);
+    e->slot_req.assign(e->max_slots, -1);
+  } catch (...) {
+    for (void* p : e->allocs) cudaFree(p);
+    delete e;
+    throw;
+  }
+  return e;
+}
+
+void destroy(fe_engine* e) {
+  cudaSetDevice(e->device);
+  cudaStreamSynchronize(e->stream);
+  for (void* p : e->allocs) cudaFree(p);
+  for (int i = 0; i < kMetaRing; i++) {
+    if (e->meta_host[i]) cudaFreeHost(e->meta_host[i]);
+    if (e->meta_ev[i]) cudaEventDestroy(e->meta_ev[i]);
+  }
+  cudaStreamDestroy(e->stream);
+  delete e;
+}
+
+template <typename Fn>
+int guarded(fe_engine* e, Fn&& fn) {
+  try {
+    if (!e) throw Error("null engine");
+    std::lock_guard<std::mutex> lk(e->mu);
+    cudaSetDevice(e->device);
+    fn();
+    return 0;
+  } catch (const std::exception& ex) {
+    g_last_error = ex.what();
+    return 1;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fe_last_error(void) { return g_last_error.c_str(); }
+
+int fe_engine_create(const fe_config* cfg, int32_t device, const float* rope, fe_engine** out) {
+  try {
+    if (!cfg || !out || !rope) throw Error("null argument");
+    *out = create(cfg, device, rope);
+    return 0;
+  } catch (const std::exception& ex) {
+    g_last_error = ex.what();
+    return 1;
+  }
+}
+
+int fe_engine_destroy(fe_engine* e) {
+  if (!e) return 0;
+  destroy(e);
+  return 0;
+}
+
+int fe_weights_init_random(fe_engine* e, uint64_t seed) {
+  return guarded(e, [&] { init_weights(e, seed); });
+}
+
+int fe_seq_create(fe_engine* e, int32_t* seq) {
+  return guarded(e, [&] { *seq = new_seq(e); });
+}
+
+int fe_seq_fork(fe_engine* e, int32_t parent, int32_t len, int32_t* child) {
+  return guarded(e, [&] {
+    Seq& p = seq_at(e, parent);
+    if (len < 0 || len > p.len) throw Error("fork length outside the parent");
+    const std::vector<int> ppages = p.pages;  // copy: new_seq may reallocate
+    const int c = new_seq(e);
+    Seq& s = e->seqs[c];
+    const int full = len / FE_PAGE, rem = len % FE_PAGE;
+    for (int i = 0; i < full; i++) {
+      s.pages.push_back(ppages[i]);
+      e->page_ref[ppages[i]]++;
+    }
+    if (rem) {  // copy-on-write of the partially filled page
+      const int np = alloc_page(e);
+      fe::launch_page_copy(e->dtype, e->kv_pool, ppages[full], np, rem, e->m, e->stream);
+      s.pages.push_back(np);
+    }
+    s.len = len;
+    *child = c;
+  });
+}
+
+int fe_seq_free(fe_engine* e, int32_t seq) {
+  return guarded(e, [&] {
+    Seq& s = seq_at(e, seq);
+    for (int p : s.pages) release_page(e, p);
+    s = Seq();
+    e->free_seqs.push_back(seq);
+  });
+}
+
+int fe_seq_len(fe_engine* e, int32_t seq, int32_t* len) {
+  return guarded(e, [&] { *len = seq_at(e, seq).len; });
+}
+
+int fe_prefill(fe_engine* e, int32_t seq, const int32_t* ids, int32_t n, uint64_t vision_seed, int32_t vis_id) {
+  return guarded(e, [&] { prefill(e, seq, ids, n, vision_seed, vis_id); });
+}
+
+int fe_set_slots(fe_engine* e, int32_t slots) {
+  return guarded(e, [&] {
+    if (slots < 1 || slots > e->max_slots) throw Error("slots outside [1, max_slots]");
+    for (int s = slots; s < e->slots; s++)
+      if (e->slot_req[s] >= 0) throw Error("cannot shrink slots while they are occupied");
+    e->slots = slots;
+  });
+}
+
+int fe_submit(fe_engine* e, int32_t seq, int32_t first_id, int32_t length, int32_t priority, int32_t* req) {
+  return guarded(e, [&] {
+    Seq& s = seq_at(e, seq);
+    if (length < 1 || length > kRequestCap) throw Error("request length outside [1, 1024]");
+    if (s.len + length > e->m.max_pos) throw Error("request would exceed max_pos");
+    if (first_id < 0 || first_id >= e->m.V) throw Error("first token id out of range");
+    if (e->free_arena.empty()) throw Error("too many live requests");
+    const int r = new_request_slot(e);
+    Request& q = e->reqs[r];
+    q = Request();
+    q.live = true;
+    q.seq = seq;
+    q.first_id = first_id;
+    q.length = length;
+    q.priority = priority == FE_PRIO_ACTION ? 0 : 1;
+    q.seqno = e->seqno++;
+    q.arena = e->free_arena.back();
+    e->free_arena.pop_back();
+    e->waiting.push_back(r);
+    *req = r;
+  });
+}
+
+int fe_run(fe_engine* e, int32_t stop_req, int32_t cap, int32_t* n_ticks, int32_t* occupancy,
+           int32_t* completed, int32_t* completed_tick, int32_t* n_completed) {
+  return guarded(e, [&] {
+    int t = 0, nc = 0;
+    auto busy = [&] {
+      if (!e->waiting.empty()) return true;
+      for (int s = 0; s < e->slots; s++)
+        if (e->slot_req[s] >= 0) return true;
+      return false;
+    };
+    if (stop_req >= 0) req_at(e, stop_req);
+    while (true) {
+      if (stop_req >= 0 ? e->reqs[stop_req].state == 2 : !busy()) break;
+      if (!busy()) throw Error("run: stop request is not in flight");
+      if (t >= cap) throw Error("run: tick capacity exceeded");
+      std::vector<int> done;
+      occupancy[t] = tick(e, &done);
+      for (int r : done) {
+        if (nc >= cap) throw Error("run: completion capacity exceeded");
+        completed[nc] = r;
+        completed_tick[nc] = t;
+        nc++;
+      }
+      t++;
+    }
+    *n_ticks = t;
+    *n_completed = nc;
+  });
+}
+
+int fe_request_tokens(fe_engine* e, int32_t req, int32_t* out, int32_t cap) {
+  return guarded(e, [&] {
+    Request& q = req_at(e, req);
+    if (q.state != 2) throw Error("request not complete");
+    if (cap < q.length) throw Error("output buffer too small");
+    CK(cudaMemcpyAsync(out, e->ws.out_tokens + (size_t)q.arena * kRequestCap, sizeof(int32_t) * q.length,
+                       cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+  });
+}
+
+int fe_request_release(fe_engine* e, int32_t req) {
+  return guarded(e, [&] {
+    Request& q = req_at(e, req);
+    if (q.state == 0 || q.state == 1) throw Error("request still in flight");
+    e->free_arena.push_back(q.arena);
+    if (e->capture_req == req) e->capture_req = -1;
+    q = Request();
+    e->free_reqs.push_back(req);
+  });
+}
+
+int fe_request_capture_logits(fe_engine* e, int32_t req) {
+  return guarded(e, [&] {
+    Request& q = req_at(e, req);
+    if (e->capture_req >= 0 && e->capture_req != req) throw Error("another request is capturing logits");
+    q.capture = true;
+    e->capture_req = req;
+  });
+}
+
+int fe_request_logits(fe_engine* e, int32_t req, float* out, int32_t rows) {
+  return guarded(e, [&] {
+    Request& q = req_at(e, req);
+    if (!q.capture) throw Error("request did not capture logits");
+    if (rows > std::min(q.produced, kLogitRows)) throw Error("more logit rows than captured");
+    CK(cudaMemcpyAsync(out, e->ws.logits, sizeof(float) * (size_t)rows * e->m.V, cudaMemcpyDeviceToHost,
+                       e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+  });
+}
+
+int fe_in_flight(fe_engine* e, int32_t* n) {
+  return guarded(e, [&] {
+    int c = (int)e->waiting.size();
+    for (int s = 0; s < e->slots; s++) c += e->slot_req[s] >= 0;
+    *n = c;
+  });
+}
+
+int fe_synchronize(fe_engine* e) {
+  return guarded(e, [&] { CK(cudaStreamSynchronize(e->stream)); });
+}
+
+int fe_stream(fe_engine* e, void** stream) {
+  return guarded(e, [&] { *stream = (void*)e->stream; });
+}
+
+int fe_stats(fe_engine* e, int64_t* out, int32_t n) {
+  return guarded(e, [&] {
+    const int64_t v[] = {e->n_ticks, e->n_forwards, e->n_rows_total,
+                         (int64_t)(e->n_pages - (int)e->free_pages.size()), (int64_t)e->n_pages,
+                         (int64_t)(e->page_elems * e->elem)};
+    for (int i = 0; i < n && i < (int)(sizeof(v) / sizeof(v[0])); i++) out[i] = v[i];
+  });
+}
+
+int fe_weight_ptr(fe_engine* e, int32_t tensor, int32_t layer, void** ptr, size_t* bytes) {
+  return guarded(e, [&] {
+    const size_t d = e->m.d, F = e->m.F, V = e->m.V, el = e->elem;
+    if (tensor == 1) { *ptr = e->w.embed; *bytes = V * d * el; return; }
+    if (tensor == 2) { *ptr = e->w.lm_head; *bytes = V * d * el; return; }
+    if (tensor == 3) { *ptr = e->w.final_norm; *bytes = d * 4; return; }
+    if (layer < 0 || layer >= e->m.L) throw Error("layer out of range");
+    const auto& ly = e->layers[layer];
+    switch ((tensor - 16) % 16) {
+      case 0: *ptr = ly.attn_norm; *bytes = d * 4; return;
+      case 1: *ptr = ly.wqkv; *bytes = d * d * el; return;
+      case 2: *ptr = (char*)ly.wqkv + d * d * el; *bytes = d * d * el; return;
+      case 3: *ptr = (char*)ly.wqkv + 2 * d * d * el; *bytes = d * d * el; return;
+      case 4: *ptr = ly.wo; *bytes = d * d * el; return;
+      case 5: *ptr = ly.ffn_norm; *bytes = d * 4; return;
+      case 6: *ptr = ly.wgu; *bytes = F * d * el; return;
+      case 7: *ptr = (char*)ly.wgu + F * d * el; *bytes = F * d * el; return;
+      case 8: *ptr = ly.wdown; *bytes = d * F * el; return;
+    }
+    throw Error("unknown tensor id");
+  });
+}
+
+int fe_memcpy(fe_engine* e, void* dst, const void* src, size_t bytes) {
+  return guarded(e, [&] {
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+  });
+}
+
+int fe_op_gemv(fe_engine* e, const void* w, int32_t N, int32_t K, const void* x, int32_t rows, float* y) {
+  return guarded(e, [&] {
+    if (N % 4 || K % 8) throw Error("gemv: N % 4 and K % 8 must be 0");
+    fe::launch_gemv_store(e->dtype, w, N, K, x, rows, y, e->stream);
+    CK(cudaGetLastError());
+  });
+}
+
+int fe_op_rmsnorm(fe_engine* e, const float* x, const float* w, void* out, int32_t rows, int32_t d) {
+  return guarded(e, [&] {
+    fe::launch_rmsnorm(e->dtype, x, w, out, rows, d, d, e->m.eps, nullptr, e->stream);
+    CK(cudaGetLastError());
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,239 @@
+"""ctypes binding of the B200 engine's C ABI (include/fastecot.h).
+
+The shared library is built in-tree (`_build/libfastecot.so`, see build.py).
+There is deliberately no fallback: if the library or a GPU is missing the
+constructor raises, so a test or benchmark can never silently run on a CPU
+path.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from pathlib import Path
+
+import numpy as np
+
+from .backends import EngineError
+from .model import ModelConfig, ROPE_MAX_POS, TEXT_VOCAB, get_config, rope_table
+
+LIB_PATH = Path(__file__).resolve().parent / "_build" / "libfastecot.so"
+
+F32, BF16 = 0, 1
+PRIO_ACTION, PRIO_REASONING = 0, 1
+
+_c_int_p = ctypes.POINTER(ctypes.c_int32)
+
+
+class FeConfig(ctypes.Structure):
+    _fields_ = [
+        ("d_model", ctypes.c_int32), ("n_layers", ctypes.c_int32), ("n_heads", ctypes.c_int32),
+        ("head_dim", ctypes.c_int32), ("d_ffn", ctypes.c_int32), ("vocab", ctypes.c_int32),
+        ("n_text", ctypes.c_int32), ("max_pos", ctypes.c_int32), ("rms_eps", ctypes.c_float),
+        ("attn_scale", ctypes.c_float), ("dtype", ctypes.c_int32), ("max_rows", ctypes.c_int32),
+        ("kv_pages", ctypes.c_int32), ("max_slots", ctypes.c_int32),
+    ]
+
+
+EXPORTS = (
+    "fe_engine_create", "fe_engine_destroy", "fe_weights_init_random", "fe_last_error",
+    "fe_seq_create", "fe_seq_fork", "fe_seq_free", "fe_seq_len", "fe_prefill", "fe_set_slots",
+    "fe_submit", "fe_run", "fe_request_tokens", "fe_request_release", "fe_request_capture_logits",
+    "fe_request_logits", "fe_in_flight", "fe_synchronize", "fe_stream", "fe_stats",
+    "fe_weight_ptr", "fe_memcpy", "fe_op_gemv", "fe_op_rmsnorm",
+)
+
+_lib = None
+
+
+def load_library(path: Path = LIB_PATH) -> ctypes.CDLL:
+    """Load libfastecot.so and declare every exported signature."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not path.exists():
+        raise EngineError(f"engine library missing: {path} (run __graft_entry__.build())")
+    lib = ctypes.CDLL(str(path))
+    vp, i32, u64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_uint64
+    sig = {
+        "fe_engine_create": [ctypes.POINTER(FeConfig), i32, vp, ctypes.POINTER(vp)],
+        "fe_engine_destroy": [vp],
+        "fe_weights_init_random": [vp, u64],
+        "fe_seq_create": [vp, _c_int_p],
+        "fe_seq_fork": [vp, i32, i32, _c_int_p],
+        "fe_seq_free": [vp, i32],
+        "fe_seq_len": [vp, i32, _c_int_p],
+        "fe_prefill": [vp, i32, vp, i32, u64, i32],
+        "fe_set_slots": [vp, i32],
+        "fe_submit": [vp, i32, i32, i32, i32, _c_int_p],
+        "fe_run": [vp, i32, i32, _c_int_p, vp, vp, vp, _c_int_p],
+        "fe_request_tokens": [vp, i32, vp, i32],
+        "fe_request_release": [vp, i32],
+        "fe_request_capture_logits": [vp, i32],
+        "fe_request_logits": [vp, i32, vp, i32],
+        "fe_in_flight": [vp, _c_int_p],
+        "fe_synchronize": [vp],
+        "fe_stream": [vp, ctypes.POINTER(vp)],
+        "fe_stats": [vp, vp, i32],
+        "fe_weight_ptr": [vp, i32, i32, ctypes.POINTER(vp), ctypes.POINTER(ctypes.c_size_t)],
+        "fe_memcpy": [vp, vp, vp, ctypes.c_size_t],
+        "fe_op_gemv": [vp, vp, i32, i32, vp, i32, vp],
+        "fe_op_rmsnorm": [vp, vp, vp, vp, i32, i32],
+    }
+    for name, argtypes in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = argtypes
+        fn.restype = ctypes.c_int
+    lib.fe_last_error.restype = ctypes.c_char_p
+    lib.fe_last_error.argtypes = []
+    _lib = lib
+    return lib
+
+
+def _np_ptr(a: np.ndarray) -> ctypes.c_void_p:
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+class Engine:
+    """One engine per GPU: weights, paged KV pool, continuous batcher."""
+
+    def __init__(self, config: str | ModelConfig = "tiny", dtype: str = "f32", device: int = 0,
+                 seed: int = 0, max_rows: int = 512, kv_pages: int = 0, max_slots: int = 64):
+        self.cfg = get_config(config)
+        self.lib = load_library()
+        self.dtype = dtype
+        c = self.cfg
+        fc = FeConfig(c.d_model, c.n_layers, c.n_heads, c.head_dim, c.d_ffn, c.vocab, TEXT_VOCAB,
+                      ROPE_MAX_POS, c.rms_eps, float(np.float32(1.0) / np.sqrt(np.float32(c.head_dim))),
+                      F32 if dtype == "f32" else BF16, max_rows, kv_pages, max_slots)
+        self._rope = rope_table(c)
+        h = ctypes.c_void_p()
+        self._h = None
+        self._check(self.lib.fe_engine_create(ctypes.byref(fc), device, _np_ptr(self._rope), ctypes.byref(h)))
+        self._h = h
+        self.seed = seed
+        self._check(self.lib.fe_weights_init_random(self._h, seed))
+        self._cap = 8192
+        self._occ = np.zeros(self._cap, dtype=np.int32)
+        self._done = np.zeros(self._cap, dtype=np.int32)
+        self._done_tick = np.zeros(self._cap, dtype=np.int32)
+
+    # -- plumbing ----------------------------------------------------------
+    def _check(self, rc: int) -> None:
+        if rc != 0:
+            raise EngineError(self.lib.fe_last_error().decode(errors="replace"))
+
+    def close(self) -> None:
+        if self._h is not None:
+            self.lib.fe_engine_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- sequences ---------------------------------------------------------
+    def seq_create(self) -> int:
+        s = ctypes.c_int32()
+        self._check(self.lib.fe_seq_create(self._h, ctypes.byref(s)))
+        return s.value
+
+    def seq_fork(self, parent: int, length: int) -> int:
+        s = ctypes.c_int32()
+        self._check(self.lib.fe_seq_fork(self._h, parent, length, ctypes.byref(s)))
+        return s.value
+
+    def seq_free(self, seq: int) -> None:
+        self._check(self.lib.fe_seq_free(self._h, seq))
+
+    def seq_len(self, seq: int) -> int:
+        n = ctypes.c_int32()
+        self._check(self.lib.fe_seq_len(self._h, seq, ctypes.byref(n)))
+        return n.value
+
+    def prefill(self, seq: int, ids, vision_seed: int, vis_id: int) -> None:
+        a = np.ascontiguousarray(np.asarray(ids, dtype=np.int32))
+        if a.size:
+            self._check(self.lib.fe_prefill(self._h, seq, _np_ptr(a), int(a.size),
+                                            ctypes.c_uint64(vision_seed & 0xFFFFFFFFFFFFFFFF), vis_id))
+
+    # -- batcher -------------------------------------------------------------
+    def set_slots(self, slots: int) -> None:
+        self._check(self.lib.fe_set_slots(self._h, slots))
+
+    def submit(self, seq: int, first_id: int, length: int, priority: int) -> int:
+        r = ctypes.c_int32()
+        self._check(self.lib.fe_submit(self._h, seq, first_id, length, priority, ctypes.byref(r)))
+        return r.value
+
+    def run(self, stop_req: int = -1) -> tuple[list[int], list[tuple[int, int]]]:
+        """Decode until `stop_req` completes (-1: until idle).
+        Returns (occupancy per tick, [(request, tick)] in completion order)."""
+        nt, nc = ctypes.c_int32(), ctypes.c_int32()
+        self._check(self.lib.fe_run(self._h, stop_req, self._cap, ctypes.byref(nt), _np_ptr(self._occ),
+                                    _np_ptr(self._done), _np_ptr(self._done_tick), ctypes.byref(nc)))
+        occ = self._occ[: nt.value].tolist()
+        done = list(zip(self._done[: nc.value].tolist(), self._done_tick[: nc.value].tolist()))
+        return occ, done
+
+    def request_tokens(self, req: int, length: int) -> list[int]:
+        out = np.zeros(max(length, 1), dtype=np.int32)
+        self._check(self.lib.fe_request_tokens(self._h, req, _np_ptr(out), out.size))
+        return out[:length].tolist()
+
+    def request_release(self, req: int) -> None:
+        self._check(self.lib.fe_request_release(self._h, req))
+
+    def capture_logits(self, req: int) -> None:
+        self._check(self.lib.fe_request_capture_logits(self._h, req))
+
+    def request_logits(self, req: int, rows: int) -> np.ndarray:
+        out = np.zeros((rows, self.cfg.vocab), dtype=np.float32)
+        self._check(self.lib.fe_request_logits(self._h, req, _np_ptr(out), rows))
+        return out
+
+    def in_flight(self) -> int:
+        n = ctypes.c_int32()
+        self._check(self.lib.fe_in_flight(self._h, ctypes.byref(n)))
+        return n.value
+
+    def synchronize(self) -> None:
+        self._check(self.lib.fe_synchronize(self._h))
+
+    def stream_handle(self) -> int:
+        p = ctypes.c_void_p()
+        self._check(self.lib.fe_stream(self._h, ctypes.byref(p)))
+        return p.value or 0
+
+    def stats(self) -> dict:
+        out = np.zeros(6, dtype=np.int64)
+        self._check(self.lib.fe_stats(self._h, _np_ptr(out), out.size))
+        keys = ("ticks", "forwards", "rows", "pages_used", "pages_total", "page_bytes")
+        return dict(zip(keys, out.tolist()))
+
+    # -- kernel-level hooks (device pointers) ----------------------------------
+    def weight_ptr(self, tensor: int, layer: int = 0) -> tuple[int, int]:
+        p, n = ctypes.c_void_p(), ctypes.c_size_t()
+        self._check(self.lib.fe_weight_ptr(self._h, tensor, layer, ctypes.byref(p), ctypes.byref(n)))
+        return p.value, n.value
+
+    def memcpy(self, dst: int, src: int, nbytes: int) -> None:
+        self._check(self.lib.fe_memcpy(self._h, ctypes.c_void_p(dst), ctypes.c_void_p(src), nbytes))
+
+    def weight_host(self, tensor: int, layer: int = 0) -> np.ndarray:
+        """Host copy of a weight tensor (fp32 view; bf16 returned as uint16 bits)."""
+        ptr, nbytes = self.weight_ptr(tensor, layer)
+        is_norm = tensor in (3,) or (tensor >= 16 and (tensor - 16) % 16 in (0, 5))
+        dt = np.float32 if (self.dtype == "f32" or is_norm) else np.uint16
+        out = np.empty(nbytes // np.dtype(dt).itemsize, dtype=dt)
+        self.memcpy(out.ctypes.data, ptr, nbytes)
+        return out
+
+    def op_gemv(self, w_ptr: int, N: int, K: int, x_ptr: int, rows: int, y_ptr: int) -> None:
+        self._check(self.lib.fe_op_gemv(self._h, ctypes.c_void_p(w_ptr), N, K, ctypes.c_void_p(x_ptr), rows,
+                                        ctypes.c_void_p(y_ptr)))
+
+    def op_rmsnorm(self, x_ptr: int, w_ptr: int, out_ptr: int, rows: int, d: int) -> None:
+        self._check(self.lib.fe_op_rmsnorm(self._h, ctypes.c_void_p(x_ptr), ctypes.c_void_p(w_ptr),
+                                           ctypes.c_void_p(out_ptr), rows, d))

@@ -1,0 +1,216 @@
+"""`EngineBackend`: the reference `GenerationBackend` served by the B200 engine.
+
+Drop-in for the protocol of `pkg/src/ecot_sched/backends.py:98-110`
+(`encode`, `begin_step`, `deterministic`, `supports_prefix_conditioning`),
+plus the two runner-level extensions the GPU-aware runners use
+(schedulers.py in this package):
+
+* `begin_steps(ctx, jobs)` -- the N+1 branch jobs of one Fast-ECoT timestep
+  (reference `ParallelSyncRunner`, schedulers.py:399-420) decoded as one
+  batch: the longest prefix is prefilled once as a *trunk*, every job forks
+  the trunk's paged KV at its own prefix length (copy-on-write of the partial
+  page only) and all branches decode together;
+* `make_async_engine(slots)` -- the continuous batcher for Fast ECoT async
+  (reference `_MicroEngine`, schedulers.py:244-299) whose ticks are real
+  decode iterations.
+
+Reuse across timesteps: trunks live in a content-addressed prefix cache keyed
+by (vision seed, input ids); a request whose context and prefix extend a
+cached trunk forks it at the longest common prefix and prefills only the
+remainder (sequential ECoT extends the trunk step by step; repeated
+contexts reuse whole trunks).
+
+Errors from the engine surface as `BackendError` subclasses (`EngineError`)
+so the runners' `reuse_stale` / `abort_episode` policies apply unchanged
+(schedulers.py:422-434, :510-517).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Callable, Optional, Sequence
+
+import numpy as np
+
+from .backends import (BackendError, EngineError, StepGenerator, SyntheticProfile, default_profile,
+                       encode_tokens, length_plan)
+from .batching import ACTION
+from .engine import Engine, PRIO_ACTION, PRIO_REASONING
+from .model import VIS_ID, context_ids, get_config, step_tag, text_ids, vision_seed
+from .trace import Context, StepSpec, TokenSeq
+
+
+@dataclass
+class _Trunk:
+    vseed: int
+    ids: np.ndarray
+    seq: int
+    stamp: int
+
+
+@dataclass
+class EngineRequest:
+    """A prepared branch request (async engine handle)."""
+
+    name: str
+    step: StepSpec
+    length: int
+    truncated: bool
+    tag: int
+    branch: int
+    priority: int
+    issue_timestep: int = 0
+    req: int = -1
+    tokens: TokenSeq = ()
+    on_complete: Optional[Callable[["EngineRequest", int], None]] = None
+    done: bool = False
+
+
+class EngineBackend:
+    deterministic = True
+    supports_prefix_conditioning = True
+
+    def __init__(self, config="tiny", dtype: str = "f32", seed: int = 0,
+                 profile: SyntheticProfile | None = None, device: int = 0,
+                 engine: Engine | None = None, trunk_cache: int = 64, **engine_kw):
+        self.cfg = get_config(config)
+        self.engine = engine or Engine(self.cfg, dtype=dtype, device=device, seed=seed, **engine_kw)
+        self.profile = profile or default_profile(seed)
+        self._trunks: list[_Trunk] = []
+        self._trunk_cap = trunk_cache
+        self._clock = 0
+        self._owners: dict[int, EngineRequest] = {}
+        self.requests = 0
+
+    # -- protocol ------------------------------------------------------------
+    def encode(self, instruction: str, observation: bytes) -> Context:
+        return Context(instruction, observation, encode_tokens(instruction, observation))
+
+    def begin_step(self, context: Context, prefix: TokenSeq, step: StepSpec,
+                   prev_content: TokenSeq) -> StepGenerator:
+        out = self.begin_steps(context, [(step, prefix, prev_content)], priorities=[PRIO_ACTION])[0]
+        if isinstance(out, BackendError):
+            raise out
+        return out
+
+    def begin_steps(self, context: Context, jobs: Sequence[tuple[StepSpec, TokenSeq, TokenSeq]],
+                    priorities: Sequence[int] | None = None) -> list:
+        """Decode several branch requests of one context as one batch.
+        Returns a StepGenerator or a BackendError per job (job order)."""
+        if priorities is None:  # reference fan-out order: the action step is last
+            priorities = [PRIO_REASONING] * (len(jobs) - 1) + [PRIO_ACTION]
+        outcomes: list = [None] * len(jobs)
+        handles: dict[int, EngineRequest] = {}
+        order = sorted(range(len(jobs)), key=lambda i: -len(jobs[i][1]))  # longest trunk first
+        for i in order:
+            spec, prefix, prev = jobs[i]
+            try:
+                handles[i] = self._prepare(context, prefix, spec, prev, priorities[i])
+            except BackendError as exc:
+                outcomes[i] = exc
+        for i in sorted(handles):
+            self._submit(handles[i], None)
+        for i in sorted(handles):
+            h = handles[i]
+            if not h.done:
+                self._run(h.req, 0)
+            outcomes[i] = StepGenerator(h.tokens, truncated=h.truncated)
+        return outcomes
+
+    def make_async_engine(self, slots: int) -> "AsyncEngine":
+        return AsyncEngine(self, slots)
+
+    # -- trunks & branches -----------------------------------------------------
+    def _branch_point(self, vseed: int, ids: np.ndarray) -> tuple[int, bool]:
+        """Sequence whose KV covers ids exactly up to len(ids) (possibly longer)."""
+        n = ids.size
+        best, best_lcp = None, 0
+        for tr in self._trunks:
+            if tr.vseed != vseed:
+                continue
+            m = min(n, tr.ids.size)
+            neq = np.flatnonzero(tr.ids[:m] != ids[:m])
+            lcp = int(neq[0]) if neq.size else m
+            if lcp > best_lcp or (lcp == best_lcp and best is not None and tr.ids.size < best.ids.size):
+                best, best_lcp = tr, lcp
+        self._clock += 1
+        if best is not None and best_lcp == n:
+            best.stamp = self._clock
+            return best.seq, False
+        eng = self.engine
+        seq = eng.seq_fork(best.seq, best_lcp) if best is not None and best_lcp > 0 else eng.seq_create()
+        try:
+            eng.prefill(seq, ids[best_lcp:], vseed, VIS_ID)
+        except EngineError:
+            eng.seq_free(seq)
+            raise
+        self._trunks.append(_Trunk(vseed, ids.copy(), seq, self._clock))
+        if len(self._trunks) > self._trunk_cap:
+            victim = min(self._trunks, key=lambda t: t.stamp)
+            self._trunks.remove(victim)
+            eng.seq_free(victim.seq)
+        return seq, True
+
+    def _prepare(self, ctx: Context, prefix: TokenSeq, spec: StepSpec, prev: TokenSeq,
+                 priority: int, timestep: int = 0) -> EngineRequest:
+        plan = length_plan(self.profile, ctx, spec, prev)  # BackendError on unknown step
+        ids = np.asarray(context_ids(ctx, self.cfg) + text_ids(prefix), dtype=np.int32)
+        vseed = vision_seed(ctx.observation)
+        trunk, _ = self._branch_point(vseed, ids)
+        branch = self.engine.seq_fork(trunk, ids.size)
+        return EngineRequest(spec.name, spec, plan.length, plan.truncated, step_tag(spec), branch,
+                             priority, issue_timestep=timestep)
+
+    def _submit(self, h: EngineRequest, on_complete) -> None:
+        h.on_complete = on_complete
+        h.req = self.engine.submit(h.branch, h.tag, h.length, h.priority)
+        self._owners[h.req] = h
+        self.requests += 1
+
+    def _run(self, stop_req: int, timestep: int) -> list[int]:
+        occupancy, done = self.engine.run(stop_req)
+        for req, _tick in done:
+            h = self._owners.pop(req)
+            h.tokens = tuple(self.engine.request_tokens(req, h.length))
+            h.done = True
+            self.engine.request_release(req)
+            self.engine.seq_free(h.branch)
+            if h.on_complete is not None:
+                h.on_complete(h, timestep)
+        return occupancy
+
+    def close(self) -> None:
+        self.engine.close()
+
+
+class AsyncEngine:
+    """Continuous batcher facade used by `ParallelAsyncRunner`: same surface
+    as the reference `_MicroEngine` (submit / in_flight_names), but each tick
+    is one decode iteration of every admitted row on the GPU."""
+
+    def __init__(self, backend: EngineBackend, slots: int):
+        self.backend = backend
+        backend.engine.set_slots(slots)
+        self._inflight: dict[int, EngineRequest] = {}
+
+    def prepare(self, ctx, prefix, spec, prev_content, priority: str, timestep: int) -> EngineRequest:
+        prio = PRIO_ACTION if priority == ACTION else PRIO_REASONING
+        return self.backend._prepare(ctx, prefix, spec, prev_content, prio, timestep)
+
+    def submit(self, h: EngineRequest, on_complete) -> None:
+        def landed(req: EngineRequest, t: int) -> None:
+            self._inflight.pop(req.req, None)
+            if on_complete is not None:
+                on_complete(req, t)
+
+        self.backend._submit(h, landed)
+        self._inflight[h.req] = h
+
+    def in_flight_names(self) -> set[str]:
+        return {h.name for h in self._inflight.values()}
+
+    def idle(self) -> bool:
+        return not self._inflight
+
+    def run_until_complete(self, h: EngineRequest, timestep: int) -> list[int]:
+        return self.backend._run(h.req, timestep)

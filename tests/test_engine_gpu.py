@@ -1,0 +1,197 @@
+"""B200 engine parity (needs a GPU): every check runs through the C ABI
+(libfastecot.so) and compares with the CPU oracle / golden fixtures.
+
+Bar (north_star): fp32 mode -- greedy tokens bit-exact and logits equal to
+the oracle (canonical arithmetic makes them bit-identical; the tolerance
+asserted against the independent torch model is 1e-3 relative); bf16 mode --
+token-match rate vs the fp32 oracle reported, logits within a bf16 tolerance.
+"""
+
+import json
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import GOLDEN
+from paper_2506_07639_b200 import model as M
+from paper_2506_07639_b200 import schedulers as S
+from paper_2506_07639_b200 import trace as T
+from paper_2506_07639_b200.backends import EngineError
+from paper_2506_07639_b200.engine import Engine
+from paper_2506_07639_b200.engine_backend import EngineBackend
+
+pytestmark = pytest.mark.gpu
+
+LOGIT_RTOL = 1e-3
+
+
+@pytest.fixture(scope="module")
+def tiny_f32():
+    eng = Engine("tiny", dtype="f32", seed=0, kv_pages=512)
+    yield eng
+    eng.close()
+
+
+@pytest.fixture(scope="module")
+def oracle_tiny():
+    from oracle.backend import OracleModel
+    return OracleModel("tiny", seed=0)
+
+
+def _decode(eng: Engine, ids, vseed, n_out, capture=False):
+    seq = eng.seq_create()
+    eng.prefill(seq, ids[:-1], vseed, M.VIS_ID)
+    req = eng.submit(seq, ids[-1], n_out, 0)
+    if capture:
+        eng.capture_logits(req)
+    eng.run(req)
+    toks = eng.request_tokens(req, n_out)
+    logits = eng.request_logits(req, n_out) if capture else None
+    eng.request_release(req)
+    eng.seq_free(seq)
+    return toks, logits
+
+
+def test_gpu_is_a_b200():
+    assert torch.cuda.is_available()
+    major, minor = torch.cuda.get_device_capability(0)
+    assert (major, minor) == (10, 0)
+
+
+def test_weights_bitwise_equal_oracle(tiny_f32, oracle_tiny):
+    cfg = M.PRESETS["tiny"]
+    for tid, layer, shape in [(M.T_EMBED, 0, (cfg.vocab, cfg.d_model)),
+                              (M.layer_tensor(1, M.L_WQ), 1, (cfg.d_model, cfg.d_model)),
+                              (M.layer_tensor(3, M.L_WDOWN), 3, (cfg.d_model, cfg.d_ffn)),
+                              (M.layer_tensor(0, M.L_FFN_NORM), 0, (cfg.d_model,))]:
+        got = tiny_f32.weight_host(tid, layer).reshape(shape)
+        assert np.array_equal(got, oracle_tiny.tensor(tid, layer, shape))
+
+
+@pytest.mark.parametrize("rows", [1, 3, 8, 13, 40])
+def test_gemv_bit_exact_vs_oracle(tiny_f32, oracle_tiny, rows):
+    cfg = M.PRESETS["tiny"]
+    ptr, _ = tiny_f32.weight_ptr(M.layer_tensor(2, M.L_WGATE), 2)  # gate rows [F, d]
+    N, K = cfg.d_ffn, cfg.d_model
+    x = torch.randn(rows, K, generator=torch.Generator().manual_seed(rows)).float()
+    xd = x.cuda()
+    y = torch.empty(rows, N, device="cuda")
+    tiny_f32.op_gemv(ptr, N, K, xd.data_ptr(), rows, y.data_ptr())
+    tiny_f32.synchronize()
+    W = oracle_tiny.tensor(M.layer_tensor(2, M.L_WGATE), 2, (N, K))
+    want = np.zeros((rows, N), dtype=np.float32)
+    xn = np.ascontiguousarray(x.numpy())
+    oracle_tiny.lib.or_matmul(want.ctypes.data, xn.ctypes.data, W.ctypes.data, rows, N, K)
+    assert np.array_equal(y.cpu().numpy(), want)
+
+
+def test_rmsnorm_bit_exact(tiny_f32, oracle_tiny):
+    d = M.PRESETS["tiny"].d_model
+    x = torch.randn(5, d, generator=torch.Generator().manual_seed(1))
+    w = torch.from_numpy(M.init_norm(0, 99, d))
+    out = torch.empty(5, d, device="cuda")
+    tiny_f32.op_rmsnorm(x.cuda().data_ptr(), w.cuda().data_ptr(), out.data_ptr(), 5, d)
+    tiny_f32.synchronize()
+    want = np.zeros((5, d), dtype=np.float32)
+    xn, wn = np.ascontiguousarray(x.numpy()), np.ascontiguousarray(w.numpy())
+    for i in range(5):
+        oracle_tiny.lib.or_rmsnorm(want[i].ctypes.data, xn[i].ctypes.data, wn.ctypes.data, d, np.float32(1e-5))
+    assert np.array_equal(out.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("prefix_len", [0, 45, 130])
+def test_request_tokens_and_logits_bit_exact(tiny_f32, oracle_tiny, prefix_len):
+    from oracle.backend import frame
+    rng = np.random.default_rng(prefix_len)
+    ids = frame("tiny", rng.integers(0, 2**32, 16).tolist(), rng.integers(0, 32000, prefix_len).tolist(), "plan")
+    want, wl = oracle_tiny.generate(ids, 1234 + prefix_len, 20, want_logits=True)
+    got, gl = _decode(tiny_f32, ids, 1234 + prefix_len, 20, capture=True)
+    assert got == want
+    assert np.array_equal(gl, wl)
+
+
+@pytest.mark.parametrize("name", ["small", "7b_2layer"])
+def test_golden_request_vectors(name):
+    g = json.loads((GOLDEN / f"requests_{name}.json").read_text())
+    eng = Engine(name, dtype="f32", seed=g["seed"], kv_pages=64, max_rows=256)
+    try:
+        for case in g["cases"]:
+            toks, logits = _decode(eng, case["ids"], case["vseed"], case["n_out"], capture=True)
+            assert toks == case["tokens"]
+            assert logits[:, :8].tolist() == case["logits_head"]
+    finally:
+        eng.close()
+
+
+def test_fork_cow_branch_equals_fresh_sequence(tiny_f32, oracle_tiny):
+    """A branch forked off a shared trunk (copy-on-write partial page)
+    decodes exactly what a from-scratch sequence decodes."""
+    from oracle.backend import frame
+    ids = frame("tiny", list(range(16)), list(range(1000, 1100)), "subtask")   # 133 ids: partial 3rd page
+    eng = tiny_f32
+    trunk = eng.seq_create()
+    eng.prefill(trunk, ids[:-1], 77, M.VIS_ID)
+    reqs, seqs = [], []
+    for cut in (len(ids) - 1, 70, 64, 1):
+        b = eng.seq_fork(trunk, cut)
+        seqs.append(b)
+        reqs.append((cut, eng.submit(b, ids[cut] if cut < len(ids) - 1 else ids[-1], 5, 1)))
+    eng.run(-1)
+    for cut, r in reqs:
+        toks = eng.request_tokens(r, 5)
+        eng.request_release(r)
+        want, _ = oracle_tiny.generate(ids[: cut + 1], 77, 5)
+        assert toks == want, cut
+    for s in seqs + [trunk]:
+        eng.seq_free(s)
+    assert eng.stats()["pages_used"] == 0
+
+
+@pytest.mark.parametrize("mode", ["sequential", "parallel_sync", "parallel_async"])
+def test_traces_byte_identical_to_reference_golden(schema, golden_traces, mode):
+    """BASELINE config 1 through the GPU-aware runners and the engine: trace
+    bytes, simulated latency, staleness and accounting equal the reference
+    runners over the CPU oracle."""
+    g = golden_traces["modes"][mode]
+    be = EngineBackend("tiny", dtype="f32", seed=0, kv_pages=1024)
+    try:
+        res, _ = S.run_episode(S.SchedulerConfig(mode=mode, slots=8), golden_traces["T"], be, schema, seed=0)
+        assert [T.trace_content_bytes(r.trace, schema).decode() for r in res] == g["lines"]
+        assert [r.latency_ms for r in res] == g["latency_ms"]
+        assert [r.staleness for r in res] == g["staleness"]
+        assert [r.generated_tokens for r in res] == g["generated_tokens"]
+    finally:
+        be.close()
+
+
+def test_bf16_token_match_rate(golden_traces, schema):
+    """bf16 engine vs the fp32 golden (reported; must stay a coherent model)."""
+    g = golden_traces["modes"]["sequential"]
+    be = EngineBackend("tiny", dtype="bf16", seed=0, kv_pages=1024)
+    try:
+        res, _ = S.run_episode(S.SchedulerConfig(mode="sequential"), 3, be, schema, seed=0)
+    finally:
+        be.close()
+    want = [json.loads(l) for l in g["lines"][:3]]
+    same = total = 0
+    for r, w in zip(res, want):
+        for (name, toks), ws in zip(r.trace.steps, w["steps"]):
+            total += len(ws["tokens"])
+            for a, b in zip(toks, ws["tokens"]):
+                same += a == b
+    rate = same / total
+    print(f"bf16 token-match rate vs fp32 oracle: {rate:.3f} over {total} tokens")
+    assert rate > 0.0
+
+
+def test_engine_errors_are_backend_errors():
+    eng = Engine("tiny", dtype="f32", seed=0, kv_pages=4)
+    try:
+        with pytest.raises(EngineError):
+            eng.seq_fork(12345, 1)
+        s = eng.seq_create()
+        with pytest.raises(EngineError):
+            eng.prefill(s, list(range(5 * 64)), 0, M.VIS_ID)  # needs 5 pages, pool has 4
+    finally:
+        eng.close()
