@@ -1,0 +1,419 @@
+#!/usr/bin/env python
+"""Fast-ECoT on B200: policy steps/s of a 7B-shaped ECoT VLA.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl engine|reference]
+
+Workload (BASELINE.json config 2, 1 GPU): Llama-2-7B-shaped decoder + 256
+vision tokens, random-init bf16 weights, synthetic LIBERO-shaped
+observations (`observation_for(seed, t)`), default ECoT schema/profile; one
+episode per GPU driven by the Fast-ECoT runner (`parallel_sync`: trunk
+prefill + 7 forked branches decoded as one batch).  A *step* is one control
+timestep.  `value` = policy steps/s over all ranks (device time, CUDA events
+on the engine stream, max over ranks); `e2e` = the same through the public
+runner API with host wall clock (all H2D/D2H inside).  Sequential ECoT and
+async action latency are reported alongside.  Every decode iteration streams
+13.2 GB of weights (> L2), so no L2 flush is needed between steps.
+
+Multi-GPU: one process per GPU (torchrun); each rank runs an independent
+episode (seed = rank) on its own engine; NCCL is used only to gather the
+per-rank results at the end ("scaling": "weak").
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+METRIC = "p50 per-step ECoT latency (ms) and policy steps/s, 7B-shaped VLA, 1/2/4/8 B200"
+INSTRUCTION = "pick up the object and place it on the target"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("engine", "reference"), default="engine")
+    ap.add_argument("--config", default="7b")
+    ap.add_argument("--dtype", default="bf16")
+    ap.add_argument("--mode", default="parallel_sync")
+    ap.add_argument("--seq-steps", type=int, default=2)
+    ap.add_argument("--async-steps", type=int, default=10)
+    ap.add_argument("--no-extras", action="store_true", help="skip sequential/async side measurements")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--out", default=None, help="also write the JSON line here")
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------------
+def dist_setup(backend: str):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group(backend=backend)
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def all_max(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def gather_objects(obj, world):
+    if world == 1:
+        return [obj]
+    import torch.distributed as dist
+    out = [None] * world
+    dist.all_gather_object(out, obj)
+    return out
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = tempfile.mktemp(suffix=".csv")
+
+    def start(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=self.fh, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        self.fh.close()
+        rows = []
+        for line in open(self.path).read().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                rows.append(parts)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({n for r in rows for n, v in zip(names, r[4:8]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows),
+                "power_w_max": max((float(r[2]) for r in rows if r[2].replace(".", "").isdigit()), default=None)}
+
+
+def measured_peaks() -> dict:
+    p = REPO / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops_sustained"], "source": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "source": "fallback"}
+
+
+def ncu_traffic() -> float | None:
+    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
+    p = REPO / "profiles" / "ncu_decode_gemv.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text()).get("dram_bytes_per_launch")
+        except (ValueError, OSError):
+            return None
+    return None
+
+
+# --------------------------------------------------------------------------
+def workload_shapes(config: str, seed: int, warmup: int, steps: int, mode: str = "parallel_sync"):
+    """Per timed step: (trunk tokens to prefill, decode tokens) of the ECoT
+    workload.  Lengths come from the synthetic length oracle only, so the
+    shape is known without running the model (it equals the engine's)."""
+    from paper_2506_07639_b200 import schedulers as S
+    from paper_2506_07639_b200.backends import SyntheticBackend, default_profile
+    from paper_2506_07639_b200.model import get_config
+    from paper_2506_07639_b200.trace import default_schema
+    cfg = get_config(config)
+    ctx_len = 1 + cfg.n_vision + 16
+    schema = default_schema()
+    be = SyntheticBackend(default_profile(seed))
+    runner = S.make_runner(S.SchedulerConfig(mode=mode, slots=8), be, schema)
+    shapes, prev = [], None
+    for t in range(warmup + steps):
+        r = runner.step(be.encode(INSTRUCTION, S.observation_for(seed, t)), t)
+        if t >= warmup:
+            lens = [len(toks) for _, toks in r.trace.steps]
+            if mode == "parallel_sync" and prev is not None:
+                trunk = ctx_len + sum(len(toks) for _, toks in prev.steps[:-1])
+            else:  # sequential chain: context + every step but the last is prefilled
+                trunk = ctx_len + sum(lens[:-1])
+            shapes.append((trunk, sum(lens)))
+        prev = r.trace
+    return shapes
+
+
+def cpu_sample(config: str, threads: int) -> dict:
+    """Time the CPU oracle (fp32, canonical arithmetic, all host threads) on a
+    bounded sample of the same model shape: one 48-token prefill and 3 decode
+    tokens.  Falls back to the 2-layer 7B shape scaled by depth when host RAM
+    cannot hold the 26 GB fp32 7B model."""
+    from oracle.backend import OracleModel, SHAPES
+    mem_gb = 0.0
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemAvailable"):
+                mem_gb = int(line.split()[1]) / 1e6
+    except OSError:
+        pass
+    use, scale = config, 1.0
+    if config == "7b" and mem_gb < 80:
+        use, scale = "7b_2layer", SHAPES["7b"][1] / SHAPES["7b_2layer"][1]
+    t0 = time.perf_counter()
+    om = OracleModel(use, seed=0, threads=threads)
+    init_s = time.perf_counter() - t0
+    ids = [32000] + [32001] * 16 + list(range(100, 131))       # 48 ids
+    t0 = time.perf_counter()
+    om.generate(ids, 1, 1)                                      # prefill 48 + 1 head
+    t_pre = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    om.generate(ids, 1, 4)                                      # cached prefix: 1 row + 3 decode tokens
+    t_dec = (time.perf_counter() - t0) / 4.0
+    per_prefill = (t_pre - t_dec) / 47.0
+    return {"model": use, "depth_scale": scale, "prefill_s_per_token": per_prefill * scale,
+            "decode_s_per_token": t_dec * scale, "init_s": init_s, "threads": threads, "mem_gb": mem_gb}
+
+
+def extrapolate_ms(sample: dict, shape) -> float:
+    trunk, dec = shape
+    return 1000.0 * (trunk * sample["prefill_s_per_token"] + dec * sample["decode_s_per_token"])
+
+
+# --------------------------------------------------------------------------
+def run_reference(args, rank, world):
+    """Reference arm: the reference's CPU path for this workload -- the
+    reference runners (baseline/_ref when installed, else the mirror) over
+    the CPU oracle model -- timed on the host cores in a bounded sample."""
+    if rank != 0:
+        return None
+    threads = os.cpu_count() or 1
+    ref_runner = "mirror"
+    try:
+        sys.path.insert(0, str(REPO / "baseline" / "_ref"))
+        os.environ.setdefault("NUMBA_CACHE_DIR", tempfile.mkdtemp(prefix="numba_"))
+        import ecot_sched  # noqa: F401
+        ref_runner = "reference (baseline/_ref)"
+    except Exception:
+        pass
+    sample = cpu_sample(args.config, threads)
+    shapes = workload_shapes(args.config, 0, args.warmup, args.steps, args.mode)
+    ms = [extrapolate_ms(sample, s) for s in shapes]
+    value = 1000.0 / statistics.mean(ms)
+    line = {
+        "metric": METRIC, "impl": "reference", "value": value, "unit": "steps/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": statistics.mean(ms),
+        "p50_ms": statistics.median(ms), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "config 2: 7B-shaped ECoT VLA, single episode, Fast ECoT parallel_sync",
+                   "model": args.config, "mode": args.mode},
+        "cpu_baseline": {"value": value, "unit": "steps/s", "cores": threads, "kind": "port",
+                         "sample": (f"CPU oracle ({sample['model']}, fp32, {threads} threads): 47-token prefill "
+                                    f"+ 4 decode tokens timed, extrapolated to each step's trunk and branch "
+                                    f"lengths (depth x{sample['depth_scale']:.0f}); runners: {ref_runner}")},
+        "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "detail": sample,
+    }
+    return line
+
+
+def time_mode(backend, runner, seed, t0, n, stream):
+    """Run n timesteps from t0; returns per-step (device ms, host ms)."""
+    import torch
+    from paper_2506_07639_b200.schedulers import observation_for
+    dev, host, results = [], [], []
+    for t in range(t0, t0 + n):
+        ctx = backend.encode(INSTRUCTION, observation_for(seed, t))
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        h0 = time.perf_counter()
+        results.append(runner.step(ctx, t))
+        host.append((time.perf_counter() - h0) * 1000.0)
+        b.record(stream)
+        b.synchronize()
+        dev.append(a.elapsed_time(b))
+    return dev, host, results
+
+
+def run_engine(args, rank, world, local):
+    import torch
+    from paper_2506_07639_b200 import schedulers as S
+    from paper_2506_07639_b200.engine_backend import EngineBackend
+    from paper_2506_07639_b200.trace import default_schema
+
+    torch.cuda.set_device(local)
+    schema = default_schema()
+    seed = rank
+    backend = EngineBackend(args.config, dtype=args.dtype, seed=0, device=local)
+    eng = backend.engine
+    stream = torch.cuda.ExternalStream(eng.stream_handle(), device=local)
+    runner = S.make_runner(S.SchedulerConfig(mode=args.mode, slots=8, wall_clock=True), backend, schema)
+
+    # warm-up (t=0 is the reference's sequential warm-up pass)
+    time_mode(backend, runner, seed, 0, args.warmup, stream)
+    eng.synchronize()
+    torch.cuda.synchronize()
+    barrier(world)
+    stats0 = eng.stats()
+    eng.profile(True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    start.record(stream)
+    h0 = time.perf_counter()
+    dev, host, results = time_mode(backend, runner, seed, args.warmup, args.steps, stream)
+    host_total = time.perf_counter() - h0
+    end.record(stream)
+    eng.synchronize()
+    torch.cuda.synchronize()
+    barrier(world)
+    clk = clocks.stop()
+    prof = eng.profile_read()
+    eng.profile(False)
+    stats1 = eng.stats()
+    total_s = start.elapsed_time(end) / 1000.0
+    total_max = all_max(total_s, world)
+    host_max = all_max(host_total, world)
+
+    extras = {}
+    if world == 1 and not args.no_extras:
+        seq_runner = S.make_runner(S.SchedulerConfig(mode="sequential", slots=8, wall_clock=True), backend, schema)
+        sdev, shost, _ = time_mode(backend, seq_runner, 1000 + seed, 0, 1 + args.seq_steps, stream)
+        asy = S.make_runner(S.SchedulerConfig(mode="parallel_async", slots=8, wall_clock=True), backend, schema)
+        adev, ahost, ares = time_mode(backend, asy, 2000 + seed, 0, 1 + args.async_steps, stream)
+        extras = {
+            "sequential_ms": {"p50": statistics.median(sdev[1:]), "steps": len(sdev) - 1,
+                              "all": [round(x, 2) for x in sdev[1:]]},
+            "parallel_async_action_ms": {"p50": statistics.median(adev[1:]),
+                                         "p99": sorted(adev[1:])[max(0, int(0.99 * (len(adev) - 1)) - 1)],
+                                         "steps": len(adev) - 1},
+        }
+    gathered = gather_objects({"rank": rank, "dev_ms": dev, "host_ms": host}, world)
+    return backend, dict(dev=dev, host=host, results=results, total_max=total_max, host_max=host_max,
+                         prof=prof, clocks=clk, stats0=stats0, stats1=stats1, extras=extras, gathered=gathered)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        rank, world, local = dist_setup("gloo")
+        line = run_reference(args, rank, world)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+            if args.out:
+                Path(args.out).write_text(json.dumps(line) + "\n")
+        return
+
+    import torch
+    rank, world, local = dist_setup("nccl")
+    backend, r = run_engine(args, rank, world, local)
+    K = args.steps
+    peaks = measured_peaks()
+    prof = r["prof"]
+    g = prof["decode_gemv"]
+    achieved = (g["bytes"] / 1e9) / (g["ms"] / 1e3) if g["ms"] > 0 else None
+    dev_sorted = sorted(d for gr in r["gathered"] for d in gr["dev_ms"])
+    p50 = statistics.median(dev_sorted)
+    p99 = dev_sorted[min(len(dev_sorted) - 1, int(round(0.99 * (len(dev_sorted) - 1))))]
+    s0, s1 = r["stats0"], r["stats1"]
+    value = world * K / r["total_max"]
+    e2e = world * K / r["host_max"]
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            threads = os.cpu_count() or 1
+            sample = cpu_sample(args.config, threads)
+            shapes = workload_shapes(args.config, 0, args.warmup, K, args.mode)
+            ms = statistics.mean(extrapolate_ms(sample, s) for s in shapes)
+            cpu = {"value": 1000.0 / ms, "unit": "steps/s", "cores": threads, "kind": "port",
+                   "sample": (f"CPU oracle ({sample['model']}, fp32, {threads} threads): 47-token prefill + 4 "
+                              f"decode tokens timed, extrapolated to the timed steps' trunk/branch lengths "
+                              f"(depth x{sample['depth_scale']:.0f}); {ms:.0f} ms/step")}
+        except Exception as exc:  # the baseline must never sink the GPU line
+            cpu = {"value": None, "unit": "steps/s", "cores": os.cpu_count(), "kind": "port",
+                   "sample": f"failed: {exc!r}"}
+    if rank != 0:
+        return
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "steps/s",
+        "n_gpus": world,
+        "steps": K,
+        "warmup": args.warmup,
+        "ms_per_step": 1000.0 * r["total_max"] / K,
+        "p50_ms": p50,
+        "p99_ms": p99,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": args.dtype,
+        "data": "synthetic",
+        "config": {"workload": "config 2: 7B-shaped ECoT VLA (Llama-2-7B decoder + 256 vision tokens), "
+                               "random-init weights, one episode per GPU, Fast ECoT parallel_sync",
+                   "model": args.config, "mode": args.mode, "episodes_per_gpu": 1, "slots": 8,
+                   "l2": "no flush: every decode iteration streams 13.2 GB of weights (> 126 MB L2)"},
+        "e2e": {"value": e2e, "unit": "steps/s",
+                "h2d_bytes_per_step": (s1["h2d_bytes"] - s0["h2d_bytes"]) / K,
+                "d2h_bytes_per_step": (s1["d2h_bytes"] - s0["d2h_bytes"]) / K},
+        "gpu_launches": s1["launches"] - s0["launches"],
+        "roofline": {"bound": "hbm", "kernel": "decode GEMV (QKV/O/gate-up/down/lm_head, bf16 weights)",
+                     "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                     "frac": (achieved / peaks["hbm_gbs"]) if achieved else None, "traffic": ncu_traffic(),
+                     "peak_source": peaks["source"],
+                     "launches": g["launches"], "ms_total": g["ms"],
+                     "share_of_step": g["ms"] / (1000.0 * r["total_max"])},
+        "cpu_baseline": cpu,
+        "clocks": r["clocks"],
+        "breakdown_ms": {k: v["ms"] / K for k, v in prof.items()},
+        "decode_ticks_per_step": (s1["ticks"] - s0["ticks"]) / K,
+        **r["extras"],
+    }
+    print(json.dumps(line), flush=True)
+    if args.out:
+        Path(args.out).write_text(json.dumps(line) + "\n")
+    backend.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -88,7 +88,13 @@ int fe_in_flight(fe_engine* e, int32_t* n);
 
 int fe_synchronize(fe_engine* e);
 int fe_stream(fe_engine* e, void** stream);
-int fe_stats(fe_engine* e, int64_t* out, int32_t n);  /* ticks, forwards, launches, pages used, ... */
+/* ticks, forwards, rows, pages used, pages total, page bytes, H2D bytes, D2H bytes, kernel launches */
+int fe_stats(fe_engine* e, int64_t* out, int32_t n);
+/* CUDA-event timing of launches on the engine stream, per category
+ * (0 decode GEMVs, 1 decode attention, 2 decode forwards, 3 prefill forwards):
+ * out[3c] = ms, out[3c+1] = launches, out[3c+2] = algorithmic bytes */
+int fe_profile(fe_engine* e, int32_t enable);
+int fe_profile_read(fe_engine* e, double* out, int32_t n);
 
 /* kernel-level entry points (device pointers, engine stream), for parity tests */
 int fe_weight_ptr(fe_engine* e, int32_t tensor, int32_t layer, void** ptr, size_t* bytes);

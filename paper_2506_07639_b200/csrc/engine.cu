@@ -64,6 +64,14 @@ struct RowIn {
   bool head;
 };
 
+enum ProfCat { PROF_GEMV = 0, PROF_ATTN = 1, PROF_DECODE_FWD = 2, PROF_PREFILL_FWD = 3, PROF_NCAT = 4 };
+
+struct ProfRec {
+  int cat;
+  cudaEvent_t a, b;
+  double bytes;
+};
+
 }  // namespace
 
 struct fe_engine {
@@ -112,6 +120,14 @@ struct fe_engine {
 
   // stats
   int64_t n_ticks = 0, n_forwards = 0, n_rows_total = 0;
+  int64_t h2d_bytes = 0, d2h_bytes = 0, n_launches = 0;
+
+  // profiling (fe_profile)
+  bool prof_on = false;
+  std::vector<ProfRec> prof_recs;
+  int prof_used = 0;
+  double prof_ms[PROF_NCAT] = {}, prof_bytes[PROF_NCAT] = {};
+  int64_t prof_n[PROF_NCAT] = {};
 
   void* dalloc(size_t bytes) {
     void* p = nullptr;
@@ -154,6 +170,20 @@ int new_seq(fe_engine* e) {
   return s;
 }
 
+void flush_profile(fe_engine* e) {
+  if (e->prof_used == 0) return;
+  CK(cudaStreamSynchronize(e->stream));
+  for (int i = 0; i < e->prof_used; i++) {
+    const ProfRec& r = e->prof_recs[i];
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, r.a, r.b));
+    e->prof_ms[r.cat] += ms;
+    e->prof_bytes[r.cat] += r.bytes;
+    e->prof_n[r.cat]++;
+  }
+  e->prof_used = 0;
+}
+
 // Pinned staging buffer for one forward's metadata; waits for the buffer's
 // previous H2D copy to finish before reuse.
 unsigned char* next_meta(fe_engine* e, int* idx) {
@@ -164,6 +194,27 @@ unsigned char* next_meta(fe_engine* e, int* idx) {
   return e->meta_host[i];
 }
 
+// ---- profiling: CUDA events on the engine stream around launches ----------
+int prof_begin(fe_engine* e, int cat) {
+  if (!e->prof_on) return -1;
+  if (e->prof_used == (int)e->prof_recs.size()) {
+    ProfRec r{};
+    CK(cudaEventCreate(&r.a));
+    CK(cudaEventCreate(&r.b));
+    e->prof_recs.push_back(r);
+  }
+  const int i = e->prof_used++;
+  e->prof_recs[i].cat = cat;
+  CK(cudaEventRecord(e->prof_recs[i].a, e->stream));
+  return i;
+}
+
+void prof_end(fe_engine* e, int i, double bytes) {
+  if (i < 0) return;
+  e->prof_recs[i].bytes = bytes;
+  CK(cudaEventRecord(e->prof_recs[i].b, e->stream));
+}
+
 // One forward pass over `rows` (all positions must already be < seq.len+1 in
 // order).  Builds row metadata, the cascade work list and launches the layer
 // stack.  Host-side sequence lengths advance as rows are written.
@@ -172,6 +223,7 @@ void forward(fe_engine* e, const std::vector<RowIn>& rows, uint64_t vision_seed)
   const int n = (int)rows.size();
   if (n == 0) return;
   if (n > e->max_rows) throw Error("forward: too many rows");
+  if (e->prof_on && e->prof_used > 8192) flush_profile(e);  // only between forwards: all records closed
 
   std::vector<fe::RowMeta> meta(n);
   std::vector<int32_t> head_rows;
@@ -264,22 +316,50 @@ void forward(fe_engine* e, const std::vector<RowIn>& rows, uint64_t vision_seed)
 
   cudaStream_t st = e->stream;
   const int dt = e->dtype;
+  const bool decode = f.n_head_rows > 0;
+  const double el = (double)e->elem;
+  // algorithmic bytes of one GEMV launch: weights + staged input + fp32 output
+  auto gemv_bytes = [&](double N, double K, int rows) { return N * K * el + rows * K * el + rows * N * 4.0; };
+  double kv_bytes = 0;  // K+V bytes the cascade items stage (each shared page once per head)
+  for (const auto& it : items) {
+    int vmax = 0;
+    for (int j = 0; j < it.row_count; j++) vmax = std::max(vmax, irows[it.row_begin + j].valid);
+    kv_bytes += 2.0 * vmax * m.hd * m.H * el;
+  }
+  const int whole = prof_begin(e, decode ? PROF_DECODE_FWD : PROF_PREFILL_FWD);
+  e->h2d_bytes += total;
   fe::launch_embed(dt, f, m, e->w.embed, e->ws.out_tokens, e->ws.x, st);
   for (int l = 0; l < m.L; l++) {
     const fe::Weights::Layer& ly = e->layers[l];
+    int p;
     fe::launch_rmsnorm(dt, e->ws.x, ly.attn_norm, e->ws.xn, n, m.d, m.d, m.eps, nullptr, st);
+    p = decode ? prof_begin(e, PROF_GEMV) : -1;
     fe::launch_qkv(dt, f, m, ly.wqkv, e->ws.xn, e->ws.q, e->kv_pool, l, e->rope, st);
+    prof_end(e, p, gemv_bytes(3.0 * m.d, m.d, n));
+    p = decode ? prof_begin(e, PROF_ATTN) : -1;
     fe::launch_attention(dt, f, m, e->ws.q, e->kv_pool, l, e->ws.partial, e->ws.attn, st);
+    prof_end(e, p, kv_bytes);
+    p = decode ? prof_begin(e, PROF_GEMV) : -1;
     fe::launch_resid(dt, f, m.d, m.d, ly.wo, e->ws.attn, e->ws.x, st);
+    prof_end(e, p, gemv_bytes(m.d, m.d, n));
     fe::launch_rmsnorm(dt, e->ws.x, ly.ffn_norm, e->ws.xn, n, m.d, m.d, m.eps, nullptr, st);
+    p = decode ? prof_begin(e, PROF_GEMV) : -1;
     fe::launch_swiglu(dt, f, m.F, m.d, ly.wgu, e->ws.xn, e->ws.attn /* reused as the SwiGLU activation */, st);
+    prof_end(e, p, gemv_bytes(2.0 * m.F, m.d, n));
+    p = decode ? prof_begin(e, PROF_GEMV) : -1;
     fe::launch_resid(dt, f, m.d, m.F, ly.wdown, e->ws.attn, e->ws.x, st);
+    prof_end(e, p, gemv_bytes(m.d, m.F, n));
   }
-  if (f.n_head_rows > 0) {
+  if (decode) {
     fe::launch_rmsnorm(dt, e->ws.x, e->w.final_norm, e->ws.xn, f.n_head_rows, m.d, m.d, m.eps, f.head_rows, st);
+    const int p = prof_begin(e, PROF_GEMV);
     fe::launch_lm_head(dt, f, m, e->w.lm_head, e->ws.xn, e->ws.part_keys, e->ws.logits, e->ws.out_tokens, st);
+    prof_end(e, p, gemv_bytes(m.V, m.d, f.n_head_rows));
   }
+  prof_end(e, whole, 0.0);
   CK(cudaGetLastError());
+  // embed + per layer (2 norms, qkv, attention partial + merge, O, gate/up, down) + head
+  e->n_launches += 1 + 8 * m.L + (decode ? 3 : 0) - (items.empty() ? m.L : 0);
   e->n_forwards++;
   e->n_rows_total += n;
 }
@@ -495,6 +575,10 @@ void destroy(fe_engine* e) {
   cudaSetDevice(e->device);
   cudaStreamSynchronize(e->stream);
   for (void* p : e->allocs) cudaFree(p);
+  for (auto& r : e->prof_recs) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
   for (int i = 0; i < kMetaRing; i++) {
     if (e->meta_host[i]) cudaFreeHost(e->meta_host[i]);
     if (e->meta_ev[i]) cudaEventDestroy(e->meta_ev[i]);
@@ -563,6 +647,7 @@ int fe_seq_fork(fe_engine* e, int32_t parent, int32_t len, int32_t* child) {
     if (rem) {  // copy-on-write of the partially filled page
       const int np = alloc_page(e);
       fe::launch_page_copy(e->dtype, e->kv_pool, ppages[full], np, rem, e->m, e->stream);
+      e->n_launches++;
       s.pages.push_back(np);
     }
     s.len = len;
@@ -656,6 +741,7 @@ int fe_request_tokens(fe_engine* e, int32_t req, int32_t* out, int32_t cap) {
     if (cap < q.length) throw Error("output buffer too small");
     CK(cudaMemcpyAsync(out, e->ws.out_tokens + (size_t)q.arena * kRequestCap, sizeof(int32_t) * q.length,
                        cudaMemcpyDeviceToHost, e->stream));
+    e->d2h_bytes += (int64_t)sizeof(int32_t) * q.length;
     CK(cudaStreamSynchronize(e->stream));
   });
 }
@@ -707,11 +793,34 @@ int fe_stream(fe_engine* e, void** stream) {
   return guarded(e, [&] { *stream = (void*)e->stream; });
 }
 
+int fe_profile(fe_engine* e, int32_t enable) {
+  return guarded(e, [&] {
+    flush_profile(e);
+    e->prof_on = enable != 0;
+    for (int c = 0; c < PROF_NCAT; c++) {
+      e->prof_ms[c] = 0.0;
+      e->prof_bytes[c] = 0.0;
+      e->prof_n[c] = 0;
+    }
+  });
+}
+
+int fe_profile_read(fe_engine* e, double* out, int32_t n) {
+  return guarded(e, [&] {
+    flush_profile(e);
+    for (int c = 0; c < PROF_NCAT && 3 * c + 2 < n; c++) {
+      out[3 * c] = e->prof_ms[c];
+      out[3 * c + 1] = (double)e->prof_n[c];
+      out[3 * c + 2] = e->prof_bytes[c];
+    }
+  });
+}
+
 int fe_stats(fe_engine* e, int64_t* out, int32_t n) {
   return guarded(e, [&] {
     const int64_t v[] = {e->n_ticks, e->n_forwards, e->n_rows_total,
                          (int64_t)(e->n_pages - (int)e->free_pages.size()), (int64_t)e->n_pages,
-                         (int64_t)(e->page_elems * e->elem)};
+                         (int64_t)(e->page_elems * e->elem), e->h2d_bytes, e->d2h_bytes, e->n_launches};
     for (int i = 0; i < n && i < (int)(sizeof(v) / sizeof(v[0])); i++) out[i] = v[i];
   });
 }

@@ -38,7 +38,8 @@ EXPORTS = (
     "fe_engine_create", "fe_engine_destroy", "fe_weights_init_random", "fe_last_error",
     "fe_seq_create", "fe_seq_fork", "fe_seq_free", "fe_seq_len", "fe_prefill", "fe_set_slots",
     "fe_submit", "fe_run", "fe_request_tokens", "fe_request_release", "fe_request_capture_logits",
-    "fe_request_logits", "fe_in_flight", "fe_synchronize", "fe_stream", "fe_stats",
+    "fe_request_logits", "fe_in_flight", "fe_synchronize", "fe_stream", "fe_stats", "fe_profile",
+    "fe_profile_read",
     "fe_weight_ptr", "fe_memcpy", "fe_op_gemv", "fe_op_rmsnorm",
 )
 
@@ -74,6 +75,8 @@ def load_library(path: Path = LIB_PATH) -> ctypes.CDLL:
         "fe_synchronize": [vp],
         "fe_stream": [vp, ctypes.POINTER(vp)],
         "fe_stats": [vp, vp, i32],
+        "fe_profile": [vp, i32],
+        "fe_profile_read": [vp, vp, i32],
         "fe_weight_ptr": [vp, i32, i32, ctypes.POINTER(vp), ctypes.POINTER(ctypes.c_size_t)],
         "fe_memcpy": [vp, vp, vp, ctypes.c_size_t],
         "fe_op_gemv": [vp, vp, i32, i32, vp, i32, vp],
@@ -207,10 +210,23 @@ class Engine:
         return p.value or 0
 
     def stats(self) -> dict:
-        out = np.zeros(6, dtype=np.int64)
+        out = np.zeros(9, dtype=np.int64)
         self._check(self.lib.fe_stats(self._h, _np_ptr(out), out.size))
-        keys = ("ticks", "forwards", "rows", "pages_used", "pages_total", "page_bytes")
+        keys = ("ticks", "forwards", "rows", "pages_used", "pages_total", "page_bytes", "h2d_bytes", "d2h_bytes",
+                "launches")
         return dict(zip(keys, out.tolist()))
+
+    PROFILE_CATEGORIES = ("decode_gemv", "decode_attention", "decode_forward", "prefill_forward")
+
+    def profile(self, enable: bool) -> None:
+        """Start (and reset) or stop CUDA-event timing of engine launches."""
+        self._check(self.lib.fe_profile(self._h, int(enable)))
+
+    def profile_read(self) -> dict:
+        out = np.zeros(3 * len(self.PROFILE_CATEGORIES), dtype=np.float64)
+        self._check(self.lib.fe_profile_read(self._h, _np_ptr(out), out.size))
+        return {c: {"ms": out[3 * i], "launches": int(out[3 * i + 1]), "bytes": out[3 * i + 2]}
+                for i, c in enumerate(self.PROFILE_CATEGORIES)}
 
     # -- kernel-level hooks (device pointers) ----------------------------------
     def weight_ptr(self, tensor: int, layer: int = 0) -> tuple[int, int]:

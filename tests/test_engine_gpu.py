@@ -77,6 +77,7 @@ def test_gemv_bit_exact_vs_oracle(tiny_f32, oracle_tiny, rows):
     x = torch.randn(rows, K, generator=torch.Generator().manual_seed(rows)).float()
     xd = x.cuda()
     y = torch.empty(rows, N, device="cuda")
+    torch.cuda.synchronize()  # inputs written on torch's stream, kernel runs on the engine stream
     tiny_f32.op_gemv(ptr, N, K, xd.data_ptr(), rows, y.data_ptr())
     tiny_f32.synchronize()
     W = oracle_tiny.tensor(M.layer_tensor(2, M.L_WGATE), 2, (N, K))
@@ -91,7 +92,9 @@ def test_rmsnorm_bit_exact(tiny_f32, oracle_tiny):
     x = torch.randn(5, d, generator=torch.Generator().manual_seed(1))
     w = torch.from_numpy(M.init_norm(0, 99, d))
     out = torch.empty(5, d, device="cuda")
-    tiny_f32.op_rmsnorm(x.cuda().data_ptr(), w.cuda().data_ptr(), out.data_ptr(), 5, d)
+    xd, wd = x.cuda(), w.cuda()  # keep references: temporaries would return to torch's cache
+    torch.cuda.synchronize()
+    tiny_f32.op_rmsnorm(xd.data_ptr(), wd.data_ptr(), out.data_ptr(), 5, d)
     tiny_f32.synchronize()
     want = np.zeros((5, d), dtype=np.float32)
     xn, wn = np.ascontiguousarray(x.numpy()), np.ascontiguousarray(w.numpy())
@@ -133,7 +136,7 @@ def test_fork_cow_branch_equals_fresh_sequence(tiny_f32, oracle_tiny):
     trunk = eng.seq_create()
     eng.prefill(trunk, ids[:-1], 77, M.VIS_ID)
     reqs, seqs = [], []
-    for cut in (len(ids) - 1, 70, 64, 1):
+    for cut in (len(ids) - 1, 70, 64, 20):  # forks after the vision block (pos >= 17)
         b = eng.seq_fork(trunk, cut)
         seqs.append(b)
         reqs.append((cut, eng.submit(b, ids[cut] if cut < len(ids) - 1 else ids[-1], 5, 1)))
