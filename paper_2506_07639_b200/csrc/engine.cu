@@ -9,6 +9,7 @@
 // (SPEC.md:166, :250): it is the decoder of DESIGN.md.
 #include "common.cuh"
 #include "engine_internal.h"
+#include "gemm_tc.h"
 #include "../../include/fastecot.h"
 
 #include <algorithm>
@@ -117,6 +118,15 @@ struct fe_engine {
   uint64_t seqno = 0;
   std::vector<int> free_arena;
   int capture_req = -1;
+
+  // tcgen05 GEMM path (bf16, wide forwards)
+  struct LayerMaps {
+    fe::TmaMap qkv, wo, wgu, wdown;
+  };
+  bool use_tc = false;
+  int tc_min_rows = 64;
+  std::vector<LayerMaps> tc_maps;
+  fe::TmaMap map_xn{}, map_attn{}, map_act{};
 
   // stats
   int64_t n_ticks = 0, n_forwards = 0, n_rows_total = 0;
@@ -329,25 +339,45 @@ void forward(fe_engine* e, const std::vector<RowIn>& rows, uint64_t vision_seed)
   const int whole = prof_begin(e, decode ? PROF_DECODE_FWD : PROF_PREFILL_FWD);
   e->h2d_bytes += total;
   fe::launch_embed(dt, f, m, e->w.embed, e->ws.out_tokens, e->ws.x, st);
+  // dense contractions of wide forwards go to the tcgen05 GEMM (bf16 only)
+  const bool tc = e->use_tc && n >= e->tc_min_rows;
+  auto tc_launch = [&](int epi, const fe::TmaMap& amap, const fe::TmaMap& bmap, int N, int K) {
+    fe::TcLaunch t{};
+    t.M = n; t.N = N; t.K = K; t.epi = epi;
+    t.y = e->ws.x; t.ldy = m.d;
+    t.act = (__nv_bfloat16*)e->ws.attn; t.F = m.F;
+    t.q = e->ws.q; t.kv_pool = (__nv_bfloat16*)e->kv_pool; t.page_elems = e->page_elems;
+    t.rope = e->rope; t.rows = f.rows; t.H = m.H; t.hd = m.hd; t.d = m.d;
+    return t;
+  };
   for (int l = 0; l < m.L; l++) {
     const fe::Weights::Layer& ly = e->layers[l];
     int p;
     fe::launch_rmsnorm(dt, e->ws.x, ly.attn_norm, e->ws.xn, n, m.d, m.d, m.eps, nullptr, st);
     p = decode ? prof_begin(e, PROF_GEMV) : -1;
-    fe::launch_qkv(dt, f, m, ly.wqkv, e->ws.xn, e->ws.q, e->kv_pool, l, e->rope, st);
+    if (tc) {
+      fe::TcLaunch t = tc_launch(fe::TC_QKV, e->map_xn, e->tc_maps[l].qkv, 3 * m.d, m.d);
+      t.layer_off = (size_t)l * 2 * m.H * FE_PAGE * m.hd;
+      fe::launch_gemm_tc(e->map_xn, e->tc_maps[l].qkv, t, st);
+    } else {
+      fe::launch_qkv(dt, f, m, ly.wqkv, e->ws.xn, e->ws.q, e->kv_pool, l, e->rope, st);
+    }
     prof_end(e, p, gemv_bytes(3.0 * m.d, m.d, n));
     p = decode ? prof_begin(e, PROF_ATTN) : -1;
     fe::launch_attention(dt, f, m, e->ws.q, e->kv_pool, l, e->ws.partial, e->ws.attn, st);
     prof_end(e, p, kv_bytes);
     p = decode ? prof_begin(e, PROF_GEMV) : -1;
-    fe::launch_resid(dt, f, m.d, m.d, ly.wo, e->ws.attn, e->ws.x, st);
+    if (tc) fe::launch_gemm_tc(e->map_attn, e->tc_maps[l].wo, tc_launch(fe::TC_RESID, e->map_attn, e->tc_maps[l].wo, m.d, m.d), st);
+    else fe::launch_resid(dt, f, m.d, m.d, ly.wo, e->ws.attn, e->ws.x, st);
     prof_end(e, p, gemv_bytes(m.d, m.d, n));
     fe::launch_rmsnorm(dt, e->ws.x, ly.ffn_norm, e->ws.xn, n, m.d, m.d, m.eps, nullptr, st);
     p = decode ? prof_begin(e, PROF_GEMV) : -1;
-    fe::launch_swiglu(dt, f, m.F, m.d, ly.wgu, e->ws.xn, e->ws.attn /* reused as the SwiGLU activation */, st);
+    if (tc) fe::launch_gemm_tc(e->map_xn, e->tc_maps[l].wgu, tc_launch(fe::TC_SWIGLU, e->map_xn, e->tc_maps[l].wgu, 2 * m.F, m.d), st);
+    else fe::launch_swiglu(dt, f, m.F, m.d, ly.wgu, e->ws.xn, e->ws.attn /* reused as the SwiGLU activation */, st);
     prof_end(e, p, gemv_bytes(2.0 * m.F, m.d, n));
     p = decode ? prof_begin(e, PROF_GEMV) : -1;
-    fe::launch_resid(dt, f, m.d, m.F, ly.wdown, e->ws.attn, e->ws.x, st);
+    if (tc) fe::launch_gemm_tc(e->map_act, e->tc_maps[l].wdown, tc_launch(fe::TC_RESID, e->map_act, e->tc_maps[l].wdown, m.d, m.F), st);
+    else fe::launch_resid(dt, f, m.d, m.F, ly.wdown, e->ws.attn, e->ws.x, st);
     prof_end(e, p, gemv_bytes(m.d, m.F, n));
   }
   if (decode) {
@@ -563,6 +593,24 @@ fe_engine* create(const fe_config* c, int device, const float* rope_host) {
     e->page_ref.assign(pages, 0);
     for (int p = (int)pages - 1; p >= 0; p--) e->free_pages.push_back(p);
     e->slot_req.assign(e->max_slots, -1);
+
+    // tensor maps for the tcgen05 path: weights (B operand) and the staged
+    // activation buffers (A operand), all K-major bf16 with 128B swizzle
+    e->use_tc = e->dtype == FE_BF16 && m.hd == 128 && m.d % 128 == 0 && m.F % 64 == 0 && e->max_rows >= 64;
+    if (e->use_tc) {
+      const int R = e->max_rows;
+      e->map_xn = fe::make_kmajor_map(e->ws.xn, R, m.d, m.d, 128);
+      e->map_attn = fe::make_kmajor_map(e->ws.attn, R, m.d, m.d, 128);
+      e->map_act = fe::make_kmajor_map(e->ws.attn, R, m.F, m.F, 128);
+      e->tc_maps.resize(m.L);
+      for (int l = 0; l < m.L; l++) {
+        auto& ly = e->layers[l];
+        e->tc_maps[l].qkv = fe::make_kmajor_map(ly.wqkv, 3 * m.d, m.d, m.d, 128);
+        e->tc_maps[l].wo = fe::make_kmajor_map(ly.wo, m.d, m.d, m.d, 128);
+        e->tc_maps[l].wgu = fe::make_kmajor_map(ly.wgu, 2 * m.F, m.d, m.d, fe::tc_box_rows(fe::TC_SWIGLU));
+        e->tc_maps[l].wdown = fe::make_kmajor_map(ly.wdown, m.d, m.F, m.F, 128);
+      }
+    }
   } catch (...) {
     for (void* p : e->allocs) cudaFree(p);
     delete e;
@@ -860,6 +908,27 @@ int fe_op_gemv(fe_engine* e, const void* w, int32_t N, int32_t K, const void* x,
     if (N % 4 || K % 8) throw Error("gemv: N % 4 and K % 8 must be 0");
     fe::launch_gemv_store(e->dtype, w, N, K, x, rows, y, e->stream);
     CK(cudaGetLastError());
+  });
+}
+
+int fe_op_gemm_tc(fe_engine* e, const void* x, const void* w, int32_t M, int32_t N, int32_t K, float* y) {
+  return guarded(e, [&] {
+    if (N % 128 || K % 64) throw Error("gemm_tc: N % 128 and K % 64 must be 0");
+    const fe::TmaMap am = fe::make_kmajor_map(x, M, K, K, 128);
+    const fe::TmaMap bm = fe::make_kmajor_map(w, N, K, K, 128);
+    fe::TcLaunch t{};
+    t.M = M; t.N = N; t.K = K; t.epi = fe::TC_STORE; t.y = y; t.ldy = N;
+    fe::launch_gemm_tc(am, bm, t, e->stream);
+    CK(cudaGetLastError());
+  });
+}
+
+int fe_set_option(fe_engine* e, const char* key, int64_t value) {
+  return guarded(e, [&] {
+    const std::string k = key ? key : "";
+    if (k == "tc_min_rows") e->tc_min_rows = (int)value;
+    else if (k == "use_tc") e->use_tc = value != 0 && !e->tc_maps.empty();
+    else throw Error("unknown option " + k);
   });
 }
 

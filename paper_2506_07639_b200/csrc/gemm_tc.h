@@ -1,0 +1,38 @@
+// tcgen05 GEMM interface (gemm_tc.cu).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stddef.h>
+
+namespace fe {
+
+struct RowMeta;
+
+enum TcEpi { TC_STORE = 0, TC_QKV = 1, TC_RESID = 2, TC_SWIGLU = 3 };
+
+// Opaque CUtensorMap storage (128 bytes, 64-byte aligned).
+struct alignas(64) TmaMap {
+  unsigned char bytes[128];
+};
+
+struct TcLaunch {
+  int M, N, K, epi;
+  float* y;
+  int ldy;
+  __nv_bfloat16* act;
+  int F;
+  float* q;
+  __nv_bfloat16* kv_pool;
+  size_t page_elems, layer_off;
+  const float* rope;
+  const RowMeta* rows;
+  int H, hd, d;
+};
+
+// 2-D K-major bf16 tensor [rows][K] with row stride ld_elems, box [box_rows x 64], 128B swizzle
+TmaMap make_kmajor_map(const void* base, int rows, int K, int ld_elems, int box_rows);
+int tc_box_rows(int epi);
+void launch_gemm_tc(const TmaMap& a_map, const TmaMap& b_map, const TcLaunch& l, cudaStream_t s);
+
+}  // namespace fe
