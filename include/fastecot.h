@@ -103,6 +103,8 @@ int fe_op_gemv(fe_engine* e, const void* w, int32_t N, int32_t K, const void* x,
 int fe_op_rmsnorm(fe_engine* e, const float* x, const float* w, void* out, int32_t rows, int32_t d);
 /* bf16 tcgen05 GEMM: y[M][N] (fp32) = x[M][K] . w[N][K]^T */
 int fe_op_gemm_tc(fe_engine* e, const void* x, const void* w, int32_t M, int32_t N, int32_t K, float* y);
+/* bf16 tcgen05 swap-AB decode GEMM (M <= 16 rows): y[M][N] = x[M][K] . w[N][K]^T */
+int fe_op_skinny_tc(fe_engine* e, const void* x, const void* w, int32_t M, int32_t N, int32_t K, float* y);
 /* engine options: "tc_min_rows" (rows from which a forward uses the tcgen05
  * GEMMs, bf16 only), "use_tc" (0/1) */
 int fe_set_option(fe_engine* e, const char* key, int64_t value);

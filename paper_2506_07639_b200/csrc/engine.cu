@@ -124,9 +124,14 @@ struct fe_engine {
     fe::TmaMap qkv, wo, wgu, wdown;
   };
   bool use_tc = false;
-  int tc_min_rows = 64;
+  int tc_min_rows = 17;
+  int sk_mask = 31;  // skinny path per matrix: 1 QKV, 2 O, 4 gate/up, 8 down, 16 lm_head
   std::vector<LayerMaps> tc_maps;
-  fe::TmaMap map_xn{}, map_attn{}, map_act{};
+  fe::TmaMap map_xn{}, map_attn{}, map_act{};          // 128-row boxes (prefill GEMM A operand)
+  fe::TmaMap map_xn16{}, map_attn16{}, map_act16{};    // 16-row boxes (skinny GEMM B operand)
+  fe::TmaMap map_lm{};
+  float* sk_partial = nullptr;
+  int* sk_counters = nullptr;
 
   // stats
   int64_t n_ticks = 0, n_forwards = 0, n_rows_total = 0;
@@ -148,6 +153,11 @@ struct fe_engine {
 };
 
 namespace {
+
+const fe_engine::LayerMaps& EngineMapsDummy() {
+  static fe_engine::LayerMaps d{};
+  return d;
+}
 
 int alloc_page(fe_engine* e) {
   if (e->free_pages.empty()) throw Error("KV pool exhausted (" + std::to_string(e->n_pages) + " pages)");
@@ -339,9 +349,12 @@ void forward(fe_engine* e, const std::vector<RowIn>& rows, uint64_t vision_seed)
   const int whole = prof_begin(e, decode ? PROF_DECODE_FWD : PROF_PREFILL_FWD);
   e->h2d_bytes += total;
   fe::launch_embed(dt, f, m, e->w.embed, e->ws.out_tokens, e->ws.x, st);
-  // dense contractions of wide forwards go to the tcgen05 GEMM (bf16 only)
-  const bool tc = e->use_tc && n >= e->tc_min_rows;
-  auto tc_launch = [&](int epi, const fe::TmaMap& amap, const fe::TmaMap& bmap, int N, int K) {
+  // bf16: skinny tcgen05 swap-AB GEMM for <= 16 rows (decode), the tile
+  // tcgen05 GEMM for wide forwards (prefill); fp32: canonical CUDA-core GEMV
+  const bool sk_any = e->use_tc && n <= fe::skinny_max_rows();
+  const bool tc = e->use_tc && !sk_any && n >= e->tc_min_rows;
+  auto sk_on = [&](int bit) { return sk_any && (e->sk_mask >> bit & 1); };
+  auto tc_launch = [&](int epi, int N, int K) {
     fe::TcLaunch t{};
     t.M = n; t.N = N; t.K = K; t.epi = epi;
     t.y = e->ws.x; t.ldy = m.d;
@@ -350,15 +363,32 @@ void forward(fe_engine* e, const std::vector<RowIn>& rows, uint64_t vision_seed)
     t.rope = e->rope; t.rows = f.rows; t.H = m.H; t.hd = m.hd; t.d = m.d;
     return t;
   };
+  auto sk_launch = [&](int epi, int N, int K) {
+    fe::SkLaunch t{};
+    t.N = N; t.K = K; t.B = n; t.epi = epi;
+    t.partial = e->sk_partial; t.counters = e->sk_counters;
+    t.y = e->ws.x; t.ldy = m.d;
+    t.act = (__nv_bfloat16*)e->ws.attn; t.F = m.F;
+    t.q = e->ws.q; t.kv_pool = (__nv_bfloat16*)e->kv_pool; t.page_elems = e->page_elems;
+    t.rope = e->rope; t.rows = f.rows; t.head_rows = f.head_rows; t.H = m.H; t.hd = m.hd; t.d = m.d;
+    t.part_keys = e->ws.part_keys; t.logits = e->ws.logits; t.V = m.V; t.n_text = m.n_text;
+    return t;
+  };
   for (int l = 0; l < m.L; l++) {
     const fe::Weights::Layer& ly = e->layers[l];
+    const auto& mp = e->tc_maps.empty() ? EngineMapsDummy() : e->tc_maps[l];
+    const size_t layer_off = (size_t)l * 2 * m.H * FE_PAGE * m.hd;
     int p;
     fe::launch_rmsnorm(dt, e->ws.x, ly.attn_norm, e->ws.xn, n, m.d, m.d, m.eps, nullptr, st);
     p = decode ? prof_begin(e, PROF_GEMV) : -1;
-    if (tc) {
-      fe::TcLaunch t = tc_launch(fe::TC_QKV, e->map_xn, e->tc_maps[l].qkv, 3 * m.d, m.d);
-      t.layer_off = (size_t)l * 2 * m.H * FE_PAGE * m.hd;
-      fe::launch_gemm_tc(e->map_xn, e->tc_maps[l].qkv, t, st);
+    if (sk_on(0)) {
+      fe::SkLaunch t = sk_launch(fe::TC_QKV, 3 * m.d, m.d);
+      t.layer_off = layer_off;
+      fe::launch_skinny_tc(mp.qkv, e->map_xn16, t, st);
+    } else if (tc) {
+      fe::TcLaunch t = tc_launch(fe::TC_QKV, 3 * m.d, m.d);
+      t.layer_off = layer_off;
+      fe::launch_gemm_tc(e->map_xn, mp.qkv, t, st);
     } else {
       fe::launch_qkv(dt, f, m, ly.wqkv, e->ws.xn, e->ws.q, e->kv_pool, l, e->rope, st);
     }
@@ -367,23 +397,33 @@ void forward(fe_engine* e, const std::vector<RowIn>& rows, uint64_t vision_seed)
     fe::launch_attention(dt, f, m, e->ws.q, e->kv_pool, l, e->ws.partial, e->ws.attn, st);
     prof_end(e, p, kv_bytes);
     p = decode ? prof_begin(e, PROF_GEMV) : -1;
-    if (tc) fe::launch_gemm_tc(e->map_attn, e->tc_maps[l].wo, tc_launch(fe::TC_RESID, e->map_attn, e->tc_maps[l].wo, m.d, m.d), st);
+    if (sk_on(1)) fe::launch_skinny_tc(mp.wo, e->map_attn16, sk_launch(fe::TC_RESID, m.d, m.d), st);
+    else if (tc) fe::launch_gemm_tc(e->map_attn, mp.wo, tc_launch(fe::TC_RESID, m.d, m.d), st);
     else fe::launch_resid(dt, f, m.d, m.d, ly.wo, e->ws.attn, e->ws.x, st);
     prof_end(e, p, gemv_bytes(m.d, m.d, n));
     fe::launch_rmsnorm(dt, e->ws.x, ly.ffn_norm, e->ws.xn, n, m.d, m.d, m.eps, nullptr, st);
     p = decode ? prof_begin(e, PROF_GEMV) : -1;
-    if (tc) fe::launch_gemm_tc(e->map_xn, e->tc_maps[l].wgu, tc_launch(fe::TC_SWIGLU, e->map_xn, e->tc_maps[l].wgu, 2 * m.F, m.d), st);
+    if (sk_on(2)) fe::launch_skinny_tc(mp.wgu, e->map_xn16, sk_launch(fe::TC_SWIGLU, 2 * m.F, m.d), st);
+    else if (tc) fe::launch_gemm_tc(e->map_xn, mp.wgu, tc_launch(fe::TC_SWIGLU, 2 * m.F, m.d), st);
     else fe::launch_swiglu(dt, f, m.F, m.d, ly.wgu, e->ws.xn, e->ws.attn /* reused as the SwiGLU activation */, st);
     prof_end(e, p, gemv_bytes(2.0 * m.F, m.d, n));
     p = decode ? prof_begin(e, PROF_GEMV) : -1;
-    if (tc) fe::launch_gemm_tc(e->map_act, e->tc_maps[l].wdown, tc_launch(fe::TC_RESID, e->map_act, e->tc_maps[l].wdown, m.d, m.F), st);
+    if (sk_on(3)) fe::launch_skinny_tc(mp.wdown, e->map_act16, sk_launch(fe::TC_RESID, m.d, m.F), st);
+    else if (tc) fe::launch_gemm_tc(e->map_act, mp.wdown, tc_launch(fe::TC_RESID, m.d, m.F), st);
     else fe::launch_resid(dt, f, m.d, m.F, ly.wdown, e->ws.attn, e->ws.x, st);
     prof_end(e, p, gemv_bytes(m.d, m.F, n));
   }
   if (decode) {
     fe::launch_rmsnorm(dt, e->ws.x, e->w.final_norm, e->ws.xn, f.n_head_rows, m.d, m.d, m.eps, f.head_rows, st);
     const int p = prof_begin(e, PROF_GEMV);
-    fe::launch_lm_head(dt, f, m, e->w.lm_head, e->ws.xn, e->ws.part_keys, e->ws.logits, e->ws.out_tokens, st);
+    if (e->use_tc && (e->sk_mask >> 4 & 1) && f.n_head_rows <= fe::skinny_max_rows()) {
+      fe::SkLaunch t = sk_launch(fe::TC_ARGMAX, m.V, m.d);
+      t.B = f.n_head_rows;
+      fe::launch_skinny_tc(e->map_lm, e->map_xn16, t, st);
+      fe::launch_finalize(f, e->ws.part_keys, fe::skinny_tiles(fe::TC_ARGMAX, m.V, m.F), e->ws.out_tokens, st);
+    } else {
+      fe::launch_lm_head(dt, f, m, e->w.lm_head, e->ws.xn, e->ws.part_keys, e->ws.logits, e->ws.out_tokens, st);
+    }
     prof_end(e, p, gemv_bytes(m.V, m.d, f.n_head_rows));
   }
   prof_end(e, whole, 0.0);
@@ -602,6 +642,14 @@ fe_engine* create(const fe_config* c, int device, const float* rope_host) {
       e->map_xn = fe::make_kmajor_map(e->ws.xn, R, m.d, m.d, 128);
       e->map_attn = fe::make_kmajor_map(e->ws.attn, R, m.d, m.d, 128);
       e->map_act = fe::make_kmajor_map(e->ws.attn, R, m.F, m.F, 128);
+      e->map_xn16 = fe::make_kmajor_map(e->ws.xn, R, m.d, m.d, fe::skinny_max_rows());
+      e->map_attn16 = fe::make_kmajor_map(e->ws.attn, R, m.d, m.d, fe::skinny_max_rows());
+      e->map_act16 = fe::make_kmajor_map(e->ws.attn, R, m.F, m.F, fe::skinny_max_rows());
+      e->map_lm = fe::make_kmajor_map(e->w.lm_head, m.V, m.d, m.d, 128);
+      const size_t part_floats = (size_t)64 * std::max<size_t>(3 * m.d, 2 * (size_t)m.F) * fe::skinny_max_rows();
+      e->sk_partial = (float*)e->dalloc(part_floats * 4);
+      e->sk_counters = (int*)e->dalloc(4096 * sizeof(int));
+      CK(cudaMemset(e->sk_counters, 0, 4096 * sizeof(int)));
       e->tc_maps.resize(m.L);
       for (int l = 0; l < m.L; l++) {
         auto& ly = e->layers[l];
@@ -923,11 +971,30 @@ int fe_op_gemm_tc(fe_engine* e, const void* x, const void* w, int32_t M, int32_t
   });
 }
 
+int fe_op_skinny_tc(fe_engine* e, const void* x, const void* w, int32_t M, int32_t N, int32_t K, float* y) {
+  return guarded(e, [&] {
+    if (M > fe::skinny_max_rows() || N % 128 || K % 64) throw Error("skinny_tc: M <= 16, N % 128, K % 64");
+    if (!e->sk_partial) {
+      e->sk_partial = (float*)e->dalloc((size_t)64 * N * 16 * 4);
+      e->sk_counters = (int*)e->dalloc(4096 * sizeof(int));
+      CK(cudaMemset(e->sk_counters, 0, 4096 * sizeof(int)));
+    }
+    const fe::TmaMap xm = fe::make_kmajor_map(x, M, K, K, fe::skinny_max_rows());
+    const fe::TmaMap wm = fe::make_kmajor_map(w, N, K, K, 128);
+    fe::SkLaunch t{};
+    t.N = N; t.K = K; t.B = M; t.epi = fe::TC_STORE; t.y = y; t.ldy = N;
+    t.partial = e->sk_partial; t.counters = e->sk_counters;
+    fe::launch_skinny_tc(wm, xm, t, e->stream);
+    CK(cudaGetLastError());
+  });
+}
+
 int fe_set_option(fe_engine* e, const char* key, int64_t value) {
   return guarded(e, [&] {
     const std::string k = key ? key : "";
     if (k == "tc_min_rows") e->tc_min_rows = (int)value;
     else if (k == "use_tc") e->use_tc = value != 0 && !e->tc_maps.empty();
+    else if (k == "sk_mask") e->sk_mask = (int)value;
     else throw Error("unknown option " + k);
   });
 }

@@ -99,6 +99,8 @@ void launch_swiglu(int dtype, const Fwd& f, int F, int K, const void* w, const v
                    cudaStream_t s);
 void launch_lm_head(int dtype, const Fwd& f, const ModelDims& m, const void* w, const void* xn,
                     unsigned long long* part_keys, float* logits, int32_t* out_tokens, cudaStream_t s);
+void launch_finalize(const Fwd& f, const unsigned long long* part_keys, int n_ctas, int32_t* out_tokens,
+                     cudaStream_t s);
 void launch_page_copy(int dtype, void* pool, int src, int dst, int n_slots, const ModelDims& m,
                       cudaStream_t s);
 // plain y[n][N] = x[n][K] . W^T (parity tests)

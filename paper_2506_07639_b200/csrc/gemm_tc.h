@@ -4,12 +4,13 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stddef.h>
+#include <stdint.h>
 
 namespace fe {
 
 struct RowMeta;
 
-enum TcEpi { TC_STORE = 0, TC_QKV = 1, TC_RESID = 2, TC_SWIGLU = 3 };
+enum TcEpi { TC_STORE = 0, TC_QKV = 1, TC_RESID = 2, TC_SWIGLU = 3, TC_ARGMAX = 4 };
 
 // Opaque CUtensorMap storage (128 bytes, 64-byte aligned).
 struct alignas(64) TmaMap {
@@ -30,9 +31,33 @@ struct TcLaunch {
   int H, hd, d;
 };
 
+// skinny decode GEMM (swap-AB, <= skinny_max_rows() batch rows)
+struct SkLaunch {
+  int N, K, B, epi;
+  float* partial;
+  int* counters;
+  float* y;
+  int ldy;
+  __nv_bfloat16* act;
+  int F;
+  float* q;
+  __nv_bfloat16* kv_pool;
+  size_t page_elems, layer_off;
+  const float* rope;
+  const RowMeta* rows;
+  const int32_t* head_rows;
+  int H, hd, d;
+  unsigned long long* part_keys;
+  float* logits;
+  int V, n_text;
+};
+
 // 2-D K-major bf16 tensor [rows][K] with row stride ld_elems, box [box_rows x 64], 128B swizzle
 TmaMap make_kmajor_map(const void* base, int rows, int K, int ld_elems, int box_rows);
 int tc_box_rows(int epi);
 void launch_gemm_tc(const TmaMap& a_map, const TmaMap& b_map, const TcLaunch& l, cudaStream_t s);
+int skinny_max_rows();
+int skinny_tiles(int epi, int N, int F);
+void launch_skinny_tc(const TmaMap& w_map, const TmaMap& x_map, const SkLaunch& l, cudaStream_t s);
 
 }  // namespace fe

@@ -92,9 +92,52 @@ __global__ void rmsnorm_kernel(const float* __restrict__ x, const float* __restr
   for (int k = lane; k < d; k += 32) o[k] = Elem<XT>::from_f(__fmul_rn(__fmul_rn(xr[k], r), w[k]));
 }
 
+// bf16 mode: one 256-thread block per row, 8 elements per thread-step,
+// block-wide sum of squares (free reduction order).
+__global__ void __launch_bounds__(256)
+rmsnorm_bf16_kernel(const float* __restrict__ x, const float* __restrict__ w, __nv_bfloat16* __restrict__ out,
+                    int d, int ld_out, float eps, const int32_t* __restrict__ row_index) {
+  __shared__ float red[8];
+  const int row = blockIdx.x;
+  const int src = row_index ? row_index[row] : row;
+  const float* xr = x + (size_t)src * d;
+  float ss = 0.0f;
+  for (int k = 8 * threadIdx.x; k < d; k += 8 * blockDim.x) {
+    const float4 a = *reinterpret_cast<const float4*>(xr + k);
+    const float4 b = *reinterpret_cast<const float4*>(xr + k + 4);
+    ss = fmaf(a.x, a.x, fmaf(a.y, a.y, fmaf(a.z, a.z, fmaf(a.w, a.w, ss))));
+    ss = fmaf(b.x, b.x, fmaf(b.y, b.y, fmaf(b.z, b.z, fmaf(b.w, b.w, ss))));
+  }
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  float tot = 0.0f;
+#pragma unroll
+  for (int i = 0; i < 8; i++) tot += red[i];
+  const float r = rsqrtf(tot / (float)d + eps);
+  __nv_bfloat16* o = out + (size_t)row * ld_out;
+  for (int k = 8 * threadIdx.x; k < d; k += 8 * blockDim.x) {
+    const float4 a = *reinterpret_cast<const float4*>(xr + k);
+    const float4 b = *reinterpret_cast<const float4*>(xr + k + 4);
+    const float4 wa = *reinterpret_cast<const float4*>(w + k);
+    const float4 wb = *reinterpret_cast<const float4*>(w + k + 4);
+    __nv_bfloat162 v[4];
+    v[0] = __floats2bfloat162_rn(a.x * r * wa.x, a.y * r * wa.y);
+    v[1] = __floats2bfloat162_rn(a.z * r * wa.z, a.w * r * wa.w);
+    v[2] = __floats2bfloat162_rn(b.x * r * wb.x, b.y * r * wb.y);
+    v[3] = __floats2bfloat162_rn(b.z * r * wb.z, b.w * r * wb.w);
+    *reinterpret_cast<uint4*>(o + k) = *reinterpret_cast<const uint4*>(v);
+  }
+}
+
 void launch_rmsnorm(int dtype, const float* x, const float* w, void* out, int n_rows, int d, int ld_out,
                     float eps, const int32_t* row_index, cudaStream_t s) {
   if (n_rows == 0) return;
+  if (dtype == BF16) {
+    rmsnorm_bf16_kernel<<<n_rows, 256, 0, s>>>(x, w, (__nv_bfloat16*)out, d, ld_out, eps, row_index);
+    return;
+  }
   const int blocks = (n_rows + 7) / 8;
   if (dtype == F32) rmsnorm_kernel<float><<<blocks, 256, 0, s>>>(x, w, (float*)out, n_rows, d, ld_out, eps, row_index);
   else rmsnorm_kernel<__nv_bfloat16><<<blocks, 256, 0, s>>>(x, w, (__nv_bfloat16*)out, n_rows, d, ld_out, eps, row_index);
@@ -380,6 +423,11 @@ __global__ void finalize_kernel(const RowMeta* rows, const int32_t* head_rows, c
   }
 }
 
+void launch_finalize(const Fwd& f, const unsigned long long* part_keys, int n_ctas, int32_t* out_tokens,
+                     cudaStream_t s) {
+  if (f.n_head_rows > 0) finalize_kernel<<<f.n_head_rows, 256, 0, s>>>(f.rows, f.head_rows, part_keys, n_ctas, out_tokens);
+}
+
 void launch_lm_head(int dtype, const Fwd& f, const ModelDims& m, const void* w, const void* xn,
                     unsigned long long* part_keys, float* logits, int32_t* out_tokens, cudaStream_t s) {
   if (f.n_head_rows == 0) return;
@@ -518,6 +566,196 @@ attn_merge_kernel(const RowMeta* __restrict__ rows, const float* __restrict__ pa
   }
 }
 
+// ------------------------------------------------- bf16 (fast) attention ----
+// Same cascade work items as the canonical kernel, but free reduction order:
+// 8 warps per (page, head) CTA, one query row per warp; scores for 8 keys at a
+// time are reduced with a reduce-scatter butterfly (9 shuffles per 8 keys
+// instead of 5 per key), softmax in the exp2 domain with fast intrinsics.
+template <int HD>
+__global__ void __launch_bounds__(256)
+attn_partial_bf16_kernel(const AttnItem* __restrict__ items, const ItemRow* __restrict__ item_rows,
+                         const RowMeta* __restrict__ rows, const float* __restrict__ q,
+                         const __nv_bfloat16* __restrict__ pool, size_t page_elems, size_t layer_off, int H, int d,
+                         float scale_log2, float* __restrict__ partial) {
+  constexpr int DPL = HD / 32;  // head dims per lane
+  extern __shared__ __align__(16) unsigned char smem_kv[];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ float pbuf[8][FE_PAGE];
+  __nv_bfloat16* ks = reinterpret_cast<__nv_bfloat16*>(smem_kv);
+  __nv_bfloat16* vs = ks + FE_PAGE * HD;
+  const AttnItem it = items[blockIdx.x];
+  const int h = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  int vmax = 0;
+  for (int i = 0; i < it.row_count; i++) vmax = max(vmax, item_rows[it.row_begin + i].valid);
+  const __nv_bfloat16* kg = pool + (size_t)it.page * page_elems + layer_off + (size_t)h * FE_PAGE * HD;
+  const __nv_bfloat16* vg = kg + (size_t)H * FE_PAGE * HD;
+  const uint32_t bytes = (uint32_t)(vmax * HD * 2);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar)), "r"(2 * bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(ks)), "l"(kg), "r"(bytes), "r"(smem_u32(&bar)) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(vs)), "l"(vg), "r"(bytes), "r"(smem_u32(&bar)) : "memory");
+  }
+  for (int i = warp; i < it.row_count; i += 8) {
+    const ItemRow ir = item_rows[it.row_begin + i];
+    const RowMeta m = rows[ir.row];
+    float qv[DPL];
+#pragma unroll
+    for (int c = 0; c < DPL; c++) qv[c] = q[(size_t)ir.row * d + h * HD + DPL * lane + c] * scale_log2;
+    if (i == warp) {  // first row of this warp: wait for the K/V tiles
+      uint32_t done = 0;
+      while (!done)
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(done) : "r"(smem_u32(&bar)) : "memory");
+    }
+    // scores, 8 keys per step
+    for (int j0 = 0; j0 < ir.valid; j0 += 8) {
+      float part[8];
+#pragma unroll
+      for (int t = 0; t < 8; t++) {
+        const __nv_bfloat16* kr = ks + (j0 + t) * HD + DPL * lane;
+        float a = 0.0f;
+        if (DPL == 4) {
+          const uint2 raw = *reinterpret_cast<const uint2*>(kr);
+          a = fmaf(qv[0], __uint_as_float(raw.x << 16), a);
+          a = fmaf(qv[1], __uint_as_float(raw.x & 0xffff0000u), a);
+          a = fmaf(qv[2], __uint_as_float(raw.y << 16), a);
+          a = fmaf(qv[3], __uint_as_float(raw.y & 0xffff0000u), a);
+        } else {
+          const uint32_t raw = *reinterpret_cast<const uint32_t*>(kr);
+          a = fmaf(qv[0], __uint_as_float(raw << 16), a);
+          a = fmaf(qv[DPL - 1], __uint_as_float(raw & 0xffff0000u), a);
+        }
+        part[t] = a;
+      }
+      // reduce-scatter: after the xor-16/8/4 steps lane holds key (lane >> 2) & 7
+#pragma unroll
+      for (int t = 0; t < 4; t++) {
+        const bool up = lane & 16;
+        const float send = up ? part[t] : part[t + 4];
+        const float keep = up ? part[t + 4] : part[t];
+        part[t] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+      }
+#pragma unroll
+      for (int t = 0; t < 2; t++) {
+        const bool up = lane & 8;
+        const float send = up ? part[t] : part[t + 2];
+        const float keep = up ? part[t + 2] : part[t];
+        part[t] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+      }
+      {
+        const bool up = lane & 4;
+        const float send = up ? part[0] : part[1];
+        const float keep = up ? part[1] : part[0];
+        part[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+      }
+      float s = part[0];
+      s += __shfl_xor_sync(0xffffffffu, s, 2);
+      s += __shfl_xor_sync(0xffffffffu, s, 1);
+      const int j = j0 + ((lane >> 2) & 7);
+      if ((lane & 3) == 0) pbuf[warp][j] = j < ir.valid ? s : -INFINITY;
+    }
+    __syncwarp();
+    const float s0 = lane < ir.valid ? pbuf[warp][lane] : -INFINITY;
+    const float s1 = lane + 32 < ir.valid ? pbuf[warp][lane + 32] : -INFINITY;
+    float mx = fmaxf(s0, s1);
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    const float p0 = lane < ir.valid ? exp2f(s0 - mx) : 0.0f;
+    const float p1 = lane + 32 < ir.valid ? exp2f(s1 - mx) : 0.0f;
+    float l = p0 + p1;
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
+    __syncwarp();
+    pbuf[warp][lane] = p0;
+    pbuf[warp][lane + 32] = p1;
+    __syncwarp();
+    float o[DPL];
+#pragma unroll
+    for (int c = 0; c < DPL; c++) o[c] = 0.0f;
+    for (int j = 0; j < ir.valid; j++) {
+      const float p = pbuf[warp][j];
+      const __nv_bfloat16* vr = vs + j * HD + DPL * lane;
+      if (DPL == 4) {
+        const uint2 raw = *reinterpret_cast<const uint2*>(vr);
+        o[0] = fmaf(p, __uint_as_float(raw.x << 16), o[0]);
+        o[1] = fmaf(p, __uint_as_float(raw.x & 0xffff0000u), o[1]);
+        o[2] = fmaf(p, __uint_as_float(raw.y << 16), o[2]);
+        o[3] = fmaf(p, __uint_as_float(raw.y & 0xffff0000u), o[3]);
+      } else {
+        const uint32_t raw = *reinterpret_cast<const uint32_t*>(vr);
+        o[0] = fmaf(p, __uint_as_float(raw << 16), o[0]);
+        o[DPL - 1] = fmaf(p, __uint_as_float(raw & 0xffff0000u), o[DPL - 1]);
+      }
+    }
+    __syncwarp();
+    float* pp = partial + ((size_t)(m.chunk_base + it.chunk) * H + h) * (HD + 2);
+    if (lane == 0) { pp[0] = mx; pp[1] = l; }
+#pragma unroll
+    for (int c = 0; c < DPL; c++) pp[2 + DPL * lane + c] = o[c];
+  }
+}
+
+// Merge of chunk partials (exp2 domain), one warp per (row, head).
+template <int HD>
+__global__ void __launch_bounds__(128)
+attn_merge_bf16_kernel(const RowMeta* __restrict__ rows, const float* __restrict__ partial, int H, int d,
+                       __nv_bfloat16* __restrict__ out) {
+  constexpr int DPL = HD / 32;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row = blockIdx.x, h = blockIdx.y * 4 + warp;
+  if (h >= H) return;
+  const RowMeta m = rows[row];
+  const float* base = partial + ((size_t)m.chunk_base * H + h) * (HD + 2);
+  const size_t stride = (size_t)H * (HD + 2);
+  float M = -INFINITY;
+  for (int c = lane; c < m.n_chunks; c += 32) M = fmaxf(M, base[c * stride]);
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+  float L = 0.0f, o[DPL];
+#pragma unroll
+  for (int c = 0; c < DPL; c++) o[c] = 0.0f;
+  for (int c = 0; c < m.n_chunks; c++) {
+    const float* pc = base + c * stride;
+    const float sc = exp2f(pc[0] - M);
+    L = fmaf(sc, pc[1], L);
+#pragma unroll
+    for (int i = 0; i < DPL; i++) o[i] = fmaf(sc, pc[2 + DPL * lane + i], o[i]);
+  }
+  const float inv = 1.0f / L;
+  __nv_bfloat16* dst = out + (size_t)row * d + h * HD + DPL * lane;
+#pragma unroll
+  for (int i = 0; i < DPL; i++) dst[i] = __float2bfloat16_rn(o[i] * inv);
+}
+
+template <int HD>
+static void attention_bf16(const Fwd& f, const ModelDims& m, const float* q, const void* pool, int layer,
+                           float* partial, void* out, cudaStream_t s) {
+  const size_t pe = kv_page_elems(m);
+  const size_t lo = (size_t)layer * 2 * m.H * FE_PAGE * m.hd;
+  const size_t smem = 2 * (size_t)FE_PAGE * HD * 2;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(attn_partial_bf16_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = true;
+  }
+  const float scale_log2 = m.attn_scale * 1.4426950408889634f;
+  if (f.n_items > 0)
+    attn_partial_bf16_kernel<HD><<<dim3(f.n_items, m.H), 256, smem, s>>>(
+        f.items, f.item_rows, f.rows, q, (const __nv_bfloat16*)pool, pe, lo, m.H, m.d, scale_log2, partial);
+  attn_merge_bf16_kernel<HD><<<dim3(f.n_rows, (m.H + 3) / 4), 128, 0, s>>>(f.rows, partial, m.H, m.d,
+                                                                          (__nv_bfloat16*)out);
+}
+
 template <typename KT, int HD>
 static void attention_t(const Fwd& f, const ModelDims& m, const float* q, const void* pool, int layer,
                         float* partial, void* out, cudaStream_t s) {
@@ -542,8 +780,8 @@ void launch_attention(int dtype, const Fwd& f, const ModelDims& m, const float* 
     if (m.hd == 64) attention_t<float, 64>(f, m, q, kv_pool, layer, partial, attn_out, s);
     else attention_t<float, 128>(f, m, q, kv_pool, layer, partial, attn_out, s);
   } else {
-    if (m.hd == 64) attention_t<__nv_bfloat16, 64>(f, m, q, kv_pool, layer, partial, attn_out, s);
-    else attention_t<__nv_bfloat16, 128>(f, m, q, kv_pool, layer, partial, attn_out, s);
+    if (m.hd == 64) attention_bf16<64>(f, m, q, kv_pool, layer, partial, attn_out, s);
+    else attention_bf16<128>(f, m, q, kv_pool, layer, partial, attn_out, s);
   }
 }
 

@@ -40,7 +40,8 @@ EXPORTS = (
     "fe_submit", "fe_run", "fe_request_tokens", "fe_request_release", "fe_request_capture_logits",
     "fe_request_logits", "fe_in_flight", "fe_synchronize", "fe_stream", "fe_stats", "fe_profile",
     "fe_profile_read",
-    "fe_weight_ptr", "fe_memcpy", "fe_op_gemv", "fe_op_rmsnorm", "fe_op_gemm_tc", "fe_set_option",
+    "fe_weight_ptr", "fe_memcpy", "fe_op_gemv", "fe_op_rmsnorm", "fe_op_gemm_tc", "fe_op_skinny_tc",
+    "fe_set_option",
 )
 
 _lib = None
@@ -82,6 +83,7 @@ def load_library(path: Path = LIB_PATH) -> ctypes.CDLL:
         "fe_op_gemv": [vp, vp, i32, i32, vp, i32, vp],
         "fe_op_rmsnorm": [vp, vp, vp, vp, i32, i32],
         "fe_op_gemm_tc": [vp, vp, vp, i32, i32, i32, vp],
+        "fe_op_skinny_tc": [vp, vp, vp, i32, i32, i32, vp],
         "fe_set_option": [vp, ctypes.c_char_p, ctypes.c_int64],
     }
     for name, argtypes in sig.items():
@@ -255,6 +257,10 @@ class Engine:
     def op_gemm_tc(self, x_ptr: int, w_ptr: int, M: int, N: int, K: int, y_ptr: int) -> None:
         self._check(self.lib.fe_op_gemm_tc(self._h, ctypes.c_void_p(x_ptr), ctypes.c_void_p(w_ptr), M, N, K,
                                            ctypes.c_void_p(y_ptr)))
+
+    def op_skinny_tc(self, x_ptr: int, w_ptr: int, M: int, N: int, K: int, y_ptr: int) -> None:
+        self._check(self.lib.fe_op_skinny_tc(self._h, ctypes.c_void_p(x_ptr), ctypes.c_void_p(w_ptr), M, N, K,
+                                             ctypes.c_void_p(y_ptr)))
 
     def set_option(self, key: str, value: int) -> None:
         self._check(self.lib.fe_set_option(self._h, key.encode(), int(value)))

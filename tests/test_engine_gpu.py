@@ -220,8 +220,10 @@ def test_gemm_tc_matches_torch(M, N, K):
 
 
 def test_bf16_prefill_tcgen05_matches_gemv_path():
-    """Same request through the tcgen05 prefill and through the GEMV prefill:
-    logits agree to bf16 accuracy and the greedy tokens mostly agree."""
+    """Same request through the tcgen05 prefill + skinny decode and through the
+    CUDA-core GEMV path: first-step logits agree to bf16 accuracy and the first
+    greedy token is identical (later tokens may legitimately diverge after a
+    bf16 near-tie, so free-running logits are not compared)."""
     from oracle.backend import frame
     ids = frame("small", list(range(16)), list(range(500, 700)), "plan")   # 281 ids
     out = {}
@@ -232,6 +234,77 @@ def test_bf16_prefill_tcgen05_matches_gemv_path():
         out[use_tc] = _decode(eng, ids, 4242, 8, capture=True)
         eng.close()
     (t1, l1), (t0, l0) = out[1], out[0]
-    rel = np.abs(l1 - l0).max() / np.abs(l0).max()
-    assert rel < 3e-2, rel
-    assert sum(a == b for a, b in zip(t1, t0)) >= 4
+    rel = np.abs(l1[0] - l0[0]).max() / np.abs(l0[0]).max()
+    assert rel < 2e-2, rel
+    assert t1[0] == t0[0]
+
+
+def test_bf16_skinny_batch_matches_gemv_batch():
+    """7 forked branches decoded as one batch: tcgen05 skinny path vs GEMV path
+    (bf16 both): the first greedy token of every branch agrees."""
+    from oracle.backend import frame
+    ids = frame("small", list(range(16)), list(range(900, 1150)), "plan")
+    firsts = {}
+    for use_tc in (1, 0):
+        eng = Engine("small", dtype="bf16", seed=0, kv_pages=128, max_rows=512)
+        eng.set_option("use_tc", use_tc)
+        trunk = eng.seq_create()
+        eng.prefill(trunk, ids[:-1], 99, M.VIS_ID)
+        reqs = []
+        for j, cut in enumerate((len(ids) - 1, 300, 250, 200, 150, 100, 90)):
+            b = eng.seq_fork(trunk, cut)
+            reqs.append(eng.submit(b, M.TAG_BASE + j, 3, 1))
+        eng.run(-1)
+        firsts[use_tc] = [eng.request_tokens(r, 3)[0] for r in reqs]
+        eng.close()
+    assert sum(a == b for a, b in zip(firsts[1], firsts[0])) >= 6, firsts
+
+
+@pytest.mark.parametrize("M,N,K", [(1, 128, 64), (7, 256, 512), (16, 384, 4096), (3, 4096, 11008)])
+def test_skinny_tc_matches_torch(M, N, K):
+    eng = Engine("small", dtype="bf16", seed=0, kv_pages=8, max_rows=64)
+    try:
+        g = torch.Generator().manual_seed(M * 7 + N)
+        x = torch.randn(M, K, generator=g).to(torch.bfloat16).cuda()
+        w = (torch.randn(N, K, generator=g) * 0.05).to(torch.bfloat16).cuda()
+        y = torch.full((M, N), float("nan"), device="cuda")
+        torch.cuda.synchronize()
+        eng.op_skinny_tc(x.data_ptr(), w.data_ptr(), M, N, K, y.data_ptr())
+        eng.synchronize()
+        ref = x.float() @ w.float().T
+        err = ((y - ref).abs().max() / ref.abs().max()).item()
+        assert err < 1e-5, (err, y[0, :4].tolist(), ref[0, :4].tolist())
+    finally:
+        eng.close()
+
+
+@pytest.mark.parametrize("mask", [1, 2, 4, 8, 16, 31])
+def test_bf16_skinny_per_matrix_matches_gemv(mask):
+    """Decode logits with the skinny tcgen05 path enabled per matrix (bit mask:
+    1 QKV, 2 O, 4 gate/up, 8 down, 16 lm_head) vs the CUDA-core GEMV path."""
+    from oracle.backend import frame
+    ids = frame("small", list(range(16)), list(range(500, 560)), "plan")
+    out = {}
+    for m in (mask, 0):
+        eng = Engine("small", dtype="bf16", seed=0, kv_pages=64, max_rows=512)
+        eng.set_option("tc_min_rows", 100000)   # prefill through the GEMV path in both runs
+        eng.set_option("sk_mask", m)
+        out[m] = _decode(eng, ids, 4242, 4, capture=True)
+        eng.close()
+    rel = np.abs(out[mask][1] - out[0][1]).max() / np.abs(out[0][1]).max()
+    assert rel < 2e-2, rel
+
+
+@pytest.mark.parametrize("plen,tc_rows", [(60, 100000), (280, 100000), (60, 17), (280, 17)])
+def test_bf16_skinny_after_prefill_paths(plen, tc_rows):
+    from oracle.backend import frame
+    ids = frame("small", list(range(16)), list(range(500, 500 + plen)), "plan")
+    out = {}
+    for m in (31, 0):
+        eng = Engine("small", dtype="bf16", seed=0, kv_pages=64, max_rows=512)
+        eng.set_option("tc_min_rows", tc_rows)
+        eng.set_option("sk_mask", m)
+        out[m] = _decode(eng, ids, 4242, 4, capture=True)
+        eng.close()
+    rel = np.abs(out[31][1] - out[0][1]).max() / np.abs(out[0][1]).max()
+    assert rel < 2e-2, rel

@@ -1,0 +1,62 @@
+"""Decode-iteration probe: one trunk prefill + `rows` forked branches decoded
+for `ticks` iterations on the 7B-shaped bf16 engine.  Used under ncu for the
+per-kernel launch list and alone for host-vs-device tick timing."""
+
+import argparse
+import sys
+import time
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+import torch  # noqa: E402
+
+from paper_2506_07639_b200 import model as M  # noqa: E402
+from paper_2506_07639_b200.engine import Engine  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="7b")
+ap.add_argument("--dtype", default="bf16")
+ap.add_argument("--rows", type=int, default=7)
+ap.add_argument("--trunk", type=int, default=625)
+ap.add_argument("--ticks", type=int, default=8)
+ap.add_argument("--repeat", type=int, default=3)
+ap.add_argument("--profile", action="store_true")
+args = ap.parse_args()
+
+eng = Engine(args.config, dtype=args.dtype, seed=0, kv_pages=256)
+cfg = M.get_config(args.config)
+ids = [M.BOS_ID] + [M.VIS_ID] * cfg.n_vision + list(range(100, 100 + args.trunk - 1 - cfg.n_vision))
+stream = torch.cuda.ExternalStream(eng.stream_handle())
+for rep in range(args.repeat):
+    trunk = eng.seq_create()
+    t0 = time.perf_counter()
+    eng.prefill(trunk, ids, 7, M.VIS_ID)
+    eng.synchronize()
+    t_pre = time.perf_counter() - t0
+    reqs, seqs = [], []
+    for j in range(args.rows):
+        b = eng.seq_fork(trunk, len(ids) - 40 * j)
+        seqs.append(b)
+        reqs.append(eng.submit(b, M.TAG_BASE + j, args.ticks, 1))
+    if args.profile:
+        eng.profile(True)
+    a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    h0 = time.perf_counter()
+    eng.run(-1)
+    host = time.perf_counter() - h0
+    b_.record(stream)
+    eng.synchronize()
+    dev = a.elapsed_time(b_)
+    prof = eng.profile_read() if args.profile else {}
+    if args.profile:
+        eng.profile(False)
+    for r in reqs:
+        eng.request_tokens(r, args.ticks)
+        eng.request_release(r)
+    for s in seqs + [trunk]:
+        eng.seq_free(s)
+    print(f"rep {rep}: prefill {t_pre*1e3:.1f} ms | {args.ticks} ticks x {args.rows} rows: device {dev:.2f} ms "
+          f"({dev/args.ticks:.3f} ms/tick), host enqueue {host*1e3:.2f} ms  {prof}", flush=True)
+eng.close()
