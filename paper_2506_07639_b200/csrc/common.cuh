@@ -120,4 +120,11 @@ __device__ __forceinline__ int argmax_index(unsigned long long key) {
   return (int)(0xffffffffu - (uint32_t)(key & 0xffffffffull));
 }
 
+// Programmatic dependent launch: kernels of the decode chain are launched
+// with cudaLaunchAttributeProgrammaticStreamSerialization, may start while the
+// previous kernel drains, and must call pdl_wait() before touching anything the
+// previous kernel writes (or reads).  Both are no-ops for normal launches.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 }  // namespace fe

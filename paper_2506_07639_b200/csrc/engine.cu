@@ -40,6 +40,13 @@ constexpr int kRequestCap = 1024;   // tokens per request (out_tokens arena slot
 constexpr int kMetaRing = 4;
 constexpr int kItemRows = 16;       // query rows per cascade work item
 constexpr int kLogitRows = 256;
+constexpr int kMaxGraphRows = 64;    // decode ticks with <= this many rows replay CUDA graphs
+constexpr int kGraphItemCtas = 32;   // attention CTAs per head (persistent over work items)
+
+struct MetaLayout {
+  size_t o_rows, o_items, o_irows, o_heads, total;
+  int cap_rows, cap_items, cap_irows;
+};
 
 struct Seq {
   std::vector<int> pages;
@@ -118,6 +125,14 @@ struct fe_engine {
   uint64_t seqno = 0;
   std::vector<int> free_arena;
   int capture_req = -1;
+
+  // metadata layout + decode graphs (one per row count)
+  MetaLayout meta_layout{};
+  bool graphs_on = true;
+  struct GraphSlot {
+    bool seen = false;
+    cudaGraphExec_t exec = nullptr;
+  } graphs[kMaxGraphRows + 1];
 
   // tcgen05 GEMM path (bf16, wide forwards)
   struct LayerMaps {
@@ -235,119 +250,13 @@ void prof_end(fe_engine* e, int i, double bytes) {
   CK(cudaEventRecord(e->prof_recs[i].b, e->stream));
 }
 
-// One forward pass over `rows` (all positions must already be < seq.len+1 in
-// order).  Builds row metadata, the cascade work list and launches the layer
-// stack.  Host-side sequence lengths advance as rows are written.
-void forward(fe_engine* e, const std::vector<RowIn>& rows, uint64_t vision_seed) {
+// The kernel sequence of one forward pass (eager or under graph capture).
+template <typename GB>
+void launch_layers(fe_engine* e, const fe::Fwd& f, int n, bool decode, double kv_bytes, GB gemv_bytes) {
   const fe::ModelDims& m = e->m;
-  const int n = (int)rows.size();
-  if (n == 0) return;
-  if (n > e->max_rows) throw Error("forward: too many rows");
-  if (e->prof_on && e->prof_used > 8192) flush_profile(e);  // only between forwards: all records closed
-
-  std::vector<fe::RowMeta> meta(n);
-  std::vector<int32_t> head_rows;
-  int chunk_total = 0;
-  for (int i = 0; i < n; i++) {
-    const RowIn& r = rows[i];
-    Seq& s = seq_at(e, r.seq);
-    if (r.pos != s.len) throw Error("forward: non-contiguous append");
-    if (r.pos >= m.max_pos) throw Error("forward: position beyond max_pos");
-    const int pg = r.pos / FE_PAGE;
-    if (pg == (int)s.pages.size()) s.pages.push_back(alloc_page(e));
-    if (e->page_ref[s.pages[pg]] != 1) throw Error("forward: write into a shared page");
-    s.len = r.pos + 1;
-    fe::RowMeta& mm = meta[i];
-    mm.pos = r.pos;
-    mm.tok = r.tok;
-    mm.tok_src = r.tok_src;
-    mm.vis_row = r.vis_row;
-    mm.kv_page = s.pages[pg];
-    mm.kv_slot = r.pos % FE_PAGE;
-    mm.out_idx = r.out_idx;
-    mm.chunk_base = chunk_total;
-    mm.n_chunks = pg + 1;
-    mm.logit_row = r.logit_row;
-    mm.head_row = -1;
-    chunk_total += pg + 1;
-    if (r.head) {
-      mm.head_row = (int)head_rows.size();
-      head_rows.push_back(i);
-    }
-  }
-  if (chunk_total > e->max_partials) throw Error("forward: partial workspace too small");
-
-  // cascade work list: group rows by the physical page their chunk maps to.
-  // Rows sharing a trunk point at the same pages, so each shared page is
-  // staged once per (page, head) CTA and serves all of them.
-  std::map<int, std::vector<std::pair<int, int>>> by_page;  // page -> (row, valid)
-  std::unordered_map<int, int> page_chunk;
-  for (int i = 0; i < n; i++) {
-    const Seq& s = e->seqs[rows[i].seq];
-    const int pos = rows[i].pos;
-    for (int c = 0; c <= pos / FE_PAGE; c++) {
-      const int pg = s.pages[c];
-      by_page[pg].push_back({i, std::min(FE_PAGE, pos + 1 - c * FE_PAGE)});
-      page_chunk[pg] = c;
-    }
-  }
-  std::vector<fe::AttnItem> items;
-  std::vector<fe::ItemRow> irows;
-  for (auto& kv : by_page) {
-    const auto& lst = kv.second;
-    for (size_t b = 0; b < lst.size(); b += kItemRows) {
-      fe::AttnItem it;
-      it.page = kv.first;
-      it.chunk = page_chunk[kv.first];
-      it.row_begin = (int)irows.size();
-      it.row_count = (int)std::min<size_t>(kItemRows, lst.size() - b);
-      for (int j = 0; j < it.row_count; j++) irows.push_back({lst[b + j].first, lst[b + j].second});
-      items.push_back(it);
-    }
-  }
-  if ((int)items.size() > e->max_items) throw Error("forward: too many attention items");
-
-  // pack metadata into one pinned buffer -> one H2D copy
-  const size_t o_rows = 0;
-  const size_t o_items = o_rows + sizeof(fe::RowMeta) * n;
-  const size_t o_irows = o_items + sizeof(fe::AttnItem) * items.size();
-  const size_t o_heads = o_irows + sizeof(fe::ItemRow) * irows.size();
-  const size_t total = o_heads + sizeof(int32_t) * head_rows.size();
-  if (total > e->meta_bytes) throw Error("forward: metadata buffer too small");
-  int mi;
-  unsigned char* hbuf = next_meta(e, &mi);
-  std::memcpy(hbuf + o_rows, meta.data(), sizeof(fe::RowMeta) * n);
-  if (!items.empty()) std::memcpy(hbuf + o_items, items.data(), sizeof(fe::AttnItem) * items.size());
-  if (!irows.empty()) std::memcpy(hbuf + o_irows, irows.data(), sizeof(fe::ItemRow) * irows.size());
-  if (!head_rows.empty()) std::memcpy(hbuf + o_heads, head_rows.data(), sizeof(int32_t) * head_rows.size());
-  unsigned char* dbuf = (unsigned char*)e->ws.meta;
-  CK(cudaMemcpyAsync(dbuf, hbuf, total, cudaMemcpyHostToDevice, e->stream));
-  CK(cudaEventRecord(e->meta_ev[mi], e->stream));
-
-  fe::Fwd f{};
-  f.rows = (const fe::RowMeta*)(dbuf + o_rows);
-  f.n_rows = n;
-  f.items = (const fe::AttnItem*)(dbuf + o_items);
-  f.n_items = (int)items.size();
-  f.item_rows = (const fe::ItemRow*)(dbuf + o_irows);
-  f.n_head_rows = (int)head_rows.size();
-  f.head_rows = (const int32_t*)(dbuf + o_heads);
-  f.vision_key = fe::tensor_key(vision_seed, 4 /* T_VISION */);
-
   cudaStream_t st = e->stream;
   const int dt = e->dtype;
-  const bool decode = f.n_head_rows > 0;
-  const double el = (double)e->elem;
-  // algorithmic bytes of one GEMV launch: weights + staged input + fp32 output
-  auto gemv_bytes = [&](double N, double K, int rows) { return N * K * el + rows * K * el + rows * N * 4.0; };
-  double kv_bytes = 0;  // K+V bytes the cascade items stage (each shared page once per head)
-  for (const auto& it : items) {
-    int vmax = 0;
-    for (int j = 0; j < it.row_count; j++) vmax = std::max(vmax, irows[it.row_begin + j].valid);
-    kv_bytes += 2.0 * vmax * m.hd * m.H * el;
-  }
   const int whole = prof_begin(e, decode ? PROF_DECODE_FWD : PROF_PREFILL_FWD);
-  e->h2d_bytes += total;
   fe::launch_embed(dt, f, m, e->w.embed, e->ws.out_tokens, e->ws.x, st);
   // bf16: skinny tcgen05 swap-AB GEMM for <= 16 rows (decode), the tile
   // tcgen05 GEMM for wide forwards (prefill); fp32: canonical CUDA-core GEMV
@@ -427,6 +336,152 @@ void forward(fe_engine* e, const std::vector<RowIn>& rows, uint64_t vision_seed)
     prof_end(e, p, gemv_bytes(m.V, m.d, f.n_head_rows));
   }
   prof_end(e, whole, 0.0);
+}
+
+// One forward pass over `rows` (all positions must already be < seq.len+1 in
+// order).  Builds row metadata, the cascade work list and launches the layer
+// stack.  Host-side sequence lengths advance as rows are written.
+void forward(fe_engine* e, const std::vector<RowIn>& rows, uint64_t vision_seed) {
+  const fe::ModelDims& m = e->m;
+  const int n = (int)rows.size();
+  if (n == 0) return;
+  if (n > e->max_rows) throw Error("forward: too many rows");
+  if (e->prof_on && e->prof_used > 8192) flush_profile(e);  // only between forwards: all records closed
+
+  std::vector<fe::RowMeta> meta(n);
+  std::vector<int32_t> head_rows;
+  int chunk_total = 0;
+  for (int i = 0; i < n; i++) {
+    const RowIn& r = rows[i];
+    Seq& s = seq_at(e, r.seq);
+    if (r.pos != s.len) throw Error("forward: non-contiguous append");
+    if (r.pos >= m.max_pos) throw Error("forward: position beyond max_pos");
+    const int pg = r.pos / FE_PAGE;
+    if (pg == (int)s.pages.size()) s.pages.push_back(alloc_page(e));
+    if (e->page_ref[s.pages[pg]] != 1) throw Error("forward: write into a shared page");
+    s.len = r.pos + 1;
+    fe::RowMeta& mm = meta[i];
+    mm.pos = r.pos;
+    mm.tok = r.tok;
+    mm.tok_src = r.tok_src;
+    mm.vis_row = r.vis_row;
+    mm.kv_page = s.pages[pg];
+    mm.kv_slot = r.pos % FE_PAGE;
+    mm.out_idx = r.out_idx;
+    mm.chunk_base = chunk_total;
+    mm.n_chunks = pg + 1;
+    mm.logit_row = r.logit_row;
+    mm.head_row = -1;
+    chunk_total += pg + 1;
+    if (r.head) {
+      mm.head_row = (int)head_rows.size();
+      head_rows.push_back(i);
+    }
+  }
+  if (chunk_total > e->max_partials) throw Error("forward: partial workspace too small");
+
+  // cascade work list: group rows by the physical page their chunk maps to.
+  // Rows sharing a trunk point at the same pages, so each shared page is
+  // staged once per (page, head) CTA and serves all of them.
+  std::map<int, std::vector<std::pair<int, int>>> by_page;  // page -> (row, valid)
+  std::unordered_map<int, int> page_chunk;
+  for (int i = 0; i < n; i++) {
+    const Seq& s = e->seqs[rows[i].seq];
+    const int pos = rows[i].pos;
+    for (int c = 0; c <= pos / FE_PAGE; c++) {
+      const int pg = s.pages[c];
+      by_page[pg].push_back({i, std::min(FE_PAGE, pos + 1 - c * FE_PAGE)});
+      page_chunk[pg] = c;
+    }
+  }
+  std::vector<fe::AttnItem> items;
+  std::vector<fe::ItemRow> irows;
+  for (auto& kv : by_page) {
+    const auto& lst = kv.second;
+    for (size_t b = 0; b < lst.size(); b += kItemRows) {
+      fe::AttnItem it;
+      it.page = kv.first;
+      it.chunk = page_chunk[kv.first];
+      it.row_begin = (int)irows.size();
+      it.row_count = (int)std::min<size_t>(kItemRows, lst.size() - b);
+      for (int j = 0; j < it.row_count; j++) irows.push_back({lst[b + j].first, lst[b + j].second});
+      items.push_back(it);
+    }
+  }
+  if ((int)items.size() > e->max_items) throw Error("forward: too many attention items");
+
+  // Metadata at fixed offsets of the device buffer (header, rows, items,
+  // item rows, head rows) so a captured decode graph can be replayed with new
+  // contents: counts that vary per tick (attention items) are read on device.
+  const MetaLayout& L = e->meta_layout;
+  if (n > L.cap_rows || (int)items.size() > L.cap_items || (int)irows.size() > L.cap_irows)
+    throw Error("forward: metadata capacity exceeded");
+  int mi;
+  unsigned char* hbuf = next_meta(e, &mi);
+  int32_t* hdr = reinterpret_cast<int32_t*>(hbuf);
+  hdr[0] = n;
+  hdr[1] = (int)items.size();
+  hdr[2] = (int)head_rows.size();
+  hdr[3] = 0;
+  std::memcpy(hbuf + L.o_rows, meta.data(), sizeof(fe::RowMeta) * n);
+  std::memcpy(hbuf + L.o_items, items.data(), sizeof(fe::AttnItem) * items.size());
+  std::memcpy(hbuf + L.o_irows, irows.data(), sizeof(fe::ItemRow) * irows.size());
+  std::memcpy(hbuf + L.o_heads, head_rows.data(), sizeof(int32_t) * head_rows.size());
+  unsigned char* dbuf = (unsigned char*)e->ws.meta;
+  size_t h2d = 0;
+  auto copy = [&](size_t off, size_t bytes) {
+    if (bytes == 0) return;
+    CK(cudaMemcpyAsync(dbuf + off, hbuf + off, bytes, cudaMemcpyHostToDevice, e->stream));
+    h2d += bytes;
+  };
+  copy(0, L.o_rows + sizeof(fe::RowMeta) * n);  // header + rows
+  copy(L.o_items, sizeof(fe::AttnItem) * items.size());
+  copy(L.o_irows, sizeof(fe::ItemRow) * irows.size());
+  copy(L.o_heads, sizeof(int32_t) * head_rows.size());
+  CK(cudaEventRecord(e->meta_ev[mi], e->stream));
+  e->h2d_bytes += h2d;
+
+  fe::Fwd f{};
+  f.hdr = reinterpret_cast<const int32_t*>(dbuf);
+  f.rows = (const fe::RowMeta*)(dbuf + L.o_rows);
+  f.n_rows = n;
+  f.items = (const fe::AttnItem*)(dbuf + L.o_items);
+  f.n_items = (int)items.size();
+  // decode: fixed CTA count per head (graph-replayable); prefill: one CTA per item
+  f.item_cap = items.empty() ? 0 : (head_rows.empty() ? (int)items.size() : kGraphItemCtas);
+  f.item_rows = (const fe::ItemRow*)(dbuf + L.o_irows);
+  f.n_head_rows = (int)head_rows.size();
+  f.head_rows = (const int32_t*)(dbuf + L.o_heads);
+  f.vision_key = fe::tensor_key(vision_seed, 4 /* T_VISION */);
+
+  const bool decode = f.n_head_rows > 0;
+  const double el = (double)e->elem;
+  // algorithmic bytes of one GEMV launch: weights + staged input + fp32 output
+  auto gemv_bytes = [&](double N, double K, int rows) { return N * K * el + rows * K * el + rows * N * 4.0; };
+  double kv_bytes = 0;  // K+V bytes the cascade items stage (each shared page once per head)
+  for (const auto& it : items) {
+    int vmax = 0;
+    for (int j = 0; j < it.row_count; j++) vmax = std::max(vmax, irows[it.row_begin + j].valid);
+    kv_bytes += 2.0 * vmax * m.hd * m.H * el;
+  }
+
+  // decode ticks replay a CUDA graph per row count (captured on the second
+  // tick with that row count); prefill and profiled runs launch eagerly
+  const bool graphable = decode && e->graphs_on && !e->prof_on && n <= kMaxGraphRows;
+  if (graphable && e->graphs[n].exec) {
+    CK(cudaGraphLaunch(e->graphs[n].exec, e->stream));
+  } else if (graphable && e->graphs[n].seen) {
+    cudaGraph_t g = nullptr;
+    CK(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
+    launch_layers(e, f, n, decode, kv_bytes, gemv_bytes);
+    CK(cudaStreamEndCapture(e->stream, &g));
+    CK(cudaGraphInstantiate(&e->graphs[n].exec, g, 0));
+    CK(cudaGraphDestroy(g));
+    CK(cudaGraphLaunch(e->graphs[n].exec, e->stream));
+  } else {
+    if (graphable) e->graphs[n].seen = true;
+    launch_layers(e, f, n, decode, kv_bytes, gemv_bytes);
+  }
   CK(cudaGetLastError());
   // embed + per layer (2 norms, qkv, attention partial + merge, O, gate/up, down) + head
   e->n_launches += 1 + 8 * m.L + (decode ? 3 : 0) - (items.empty() ? m.L : 0);
@@ -609,8 +664,19 @@ fe_engine* create(const fe_config* c, int device, const float* rope_host) {
     e->ws.out_tokens = (int32_t*)e->dalloc((size_t)n_arena * kRequestCap * 4);
     CK(cudaMemset(e->ws.out_tokens, 0, (size_t)n_arena * kRequestCap * 4));
     for (int i = n_arena - 1; i >= 0; i--) e->free_arena.push_back(i);
-    e->meta_bytes = R * sizeof(fe::RowMeta) + (size_t)e->max_items * sizeof(fe::AttnItem) +
-                    (size_t)e->max_partials * sizeof(fe::ItemRow) + R * 4 + 4096;
+    {  // fixed-offset metadata layout (16-byte aligned sections)
+      MetaLayout& L = e->meta_layout;
+      auto up16 = [](size_t v) { return (v + 15) & ~(size_t)15; };
+      L.cap_rows = (int)R;
+      L.cap_items = e->max_items;
+      L.cap_irows = e->max_partials;
+      L.o_rows = 64;
+      L.o_items = up16(L.o_rows + R * sizeof(fe::RowMeta));
+      L.o_irows = up16(L.o_items + (size_t)L.cap_items * sizeof(fe::AttnItem));
+      L.o_heads = up16(L.o_irows + (size_t)L.cap_irows * sizeof(fe::ItemRow));
+      L.total = up16(L.o_heads + R * 4);
+      e->meta_bytes = L.total;
+    }
     e->ws.meta = e->dalloc(e->meta_bytes);
     for (int i = 0; i < kMetaRing; i++) {
       CK(cudaMallocHost((void**)&e->meta_host[i], e->meta_bytes));
@@ -670,6 +736,8 @@ fe_engine* create(const fe_config* c, int device, const float* rope_host) {
 void destroy(fe_engine* e) {
   cudaSetDevice(e->device);
   cudaStreamSynchronize(e->stream);
+  for (auto& g : e->graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
   for (void* p : e->allocs) cudaFree(p);
   for (auto& r : e->prof_recs) {
     cudaEventDestroy(r.a);
@@ -995,6 +1063,8 @@ int fe_set_option(fe_engine* e, const char* key, int64_t value) {
     if (k == "tc_min_rows") e->tc_min_rows = (int)value;
     else if (k == "use_tc") e->use_tc = value != 0 && !e->tc_maps.empty();
     else if (k == "sk_mask") e->sk_mask = (int)value;
+    else if (k == "graphs") e->graphs_on = value != 0;
+    else if (k == "pdl") fe::g_pdl = value != 0;
     else throw Error("unknown option " + k);
   });
 }

@@ -6,6 +6,8 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#include <utility>
+
 namespace fe {
 
 enum DType { F32 = 0, BF16 = 1 };
@@ -46,10 +48,12 @@ struct ModelDims {
 
 // Device-side view of a forward pass.
 struct Fwd {
+  const int32_t* hdr;      // device header: [n_rows, n_items, n_head_rows, 0]
   const RowMeta* rows;
   int n_rows;
   const AttnItem* items;
-  int n_items;
+  int n_items;             // host-side count (eager launches); kernels read hdr[1]
+  int item_cap;            // attention CTAs per head (persistent over items)
   const ItemRow* item_rows;
   int n_head_rows;         // rows that need the lm_head
   const int32_t* head_rows;  // row index of each lm_head row
@@ -81,6 +85,24 @@ struct Workspace {
   int32_t* out_tokens;
   void* meta;        // device copy of the per-forward metadata
 };
+
+// --- programmatic dependent launch -------------------------------------------
+extern bool g_pdl;  // engine option "pdl"
+
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = g_pdl ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // --- kernel launchers (kernels.cu) -----------------------------------------
 void launch_init_linear(int dtype, void* w, uint64_t key, size_t n, cudaStream_t s);

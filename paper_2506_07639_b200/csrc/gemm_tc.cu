@@ -342,6 +342,7 @@ skinny_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constan
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kb_total = (a.K + BK - 1) / BK;
   const bool swiglu = a.epi == TC_SWIGLU;
+  pdl_trigger();
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_w) : "memory");
@@ -368,20 +369,44 @@ skinny_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constan
 
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer, runs ahead across units
+      // Weights do not depend on the previous kernel: the first ring's worth of
+      // weight tiles is requested before griddepcontrol.wait (PDL), the
+      // activation tiles after it.
+      auto load_w = [&](int s, int tl, int kb) {
+        if (swiglu) {
+          const int f0 = tl * (BM / 2);
+          tma_load_2d(sa + s * kSkA, &map_w, &full[s], kb * BK, f0);
+          tma_load_2d(sa + s * kSkA + kSkA / 2, &map_w, &full[s], kb * BK, a.F + f0);
+        } else {
+          tma_load_2d(sa + s * kSkA, &map_w, &full[s], kb * BK, tl * BM);
+        }
+      };
+      int pre = 0;  // stages prefetched before the dependency wait
+      {
+        int u = blockIdx.x, tl, sp, kb0, kb1;
+        if (u < a.units) unit_of(a, u, kb_total, &tl, &sp, &kb0, &kb1);
+        int kb = u < a.units ? kb0 : 0;
+        while (u < a.units && pre < kSkStages) {
+          mbar_expect_tx(&full[pre], kSkA + kSkB);
+          load_w(pre, tl, kb);
+          pre++;
+          if (++kb == kb1) {
+            u += gridDim.x;
+            if (u < a.units) { unit_of(a, u, kb_total, &tl, &sp, &kb0, &kb1); kb = kb0; }
+          }
+        }
+      }
+      pdl_wait();
       int it = 0;
       for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
         int tl, sp, kb0, kb1;
         unit_of(a, u, kb_total, &tl, &sp, &kb0, &kb1);
         for (int kb = kb0; kb < kb1; kb++, it++) {
           const int s = it % kSkStages;
-          mbar_wait(&empty[s], ((it / kSkStages) & 1) ^ 1);
-          mbar_expect_tx(&full[s], kSkA + kSkB);
-          if (swiglu) {
-            const int f0 = tl * (BM / 2);
-            tma_load_2d(sa + s * kSkA, &map_w, &full[s], kb * BK, f0);
-            tma_load_2d(sa + s * kSkA + kSkA / 2, &map_w, &full[s], kb * BK, a.F + f0);
-          } else {
-            tma_load_2d(sa + s * kSkA, &map_w, &full[s], kb * BK, tl * BM);
+          if (it >= pre) {
+            mbar_wait(&empty[s], ((it / kSkStages) & 1) ^ 1);
+            mbar_expect_tx(&full[s], kSkA + kSkB);
+            load_w(s, tl, kb);
           }
           tma_load_2d(sb + s * kSkB, &map_x, &full[s], kb * BK, 0);
         }
@@ -423,6 +448,7 @@ skinny_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constan
     // ---- epilogue warps: thread <-> weight row r of the tile
     const int r = 32 * (warp & 3) + lane;
     const int et = threadIdx.x - 64;  // 0..127
+    pdl_wait();  // epilogue writes / reads outputs of earlier kernels
     int lu = 0;
     for (int u = blockIdx.x; u < a.units; u += gridDim.x, lu++) {
       int tl, sp, kb0, kb1;
@@ -637,8 +663,8 @@ void launch_skinny_tc(const TmaMap& w_map, const TmaMap& x_map, const SkLaunch& 
   a.head_rows = l.head_rows; a.H = l.H; a.hd = l.hd; a.d = l.d; a.part_keys = l.part_keys;
   a.logits = l.logits; a.V = l.V; a.n_text = l.n_text;
   const int grid = std::min(a.units, n_sm);
-  skinny_tc_kernel<<<grid, kThreads, kSkSmem, s>>>(
-      *reinterpret_cast<const CUtensorMap*>(w_map.bytes), *reinterpret_cast<const CUtensorMap*>(x_map.bytes), a);
+  launch_k(skinny_tc_kernel, dim3(grid), dim3(kThreads), (size_t)kSkSmem, s,
+           *reinterpret_cast<const CUtensorMap*>(w_map.bytes), *reinterpret_cast<const CUtensorMap*>(x_map.bytes), a);
 }
 
 void launch_gemm_tc(const TmaMap& a_map, const TmaMap& b_map, const TcLaunch& l, cudaStream_t s) {

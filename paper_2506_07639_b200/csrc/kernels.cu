@@ -22,6 +22,8 @@
 
 namespace fe {
 
+bool g_pdl = true;
+
 // ---------------------------------------------------------------- init ----
 template <typename WT>
 __global__ void init_linear_kernel(WT* w, uint64_t key, size_t n) {
@@ -45,6 +47,8 @@ void launch_init_norm(float* w, uint64_t key, size_t n, cudaStream_t s) {
 // --------------------------------------------------------------- embed ----
 template <typename WT>
 __global__ void embed_kernel(Fwd f, int d, const WT* embed, const int32_t* out_tokens, float* x) {
+  pdl_trigger();
+  pdl_wait();
   const RowMeta m = f.rows[blockIdx.x];
   float* xr = x + (size_t)blockIdx.x * d;
   if (m.vis_row >= 0) {
@@ -71,6 +75,8 @@ void launch_embed(int dtype, const Fwd& f, const ModelDims& m, const void* embed
 template <typename XT>
 __global__ void rmsnorm_kernel(const float* __restrict__ x, const float* __restrict__ w, XT* __restrict__ out,
                                int n, int d, int ld_out, float eps, const int32_t* __restrict__ row_index) {
+  pdl_trigger();
+  pdl_wait();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= n) return;
   const int src = row_index ? row_index[warp] : warp;
@@ -97,6 +103,8 @@ __global__ void rmsnorm_kernel(const float* __restrict__ x, const float* __restr
 __global__ void __launch_bounds__(256)
 rmsnorm_bf16_kernel(const float* __restrict__ x, const float* __restrict__ w, __nv_bfloat16* __restrict__ out,
                     int d, int ld_out, float eps, const int32_t* __restrict__ row_index) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float red[8];
   const int row = blockIdx.x;
   const int src = row_index ? row_index[row] : row;
@@ -135,12 +143,12 @@ void launch_rmsnorm(int dtype, const float* x, const float* w, void* out, int n_
                     float eps, const int32_t* row_index, cudaStream_t s) {
   if (n_rows == 0) return;
   if (dtype == BF16) {
-    rmsnorm_bf16_kernel<<<n_rows, 256, 0, s>>>(x, w, (__nv_bfloat16*)out, d, ld_out, eps, row_index);
+    launch_k(rmsnorm_bf16_kernel, dim3(n_rows), dim3(256), 0, s, x, w, (__nv_bfloat16*)out, d, ld_out, eps, row_index);
     return;
   }
   const int blocks = (n_rows + 7) / 8;
-  if (dtype == F32) rmsnorm_kernel<float><<<blocks, 256, 0, s>>>(x, w, (float*)out, n_rows, d, ld_out, eps, row_index);
-  else rmsnorm_kernel<__nv_bfloat16><<<blocks, 256, 0, s>>>(x, w, (__nv_bfloat16*)out, n_rows, d, ld_out, eps, row_index);
+  if (dtype == F32) launch_k(rmsnorm_kernel<float>, dim3(blocks), dim3(256), 0, s, x, w, (float*)out, n_rows, d, ld_out, eps, row_index);
+  else launch_k(rmsnorm_kernel<__nv_bfloat16>, dim3(blocks), dim3(256), 0, s, x, w, (__nv_bfloat16*)out, n_rows, d, ld_out, eps, row_index);
 }
 
 // ---------------------------------------------------------------- gemv ----
@@ -172,6 +180,8 @@ constexpr int kGemvWarps = 8;
 template <typename WT, typename XT, int BMAX, int EPI>
 __global__ void __launch_bounds__(kGemvWarps * 32)
 gemv_kernel(const GemvArgs a) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int V = Elem<WT>::kVec;          // elements per 16-byte weight vector
   constexpr int KC = 32 * V * 8;             // K chunk staged per pass
   constexpr int XV = 16 / sizeof(XT);        // staging elements per 16 bytes
@@ -357,7 +367,7 @@ static void gemv_dispatch(const GemvArgs& a, cudaStream_t s) {
       configured = true;
     }
     dim3 grid(gx, (a.n_rows + BM - 1) / BM);
-    kern<<<grid, kGemvWarps * 32, smem, s>>>(a);
+    launch_k(kern, grid, dim3(kGemvWarps * 32), smem, s, a);
   };
   if (a.n_rows <= 1) go(std::integral_constant<int, 1>{});
   else if (a.n_rows <= 2) go(std::integral_constant<int, 2>{});
@@ -407,6 +417,8 @@ void launch_gemv_store(int dtype, const void* w, int N, int K, const void* x, in
 // ----------------------------------------------------- lm_head + argmax ----
 __global__ void finalize_kernel(const RowMeta* rows, const int32_t* head_rows, const unsigned long long* part_keys,
                                 int n_ctas, int32_t* out_tokens) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ unsigned long long red[256];
   const int i = blockIdx.x;
   unsigned long long k = 0ull;
@@ -425,7 +437,8 @@ __global__ void finalize_kernel(const RowMeta* rows, const int32_t* head_rows, c
 
 void launch_finalize(const Fwd& f, const unsigned long long* part_keys, int n_ctas, int32_t* out_tokens,
                      cudaStream_t s) {
-  if (f.n_head_rows > 0) finalize_kernel<<<f.n_head_rows, 256, 0, s>>>(f.rows, f.head_rows, part_keys, n_ctas, out_tokens);
+  if (f.n_head_rows > 0)
+    launch_k(finalize_kernel, dim3(f.n_head_rows), dim3(256), 0, s, f.rows, f.head_rows, part_keys, n_ctas, out_tokens);
 }
 
 void launch_lm_head(int dtype, const Fwd& f, const ModelDims& m, const void* w, const void* xn,
@@ -436,7 +449,7 @@ void launch_lm_head(int dtype, const Fwd& f, const ModelDims& m, const void* w, 
   a.rows = f.rows; a.head_rows = f.head_rows; a.part_keys = part_keys; a.logits = logits;
   a.V = m.V; a.n_text = m.n_text;
   gemv_any<EPI_ARGMAX>(dtype, a, s);
-  finalize_kernel<<<f.n_head_rows, 256, 0, s>>>(f.rows, f.head_rows, part_keys, lm_head_ctas(m), out_tokens);
+  launch_k(finalize_kernel, dim3(f.n_head_rows), dim3(256), 0, s, f.rows, f.head_rows, part_keys, lm_head_ctas(m), out_tokens);
 }
 
 // ----------------------------------------------------------- attention ----
@@ -446,28 +459,34 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 
 template <typename KT, int HD>
 __global__ void __launch_bounds__(128)
-attn_partial_kernel(const AttnItem* __restrict__ items, const ItemRow* __restrict__ item_rows,
+attn_partial_kernel(const int32_t* __restrict__ hdr, const AttnItem* __restrict__ items, const ItemRow* __restrict__ item_rows,
                     const RowMeta* __restrict__ rows, const float* __restrict__ q, const KT* __restrict__ pool,
                     size_t page_elems, size_t layer_off, int H, int d, float scale, float* __restrict__ partial) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char smem_kv[];
   __shared__ __align__(8) uint64_t bar;
   KT* ks = reinterpret_cast<KT*>(smem_kv);
   KT* vs = ks + FE_PAGE * HD;
-  const AttnItem it = items[blockIdx.x];
   const int h = blockIdx.y;
+  const int n_items = hdr[1];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  uint32_t phase = 0;
+  // persistent over work items: grid.x CTAs per head stride through hdr[1] items
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x, phase ^= 1) {
+  __syncthreads();  // previous item's shared-memory reads done / barrier init visible
+  const AttnItem it = items[item];
   // valid keys the CTA needs = max over its rows
   int vmax = 0;
   for (int i = 0; i < it.row_count; i++) vmax = max(vmax, item_rows[it.row_begin + i].valid);
   const KT* kg = pool + (size_t)it.page * page_elems + layer_off + (size_t)h * FE_PAGE * HD;
   const KT* vg = kg + (size_t)H * FE_PAGE * HD;
   const uint32_t bytes = (uint32_t)(vmax * HD * sizeof(KT));
-  if (threadIdx.x == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar)), "r"(2 * bytes)
                  : "memory");
@@ -479,8 +498,8 @@ attn_partial_kernel(const AttnItem* __restrict__ items, const ItemRow* __restric
   {
     uint32_t done = 0;
     while (!done) {
-      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
-                   : "=r"(done) : "r"(smem_u32(&bar)) : "memory");
+      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                   : "=r"(done) : "r"(smem_u32(&bar)), "r"(phase) : "memory");
     }
   }
 
@@ -536,12 +555,15 @@ attn_partial_kernel(const AttnItem* __restrict__ items, const ItemRow* __restric
       pp[2 + 4 * lane + 2] = o[2]; pp[2 + 4 * lane + 3] = o[3];
     }
   }
+  }  // item loop
 }
 
 template <typename XT, int HD>
 __global__ void __launch_bounds__(128)
 attn_merge_kernel(const RowMeta* __restrict__ rows, const float* __restrict__ partial, int H, int d,
                   XT* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row = blockIdx.x, h = blockIdx.y * 4 + warp;
   if (h >= H) return;
@@ -573,30 +595,36 @@ attn_merge_kernel(const RowMeta* __restrict__ rows, const float* __restrict__ pa
 // instead of 5 per key), softmax in the exp2 domain with fast intrinsics.
 template <int HD>
 __global__ void __launch_bounds__(256)
-attn_partial_bf16_kernel(const AttnItem* __restrict__ items, const ItemRow* __restrict__ item_rows,
+attn_partial_bf16_kernel(const int32_t* __restrict__ hdr, const AttnItem* __restrict__ items, const ItemRow* __restrict__ item_rows,
                          const RowMeta* __restrict__ rows, const float* __restrict__ q,
                          const __nv_bfloat16* __restrict__ pool, size_t page_elems, size_t layer_off, int H, int d,
                          float scale_log2, float* __restrict__ partial) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int DPL = HD / 32;  // head dims per lane
   extern __shared__ __align__(16) unsigned char smem_kv[];
   __shared__ __align__(8) uint64_t bar;
   __shared__ float pbuf[8][FE_PAGE];
   __nv_bfloat16* ks = reinterpret_cast<__nv_bfloat16*>(smem_kv);
   __nv_bfloat16* vs = ks + FE_PAGE * HD;
-  const AttnItem it = items[blockIdx.x];
   const int h = blockIdx.y;
+  const int n_items = hdr[1];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  uint32_t phase = 0;
+  // persistent over work items: grid.x CTAs per head stride through hdr[1] items
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x, phase ^= 1) {
+  __syncthreads();  // previous item's shared-memory reads done / barrier init visible
+  const AttnItem it = items[item];
   int vmax = 0;
   for (int i = 0; i < it.row_count; i++) vmax = max(vmax, item_rows[it.row_begin + i].valid);
   const __nv_bfloat16* kg = pool + (size_t)it.page * page_elems + layer_off + (size_t)h * FE_PAGE * HD;
   const __nv_bfloat16* vg = kg + (size_t)H * FE_PAGE * HD;
   const uint32_t bytes = (uint32_t)(vmax * HD * 2);
-  if (threadIdx.x == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar)), "r"(2 * bytes)
                  : "memory");
@@ -614,8 +642,8 @@ attn_partial_bf16_kernel(const AttnItem* __restrict__ items, const ItemRow* __re
     if (i == warp) {  // first row of this warp: wait for the K/V tiles
       uint32_t done = 0;
       while (!done)
-        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
-                     : "=r"(done) : "r"(smem_u32(&bar)) : "memory");
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(done) : "r"(smem_u32(&bar)), "r"(phase) : "memory");
     }
     // scores, 8 keys per step
     for (int j0 = 0; j0 < ir.valid; j0 += 8) {
@@ -703,6 +731,7 @@ attn_partial_bf16_kernel(const AttnItem* __restrict__ items, const ItemRow* __re
 #pragma unroll
     for (int c = 0; c < DPL; c++) pp[2 + DPL * lane + c] = o[c];
   }
+  }  // item loop
 }
 
 // Merge of chunk partials (exp2 domain), one warp per (row, head).
@@ -710,6 +739,8 @@ template <int HD>
 __global__ void __launch_bounds__(128)
 attn_merge_bf16_kernel(const RowMeta* __restrict__ rows, const float* __restrict__ partial, int H, int d,
                        __nv_bfloat16* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int DPL = HD / 32;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row = blockIdx.x, h = blockIdx.y * 4 + warp;
@@ -749,11 +780,11 @@ static void attention_bf16(const Fwd& f, const ModelDims& m, const float* q, con
     configured = true;
   }
   const float scale_log2 = m.attn_scale * 1.4426950408889634f;
-  if (f.n_items > 0)
-    attn_partial_bf16_kernel<HD><<<dim3(f.n_items, m.H), 256, smem, s>>>(
-        f.items, f.item_rows, f.rows, q, (const __nv_bfloat16*)pool, pe, lo, m.H, m.d, scale_log2, partial);
-  attn_merge_bf16_kernel<HD><<<dim3(f.n_rows, (m.H + 3) / 4), 128, 0, s>>>(f.rows, partial, m.H, m.d,
-                                                                          (__nv_bfloat16*)out);
+  if (f.item_cap > 0)
+    launch_k(attn_partial_bf16_kernel<HD>, dim3(f.item_cap, m.H), dim3(256), smem, s, f.hdr, f.items, f.item_rows,
+             f.rows, q, (const __nv_bfloat16*)pool, pe, lo, m.H, m.d, scale_log2, partial);
+  launch_k(attn_merge_bf16_kernel<HD>, dim3(f.n_rows, (m.H + 3) / 4), dim3(128), 0, s, f.rows, (const float*)partial,
+           m.H, m.d, (__nv_bfloat16*)out);
 }
 
 template <typename KT, int HD>
@@ -767,10 +798,11 @@ static void attention_t(const Fwd& f, const ModelDims& m, const float* q, const 
     cudaFuncSetAttribute(attn_partial_kernel<KT, HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = true;
   }
-  if (f.n_items > 0)
-    attn_partial_kernel<KT, HD><<<dim3(f.n_items, m.H), 128, smem, s>>>(
-        f.items, f.item_rows, f.rows, q, (const KT*)pool, pe, lo, m.H, m.d, m.attn_scale, partial);
-  attn_merge_kernel<KT, HD><<<dim3(f.n_rows, (m.H + 3) / 4), 128, 0, s>>>(f.rows, partial, m.H, m.d, (KT*)out);
+  if (f.item_cap > 0)
+    launch_k(attn_partial_kernel<KT, HD>, dim3(f.item_cap, m.H), dim3(128), smem, s, f.hdr, f.items, f.item_rows,
+             f.rows, q, (const KT*)pool, pe, lo, m.H, m.d, m.attn_scale, partial);
+  launch_k(attn_merge_kernel<KT, HD>, dim3(f.n_rows, (m.H + 3) / 4), dim3(128), 0, s, f.rows, (const float*)partial,
+           m.H, m.d, (KT*)out);
 }
 
 void launch_attention(int dtype, const Fwd& f, const ModelDims& m, const float* q, const void* kv_pool,
