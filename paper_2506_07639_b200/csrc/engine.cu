@@ -41,7 +41,6 @@ constexpr int kMetaRing = 4;
 constexpr int kItemRows = 16;       // query rows per cascade work item
 constexpr int kLogitRows = 256;
 constexpr int kMaxGraphRows = 64;    // decode ticks with <= this many rows replay CUDA graphs
-constexpr int kGraphItemCtas = 32;   // attention CTAs per head (persistent over work items)
 
 struct MetaLayout {
   size_t o_rows, o_items, o_irows, o_heads, total;
@@ -129,10 +128,12 @@ struct fe_engine {
   // metadata layout + decode graphs (one per row count)
   MetaLayout meta_layout{};
   bool graphs_on = true;
+  int debug_skip = 0;  // timing experiments only: 1 attention, 2 rmsnorm, 4 layer GEMMs, 8 lm_head
   struct GraphSlot {
     bool seen = false;
     cudaGraphExec_t exec = nullptr;
-  } graphs[kMaxGraphRows + 1];
+  };
+  std::unordered_map<long, GraphSlot> graphs;  // key: rows * 4096 + attention item bucket
 
   // tcgen05 GEMM path (bf16, wide forwards)
   struct LayerMaps {
@@ -147,6 +148,7 @@ struct fe_engine {
   fe::TmaMap map_lm{};
   float* sk_partial = nullptr;
   int* sk_counters = nullptr;
+  int* attn_counters = nullptr;
 
   // stats
   int64_t n_ticks = 0, n_forwards = 0, n_rows_total = 0;
@@ -288,9 +290,11 @@ void launch_layers(fe_engine* e, const fe::Fwd& f, int n, bool decode, double kv
     const auto& mp = e->tc_maps.empty() ? EngineMapsDummy() : e->tc_maps[l];
     const size_t layer_off = (size_t)l * 2 * m.H * FE_PAGE * m.hd;
     int p;
-    fe::launch_rmsnorm(dt, e->ws.x, ly.attn_norm, e->ws.xn, n, m.d, m.d, m.eps, nullptr, st);
+    const bool skip_norm = e->debug_skip & 2, skip_gemm = e->debug_skip & 4;
+    if (!skip_norm) fe::launch_rmsnorm(dt, e->ws.x, ly.attn_norm, e->ws.xn, n, m.d, m.d, m.eps, nullptr, st);
     p = decode ? prof_begin(e, PROF_GEMV) : -1;
-    if (sk_on(0)) {
+    if (skip_gemm) {
+    } else if (sk_on(0)) {
       fe::SkLaunch t = sk_launch(fe::TC_QKV, 3 * m.d, m.d);
       t.layer_off = layer_off;
       fe::launch_skinny_tc(mp.qkv, e->map_xn16, t, st);
@@ -303,26 +307,29 @@ void launch_layers(fe_engine* e, const fe::Fwd& f, int n, bool decode, double kv
     }
     prof_end(e, p, gemv_bytes(3.0 * m.d, m.d, n));
     p = decode ? prof_begin(e, PROF_ATTN) : -1;
-    fe::launch_attention(dt, f, m, e->ws.q, e->kv_pool, l, e->ws.partial, e->ws.attn, st);
+    if (!(e->debug_skip & 1)) fe::launch_attention(dt, f, m, e->ws.q, e->kv_pool, l, e->ws.partial, e->ws.attn, st);
     prof_end(e, p, kv_bytes);
     p = decode ? prof_begin(e, PROF_GEMV) : -1;
-    if (sk_on(1)) fe::launch_skinny_tc(mp.wo, e->map_attn16, sk_launch(fe::TC_RESID, m.d, m.d), st);
+    if (skip_gemm) {
+    } else if (sk_on(1)) fe::launch_skinny_tc(mp.wo, e->map_attn16, sk_launch(fe::TC_RESID, m.d, m.d), st);
     else if (tc) fe::launch_gemm_tc(e->map_attn, mp.wo, tc_launch(fe::TC_RESID, m.d, m.d), st);
     else fe::launch_resid(dt, f, m.d, m.d, ly.wo, e->ws.attn, e->ws.x, st);
     prof_end(e, p, gemv_bytes(m.d, m.d, n));
-    fe::launch_rmsnorm(dt, e->ws.x, ly.ffn_norm, e->ws.xn, n, m.d, m.d, m.eps, nullptr, st);
+    if (!skip_norm) fe::launch_rmsnorm(dt, e->ws.x, ly.ffn_norm, e->ws.xn, n, m.d, m.d, m.eps, nullptr, st);
     p = decode ? prof_begin(e, PROF_GEMV) : -1;
-    if (sk_on(2)) fe::launch_skinny_tc(mp.wgu, e->map_xn16, sk_launch(fe::TC_SWIGLU, 2 * m.F, m.d), st);
+    if (skip_gemm) {
+    } else if (sk_on(2)) fe::launch_skinny_tc(mp.wgu, e->map_xn16, sk_launch(fe::TC_SWIGLU, 2 * m.F, m.d), st);
     else if (tc) fe::launch_gemm_tc(e->map_xn, mp.wgu, tc_launch(fe::TC_SWIGLU, 2 * m.F, m.d), st);
     else fe::launch_swiglu(dt, f, m.F, m.d, ly.wgu, e->ws.xn, e->ws.attn /* reused as the SwiGLU activation */, st);
     prof_end(e, p, gemv_bytes(2.0 * m.F, m.d, n));
     p = decode ? prof_begin(e, PROF_GEMV) : -1;
-    if (sk_on(3)) fe::launch_skinny_tc(mp.wdown, e->map_act16, sk_launch(fe::TC_RESID, m.d, m.F), st);
+    if (skip_gemm) {
+    } else if (sk_on(3)) fe::launch_skinny_tc(mp.wdown, e->map_act16, sk_launch(fe::TC_RESID, m.d, m.F), st);
     else if (tc) fe::launch_gemm_tc(e->map_act, mp.wdown, tc_launch(fe::TC_RESID, m.d, m.F), st);
     else fe::launch_resid(dt, f, m.d, m.F, ly.wdown, e->ws.attn, e->ws.x, st);
     prof_end(e, p, gemv_bytes(m.d, m.F, n));
   }
-  if (decode) {
+  if (decode && !(e->debug_skip & 8)) {
     fe::launch_rmsnorm(dt, e->ws.x, e->w.final_norm, e->ws.xn, f.n_head_rows, m.d, m.d, m.eps, f.head_rows, st);
     const int p = prof_begin(e, PROF_GEMV);
     if (e->use_tc && (e->sk_mask >> 4 & 1) && f.n_head_rows <= fe::skinny_max_rows()) {
@@ -404,7 +411,12 @@ void forward(fe_engine* e, const std::vector<RowIn>& rows, uint64_t vision_seed)
       it.chunk = page_chunk[kv.first];
       it.row_begin = (int)irows.size();
       it.row_count = (int)std::min<size_t>(kItemRows, lst.size() - b);
-      for (int j = 0; j < it.row_count; j++) irows.push_back({lst[b + j].first, lst[b + j].second});
+      it.valid_max = 0;
+      it.pad[0] = it.pad[1] = it.pad[2] = 0;
+      for (int j = 0; j < it.row_count; j++) {
+        irows.push_back({lst[b + j].first, lst[b + j].second});
+        it.valid_max = std::max(it.valid_max, lst[b + j].second);
+      }
       items.push_back(it);
     }
   }
@@ -447,11 +459,15 @@ void forward(fe_engine* e, const std::vector<RowIn>& rows, uint64_t vision_seed)
   f.n_rows = n;
   f.items = (const fe::AttnItem*)(dbuf + L.o_items);
   f.n_items = (int)items.size();
-  // decode: fixed CTA count per head (graph-replayable); prefill: one CTA per item
-  f.item_cap = items.empty() ? 0 : (head_rows.empty() ? (int)items.size() : kGraphItemCtas);
+  // one attention CTA per (item, head); decode graphs are keyed by (rows,
+  // item bucket of 8) so the grid tracks the item count without re-capture
+  // every tick (CTAs beyond the device-side count exit immediately)
+  const int item_bucket = ((int)items.size() + 7) / 8;
+  f.item_cap = items.empty() ? 0 : (head_rows.empty() ? (int)items.size() : item_bucket * 8);
   f.item_rows = (const fe::ItemRow*)(dbuf + L.o_irows);
   f.n_head_rows = (int)head_rows.size();
   f.head_rows = (const int32_t*)(dbuf + L.o_heads);
+  f.attn_counters = e->attn_counters;
   f.vision_key = fe::tensor_key(vision_seed, 4 /* T_VISION */);
 
   const bool decode = f.n_head_rows > 0;
@@ -468,23 +484,25 @@ void forward(fe_engine* e, const std::vector<RowIn>& rows, uint64_t vision_seed)
   // decode ticks replay a CUDA graph per row count (captured on the second
   // tick with that row count); prefill and profiled runs launch eagerly
   const bool graphable = decode && e->graphs_on && !e->prof_on && n <= kMaxGraphRows;
-  if (graphable && e->graphs[n].exec) {
-    CK(cudaGraphLaunch(e->graphs[n].exec, e->stream));
-  } else if (graphable && e->graphs[n].seen) {
+  const long key = (long)n * 4096 + item_bucket;
+  if (graphable && e->graphs.count(key) && e->graphs[key].exec) {
+    CK(cudaGraphLaunch(e->graphs[key].exec, e->stream));
+  } else if (graphable && e->graphs.count(key) && e->graphs[key].seen) {
     cudaGraph_t g = nullptr;
     CK(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
     launch_layers(e, f, n, decode, kv_bytes, gemv_bytes);
     CK(cudaStreamEndCapture(e->stream, &g));
-    CK(cudaGraphInstantiate(&e->graphs[n].exec, g, 0));
+    CK(cudaGraphInstantiate(&e->graphs[key].exec, g, 0));
     CK(cudaGraphDestroy(g));
-    CK(cudaGraphLaunch(e->graphs[n].exec, e->stream));
+    CK(cudaGraphLaunch(e->graphs[key].exec, e->stream));
   } else {
-    if (graphable) e->graphs[n].seen = true;
+    if (graphable) e->graphs[key].seen = true;
     launch_layers(e, f, n, decode, kv_bytes, gemv_bytes);
   }
   CK(cudaGetLastError());
   // embed + per layer (2 norms, qkv, attention partial + merge, O, gate/up, down) + head
-  e->n_launches += 1 + 8 * m.L + (decode ? 3 : 0) - (items.empty() ? m.L : 0);
+  const int attn_kernels = e->dtype == FE_BF16 ? 1 : 2;  // bf16: merge fused into the attention kernel
+  e->n_launches += 1 + (6 + attn_kernels) * m.L + (decode ? 3 : 0) - (items.empty() ? m.L : 0);
   e->n_forwards++;
   e->n_rows_total += n;
 }
@@ -660,6 +678,8 @@ fe_engine* create(const fe_config* c, int device, const float* rope_host) {
     e->ws.partial = (float*)e->dalloc((size_t)e->max_partials * m.H * (m.hd + 2) * 4);
     e->ws.part_keys = (unsigned long long*)e->dalloc(R * (size_t)fe::lm_head_ctas(m) * 8);
     e->ws.logits = (float*)e->dalloc((size_t)kLogitRows * V * 4);
+    e->attn_counters = (int*)e->dalloc(R * m.H * sizeof(int));
+    CK(cudaMemset(e->attn_counters, 0, R * m.H * sizeof(int)));
     const int n_arena = std::max(4 * e->max_slots, 256);
     e->ws.out_tokens = (int32_t*)e->dalloc((size_t)n_arena * kRequestCap * 4);
     CK(cudaMemset(e->ws.out_tokens, 0, (size_t)n_arena * kRequestCap * 4));
@@ -737,7 +757,7 @@ void destroy(fe_engine* e) {
   cudaSetDevice(e->device);
   cudaStreamSynchronize(e->stream);
   for (auto& g : e->graphs)
-    if (g.exec) cudaGraphExecDestroy(g.exec);
+    if (g.second.exec) cudaGraphExecDestroy(g.second.exec);
   for (void* p : e->allocs) cudaFree(p);
   for (auto& r : e->prof_recs) {
     cudaEventDestroy(r.a);
@@ -1064,7 +1084,19 @@ int fe_set_option(fe_engine* e, const char* key, int64_t value) {
     else if (k == "use_tc") e->use_tc = value != 0 && !e->tc_maps.empty();
     else if (k == "sk_mask") e->sk_mask = (int)value;
     else if (k == "graphs") e->graphs_on = value != 0;
+    else if (k == "debug_skip") {
+      e->debug_skip = (int)value;
+      for (auto& g : e->graphs)
+        if (g.second.exec) cudaGraphExecDestroy(g.second.exec);
+      e->graphs.clear();
+    }
     else if (k == "pdl") fe::g_pdl = value != 0;
+    else if (k == "sk_stages") {
+      fe::g_sk_stages = (int)value;
+      for (auto& g : e->graphs)
+        if (g.second.exec) cudaGraphExecDestroy(g.second.exec);
+      e->graphs.clear();
+    }
     else throw Error("unknown option " + k);
   });
 }

@@ -35,6 +35,8 @@ struct AttnItem {
   int32_t chunk;
   int32_t row_begin;   // into ItemRow[]
   int32_t row_count;
+  int32_t valid_max;   // keys of the page any of the rows needs (bytes to stage)
+  int32_t pad[3];
 };
 struct ItemRow {
   int32_t row;
@@ -55,6 +57,7 @@ struct Fwd {
   int n_items;             // host-side count (eager launches); kernels read hdr[1]
   int item_cap;            // attention CTAs per head (persistent over items)
   const ItemRow* item_rows;
+  int* attn_counters;      // [max_rows][H] arrival counters of the fused attention merge
   int n_head_rows;         // rows that need the lm_head
   const int32_t* head_rows;  // row index of each lm_head row
   uint64_t vision_key;
@@ -87,7 +90,8 @@ struct Workspace {
 };
 
 // --- programmatic dependent launch -------------------------------------------
-extern bool g_pdl;  // engine option "pdl"
+extern bool g_pdl;       // engine option "pdl"
+extern int g_sk_stages;  // engine option "sk_stages" (5 or 10)
 
 template <typename... KArgs, typename... Args>
 inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {

@@ -28,6 +28,8 @@
 
 namespace fe {
 
+int g_sk_stages = 10;
+
 namespace {
 
 constexpr int BM = 128, BN = 128, BK = 64, kStages = 6;
@@ -284,11 +286,12 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
 // in a fixed order by the last CTA of each tile (deterministic), which then
 // applies the fused epilogue.
 constexpr int SN = 16;                        // batch columns per MMA
-constexpr int kSkStages = 10;
+constexpr int kSkStagesMax = 10;
 constexpr int kSkAcc = 4;                     // TMEM accumulator ring (units in flight)
 constexpr int kSkA = BM * BK * 2;             // 16 KB weights per stage
 constexpr int kSkB = SN * BK * 2;             // 2 KB activations per stage
-constexpr int kSkSmem = kSkStages * (kSkA + kSkB) + BM * (SN + 1) * 4 + 1024 + 2048;
+template <int STAGES>
+constexpr int sk_smem() { return STAGES * (kSkA + kSkB) + BM * (SN + 1) * 4 + 1024 + 2048; }
 constexpr uint32_t kSkIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(SN >> 3) << 17) |
                               ((uint32_t)(BM >> 4) << 24);
 
@@ -323,6 +326,7 @@ __device__ __forceinline__ void unit_of(const SkArgs& a, int u, int kb_total, in
   *kb1 = min(kb_total, *kb0 + a.kb_per_split);
 }
 
+template <int kSkStages>
 __global__ void __launch_bounds__(kThreads, 1)
 skinny_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x,
                  const SkArgs a) {
@@ -484,9 +488,9 @@ skinny_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constan
                                       __uint_as_float(raw[4 * i + 2]), __uint_as_float(raw[4 * i + 3])));
         // one gpu-scope fence per CTA after the CTA barrier publishes all 128
         // threads' partials before the arrival count (split-K serial pattern)
+        __threadfence();  // each thread publishes its rows of the partial
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (et == 0) {
-          __threadfence();
           const int prev = atomicAdd(&a.counters[tl], 1);
           const bool last = prev == a.splits - 1;
           if (last) {
@@ -626,7 +630,8 @@ void launch_skinny_tc(const TmaMap& w_map, const TmaMap& x_map, const SkLaunch& 
   static bool configured = false;
   static int n_sm = 148;
   if (!configured) {
-    cudaFuncSetAttribute(skinny_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSkSmem);
+    cudaFuncSetAttribute(skinny_tc_kernel<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, sk_smem<10>());
+    cudaFuncSetAttribute(skinny_tc_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, sk_smem<5>());
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
@@ -663,8 +668,10 @@ void launch_skinny_tc(const TmaMap& w_map, const TmaMap& x_map, const SkLaunch& 
   a.head_rows = l.head_rows; a.H = l.H; a.hd = l.hd; a.d = l.d; a.part_keys = l.part_keys;
   a.logits = l.logits; a.V = l.V; a.n_text = l.n_text;
   const int grid = std::min(a.units, n_sm);
-  launch_k(skinny_tc_kernel, dim3(grid), dim3(kThreads), (size_t)kSkSmem, s,
-           *reinterpret_cast<const CUtensorMap*>(w_map.bytes), *reinterpret_cast<const CUtensorMap*>(x_map.bytes), a);
+  const CUtensorMap& wm = *reinterpret_cast<const CUtensorMap*>(w_map.bytes);
+  const CUtensorMap& xm = *reinterpret_cast<const CUtensorMap*>(x_map.bytes);
+  if (g_sk_stages <= 5) launch_k(skinny_tc_kernel<5>, dim3(grid), dim3(kThreads), (size_t)sk_smem<5>(), s, wm, xm, a);
+  else launch_k(skinny_tc_kernel<10>, dim3(grid), dim3(kThreads), (size_t)sk_smem<10>(), s, wm, xm, a);
 }
 
 void launch_gemm_tc(const TmaMap& a_map, const TmaMap& b_map, const TcLaunch& l, cudaStream_t s) {

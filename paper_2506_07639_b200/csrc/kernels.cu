@@ -590,182 +590,211 @@ attn_merge_kernel(const RowMeta* __restrict__ rows, const float* __restrict__ pa
 
 // ------------------------------------------------- bf16 (fast) attention ----
 // Same cascade work items as the canonical kernel, but free reduction order:
-// 8 warps per (page, head) CTA, one query row per warp; scores for 8 keys at a
-// time are reduced with a reduce-scatter butterfly (9 shuffles per 8 keys
-// instead of 5 per key), softmax in the exp2 domain with fast intrinsics.
+// 8 warps per (page, head) CTA, one query row per warp.  K and V land through
+// two 1-D TMA bulk copies with separate mbarriers, so q.K^T starts while V is
+// still in flight; scores for 8 keys at a time are reduced with a
+// reduce-scatter butterfly (9 shuffles per 8 keys); softmax in the exp2 domain.
+// The chunk merge is fused: after writing its chunk partial, a warp bumps the
+// (row, head) arrival counter and the warp that completes the set merges all
+// chunks of that (row, head) in chunk order (deterministic) and writes the
+// attention output -- no separate merge launch.
 template <int HD>
 __global__ void __launch_bounds__(256)
-attn_partial_bf16_kernel(const int32_t* __restrict__ hdr, const AttnItem* __restrict__ items, const ItemRow* __restrict__ item_rows,
-                         const RowMeta* __restrict__ rows, const float* __restrict__ q,
-                         const __nv_bfloat16* __restrict__ pool, size_t page_elems, size_t layer_off, int H, int d,
-                         float scale_log2, float* __restrict__ partial) {
-  pdl_trigger();
-  pdl_wait();
+attn_fused_bf16_kernel(const int32_t* __restrict__ hdr, const AttnItem* __restrict__ items,
+                       const ItemRow* __restrict__ item_rows, const RowMeta* __restrict__ rows,
+                       const float* __restrict__ q, const __nv_bfloat16* __restrict__ pool, size_t page_elems,
+                       size_t layer_off, int H, int d, float scale_log2, float* __restrict__ partial,
+                       int* __restrict__ counters, __nv_bfloat16* __restrict__ out) {
   constexpr int DPL = HD / 32;  // head dims per lane
+  pdl_trigger();
   extern __shared__ __align__(16) unsigned char smem_kv[];
-  __shared__ __align__(8) uint64_t bar;
+  __shared__ __align__(8) uint64_t bar[2];
   __shared__ float pbuf[8][FE_PAGE];
   __nv_bfloat16* ks = reinterpret_cast<__nv_bfloat16*>(smem_kv);
   __nv_bfloat16* vs = ks + FE_PAGE * HD;
   const int h = blockIdx.y;
-  const int n_items = hdr[1];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
   if (threadIdx.x == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[0])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[1])));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  uint32_t phase = 0;
-  // persistent over work items: grid.x CTAs per head stride through hdr[1] items
-  for (int item = blockIdx.x; item < n_items; item += gridDim.x, phase ^= 1) {
-  __syncthreads();  // previous item's shared-memory reads done / barrier init visible
-  const AttnItem it = items[item];
-  int vmax = 0;
-  for (int i = 0; i < it.row_count; i++) vmax = max(vmax, item_rows[it.row_begin + i].valid);
-  const __nv_bfloat16* kg = pool + (size_t)it.page * page_elems + layer_off + (size_t)h * FE_PAGE * HD;
-  const __nv_bfloat16* vg = kg + (size_t)H * FE_PAGE * HD;
-  const uint32_t bytes = (uint32_t)(vmax * HD * 2);
-  if (threadIdx.x == 0) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar)), "r"(2 * bytes)
-                 : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 ::"r"(smem_u32(ks)), "l"(kg), "r"(bytes), "r"(smem_u32(&bar)) : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 ::"r"(smem_u32(vs)), "l"(vg), "r"(bytes), "r"(smem_u32(&bar)) : "memory");
-  }
-  for (int i = warp; i < it.row_count; i += 8) {
-    const ItemRow ir = item_rows[it.row_begin + i];
-    const RowMeta m = rows[ir.row];
-    float qv[DPL];
-#pragma unroll
-    for (int c = 0; c < DPL; c++) qv[c] = q[(size_t)ir.row * d + h * HD + DPL * lane + c] * scale_log2;
-    if (i == warp) {  // first row of this warp: wait for the K/V tiles
-      uint32_t done = 0;
-      while (!done)
-        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-                     : "=r"(done) : "r"(smem_u32(&bar)), "r"(phase) : "memory");
-    }
-    // scores, 8 keys per step
-    for (int j0 = 0; j0 < ir.valid; j0 += 8) {
-      float part[8];
-#pragma unroll
-      for (int t = 0; t < 8; t++) {
-        const __nv_bfloat16* kr = ks + (j0 + t) * HD + DPL * lane;
-        float a = 0.0f;
-        if (DPL == 4) {
-          const uint2 raw = *reinterpret_cast<const uint2*>(kr);
-          a = fmaf(qv[0], __uint_as_float(raw.x << 16), a);
-          a = fmaf(qv[1], __uint_as_float(raw.x & 0xffff0000u), a);
-          a = fmaf(qv[2], __uint_as_float(raw.y << 16), a);
-          a = fmaf(qv[3], __uint_as_float(raw.y & 0xffff0000u), a);
-        } else {
-          const uint32_t raw = *reinterpret_cast<const uint32_t*>(kr);
-          a = fmaf(qv[0], __uint_as_float(raw << 16), a);
-          a = fmaf(qv[DPL - 1], __uint_as_float(raw & 0xffff0000u), a);
-        }
-        part[t] = a;
-      }
-      // reduce-scatter: after the xor-16/8/4 steps lane holds key (lane >> 2) & 7
-#pragma unroll
-      for (int t = 0; t < 4; t++) {
-        const bool up = lane & 16;
-        const float send = up ? part[t] : part[t + 4];
-        const float keep = up ? part[t + 4] : part[t];
-        part[t] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-      }
-#pragma unroll
-      for (int t = 0; t < 2; t++) {
-        const bool up = lane & 8;
-        const float send = up ? part[t] : part[t + 2];
-        const float keep = up ? part[t + 2] : part[t];
-        part[t] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-      }
-      {
-        const bool up = lane & 4;
-        const float send = up ? part[0] : part[1];
-        const float keep = up ? part[1] : part[0];
-        part[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-      }
-      float s = part[0];
-      s += __shfl_xor_sync(0xffffffffu, s, 2);
-      s += __shfl_xor_sync(0xffffffffu, s, 1);
-      const int j = j0 + ((lane >> 2) & 7);
-      if ((lane & 3) == 0) pbuf[warp][j] = j < ir.valid ? s : -INFINITY;
-    }
-    __syncwarp();
-    const float s0 = lane < ir.valid ? pbuf[warp][lane] : -INFINITY;
-    const float s1 = lane + 32 < ir.valid ? pbuf[warp][lane + 32] : -INFINITY;
-    float mx = fmaxf(s0, s1);
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-    const float p0 = lane < ir.valid ? exp2f(s0 - mx) : 0.0f;
-    const float p1 = lane + 32 < ir.valid ? exp2f(s1 - mx) : 0.0f;
-    float l = p0 + p1;
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
-    __syncwarp();
-    pbuf[warp][lane] = p0;
-    pbuf[warp][lane + 32] = p1;
-    __syncwarp();
-    float o[DPL];
-#pragma unroll
-    for (int c = 0; c < DPL; c++) o[c] = 0.0f;
-    for (int j = 0; j < ir.valid; j++) {
-      const float p = pbuf[warp][j];
-      const __nv_bfloat16* vr = vs + j * HD + DPL * lane;
-      if (DPL == 4) {
-        const uint2 raw = *reinterpret_cast<const uint2*>(vr);
-        o[0] = fmaf(p, __uint_as_float(raw.x << 16), o[0]);
-        o[1] = fmaf(p, __uint_as_float(raw.x & 0xffff0000u), o[1]);
-        o[2] = fmaf(p, __uint_as_float(raw.y << 16), o[2]);
-        o[3] = fmaf(p, __uint_as_float(raw.y & 0xffff0000u), o[3]);
-      } else {
-        const uint32_t raw = *reinterpret_cast<const uint32_t*>(vr);
-        o[0] = fmaf(p, __uint_as_float(raw << 16), o[0]);
-        o[DPL - 1] = fmaf(p, __uint_as_float(raw & 0xffff0000u), o[DPL - 1]);
-      }
-    }
-    __syncwarp();
-    float* pp = partial + ((size_t)(m.chunk_base + it.chunk) * H + h) * (HD + 2);
-    if (lane == 0) { pp[0] = mx; pp[1] = l; }
-#pragma unroll
-    for (int c = 0; c < DPL; c++) pp[2 + DPL * lane + c] = o[c];
-  }
-  }  // item loop
-}
-
-// Merge of chunk partials (exp2 domain), one warp per (row, head).
-template <int HD>
-__global__ void __launch_bounds__(128)
-attn_merge_bf16_kernel(const RowMeta* __restrict__ rows, const float* __restrict__ partial, int H, int d,
-                       __nv_bfloat16* __restrict__ out) {
-  pdl_trigger();
   pdl_wait();
-  constexpr int DPL = HD / 32;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int row = blockIdx.x, h = blockIdx.y * 4 + warp;
-  if (h >= H) return;
-  const RowMeta m = rows[row];
-  const float* base = partial + ((size_t)m.chunk_base * H + h) * (HD + 2);
-  const size_t stride = (size_t)H * (HD + 2);
-  float M = -INFINITY;
-  for (int c = lane; c < m.n_chunks; c += 32) M = fmaxf(M, base[c * stride]);
+  const int n_items = hdr[1];
+  uint32_t phase = 0;
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x, phase ^= 1) {
+    __syncthreads();  // previous item's shared-memory reads done / barrier init visible
+    const AttnItem it = items[item];
+    const int vmax = it.valid_max;
+    const __nv_bfloat16* kg = pool + (size_t)it.page * page_elems + layer_off + (size_t)h * FE_PAGE * HD;
+    const __nv_bfloat16* vg = kg + (size_t)H * FE_PAGE * HD;
+    const uint32_t bytes = (uint32_t)(vmax * HD * 2);
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar[0])), "r"(bytes)
+                   : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(smem_u32(ks)), "l"(kg), "r"(bytes), "r"(smem_u32(&bar[0])) : "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar[1])), "r"(bytes)
+                   : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(smem_u32(vs)), "l"(vg), "r"(bytes), "r"(smem_u32(&bar[1])) : "memory");
+    }
+    for (int i = warp; i < it.row_count; i += 8) {
+      const ItemRow ir = item_rows[it.row_begin + i];
+      const RowMeta m = rows[ir.row];
+      float qv[DPL];
 #pragma unroll
-  for (int off = 16; off >= 1; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
-  float L = 0.0f, o[DPL];
+      for (int c = 0; c < DPL; c++) qv[c] = q[(size_t)ir.row * d + h * HD + DPL * lane + c] * scale_log2;
+      if (i == warp) {
+        uint32_t done = 0;
+        while (!done)
+          asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                       : "=r"(done) : "r"(smem_u32(&bar[0])), "r"(phase) : "memory");
+      }
+      for (int j0 = 0; j0 < ir.valid; j0 += 8) {
+        float part[8];
 #pragma unroll
-  for (int c = 0; c < DPL; c++) o[c] = 0.0f;
-  for (int c = 0; c < m.n_chunks; c++) {
-    const float* pc = base + c * stride;
-    const float sc = exp2f(pc[0] - M);
-    L = fmaf(sc, pc[1], L);
+        for (int t = 0; t < 8; t++) {
+          const __nv_bfloat16* kr = ks + (j0 + t) * HD + DPL * lane;
+          float a = 0.0f;
+          if (DPL == 4) {
+            const uint2 raw = *reinterpret_cast<const uint2*>(kr);
+            a = fmaf(qv[0], __uint_as_float(raw.x << 16), a);
+            a = fmaf(qv[1], __uint_as_float(raw.x & 0xffff0000u), a);
+            a = fmaf(qv[2], __uint_as_float(raw.y << 16), a);
+            a = fmaf(qv[3], __uint_as_float(raw.y & 0xffff0000u), a);
+          } else {
+            const uint32_t raw = *reinterpret_cast<const uint32_t*>(kr);
+            a = fmaf(qv[0], __uint_as_float(raw << 16), a);
+            a = fmaf(qv[DPL - 1], __uint_as_float(raw & 0xffff0000u), a);
+          }
+          part[t] = a;
+        }
 #pragma unroll
-    for (int i = 0; i < DPL; i++) o[i] = fmaf(sc, pc[2 + DPL * lane + i], o[i]);
-  }
-  const float inv = 1.0f / L;
-  __nv_bfloat16* dst = out + (size_t)row * d + h * HD + DPL * lane;
+        for (int t = 0; t < 4; t++) {
+          const bool up = lane & 16;
+          const float send = up ? part[t] : part[t + 4];
+          const float keep = up ? part[t + 4] : part[t];
+          part[t] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+        }
 #pragma unroll
-  for (int i = 0; i < DPL; i++) dst[i] = __float2bfloat16_rn(o[i] * inv);
+        for (int t = 0; t < 2; t++) {
+          const bool up = lane & 8;
+          const float send = up ? part[t] : part[t + 2];
+          const float keep = up ? part[t + 2] : part[t];
+          part[t] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+        }
+        {
+          const bool up = lane & 4;
+          const float send = up ? part[0] : part[1];
+          const float keep = up ? part[1] : part[0];
+          part[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+        }
+        float sc = part[0];
+        sc += __shfl_xor_sync(0xffffffffu, sc, 2);
+        sc += __shfl_xor_sync(0xffffffffu, sc, 1);
+        const int j = j0 + ((lane >> 2) & 7);
+        if ((lane & 3) == 0) pbuf[warp][j] = j < ir.valid ? sc : -INFINITY;
+      }
+      __syncwarp();
+      const float s0 = lane < ir.valid ? pbuf[warp][lane] : -INFINITY;
+      const float s1 = lane + 32 < ir.valid ? pbuf[warp][lane + 32] : -INFINITY;
+      float mx = fmaxf(s0, s1);
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+      const float p0 = lane < ir.valid ? exp2f(s0 - mx) : 0.0f;
+      const float p1 = lane + 32 < ir.valid ? exp2f(s1 - mx) : 0.0f;
+      float l = p0 + p1;
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
+      __syncwarp();
+      pbuf[warp][lane] = p0;
+      pbuf[warp][lane + 32] = p1;
+      __syncwarp();
+      if (i == warp) {
+        uint32_t done = 0;
+        while (!done)
+          asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                       : "=r"(done) : "r"(smem_u32(&bar[1])), "r"(phase) : "memory");
+      }
+      float o[DPL];
+#pragma unroll
+      for (int c = 0; c < DPL; c++) o[c] = 0.0f;
+#pragma unroll 8
+      for (int j = 0; j < ir.valid; j++) {
+        const float p = pbuf[warp][j];
+        const __nv_bfloat16* vr = vs + j * HD + DPL * lane;
+        if (DPL == 4) {
+          const uint2 raw = *reinterpret_cast<const uint2*>(vr);
+          o[0] = fmaf(p, __uint_as_float(raw.x << 16), o[0]);
+          o[1] = fmaf(p, __uint_as_float(raw.x & 0xffff0000u), o[1]);
+          o[2] = fmaf(p, __uint_as_float(raw.y << 16), o[2]);
+          o[3] = fmaf(p, __uint_as_float(raw.y & 0xffff0000u), o[3]);
+        } else {
+          const uint32_t raw = *reinterpret_cast<const uint32_t*>(vr);
+          o[0] = fmaf(p, __uint_as_float(raw << 16), o[0]);
+          o[DPL - 1] = fmaf(p, __uint_as_float(raw & 0xffff0000u), o[DPL - 1]);
+        }
+      }
+      float* pp = partial + ((size_t)(m.chunk_base + it.chunk) * H + h) * (HD + 2);
+      if (lane == 0) { pp[0] = mx; pp[1] = l; }
+#pragma unroll
+      for (int c = 0; c < DPL; c++) pp[2 + DPL * lane + c] = o[c];
+
+      // ---- fused merge: the warp that delivers the last chunk of (row, head)
+      int prev = 0;
+      __syncwarp();
+      __threadfence();  // every lane publishes its slice of the partial
+      if (lane == 0) prev = atomicAdd(&counters[ir.row * H + h], 1);
+      prev = __shfl_sync(0xffffffffu, prev, 0);
+      if (prev == m.n_chunks - 1) {
+        if (lane == 0) counters[ir.row * H + h] = 0;  // ready for the next launch
+        __threadfence();
+        const float* base = partial + ((size_t)m.chunk_base * H + h) * (HD + 2);
+        const size_t stride = (size_t)H * (HD + 2);
+        // chunk weights lane-parallel (lane c <-> chunk c, c + 32, ...), then
+        // every lane accumulates its head dims over all chunks with the loads
+        // of a group of 8 chunks in flight together
+        float M = -INFINITY;
+        for (int c = lane; c < m.n_chunks; c += 32) M = fmaxf(M, __ldcg(base + c * stride));
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+        float L = 0.0f, acc[DPL];
+#pragma unroll
+        for (int c = 0; c < DPL; c++) acc[c] = 0.0f;
+        for (int c0 = 0; c0 < m.n_chunks; c0 += 32) {
+          const int c = c0 + lane;
+          const float wl = c < m.n_chunks ? exp2f(__ldcg(base + c * stride) - M) : 0.0f;
+          float lsum = c < m.n_chunks ? wl * __ldcg(base + c * stride + 1) : 0.0f;
+#pragma unroll
+          for (int off = 16; off >= 1; off >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, off);
+          L += lsum;
+          const int nc = min(32, m.n_chunks - c0);
+          for (int g = 0; g < nc; g += 8) {
+            float v[8][DPL], w[8];
+#pragma unroll
+            for (int t = 0; t < 8; t++) {
+              w[t] = __shfl_sync(0xffffffffu, wl, (g + t) & 31);
+              if (g + t < nc) {
+#pragma unroll
+                for (int e = 0; e < DPL; e++) v[t][e] = __ldcg(base + (c0 + g + t) * stride + 2 + DPL * lane + e);
+              }
+            }
+#pragma unroll
+            for (int t = 0; t < 8; t++)
+              if (g + t < nc) {
+#pragma unroll
+                for (int e = 0; e < DPL; e++) acc[e] = fmaf(w[t], v[t][e], acc[e]);
+              }
+          }
+        }
+        const float inv = 1.0f / L;
+        __nv_bfloat16* dst = out + (size_t)ir.row * d + h * HD + DPL * lane;
+#pragma unroll
+        for (int e = 0; e < DPL; e++) dst[e] = __float2bfloat16_rn(acc[e] * inv);
+      }
+    }
+  }  // item loop
 }
 
 template <int HD>
@@ -776,15 +805,14 @@ static void attention_bf16(const Fwd& f, const ModelDims& m, const float* q, con
   const size_t smem = 2 * (size_t)FE_PAGE * HD * 2;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(attn_partial_bf16_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(attn_fused_bf16_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = true;
   }
   const float scale_log2 = m.attn_scale * 1.4426950408889634f;
   if (f.item_cap > 0)
-    launch_k(attn_partial_bf16_kernel<HD>, dim3(f.item_cap, m.H), dim3(256), smem, s, f.hdr, f.items, f.item_rows,
-             f.rows, q, (const __nv_bfloat16*)pool, pe, lo, m.H, m.d, scale_log2, partial);
-  launch_k(attn_merge_bf16_kernel<HD>, dim3(f.n_rows, (m.H + 3) / 4), dim3(128), 0, s, f.rows, (const float*)partial,
-           m.H, m.d, (__nv_bfloat16*)out);
+    launch_k(attn_fused_bf16_kernel<HD>, dim3(f.item_cap, m.H), dim3(256), smem, s, f.hdr, f.items, f.item_rows,
+             f.rows, q, (const __nv_bfloat16*)pool, pe, lo, m.H, m.d, scale_log2, partial, f.attn_counters,
+             (__nv_bfloat16*)out);
 }
 
 template <typename KT, int HD>

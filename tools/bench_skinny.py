@@ -9,6 +9,9 @@ import torch  # noqa: E402
 from paper_2506_07639_b200.engine import Engine  # noqa: E402
 
 eng = Engine("small", dtype="bf16", seed=0, kv_pages=8, max_rows=64)
+import os
+if os.environ.get("SK_STAGES"):
+    eng.set_option("sk_stages", int(os.environ["SK_STAGES"]))
 stream = torch.cuda.ExternalStream(eng.stream_handle())
 shapes = {"qkv": (12288, 4096), "o": (4096, 4096), "gate_up": (22016, 4096), "down": (4096, 11008),
           "lm_head": (32128, 4096)}

@@ -22,9 +22,15 @@ ap.add_argument("--trunk", type=int, default=625)
 ap.add_argument("--ticks", type=int, default=8)
 ap.add_argument("--repeat", type=int, default=3)
 ap.add_argument("--profile", action="store_true")
+ap.add_argument("--skip", type=int, default=0, help="debug_skip mask (timing attribution only)")
+ap.add_argument("--stages", type=int, default=0)
 args = ap.parse_args()
 
 eng = Engine(args.config, dtype=args.dtype, seed=0, kv_pages=256)
+if args.skip:
+    eng.set_option("debug_skip", args.skip)
+if args.stages:
+    eng.set_option("sk_stages", args.stages)
 cfg = M.get_config(args.config)
 ids = [M.BOS_ID] + [M.VIS_ID] * cfg.n_vision + list(range(100, 100 + args.trunk - 1 - cfg.n_vision))
 stream = torch.cuda.ExternalStream(eng.stream_handle())
