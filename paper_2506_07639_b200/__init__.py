@@ -10,7 +10,7 @@ from .backends import (BackendError, EngineError, GenerationBackend, StepGenerat
                        SyntheticBackend, SyntheticProfile, default_profile, length_plan, stable_digest)
 from .batching import (EMPTY, PAD, BatchError, BatchSchedule, GenerationRequest, LatencyModel,
                        continuous_batch, padding_waste, schedule_cost, schedule_to_csv, static_batch)
-from .schedulers import (MODES, CachedTrace, CacheSnapshot, ConfigError, EpisodeAborted,
+from .schedulers import (MODES, BatchedEpisodes, CachedTrace, CacheSnapshot, ConfigError, EpisodeAborted,
                          ParallelAsyncRunner, ParallelSyncRunner, SchedulerConfig, SequentialRunner,
                          StepResult, decode_action, make_runner, observation_for, run_episode,
                          run_parallel_async, run_parallel_sync, run_sequential, summarize_results)

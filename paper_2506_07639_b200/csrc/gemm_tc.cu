@@ -117,7 +117,10 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
   uint32_t* tmem_slot = (uint32_t*)(tmem_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM;
+  // M tiles fastest: the CTAs sharing a weight tile run together, so wide
+  // batches read each weight tile from DRAM once (L2 serves the others)
+  const int m_tile = blockIdx.x, n_tile = blockIdx.y;
+  const int n0 = n_tile * BN, m0 = m_tile * BM;
   const int kblocks = (a.K + BK - 1) / BK;
 
   if (warp == 0 && lane == 0) {
@@ -148,7 +151,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         mbar_expect_tx(&full[s], 2 * kTileBytes);
         tma_load_2d(sa + s * kTileBytes, &map_a, &full[s], kb * BK, m0);
         if (a.epi == TC_SWIGLU) {  // 64 gate rows ++ 64 up rows of the same features
-          const int f0 = blockIdx.x * (BN / 2);
+          const int f0 = n_tile * (BN / 2);
           tma_load_2d(sb + s * kTileBytes, &map_b, &full[s], kb * BK, f0);
           tma_load_2d(sb + s * kTileBytes + kTileBytes / 2, &map_b, &full[s], kb * BK, a.F + f0);
         } else {
@@ -207,7 +210,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         }
       }
     } else if (a.epi == TC_SWIGLU) {
-      const int f0 = blockIdx.x * (BN / 2);
+      const int f0 = n_tile * (BN / 2);
       for (int c = 0; c < BN / 2; c += 32) {
         float g[32], u[32];
         tmem_ld32(tbase + c, g);
@@ -686,7 +689,7 @@ void launch_gemm_tc(const TmaMap& a_map, const TmaMap& b_map, const TcLaunch& l,
   a.q = l.q; a.kv_pool = l.kv_pool; a.page_elems = l.page_elems; a.layer_off = l.layer_off;
   a.rope = l.rope; a.rows = l.rows; a.H = l.H; a.hd = l.hd; a.d = l.d;
   const int n_tiles = l.epi == TC_SWIGLU ? (l.F / (BN / 2)) : (l.N / BN);
-  dim3 grid(n_tiles, (l.M + BM - 1) / BM);
+  dim3 grid((l.M + BM - 1) / BM, n_tiles);
   gemm_tc_kernel<<<grid, kThreads, kSmem, s>>>(*reinterpret_cast<const CUtensorMap*>(a_map.bytes),
                                                *reinterpret_cast<const CUtensorMap*>(b_map.bytes), a);
 }

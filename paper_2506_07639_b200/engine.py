@@ -104,10 +104,11 @@ class Engine:
     """One engine per GPU: weights, paged KV pool, continuous batcher."""
 
     def __init__(self, config: str | ModelConfig = "tiny", dtype: str = "f32", device: int = 0,
-                 seed: int = 0, max_rows: int = 512, kv_pages: int = 0, max_slots: int = 64):
+                 seed: int = 0, max_rows: int = 512, kv_pages: int = 0, max_slots: int = 512):
         self.cfg = get_config(config)
         self.lib = load_library()
         self.dtype = dtype
+        self.max_slots = max_slots
         c = self.cfg
         fc = FeConfig(c.d_model, c.n_layers, c.n_heads, c.head_dim, c.d_ffn, c.vocab, TEXT_VOCAB,
                       ROPE_MAX_POS, c.rms_eps, float(np.float32(1.0) / np.sqrt(np.float32(c.head_dim))),

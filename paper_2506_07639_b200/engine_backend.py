@@ -80,6 +80,7 @@ class EngineBackend:
         self._trunk_cap = trunk_cache
         self._clock = 0
         self._owners: dict[int, EngineRequest] = {}
+        self._slots = 8
         self.requests = 0
 
     # -- protocol ------------------------------------------------------------
@@ -117,8 +118,39 @@ class EngineBackend:
             outcomes[i] = StepGenerator(h.tokens, truncated=h.truncated)
         return outcomes
 
+    def begin_steps_multi(self, contexts: Sequence[Context], jobs_per_context: Sequence[Sequence],
+                          priorities=None) -> list[list]:
+        """Branch jobs of several independent contexts (episodes) decoded as one
+        batch (BASELINE config 4).  Returns per context a list of
+        StepGenerator / BackendError in job order."""
+        outcomes: list[list] = [[None] * len(j) for j in jobs_per_context]
+        handles: dict[tuple[int, int], EngineRequest] = {}
+        self._ensure_slots(sum(len(j) for j in jobs_per_context))
+        for e, (ctx, jobs) in enumerate(zip(contexts, jobs_per_context)):
+            prios = priorities[e] if priorities else [PRIO_REASONING] * (len(jobs) - 1) + [PRIO_ACTION]
+            for i in sorted(range(len(jobs)), key=lambda i: -len(jobs[i][1])):
+                spec, prefix, prev = jobs[i]
+                try:
+                    handles[(e, i)] = self._prepare(ctx, prefix, spec, prev, prios[i])
+                except BackendError as exc:
+                    outcomes[e][i] = exc
+        for key in sorted(handles):
+            self._submit(handles[key], None)
+        for key in sorted(handles):
+            h = handles[key]
+            if not h.done:
+                self._run(h.req, 0)
+            outcomes[key[0]][key[1]] = StepGenerator(h.tokens, truncated=h.truncated)
+        return outcomes
+
     def make_async_engine(self, slots: int) -> "AsyncEngine":
         return AsyncEngine(self, slots)
+
+    def _ensure_slots(self, n: int) -> None:
+        """Grow the batcher so a multi-episode barrier fits in one batch."""
+        if n > self._slots:
+            self._slots = min(n, self.engine.max_slots)
+            self.engine.set_slots(self._slots)
 
     # -- trunks & branches -----------------------------------------------------
     def _branch_point(self, vseed: int, ids: np.ndarray) -> tuple[int, bool]:
@@ -191,6 +223,7 @@ class AsyncEngine:
     def __init__(self, backend: EngineBackend, slots: int):
         self.backend = backend
         backend.engine.set_slots(slots)
+        backend._slots = slots
         self._inflight: dict[int, EngineRequest] = {}
 
     def prepare(self, ctx, prefix, spec, prev_content, priority: str, timestep: int) -> EngineRequest:

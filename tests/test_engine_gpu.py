@@ -308,3 +308,36 @@ def test_bf16_skinny_after_prefill_paths(plen, tc_rows):
         eng.close()
     rel = np.abs(out[31][1] - out[0][1]).max() / np.abs(out[0][1]).max()
     assert rel < 2e-2, rel
+
+
+def test_batched_episodes_bit_exact_vs_independent_oracle_episodes(schema):
+    """Config 4 path: 3 episodes stepped in lockstep, all branches of a
+    timestep in one decode batch (21 rows), fp32 engine == each episode run
+    alone through the runners over the CPU oracle (batch invariance)."""
+    from oracle.backend import OracleBackend, OracleModel
+    seeds, T_ = [0, 1, 2], 3
+    be = EngineBackend("tiny", dtype="f32", seed=0, kv_pages=1024)
+    try:
+        drv = S.BatchedEpisodes(S.SchedulerConfig(mode="parallel_sync", slots=8), be, schema, seeds)
+        got = [drv.step(t) for t in range(T_)]
+    finally:
+        be.close()
+    model = OracleModel("tiny", seed=0)
+    for e, seed in enumerate(seeds):
+        want, _ = S.run_episode(S.SchedulerConfig(mode="parallel_sync", slots=8), T_,
+                                OracleBackend("tiny", seed=0, model=model), schema, seed=seed)
+        for t in range(T_):
+            assert T.trace_content_bytes(got[t][e].trace, schema) == T.trace_content_bytes(want[t].trace, schema)
+            assert got[t][e].latency_ms == want[t].latency_ms
+
+
+def test_bf16_wide_batch_decode_runs(schema):
+    """Config 4 shape on the small model: 8 episodes x 7 branches = 56 rows per
+    tick through the tcgen05 tile GEMM (M-fastest raster)."""
+    be = EngineBackend("small", dtype="bf16", seed=0, kv_pages=2048)
+    try:
+        drv = S.BatchedEpisodes(S.SchedulerConfig(mode="parallel_sync", slots=8), be, schema, list(range(8)))
+        res = [drv.step(t) for t in range(2)]
+    finally:
+        be.close()
+    assert all(len(r.trace.steps) == len(schema.steps) for step in res for r in step)
