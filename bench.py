@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--config", default="7b")
     ap.add_argument("--dtype", default="bf16")
     ap.add_argument("--mode", default="parallel_sync")
+    ap.add_argument("--workload", choices=("config2", "stress"), default="config2",
+                    help="config2: default ECoT schema; stress: config 5 (8-way fan-out, ~2k-token cached prefix)")
     ap.add_argument("--episodes", type=int, default=1,
                     help="total episodes (config 4: >1 shards them over ranks, batched per timestep)")
     ap.add_argument("--seq-steps", type=int, default=2)
@@ -287,10 +289,12 @@ def run_engine(args, rank, world, local):
     from paper_2506_07639_b200.engine_backend import EngineBackend
     from paper_2506_07639_b200.trace import default_schema
 
+    from paper_2506_07639_b200.workloads import WORKLOADS
     torch.cuda.set_device(local)
-    schema = default_schema()
+    make_schema, make_profile = WORKLOADS[args.workload]
+    schema = make_schema()
     seed = rank
-    backend = EngineBackend(args.config, dtype=args.dtype, seed=0, device=local)
+    backend = EngineBackend(args.config, dtype=args.dtype, seed=0, device=local, profile=make_profile(0))
     eng = backend.engine
     stream = torch.cuda.ExternalStream(eng.stream_handle(), device=local)
     cfg_run = S.SchedulerConfig(mode=args.mode, slots=8, wall_clock=True)
@@ -340,12 +344,26 @@ def run_engine(args, rank, world, local):
         sdev, shost, _ = time_mode(backend, seq_runner, 1000 + seed, 0, 1 + args.seq_steps, stream)
         asy = S.make_runner(S.SchedulerConfig(mode="parallel_async", slots=8, wall_clock=True), backend, schema)
         adev, ahost, ares = time_mode(backend, asy, 2000 + seed, 0, 1 + args.async_steps, stream)
+        # config 3 proper: two CUDA streams, reasoning refresh free-running on the
+        # low-priority lane between and during control steps
+        backend2 = EngineBackend(args.config, dtype=args.dtype, seed=0, device=local, profile=make_profile(0),
+                                 engine=backend.engine, async_streams=2)
+        asy2 = S.make_runner(S.SchedulerConfig(mode="parallel_async", slots=8, wall_clock=True), backend2, schema)
+        a2dev, a2host, a2res = time_mode(backend2, asy2, 3000 + seed, 0, 1 + args.async_steps, stream)
+        asy2.engine.drain()
+        asy2.engine.close()
+        stal = [max(v for k, v in r.staleness.items() if k != schema.action_step.name) for r in a2res[1:]]
         extras = {
             "sequential_ms": {"p50": statistics.median(sdev[1:]), "steps": len(sdev) - 1,
                               "all": [round(x, 2) for x in sdev[1:]]},
             "parallel_async_action_ms": {"p50": statistics.median(adev[1:]),
                                          "p99": sorted(adev[1:])[max(0, int(0.99 * (len(adev) - 1)) - 1)],
-                                         "steps": len(adev) - 1},
+                                         "steps": len(adev) - 1, "scheduler": "lockstep (reference landing order)"},
+            "parallel_async_2stream_action_ms": {"p50": statistics.median(a2host[1:]),
+                                                 "p99": sorted(a2host[1:])[max(0, int(0.99 * (len(a2host) - 1)) - 1)],
+                                                 "steps": len(a2host) - 1,
+                                                 "max_reasoning_staleness_p50": statistics.median(stal),
+                                                 "scheduler": "two CUDA streams, host wall clock per action"},
         }
     gathered = gather_objects({"rank": rank, "dev_ms": dev, "host_ms": host}, world)
     return backend, dict(dev=dev, host=host, results=results, total_max=total_max, host_max=host_max,
@@ -417,7 +435,7 @@ def main():
                                (f"config 4: batched rollouts of {args.episodes} independent episodes sharded "
                                 f"over {world} GPU(s), 7B-shaped, Fast ECoT parallel_sync, one decode batch "
                                 f"per timestep per GPU"),
-                   "model": args.config, "mode": args.mode,
+                   "model": args.config, "mode": args.mode, "schema": args.workload,
                    "episodes": args.episodes if args.episodes > 1 else world,
                    "episodes_per_gpu": (args.episodes / world) if args.episodes > 1 else 1, "slots": 8,
                    "l2": "no flush: every decode iteration streams 13.2 GB of weights (> 126 MB L2)"},

@@ -80,6 +80,17 @@ int fe_submit(fe_engine* e, int32_t seq, int32_t first_id, int32_t length, int32
  * completed_tick[i].  Arrays need room for `cap` entries. */
 int fe_run(fe_engine* e, int32_t stop_req, int32_t cap, int32_t* n_ticks, int32_t* occupancy,
            int32_t* completed, int32_t* completed_tick, int32_t* n_completed);
+/* lanes: 0 = foreground (highest stream priority; prefills, forks and the
+ * calls above), 1 = background (lowest priority; reasoning refresh of the
+ * two-stream async scheduler).  Each lane has its own stream, batcher and
+ * decode graphs; fe_run_lane locks the engine per tick, so two host threads
+ * may drive the two lanes concurrently.  max_ticks <= 0: unbounded. */
+int fe_set_slots_lane(fe_engine* e, int32_t lane, int32_t slots);
+int fe_submit_lane(fe_engine* e, int32_t lane, int32_t seq, int32_t first_id, int32_t length, int32_t priority,
+                   int32_t* req);
+int fe_run_lane(fe_engine* e, int32_t lane, int32_t stop_req, int32_t max_ticks, int32_t cap, int32_t* n_ticks,
+                int32_t* occupancy, int32_t* completed, int32_t* completed_tick, int32_t* n_completed);
+int fe_stream_lane(fe_engine* e, int32_t lane, void** stream);
 int fe_request_tokens(fe_engine* e, int32_t req, int32_t* out, int32_t cap);
 int fe_request_release(fe_engine* e, int32_t req);
 int fe_request_capture_logits(fe_engine* e, int32_t req);  /* parity mode: keep fp32 logits */

@@ -1,5 +1,5 @@
 // Host side of the Fast-ECoT B200 engine: weights, paged KV pool, forward
-// passes, the continuous batcher and the C ABI (include/fastecot.h).
+// passes, the continuous batcher(s) and the C ABI (include/fastecot.h).
 //
 // Reference anchors: the batcher's admission policy restates the simulated
 // `_MicroEngine.tick` (pkg/src/ecot_sched/schedulers.py:277-299: admit
@@ -7,6 +7,15 @@
 // every occupied slot emits one token per tick; a slot freed at tick k is
 // reusable at k+1).  Token generation itself has no reference counterpart
 // (SPEC.md:166, :250): it is the decoder of DESIGN.md.
+//
+// Lanes.  The engine owns two lanes, each a CUDA stream with its own work
+// buffers, metadata ring, decode graphs and continuous batcher; weights, the
+// paged KV pool, sequences and the token arena are shared.  Lane 0 (highest
+// stream priority) serves prefills and everything synchronous; lane 1
+// (lowest priority) serves the background reasoning refresh of the two-stream
+// async scheduler (north_star item 4).  Lane 1 orders itself after lane 0's
+// prefills/forks with an event; freed KV pages are recycled only after both
+// lanes have passed the point of release.
 #include "common.cuh"
 #include "engine_internal.h"
 #include "gemm_tc.h"
@@ -40,7 +49,9 @@ constexpr int kRequestCap = 1024;   // tokens per request (out_tokens arena slot
 constexpr int kMetaRing = 4;
 constexpr int kItemRows = 16;       // query rows per cascade work item
 constexpr int kLogitRows = 256;
-constexpr int kMaxGraphRows = 64;    // decode ticks with <= this many rows replay CUDA graphs
+constexpr int kMaxGraphRows = 64;   // decode ticks with <= this many rows replay CUDA graphs
+constexpr int kLanes = 2;
+constexpr int kLane1Rows = 64;      // background lane: decode rows only
 
 struct MetaLayout {
   size_t o_rows, o_items, o_irows, o_heads, total;
@@ -61,7 +72,8 @@ struct Request {
   int priority = 1;
   uint64_t seqno = 0;
   int arena = -1;
-  int state = 0;      // 0 waiting, 1 running, 2 done, 3 released
+  int lane = 0;
+  int state = 0;      // 0 waiting, 1 running, 2 done
   bool capture = false;
   bool live = false;
 };
@@ -79,6 +91,40 @@ struct ProfRec {
   double bytes;
 };
 
+struct GraphSlot {
+  bool seen = false;
+  cudaGraphExec_t exec = nullptr;
+};
+
+struct PendingPage {
+  int page;
+  cudaEvent_t ev[kLanes];
+};
+
+// One stream with everything a forward pass needs.
+struct Lane {
+  int id = 0;
+  cudaStream_t stream = nullptr;
+  int max_rows = 0;
+  int max_partials = 0;
+  int max_items = 0;
+  fe::Workspace ws{};
+  int* attn_counters = nullptr;
+  float* sk_partial = nullptr;
+  int* sk_counters = nullptr;
+  MetaLayout layout{};
+  unsigned char* meta_host[kMetaRing] = {};
+  cudaEvent_t meta_ev[kMetaRing] = {};
+  int meta_next = 0;
+  fe::TmaMap map_xn{}, map_attn{}, map_act{};        // 128-row boxes (tile GEMM A operand)
+  fe::TmaMap map_xn16{}, map_attn16{}, map_act16{};  // 16-row boxes (skinny GEMM B operand)
+  std::unordered_map<long, GraphSlot> graphs;       // key: rows * 4096 + attention item bucket
+  // continuous batcher
+  int slots = 8;
+  std::vector<int> slot_req;
+  std::vector<int> waiting;
+};
+
 }  // namespace
 
 struct fe_engine {
@@ -86,10 +132,7 @@ struct fe_engine {
   int dtype = 0;
   int device = 0;
   size_t elem = 4;
-  int max_rows = 0;
   int max_slots = 0;
-  int slots = 8;
-  cudaStream_t stream = nullptr;
   std::mutex mu;
 
   // weights
@@ -98,44 +141,30 @@ struct fe_engine {
   std::vector<fe::Weights::Layer> layers;
   float* rope = nullptr;
 
-  // KV pool
+  // KV pool (shared by the lanes)
   void* kv_pool = nullptr;
   int n_pages = 0;
   size_t page_elems = 0;
   std::vector<int> page_ref;
   std::vector<int> free_pages;
+  std::vector<PendingPage> pending_pages;
+  std::vector<cudaEvent_t> free_events;
   std::vector<Seq> seqs;
   std::vector<int> free_seqs;
+  cudaEvent_t lane0_ev = nullptr;  // lane 0's latest prefill / fork, awaited by lane 1
 
-  // work buffers
-  fe::Workspace ws{};
-  int max_partials = 0;
-  int max_items = 0;
-  size_t meta_bytes = 0;
-  unsigned char* meta_host[kMetaRing] = {};
-  cudaEvent_t meta_ev[kMetaRing] = {};
-  int meta_next = 0;
-
-  // batcher
+  // requests and the token arena (shared)
   std::vector<Request> reqs;
   std::vector<int> free_reqs;
-  std::vector<int> slot_req;
-  std::vector<int> waiting;
   uint64_t seqno = 0;
   std::vector<int> free_arena;
+  int32_t* out_tokens = nullptr;
+  float* logits = nullptr;  // lane 0 capture buffer
   int capture_req = -1;
 
-  // metadata layout + decode graphs (one per row count)
-  MetaLayout meta_layout{};
-  bool graphs_on = true;
-  int debug_skip = 0;  // timing experiments only: 1 attention, 2 rmsnorm, 4 layer GEMMs, 8 lm_head
-  struct GraphSlot {
-    bool seen = false;
-    cudaGraphExec_t exec = nullptr;
-  };
-  std::unordered_map<long, GraphSlot> graphs;  // key: rows * 4096 + attention item bucket
+  Lane lanes[kLanes];
 
-  // tcgen05 GEMM path (bf16, wide forwards)
+  // tcgen05 path (bf16)
   struct LayerMaps {
     fe::TmaMap qkv, wo, wgu, wdown;
   };
@@ -143,18 +172,15 @@ struct fe_engine {
   int tc_min_rows = 17;
   int sk_mask = 31;  // skinny path per matrix: 1 QKV, 2 O, 4 gate/up, 8 down, 16 lm_head
   std::vector<LayerMaps> tc_maps;
-  fe::TmaMap map_xn{}, map_attn{}, map_act{};          // 128-row boxes (prefill GEMM A operand)
-  fe::TmaMap map_xn16{}, map_attn16{}, map_act16{};    // 16-row boxes (skinny GEMM B operand)
   fe::TmaMap map_lm{};
-  float* sk_partial = nullptr;
-  int* sk_counters = nullptr;
-  int* attn_counters = nullptr;
+  bool graphs_on = true;
+  int debug_skip = 0;  // timing experiments only: 1 attention, 2 rmsnorm, 4 layer GEMMs, 8 lm_head
 
   // stats
   int64_t n_ticks = 0, n_forwards = 0, n_rows_total = 0;
   int64_t h2d_bytes = 0, d2h_bytes = 0, n_launches = 0;
 
-  // profiling (fe_profile)
+  // profiling (fe_profile), lane 0 only
   bool prof_on = false;
   std::vector<ProfRec> prof_recs;
   int prof_used = 0;
@@ -176,7 +202,34 @@ const fe_engine::LayerMaps& EngineMapsDummy() {
   return d;
 }
 
+Lane& lane_at(fe_engine* e, int lane) {
+  if (lane < 0 || lane >= kLanes) throw Error("lane must be 0 or 1");
+  return e->lanes[lane];
+}
+
+// ---- KV pages ---------------------------------------------------------------
+void reclaim_pages(fe_engine* e) {
+  for (size_t i = 0; i < e->pending_pages.size();) {
+    PendingPage& pp = e->pending_pages[i];
+    bool done = true;
+    for (int l = 0; l < kLanes; l++) done = done && cudaEventQuery(pp.ev[l]) == cudaSuccess;
+    if (done) {
+      e->free_pages.push_back(pp.page);
+      for (int l = 0; l < kLanes; l++) e->free_events.push_back(pp.ev[l]);
+      pp = e->pending_pages.back();
+      e->pending_pages.pop_back();
+    } else {
+      i++;
+    }
+  }
+}
+
 int alloc_page(fe_engine* e) {
+  if (e->free_pages.empty()) reclaim_pages(e);
+  if (e->free_pages.empty() && !e->pending_pages.empty()) {
+    for (int l = 0; l < kLanes; l++) CK(cudaStreamSynchronize(e->lanes[l].stream));
+    reclaim_pages(e);
+  }
   if (e->free_pages.empty()) throw Error("KV pool exhausted (" + std::to_string(e->n_pages) + " pages)");
   int p = e->free_pages.back();
   e->free_pages.pop_back();
@@ -184,8 +237,28 @@ int alloc_page(fe_engine* e) {
   return p;
 }
 
+cudaEvent_t take_event(fe_engine* e) {
+  if (!e->free_events.empty()) {
+    cudaEvent_t ev = e->free_events.back();
+    e->free_events.pop_back();
+    return ev;
+  }
+  cudaEvent_t ev;
+  CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  return ev;
+}
+
+// A page whose last reference is dropped may still be read by kernels queued
+// on either lane: recycle it once both lanes pass this point.
 void release_page(fe_engine* e, int p) {
-  if (--e->page_ref[p] == 0) e->free_pages.push_back(p);
+  if (--e->page_ref[p] != 0) return;
+  PendingPage pp;
+  pp.page = p;
+  for (int l = 0; l < kLanes; l++) {
+    pp.ev[l] = take_event(e);
+    CK(cudaEventRecord(pp.ev[l], e->lanes[l].stream));
+  }
+  e->pending_pages.push_back(pp);
 }
 
 Seq& seq_at(fe_engine* e, int s) {
@@ -207,9 +280,10 @@ int new_seq(fe_engine* e) {
   return s;
 }
 
+// ---- profiling: CUDA events on lane 0 around launches ------------------------
 void flush_profile(fe_engine* e) {
   if (e->prof_used == 0) return;
-  CK(cudaStreamSynchronize(e->stream));
+  CK(cudaStreamSynchronize(e->lanes[0].stream));
   for (int i = 0; i < e->prof_used; i++) {
     const ProfRec& r = e->prof_recs[i];
     float ms = 0.f;
@@ -221,19 +295,8 @@ void flush_profile(fe_engine* e) {
   e->prof_used = 0;
 }
 
-// Pinned staging buffer for one forward's metadata; waits for the buffer's
-// previous H2D copy to finish before reuse.
-unsigned char* next_meta(fe_engine* e, int* idx) {
-  int i = e->meta_next;
-  e->meta_next = (i + 1) % kMetaRing;
-  CK(cudaEventSynchronize(e->meta_ev[i]));
-  *idx = i;
-  return e->meta_host[i];
-}
-
-// ---- profiling: CUDA events on the engine stream around launches ----------
-int prof_begin(fe_engine* e, int cat) {
-  if (!e->prof_on) return -1;
+int prof_begin(fe_engine* e, const Lane& ln, int cat) {
+  if (!e->prof_on || ln.id != 0) return -1;
   if (e->prof_used == (int)e->prof_recs.size()) {
     ProfRec r{};
     CK(cudaEventCreate(&r.a));
@@ -242,24 +305,44 @@ int prof_begin(fe_engine* e, int cat) {
   }
   const int i = e->prof_used++;
   e->prof_recs[i].cat = cat;
-  CK(cudaEventRecord(e->prof_recs[i].a, e->stream));
+  CK(cudaEventRecord(e->prof_recs[i].a, ln.stream));
   return i;
 }
 
-void prof_end(fe_engine* e, int i, double bytes) {
+void prof_end(fe_engine* e, const Lane& ln, int i, double bytes) {
   if (i < 0) return;
   e->prof_recs[i].bytes = bytes;
-  CK(cudaEventRecord(e->prof_recs[i].b, e->stream));
+  CK(cudaEventRecord(e->prof_recs[i].b, ln.stream));
 }
 
+// Pinned staging buffer for one forward's metadata; waits for the buffer's
+// previous H2D copy to finish before reuse.
+unsigned char* next_meta(Lane& ln, int* idx) {
+  int i = ln.meta_next;
+  ln.meta_next = (i + 1) % kMetaRing;
+  CK(cudaEventSynchronize(ln.meta_ev[i]));
+  *idx = i;
+  return ln.meta_host[i];
+}
+
+void clear_graphs(fe_engine* e) {
+  for (auto& ln : e->lanes) {
+    for (auto& g : ln.graphs)
+      if (g.second.exec) cudaGraphExecDestroy(g.second.exec);
+    ln.graphs.clear();
+  }
+}
+
+// ---- forward pass -----------------------------------------------------------
 // The kernel sequence of one forward pass (eager or under graph capture).
 template <typename GB>
-void launch_layers(fe_engine* e, const fe::Fwd& f, int n, bool decode, double kv_bytes, GB gemv_bytes) {
+void launch_layers(fe_engine* e, Lane& ln, const fe::Fwd& f, int n, bool decode, double kv_bytes, GB gemv_bytes) {
   const fe::ModelDims& m = e->m;
-  cudaStream_t st = e->stream;
+  cudaStream_t st = ln.stream;
   const int dt = e->dtype;
-  const int whole = prof_begin(e, decode ? PROF_DECODE_FWD : PROF_PREFILL_FWD);
-  fe::launch_embed(dt, f, m, e->w.embed, e->ws.out_tokens, e->ws.x, st);
+  fe::Workspace& ws = ln.ws;
+  const int whole = prof_begin(e, ln, decode ? PROF_DECODE_FWD : PROF_PREFILL_FWD);
+  fe::launch_embed(dt, f, m, e->w.embed, e->out_tokens, ws.x, st);
   // bf16: skinny tcgen05 swap-AB GEMM for <= 16 rows (decode), the tile
   // tcgen05 GEMM for wide forwards (prefill); fp32: canonical CUDA-core GEMV
   const bool sk_any = e->use_tc && n <= fe::skinny_max_rows();
@@ -268,92 +351,93 @@ void launch_layers(fe_engine* e, const fe::Fwd& f, int n, bool decode, double kv
   auto tc_launch = [&](int epi, int N, int K) {
     fe::TcLaunch t{};
     t.M = n; t.N = N; t.K = K; t.epi = epi;
-    t.y = e->ws.x; t.ldy = m.d;
-    t.act = (__nv_bfloat16*)e->ws.attn; t.F = m.F;
-    t.q = e->ws.q; t.kv_pool = (__nv_bfloat16*)e->kv_pool; t.page_elems = e->page_elems;
+    t.y = ws.x; t.ldy = m.d;
+    t.act = (__nv_bfloat16*)ws.attn; t.F = m.F;
+    t.q = ws.q; t.kv_pool = (__nv_bfloat16*)e->kv_pool; t.page_elems = e->page_elems;
     t.rope = e->rope; t.rows = f.rows; t.H = m.H; t.hd = m.hd; t.d = m.d;
     return t;
   };
   auto sk_launch = [&](int epi, int N, int K) {
     fe::SkLaunch t{};
     t.N = N; t.K = K; t.B = n; t.epi = epi;
-    t.partial = e->sk_partial; t.counters = e->sk_counters;
-    t.y = e->ws.x; t.ldy = m.d;
-    t.act = (__nv_bfloat16*)e->ws.attn; t.F = m.F;
-    t.q = e->ws.q; t.kv_pool = (__nv_bfloat16*)e->kv_pool; t.page_elems = e->page_elems;
+    t.partial = ln.sk_partial; t.counters = ln.sk_counters;
+    t.y = ws.x; t.ldy = m.d;
+    t.act = (__nv_bfloat16*)ws.attn; t.F = m.F;
+    t.q = ws.q; t.kv_pool = (__nv_bfloat16*)e->kv_pool; t.page_elems = e->page_elems;
     t.rope = e->rope; t.rows = f.rows; t.head_rows = f.head_rows; t.H = m.H; t.hd = m.hd; t.d = m.d;
-    t.part_keys = e->ws.part_keys; t.logits = e->ws.logits; t.V = m.V; t.n_text = m.n_text;
+    t.part_keys = ws.part_keys; t.logits = ws.logits; t.V = m.V; t.n_text = m.n_text;
     return t;
   };
   for (int l = 0; l < m.L; l++) {
     const fe::Weights::Layer& ly = e->layers[l];
     const auto& mp = e->tc_maps.empty() ? EngineMapsDummy() : e->tc_maps[l];
     const size_t layer_off = (size_t)l * 2 * m.H * FE_PAGE * m.hd;
-    int p;
     const bool skip_norm = e->debug_skip & 2, skip_gemm = e->debug_skip & 4;
-    if (!skip_norm) fe::launch_rmsnorm(dt, e->ws.x, ly.attn_norm, e->ws.xn, n, m.d, m.d, m.eps, nullptr, st);
-    p = decode ? prof_begin(e, PROF_GEMV) : -1;
+    int p;
+    if (!skip_norm) fe::launch_rmsnorm(dt, ws.x, ly.attn_norm, ws.xn, n, m.d, m.d, m.eps, nullptr, st);
+    p = decode ? prof_begin(e, ln, PROF_GEMV) : -1;
     if (skip_gemm) {
     } else if (sk_on(0)) {
       fe::SkLaunch t = sk_launch(fe::TC_QKV, 3 * m.d, m.d);
       t.layer_off = layer_off;
-      fe::launch_skinny_tc(mp.qkv, e->map_xn16, t, st);
+      fe::launch_skinny_tc(mp.qkv, ln.map_xn16, t, st);
     } else if (tc) {
       fe::TcLaunch t = tc_launch(fe::TC_QKV, 3 * m.d, m.d);
       t.layer_off = layer_off;
-      fe::launch_gemm_tc(e->map_xn, mp.qkv, t, st);
+      fe::launch_gemm_tc(ln.map_xn, mp.qkv, t, st);
     } else {
-      fe::launch_qkv(dt, f, m, ly.wqkv, e->ws.xn, e->ws.q, e->kv_pool, l, e->rope, st);
+      fe::launch_qkv(dt, f, m, ly.wqkv, ws.xn, ws.q, e->kv_pool, l, e->rope, st);
     }
-    prof_end(e, p, gemv_bytes(3.0 * m.d, m.d, n));
-    p = decode ? prof_begin(e, PROF_ATTN) : -1;
-    if (!(e->debug_skip & 1)) fe::launch_attention(dt, f, m, e->ws.q, e->kv_pool, l, e->ws.partial, e->ws.attn, st);
-    prof_end(e, p, kv_bytes);
-    p = decode ? prof_begin(e, PROF_GEMV) : -1;
+    prof_end(e, ln, p, gemv_bytes(3.0 * m.d, m.d, n));
+    p = decode ? prof_begin(e, ln, PROF_ATTN) : -1;
+    if (!(e->debug_skip & 1)) fe::launch_attention(dt, f, m, ws.q, e->kv_pool, l, ws.partial, ws.attn, st);
+    prof_end(e, ln, p, kv_bytes);
+    p = decode ? prof_begin(e, ln, PROF_GEMV) : -1;
     if (skip_gemm) {
-    } else if (sk_on(1)) fe::launch_skinny_tc(mp.wo, e->map_attn16, sk_launch(fe::TC_RESID, m.d, m.d), st);
-    else if (tc) fe::launch_gemm_tc(e->map_attn, mp.wo, tc_launch(fe::TC_RESID, m.d, m.d), st);
-    else fe::launch_resid(dt, f, m.d, m.d, ly.wo, e->ws.attn, e->ws.x, st);
-    prof_end(e, p, gemv_bytes(m.d, m.d, n));
-    if (!skip_norm) fe::launch_rmsnorm(dt, e->ws.x, ly.ffn_norm, e->ws.xn, n, m.d, m.d, m.eps, nullptr, st);
-    p = decode ? prof_begin(e, PROF_GEMV) : -1;
+    } else if (sk_on(1)) fe::launch_skinny_tc(mp.wo, ln.map_attn16, sk_launch(fe::TC_RESID, m.d, m.d), st);
+    else if (tc) fe::launch_gemm_tc(ln.map_attn, mp.wo, tc_launch(fe::TC_RESID, m.d, m.d), st);
+    else fe::launch_resid(dt, f, m.d, m.d, ly.wo, ws.attn, ws.x, st);
+    prof_end(e, ln, p, gemv_bytes(m.d, m.d, n));
+    if (!skip_norm) fe::launch_rmsnorm(dt, ws.x, ly.ffn_norm, ws.xn, n, m.d, m.d, m.eps, nullptr, st);
+    p = decode ? prof_begin(e, ln, PROF_GEMV) : -1;
     if (skip_gemm) {
-    } else if (sk_on(2)) fe::launch_skinny_tc(mp.wgu, e->map_xn16, sk_launch(fe::TC_SWIGLU, 2 * m.F, m.d), st);
-    else if (tc) fe::launch_gemm_tc(e->map_xn, mp.wgu, tc_launch(fe::TC_SWIGLU, 2 * m.F, m.d), st);
-    else fe::launch_swiglu(dt, f, m.F, m.d, ly.wgu, e->ws.xn, e->ws.attn /* reused as the SwiGLU activation */, st);
-    prof_end(e, p, gemv_bytes(2.0 * m.F, m.d, n));
-    p = decode ? prof_begin(e, PROF_GEMV) : -1;
+    } else if (sk_on(2)) fe::launch_skinny_tc(mp.wgu, ln.map_xn16, sk_launch(fe::TC_SWIGLU, 2 * m.F, m.d), st);
+    else if (tc) fe::launch_gemm_tc(ln.map_xn, mp.wgu, tc_launch(fe::TC_SWIGLU, 2 * m.F, m.d), st);
+    else fe::launch_swiglu(dt, f, m.F, m.d, ly.wgu, ws.xn, ws.attn /* reused as the SwiGLU activation */, st);
+    prof_end(e, ln, p, gemv_bytes(2.0 * m.F, m.d, n));
+    p = decode ? prof_begin(e, ln, PROF_GEMV) : -1;
     if (skip_gemm) {
-    } else if (sk_on(3)) fe::launch_skinny_tc(mp.wdown, e->map_act16, sk_launch(fe::TC_RESID, m.d, m.F), st);
-    else if (tc) fe::launch_gemm_tc(e->map_act, mp.wdown, tc_launch(fe::TC_RESID, m.d, m.F), st);
-    else fe::launch_resid(dt, f, m.d, m.F, ly.wdown, e->ws.attn, e->ws.x, st);
-    prof_end(e, p, gemv_bytes(m.d, m.F, n));
+    } else if (sk_on(3)) fe::launch_skinny_tc(mp.wdown, ln.map_act16, sk_launch(fe::TC_RESID, m.d, m.F), st);
+    else if (tc) fe::launch_gemm_tc(ln.map_act, mp.wdown, tc_launch(fe::TC_RESID, m.d, m.F), st);
+    else fe::launch_resid(dt, f, m.d, m.F, ly.wdown, ws.attn, ws.x, st);
+    prof_end(e, ln, p, gemv_bytes(m.d, m.F, n));
   }
   if (decode && !(e->debug_skip & 8)) {
-    fe::launch_rmsnorm(dt, e->ws.x, e->w.final_norm, e->ws.xn, f.n_head_rows, m.d, m.d, m.eps, f.head_rows, st);
-    const int p = prof_begin(e, PROF_GEMV);
+    fe::launch_rmsnorm(dt, ws.x, e->w.final_norm, ws.xn, f.n_head_rows, m.d, m.d, m.eps, f.head_rows, st);
+    const int p = prof_begin(e, ln, PROF_GEMV);
     if (e->use_tc && (e->sk_mask >> 4 & 1) && f.n_head_rows <= fe::skinny_max_rows()) {
       fe::SkLaunch t = sk_launch(fe::TC_ARGMAX, m.V, m.d);
       t.B = f.n_head_rows;
-      fe::launch_skinny_tc(e->map_lm, e->map_xn16, t, st);
-      fe::launch_finalize(f, e->ws.part_keys, fe::skinny_tiles(fe::TC_ARGMAX, m.V, m.F), e->ws.out_tokens, st);
+      fe::launch_skinny_tc(e->map_lm, ln.map_xn16, t, st);
+      fe::launch_finalize(f, ws.part_keys, fe::skinny_tiles(fe::TC_ARGMAX, m.V, m.F), e->out_tokens, st);
     } else {
-      fe::launch_lm_head(dt, f, m, e->w.lm_head, e->ws.xn, e->ws.part_keys, e->ws.logits, e->ws.out_tokens, st);
+      fe::launch_lm_head(dt, f, m, e->w.lm_head, ws.xn, ws.part_keys, ws.logits, e->out_tokens, st);
     }
-    prof_end(e, p, gemv_bytes(m.V, m.d, f.n_head_rows));
+    prof_end(e, ln, p, gemv_bytes(m.V, m.d, f.n_head_rows));
   }
-  prof_end(e, whole, 0.0);
+  prof_end(e, ln, whole, 0.0);
 }
 
-// One forward pass over `rows` (all positions must already be < seq.len+1 in
-// order).  Builds row metadata, the cascade work list and launches the layer
-// stack.  Host-side sequence lengths advance as rows are written.
-void forward(fe_engine* e, const std::vector<RowIn>& rows, uint64_t vision_seed) {
+// One forward pass over `rows` on a lane (positions must extend each
+// sequence contiguously, in order).  Builds row metadata and the cascade work
+// list, then launches the layer stack (or replays the lane's decode graph).
+void forward(fe_engine* e, Lane& ln, const std::vector<RowIn>& rows, uint64_t vision_seed) {
   const fe::ModelDims& m = e->m;
   const int n = (int)rows.size();
   if (n == 0) return;
-  if (n > e->max_rows) throw Error("forward: too many rows");
+  if (n > ln.max_rows) throw Error("forward: too many rows for lane " + std::to_string(ln.id));
   if (e->prof_on && e->prof_used > 8192) flush_profile(e);  // only between forwards: all records closed
+  if (ln.id != 0) CK(cudaStreamWaitEvent(ln.stream, e->lane0_ev, 0));  // trunks prefilled / forked on lane 0
 
   std::vector<fe::RowMeta> meta(n);
   std::vector<int32_t> head_rows;
@@ -379,13 +463,14 @@ void forward(fe_engine* e, const std::vector<RowIn>& rows, uint64_t vision_seed)
     mm.n_chunks = pg + 1;
     mm.logit_row = r.logit_row;
     mm.head_row = -1;
+    mm.pad = 0;
     chunk_total += pg + 1;
     if (r.head) {
       mm.head_row = (int)head_rows.size();
       head_rows.push_back(i);
     }
   }
-  if (chunk_total > e->max_partials) throw Error("forward: partial workspace too small");
+  if (chunk_total > ln.max_partials) throw Error("forward: partial workspace too small");
 
   // cascade work list: group rows by the physical page their chunk maps to.
   // Rows sharing a trunk point at the same pages, so each shared page is
@@ -420,16 +505,15 @@ void forward(fe_engine* e, const std::vector<RowIn>& rows, uint64_t vision_seed)
       items.push_back(it);
     }
   }
-  if ((int)items.size() > e->max_items) throw Error("forward: too many attention items");
 
-  // Metadata at fixed offsets of the device buffer (header, rows, items,
-  // item rows, head rows) so a captured decode graph can be replayed with new
-  // contents: counts that vary per tick (attention items) are read on device.
-  const MetaLayout& L = e->meta_layout;
+  // Metadata at fixed offsets of the lane's device buffer (header, rows,
+  // items, item rows, head rows) so a captured decode graph can be replayed
+  // with new contents: counts that vary per tick are read on device.
+  const MetaLayout& L = ln.layout;
   if (n > L.cap_rows || (int)items.size() > L.cap_items || (int)irows.size() > L.cap_irows)
     throw Error("forward: metadata capacity exceeded");
   int mi;
-  unsigned char* hbuf = next_meta(e, &mi);
+  unsigned char* hbuf = next_meta(ln, &mi);
   int32_t* hdr = reinterpret_cast<int32_t*>(hbuf);
   hdr[0] = n;
   hdr[1] = (int)items.size();
@@ -439,18 +523,18 @@ void forward(fe_engine* e, const std::vector<RowIn>& rows, uint64_t vision_seed)
   std::memcpy(hbuf + L.o_items, items.data(), sizeof(fe::AttnItem) * items.size());
   std::memcpy(hbuf + L.o_irows, irows.data(), sizeof(fe::ItemRow) * irows.size());
   std::memcpy(hbuf + L.o_heads, head_rows.data(), sizeof(int32_t) * head_rows.size());
-  unsigned char* dbuf = (unsigned char*)e->ws.meta;
+  unsigned char* dbuf = (unsigned char*)ln.ws.meta;
   size_t h2d = 0;
   auto copy = [&](size_t off, size_t bytes) {
     if (bytes == 0) return;
-    CK(cudaMemcpyAsync(dbuf + off, hbuf + off, bytes, cudaMemcpyHostToDevice, e->stream));
+    CK(cudaMemcpyAsync(dbuf + off, hbuf + off, bytes, cudaMemcpyHostToDevice, ln.stream));
     h2d += bytes;
   };
   copy(0, L.o_rows + sizeof(fe::RowMeta) * n);  // header + rows
   copy(L.o_items, sizeof(fe::AttnItem) * items.size());
   copy(L.o_irows, sizeof(fe::ItemRow) * irows.size());
   copy(L.o_heads, sizeof(int32_t) * head_rows.size());
-  CK(cudaEventRecord(e->meta_ev[mi], e->stream));
+  CK(cudaEventRecord(ln.meta_ev[mi], ln.stream));
   e->h2d_bytes += h2d;
 
   fe::Fwd f{};
@@ -467,40 +551,36 @@ void forward(fe_engine* e, const std::vector<RowIn>& rows, uint64_t vision_seed)
   f.item_rows = (const fe::ItemRow*)(dbuf + L.o_irows);
   f.n_head_rows = (int)head_rows.size();
   f.head_rows = (const int32_t*)(dbuf + L.o_heads);
-  f.attn_counters = e->attn_counters;
+  f.attn_counters = ln.attn_counters;
   f.vision_key = fe::tensor_key(vision_seed, 4 /* T_VISION */);
 
   const bool decode = f.n_head_rows > 0;
   const double el = (double)e->elem;
   // algorithmic bytes of one GEMV launch: weights + staged input + fp32 output
-  auto gemv_bytes = [&](double N, double K, int rows) { return N * K * el + rows * K * el + rows * N * 4.0; };
+  auto gemv_bytes = [&](double N, double K, int rws) { return N * K * el + rws * K * el + rws * N * 4.0; };
   double kv_bytes = 0;  // K+V bytes the cascade items stage (each shared page once per head)
-  for (const auto& it : items) {
-    int vmax = 0;
-    for (int j = 0; j < it.row_count; j++) vmax = std::max(vmax, irows[it.row_begin + j].valid);
-    kv_bytes += 2.0 * vmax * m.hd * m.H * el;
-  }
+  for (const auto& it : items) kv_bytes += 2.0 * it.valid_max * m.hd * m.H * el;
 
-  // decode ticks replay a CUDA graph per row count (captured on the second
-  // tick with that row count); prefill and profiled runs launch eagerly
-  const bool graphable = decode && e->graphs_on && !e->prof_on && n <= kMaxGraphRows;
+  // decode ticks replay a CUDA graph per (rows, item bucket), captured on the
+  // second tick with that key; prefill and profiled runs launch eagerly
+  const bool graphable = decode && e->graphs_on && !(e->prof_on && ln.id == 0) && n <= kMaxGraphRows;
   const long key = (long)n * 4096 + item_bucket;
-  if (graphable && e->graphs.count(key) && e->graphs[key].exec) {
-    CK(cudaGraphLaunch(e->graphs[key].exec, e->stream));
-  } else if (graphable && e->graphs.count(key) && e->graphs[key].seen) {
+  auto it_g = ln.graphs.find(key);
+  if (graphable && it_g != ln.graphs.end() && it_g->second.exec) {
+    CK(cudaGraphLaunch(it_g->second.exec, ln.stream));
+  } else if (graphable && it_g != ln.graphs.end() && it_g->second.seen) {
     cudaGraph_t g = nullptr;
-    CK(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
-    launch_layers(e, f, n, decode, kv_bytes, gemv_bytes);
-    CK(cudaStreamEndCapture(e->stream, &g));
-    CK(cudaGraphInstantiate(&e->graphs[key].exec, g, 0));
+    CK(cudaStreamBeginCapture(ln.stream, cudaStreamCaptureModeThreadLocal));
+    launch_layers(e, ln, f, n, decode, kv_bytes, gemv_bytes);
+    CK(cudaStreamEndCapture(ln.stream, &g));
+    CK(cudaGraphInstantiate(&it_g->second.exec, g, 0));
     CK(cudaGraphDestroy(g));
-    CK(cudaGraphLaunch(e->graphs[key].exec, e->stream));
+    CK(cudaGraphLaunch(it_g->second.exec, ln.stream));
   } else {
-    if (graphable) e->graphs[key].seen = true;
-    launch_layers(e, f, n, decode, kv_bytes, gemv_bytes);
+    if (graphable) ln.graphs[key].seen = true;
+    launch_layers(e, ln, f, n, decode, kv_bytes, gemv_bytes);
   }
   CK(cudaGetLastError());
-  // embed + per layer (2 norms, qkv, attention partial + merge, O, gate/up, down) + head
   const int attn_kernels = e->dtype == FE_BF16 ? 1 : 2;  // bf16: merge fused into the attention kernel
   e->n_launches += 1 + (6 + attn_kernels) * m.L + (decode ? 3 : 0) - (items.empty() ? m.L : 0);
   e->n_forwards++;
@@ -508,15 +588,16 @@ void forward(fe_engine* e, const std::vector<RowIn>& rows, uint64_t vision_seed)
 }
 
 void prefill(fe_engine* e, int seq, const int32_t* ids, int n, uint64_t vseed, int vis_id) {
+  Lane& ln = e->lanes[0];
   Seq& s = seq_at(e, seq);
   int pos = s.len;
   int i = 0;
   while (i < n) {
     std::vector<RowIn> rows;
     int chunks = 0;
-    while (i < n && (int)rows.size() < e->max_rows) {
+    while (i < n && (int)rows.size() < ln.max_rows) {
       const int c = pos / FE_PAGE + 1;
-      if (chunks + c > e->max_partials && !rows.empty()) break;
+      if (chunks + c > ln.max_partials && !rows.empty()) break;
       RowIn r{};
       r.seq = seq;
       r.pos = pos;
@@ -533,8 +614,9 @@ void prefill(fe_engine* e, int seq, const int32_t* ids, int n, uint64_t vseed, i
       pos++;
       i++;
     }
-    forward(e, rows, vseed);
+    forward(e, ln, rows, vseed);
   }
+  CK(cudaEventRecord(e->lane0_ev, ln.stream));
 }
 
 int new_request_slot(fe_engine* e) {
@@ -554,26 +636,33 @@ Request& req_at(fe_engine* e, int r) {
   return e->reqs[r];
 }
 
-// One decode iteration (= one tick of the reference _MicroEngine).
-int tick(fe_engine* e, std::vector<int>* completed) {
+bool lane_busy(const Lane& ln) {
+  if (!ln.waiting.empty()) return true;
+  for (int s = 0; s < ln.slots; s++)
+    if (ln.slot_req[s] >= 0) return true;
+  return false;
+}
+
+// One decode iteration of a lane (= one tick of the reference _MicroEngine).
+int tick(fe_engine* e, Lane& ln, std::vector<int>* completed) {
   // admission: action class first, then FIFO by seqno (schedulers.py:279-285)
-  if (!e->waiting.empty()) {
-    std::stable_sort(e->waiting.begin(), e->waiting.end(), [&](int a, int b) {
+  if (!ln.waiting.empty()) {
+    std::stable_sort(ln.waiting.begin(), ln.waiting.end(), [&](int a, int b) {
       const Request &ra = e->reqs[a], &rb = e->reqs[b];
       if (ra.priority != rb.priority) return ra.priority < rb.priority;
       return ra.seqno < rb.seqno;
     });
-    for (int s = 0; s < e->slots && !e->waiting.empty(); s++) {
-      if (e->slot_req[s] < 0) {
-        e->slot_req[s] = e->waiting.front();
-        e->reqs[e->waiting.front()].state = 1;
-        e->waiting.erase(e->waiting.begin());
+    for (int s = 0; s < ln.slots && !ln.waiting.empty(); s++) {
+      if (ln.slot_req[s] < 0) {
+        ln.slot_req[s] = ln.waiting.front();
+        e->reqs[ln.waiting.front()].state = 1;
+        ln.waiting.erase(ln.waiting.begin());
       }
     }
   }
   std::vector<RowIn> rows;
-  for (int s = 0; s < e->slots; s++) {
-    const int ri = e->slot_req[s];
+  for (int s = 0; s < ln.slots; s++) {
+    const int ri = ln.slot_req[s];
     if (ri < 0) continue;
     Request& q = e->reqs[ri];
     RowIn r{};
@@ -588,14 +677,14 @@ int tick(fe_engine* e, std::vector<int>* completed) {
     rows.push_back(r);
   }
   const int occupied = (int)rows.size();
-  forward(e, rows, 0);
-  for (int s = 0; s < e->slots; s++) {
-    const int ri = e->slot_req[s];
+  forward(e, ln, rows, 0);
+  for (int s = 0; s < ln.slots; s++) {
+    const int ri = ln.slot_req[s];
     if (ri < 0) continue;
     Request& q = e->reqs[ri];
     if (++q.produced == q.length) {
       q.state = 2;
-      e->slot_req[s] = -1;
+      ln.slot_req[s] = -1;
       completed->push_back(ri);
     }
   }
@@ -605,7 +694,7 @@ int tick(fe_engine* e, std::vector<int>* completed) {
 
 void init_weights(fe_engine* e, uint64_t seed) {
   const fe::ModelDims& m = e->m;
-  cudaStream_t st = e->stream;
+  cudaStream_t st = e->lanes[0].stream;
   const size_t d = m.d, F = m.F, V = m.V;
   auto key = [&](uint64_t tid) { return fe::tensor_key(seed, tid); };
   fe::launch_init_linear(e->dtype, e->w.embed, key(1), V * d, st);
@@ -630,6 +719,58 @@ void init_weights(fe_engine* e, uint64_t seed) {
   CK(cudaStreamSynchronize(st));
 }
 
+void create_lane(fe_engine* e, Lane& ln, int id, int rows, int priority) {
+  const fe::ModelDims& m = e->m;
+  const size_t d = m.d, F = m.F, V = m.V, el = e->elem, R = rows;
+  ln.id = id;
+  ln.max_rows = rows;
+  CK(cudaStreamCreateWithPriority(&ln.stream, cudaStreamNonBlocking, priority));
+  ln.ws.x = (float*)e->dalloc(R * d * 4);
+  ln.ws.xn = e->dalloc(R * std::max(d, F) * el);
+  ln.ws.q = (float*)e->dalloc(R * d * 4);
+  ln.ws.attn = e->dalloc(R * std::max(d, F) * el);
+  ln.max_partials = (int)std::min<size_t>(R * (size_t)(m.max_pos / FE_PAGE), 65536);
+  ln.max_items = ln.max_partials;
+  ln.ws.partial = (float*)e->dalloc((size_t)ln.max_partials * m.H * (m.hd + 2) * 4);
+  ln.ws.part_keys = (unsigned long long*)e->dalloc(R * (size_t)fe::lm_head_ctas(m) * 8);
+  ln.ws.logits = id == 0 ? e->logits : nullptr;
+  ln.attn_counters = (int*)e->dalloc(R * m.H * sizeof(int));
+  CK(cudaMemset(ln.attn_counters, 0, R * m.H * sizeof(int)));
+  {  // fixed-offset metadata layout (16-byte aligned sections)
+    MetaLayout& L = ln.layout;
+    auto up16 = [](size_t v) { return (v + 15) & ~(size_t)15; };
+    L.cap_rows = (int)R;
+    L.cap_items = ln.max_items;
+    L.cap_irows = ln.max_partials;
+    L.o_rows = 64;
+    L.o_items = up16(L.o_rows + R * sizeof(fe::RowMeta));
+    L.o_irows = up16(L.o_items + (size_t)L.cap_items * sizeof(fe::AttnItem));
+    L.o_heads = up16(L.o_irows + (size_t)L.cap_irows * sizeof(fe::ItemRow));
+    L.total = up16(L.o_heads + R * 4);
+  }
+  ln.ws.meta = e->dalloc(ln.layout.total);
+  for (int i = 0; i < kMetaRing; i++) {
+    CK(cudaMallocHost((void**)&ln.meta_host[i], ln.layout.total));
+    CK(cudaEventCreateWithFlags(&ln.meta_ev[i], cudaEventDisableTiming));
+    CK(cudaEventRecord(ln.meta_ev[i], ln.stream));
+  }
+  ln.slot_req.assign(e->max_slots, -1);
+  ln.slots = std::min(8, e->max_slots);
+  if (e->use_tc) {
+    ln.map_xn = fe::make_kmajor_map(ln.ws.xn, rows, m.d, m.d, 128);
+    ln.map_attn = fe::make_kmajor_map(ln.ws.attn, rows, m.d, m.d, 128);
+    ln.map_act = fe::make_kmajor_map(ln.ws.attn, rows, m.F, m.F, 128);
+    ln.map_xn16 = fe::make_kmajor_map(ln.ws.xn, rows, m.d, m.d, fe::skinny_max_rows());
+    ln.map_attn16 = fe::make_kmajor_map(ln.ws.attn, rows, m.d, m.d, fe::skinny_max_rows());
+    ln.map_act16 = fe::make_kmajor_map(ln.ws.attn, rows, m.F, m.F, fe::skinny_max_rows());
+    const size_t part_floats = (size_t)64 * std::max<size_t>(3 * m.d, 2 * (size_t)m.F) * fe::skinny_max_rows();
+    ln.sk_partial = (float*)e->dalloc(part_floats * 4);
+    ln.sk_counters = (int*)e->dalloc(4096 * sizeof(int));
+    CK(cudaMemset(ln.sk_counters, 0, 4096 * sizeof(int)));
+  }
+  (void)V;
+}
+
 fe_engine* create(const fe_config* c, int device, const float* rope_host) {
   if (c->head_dim != 64 && c->head_dim != 128) throw Error("head_dim must be 64 or 128");
   if (c->n_heads * c->head_dim != c->d_model) throw Error("n_heads * head_dim != d_model");
@@ -643,10 +784,8 @@ fe_engine* create(const fe_config* c, int device, const float* rope_host) {
             c->rms_eps, c->attn_scale};
     e->dtype = c->dtype;
     e->elem = c->dtype == FE_F32 ? 4 : 2;
-    e->max_rows = c->max_rows > 0 ? c->max_rows : 512;
+    const int max_rows = c->max_rows > 0 ? c->max_rows : 512;
     e->max_slots = c->max_slots > 0 ? c->max_slots : 64;
-    e->slots = std::min(8, e->max_slots);
-    CK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
     const fe::ModelDims& m = e->m;
     const size_t d = m.d, F = m.F, V = m.V, el = e->elem;
 
@@ -667,42 +806,34 @@ fe_engine* create(const fe_config* c, int device, const float* rope_host) {
     e->rope = (float*)e->dalloc(sizeof(float) * (size_t)m.max_pos * m.hd);
     CK(cudaMemcpy(e->rope, rope_host, sizeof(float) * (size_t)m.max_pos * m.hd, cudaMemcpyHostToDevice));
 
-    // work buffers
-    const size_t R = e->max_rows;
-    e->ws.x = (float*)e->dalloc(R * d * 4);
-    e->ws.xn = e->dalloc(R * std::max(d, F) * el);
-    e->ws.q = (float*)e->dalloc(R * d * 4);
-    e->ws.attn = e->dalloc(R * std::max(d, F) * el);
-    e->max_partials = (int)std::min<size_t>(R * (size_t)(m.max_pos / FE_PAGE), 65536);
-    e->max_items = e->max_partials;
-    e->ws.partial = (float*)e->dalloc((size_t)e->max_partials * m.H * (m.hd + 2) * 4);
-    e->ws.part_keys = (unsigned long long*)e->dalloc(R * (size_t)fe::lm_head_ctas(m) * 8);
-    e->ws.logits = (float*)e->dalloc((size_t)kLogitRows * V * 4);
-    e->attn_counters = (int*)e->dalloc(R * m.H * sizeof(int));
-    CK(cudaMemset(e->attn_counters, 0, R * m.H * sizeof(int)));
+    // shared token arena and logits capture
+    e->logits = (float*)e->dalloc((size_t)kLogitRows * V * 4);
     const int n_arena = std::max(4 * e->max_slots, 256);
-    e->ws.out_tokens = (int32_t*)e->dalloc((size_t)n_arena * kRequestCap * 4);
-    CK(cudaMemset(e->ws.out_tokens, 0, (size_t)n_arena * kRequestCap * 4));
+    e->out_tokens = (int32_t*)e->dalloc((size_t)n_arena * kRequestCap * 4);
+    CK(cudaMemset(e->out_tokens, 0, (size_t)n_arena * kRequestCap * 4));
     for (int i = n_arena - 1; i >= 0; i--) e->free_arena.push_back(i);
-    {  // fixed-offset metadata layout (16-byte aligned sections)
-      MetaLayout& L = e->meta_layout;
-      auto up16 = [](size_t v) { return (v + 15) & ~(size_t)15; };
-      L.cap_rows = (int)R;
-      L.cap_items = e->max_items;
-      L.cap_irows = e->max_partials;
-      L.o_rows = 64;
-      L.o_items = up16(L.o_rows + R * sizeof(fe::RowMeta));
-      L.o_irows = up16(L.o_items + (size_t)L.cap_items * sizeof(fe::AttnItem));
-      L.o_heads = up16(L.o_irows + (size_t)L.cap_irows * sizeof(fe::ItemRow));
-      L.total = up16(L.o_heads + R * 4);
-      e->meta_bytes = L.total;
+
+    // tcgen05 path: weight tensor maps (A operand of the skinny GEMM, B of the tile GEMM)
+    e->use_tc = e->dtype == FE_BF16 && m.hd == 128 && m.d % 128 == 0 && m.F % 64 == 0 && max_rows >= 64;
+    if (e->use_tc) {
+      e->map_lm = fe::make_kmajor_map(e->w.lm_head, m.V, m.d, m.d, 128);
+      e->tc_maps.resize(m.L);
+      for (int l = 0; l < m.L; l++) {
+        auto& ly = e->layers[l];
+        e->tc_maps[l].qkv = fe::make_kmajor_map(ly.wqkv, 3 * m.d, m.d, m.d, 128);
+        e->tc_maps[l].wo = fe::make_kmajor_map(ly.wo, m.d, m.d, m.d, 128);
+        e->tc_maps[l].wgu = fe::make_kmajor_map(ly.wgu, 2 * m.F, m.d, m.d, fe::tc_box_rows(fe::TC_SWIGLU));
+        e->tc_maps[l].wdown = fe::make_kmajor_map(ly.wdown, m.d, m.F, m.F, 128);
+      }
     }
-    e->ws.meta = e->dalloc(e->meta_bytes);
-    for (int i = 0; i < kMetaRing; i++) {
-      CK(cudaMallocHost((void**)&e->meta_host[i], e->meta_bytes));
-      CK(cudaEventCreateWithFlags(&e->meta_ev[i], cudaEventDisableTiming));
-      CK(cudaEventRecord(e->meta_ev[i], e->stream));
-    }
+
+    // lanes: 0 = foreground (highest priority), 1 = background reasoning
+    int prio_low = 0, prio_high = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&prio_low, &prio_high));
+    create_lane(e, e->lanes[0], 0, max_rows, prio_high);
+    create_lane(e, e->lanes[1], 1, std::min(max_rows, kLane1Rows), prio_low);
+    CK(cudaEventCreateWithFlags(&e->lane0_ev, cudaEventDisableTiming));
+    CK(cudaEventRecord(e->lane0_ev, e->lanes[0].stream));
 
     // KV pool: 64-token pages [L][2][H][64][hd]
     e->page_elems = fe::kv_page_elems(m);
@@ -718,33 +849,6 @@ fe_engine* create(const fe_config* c, int device, const float* rope_host) {
     e->kv_pool = e->dalloc(pages * e->page_elems * el);
     e->page_ref.assign(pages, 0);
     for (int p = (int)pages - 1; p >= 0; p--) e->free_pages.push_back(p);
-    e->slot_req.assign(e->max_slots, -1);
-
-    // tensor maps for the tcgen05 path: weights (B operand) and the staged
-    // activation buffers (A operand), all K-major bf16 with 128B swizzle
-    e->use_tc = e->dtype == FE_BF16 && m.hd == 128 && m.d % 128 == 0 && m.F % 64 == 0 && e->max_rows >= 64;
-    if (e->use_tc) {
-      const int R = e->max_rows;
-      e->map_xn = fe::make_kmajor_map(e->ws.xn, R, m.d, m.d, 128);
-      e->map_attn = fe::make_kmajor_map(e->ws.attn, R, m.d, m.d, 128);
-      e->map_act = fe::make_kmajor_map(e->ws.attn, R, m.F, m.F, 128);
-      e->map_xn16 = fe::make_kmajor_map(e->ws.xn, R, m.d, m.d, fe::skinny_max_rows());
-      e->map_attn16 = fe::make_kmajor_map(e->ws.attn, R, m.d, m.d, fe::skinny_max_rows());
-      e->map_act16 = fe::make_kmajor_map(e->ws.attn, R, m.F, m.F, fe::skinny_max_rows());
-      e->map_lm = fe::make_kmajor_map(e->w.lm_head, m.V, m.d, m.d, 128);
-      const size_t part_floats = (size_t)64 * std::max<size_t>(3 * m.d, 2 * (size_t)m.F) * fe::skinny_max_rows();
-      e->sk_partial = (float*)e->dalloc(part_floats * 4);
-      e->sk_counters = (int*)e->dalloc(4096 * sizeof(int));
-      CK(cudaMemset(e->sk_counters, 0, 4096 * sizeof(int)));
-      e->tc_maps.resize(m.L);
-      for (int l = 0; l < m.L; l++) {
-        auto& ly = e->layers[l];
-        e->tc_maps[l].qkv = fe::make_kmajor_map(ly.wqkv, 3 * m.d, m.d, m.d, 128);
-        e->tc_maps[l].wo = fe::make_kmajor_map(ly.wo, m.d, m.d, m.d, 128);
-        e->tc_maps[l].wgu = fe::make_kmajor_map(ly.wgu, 2 * m.F, m.d, m.d, fe::tc_box_rows(fe::TC_SWIGLU));
-        e->tc_maps[l].wdown = fe::make_kmajor_map(ly.wdown, m.d, m.F, m.F, 128);
-      }
-    }
   } catch (...) {
     for (void* p : e->allocs) cudaFree(p);
     delete e;
@@ -755,19 +859,25 @@ fe_engine* create(const fe_config* c, int device, const float* rope_host) {
 
 void destroy(fe_engine* e) {
   cudaSetDevice(e->device);
-  cudaStreamSynchronize(e->stream);
-  for (auto& g : e->graphs)
-    if (g.second.exec) cudaGraphExecDestroy(g.second.exec);
+  for (auto& ln : e->lanes)
+    if (ln.stream) cudaStreamSynchronize(ln.stream);
+  clear_graphs(e);
   for (void* p : e->allocs) cudaFree(p);
   for (auto& r : e->prof_recs) {
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);
   }
-  for (int i = 0; i < kMetaRing; i++) {
-    if (e->meta_host[i]) cudaFreeHost(e->meta_host[i]);
-    if (e->meta_ev[i]) cudaEventDestroy(e->meta_ev[i]);
+  for (auto& pp : e->pending_pages)
+    for (int l = 0; l < kLanes; l++) cudaEventDestroy(pp.ev[l]);
+  for (auto ev : e->free_events) cudaEventDestroy(ev);
+  for (auto& ln : e->lanes) {
+    for (int i = 0; i < kMetaRing; i++) {
+      if (ln.meta_host[i]) cudaFreeHost(ln.meta_host[i]);
+      if (ln.meta_ev[i]) cudaEventDestroy(ln.meta_ev[i]);
+    }
+    if (ln.stream) cudaStreamDestroy(ln.stream);
   }
-  cudaStreamDestroy(e->stream);
+  if (e->lane0_ev) cudaEventDestroy(e->lane0_ev);
   delete e;
 }
 
@@ -778,6 +888,70 @@ int guarded(fe_engine* e, Fn&& fn) {
     std::lock_guard<std::mutex> lk(e->mu);
     cudaSetDevice(e->device);
     fn();
+    return 0;
+  } catch (const std::exception& ex) {
+    g_last_error = ex.what();
+    return 1;
+  }
+}
+
+int submit(fe_engine* e, int lane, int32_t seq, int32_t first_id, int32_t length, int32_t priority) {
+  Lane& ln = lane_at(e, lane);
+  Seq& s = seq_at(e, seq);
+  if (length < 1 || length > kRequestCap) throw Error("request length outside [1, 1024]");
+  if (s.len + length > e->m.max_pos) throw Error("request would exceed max_pos");
+  if (first_id < 0 || first_id >= e->m.V) throw Error("first token id out of range");
+  if (e->free_arena.empty()) throw Error("too many live requests");
+  const int r = new_request_slot(e);
+  Request& q = e->reqs[r];
+  q = Request();
+  q.live = true;
+  q.seq = seq;
+  q.first_id = first_id;
+  q.length = length;
+  q.lane = lane;
+  q.priority = priority == FE_PRIO_ACTION ? 0 : 1;
+  q.seqno = e->seqno++;
+  q.arena = e->free_arena.back();
+  e->free_arena.pop_back();
+  ln.waiting.push_back(r);
+  return r;
+}
+
+// Tick a lane until `stop_req` completes (-1: until idle) or `max_ticks`
+// (<= 0: unbounded).  The engine lock is held per tick, so the two lanes can
+// be driven by two host threads concurrently.
+int run_lane(fe_engine* e, int lane, int32_t stop_req, int32_t max_ticks, int32_t cap, int32_t* n_ticks,
+             int32_t* occupancy, int32_t* completed, int32_t* completed_tick, int32_t* n_completed) {
+  try {
+    if (!e) throw Error("null engine");
+    int t = 0, nc = 0;
+    while (true) {
+      std::lock_guard<std::mutex> lk(e->mu);
+      cudaSetDevice(e->device);
+      Lane& ln = lane_at(e, lane);
+      if (stop_req >= 0) {
+        Request& q = req_at(e, stop_req);
+        if (q.lane != lane) throw Error("run: stop request belongs to the other lane");
+        if (q.state == 2) break;
+      } else if (!lane_busy(ln)) {
+        break;
+      }
+      if (max_ticks > 0 && t >= max_ticks) break;
+      if (!lane_busy(ln)) throw Error("run: stop request is not in flight");
+      if (t >= cap) throw Error("run: tick capacity exceeded");
+      std::vector<int> done;
+      occupancy[t] = tick(e, ln, &done);
+      for (int r : done) {
+        if (nc >= cap) throw Error("run: completion capacity exceeded");
+        completed[nc] = r;
+        completed_tick[nc] = t;
+        nc++;
+      }
+      t++;
+    }
+    *n_ticks = t;
+    *n_completed = nc;
     return 0;
   } catch (const std::exception& ex) {
     g_last_error = ex.what();
@@ -828,11 +1002,12 @@ int fe_seq_fork(fe_engine* e, int32_t parent, int32_t len, int32_t* child) {
       s.pages.push_back(ppages[i]);
       e->page_ref[ppages[i]]++;
     }
-    if (rem) {  // copy-on-write of the partially filled page
+    if (rem) {  // copy-on-write of the partially filled page (lane 0)
       const int np = alloc_page(e);
-      fe::launch_page_copy(e->dtype, e->kv_pool, ppages[full], np, rem, e->m, e->stream);
-      e->n_launches++;
+      fe::launch_page_copy(e->dtype, e->kv_pool, ppages[full], np, rem, e->m, e->lanes[0].stream);
+      CK(cudaEventRecord(e->lane0_ev, e->lanes[0].stream));
       s.pages.push_back(np);
+      e->n_launches++;
     }
     s.len = len;
     *child = c;
@@ -856,78 +1031,65 @@ int fe_prefill(fe_engine* e, int32_t seq, const int32_t* ids, int32_t n, uint64_
   return guarded(e, [&] { prefill(e, seq, ids, n, vision_seed, vis_id); });
 }
 
-int fe_set_slots(fe_engine* e, int32_t slots) {
+int fe_set_slots(fe_engine* e, int32_t slots) { return fe_set_slots_lane(e, 0, slots); }
+
+int fe_set_slots_lane(fe_engine* e, int32_t lane, int32_t slots) {
   return guarded(e, [&] {
-    if (slots < 1 || slots > e->max_slots) throw Error("slots outside [1, max_slots]");
-    for (int s = slots; s < e->slots; s++)
-      if (e->slot_req[s] >= 0) throw Error("cannot shrink slots while they are occupied");
-    e->slots = slots;
+    Lane& ln = lane_at(e, lane);
+    if (slots < 1 || slots > e->max_slots || slots > ln.max_rows) throw Error("slots outside [1, lane capacity]");
+    for (int s = slots; s < ln.slots; s++)
+      if (ln.slot_req[s] >= 0) throw Error("cannot shrink slots while they are occupied");
+    ln.slots = slots;
   });
 }
 
 int fe_submit(fe_engine* e, int32_t seq, int32_t first_id, int32_t length, int32_t priority, int32_t* req) {
-  return guarded(e, [&] {
-    Seq& s = seq_at(e, seq);
-    if (length < 1 || length > kRequestCap) throw Error("request length outside [1, 1024]");
-    if (s.len + length > e->m.max_pos) throw Error("request would exceed max_pos");
-    if (first_id < 0 || first_id >= e->m.V) throw Error("first token id out of range");
-    if (e->free_arena.empty()) throw Error("too many live requests");
-    const int r = new_request_slot(e);
-    Request& q = e->reqs[r];
-    q = Request();
-    q.live = true;
-    q.seq = seq;
-    q.first_id = first_id;
-    q.length = length;
-    q.priority = priority == FE_PRIO_ACTION ? 0 : 1;
-    q.seqno = e->seqno++;
-    q.arena = e->free_arena.back();
-    e->free_arena.pop_back();
-    e->waiting.push_back(r);
-    *req = r;
-  });
+  return guarded(e, [&] { *req = submit(e, 0, seq, first_id, length, priority); });
 }
 
-int fe_run(fe_engine* e, int32_t stop_req, int32_t cap, int32_t* n_ticks, int32_t* occupancy,
-           int32_t* completed, int32_t* completed_tick, int32_t* n_completed) {
-  return guarded(e, [&] {
-    int t = 0, nc = 0;
-    auto busy = [&] {
-      if (!e->waiting.empty()) return true;
-      for (int s = 0; s < e->slots; s++)
-        if (e->slot_req[s] >= 0) return true;
-      return false;
-    };
-    if (stop_req >= 0) req_at(e, stop_req);
-    while (true) {
-      if (stop_req >= 0 ? e->reqs[stop_req].state == 2 : !busy()) break;
-      if (!busy()) throw Error("run: stop request is not in flight");
-      if (t >= cap) throw Error("run: tick capacity exceeded");
-      std::vector<int> done;
-      occupancy[t] = tick(e, &done);
-      for (int r : done) {
-        if (nc >= cap) throw Error("run: completion capacity exceeded");
-        completed[nc] = r;
-        completed_tick[nc] = t;
-        nc++;
-      }
-      t++;
-    }
-    *n_ticks = t;
-    *n_completed = nc;
-  });
+int fe_submit_lane(fe_engine* e, int32_t lane, int32_t seq, int32_t first_id, int32_t length, int32_t priority,
+                   int32_t* req) {
+  return guarded(e, [&] { *req = submit(e, lane, seq, first_id, length, priority); });
+}
+
+int fe_run(fe_engine* e, int32_t stop_req, int32_t cap, int32_t* n_ticks, int32_t* occupancy, int32_t* completed,
+           int32_t* completed_tick, int32_t* n_completed) {
+  return run_lane(e, 0, stop_req, 0, cap, n_ticks, occupancy, completed, completed_tick, n_completed);
+}
+
+int fe_run_lane(fe_engine* e, int32_t lane, int32_t stop_req, int32_t max_ticks, int32_t cap, int32_t* n_ticks,
+                int32_t* occupancy, int32_t* completed, int32_t* completed_tick, int32_t* n_completed) {
+  return run_lane(e, lane, stop_req, max_ticks, cap, n_ticks, occupancy, completed, completed_tick, n_completed);
 }
 
 int fe_request_tokens(fe_engine* e, int32_t req, int32_t* out, int32_t cap) {
-  return guarded(e, [&] {
+  // enqueue the completion marker under the lock, wait and copy outside it so
+  // the other lane's driver is not blocked behind this synchronisation
+  cudaEvent_t ev = nullptr;
+  const int32_t* src = nullptr;
+  int length = 0;
+  int rc = guarded(e, [&] {
     Request& q = req_at(e, req);
     if (q.state != 2) throw Error("request not complete");
     if (cap < q.length) throw Error("output buffer too small");
-    CK(cudaMemcpyAsync(out, e->ws.out_tokens + (size_t)q.arena * kRequestCap, sizeof(int32_t) * q.length,
-                       cudaMemcpyDeviceToHost, e->stream));
+    ev = take_event(e);
+    CK(cudaEventRecord(ev, e->lanes[q.lane].stream));
+    src = e->out_tokens + (size_t)q.arena * kRequestCap;
+    length = q.length;
     e->d2h_bytes += (int64_t)sizeof(int32_t) * q.length;
-    CK(cudaStreamSynchronize(e->stream));
   });
+  if (rc) return rc;
+  try {
+    cudaSetDevice(e->device);
+    CK(cudaEventSynchronize(ev));
+    CK(cudaMemcpy(out, src, sizeof(int32_t) * length, cudaMemcpyDeviceToHost));
+  } catch (const std::exception& ex) {
+    g_last_error = ex.what();
+    rc = 1;
+  }
+  std::lock_guard<std::mutex> lk(e->mu);
+  e->free_events.push_back(ev);
+  return rc;
 }
 
 int fe_request_release(fe_engine* e, int32_t req) {
@@ -944,6 +1106,7 @@ int fe_request_release(fe_engine* e, int32_t req) {
 int fe_request_capture_logits(fe_engine* e, int32_t req) {
   return guarded(e, [&] {
     Request& q = req_at(e, req);
+    if (q.lane != 0) throw Error("logit capture is a lane-0 feature");
     if (e->capture_req >= 0 && e->capture_req != req) throw Error("another request is capturing logits");
     q.capture = true;
     e->capture_req = req;
@@ -955,26 +1118,34 @@ int fe_request_logits(fe_engine* e, int32_t req, float* out, int32_t rows) {
     Request& q = req_at(e, req);
     if (!q.capture) throw Error("request did not capture logits");
     if (rows > std::min(q.produced, kLogitRows)) throw Error("more logit rows than captured");
-    CK(cudaMemcpyAsync(out, e->ws.logits, sizeof(float) * (size_t)rows * e->m.V, cudaMemcpyDeviceToHost,
-                       e->stream));
-    CK(cudaStreamSynchronize(e->stream));
+    CK(cudaStreamSynchronize(e->lanes[0].stream));
+    CK(cudaMemcpy(out, e->logits, sizeof(float) * (size_t)rows * e->m.V, cudaMemcpyDeviceToHost));
   });
 }
 
 int fe_in_flight(fe_engine* e, int32_t* n) {
   return guarded(e, [&] {
-    int c = (int)e->waiting.size();
-    for (int s = 0; s < e->slots; s++) c += e->slot_req[s] >= 0;
+    int c = 0;
+    for (auto& ln : e->lanes) {
+      c += (int)ln.waiting.size();
+      for (int s = 0; s < ln.slots; s++) c += ln.slot_req[s] >= 0;
+    }
     *n = c;
   });
 }
 
 int fe_synchronize(fe_engine* e) {
-  return guarded(e, [&] { CK(cudaStreamSynchronize(e->stream)); });
+  return guarded(e, [&] {
+    for (auto& ln : e->lanes) CK(cudaStreamSynchronize(ln.stream));
+  });
 }
 
 int fe_stream(fe_engine* e, void** stream) {
-  return guarded(e, [&] { *stream = (void*)e->stream; });
+  return guarded(e, [&] { *stream = (void*)e->lanes[0].stream; });
+}
+
+int fe_stream_lane(fe_engine* e, int32_t lane, void** stream) {
+  return guarded(e, [&] { *stream = (void*)lane_at(e, lane).stream; });
 }
 
 int fe_profile(fe_engine* e, int32_t enable) {
@@ -1002,8 +1173,8 @@ int fe_profile_read(fe_engine* e, double* out, int32_t n) {
 
 int fe_stats(fe_engine* e, int64_t* out, int32_t n) {
   return guarded(e, [&] {
-    const int64_t v[] = {e->n_ticks, e->n_forwards, e->n_rows_total,
-                         (int64_t)(e->n_pages - (int)e->free_pages.size()), (int64_t)e->n_pages,
+    const int64_t used = e->n_pages - (int)e->free_pages.size() - (int)e->pending_pages.size();
+    const int64_t v[] = {e->n_ticks, e->n_forwards, e->n_rows_total, used, (int64_t)e->n_pages,
                          (int64_t)(e->page_elems * e->elem), e->h2d_bytes, e->d2h_bytes, e->n_launches};
     for (int i = 0; i < n && i < (int)(sizeof(v) / sizeof(v[0])); i++) out[i] = v[i];
   });
@@ -1034,15 +1205,15 @@ int fe_weight_ptr(fe_engine* e, int32_t tensor, int32_t layer, void** ptr, size_
 
 int fe_memcpy(fe_engine* e, void* dst, const void* src, size_t bytes) {
   return guarded(e, [&] {
-    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, e->stream));
-    CK(cudaStreamSynchronize(e->stream));
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, e->lanes[0].stream));
+    CK(cudaStreamSynchronize(e->lanes[0].stream));
   });
 }
 
 int fe_op_gemv(fe_engine* e, const void* w, int32_t N, int32_t K, const void* x, int32_t rows, float* y) {
   return guarded(e, [&] {
     if (N % 4 || K % 8) throw Error("gemv: N % 4 and K % 8 must be 0");
-    fe::launch_gemv_store(e->dtype, w, N, K, x, rows, y, e->stream);
+    fe::launch_gemv_store(e->dtype, w, N, K, x, rows, y, e->lanes[0].stream);
     CK(cudaGetLastError());
   });
 }
@@ -1054,7 +1225,7 @@ int fe_op_gemm_tc(fe_engine* e, const void* x, const void* w, int32_t M, int32_t
     const fe::TmaMap bm = fe::make_kmajor_map(w, N, K, K, 128);
     fe::TcLaunch t{};
     t.M = M; t.N = N; t.K = K; t.epi = fe::TC_STORE; t.y = y; t.ldy = N;
-    fe::launch_gemm_tc(am, bm, t, e->stream);
+    fe::launch_gemm_tc(am, bm, t, e->lanes[0].stream);
     CK(cudaGetLastError());
   });
 }
@@ -1062,17 +1233,18 @@ int fe_op_gemm_tc(fe_engine* e, const void* x, const void* w, int32_t M, int32_t
 int fe_op_skinny_tc(fe_engine* e, const void* x, const void* w, int32_t M, int32_t N, int32_t K, float* y) {
   return guarded(e, [&] {
     if (M > fe::skinny_max_rows() || N % 128 || K % 64) throw Error("skinny_tc: M <= 16, N % 128, K % 64");
-    if (!e->sk_partial) {
-      e->sk_partial = (float*)e->dalloc((size_t)64 * N * 16 * 4);
-      e->sk_counters = (int*)e->dalloc(4096 * sizeof(int));
-      CK(cudaMemset(e->sk_counters, 0, 4096 * sizeof(int)));
+    Lane& ln = e->lanes[0];
+    if (!ln.sk_partial) {
+      ln.sk_partial = (float*)e->dalloc((size_t)64 * N * 16 * 4);
+      ln.sk_counters = (int*)e->dalloc(4096 * sizeof(int));
+      CK(cudaMemset(ln.sk_counters, 0, 4096 * sizeof(int)));
     }
     const fe::TmaMap xm = fe::make_kmajor_map(x, M, K, K, fe::skinny_max_rows());
     const fe::TmaMap wm = fe::make_kmajor_map(w, N, K, K, 128);
     fe::SkLaunch t{};
     t.N = N; t.K = K; t.B = M; t.epi = fe::TC_STORE; t.y = y; t.ldy = N;
-    t.partial = e->sk_partial; t.counters = e->sk_counters;
-    fe::launch_skinny_tc(wm, xm, t, e->stream);
+    t.partial = ln.sk_partial; t.counters = ln.sk_counters;
+    fe::launch_skinny_tc(wm, xm, t, ln.stream);
     CK(cudaGetLastError());
   });
 }
@@ -1084,26 +1256,22 @@ int fe_set_option(fe_engine* e, const char* key, int64_t value) {
     else if (k == "use_tc") e->use_tc = value != 0 && !e->tc_maps.empty();
     else if (k == "sk_mask") e->sk_mask = (int)value;
     else if (k == "graphs") e->graphs_on = value != 0;
-    else if (k == "debug_skip") {
-      e->debug_skip = (int)value;
-      for (auto& g : e->graphs)
-        if (g.second.exec) cudaGraphExecDestroy(g.second.exec);
-      e->graphs.clear();
-    }
     else if (k == "pdl") fe::g_pdl = value != 0;
     else if (k == "sk_stages") {
       fe::g_sk_stages = (int)value;
-      for (auto& g : e->graphs)
-        if (g.second.exec) cudaGraphExecDestroy(g.second.exec);
-      e->graphs.clear();
+      clear_graphs(e);
+    } else if (k == "debug_skip") {
+      e->debug_skip = (int)value;
+      clear_graphs(e);
+    } else {
+      throw Error("unknown option " + k);
     }
-    else throw Error("unknown option " + k);
   });
 }
 
 int fe_op_rmsnorm(fe_engine* e, const float* x, const float* w, void* out, int32_t rows, int32_t d) {
   return guarded(e, [&] {
-    fe::launch_rmsnorm(e->dtype, x, w, out, rows, d, d, e->m.eps, nullptr, e->stream);
+    fe::launch_rmsnorm(e->dtype, x, w, out, rows, d, d, e->m.eps, nullptr, e->lanes[0].stream);
     CK(cudaGetLastError());
   });
 }

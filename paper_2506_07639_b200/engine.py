@@ -37,6 +37,7 @@ class FeConfig(ctypes.Structure):
 EXPORTS = (
     "fe_engine_create", "fe_engine_destroy", "fe_weights_init_random", "fe_last_error",
     "fe_seq_create", "fe_seq_fork", "fe_seq_free", "fe_seq_len", "fe_prefill", "fe_set_slots",
+    "fe_set_slots_lane", "fe_submit_lane", "fe_run_lane", "fe_stream_lane",
     "fe_submit", "fe_run", "fe_request_tokens", "fe_request_release", "fe_request_capture_logits",
     "fe_request_logits", "fe_in_flight", "fe_synchronize", "fe_stream", "fe_stats", "fe_profile",
     "fe_profile_read",
@@ -66,6 +67,10 @@ def load_library(path: Path = LIB_PATH) -> ctypes.CDLL:
         "fe_seq_len": [vp, i32, _c_int_p],
         "fe_prefill": [vp, i32, vp, i32, u64, i32],
         "fe_set_slots": [vp, i32],
+        "fe_set_slots_lane": [vp, i32, i32],
+        "fe_submit_lane": [vp, i32, i32, i32, i32, i32, _c_int_p],
+        "fe_run_lane": [vp, i32, i32, i32, i32, _c_int_p, vp, vp, vp, _c_int_p],
+        "fe_stream_lane": [vp, i32, ctypes.POINTER(vp)],
         "fe_submit": [vp, i32, i32, i32, i32, _c_int_p],
         "fe_run": [vp, i32, i32, _c_int_p, vp, vp, vp, _c_int_p],
         "fe_request_tokens": [vp, i32, vp, i32],
@@ -175,15 +180,38 @@ class Engine:
         self._check(self.lib.fe_submit(self._h, seq, first_id, length, priority, ctypes.byref(r)))
         return r.value
 
-    def run(self, stop_req: int = -1) -> tuple[list[int], list[tuple[int, int]]]:
-        """Decode until `stop_req` completes (-1: until idle).
+    def run(self, stop_req: int = -1, lane: int = 0, max_ticks: int = 0) -> tuple[list[int], list[tuple[int, int]]]:
+        """Decode on a lane until `stop_req` completes (-1: until idle) or
+        `max_ticks` ticks (0: unbounded).
         Returns (occupancy per tick, [(request, tick)] in completion order)."""
         nt, nc = ctypes.c_int32(), ctypes.c_int32()
-        self._check(self.lib.fe_run(self._h, stop_req, self._cap, ctypes.byref(nt), _np_ptr(self._occ),
-                                    _np_ptr(self._done), _np_ptr(self._done_tick), ctypes.byref(nc)))
-        occ = self._occ[: nt.value].tolist()
-        done = list(zip(self._done[: nc.value].tolist(), self._done_tick[: nc.value].tolist()))
+        occ_buf, done_buf, tick_buf = self._run_bufs(lane)
+        self._check(self.lib.fe_run_lane(self._h, lane, stop_req, max_ticks, self._cap, ctypes.byref(nt),
+                                         _np_ptr(occ_buf), _np_ptr(done_buf), _np_ptr(tick_buf), ctypes.byref(nc)))
+        occ = occ_buf[: nt.value].tolist()
+        done = list(zip(done_buf[: nc.value].tolist(), tick_buf[: nc.value].tolist()))
         return occ, done
+
+    def _run_bufs(self, lane: int):
+        # per-lane output arrays: the two lanes may be driven from two threads
+        if lane == 0:
+            return self._occ, self._done, self._done_tick
+        if not hasattr(self, "_bufs1"):
+            self._bufs1 = tuple(np.zeros(self._cap, dtype=np.int32) for _ in range(3))
+        return self._bufs1
+
+    def submit_lane(self, lane: int, seq: int, first_id: int, length: int, priority: int) -> int:
+        r = ctypes.c_int32()
+        self._check(self.lib.fe_submit_lane(self._h, lane, seq, first_id, length, priority, ctypes.byref(r)))
+        return r.value
+
+    def set_slots_lane(self, lane: int, slots: int) -> None:
+        self._check(self.lib.fe_set_slots_lane(self._h, lane, slots))
+
+    def stream_handle_lane(self, lane: int) -> int:
+        p = ctypes.c_void_p()
+        self._check(self.lib.fe_stream_lane(self._h, lane, ctypes.byref(p)))
+        return p.value or 0
 
     def request_tokens(self, req: int, length: int) -> list[int]:
         out = np.zeros(max(length, 1), dtype=np.int32)

@@ -27,6 +27,7 @@ so the runners' `reuse_stale` / `abort_episode` policies apply unchanged
 
 from __future__ import annotations
 
+import threading
 from dataclasses import dataclass, field
 from typing import Callable, Optional, Sequence
 
@@ -60,6 +61,7 @@ class EngineRequest:
     branch: int
     priority: int
     issue_timestep: int = 0
+    lane: int = 0
     req: int = -1
     tokens: TokenSeq = ()
     on_complete: Optional[Callable[["EngineRequest", int], None]] = None
@@ -72,14 +74,24 @@ class EngineBackend:
 
     def __init__(self, config="tiny", dtype: str = "f32", seed: int = 0,
                  profile: SyntheticProfile | None = None, device: int = 0,
-                 engine: Engine | None = None, trunk_cache: int = 64, **engine_kw):
+                 engine: Engine | None = None, trunk_cache: int = 64, async_streams: int = 1,
+                 request_log: list | None = None, **engine_kw):
+        """`async_streams=1`: lockstep async batcher (reference landing order,
+        byte-comparable traces); `2`: two-stream async scheduler (action on the
+        high-priority lane, reasoning refresh running on the low-priority lane in
+        the background, across control steps).  `request_log`: if a list,
+        every completed request appends (context, prefix, step name,
+        prev_content, tokens) -- used by per-request parity checks."""
         self.cfg = get_config(config)
+        self.async_streams = async_streams
+        self.request_log = request_log
         self.engine = engine or Engine(self.cfg, dtype=dtype, device=device, seed=seed, **engine_kw)
         self.profile = profile or default_profile(seed)
         self._trunks: list[_Trunk] = []
         self._trunk_cap = trunk_cache
         self._clock = 0
         self._owners: dict[int, EngineRequest] = {}
+        self._async_engines: list = []
         self._slots = 8
         self.requests = 0
 
@@ -143,7 +155,9 @@ class EngineBackend:
             outcomes[key[0]][key[1]] = StepGenerator(h.tokens, truncated=h.truncated)
         return outcomes
 
-    def make_async_engine(self, slots: int) -> "AsyncEngine":
+    def make_async_engine(self, slots: int):
+        if self.async_streams == 2:
+            return TwoStreamAsyncEngine(self, slots)
         return AsyncEngine(self, slots)
 
     def _ensure_slots(self, n: int) -> None:
@@ -190,8 +204,11 @@ class EngineBackend:
         vseed = vision_seed(ctx.observation)
         trunk, _ = self._branch_point(vseed, ids)
         branch = self.engine.seq_fork(trunk, ids.size)
-        return EngineRequest(spec.name, spec, plan.length, plan.truncated, step_tag(spec), branch,
-                             priority, issue_timestep=timestep)
+        h = EngineRequest(spec.name, spec, plan.length, plan.truncated, step_tag(spec), branch,
+                          priority, issue_timestep=timestep)
+        if self.request_log is not None:
+            h.log = (ctx, tuple(prefix), spec.name, tuple(prev))
+        return h
 
     def _submit(self, h: EngineRequest, on_complete) -> None:
         h.on_complete = on_complete
@@ -205,13 +222,20 @@ class EngineBackend:
             h = self._owners.pop(req)
             h.tokens = tuple(self.engine.request_tokens(req, h.length))
             h.done = True
+            self._log(h)
             self.engine.request_release(req)
             self.engine.seq_free(h.branch)
             if h.on_complete is not None:
                 h.on_complete(h, timestep)
         return occupancy
 
+    def _log(self, h: EngineRequest) -> None:
+        if self.request_log is not None and getattr(h, "log", None) is not None:
+            self.request_log.append(h.log + (h.tokens,))
+
     def close(self) -> None:
+        for eng in list(self._async_engines):
+            eng.close()
         self.engine.close()
 
 
@@ -247,3 +271,119 @@ class AsyncEngine:
 
     def run_until_complete(self, h: EngineRequest, timestep: int) -> list[int]:
         return self.backend._run(h.req, timestep)
+
+
+class TwoStreamAsyncEngine:
+    """Fast ECoT async as two CUDA streams (north_star item 4).
+
+    The action request of each control step decodes on lane 0 (highest stream
+    priority) against the last committed reasoning; reasoning-refresh requests
+    decode on lane 1 (lowest priority), driven by a background host thread
+    that keeps ticking across control steps.  A request's content is fixed at
+    issue (the snapshot it was prepared against, as in the reference,
+    `schedulers.py:471-492`); it lands into the cache at the control timestep
+    current when it completes.  Landing order is real-time, so traces are
+    checked per request (identical (context, prefix, step) -> identical tokens)
+    rather than byte-for-byte against the simulated clock."""
+
+    def __init__(self, backend: EngineBackend, slots: int):
+        self.backend = backend
+        eng = backend.engine
+        eng.set_slots(slots)
+        eng.set_slots_lane(1, slots)
+        backend._slots = slots
+        self._lock = threading.Lock()
+        self._inflight: dict[int, EngineRequest] = {}
+        self._now = 0
+        self._errors: list[BaseException] = []
+        self._stop = threading.Event()
+        self._work = threading.Event()
+        self._thread = threading.Thread(target=self._loop, name="fastecot-reasoning-lane", daemon=True)
+        self._thread.start()
+        backend._async_engines.append(self)
+
+    # -- runner surface (same as AsyncEngine / the reference _MicroEngine) ----
+    def prepare(self, ctx, prefix, spec, prev_content, priority: str, timestep: int) -> EngineRequest:
+        prio = PRIO_ACTION if priority == ACTION else PRIO_REASONING
+        with self._lock:  # trunk cache / prefill / fork all happen on lane 0
+            h = self.backend._prepare(ctx, prefix, spec, prev_content, prio, timestep)
+        h.lane = 0 if prio == PRIO_ACTION else 1
+        return h
+
+    def submit(self, h: EngineRequest, on_complete) -> None:
+        h.on_complete = on_complete
+        if h.lane == 0:
+            h.req = self.backend.engine.submit_lane(0, h.branch, h.tag, h.length, h.priority)
+            return
+        with self._lock:
+            h.req = self.backend.engine.submit_lane(1, h.branch, h.tag, h.length, h.priority)
+            self._inflight[h.req] = h
+        self._work.set()
+
+    def in_flight_names(self) -> set[str]:
+        with self._lock:
+            return {h.name for h in self._inflight.values()}
+
+    def idle(self) -> bool:
+        with self._lock:
+            return not self._inflight
+
+    def run_until_complete(self, h: EngineRequest, timestep: int) -> list[int]:
+        self._raise_background_error()
+        self._now = timestep
+        eng = self.backend.engine
+        occupancy, _ = eng.run(h.req, lane=0)
+        h.tokens = tuple(eng.request_tokens(h.req, h.length))
+        h.done = True
+        eng.request_release(h.req)
+        eng.seq_free(h.branch)
+        self.backend._log(h)
+        return occupancy
+
+    def set_timestep(self, timestep: int) -> None:
+        self._now = timestep
+
+    # -- background lane ----------------------------------------------------
+    def _loop(self) -> None:
+        eng = self.backend.engine
+        while not self._stop.is_set():
+            with self._lock:
+                busy = bool(self._inflight)
+            if not busy:
+                self._work.wait(0.05)
+                self._work.clear()
+                continue
+            try:
+                _, done = eng.run(-1, lane=1, max_ticks=4)
+                for req, _tick in done:
+                    with self._lock:
+                        h = self._inflight.get(req)
+                    h.tokens = tuple(eng.request_tokens(req, h.length))
+                    h.done = True
+                    eng.request_release(req)
+                    eng.seq_free(h.branch)
+                    self.backend._log(h)
+                    if h.on_complete is not None:
+                        h.on_complete(h, self._now)
+                    with self._lock:
+                        self._inflight.pop(req, None)
+            except BaseException as exc:  # surfaced on the runner thread
+                self._errors.append(exc)
+                self._stop.set()
+
+    def _raise_background_error(self) -> None:
+        if self._errors:
+            raise EngineError(f"background reasoning lane failed: {self._errors[0]!r}")
+
+    def drain(self, timeout: float = 60.0) -> None:
+        """Wait until every background request has landed."""
+        import time
+        t0 = time.time()
+        while not self.idle() and time.time() - t0 < timeout:
+            self._raise_background_error()
+            time.sleep(0.002)
+
+    def close(self) -> None:
+        self._stop.set()
+        self._work.set()
+        self._thread.join(timeout=10.0)

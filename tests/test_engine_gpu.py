@@ -341,3 +341,50 @@ def test_bf16_wide_batch_decode_runs(schema):
     finally:
         be.close()
     assert all(len(r.trace.steps) == len(schema.steps) for step in res for r in step)
+
+
+def test_two_stream_async_per_request_parity(schema):
+    """Two-stream async (action on the high-priority lane, reasoning refresh on
+    the low-priority lane in a background thread): landing order is real-time,
+    so parity is per request -- every request's tokens equal the CPU oracle's
+    greedy decode of the same framed (context, prefix, step)."""
+    import time
+    from oracle.backend import OracleModel, frame
+    log = []
+    be = EngineBackend("tiny", dtype="f32", seed=0, kv_pages=2048, async_streams=2, request_log=log)
+    try:
+        runner = S.make_runner(S.SchedulerConfig(mode="parallel_async", slots=8, wall_clock=True), be, schema)
+        results = []
+        for t in range(8):
+            ctx = be.encode("pick up the object and place it on the target", S.observation_for(0, t))
+            results.append(runner.step(ctx, t))
+            time.sleep(0.01)  # paced control loop: the reasoning lane keeps running in between
+        runner.engine.drain()
+    finally:
+        be.close()
+    assert all(len(r.trace.steps) == len(schema.steps) for r in results)
+    assert len(log) >= 7 + 7  # warm-up chain + at least one action per step
+    model = OracleModel("tiny", seed=0)
+    for ctx, prefix, name, prev, tokens in log:
+        ids = frame("tiny", ctx.encoded, prefix, name)
+        want, _ = model.generate(ids, M.vision_seed(ctx.observation), len(tokens))
+        assert tuple(want) == tokens, name
+
+
+def test_stress_schema_parallel_sync_bit_exact():
+    """Config 5 shape (8-way fan-out, every step regenerated) on the tiny model:
+    fp32 engine == CPU oracle through the same runner, 2 timesteps."""
+    from oracle.backend import OracleBackend
+    from paper_2506_07639_b200.workloads import stress_profile, stress_schema
+    sch = stress_schema()
+    cfg = S.SchedulerConfig(mode="parallel_sync", slots=8)
+    be = EngineBackend("tiny", dtype="f32", seed=0, kv_pages=2048, profile=stress_profile(0))
+    try:
+        got, _ = S.run_episode(cfg, 2, be, sch, seed=0)
+    finally:
+        be.close()
+    want, _ = S.run_episode(cfg, 2, OracleBackend("tiny", seed=0, profile=stress_profile(0)), sch, seed=0)
+    for a, b in zip(got, want):
+        assert T.trace_content_bytes(a.trace, sch) == T.trace_content_bytes(b.trace, sch)
+        assert a.latency_ms == b.latency_ms
+    assert sum(len(t) for _, t in got[1].trace.steps) > 1500
