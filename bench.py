@@ -344,6 +344,7 @@ def run_engine(args, rank, world, local):
         sdev, shost, _ = time_mode(backend, seq_runner, 1000 + seed, 0, 1 + args.seq_steps, stream)
         asy = S.make_runner(S.SchedulerConfig(mode="parallel_async", slots=8, wall_clock=True), backend, schema)
         adev, ahost, ares = time_mode(backend, asy, 2000 + seed, 0, 1 + args.async_steps, stream)
+        asy.engine.drain()  # land the lockstep runner's in-flight reasoning before the engine is reused
         # config 3 proper: two CUDA streams, reasoning refresh free-running on the
         # low-priority lane between and during control steps
         backend2 = EngineBackend(args.config, dtype=args.dtype, seed=0, device=local, profile=make_profile(0),

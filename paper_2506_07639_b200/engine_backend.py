@@ -90,7 +90,11 @@ class EngineBackend:
         self._trunks: list[_Trunk] = []
         self._trunk_cap = trunk_cache
         self._clock = 0
-        self._owners: dict[int, EngineRequest] = {}
+        # request -> handle, shared by every backend driving this engine (a
+        # request left in flight by one backend may complete in another's run)
+        if not hasattr(self.engine, "owners"):
+            self.engine.owners = {}
+        self._owners: dict[int, EngineRequest] = self.engine.owners
         self._async_engines: list = []
         self._slots = 8
         self.requests = 0
@@ -219,7 +223,9 @@ class EngineBackend:
     def _run(self, stop_req: int, timestep: int) -> list[int]:
         occupancy, done = self.engine.run(stop_req)
         for req, _tick in done:
-            h = self._owners.pop(req)
+            h = self._owners.pop(req, None)
+            if h is None:
+                raise EngineError(f"request {req} completed without an owner")
             h.tokens = tuple(self.engine.request_tokens(req, h.length))
             h.done = True
             self._log(h)
@@ -270,7 +276,17 @@ class AsyncEngine:
         return not self._inflight
 
     def run_until_complete(self, h: EngineRequest, timestep: int) -> list[int]:
+        self._now = timestep
         return self.backend._run(h.req, timestep)
+
+    def drain(self) -> None:
+        """Decode every request still in flight (they land at the last control
+        timestep) so the engine is idle before it is handed to another runner."""
+        if self._inflight:
+            self.backend._run(-1, getattr(self, "_now", 0))
+
+    def close(self) -> None:
+        pass
 
 
 class TwoStreamAsyncEngine:

@@ -388,3 +388,24 @@ def test_stress_schema_parallel_sync_bit_exact():
         assert T.trace_content_bytes(a.trace, sch) == T.trace_content_bytes(b.trace, sch)
         assert a.latency_ms == b.latency_ms
     assert sum(len(t) for _, t in got[1].trace.steps) > 1500
+
+
+def test_engine_shared_by_lockstep_then_two_stream_backends(schema):
+    """bench.py's config-3 sequence: a lockstep async episode leaves reasoning
+    requests in flight; after drain() a second backend (two streams) drives the
+    same engine from its own warm-up without stray completions."""
+    be = EngineBackend("tiny", dtype="f32", seed=0, kv_pages=2048)
+    try:
+        asy = S.make_runner(S.SchedulerConfig(mode="parallel_async", slots=8, wall_clock=True), be, schema)
+        for t in range(3):
+            asy.step(be.encode("pick up the object", S.observation_for(1, t)), t)
+        asy.engine.drain()
+        assert be.engine.in_flight() == 0
+        be2 = EngineBackend("tiny", dtype="f32", seed=0, engine=be.engine, async_streams=2)
+        asy2 = S.make_runner(S.SchedulerConfig(mode="parallel_async", slots=8, wall_clock=True), be2, schema)
+        res = [asy2.step(be2.encode("pick up the object", S.observation_for(2, t)), t) for t in range(3)]
+        asy2.engine.drain()
+        asy2.engine.close()
+    finally:
+        be.close()
+    assert all(len(r.trace.steps) == len(schema.steps) for r in res)
