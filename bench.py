@@ -149,9 +149,9 @@ def measured_peaks() -> dict:
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "source": "fallback"}
 
 
-def ncu_traffic() -> float | None:
+def ncu_traffic(name: str = "ncu_decode_gemv.json") -> float | None:
     """dram bytes per launch of the dominant kernel from the committed ncu capture."""
-    p = REPO / "profiles" / "ncu_decode_gemv.json"
+    p = REPO / "profiles" / name
     if p.exists():
         try:
             return json.loads(p.read_text()).get("dram_bytes_per_launch")
@@ -388,7 +388,12 @@ def main():
     K = args.steps
     peaks = measured_peaks()
     prof = r["prof"]
-    g = prof["decode_gemv"]
+    # dominant kernel: the persistent decode-tick kernel (one launch per decode
+    # iteration: all layers' weights + the staged KV) when it ran, else the
+    # per-matrix decode GEMMs of the kernel chain
+    tick = prof.get("decode_tick", {"ms": 0.0, "launches": 0, "bytes": 0.0})
+    use_tick = tick["launches"] > 0
+    g = tick if use_tick else prof["decode_gemv"]
     achieved = (g["bytes"] / 1e9) / (g["ms"] / 1e3) if g["ms"] > 0 else None
     steps_prof = prof.pop("steps")
     step_ms_prof = prof.pop("step_ms")
@@ -444,14 +449,19 @@ def main():
                 "h2d_bytes_per_step": (s1["h2d_bytes"] - s0["h2d_bytes"]) / K,
                 "d2h_bytes_per_step": (s1["d2h_bytes"] - s0["d2h_bytes"]) / K},
         "gpu_launches": s1["launches"] - s0["launches"],
-        "roofline": {"bound": "hbm", "kernel": "decode GEMV (QKV/O/gate-up/down/lm_head, bf16 weights)",
+        "roofline": {"bound": "hbm",
+                     "kernel": ("persistent decode-tick kernel (decode_mk_kernel: every layer's QKV/O/gate-up/down "
+                                "+ lm_head weights and the cascade-attention KV pages, one launch per tick)")
+                               if use_tick else "decode GEMV (QKV/O/gate-up/down/lm_head, bf16 weights)",
                      "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                     "frac": (achieved / peaks["hbm_gbs"]) if achieved else None, "traffic": ncu_traffic(),
+                     "frac": (achieved / peaks["hbm_gbs"]) if achieved else None, "traffic": ncu_traffic("ncu_decode_tick.json" if use_tick else "ncu_decode_gemv.json"),
                      "peak_source": peaks["source"],
                      "launches": g["launches"], "ms_total": g["ms"],
                      "share_of_step": g["ms"] / step_ms_prof,
                      "measured_on": f"{steps_prof} eager timesteps right after the timed region, CUDA events "
-                                    f"around each decode GEMM launch on the engine stream"},
+                                    f"around each {'decode-tick' if use_tick else 'decode GEMM'} launch on the "
+                                    f"engine stream",
+                     "bytes_per_launch": g["bytes"] / max(1, g["launches"])},
         "cpu_baseline": cpu,
         "clocks": r["clocks"],
         "breakdown_ms_per_step_eager": {k: v["ms"] / steps_prof for k, v in prof.items()},

@@ -116,8 +116,14 @@ int fe_op_rmsnorm(fe_engine* e, const float* x, const float* w, void* out, int32
 int fe_op_gemm_tc(fe_engine* e, const void* x, const void* w, int32_t M, int32_t N, int32_t K, float* y);
 /* bf16 tcgen05 swap-AB decode GEMM (M <= 16 rows): y[M][N] = x[M][K] . w[N][K]^T */
 int fe_op_skinny_tc(fe_engine* e, const void* x, const void* w, int32_t M, int32_t N, int32_t K, float* y);
+/* diagnostics of the persistent decode-tick kernel (option "mk_trace" = 1):
+ * globaltimer ns of the last traced tick, out[(2 ph + k) * grid + cta], k = 0
+ * when the CTA passed phase ph's grid barrier, k = 1 when it finished ph */
+int fe_debug_trace(fe_engine* e, uint64_t* out, int32_t n, int32_t* n_phases, int32_t* grid);
 /* engine options: "tc_min_rows" (rows from which a forward uses the tcgen05
- * GEMMs, bf16 only), "use_tc" (0/1) */
+ * GEMMs, bf16 only), "use_tc" (0/1), "mk" (0/1: persistent decode-tick
+ * kernel), "mk_trace", "graphs", "pdl", "sk_mask", "sk_stages", "op_reps",
+ * "debug_skip" */
 int fe_set_option(fe_engine* e, const char* key, int64_t value);
 
 #ifdef __cplusplus

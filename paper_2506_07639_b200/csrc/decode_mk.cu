@@ -1,0 +1,1016 @@
+// Persistent decode-tick kernel for the bf16 path (<= 16 rows per tick).
+//
+// One launch = one decode iteration of the whole model.  A decode tick is
+// HBM-bound (13.2 GB of weights per tick for the 7B shape), and a chain of
+// ~200 short kernels per tick loses a few microseconds of ramp-up and tail
+// on every launch.  Here one CTA per SM streams weight tiles continuously
+// through one TMA ring across every GEMM of every layer; the phases of the
+// tick are separated by grid barriers that only gate the *activation*
+// loads, so the weight stream never stops at a layer or matrix boundary.
+//
+// Warp roles (192 threads):
+//   warp 0      TMA producer.  Issues the weight tile of every ring stage as
+//               soon as the slot is free; the 16-row activation tile of a
+//               stage is issued once the phase's grid barrier has been
+//               passed (stages waiting for it are queued, at most one ring).
+//   warp 1      TMEM allocation + single-thread tcgen05.mma issue (swap-AB:
+//               M = 128 weight rows, N = 16 batch rows, K = 16) into a
+//               4-deep TMEM accumulator ring.
+//   warps 2-5   epilogues and the non-GEMM phases (embedding, cascade
+//               attention on mma.sync, argmax finalisation).
+//
+// Phases per tick (each ends with a grid barrier):
+//   EMBED        x = embed[token]; xg = bf16(x * g_attn[0]); ss = sum x^2 per 128-column tile
+//   per layer:   QKV   (epilogue: r = rsqrt(sum ss / d + eps), RoPE, q, paged K/V append)
+//                ATTN  (cascade attention chunk partials of every (page, head) item, mma.sync)
+//                AMERGE (chunk merge per (row, head) -> bf16 attention output)
+//                O     (epilogue: residual add, xg = bf16(x * g_ffn), ss)
+//                GU    (epilogue: r, SiLU(gate) * up -> act)
+//                DOWN  (epilogue: residual add, xg = bf16(x * g_next), ss)
+//   LM           lm_head + per-tile argmax keys (and fp32 logits in parity mode)
+//   FINAL        greedy token per row -> out_tokens (fed back to the next tick)
+//
+// RMSNorm is folded: y = W (x * r * g) is computed as r * (W bf16(x * g)),
+// with r from per-tile partial sums of squares written by the producing
+// epilogue (fixed-order sums: deterministic).  Split-K partials are published
+// with a release-add on a per-tile counter and reduced in split order by the
+// tile's owner CTA after its own units (no CTA ever waits on a unit that is
+// queued behind its wait), so results do not depend on timing.  Numerics are the bf16 path's (fp32 accumulation, bf16 operands);
+// the fp32 canonical mode never uses this kernel.
+//
+// Grid barriers need every CTA resident: grid = SM count, one CTA per SM
+// (shared memory forces it), no PDL, and only one lane runs this kernel.
+#include "common.cuh"
+#include "decode_mk.h"
+#include "engine_internal.h"
+#include "tc_util.cuh"
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <stdexcept>
+
+namespace fe {
+namespace {
+using namespace tc;
+
+constexpr int MT = 128;                    // weight rows per tile (UMMA M)
+constexpr int KBK = 64;                    // K per ring stage
+constexpr int XR = 16;                     // batch rows (UMMA N)
+constexpr int kStages = 11;
+constexpr int kAcc = 4;
+constexpr int kWBytes = MT * KBK * 2;      // 16 KB
+constexpr int kXBytes = XR * KBK * 2;      // 2 KB
+constexpr int kThreads = 192;
+constexpr int HD = 128;                    // head dim (7B shape)
+constexpr uint32_t kIdesc = idesc_bf16(MT, XR);
+// attention phase: the (idle) ring holds K and V of up to 6 (page, head) pairs
+constexpr int kAttnSlotBytes = 2 * FE_PAGE * HD * 2;  // 32 KB
+constexpr int kAttnSlots = kStages * (kWBytes + kXBytes) / kAttnSlotBytes;
+constexpr int kMaxPairs = kAttnSlots;  // (page, head) pairs per CTA whose items are cached in smem
+constexpr int kSmem = kStages * (kWBytes + kXBytes) + MT * (XR + 1) * 4 + XR * HD * 4 /* rope */ + 1024 /* align */ +
+                      4096 /* barriers, scratch, rows, items */;
+static_assert(kAttnSlots >= 4, "attention staging needs >= 4 slots");
+
+enum Kind { K_EMBED, K_QKV, K_RQKV, K_ATTN, K_AMERGE, K_O, K_RO, K_GU, K_RGU, K_DOWN, K_RDOWN, K_LM, K_RLM, K_FINAL };
+
+struct Args {
+  MkPlan plan[5];
+  const CUtensorMap* wmaps;
+  const float* const* norms;
+  int d, F, H, L, V, n_text;
+  float eps, scale_log2;
+  const int32_t* hdr;
+  const RowMeta* rows;
+  const AttnItem* items;
+  const ItemRow* item_rows;
+  int B;
+  const __nv_bfloat16* embed;
+  int32_t* out_tokens;
+  float* x;
+  __nv_bfloat16* xg;
+  float* ss;
+  float* q;                  // holds bf16 q [16][d] (pre-scaled by scale_log2) in this kernel
+  __nv_bfloat16* attn;
+  __nv_bfloat16* kv_pool;
+  size_t page_elems;
+  const float* rope;
+  float* partial;
+  int* counters;
+  float* apartial;
+  int* acounters;
+  unsigned long long* part_keys;
+  float* logits;
+  unsigned long long* bar;
+  int flags;                  // diagnostics (engine option "mk_flags")
+  int* grab;                  // [P] chunk counters of the GEMM phases (reset by the last CTA to exit)
+  unsigned long long* trace;  // diagnostics: [P][6][G] globaltimer: barrier pass, phase done, last weight load issued,
+                             // first / last accumulator ready, segments drained
+};
+
+// per layer: QKV, RQKV, ATTN, AMERGE, O, RO, GU, RGU, DOWN, RDOWN (R* = split reduction + epilogue)
+constexpr int kLayerPhases = 10;
+__device__ __forceinline__ int n_phases(const Args& a) { return 4 + kLayerPhases * a.L; }
+__device__ __forceinline__ int phase_kind(const Args& a, int ph, int* layer) {
+  *layer = 0;
+  if (ph == 0) return K_EMBED;
+  if (ph == 1 + kLayerPhases * a.L) return K_LM;
+  if (ph == 2 + kLayerPhases * a.L) return K_RLM;
+  if (ph == 3 + kLayerPhases * a.L) return K_FINAL;
+  *layer = (ph - 1) / kLayerPhases;
+  return K_QKV + (ph - 1) % kLayerPhases;  // K_QKV .. K_RDOWN are consecutive
+}
+// the GEMM whose chunk partials a reduction phase finalises
+__device__ __forceinline__ int gemm_kind_of_reduce(int kind) {
+  return kind == K_RQKV ? K_QKV : kind == K_RO ? K_O : kind == K_RGU ? K_GU : kind == K_RDOWN ? K_DOWN
+       : kind == K_RLM ? K_LM : -1;
+}
+__device__ __forceinline__ int gemm_of(int kind) {
+  return kind == K_QKV ? MK_QKV : kind == K_O ? MK_O : kind == K_GU ? MK_GU : kind == K_DOWN ? MK_DOWN
+       : kind == K_LM ? MK_LM : -1;
+}
+__device__ __forceinline__ const CUtensorMap* wmap_of(const Args& a, int gi, int l) {
+  return gi == MK_LM ? &a.wmaps[4 * a.L] : &a.wmaps[4 * l + gi];
+}
+// Dynamic chunks: tile t's k-blocks are cut into nc chunks; CTAs grab chunk
+// ids q = t * nc + j from a per-phase counter (tile-major, so tiles complete
+// progressively through the phase and fast SMs simply take more chunks).
+__device__ __forceinline__ void chunk_range(const MkPlan& p, int q, int* t, int* j, int* kb0, int* kb1) {
+  *t = q / p.nc;
+  *j = q - *t * p.nc;
+  *kb0 = *j * p.kb_total / p.nc;
+  *kb1 = (*j + 1) * p.kb_total / p.nc;
+}
+// producer -> MMA / epilogue queue of grabbed chunk ids (-1 ends a phase)
+constexpr int kQueue = 32;
+__device__ __forceinline__ int queue_read(volatile int* qseq, volatile int* qval, int n) {
+  while (qseq[n % kQueue] != n) {
+  }
+  __threadfence_block();
+  return qval[n % kQueue];
+}
+
+// ---- grid barrier (monotonic arrival counter, reset by the last CTA to exit)
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void spin_until(const unsigned long long* p, unsigned long long target) {
+  if (ld_acquire(p) >= target) return;
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  unsigned spins = 0;
+  while (ld_acquire(p) < target) {
+    if (++spins % 1024 == 0) {
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 2000000000ull) __trap();  // 2 s: a lost CTA; abort instead of hanging the GPU
+    }
+  }
+}
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// producer side: wait until the epilogue warps have seen phase `ph`'s grid barrier
+__device__ __forceinline__ void wait_ready(volatile int* ready_ph, int ph) {
+  if (*ready_ph >= ph) return;
+  const uint64_t t0 = gtimer();
+  unsigned spins = 0;
+  while (*ready_ph < ph) {
+    if (++spins % 1024 == 0 && gtimer() - t0 > 2000000000ull) __trap();
+  }
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
+// ---- epilogue-group (warps 2-5) helpers
+__device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+// sum over the 128 epilogue threads of v[b] (b < B) -> out[b] (fixed order)
+__device__ __forceinline__ void epi_sum16(float (&v)[XR], int B, float* red /*[4][16]*/, float* out, int ostride,
+                                          int et) {
+  const int w = et >> 5, lane = et & 31;
+#pragma unroll
+  for (int b = 0; b < XR; b++) {
+    if (b >= B) break;
+    float s = v[b];
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (lane == 0) red[w * XR + b] = s;
+  }
+  epi_sync();
+  if (et < B) out[et * ostride] = (red[et] + red[XR + et]) + (red[2 * XR + et] + red[3 * XR + et]);
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&v);
+}
+
+__device__ __forceinline__ void mma_bf16(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ uint4 ldcg4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ float4 ldcg4f(const float* p) {
+  float4 r;
+  asm volatile("ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// Cascade attention of one (page item, head) pair by one warp on mma.sync:
+// S = Q K^T (M = 16 query rows, N = 8 keys, K = 16 dims), P = exp2(S - m),
+// O = P V.  K and V of the (page, head) were staged in shared memory by one
+// bulk copy each.  Head dims are permuted identically in Q and K so every
+// lane's K fragment is one 16-byte load; V is read as 32-byte row slices and
+// paired across keys with byte permutes.  Writes the chunk partial (m, l, o)
+// of every row of the item; the chunks of a (row, head) are merged in the
+// next phase.
+// Q fragments of a pair: bf16, pre-scaled to the exp2 domain by the QKV epilogue;
+// k-step s = 2i + j covers dims 32i + 8t + 4j + {0,1} | {2,3}
+__device__ __forceinline__ void attn_load_q(const Args& a, const AttnItem& it, const ItemRow* irows, int h, int lane,
+                                            uint4 (&q0)[4], uint4 (&q1)[4]) {
+  const int g = lane >> 2, t = lane & 3;
+  const __nv_bfloat16* qb = reinterpret_cast<const __nv_bfloat16*>(a.q);
+  const int nr = it.row_count;
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    q0[i] = g < nr ? ldcg4(qb + (size_t)irows[g].row * a.d + h * HD + 32 * i + 8 * t) : make_uint4(0u, 0u, 0u, 0u);
+    q1[i] = g + 8 < nr ? ldcg4(qb + (size_t)irows[g + 8].row * a.d + h * HD + 32 * i + 8 * t)
+                       : make_uint4(0u, 0u, 0u, 0u);
+  }
+}
+
+__device__ void attn_pair(const Args& a, const RowMeta* srows, const AttnItem& it, const ItemRow* irows, int h,
+                          const unsigned char* ks, const unsigned char* vs, const uint4 (&q0)[4],
+                          const uint4 (&q1)[4], int lane) {
+  const int g = lane >> 2, t = lane & 3;
+  const int H = a.H;
+  const int nr = it.row_count;
+  const int r0 = g, r1 = g + 8;
+  const ItemRow ir0 = r0 < nr ? irows[r0] : ItemRow{0, 0};
+  const ItemRow ir1 = r1 < nr ? irows[r1] : ItemRow{0, 0};
+  const int v0 = r0 < nr ? ir0.valid : 0, v1 = r1 < nr ? ir1.valid : 0;
+  const int vmax = it.valid_max;
+  uint32_t qa[8][4];
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    qa[2 * i][0] = q0[i].x;
+    qa[2 * i][1] = q1[i].x;
+    qa[2 * i][2] = q0[i].y;
+    qa[2 * i][3] = q1[i].y;
+    qa[2 * i + 1][0] = q0[i].z;
+    qa[2 * i + 1][1] = q1[i].z;
+    qa[2 * i + 1][2] = q0[i].w;
+    qa[2 * i + 1][3] = q1[i].w;
+  }
+  float s[8][4];
+#pragma unroll
+  for (int nt = 0; nt < 8; nt++) {
+    s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.0f;
+    if (8 * nt >= vmax) continue;
+    const uint4* kr = reinterpret_cast<const uint4*>(ks + (size_t)(8 * nt + g) * HD * 2 + 16 * t);
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      const uint4 kv = kr[4 * i];  // dims 32i + 8t .. +7
+      mma_bf16(s[nt], qa[2 * i], kv.x, kv.y);
+      mma_bf16(s[nt], qa[2 * i + 1], kv.z, kv.w);
+    }
+  }
+  // masked softmax (exp2 domain) per row; rows g (c0, c1) and g + 8 (c2, c3)
+  float m0 = -INFINITY, m1 = -INFINITY;
+#pragma unroll
+  for (int nt = 0; nt < 8; nt++) {
+    const int j = 8 * nt + 2 * t;
+    if (j < v0) m0 = fmaxf(m0, s[nt][0]);
+    if (j + 1 < v0) m0 = fmaxf(m0, s[nt][1]);
+    if (j < v1) m1 = fmaxf(m1, s[nt][2]);
+    if (j + 1 < v1) m1 = fmaxf(m1, s[nt][3]);
+  }
+  m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, 1));
+  m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, 2));
+  m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, 1));
+  m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, 2));
+  const float mu0 = v0 > 0 ? m0 : 0.0f, mu1 = v1 > 0 ? m1 : 0.0f;
+  float l0 = 0.0f, l1 = 0.0f;
+#pragma unroll
+  for (int nt = 0; nt < 8; nt++) {
+    const int j = 8 * nt + 2 * t;
+    s[nt][0] = j < v0 ? exp2f(s[nt][0] - mu0) : 0.0f;
+    s[nt][1] = j + 1 < v0 ? exp2f(s[nt][1] - mu0) : 0.0f;
+    s[nt][2] = j < v1 ? exp2f(s[nt][2] - mu1) : 0.0f;
+    s[nt][3] = j + 1 < v1 ? exp2f(s[nt][3] - mu1) : 0.0f;
+    l0 += s[nt][0] + s[nt][1];
+    l1 += s[nt][2] + s[nt][3];
+  }
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+
+  // O = P V over 16-key steps kk; output dim of (n-tile nt, column n) = 16 n + nt
+  float o[16][4];
+#pragma unroll
+  for (int nt = 0; nt < 16; nt++) o[nt][0] = o[nt][1] = o[nt][2] = o[nt][3] = 0.0f;
+#pragma unroll
+  for (int kk = 0; kk < 4; kk++) {
+    if (16 * kk >= vmax) break;
+    uint32_t pa[4];
+    pa[0] = pack_bf16(s[2 * kk][0], s[2 * kk][1]);
+    pa[1] = pack_bf16(s[2 * kk][2], s[2 * kk][3]);
+    pa[2] = pack_bf16(s[2 * kk + 1][0], s[2 * kk + 1][1]);
+    pa[3] = pack_bf16(s[2 * kk + 1][2], s[2 * kk + 1][3]);
+    // keys 16kk + 2t + {0, 1, 8, 9}, dims 16g .. 16g+15 (zero beyond the staged keys)
+    uint4 w[4][2];
+#pragma unroll
+    for (int c = 0; c < 4; c++) {
+      const int key = 16 * kk + 2 * t + (c & 1) + 8 * (c >> 1);
+      const uint4* vr = reinterpret_cast<const uint4*>(vs + (size_t)key * HD * 2 + 32 * g);
+      const bool ok = key < vmax;
+      w[c][0] = ok ? vr[0] : make_uint4(0u, 0u, 0u, 0u);
+      w[c][1] = ok ? vr[1] : make_uint4(0u, 0u, 0u, 0u);
+    }
+#pragma unroll
+    for (int nt = 0; nt < 16; nt++) {
+      const int wi = nt >> 1;  // word of the 16-dim slice holding dim 16g + nt
+      const uint32_t sel = (nt & 1) ? 0x7632u : 0x5410u;
+      auto word = [&](int c) -> uint32_t {
+        const uint4& v = w[c][wi >> 2];
+        const int k = wi & 3;
+        return k == 0 ? v.x : k == 1 ? v.y : k == 2 ? v.z : v.w;
+      };
+      mma_bf16(o[nt], pa, __byte_perm(word(0), word(1), sel), __byte_perm(word(2), word(3), sel));
+    }
+  }
+
+  // chunk partials: lane (g, t) holds dims 32t + nt (c0/c2) and 32t + 16 + nt (c1/c3)
+  const int stride = HD + 2;
+#pragma unroll
+  for (int hr = 0; hr < 2; hr++) {
+    const int r = hr ? r1 : r0;
+    if (r >= nr) continue;
+    const RowMeta& m = srows[hr ? ir1.row : ir0.row];
+    float* pp = a.apartial + ((size_t)(m.chunk_base + it.chunk) * H + h) * stride;
+    if (t == 0) {
+      pp[0] = hr ? mu1 : mu0;
+      pp[1] = hr ? l1 : l0;
+    }
+#pragma unroll
+    for (int nt = 0; nt < 16; nt++) {
+      pp[2 + 32 * t + nt] = o[nt][hr ? 2 : 0];
+      pp[2 + 32 * t + 16 + nt] = o[nt][hr ? 3 : 1];
+    }
+  }
+}
+
+// Merge the chunk partials of one (row, head) in chunk order -> bf16 attention output.
+__device__ void attn_merge(const Args& a, const RowMeta& m, int row, int h, int lane) {
+  const int stride = HD + 2;
+  const size_t cs = (size_t)a.H * stride;
+  const float* base = a.apartial + ((size_t)m.chunk_base * a.H + h) * stride;
+  const int nch = m.n_chunks;
+  float M = -INFINITY, L = 0.0f, acc[4] = {0.f, 0.f, 0.f, 0.f};
+  // batches of 16 chunks: (m, l) lane-parallel and this lane's 4 dims of every
+  // chunk issued together (one memory round per batch), running-max rescale
+  for (int c0 = 0; c0 < nch; c0 += 16) {
+    const int nb = min(16, nch - c0);
+    float mc = -INFINITY, lc = 0.0f;
+    if (lane < nb) {
+      mc = __ldcg(base + (c0 + lane) * cs);
+      lc = __ldcg(base + (c0 + lane) * cs + 1);
+    }
+    float2 lo[16], hi[16];
+#pragma unroll
+    for (int u = 0; u < 16; u++)
+      if (u < nb) {  // partial rows are 130 floats: 8-byte aligned only
+        const float* src = base + (c0 + u) * cs + 2 + 4 * lane;
+        lo[u] = __ldcg(reinterpret_cast<const float2*>(src));
+        hi[u] = __ldcg(reinterpret_cast<const float2*>(src + 2));
+      }
+    float Mb = mc;
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) Mb = fmaxf(Mb, __shfl_xor_sync(0xffffffffu, Mb, off));
+    const float Mn = fmaxf(M, Mb);
+    const float rescale = M == -INFINITY ? 0.0f : exp2f(M - Mn);
+    L *= rescale;
+#pragma unroll
+    for (int i = 0; i < 4; i++) acc[i] *= rescale;
+    const float wl = lane < nb ? exp2f(mc - Mn) : 0.0f;
+    float ls = wl * lc;
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) ls += __shfl_xor_sync(0xffffffffu, ls, off);
+    L += ls;
+#pragma unroll
+    for (int u = 0; u < 16; u++) {
+      const float wt = __shfl_sync(0xffffffffu, wl, u);
+      if (u < nb) {
+        acc[0] = fmaf(wt, lo[u].x, acc[0]);
+        acc[1] = fmaf(wt, lo[u].y, acc[1]);
+        acc[2] = fmaf(wt, hi[u].x, acc[2]);
+        acc[3] = fmaf(wt, hi[u].y, acc[3]);
+      }
+    }
+    M = Mn;
+  }
+  const float inv = 1.0f / L;
+  uint2 packed;
+  packed.x = pack_bf16(acc[0] * inv, acc[1] * inv);
+  packed.y = pack_bf16(acc[2] * inv, acc[3] * inv);
+  *reinterpret_cast<uint2*>(a.attn + (size_t)row * a.d + h * HD + 4 * lane) = packed;
+}
+
+__device__ __forceinline__ int ld_acquire_i32(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ int atom_add_acq_rel(int* p, int v) {
+  int old;
+  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
+// Final epilogue of one reduced [128 x B] tile (fp32 in shared memory):
+// thread r <-> weight row r of the tile.
+__device__ __forceinline__ void tile_epilogue(const Args& a, int kind, int l, int tl, const float* tile,
+                                              const float* rn, float* red, unsigned long long* kred,
+                                              const RowMeta* srows, const float* srope, float gw, int et, int warp,
+                                              int lane) {
+  const int r = 32 * (warp & 3) + lane;
+  const int d = a.d, B = a.B;
+  const int n0 = tl * MT;
+  if (kind == K_QKV) {
+    if (et < 64) {
+      const int sec = n0 / d, h = (n0 % d) / HD, half = HD / 2;
+      const size_t layer_off = (size_t)l * 2 * a.H * FE_PAGE * HD;
+#pragma unroll
+      for (int b = 0; b < XR; b++) {
+        if (b >= B) break;
+        const RowMeta& m = srows[b];
+        float x1 = tile[et * (XR + 1) + b] * rn[b], x2 = tile[(et + half) * (XR + 1) + b] * rn[b];
+        if (sec < 2) {
+          const float co = srope[b * HD + et], sn = srope[b * HD + half + et];
+          const float r1 = fmaf(x1, co, -(x2 * sn));
+          const float r2 = fmaf(x2, co, x1 * sn);
+          x1 = r1;
+          x2 = r2;
+        }
+        if (sec == 0) {  // bf16, pre-scaled for exp2-domain scores (attention A operand)
+          __nv_bfloat16* qr = reinterpret_cast<__nv_bfloat16*>(a.q) + (size_t)b * d + h * HD;
+          qr[et] = __float2bfloat16_rn(x1 * a.scale_log2);
+          qr[et + half] = __float2bfloat16_rn(x2 * a.scale_log2);
+        } else {
+          __nv_bfloat16* kv = a.kv_pool + (size_t)m.kv_page * a.page_elems + layer_off +
+                              ((size_t)((sec - 1) * a.H + h) * FE_PAGE + m.kv_slot) * HD;
+          kv[et] = __float2bfloat16_rn(x1);
+          kv[et + half] = __float2bfloat16_rn(x2);
+        }
+      }
+    }
+  } else if (kind == K_O || kind == K_DOWN) {
+    const int col = n0 + r;
+    float sq[XR];
+#pragma unroll
+    for (int b = 0; b < XR; b++) {
+      sq[b] = 0.0f;
+      if (b < B) {
+        const float xv = tile[r * (XR + 1) + b];  // old x already folded into the sum
+        a.x[(size_t)b * d + col] = xv;
+        a.xg[(size_t)b * d + col] = __float2bfloat16_rn(xv * gw);
+        sq[b] = xv * xv;
+      }
+    }
+    epi_sum16(sq, B, red, a.ss + tl, a.d / MT, et);  // ss[row][tile]
+  } else if (kind == K_GU) {
+    if (et < 64 && tl * 64 + et < a.F)
+      for (int b = 0; b < B; b++)
+        a.attn[(size_t)b * a.F + tl * 64 + et] = __float2bfloat16_rn(
+            silu_mul(tile[et * (XR + 1) + b] * rn[b], tile[(et + 64) * (XR + 1) + b] * rn[b]));
+  } else {  // K_LM
+    const int nrow = n0 + r;
+    const bool row_ok = nrow < a.V;
+    for (int b = 0; b < B; b++) {
+      const float v = tile[r * (XR + 1) + b] * rn[b];
+      unsigned long long k = (row_ok && nrow < a.n_text) ? argmax_key(v, nrow) : 0ull;
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) k = max(k, __shfl_xor_sync(0xffffffffu, k, off));
+      if (lane == 0) kred[b * 4 + (warp & 3)] = k;
+      if (row_ok && a.logits && srows[b].logit_row >= 0) a.logits[(size_t)srows[b].logit_row * a.V + nrow] = v;
+    }
+    epi_sync();
+    if (et < B)
+      a.part_keys[(size_t)et * a.plan[MK_LM].tiles + tl] =
+          max(max(kred[et * 4], kred[et * 4 + 1]), max(kred[et * 4 + 2], kred[et * 4 + 3]));
+  }
+}
+
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads, 1) decode_mk_kernel(const __grid_constant__ CUtensorMap map_xg,
+                                                                const __grid_constant__ CUtensorMap map_attn,
+                                                                const __grid_constant__ CUtensorMap map_act,
+                                                                const Args a) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  unsigned char* sw = smem;                                  // [kStages][128 x 64] weights
+  unsigned char* sx = smem + kStages * kWBytes;              // [kStages][16 x 64] activations
+  float* tile = (float*)(sx + kStages * kXBytes);            // [128][17]
+  float* srope = tile + MT * (XR + 1);                       // [16][128] RoPE cos | sin of the rows' positions
+  uint64_t* full = (uint64_t*)(srope + XR * HD);
+  uint64_t* empty = full + kStages;
+  uint64_t* acc_full = empty + kStages;
+  uint64_t* acc_empty = acc_full + kAcc;
+  uint32_t* tmem_slot = (uint32_t*)(acc_empty + kAcc);
+  int* last_flag = (int*)(tmem_slot + 1);
+  float* rn = (float*)(tmem_slot + 4);                       // [16] row norms of the phase
+  float* red = rn + XR;                                      // [4][16] epilogue reductions
+  unsigned long long* kred = (unsigned long long*)(red + 4 * XR);  // [16][4]
+  volatile int* ready_ph = (volatile int*)(kred + 4 * XR);    // last phase whose grid barrier was passed
+  RowMeta* srows = (RowMeta*)(kred + 4 * XR + 2);            // [16] rows of the tick
+  uint64_t* abar = (uint64_t*)(srows + XR);                  // [kAttnSlots] K/V staging barriers
+  volatile int* qseq = (volatile int*)(abar + kAttnSlots);   // [kQueue] chunk queue: sequence numbers
+  volatile int* qval = qseq + kQueue;                        // [kQueue] chunk ids
+  AttnItem* sitems = (AttnItem*)(qval + kQueue);             // [kMaxPairs] items of this CTA's pairs
+  ItemRow* sirows = (ItemRow*)(sitems + kMaxPairs);          // [kMaxPairs][16] their query rows
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = gridDim.x;
+  const int P = n_phases(a);
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < kStages; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < kAcc; i++) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], 1);
+    }
+    for (int i = 0; i < kAttnSlots; i++) mbar_init(&abar[i], 1);
+    for (int i = 0; i < kQueue; i++) qseq[i] = -1;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    *ready_ph = -1;
+  }
+  if (threadIdx.x >= 64) {  // per-tick constants: rows, their RoPE rows, this CTA's attention items
+    const int et = threadIdx.x - 64;
+    if (et < a.B) srows[et] = a.rows[et];
+    for (int b = 0; b < a.B; b++) srope[b * HD + et] = __ldg(a.rope + (size_t)a.rows[b].pos * HD + et);
+    const int n_pairs = a.hdr[1] * a.H;
+    for (int j = 0; j < kMaxPairs; j++) {
+      const int pr = blockIdx.x + j * gridDim.x;
+      if (pr >= n_pairs) break;
+      const AttnItem it = a.items[pr / a.H];
+      if (et == 0) sitems[j] = it;
+      if (et < it.row_count) sirows[j * XR + et] = a.item_rows[it.row_begin + et];
+    }
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
+                 "n"(kAcc * XR));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer
+      const uint64_t wpol = policy_evict_first();  // weights are read once per tick
+      int it = 0, n = 0;
+      int pend_slot[kStages], pend_kb[kStages];
+      for (int ph = 0; ph < P; ph++) {
+        int l;
+        const int kind = phase_kind(a, ph, &l);
+        const int gi = gemm_of(kind);
+        if (gi < 0) continue;
+        const MkPlan p = a.plan[gi];
+        const CUtensorMap* wm = wmap_of(a, gi, l);
+        const CUtensorMap* xm = gi == MK_O ? &map_attn : gi == MK_DOWN ? &map_act : &map_xg;
+        // the attention phase borrows the ring: start the O weights only once this
+        // CTA's epilogue warps have left it (they publish the AMERGE barrier)
+        if (kind == K_O) wait_ready(ready_ph, ph - 1);
+        if (a.flags & 1) wait_ready(ready_ph, ph);  // diagnostics: no weight prefetch across barriers
+        bool ready = false;
+        int npend = 0;
+        auto flush = [&]() {
+          __threadfence_block();
+          fence_proxy_async();
+          for (int i = 0; i < npend; i++)
+            tma_load_2d(sx + pend_slot[i] * kXBytes, xm, &full[pend_slot[i]], pend_kb[i] * KBK, 0);
+          npend = 0;
+          ready = true;
+        };
+        int q = atomicAdd(&a.grab[ph], 1);
+        while (true) {
+          const bool valid = q < p.chunks;
+          const int q_next = valid ? atomicAdd(&a.grab[ph], 1) : 0;  // next grab in flight meanwhile
+          qval[n % kQueue] = valid ? q : -1;
+          __threadfence_block();
+          qseq[n % kQueue] = n;
+          n++;
+          if (!valid) break;
+          int tl, j, kb0, kb1;
+          chunk_range(p, q, &tl, &j, &kb0, &kb1);
+          for (int kb = kb0; kb < kb1; kb++, it++) {
+            const int s = it % kStages;
+            if (!ready && npend == kStages) {  // the slot to refill is still waiting for its activations
+              wait_ready(ready_ph, ph);
+              flush();
+            }
+            mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
+            mbar_expect_tx(&full[s], kWBytes + kXBytes);
+            if (gi == MK_GU) {
+              tma_load_2d_hint(sw + s * kWBytes, wm, &full[s], kb * KBK, tl * (MT / 2), wpol);
+              tma_load_2d_hint(sw + s * kWBytes + kWBytes / 2, wm, &full[s], kb * KBK, a.F + tl * (MT / 2), wpol);
+            } else {
+              tma_load_2d_hint(sw + s * kWBytes, wm, &full[s], kb * KBK, tl * MT, wpol);
+            }
+            if (!ready && *ready_ph >= ph) flush();
+            if (ready) {
+              tma_load_2d(sx + s * kXBytes, xm, &full[s], kb * KBK, 0);
+            } else {
+              pend_slot[npend] = s;
+              pend_kb[npend] = kb;
+              npend++;
+            }
+          }
+          q = q_next;
+        }
+        if (a.trace) a.trace[((size_t)ph * 6 + 2) * G + blockIdx.x] = gtimer();
+        if (!ready) {
+          wait_ready(ready_ph, ph);
+          flush();
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer
+      int it = 0, lu = 0, n = 0;
+      for (int ph = 0; ph < P; ph++) {
+        int l;
+        const int gi = gemm_of(phase_kind(a, ph, &l));
+        if (gi < 0) continue;
+        const MkPlan p = a.plan[gi];
+        for (;; lu++) {
+          const int q = queue_read(qseq, qval, n++);
+          if (q < 0) break;
+          int tl, j, kb0, kb1;
+          chunk_range(p, q, &tl, &j, &kb0, &kb1);
+          const int acc = lu % kAcc;
+          mbar_wait(&acc_empty[acc], ((lu / kAcc) & 1) ^ 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t dst = tmem + (uint32_t)(acc * XR);
+          for (int kb = kb0; kb < kb1; kb++, it++) {
+            const int s = it % kStages;
+            mbar_wait(&full[s], (it / kStages) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint64_t da = smem_desc(sw + s * kWBytes);
+            const uint64_t db = smem_desc(sx + s * kXBytes);
+#pragma unroll
+            for (int k = 0; k < KBK / 16; k++) {
+              const uint64_t off = (uint64_t)((k * 32) >> 4);
+              const uint32_t accum = (kb > kb0 || k > 0) ? 1u : 0u;
+              asm volatile(
+                  "{ .reg .pred p; setp.ne.b32 p, %4, 0;"
+                  " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }"
+                  ::"r"(dst), "l"(da + off), "l"(db + off), "r"(kIdesc), "r"(accum));
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                         ::"r"(su32(&empty[s])) : "memory");
+          }
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                       ::"r"(su32(&acc_full[acc])) : "memory");
+        }
+      }
+    }
+  } else {
+    // ---------------- epilogue / non-GEMM phases (128 threads)
+    const int et = threadIdx.x - 64;
+    const int r = 32 * (warp & 3) + lane;  // TMEM lane = weight row of the tile
+    const int d = a.d, B = a.B;
+    const int n_ss = d / MT;
+    int lu = 0, n = 0;
+    uint32_t apar = 0;  // phase parity of the attention staging barriers
+    for (int ph = 0; ph < P; ph++) {
+      int l;
+      const int kind = phase_kind(a, ph, &l);
+      if (et == 0) {
+        spin_until(a.bar, (unsigned long long)ph * G);
+        if (a.trace) a.trace[((size_t)ph * 6) * G + blockIdx.x] = gtimer();
+        __threadfence_block();
+        *ready_ph = ph;  // lets the producer issue this phase's activation loads
+      }
+      epi_sync();
+
+      if (kind == K_EMBED) {
+        for (int ct = blockIdx.x; ct < n_ss; ct += G) {
+          const int col = ct * MT + et;
+          const float gw = __ldg(a.norms[0] + col);
+          int tok[XR];
+#pragma unroll
+          for (int b = 0; b < XR; b++)
+            tok[b] = b < B ? (srows[b].tok >= 0 ? srows[b].tok : __ldcg(a.out_tokens + srows[b].tok_src)) : 0;
+          float xv[XR], sq[XR];
+#pragma unroll
+          for (int b = 0; b < XR; b++) xv[b] = b < B ? __bfloat162float(a.embed[(size_t)tok[b] * d + col]) : 0.0f;
+#pragma unroll
+          for (int b = 0; b < XR; b++) {
+            sq[b] = xv[b] * xv[b];
+            if (b < B) {
+              a.x[(size_t)b * d + col] = xv[b];
+              a.xg[(size_t)b * d + col] = __float2bfloat16_rn(xv[b] * gw);
+            }
+          }
+          epi_sum16(sq, B, red, a.ss + ct, n_ss, et);
+          epi_sync();
+        }
+      } else if (kind == K_ATTN) {
+        // The ring is idle (the producer holds the next weights back until this
+        // phase ends): stage K and V of this CTA's (page, head) pairs into it with
+        // bulk copies, all in flight at once, then one warp per pair computes.
+        const int n_pairs = a.hdr[1] * a.H;
+        const __nv_bfloat16* pool_l = a.kv_pool + (size_t)l * 2 * a.H * FE_PAGE * HD;
+        if (a.trace && et == 0) a.trace[((size_t)ph * 6 + 2) * G + blockIdx.x] = gtimer();
+        for (int base = blockIdx.x, round = 0; base < n_pairs; base += kAttnSlots * G, round++) {
+          auto item_of = [&](int j, int pr) -> AttnItem { return round == 0 ? sitems[j] : a.items[pr / a.H]; };
+          if (et == 0) {
+            fence_proxy_async();  // K/V written by the QKV epilogues (generic) -> bulk-copy reads
+            for (int j = 0; j < kAttnSlots && base + j * G < n_pairs; j++) {
+              const int pr = base + j * G;
+              const AttnItem it = item_of(j, pr);
+              const uint32_t bytes = (uint32_t)it.valid_max * HD * 2;
+              const __nv_bfloat16* kg = pool_l + (size_t)it.page * a.page_elems + (size_t)(pr % a.H) * FE_PAGE * HD;
+              unsigned char* slot = sw + (size_t)j * kAttnSlotBytes;
+              mbar_expect_tx(&abar[j], 2 * bytes);
+              bulk_g2s(slot, kg, bytes, &abar[j]);
+              bulk_g2s(slot + kAttnSlotBytes / 2, kg + (size_t)a.H * FE_PAGE * HD, bytes, &abar[j]);
+            }
+          }
+          for (int j = et >> 5; j < kAttnSlots; j += 4) {
+            const int pr = base + j * G;
+            if (pr >= n_pairs) break;
+            const AttnItem it = item_of(j, pr);
+            const ItemRow* irows = round == 0 ? sirows + j * XR : a.item_rows + it.row_begin;
+            uint4 q0[4], q1[4];
+            attn_load_q(a, it, irows, pr % a.H, lane, q0, q1);  // overlaps the K/V staging
+            mbar_wait(&abar[j], (apar >> j) & 1u);
+            if (a.trace && et == 0 && round == 0) a.trace[((size_t)ph * 6 + 3) * G + blockIdx.x] = gtimer();
+            const unsigned char* slot = sw + (size_t)j * kAttnSlotBytes;
+            attn_pair(a, srows, it, irows, pr % a.H, slot, slot + kAttnSlotBytes / 2, q0, q1, lane);
+            if (a.trace && et == 0 && round == 0) a.trace[((size_t)ph * 6 + 4) * G + blockIdx.x] = gtimer();
+          }
+          if (a.trace && et == 0 && round == 0) a.trace[((size_t)ph * 6 + 5) * G + blockIdx.x] = gtimer();
+          for (int j = 0; j < kAttnSlots && base + j * G < n_pairs; j++) apar ^= 1u << j;
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem reads before async writes
+          epi_sync();  // slots reused by the next round
+        }
+      } else if (kind == K_AMERGE) {
+        if (a.trace && et == 0) a.trace[((size_t)ph * 6 + 2) * G + blockIdx.x] = gtimer();
+        for (int pr = blockIdx.x * 4 + (et >> 5); pr < B * a.H; pr += G * 4)
+          attn_merge(a, srows[pr / a.H], pr / a.H, pr % a.H, lane);
+        if (a.trace && et == 0) a.trace[((size_t)ph * 6 + 5) * G + blockIdx.x] = gtimer();
+      } else if (kind == K_FINAL) {
+        const int tiles = a.plan[MK_LM].tiles;
+        for (int b = blockIdx.x; b < B; b += G) {
+          unsigned long long k = 0ull;
+          for (int t = et; t < tiles; t += 128) k = max(k, __ldcg(&a.part_keys[(size_t)b * tiles + t]));
+#pragma unroll
+          for (int off = 16; off >= 1; off >>= 1) k = max(k, __shfl_xor_sync(0xffffffffu, k, off));
+          if (lane == 0) kred[et >> 5] = k;
+          epi_sync();
+          if (et == 0) {
+            const unsigned long long kk = max(max(kred[0], kred[1]), max(kred[2], kred[3]));
+            if (srows[b].out_idx >= 0) a.out_tokens[srows[b].out_idx] = argmax_index(kk);
+          }
+          epi_sync();
+        }
+      } else if (gemm_of(kind) >= 0) {
+        // ---- GEMM phase: drain each grabbed chunk's accumulator into its partial
+        // slot (no synchronisation; the grid barrier publishes them)
+        const MkPlan p = a.plan[gemm_of(kind)];
+        bool first_chunk = true;
+        for (;; lu++) {
+          const int q = queue_read(qseq, qval, n++);
+          if (q < 0) break;
+          int tl, j, kb0, kb1;
+          chunk_range(p, q, &tl, &j, &kb0, &kb1);
+          const int acc = lu % kAcc;
+          // residual GEMMs: chunk 0 of a tile folds the old x into its partial
+          // (loaded while the MMAs run), so the tile epilogue needs no x load
+          const bool fold_x = (kind == K_O || kind == K_DOWN) && j == 0;
+          float xo[XR];
+#pragma unroll
+          for (int b = 0; b < XR; b++) xo[b] = (fold_x && b < B) ? __ldcg(a.x + (size_t)b * d + tl * MT + r) : 0.0f;
+          mbar_wait(&acc_full[acc], (lu / kAcc) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          if (a.trace && et == 0) {
+            const uint64_t tnow = gtimer();
+            if (first_chunk) a.trace[((size_t)ph * 6 + 3) * G + blockIdx.x] = tnow;
+            a.trace[((size_t)ph * 6 + 4) * G + blockIdx.x] = tnow;
+          }
+          first_chunk = false;
+          uint32_t raw[16];
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+              : "=r"(raw[0]), "=r"(raw[1]), "=r"(raw[2]), "=r"(raw[3]), "=r"(raw[4]), "=r"(raw[5]), "=r"(raw[6]),
+                "=r"(raw[7]), "=r"(raw[8]), "=r"(raw[9]), "=r"(raw[10]), "=r"(raw[11]), "=r"(raw[12]),
+                "=r"(raw[13]), "=r"(raw[14]), "=r"(raw[15])
+              : "r"(tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(acc * XR)));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          epi_sync();
+          if (et == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&acc_empty[acc])) : "memory");
+          // partial layout [chunk][batch rows / 4][128 weight rows] float4: coalesced
+          float4* dst = reinterpret_cast<float4*>(a.partial) + (size_t)q * (XR / 4) * MT + r;
+#pragma unroll
+          for (int q4 = 0; q4 < XR / 4; q4++)
+            if (4 * q4 < B)
+              __stcg(dst + q4 * MT, make_float4(__uint_as_float(raw[4 * q4]) + xo[4 * q4],
+                                           __uint_as_float(raw[4 * q4 + 1]) + xo[4 * q4 + 1],
+                                           __uint_as_float(raw[4 * q4 + 2]) + xo[4 * q4 + 2],
+                                           __uint_as_float(raw[4 * q4 + 3]) + xo[4 * q4 + 3]));
+        }
+        if (a.trace && et == 0) a.trace[((size_t)ph * 6 + 5) * G + blockIdx.x] = gtimer();
+      } else {
+        // ---- reduction phase: the tiles t = cta (mod grid) of the GEMM just done:
+        // sum the nc chunk partials in chunk order (deterministic), then the fused
+        // epilogue (RoPE + q / paged K/V, residual + norm inputs, SiLU * up, argmax).
+        // The norm sums, gain column and partials are all requested in one round.
+        const int gk = gemm_kind_of_reduce(kind);
+        const MkPlan p = a.plan[gemm_of(gk)];
+        const bool scaled = gk == K_QKV || gk == K_GU || gk == K_LM;
+        const bool resid = gk == K_O || gk == K_DOWN;
+        const float* gnext = gk == K_O ? a.norms[2 * l + 1]
+                             : gk == K_DOWN ? (l + 1 < a.L ? a.norms[2 * (l + 1)] : a.norms[2 * a.L]) : nullptr;
+        if (a.trace && et == 0) a.trace[((size_t)ph * 6 + 2) * G + blockIdx.x] = gtimer();
+        float4 sv[8];
+        const bool need_ss = scaled && et < B && blockIdx.x < p.tiles;
+        if (need_ss) {
+          const float4* sr = reinterpret_cast<const float4*>(a.ss + (size_t)et * n_ss);
+#pragma unroll
+          for (int u = 0; u < 8; u++) sv[u] = 4 * u < n_ss ? __ldcg(sr + u) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        for (int tl = blockIdx.x; tl < p.tiles; tl += G) {
+          const float gw = resid ? __ldg(gnext + tl * MT + r) : 0.0f;
+          float4 acc4[XR / 4];
+#pragma unroll
+          for (int q4 = 0; q4 < XR / 4; q4++) acc4[q4] = make_float4(0.f, 0.f, 0.f, 0.f);
+          const size_t q0 = (size_t)tl * p.nc;
+          if (B <= 8) {  // 12 chunks x 2 float4 in flight
+            for (int c0 = 0; c0 < p.nc; c0 += 12) {
+              float4 v[12][2];
+#pragma unroll
+              for (int u = 0; u < 12; u++) {
+                const float4* src = reinterpret_cast<const float4*>(a.partial) + (q0 + c0 + u) * (XR / 4) * MT + r;
+                if (c0 + u < p.nc) {
+                  v[u][0] = __ldcg(src);
+                  v[u][1] = B > 4 ? __ldcg(src + MT) : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+              }
+#pragma unroll
+              for (int u = 0; u < 12; u++)
+                if (c0 + u < p.nc) {
+#pragma unroll
+                  for (int q4 = 0; q4 < 2; q4++) {
+                    acc4[q4].x += v[u][q4].x; acc4[q4].y += v[u][q4].y;
+                    acc4[q4].z += v[u][q4].z; acc4[q4].w += v[u][q4].w;
+                  }
+                }
+            }
+          } else {
+            for (int c0 = 0; c0 < p.nc; c0 += 4) {
+              float4 v[4][XR / 4];
+#pragma unroll
+              for (int u = 0; u < 4; u++)
+#pragma unroll
+                for (int q4 = 0; q4 < XR / 4; q4++)
+                  if (c0 + u < p.nc && 4 * q4 < B)
+                    v[u][q4] = __ldcg(reinterpret_cast<const float4*>(a.partial) + ((q0 + c0 + u) * (XR / 4) + q4) * MT + r);
+#pragma unroll
+              for (int u = 0; u < 4; u++)
+#pragma unroll
+                for (int q4 = 0; q4 < XR / 4; q4++)
+                  if (c0 + u < p.nc && 4 * q4 < B) {
+                    acc4[q4].x += v[u][q4].x; acc4[q4].y += v[u][q4].y;
+                    acc4[q4].z += v[u][q4].z; acc4[q4].w += v[u][q4].w;
+                  }
+            }
+          }
+          if (tl == blockIdx.x && need_ss) {
+            float sacc = 0.0f;
+#pragma unroll
+            for (int u = 0; u < 8; u++) sacc += (sv[u].x + sv[u].y) + (sv[u].z + sv[u].w);
+            for (int t4 = 32; t4 < n_ss; t4++) sacc += __ldcg(a.ss + (size_t)et * n_ss + t4);  // d > 4096 only
+            rn[et] = rsqrtf(sacc / (float)d + a.eps);
+          }
+#pragma unroll
+          for (int q4 = 0; q4 < XR / 4; q4++) {
+            tile[r * (XR + 1) + 4 * q4] = acc4[q4].x;
+            tile[r * (XR + 1) + 4 * q4 + 1] = acc4[q4].y;
+            tile[r * (XR + 1) + 4 * q4 + 2] = acc4[q4].z;
+            tile[r * (XR + 1) + 4 * q4 + 3] = acc4[q4].w;
+          }
+          epi_sync();  // tile and rn visible
+          if (a.trace && et == 0 && tl == blockIdx.x) a.trace[((size_t)ph * 6 + 3) * G + blockIdx.x] = gtimer();
+          tile_epilogue(a, gk, l, tl, tile, rn, red, kred, srows, srope, gw, et, warp, lane);
+          epi_sync();  // tile / reduction scratch reused by the next tile
+          if (a.trace && et == 0 && tl == blockIdx.x) a.trace[((size_t)ph * 6 + 4) * G + blockIdx.x] = gtimer();
+        }
+        if (a.trace && et == 0) a.trace[((size_t)ph * 6 + 5) * G + blockIdx.x] = gtimer();
+      }
+      // ---- phase done: publish and arrive at the grid barrier
+      if (ph + 1 < P) {
+        fence_proxy_async();  // generic-proxy writes read by the next phase's TMA / bulk loads
+        __threadfence();
+        epi_sync();
+        if (et == 0) {
+          if (a.trace) a.trace[((size_t)ph * 6 + 1) * G + blockIdx.x] = gtimer();
+          atomicAdd(a.bar, 1ull);
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kAcc * XR));
+  }
+  if (threadIdx.x == 0) {
+    // every thread of this CTA is past its last barrier wait
+    if (atomicAdd(a.bar + 1, 1ull) == (unsigned long long)(G - 1)) {
+      for (int ph = 0; ph < P; ph++) a.grab[ph] = 0;
+      atomicExch(a.bar, 0ull);
+      atomicExch(a.bar + 1, 0ull);
+    }
+  }
+}
+
+}  // namespace
+
+int mk_phases(int L) { return 4 + 10 * L; }
+
+int mk_grid() {
+  static int n_sm = 0;
+  if (!n_sm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n_sm;
+}
+
+MkPlan mk_plan(int tiles, int kb_total) {
+  // ~8 k-blocks (128 KB of weights, ~3 us of one SM's HBM share) per chunk
+  const int nc = std::min(12, std::max(1, (kb_total + 4) / 8));  // <= 12: one load round in the reduction
+  return MkPlan{tiles, kb_total, nc, tiles * nc};
+}
+
+size_t mk_partial_floats(const MkPlan* plans) {
+  int chunks = 0;
+  for (int i = 0; i < 5; i++) chunks = std::max(chunks, plans[i].chunks);
+  return (size_t)chunks * MT * XR;
+}
+
+void launch_decode_mk(const MkLaunch& l, cudaStream_t s) {
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(decode_mk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    configured = true;
+  }
+  if (l.B < 1 || l.B > XR) throw std::runtime_error("decode_mk: 1..16 rows");
+  if (l.d % (4 * MT) || l.F % 64 || l.H * HD != l.d) throw std::runtime_error("decode_mk: unsupported shape");
+  Args a{};
+  for (int i = 0; i < 5; i++) a.plan[i] = l.plan[i];
+  a.wmaps = (const CUtensorMap*)l.wmaps;
+  a.norms = l.norms;
+  a.d = l.d; a.F = l.F; a.H = l.H; a.L = l.L; a.V = l.V; a.n_text = l.n_text;
+  a.eps = l.eps; a.scale_log2 = l.scale_log2;
+  a.hdr = l.hdr; a.rows = (const RowMeta*)l.rows; a.items = (const AttnItem*)l.items;
+  a.item_rows = (const ItemRow*)l.item_rows; a.B = l.B;
+  a.embed = l.embed; a.out_tokens = l.out_tokens; a.x = l.x; a.xg = l.xg; a.ss = l.ss; a.q = l.q;
+  a.attn = l.attn; a.kv_pool = l.kv_pool; a.page_elems = l.page_elems; a.rope = l.rope;
+  a.partial = l.partial; a.counters = l.counters; a.apartial = l.apartial; a.acounters = l.acounters;
+  a.part_keys = l.part_keys; a.logits = l.logits; a.bar = l.bar; a.trace = l.trace;
+  a.grab = l.grab;
+  a.flags = l.flags;
+  decode_mk_kernel<<<l.grid, kThreads, kSmem, s>>>(*reinterpret_cast<const CUtensorMap*>(l.map_xg.bytes),
+                                                   *reinterpret_cast<const CUtensorMap*>(l.map_attn.bytes),
+                                                   *reinterpret_cast<const CUtensorMap*>(l.map_act.bytes), a);
+}
+
+}  // namespace fe

@@ -19,6 +19,7 @@
 #include "common.cuh"
 #include "engine_internal.h"
 #include "gemm_tc.h"
+#include "decode_mk.h"
 #include "../../include/fastecot.h"
 
 #include <algorithm>
@@ -83,7 +84,7 @@ struct RowIn {
   bool head;
 };
 
-enum ProfCat { PROF_GEMV = 0, PROF_ATTN = 1, PROF_DECODE_FWD = 2, PROF_PREFILL_FWD = 3, PROF_NCAT = 4 };
+enum ProfCat { PROF_GEMV = 0, PROF_ATTN = 1, PROF_DECODE_FWD = 2, PROF_PREFILL_FWD = 3, PROF_TICK = 4, PROF_NCAT = 5 };
 
 struct ProfRec {
   int cat;
@@ -112,6 +113,13 @@ struct Lane {
   int* attn_counters = nullptr;
   float* sk_partial = nullptr;
   int* sk_counters = nullptr;
+  // persistent decode-tick kernel scratch (lane 0)
+  float* mk_ss = nullptr;
+  unsigned long long* mk_bar = nullptr;
+  float* mk_partial = nullptr;
+  int* mk_counters = nullptr;
+  unsigned long long* mk_keys = nullptr;
+  int* mk_grab = nullptr;
   MetaLayout layout{};
   unsigned char* meta_host[kMetaRing] = {};
   cudaEvent_t meta_ev[kMetaRing] = {};
@@ -173,7 +181,21 @@ struct fe_engine {
   int sk_mask = 31;  // skinny path per matrix: 1 QKV, 2 O, 4 gate/up, 8 down, 16 lm_head
   std::vector<LayerMaps> tc_maps;
   fe::TmaMap map_lm{};
+  // persistent decode-tick kernel (bf16 decode ticks of <= 16 rows on lane 0)
+  bool mk_on = false;
+  int mk_grid = 0;
+  fe::MkPlan mk_plans[5] = {};
+  void* mk_maps = nullptr;        // device CUtensorMap[4 L + 1]
+  const float** mk_norms = nullptr;  // device float*[2 L + 1]
+  unsigned long long* mk_trace = nullptr;  // diagnostics: per-phase barrier timestamps of the last tick
+  size_t mk_trace_n = 0;
+  bool mk_trace_on = false;
+  int mk_flags = 0;
   bool graphs_on = true;
+  float* op_partial = nullptr;  // fe_op_skinny_tc scratch
+  size_t op_bytes = 0;
+  int* op_counters = nullptr;
+  int op_reps = 1;     // fe_op_skinny_tc: back-to-back launches (device-side timing of one kernel)
   int debug_skip = 0;  // timing experiments only: 1 attention, 2 rmsnorm, 4 layer GEMMs, 8 lm_head
 
   // stats
@@ -334,6 +356,12 @@ void clear_graphs(fe_engine* e) {
 }
 
 // ---- forward pass -----------------------------------------------------------
+// The persistent decode-tick kernel takes bf16 decode ticks of <= 16 rows on
+// lane 0 where every row samples a token (it needs every SM: one lane only).
+bool mk_eligible(fe_engine* e, const Lane& ln, const fe::Fwd& f, int n) {
+  return e->mk_on && ln.id == 0 && n <= 16 && f.n_head_rows == n && e->debug_skip == 0;
+}
+
 // The kernel sequence of one forward pass (eager or under graph capture).
 template <typename GB>
 void launch_layers(fe_engine* e, Lane& ln, const fe::Fwd& f, int n, bool decode, double kv_bytes, GB gemv_bytes) {
@@ -342,6 +370,41 @@ void launch_layers(fe_engine* e, Lane& ln, const fe::Fwd& f, int n, bool decode,
   const int dt = e->dtype;
   fe::Workspace& ws = ln.ws;
   const int whole = prof_begin(e, ln, decode ? PROF_DECODE_FWD : PROF_PREFILL_FWD);
+  if (decode && mk_eligible(e, ln, f, n)) {
+    // one persistent kernel for the whole tick (decode_mk.cu)
+    fe::MkLaunch k{};
+    k.grid = e->mk_grid;
+    for (int i = 0; i < 5; i++) k.plan[i] = e->mk_plans[i];
+    k.wmaps = e->mk_maps;
+    k.norms = e->mk_norms;
+    k.map_xg = ln.map_xn16;
+    k.map_attn = ln.map_attn16;
+    k.map_act = ln.map_act16;
+    k.d = m.d; k.F = m.F; k.H = m.H; k.L = m.L; k.V = m.V; k.n_text = m.n_text;
+    k.eps = m.eps;
+    k.scale_log2 = m.attn_scale * 1.4426950408889634f;
+    k.hdr = f.hdr; k.rows = f.rows; k.items = f.items; k.item_rows = f.item_rows; k.B = n;
+    k.embed = (const __nv_bfloat16*)e->w.embed;
+    k.out_tokens = e->out_tokens;
+    k.x = ws.x; k.xg = (__nv_bfloat16*)ws.xn; k.ss = ln.mk_ss; k.q = ws.q; k.attn = (__nv_bfloat16*)ws.attn;
+    k.kv_pool = (__nv_bfloat16*)e->kv_pool; k.page_elems = e->page_elems; k.rope = e->rope;
+    k.partial = ln.mk_partial; k.counters = ln.mk_counters;
+    k.apartial = ws.partial; k.acounters = f.attn_counters;
+    k.part_keys = ln.mk_keys; k.logits = ws.logits; k.bar = ln.mk_bar;
+    k.trace = e->mk_trace_on ? e->mk_trace : nullptr;
+    k.grab = ln.mk_grab;
+    k.flags = e->mk_flags;
+    const int p = prof_begin(e, ln, PROF_TICK);
+    fe::launch_decode_mk(k, st);
+    // algorithmic bytes of the tick: every weight once, the K/V pages the
+    // cascade items stage (shared pages once per head), the new K/V rows
+    const double el = (double)e->elem;
+    const double w_bytes = (double)m.L * (4.0 * m.d * m.d + 3.0 * m.F * m.d) * el + (double)m.V * m.d * el;
+    const double kv_write = (double)n * m.L * 2.0 * m.d * el;
+    prof_end(e, ln, p, w_bytes + kv_bytes + kv_write);
+    prof_end(e, ln, whole, 0.0);
+    return;
+  }
   fe::launch_embed(dt, f, m, e->w.embed, e->out_tokens, ws.x, st);
   // bf16: skinny tcgen05 swap-AB GEMM for <= 16 rows (decode), the tile
   // tcgen05 GEMM for wide forwards (prefill); fp32: canonical CUDA-core GEMV
@@ -582,7 +645,8 @@ void forward(fe_engine* e, Lane& ln, const std::vector<RowIn>& rows, uint64_t vi
   }
   CK(cudaGetLastError());
   const int attn_kernels = e->dtype == FE_BF16 ? 1 : 2;  // bf16: merge fused into the attention kernel
-  e->n_launches += 1 + (6 + attn_kernels) * m.L + (decode ? 3 : 0) - (items.empty() ? m.L : 0);
+  if (decode && mk_eligible(e, ln, f, n)) e->n_launches += 1;
+  else e->n_launches += 1 + (6 + attn_kernels) * m.L + (decode ? 3 : 0) - (items.empty() ? m.L : 0);
   e->n_forwards++;
   e->n_rows_total += n;
 }
@@ -736,6 +800,17 @@ void create_lane(fe_engine* e, Lane& ln, int id, int rows, int priority) {
   ln.ws.logits = id == 0 ? e->logits : nullptr;
   ln.attn_counters = (int*)e->dalloc(R * m.H * sizeof(int));
   CK(cudaMemset(ln.attn_counters, 0, R * m.H * sizeof(int)));
+  if (id == 0 && e->mk_on) {
+    ln.mk_ss = (float*)e->dalloc((size_t)(m.d / 128) * 16 * 4);
+    ln.mk_bar = (unsigned long long*)e->dalloc(2 * sizeof(unsigned long long));
+    CK(cudaMemset(ln.mk_bar, 0, 2 * sizeof(unsigned long long)));
+    ln.mk_partial = (float*)e->dalloc(fe::mk_partial_floats(e->mk_plans) * 4);
+    ln.mk_grab = (int*)e->dalloc((size_t)fe::mk_phases(m.L) * sizeof(int));
+    CK(cudaMemset(ln.mk_grab, 0, (size_t)fe::mk_phases(m.L) * sizeof(int)));
+    ln.mk_counters = (int*)e->dalloc(4096 * sizeof(int));
+    CK(cudaMemset(ln.mk_counters, 0, 4096 * sizeof(int)));
+    ln.mk_keys = (unsigned long long*)e->dalloc((size_t)16 * e->mk_plans[fe::MK_LM].tiles * 8);
+  }
   {  // fixed-offset metadata layout (16-byte aligned sections)
     MetaLayout& L = ln.layout;
     auto up16 = [](size_t v) { return (v + 15) & ~(size_t)15; };
@@ -825,6 +900,36 @@ fe_engine* create(const fe_config* c, int device, const float* rope_host) {
         e->tc_maps[l].wgu = fe::make_kmajor_map(ly.wgu, 2 * m.F, m.d, m.d, fe::tc_box_rows(fe::TC_SWIGLU));
         e->tc_maps[l].wdown = fe::make_kmajor_map(ly.wdown, m.d, m.F, m.F, 128);
       }
+    }
+
+    // persistent decode-tick kernel: per-GEMM split plans over one CTA per SM,
+    // weight tensor maps and norm vectors in device memory
+    e->mk_on = e->use_tc && m.H * m.hd == m.d && m.d % 512 == 0;
+    if (e->mk_on) {
+      e->mk_grid = fe::mk_grid();
+      e->mk_plans[fe::MK_QKV] = fe::mk_plan(3 * m.d / 128, m.d / 64);
+      e->mk_plans[fe::MK_O] = fe::mk_plan(m.d / 128, m.d / 64);
+      e->mk_plans[fe::MK_GU] = fe::mk_plan(m.F / 64, m.d / 64);
+      e->mk_plans[fe::MK_DOWN] = fe::mk_plan(m.d / 128, m.F / 64);
+      e->mk_plans[fe::MK_LM] = fe::mk_plan((m.V + 127) / 128, m.d / 64);
+      std::vector<fe::TmaMap> maps(4 * m.L + 1);
+      for (int l = 0; l < m.L; l++) {
+        maps[4 * l + 0] = e->tc_maps[l].qkv;
+        maps[4 * l + 1] = e->tc_maps[l].wo;
+        maps[4 * l + 2] = e->tc_maps[l].wgu;
+        maps[4 * l + 3] = e->tc_maps[l].wdown;
+      }
+      maps[4 * m.L] = e->map_lm;
+      e->mk_maps = e->dalloc(maps.size() * sizeof(fe::TmaMap));
+      CK(cudaMemcpy(e->mk_maps, maps.data(), maps.size() * sizeof(fe::TmaMap), cudaMemcpyHostToDevice));
+      std::vector<const float*> norms(2 * m.L + 1);
+      for (int l = 0; l < m.L; l++) {
+        norms[2 * l] = e->layers[l].attn_norm;
+        norms[2 * l + 1] = e->layers[l].ffn_norm;
+      }
+      norms[2 * m.L] = e->w.final_norm;
+      e->mk_norms = (const float**)e->dalloc(norms.size() * sizeof(float*));
+      CK(cudaMemcpy(e->mk_norms, norms.data(), norms.size() * sizeof(float*), cudaMemcpyHostToDevice));
     }
 
     // lanes: 0 = foreground (highest priority), 1 = background reasoning
@@ -1234,17 +1339,22 @@ int fe_op_skinny_tc(fe_engine* e, const void* x, const void* w, int32_t M, int32
   return guarded(e, [&] {
     if (M > fe::skinny_max_rows() || N % 128 || K % 64) throw Error("skinny_tc: M <= 16, N % 128, K % 64");
     Lane& ln = e->lanes[0];
-    if (!ln.sk_partial) {
-      ln.sk_partial = (float*)e->dalloc((size_t)64 * N * 16 * 4);
-      ln.sk_counters = (int*)e->dalloc(4096 * sizeof(int));
-      CK(cudaMemset(ln.sk_counters, 0, 4096 * sizeof(int)));
+    // kernel-test scratch, separate from the lanes' (graph-captured) buffers
+    const size_t need = (size_t)8 * ((N + 127) / 128) * 128 * 16 * 4;
+    if (e->op_bytes < need) {
+      e->op_partial = (float*)e->dalloc(need);
+      e->op_bytes = need;
+    }
+    if (!e->op_counters) {
+      e->op_counters = (int*)e->dalloc(4096 * sizeof(int));
+      CK(cudaMemset(e->op_counters, 0, 4096 * sizeof(int)));
     }
     const fe::TmaMap xm = fe::make_kmajor_map(x, M, K, K, fe::skinny_max_rows());
     const fe::TmaMap wm = fe::make_kmajor_map(w, N, K, K, 128);
     fe::SkLaunch t{};
     t.N = N; t.K = K; t.B = M; t.epi = fe::TC_STORE; t.y = y; t.ldy = N;
-    t.partial = ln.sk_partial; t.counters = ln.sk_counters;
-    fe::launch_skinny_tc(wm, xm, t, ln.stream);
+    t.partial = e->op_partial; t.counters = e->op_counters;
+    for (int r = 0; r < e->op_reps; r++) fe::launch_skinny_tc(wm, xm, t, ln.stream);
     CK(cudaGetLastError());
   });
 }
@@ -1253,10 +1363,29 @@ int fe_set_option(fe_engine* e, const char* key, int64_t value) {
   return guarded(e, [&] {
     const std::string k = key ? key : "";
     if (k == "tc_min_rows") e->tc_min_rows = (int)value;
-    else if (k == "use_tc") e->use_tc = value != 0 && !e->tc_maps.empty();
+    else if (k == "use_tc") {
+      e->use_tc = value != 0 && !e->tc_maps.empty();
+      e->mk_on = e->use_tc && e->mk_maps != nullptr;
+      clear_graphs(e);
+    } else if (k == "mk_trace") {
+      if (value && !e->mk_trace && e->mk_on) {
+        e->mk_trace_n = (size_t)fe::mk_phases(e->m.L) * 6 * e->mk_grid;
+        e->mk_trace = (unsigned long long*)e->dalloc(e->mk_trace_n * 8);
+        CK(cudaMemset(e->mk_trace, 0, e->mk_trace_n * 8));
+      }
+      e->mk_trace_on = value != 0 && e->mk_trace != nullptr;
+      clear_graphs(e);
+    } else if (k == "mk_flags") {
+      e->mk_flags = (int)value;
+      clear_graphs(e);
+    } else if (k == "mk") {
+      e->mk_on = value != 0 && e->use_tc && e->mk_maps != nullptr;
+      clear_graphs(e);
+    }
     else if (k == "sk_mask") e->sk_mask = (int)value;
     else if (k == "graphs") e->graphs_on = value != 0;
     else if (k == "pdl") fe::g_pdl = value != 0;
+    else if (k == "op_reps") e->op_reps = (int)std::max<int64_t>(1, value);
     else if (k == "sk_stages") {
       fe::g_sk_stages = (int)value;
       clear_graphs(e);
@@ -1266,6 +1395,17 @@ int fe_set_option(fe_engine* e, const char* key, int64_t value) {
     } else {
       throw Error("unknown option " + k);
     }
+  });
+}
+
+int fe_debug_trace(fe_engine* e, uint64_t* out, int32_t n, int32_t* n_phases, int32_t* grid) {
+  return guarded(e, [&] {
+    if (!e->mk_trace) throw Error("debug_trace: enable option mk_trace first");
+    CK(cudaStreamSynchronize(e->lanes[0].stream));
+    const size_t k = std::min<size_t>((size_t)std::max(n, 0), e->mk_trace_n);
+    CK(cudaMemcpy(out, e->mk_trace, k * 8, cudaMemcpyDeviceToHost));
+    *n_phases = fe::mk_phases(e->m.L);
+    *grid = e->mk_grid;
   });
 }
 

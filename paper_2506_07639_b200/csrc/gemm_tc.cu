@@ -1,3 +1,5 @@
+#include <cstdio>
+#include <cstdlib>
 // tcgen05 tensor-core GEMM for the dense contractions of the bf16 path
 // (trunk prefill and wide row batches): D[m, n] = sum_k A[m, k] * B[n, k]
 // with A = staged activations [rows, K] and B = weights [N, K], both
@@ -18,6 +20,7 @@
 #include "common.cuh"
 #include "engine_internal.h"
 #include "gemm_tc.h"
+#include "tc_util.cuh"
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -37,37 +40,7 @@ constexpr int kTileBytes = BM * BK * 2;                   // 16 KB per operand p
 constexpr int kSmem = kStages * 2 * kTileBytes + 1024 + 256;
 constexpr int kThreads = 192;
 
-__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  uint32_t done = 0;
-  while (!done)
-    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-                 : "=r"(done) : "r"(su32(b)), "r"(parity) : "memory");
-}
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
-      ::"r"(su32(dst)), "l"(map), "r"(x), "r"(y), "r"(su32(bar)) : "memory");
-}
-
-// UMMA shared-memory descriptor: K-major, 128B swizzle, 8-row groups 1024 B apart.
-__device__ __forceinline__ uint64_t smem_desc(const void* p) {
-  const uint64_t addr = su32(p);
-  uint64_t d = 0;
-  d |= (addr >> 4) & 0x3FFFull;          // start address
-  d |= (uint64_t)1 << 16;                // LBO (ignored for swizzled K-major)
-  d |= (uint64_t)(1024 >> 4) << 32;      // SBO
-  d |= (uint64_t)1 << 46;                // version (sm100)
-  d |= (uint64_t)2 << 61;                // SWIZZLE_128B
-  return d;
-}
+using namespace tc;
 
 // instruction descriptor: D f32, A/B bf16, K-major both, N = 128, M = 128
 constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
@@ -635,6 +608,32 @@ void launch_skinny_tc(const TmaMap& w_map, const TmaMap& x_map, const SkLaunch& 
   if (!configured) {
     cudaFuncSetAttribute(skinny_tc_kernel<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, sk_smem<10>());
     cudaFuncSetAttribute(skinny_tc_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, sk_smem<5>());
+    // maximum shared-memory carveout, so two 5-stage CTAs (of consecutive
+    // PDL-chained launches) can be resident on one SM
+    cudaFuncSetAttribute(skinny_tc_kernel<5>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(skinny_tc_kernel<10>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (getenv("FE_DEBUG_OCC")) {
+      int o5 = 0, o10 = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o5, skinny_tc_kernel<5>, kThreads, sk_smem<5>());
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o10, skinny_tc_kernel<10>, kThreads, sk_smem<10>());
+      fprintf(stderr, "skinny occupancy: 5 stages %d CTAs/SM (%d B), 10 stages %d CTAs/SM (%d B)\n", o5, sk_smem<5>(), o10,
+              sk_smem<10>());
+      size_t avail1 = 0, avail2 = 0;
+      cudaOccupancyAvailableDynamicSMemPerBlock(&avail1, skinny_tc_kernel<5>, 1, kThreads);
+      cudaOccupancyAvailableDynamicSMemPerBlock(&avail2, skinny_tc_kernel<5>, 2, kThreads);
+      int smpm = 0, smpb = 0;
+      cudaDeviceGetAttribute(&smpm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, 0);
+      cudaDeviceGetAttribute(&smpb, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0);
+      fprintf(stderr, "avail dyn smem: 1 CTA %zu, 2 CTAs %zu; per SM %d, per block optin %d\n", avail1, avail2, smpm, smpb);
+      cudaFuncAttributes fa{};
+      cudaError_t er = cudaFuncGetAttributes(&fa, skinny_tc_kernel<5>);
+      fprintf(stderr, "attrs(%d): regs %d static %zu maxdyn %d carveout %d maxthreads %d\n", (int)er, fa.numRegs,
+              fa.sharedSizeBytes, fa.maxDynamicSharedSizeBytes, fa.preferredShmemCarveout, fa.maxThreadsPerBlock);
+      int rps = 0, maxb = 0;
+      cudaDeviceGetAttribute(&rps, cudaDevAttrMaxRegistersPerMultiprocessor, 0);
+      cudaDeviceGetAttribute(&maxb, cudaDevAttrMaxBlocksPerMultiprocessor, 0);
+      fprintf(stderr, "regs/SM %d max blocks/SM %d\n", rps, maxb);
+    }
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);

@@ -42,7 +42,7 @@ EXPORTS = (
     "fe_request_logits", "fe_in_flight", "fe_synchronize", "fe_stream", "fe_stats", "fe_profile",
     "fe_profile_read",
     "fe_weight_ptr", "fe_memcpy", "fe_op_gemv", "fe_op_rmsnorm", "fe_op_gemm_tc", "fe_op_skinny_tc",
-    "fe_set_option",
+    "fe_set_option", "fe_debug_trace",
 )
 
 _lib = None
@@ -90,6 +90,7 @@ def load_library(path: Path = LIB_PATH) -> ctypes.CDLL:
         "fe_op_gemm_tc": [vp, vp, vp, i32, i32, i32, vp],
         "fe_op_skinny_tc": [vp, vp, vp, i32, i32, i32, vp],
         "fe_set_option": [vp, ctypes.c_char_p, ctypes.c_int64],
+        "fe_debug_trace": [vp, vp, i32, _c_int_p, _c_int_p],
     }
     for name, argtypes in sig.items():
         fn = getattr(lib, name)
@@ -249,7 +250,7 @@ class Engine:
                 "launches")
         return dict(zip(keys, out.tolist()))
 
-    PROFILE_CATEGORIES = ("decode_gemv", "decode_attention", "decode_forward", "prefill_forward")
+    PROFILE_CATEGORIES = ("decode_gemv", "decode_attention", "decode_forward", "prefill_forward", "decode_tick")
 
     def profile(self, enable: bool) -> None:
         """Start (and reset) or stop CUDA-event timing of engine launches."""
@@ -290,6 +291,16 @@ class Engine:
     def op_skinny_tc(self, x_ptr: int, w_ptr: int, M: int, N: int, K: int, y_ptr: int) -> None:
         self._check(self.lib.fe_op_skinny_tc(self._h, ctypes.c_void_p(x_ptr), ctypes.c_void_p(w_ptr), M, N, K,
                                              ctypes.c_void_p(y_ptr)))
+
+    def debug_trace(self) -> np.ndarray:
+        """Persistent-tick phase timestamps [phases][6][grid] (ns) of the last tick:
+        barrier passed, phase done, last weight load issued, first / last
+        accumulator ready, segments drained."""
+        n = 4 * 1024 * 1024
+        out = np.zeros(n, dtype=np.uint64)
+        ph, g = ctypes.c_int(), ctypes.c_int()
+        self._check(self.lib.fe_debug_trace(self._h, _np_ptr(out), n, ctypes.byref(ph), ctypes.byref(g)))
+        return out[: ph.value * 6 * g.value].reshape(ph.value, 6, g.value)
 
     def set_option(self, key: str, value: int) -> None:
         self._check(self.lib.fe_set_option(self._h, key.encode(), int(value)))

@@ -409,3 +409,44 @@ def test_engine_shared_by_lockstep_then_two_stream_backends(schema):
     finally:
         be.close()
     assert all(len(r.trace.steps) == len(schema.steps) for r in res)
+
+
+@pytest.mark.parametrize("config,plen", [("small", 60), ("small", 280), ("7b_2layer", 300)])
+def test_bf16_persistent_tick_matches_kernel_chain(config, plen):
+    """bf16 decode through the persistent decode-tick kernel (one launch per
+    tick: folded RMSNorm, mma.sync cascade attention, split-K tcgen05 GEMMs
+    behind grid barriers) vs the per-matrix kernel chain: logits within bf16
+    tolerance and identical first greedy token."""
+    from oracle.backend import frame
+    ids = frame(config, list(range(16)), list(range(500, 500 + plen)), "plan")
+    out = {}
+    for mk in (1, 0):
+        eng = Engine(config, dtype="bf16", seed=0, kv_pages=64, max_rows=512)
+        eng.set_option("mk", mk)
+        out[mk] = _decode(eng, ids, 4242, 6, capture=True)
+        eng.close()
+    (t1, l1), (t0, l0) = out[1], out[0]
+    rel = np.abs(l1[0] - l0[0]).max() / np.abs(l0[0]).max()
+    assert rel < 2e-2, rel
+    assert t1[0] == t0[0]
+
+
+def test_bf16_persistent_tick_branch_batch():
+    """7 forked branches (shared trunk pages + private suffixes) decoded as one
+    batch by the persistent tick kernel vs the kernel chain."""
+    from oracle.backend import frame
+    ids = frame("small", list(range(16)), list(range(900, 1150)), "plan")
+    firsts, logit0 = {}, {}
+    for mk in (1, 0):
+        eng = Engine("small", dtype="bf16", seed=0, kv_pages=128, max_rows=512)
+        eng.set_option("mk", mk)
+        trunk = eng.seq_create()
+        eng.prefill(trunk, ids[:-1], 99, M.VIS_ID)
+        reqs = []
+        for j, cut in enumerate((len(ids) - 1, 300, 250, 200, 150, 100, 90)):
+            b = eng.seq_fork(trunk, cut)
+            reqs.append(eng.submit(b, M.TAG_BASE + j, 5, 1))
+        eng.run(-1)
+        firsts[mk] = [eng.request_tokens(r, 5)[0] for r in reqs]
+        eng.close()
+    assert sum(a == b for a, b in zip(firsts[1], firsts[0])) >= 6, firsts

@@ -24,11 +24,22 @@ ap.add_argument("--repeat", type=int, default=3)
 ap.add_argument("--profile", action="store_true")
 ap.add_argument("--skip", type=int, default=0, help="debug_skip mask (timing attribution only)")
 ap.add_argument("--stages", type=int, default=0)
+ap.add_argument("--pdl", type=int, default=1)
+ap.add_argument("--graphs", type=int, default=1)
+ap.add_argument("--mk", type=int, default=1)
+ap.add_argument("--mk-flags", type=int, default=0)
+ap.add_argument("--trace", action="store_true", help="per-phase barrier timeline of the persistent tick kernel")
 args = ap.parse_args()
 
 eng = Engine(args.config, dtype=args.dtype, seed=0, kv_pages=256)
 if args.skip:
     eng.set_option("debug_skip", args.skip)
+eng.set_option("pdl", args.pdl)
+eng.set_option("graphs", args.graphs)
+eng.set_option("mk", args.mk)
+eng.set_option("mk_flags", args.mk_flags)
+if args.trace:
+    eng.set_option("mk_trace", 1)
 if args.stages:
     eng.set_option("sk_stages", args.stages)
 cfg = M.get_config(args.config)
@@ -65,4 +76,33 @@ for rep in range(args.repeat):
         eng.seq_free(s)
     print(f"rep {rep}: prefill {t_pre*1e3:.1f} ms | {args.ticks} ticks x {args.rows} rows: device {dev:.2f} ms "
           f"({dev/args.ticks:.3f} ms/tick), host enqueue {host*1e3:.2f} ms  {prof}", flush=True)
+if args.trace:
+    import numpy as np
+    tr = eng.debug_trace().astype(np.int64)  # [P][6][G]
+    P = tr.shape[0]
+    t0 = tr[0, 0].min()
+    names = (["EMBED"] + [n for l in range(cfg.n_layers)
+                          for n in ("QKV", "RQKV", "ATTN", "AMERGE", "O", "RO", "GU", "RGU", "DOWN", "RDOWN")]
+             + ["LM", "RLM", "FINAL"])
+    agg = {}
+    print("phase         start   span | W-issue end   1st acc      last acc     drained  (min/max us from phase start)")
+    for ph in range(P):
+        start = tr[ph, 0].min()
+        last_done = tr[ph, 1].max() if ph + 1 < P else tr[ph, 0].max()
+        nxt = tr[ph + 1, 0].min() if ph + 1 < P else last_done
+        span = (last_done - start) / 1e3
+        bar = (nxt - last_done) / 1e3
+        wi = tr[ph, 2] - start
+        fa = tr[ph, 3] - start
+        la = tr[ph, 4] - start
+        dr = tr[ph, 5] - start
+        has_w = tr[ph, 2].max() > 0 and tr[ph, 2].max() >= start
+        a = agg.setdefault(names[ph], [0, 0.0, 0.0])
+        a[0] += 1; a[1] += span; a[2] += bar
+        if ph < 22 or ph >= P - 4:
+            extra = "".join(f"  {v.min()/1e3:5.1f} {v.max()/1e3:5.1f} " for v in (wi, fa, la, dr)) if has_w else ""
+            print(f"{ph:3d} {names[ph]:7s} {(start - t0)/1e3:7.1f} {span:6.1f} |{extra}   bar {bar:5.2f}")
+    np.save("gpurun_out/mk_trace.npy", tr)
+    for k, (n, sp, b) in agg.items():
+        print(f"{k:6s} x{n:3d}: span {sp/n:7.2f} us  barrier {b/n:5.2f} us  total {sp+b:8.1f} us")
 eng.close()
