@@ -19,7 +19,7 @@ OUT = PKG / "_build" / "libfastecot.so"
 SOURCES = ["kernels.cu", "gemm_tc.cu", "decode_mk.cu", "engine.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "--fmad=false", "-std=c++17",
-         "-Xcompiler", "-fPIC", "-shared", "-diag-suppress", "1886"]
+         "-Xcompiler", "-fPIC", "-shared", "-diag-suppress", "1886,177"]
 
 
 def needs_build() -> bool:

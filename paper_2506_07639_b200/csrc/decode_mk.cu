@@ -68,7 +68,9 @@ constexpr uint32_t kIdesc = idesc_bf16(MT, XR);
 // attention phase: the (idle) ring holds K and V of up to 6 (page, head) pairs
 constexpr int kAttnSlotBytes = 2 * FE_PAGE * HD * 2;  // 32 KB
 constexpr int kAttnSlots = kStages * (kWBytes + kXBytes) / kAttnSlotBytes;
-constexpr int kMaxPairs = kAttnSlots;  // (page, head) pairs per CTA whose items are cached in smem
+constexpr int kMaxPairs = kAttnSlots;
+constexpr int kPartStride = HD + 4;  // attention chunk partial record: m, l, pad, pad, o[HD] (16-byte aligned)
+constexpr int kStgStride = HD + 4;   // o staging rows in shared memory  // (page, head) pairs per CTA whose items are cached in smem
 constexpr int kSmem = kStages * (kWBytes + kXBytes) + MT * (XR + 1) * 4 + XR * HD * 4 /* rope */ + 1024 /* align */ +
                       4096 /* barriers, scratch, rows, items */;
 static_assert(kAttnSlots >= 4, "attention staging needs >= 4 slots");
@@ -189,20 +191,18 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 // ---- epilogue-group (warps 2-5) helpers
 __device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
-// sum over the 128 epilogue threads of v[b] (b < B) -> out[b] (fixed order)
-__device__ __forceinline__ void epi_sum16(float (&v)[XR], int B, float* red /*[4][16]*/, float* out, int ostride,
-                                          int et) {
-  const int w = et >> 5, lane = et & 31;
-#pragma unroll
-  for (int b = 0; b < XR; b++) {
-    if (b >= B) break;
-    float s = v[b];
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    if (lane == 0) red[w * XR + b] = s;
+// out[b * ostride] = sum over the 128 tile rows of tile[c][b]^2 (b < B), fixed
+// order; the caller has synchronised the epilogue group after writing `tile`
+__device__ __forceinline__ void epi_sumsq_cols(const float* tile, int B, float* out, int ostride, int et) {
+  if (et < B) {
+    float acc = 0.0f;
+#pragma unroll 8
+    for (int c = 0; c < MT; c++) {
+      const float v = tile[c * (XR + 1) + et];
+      acc = fmaf(v, v, acc);
+    }
+    out[et * ostride] = acc;
   }
-  epi_sync();
-  if (et < B) out[et * ostride] = (red[et] + red[XR + et]) + (red[2 * XR + et] + red[3 * XR + et]);
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
@@ -255,7 +255,8 @@ __device__ __forceinline__ void attn_load_q(const Args& a, const AttnItem& it, c
 
 __device__ void attn_pair(const Args& a, const RowMeta* srows, const AttnItem& it, const ItemRow* irows, int h,
                           const unsigned char* ks, const unsigned char* vs, const uint4 (&q0)[4],
-                          const uint4 (&q1)[4], int lane) {
+                          const uint4 (&q1)[4], int lane, unsigned long long* dbg = nullptr) {
+  if (dbg) { uint64_t t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t) :: "memory"); dbg[0] = t; }
   const int g = lane >> 2, t = lane & 3;
   const int H = a.H;
   const int nr = it.row_count;
@@ -276,158 +277,192 @@ __device__ void attn_pair(const Args& a, const RowMeta* srows, const AttnItem& i
     qa[2 * i + 1][2] = q0[i].w;
     qa[2 * i + 1][3] = q1[i].w;
   }
+  // S = Q K^T: k-step outer, the 8 key tiles inner (8 independent MMA chains)
   float s[8][4];
 #pragma unroll
-  for (int nt = 0; nt < 8; nt++) {
-    s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.0f;
-    if (8 * nt >= vmax) continue;
-    const uint4* kr = reinterpret_cast<const uint4*>(ks + (size_t)(8 * nt + g) * HD * 2 + 16 * t);
+  for (int nt = 0; nt < 8; nt++) s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.0f;
 #pragma unroll
-    for (int i = 0; i < 4; i++) {
-      const uint4 kv = kr[4 * i];  // dims 32i + 8t .. +7
-      mma_bf16(s[nt], qa[2 * i], kv.x, kv.y);
-      mma_bf16(s[nt], qa[2 * i + 1], kv.z, kv.w);
-    }
+  for (int i = 0; i < 4; i++) {
+    uint4 kv[8];
+#pragma unroll
+    for (int nt = 0; nt < 8; nt++)  // key 8nt + g (swizzle key & 7 = g), dims 32i + 8t .. +7
+      kv[nt] = *reinterpret_cast<const uint4*>(ks + (size_t)(8 * nt + g) * HD * 2 + (((4 * i + t) ^ g) << 4));
+#pragma unroll
+    for (int nt = 0; nt < 8; nt++)
+      if (8 * nt < vmax) mma_bf16(s[nt], qa[2 * i], kv[nt].x, kv[nt].y);
+#pragma unroll
+    for (int nt = 0; nt < 8; nt++)
+      if (8 * nt < vmax) mma_bf16(s[nt], qa[2 * i + 1], kv[nt].z, kv[nt].w);
   }
-  // masked softmax (exp2 domain) per row; rows g (c0, c1) and g + 8 (c2, c3)
-  float m0 = -INFINITY, m1 = -INFINITY;
+  if (dbg) { uint64_t t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t) :: "memory"); dbg[1] = t + (s[0][0] == 1234.5f); }
+  // masked softmax (exp2 domain) per row; rows g (c0, c1) and g + 8 (c2, c3); tree reductions
 #pragma unroll
   for (int nt = 0; nt < 8; nt++) {
     const int j = 8 * nt + 2 * t;
-    if (j < v0) m0 = fmaxf(m0, s[nt][0]);
-    if (j + 1 < v0) m0 = fmaxf(m0, s[nt][1]);
-    if (j < v1) m1 = fmaxf(m1, s[nt][2]);
-    if (j + 1 < v1) m1 = fmaxf(m1, s[nt][3]);
+    s[nt][0] = j < v0 ? s[nt][0] : -INFINITY;
+    s[nt][1] = j + 1 < v0 ? s[nt][1] : -INFINITY;
+    s[nt][2] = j < v1 ? s[nt][2] : -INFINITY;
+    s[nt][3] = j + 1 < v1 ? s[nt][3] : -INFINITY;
   }
+  float mx0[8], mx1[8];
+#pragma unroll
+  for (int nt = 0; nt < 8; nt++) {
+    mx0[nt] = fmaxf(s[nt][0], s[nt][1]);
+    mx1[nt] = fmaxf(s[nt][2], s[nt][3]);
+  }
+#pragma unroll
+  for (int w2 = 4; w2 >= 1; w2 >>= 1)
+#pragma unroll
+    for (int nt = 0; nt < w2; nt++) {
+      mx0[nt] = fmaxf(mx0[nt], mx0[nt + w2]);
+      mx1[nt] = fmaxf(mx1[nt], mx1[nt + w2]);
+    }
+  float m0 = mx0[0], m1 = mx1[0];
   m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, 1));
-  m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, 2));
   m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, 1));
+  m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, 2));
   m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, 2));
   const float mu0 = v0 > 0 ? m0 : 0.0f, mu1 = v1 > 0 ? m1 : 0.0f;
-  float l0 = 0.0f, l1 = 0.0f;
+#pragma unroll
+  for (int nt = 0; nt < 8; nt++) {  // exp2(-inf) = 0 for the masked keys
+    s[nt][0] = exp2f(s[nt][0] - mu0);
+    s[nt][1] = exp2f(s[nt][1] - mu0);
+    s[nt][2] = exp2f(s[nt][2] - mu1);
+    s[nt][3] = exp2f(s[nt][3] - mu1);
+  }
+  float sm0[8], sm1[8];
 #pragma unroll
   for (int nt = 0; nt < 8; nt++) {
-    const int j = 8 * nt + 2 * t;
-    s[nt][0] = j < v0 ? exp2f(s[nt][0] - mu0) : 0.0f;
-    s[nt][1] = j + 1 < v0 ? exp2f(s[nt][1] - mu0) : 0.0f;
-    s[nt][2] = j < v1 ? exp2f(s[nt][2] - mu1) : 0.0f;
-    s[nt][3] = j + 1 < v1 ? exp2f(s[nt][3] - mu1) : 0.0f;
-    l0 += s[nt][0] + s[nt][1];
-    l1 += s[nt][2] + s[nt][3];
+    sm0[nt] = s[nt][0] + s[nt][1];
+    sm1[nt] = s[nt][2] + s[nt][3];
   }
+#pragma unroll
+  for (int w2 = 4; w2 >= 1; w2 >>= 1)
+#pragma unroll
+    for (int nt = 0; nt < w2; nt++) {
+      sm0[nt] += sm0[nt + w2];
+      sm1[nt] += sm1[nt + w2];
+    }
+  float l0 = sm0[0], l1 = sm1[0];
   l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
   l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
   l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
   l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
 
-  // O = P V over 16-key steps kk; output dim of (n-tile nt, column n) = 16 n + nt
-  float o[16][4];
-#pragma unroll
-  for (int nt = 0; nt < 16; nt++) o[nt][0] = o[nt][1] = o[nt][2] = o[nt][3] = 0.0f;
+  if (dbg) { uint64_t t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t) :: "memory"); dbg[2] = t + (s[0][0] == 1234.5f); }
+  // O = P V over 16-key steps kk; output dim of (n-tile nt, column n) = 16 n + nt.
+  // Two passes over the output n-tiles (8 each) keep the accumulators at 32 registers.
+  uint32_t pa[4][4];
 #pragma unroll
   for (int kk = 0; kk < 4; kk++) {
-    if (16 * kk >= vmax) break;
-    uint32_t pa[4];
-    pa[0] = pack_bf16(s[2 * kk][0], s[2 * kk][1]);
-    pa[1] = pack_bf16(s[2 * kk][2], s[2 * kk][3]);
-    pa[2] = pack_bf16(s[2 * kk + 1][0], s[2 * kk + 1][1]);
-    pa[3] = pack_bf16(s[2 * kk + 1][2], s[2 * kk + 1][3]);
-    // keys 16kk + 2t + {0, 1, 8, 9}, dims 16g .. 16g+15 (zero beyond the staged keys)
-    uint4 w[4][2];
-#pragma unroll
-    for (int c = 0; c < 4; c++) {
-      const int key = 16 * kk + 2 * t + (c & 1) + 8 * (c >> 1);
-      const uint4* vr = reinterpret_cast<const uint4*>(vs + (size_t)key * HD * 2 + 32 * g);
-      const bool ok = key < vmax;
-      w[c][0] = ok ? vr[0] : make_uint4(0u, 0u, 0u, 0u);
-      w[c][1] = ok ? vr[1] : make_uint4(0u, 0u, 0u, 0u);
+    pa[kk][0] = pack_bf16(s[2 * kk][0], s[2 * kk][1]);
+    pa[kk][1] = pack_bf16(s[2 * kk][2], s[2 * kk][3]);
+    pa[kk][2] = pack_bf16(s[2 * kk + 1][0], s[2 * kk + 1][1]);
+    pa[kk][3] = pack_bf16(s[2 * kk + 1][2], s[2 * kk + 1][3]);
+  }
+  // chunk partial records [m, l, -, -, o[128]] (kPartStride floats, 16-byte aligned)
+  if (t == 0) {
+    if (r0 < nr) {
+      float* pp = a.apartial + ((size_t)(srows[ir0.row].chunk_base + it.chunk) * H + h) * kPartStride;
+      pp[0] = mu0;
+      pp[1] = l0;
     }
-#pragma unroll
-    for (int nt = 0; nt < 16; nt++) {
-      const int wi = nt >> 1;  // word of the 16-dim slice holding dim 16g + nt
-      const uint32_t sel = (nt & 1) ? 0x7632u : 0x5410u;
-      auto word = [&](int c) -> uint32_t {
-        const uint4& v = w[c][wi >> 2];
-        const int k = wi & 3;
-        return k == 0 ? v.x : k == 1 ? v.y : k == 2 ? v.z : v.w;
-      };
-      mma_bf16(o[nt], pa, __byte_perm(word(0), word(1), sel), __byte_perm(word(2), word(3), sel));
+    if (r1 < nr) {
+      float* pp = a.apartial + ((size_t)(srows[ir1.row].chunk_base + it.chunk) * H + h) * kPartStride;
+      pp[0] = mu1;
+      pp[1] = l1;
     }
   }
-
-  // chunk partials: lane (g, t) holds dims 32t + nt (c0/c2) and 32t + 16 + nt (c1/c3)
-  const int stride = HD + 2;
+  // o is transposed through the (no longer needed) K tile so each row leaves as one 512-byte store
+  float* stg = reinterpret_cast<float*>(const_cast<unsigned char*>(ks));
+  __syncwarp();
 #pragma unroll
-  for (int hr = 0; hr < 2; hr++) {
-    const int r = hr ? r1 : r0;
-    if (r >= nr) continue;
-    const RowMeta& m = srows[hr ? ir1.row : ir0.row];
-    float* pp = a.apartial + ((size_t)(m.chunk_base + it.chunk) * H + h) * stride;
-    if (t == 0) {
-      pp[0] = hr ? mu1 : mu0;
-      pp[1] = hr ? l1 : l0;
+  for (int half = 0; half < 2; half++) {
+    float o[8][4];
+#pragma unroll
+    for (int nt = 0; nt < 8; nt++) o[nt][0] = o[nt][1] = o[nt][2] = o[nt][3] = 0.0f;
+#pragma unroll
+    for (int kk = 0; kk < 4; kk++) {
+      if (16 * kk >= vmax) break;
+      // keys 16kk + 2t + {0, 1, 8, 9}, dims 16g + 8 half .. +7 (zero beyond the staged keys)
+      uint4 w[4];
+#pragma unroll
+      for (int c = 0; c < 4; c++) {
+        const int key = 16 * kk + 2 * t + (c & 1) + 8 * (c >> 1);
+        w[c] = key < vmax ? *reinterpret_cast<const uint4*>(vs + (size_t)key * HD * 2 + (((2 * g + half) ^ (key & 7)) << 4))
+                          : make_uint4(0u, 0u, 0u, 0u);
+      }
+#pragma unroll
+      for (int nt = 0; nt < 8; nt++) {
+        const int k4 = nt >> 1;  // word of the 8-dim slice holding dim 16g + 8 half + nt
+        const uint32_t sel = (nt & 1) ? 0x7632u : 0x5410u;
+        auto word = [&](int c) -> uint32_t {
+          return k4 == 0 ? w[c].x : k4 == 1 ? w[c].y : k4 == 2 ? w[c].z : w[c].w;
+        };
+        mma_bf16(o[nt], pa[kk], __byte_perm(word(0), word(1), sel), __byte_perm(word(2), word(3), sel));
+      }
     }
+    // lane (g, t) holds dims 32t + 8 half + nt (c0/c2) and 32t + 16 + 8 half + nt (c1/c3) of rows g, g + 8
 #pragma unroll
-    for (int nt = 0; nt < 16; nt++) {
-      pp[2 + 32 * t + nt] = o[nt][hr ? 2 : 0];
-      pp[2 + 32 * t + 16 + nt] = o[nt][hr ? 3 : 1];
+    for (int nt = 0; nt < 8; nt++) {
+      stg[g * kStgStride + 32 * t + 8 * half + nt] = o[nt][0];
+      stg[g * kStgStride + 32 * t + 16 + 8 * half + nt] = o[nt][1];
+      stg[(g + 8) * kStgStride + 32 * t + 8 * half + nt] = o[nt][2];
+      stg[(g + 8) * kStgStride + 32 * t + 16 + 8 * half + nt] = o[nt][3];
     }
   }
+  __syncwarp();
+  for (int rr = 0; rr < nr; rr++) {
+    float* pp = a.apartial + ((size_t)(srows[irows[rr].row].chunk_base + it.chunk) * H + h) * kPartStride;
+    __stcg(reinterpret_cast<float4*>(pp + 4) + lane, *reinterpret_cast<const float4*>(stg + rr * kStgStride + 4 * lane));
+  }
+  if (dbg) { uint64_t t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t) :: "memory"); dbg[3] = t; }
 }
 
 // Merge the chunk partials of one (row, head) in chunk order -> bf16 attention output.
 __device__ void attn_merge(const Args& a, const RowMeta& m, int row, int h, int lane) {
-  const int stride = HD + 2;
-  const size_t cs = (size_t)a.H * stride;
-  const float* base = a.apartial + ((size_t)m.chunk_base * a.H + h) * stride;
+  const size_t cs = (size_t)a.H * kPartStride;
+  const float* mbase = a.apartial + ((size_t)m.chunk_base * a.H + h) * kPartStride;
+  const float4* base = reinterpret_cast<const float4*>(mbase + 4) + lane;
   const int nch = m.n_chunks;
-  float M = -INFINITY, L = 0.0f, acc[4] = {0.f, 0.f, 0.f, 0.f};
-  // batches of 16 chunks: (m, l) lane-parallel and this lane's 4 dims of every
-  // chunk issued together (one memory round per batch), running-max rescale
-  for (int c0 = 0; c0 < nch; c0 += 16) {
-    const int nb = min(16, nch - c0);
-    float mc = -INFINITY, lc = 0.0f;
-    if (lane < nb) {
-      mc = __ldcg(base + (c0 + lane) * cs);
-      lc = __ldcg(base + (c0 + lane) * cs + 1);
-    }
-    float2 lo[16], hi[16];
-#pragma unroll
-    for (int u = 0; u < 16; u++)
-      if (u < nb) {  // partial rows are 130 floats: 8-byte aligned only
-        const float* src = base + (c0 + u) * cs + 2 + 4 * lane;
-        lo[u] = __ldcg(reinterpret_cast<const float2*>(src));
-        hi[u] = __ldcg(reinterpret_cast<const float2*>(src + 2));
-      }
+  float M = -INFINITY, L = 0.0f, acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
+  // batches of 8 chunks: (m, l) lane-parallel plus this lane's 4 dims of each
+  // chunk, all requested together; running-max rescale across batches
+  for (int c0 = 0; c0 < nch; c0 += 8) {
+    const int nb = min(8, nch - c0);
+    const float mc = lane < nb ? __ldcg(mbase + (c0 + lane) * cs) : -INFINITY;
+    const float lc = lane < nb ? __ldcg(mbase + (c0 + lane) * cs + 1) : 0.0f;
+    float4 x0 = make_float4(0.f, 0.f, 0.f, 0.f), x1 = x0, x2 = x0, x3 = x0, x4 = x0, x5 = x0, x6 = x0, x7 = x0;
+#define MK_LD(u, X) \
+    if (u < nb) X = __ldcg(base + (c0 + u) * (cs / 4));
+    MK_LD(0, x0) MK_LD(1, x1) MK_LD(2, x2) MK_LD(3, x3) MK_LD(4, x4) MK_LD(5, x5) MK_LD(6, x6) MK_LD(7, x7)
+#undef MK_LD
     float Mb = mc;
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) Mb = fmaxf(Mb, __shfl_xor_sync(0xffffffffu, Mb, off));
     const float Mn = fmaxf(M, Mb);
     const float rescale = M == -INFINITY ? 0.0f : exp2f(M - Mn);
     L *= rescale;
-#pragma unroll
-    for (int i = 0; i < 4; i++) acc[i] *= rescale;
+    acc0 *= rescale; acc1 *= rescale; acc2 *= rescale; acc3 *= rescale;
     const float wl = lane < nb ? exp2f(mc - Mn) : 0.0f;
     float ls = wl * lc;
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) ls += __shfl_xor_sync(0xffffffffu, ls, off);
     L += ls;
-#pragma unroll
-    for (int u = 0; u < 16; u++) {
-      const float wt = __shfl_sync(0xffffffffu, wl, u);
-      if (u < nb) {
-        acc[0] = fmaf(wt, lo[u].x, acc[0]);
-        acc[1] = fmaf(wt, lo[u].y, acc[1]);
-        acc[2] = fmaf(wt, hi[u].x, acc[2]);
-        acc[3] = fmaf(wt, hi[u].y, acc[3]);
-      }
+#define MK_ACC(u, X)                                                                      \
+    {                                                                                      \
+      const float wt = __shfl_sync(0xffffffffu, wl, u);                                    \
+      acc0 = fmaf(wt, X.x, acc0); acc1 = fmaf(wt, X.y, acc1);                              \
+      acc2 = fmaf(wt, X.z, acc2); acc3 = fmaf(wt, X.w, acc3);                              \
     }
+    MK_ACC(0, x0) MK_ACC(1, x1) MK_ACC(2, x2) MK_ACC(3, x3) MK_ACC(4, x4) MK_ACC(5, x5) MK_ACC(6, x6) MK_ACC(7, x7)
+#undef MK_ACC
     M = Mn;
   }
   const float inv = 1.0f / L;
   uint2 packed;
-  packed.x = pack_bf16(acc[0] * inv, acc[1] * inv);
-  packed.y = pack_bf16(acc[2] * inv, acc[3] * inv);
+  packed.x = pack_bf16(acc0 * inv, acc1 * inv);
+  packed.y = pack_bf16(acc2 * inv, acc3 * inv);
   *reinterpret_cast<uint2*>(a.attn + (size_t)row * a.d + h * HD + 4 * lane) = packed;
 }
 
@@ -455,9 +490,8 @@ __device__ __forceinline__ void tile_epilogue(const Args& a, int kind, int l, in
     if (et < 64) {
       const int sec = n0 / d, h = (n0 % d) / HD, half = HD / 2;
       const size_t layer_off = (size_t)l * 2 * a.H * FE_PAGE * HD;
-#pragma unroll
-      for (int b = 0; b < XR; b++) {
-        if (b >= B) break;
+#pragma unroll 1
+      for (int b = 0; b < B; b++) {
         const RowMeta& m = srows[b];
         float x1 = tile[et * (XR + 1) + b] * rn[b], x2 = tile[(et + half) * (XR + 1) + b] * rn[b];
         if (sec < 2) {
@@ -481,26 +515,23 @@ __device__ __forceinline__ void tile_epilogue(const Args& a, int kind, int l, in
     }
   } else if (kind == K_O || kind == K_DOWN) {
     const int col = n0 + r;
-    float sq[XR];
-#pragma unroll
-    for (int b = 0; b < XR; b++) {
-      sq[b] = 0.0f;
-      if (b < B) {
-        const float xv = tile[r * (XR + 1) + b];  // old x already folded into the sum
-        a.x[(size_t)b * d + col] = xv;
-        a.xg[(size_t)b * d + col] = __float2bfloat16_rn(xv * gw);
-        sq[b] = xv * xv;
-      }
+#pragma unroll 1
+    for (int b = 0; b < B; b++) {
+      const float xv = tile[r * (XR + 1) + b];  // old x already folded into the sum
+      a.x[(size_t)b * d + col] = xv;
+      a.xg[(size_t)b * d + col] = __float2bfloat16_rn(xv * gw);
     }
-    epi_sum16(sq, B, red, a.ss + tl, a.d / MT, et);  // ss[row][tile]
+    epi_sumsq_cols(tile, B, a.ss + tl, a.d / MT, et);  // ss[row][tile]
   } else if (kind == K_GU) {
     if (et < 64 && tl * 64 + et < a.F)
+#pragma unroll 1
       for (int b = 0; b < B; b++)
         a.attn[(size_t)b * a.F + tl * 64 + et] = __float2bfloat16_rn(
             silu_mul(tile[et * (XR + 1) + b] * rn[b], tile[(et + 64) * (XR + 1) + b] * rn[b]));
   } else {  // K_LM
     const int nrow = n0 + r;
     const bool row_ok = nrow < a.V;
+#pragma unroll 1
     for (int b = 0; b < B; b++) {
       const float v = tile[r * (XR + 1) + b] * rn[b];
       unsigned long long k = (row_ok && nrow < a.n_text) ? argmax_key(v, nrow) : 0ull;
@@ -516,77 +547,336 @@ __device__ __forceinline__ void tile_epilogue(const Args& a, int kind, int l, in
   }
 }
 
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads, 1) decode_mk_kernel(const __grid_constant__ CUtensorMap map_xg,
-                                                                const __grid_constant__ CUtensorMap map_attn,
-                                                                const __grid_constant__ CUtensorMap map_act,
-                                                                const Args a) {
-  extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  unsigned char* sw = smem;                                  // [kStages][128 x 64] weights
-  unsigned char* sx = smem + kStages * kWBytes;              // [kStages][16 x 64] activations
-  float* tile = (float*)(sx + kStages * kXBytes);            // [128][17]
-  float* srope = tile + MT * (XR + 1);                       // [16][128] RoPE cos | sin of the rows' positions
-  uint64_t* full = (uint64_t*)(srope + XR * HD);
-  uint64_t* empty = full + kStages;
-  uint64_t* acc_full = empty + kStages;
-  uint64_t* acc_empty = acc_full + kAcc;
-  uint32_t* tmem_slot = (uint32_t*)(acc_empty + kAcc);
-  int* last_flag = (int*)(tmem_slot + 1);
-  float* rn = (float*)(tmem_slot + 4);                       // [16] row norms of the phase
-  float* red = rn + XR;                                      // [4][16] epilogue reductions
-  unsigned long long* kred = (unsigned long long*)(red + 4 * XR);  // [16][4]
-  volatile int* ready_ph = (volatile int*)(kred + 4 * XR);    // last phase whose grid barrier was passed
-  RowMeta* srows = (RowMeta*)(kred + 4 * XR + 2);            // [16] rows of the tick
-  uint64_t* abar = (uint64_t*)(srows + XR);                  // [kAttnSlots] K/V staging barriers
-  volatile int* qseq = (volatile int*)(abar + kAttnSlots);   // [kQueue] chunk queue: sequence numbers
-  volatile int* qval = qseq + kQueue;                        // [kQueue] chunk ids
-  AttnItem* sitems = (AttnItem*)(qval + kQueue);             // [kMaxPairs] items of this CTA's pairs
-  ItemRow* sirows = (ItemRow*)(sitems + kMaxPairs);          // [kMaxPairs][16] their query rows
+#define MK_SMEM_LAYOUT(smem) \
+  unsigned char* sw = smem; \
+  unsigned char* sx = smem + kStages * kWBytes; \
+  float* tile = (float*)(sx + kStages * kXBytes); \
+  float* srope = tile + MT * (XR + 1); \
+  uint64_t* full = (uint64_t*)(srope + XR * HD); \
+  uint64_t* empty = full + kStages; \
+  uint64_t* acc_full = empty + kStages; \
+  uint64_t* acc_empty = acc_full + kAcc; \
+  uint32_t* tmem_slot = (uint32_t*)(acc_empty + kAcc); \
+  int* last_flag = (int*)(tmem_slot + 1); \
+  float* rn = (float*)(tmem_slot + 4); \
+  float* red = rn + XR; \
+  unsigned long long* kred = (unsigned long long*)(red + 4 * XR); \
+  volatile int* ready_ph = (volatile int*)(kred + 4 * XR); \
+  RowMeta* srows = (RowMeta*)(kred + 4 * XR + 2); \
+  uint64_t* abar = (uint64_t*)(srows + XR); \
+  volatile int* qseq = (volatile int*)(abar + kAttnSlots); \
+  volatile int* qval = qseq + kQueue; \
+  AttnItem* sitems = (AttnItem*)(qval + kQueue); \
+  ItemRow* sirows = (ItemRow*)(sitems + kMaxPairs); \
+  (void)0
 
+__device__ __noinline__ void epi_embed(const Args& a, unsigned char* smem, int ph, int l, int kind) {
+  MK_SMEM_LAYOUT(smem);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = gridDim.x;
+  const int et = threadIdx.x - 64;
+  const int r = 32 * (warp & 3) + lane;
+  const int d = a.d, B = a.B;
+  const int n_ss = d / MT;
+  (void)r; (void)d; (void)B; (void)n_ss; (void)G;
+      for (int ct = blockIdx.x; ct < n_ss; ct += G) {
+        const int col = ct * MT + et;
+        const float gw = __ldg(a.norms[0] + col);
+        int tok[XR];
+#pragma unroll
+        for (int b = 0; b < XR; b++)
+          tok[b] = b < B ? (srows[b].tok >= 0 ? srows[b].tok : __ldcg(a.out_tokens + srows[b].tok_src)) : 0;
+        float xv[XR];
+#pragma unroll
+        for (int b = 0; b < XR; b++) xv[b] = b < B ? __bfloat162float(a.embed[(size_t)tok[b] * d + col]) : 0.0f;
+#pragma unroll
+        for (int b = 0; b < XR; b++) {
+          tile[et * (XR + 1) + b] = xv[b];
+          if (b < B) {
+            a.x[(size_t)b * d + col] = xv[b];
+            a.xg[(size_t)b * d + col] = __float2bfloat16_rn(xv[b] * gw);
+          }
+        }
+        epi_sync();
+        epi_sumsq_cols(tile, B, a.ss + ct, n_ss, et);
+        epi_sync();
+      }
+}
+
+__device__ __noinline__ void epi_attn(const Args& a, unsigned char* smem, int ph, int l, int kind) {
+  MK_SMEM_LAYOUT(smem);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = gridDim.x;
+  const int et = threadIdx.x - 64;
+  const int r = 32 * (warp & 3) + lane;
+  const int d = a.d, B = a.B;
+  const int n_ss = d / MT;
+  (void)r; (void)d; (void)B; (void)n_ss; (void)G;
+      // The ring is idle (the producer holds the next weights back until this
+      // phase ends): stage K and V of this CTA's (page, head) pairs into it with
+      // bulk copies, all in flight at once, then one warp per pair computes.
+      const int n_pairs = a.hdr[1] * a.H;
+      const __nv_bfloat16* pool_l = a.kv_pool + (size_t)l * 2 * a.H * FE_PAGE * HD;
+      if (a.trace && et == 0) a.trace[((size_t)ph * 6 + 2) * G + blockIdx.x] = gtimer();
+      for (int base = blockIdx.x, round = 0; base < n_pairs; base += kAttnSlots * G, round++) {
+        auto item_of = [&](int j, int pr) -> AttnItem { return round == 0 ? sitems[j] : a.items[pr / a.H]; };
+        // all 128 threads stage K and V of every pair of the round with 16-byte
+        // cp.async (rows 256 B, 16-byte chunks XOR-swizzled by key & 7: the
+        // fragment reads below are bank-conflict free)
+        for (int j = 0; j < kAttnSlots && base + j * G < n_pairs; j++) {
+          const int pr = base + j * G;
+          const AttnItem it = item_of(j, pr);
+          const __nv_bfloat16* kg = pool_l + (size_t)it.page * a.page_elems + (size_t)(pr % a.H) * FE_PAGE * HD;
+          const __nv_bfloat16* vg = kg + (size_t)a.H * FE_PAGE * HD;
+          unsigned char* slot = sw + (size_t)j * kAttnSlotBytes;
+          for (int x = et; x < it.valid_max * 16; x += 128) {
+            const int key = x >> 4, c = x & 15;
+            const uint32_t so = (uint32_t)(key * 256 + ((c ^ (key & 7)) << 4));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(su32(slot + so)),
+                         "l"(kg + (size_t)key * HD + c * 8) : "memory");
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(su32(slot + kAttnSlotBytes / 2 + so)),
+                         "l"(vg + (size_t)key * HD + c * 8) : "memory");
+          }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        // this warp's pairs j0, j0 + 4: the first one's Q is requested while K / V land
+        uint4 q0[4], q1[4];
+        {
+          const int j0 = et >> 5, pr0 = base + j0 * G;
+          if (pr0 < n_pairs) {
+            const AttnItem it = item_of(j0, pr0);
+            attn_load_q(a, it, round == 0 ? sirows + j0 * XR : a.item_rows + it.row_begin, pr0 % a.H, lane, q0, q1);
+          }
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        epi_sync();
+        if (a.trace && et == 0 && round == 0) a.trace[((size_t)ph * 6 + 3) * G + blockIdx.x] = gtimer();
+        for (int j = et >> 5; j < kAttnSlots; j += 4) {
+          const int pr = base + j * G;
+          if (pr >= n_pairs) break;
+          const AttnItem it = item_of(j, pr);
+          const ItemRow* irows = round == 0 ? sirows + j * XR : a.item_rows + it.row_begin;
+          if (j >= 4) attn_load_q(a, it, irows, pr % a.H, lane, q0, q1);
+          const unsigned char* slot = sw + (size_t)j * kAttnSlotBytes;
+          unsigned long long* dbg = nullptr;  // diagnostics (flags & 4): sub-step times of CTA 0's first pair
+          if ((a.flags & 4) && a.trace && blockIdx.x == 0 && et == 0 && j == 0 && round == 0)
+            dbg = a.trace + ((size_t)(n_phases(a) - 1) * 6 + 2) * G + 8 * l;  // FINAL phase slot 2, [layer][4]
+          attn_pair(a, srows, it, irows, pr % a.H, slot, slot + kAttnSlotBytes / 2, q0, q1, lane, dbg);
+        }
+        if (a.trace && et == 0 && round == 0) a.trace[((size_t)ph * 6 + 4) * G + blockIdx.x] = gtimer();
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem reads before async writes
+        epi_sync();  // slots reused by the next round
+        if (a.trace && et == 0 && round == 0) a.trace[((size_t)ph * 6 + 5) * G + blockIdx.x] = gtimer();
+      }
+}
+
+__device__ __noinline__ void epi_amerge(const Args& a, unsigned char* smem, int ph, int l, int kind) {
+  MK_SMEM_LAYOUT(smem);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = gridDim.x;
+  const int et = threadIdx.x - 64;
+  const int r = 32 * (warp & 3) + lane;
+  const int d = a.d, B = a.B;
+  const int n_ss = d / MT;
+  (void)r; (void)d; (void)B; (void)n_ss; (void)G;
+      if (a.trace && et == 0) a.trace[((size_t)ph * 6 + 2) * G + blockIdx.x] = gtimer();
+      for (int pr = blockIdx.x * 4 + (et >> 5); pr < B * a.H; pr += G * 4) {
+        attn_merge(a, srows[pr / a.H], pr / a.H, pr % a.H, lane);
+        if (a.trace && et == 0) a.trace[((size_t)ph * 6 + 3) * G + blockIdx.x] = gtimer();
+      }
+      if (a.trace && et == 0) a.trace[((size_t)ph * 6 + 4) * G + blockIdx.x] = gtimer();
+      epi_sync();
+      if (a.trace && et == 0) a.trace[((size_t)ph * 6 + 5) * G + blockIdx.x] = gtimer();
+}
+
+__device__ __noinline__ void epi_final(const Args& a, unsigned char* smem, int ph, int l, int kind) {
+  MK_SMEM_LAYOUT(smem);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = gridDim.x;
+  const int et = threadIdx.x - 64;
+  const int r = 32 * (warp & 3) + lane;
+  const int d = a.d, B = a.B;
+  const int n_ss = d / MT;
+  (void)r; (void)d; (void)B; (void)n_ss; (void)G;
+      const int tiles = a.plan[MK_LM].tiles;
+      for (int b = blockIdx.x; b < B; b += G) {
+        unsigned long long k = 0ull;
+        for (int t = et; t < tiles; t += 128) k = max(k, __ldcg(&a.part_keys[(size_t)b * tiles + t]));
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) k = max(k, __shfl_xor_sync(0xffffffffu, k, off));
+        if (lane == 0) kred[et >> 5] = k;
+        epi_sync();
+        if (et == 0) {
+          const unsigned long long kk = max(max(kred[0], kred[1]), max(kred[2], kred[3]));
+          if (srows[b].out_idx >= 0) a.out_tokens[srows[b].out_idx] = argmax_index(kk);
+        }
+        epi_sync();
+      }
+}
+
+__device__ __noinline__ void epi_gemm(const Args& a, unsigned char* smem, int ph, int l, int kind, uint32_t tmem, int& lu, int& n) {
+  MK_SMEM_LAYOUT(smem);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = gridDim.x;
+  const int et = threadIdx.x - 64;
+  const int r = 32 * (warp & 3) + lane;
+  const int d = a.d, B = a.B;
+  const int n_ss = d / MT;
+  (void)r; (void)d; (void)B; (void)n_ss; (void)G;
+      // ---- GEMM phase: drain each grabbed chunk's accumulator into its partial
+      // slot (no synchronisation; the grid barrier publishes them)
+      const MkPlan p = a.plan[gemm_of(kind)];
+      bool first_chunk = true;
+      for (;; lu++) {
+        const int q = queue_read(qseq, qval, n++);
+        if (q < 0) break;
+        int tl, j, kb0, kb1;
+        chunk_range(p, q, &tl, &j, &kb0, &kb1);
+        const int acc = lu % kAcc;
+        // residual GEMMs: chunk 0 of a tile folds the old x into its partial
+        // (loaded while the MMAs run), so the tile epilogue needs no x load
+        const bool fold_x = (kind == K_O || kind == K_DOWN) && j == 0;
+        float xo[XR];
+#pragma unroll
+        for (int b = 0; b < XR; b++) xo[b] = (fold_x && b < B) ? __ldcg(a.x + (size_t)b * d + tl * MT + r) : 0.0f;
+        mbar_wait(&acc_full[acc], (lu / kAcc) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (a.trace && et == 0) {
+          const uint64_t tnow = gtimer();
+          if (first_chunk) a.trace[((size_t)ph * 6 + 3) * G + blockIdx.x] = tnow;
+          a.trace[((size_t)ph * 6 + 4) * G + blockIdx.x] = tnow;
+        }
+        first_chunk = false;
+        uint32_t raw[16];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(raw[0]), "=r"(raw[1]), "=r"(raw[2]), "=r"(raw[3]), "=r"(raw[4]), "=r"(raw[5]), "=r"(raw[6]),
+              "=r"(raw[7]), "=r"(raw[8]), "=r"(raw[9]), "=r"(raw[10]), "=r"(raw[11]), "=r"(raw[12]),
+              "=r"(raw[13]), "=r"(raw[14]), "=r"(raw[15])
+            : "r"(tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(acc * XR)));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        epi_sync();
+        if (et == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&acc_empty[acc])) : "memory");
+        // partial layout [chunk][batch rows / 4][128 weight rows] float4: coalesced
+        float4* dst = reinterpret_cast<float4*>(a.partial) + (size_t)q * (XR / 4) * MT + r;
+#pragma unroll
+        for (int q4 = 0; q4 < XR / 4; q4++)
+          if (4 * q4 < B)
+            __stcg(dst + q4 * MT, make_float4(__uint_as_float(raw[4 * q4]) + xo[4 * q4],
+                                         __uint_as_float(raw[4 * q4 + 1]) + xo[4 * q4 + 1],
+                                         __uint_as_float(raw[4 * q4 + 2]) + xo[4 * q4 + 2],
+                                         __uint_as_float(raw[4 * q4 + 3]) + xo[4 * q4 + 3]));
+      }
+      if (a.trace && et == 0) a.trace[((size_t)ph * 6 + 5) * G + blockIdx.x] = gtimer();
+}
+
+__device__ __noinline__ void epi_reduce(const Args& a, unsigned char* smem, int ph, int l, int kind) {
+  MK_SMEM_LAYOUT(smem);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = gridDim.x;
+  const int et = threadIdx.x - 64;
+  const int r = 32 * (warp & 3) + lane;
+  const int d = a.d, B = a.B;
+  const int n_ss = d / MT;
+  (void)r; (void)d; (void)B; (void)n_ss; (void)G;
+      // ---- reduction phase: the tiles t = cta (mod grid) of the GEMM just done:
+      // sum the nc chunk partials in chunk order (deterministic), then the fused
+      // epilogue (RoPE + q / paged K/V, residual + norm inputs, SiLU * up, argmax).
+      // The norm sums, gain column and partials are all requested in one round.
+      const int gk = gemm_kind_of_reduce(kind);
+      const MkPlan p = a.plan[gemm_of(gk)];
+      const bool scaled = gk == K_QKV || gk == K_GU || gk == K_LM;
+      const bool resid = gk == K_O || gk == K_DOWN;
+      const float* gnext = gk == K_O ? a.norms[2 * l + 1]
+                           : gk == K_DOWN ? (l + 1 < a.L ? a.norms[2 * (l + 1)] : a.norms[2 * a.L]) : nullptr;
+      if (a.trace && et == 0) a.trace[((size_t)ph * 6 + 2) * G + blockIdx.x] = gtimer();
+      float4 sv[8];
+      const bool need_ss = scaled && et < B && blockIdx.x < p.tiles;
+      if (need_ss) {
+        const float4* sr = reinterpret_cast<const float4*>(a.ss + (size_t)et * n_ss);
+#pragma unroll
+        for (int u = 0; u < 8; u++) sv[u] = 4 * u < n_ss ? __ldcg(sr + u) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      for (int tl = blockIdx.x; tl < p.tiles; tl += G) {
+        const float gw = resid ? __ldg(gnext + tl * MT + r) : 0.0f;
+        float4 acc4[XR / 4];
+#pragma unroll
+        for (int q4 = 0; q4 < XR / 4; q4++) acc4[q4] = make_float4(0.f, 0.f, 0.f, 0.f);
+        const size_t q0 = (size_t)tl * p.nc;
+        if (B <= 8) {  // 12 chunks x 2 float4 in flight
+          for (int c0 = 0; c0 < p.nc; c0 += 12) {
+            float4 v[12][2];
+#pragma unroll
+            for (int u = 0; u < 12; u++) {
+              const float4* src = reinterpret_cast<const float4*>(a.partial) + (q0 + c0 + u) * (XR / 4) * MT + r;
+              if (c0 + u < p.nc) {
+                v[u][0] = __ldcg(src);
+                v[u][1] = B > 4 ? __ldcg(src + MT) : make_float4(0.f, 0.f, 0.f, 0.f);
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < 12; u++)
+              if (c0 + u < p.nc) {
+#pragma unroll
+                for (int q4 = 0; q4 < 2; q4++) {
+                  acc4[q4].x += v[u][q4].x; acc4[q4].y += v[u][q4].y;
+                  acc4[q4].z += v[u][q4].z; acc4[q4].w += v[u][q4].w;
+                }
+              }
+          }
+        } else {
+          for (int c0 = 0; c0 < p.nc; c0 += 4) {
+            float4 v[4][XR / 4];
+#pragma unroll
+            for (int u = 0; u < 4; u++)
+#pragma unroll
+              for (int q4 = 0; q4 < XR / 4; q4++)
+                if (c0 + u < p.nc && 4 * q4 < B)
+                  v[u][q4] = __ldcg(reinterpret_cast<const float4*>(a.partial) + ((q0 + c0 + u) * (XR / 4) + q4) * MT + r);
+#pragma unroll
+            for (int u = 0; u < 4; u++)
+#pragma unroll
+              for (int q4 = 0; q4 < XR / 4; q4++)
+                if (c0 + u < p.nc && 4 * q4 < B) {
+                  acc4[q4].x += v[u][q4].x; acc4[q4].y += v[u][q4].y;
+                  acc4[q4].z += v[u][q4].z; acc4[q4].w += v[u][q4].w;
+                }
+          }
+        }
+        if (tl == blockIdx.x && need_ss) {
+          float sacc = 0.0f;
+#pragma unroll
+          for (int u = 0; u < 8; u++) sacc += (sv[u].x + sv[u].y) + (sv[u].z + sv[u].w);
+          for (int t4 = 32; t4 < n_ss; t4++) sacc += __ldcg(a.ss + (size_t)et * n_ss + t4);  // d > 4096 only
+          rn[et] = rsqrtf(sacc / (float)d + a.eps);
+        }
+#pragma unroll
+        for (int q4 = 0; q4 < XR / 4; q4++) {
+          tile[r * (XR + 1) + 4 * q4] = acc4[q4].x;
+          tile[r * (XR + 1) + 4 * q4 + 1] = acc4[q4].y;
+          tile[r * (XR + 1) + 4 * q4 + 2] = acc4[q4].z;
+          tile[r * (XR + 1) + 4 * q4 + 3] = acc4[q4].w;
+        }
+        epi_sync();  // tile and rn visible
+        if (a.trace && et == 0 && tl == blockIdx.x) a.trace[((size_t)ph * 6 + 3) * G + blockIdx.x] = gtimer();
+        tile_epilogue(a, gk, l, tl, tile, rn, red, kred, srows, srope, gw, et, warp, lane);
+        epi_sync();  // tile / reduction scratch reused by the next tile
+        if (a.trace && et == 0 && tl == blockIdx.x) a.trace[((size_t)ph * 6 + 4) * G + blockIdx.x] = gtimer();
+      }
+      if (a.trace && et == 0) a.trace[((size_t)ph * 6 + 5) * G + blockIdx.x] = gtimer();
+}
+
+// The three warp roles are separate non-inlined functions so each gets its own
+// register allocation (the attention / reduction code of the epilogue warps
+// would otherwise force the producer's and MMA's loop state into local memory).
+__device__ __noinline__ void role_producer(const Args& a, unsigned char* smem, const CUtensorMap& map_xg,
+                                           const CUtensorMap& map_attn, const CUtensorMap& map_act) {
+  MK_SMEM_LAYOUT(smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = gridDim.x;
   const int P = n_phases(a);
-
-  if (warp == 0 && lane == 0) {
-    for (int s = 0; s < kStages; s++) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    for (int i = 0; i < kAcc; i++) {
-      mbar_init(&acc_full[i], 1);
-      mbar_init(&acc_empty[i], 1);
-    }
-    for (int i = 0; i < kAttnSlots; i++) mbar_init(&abar[i], 1);
-    for (int i = 0; i < kQueue; i++) qseq[i] = -1;
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    *ready_ph = -1;
-  }
-  if (threadIdx.x >= 64) {  // per-tick constants: rows, their RoPE rows, this CTA's attention items
-    const int et = threadIdx.x - 64;
-    if (et < a.B) srows[et] = a.rows[et];
-    for (int b = 0; b < a.B; b++) srope[b * HD + et] = __ldg(a.rope + (size_t)a.rows[b].pos * HD + et);
-    const int n_pairs = a.hdr[1] * a.H;
-    for (int j = 0; j < kMaxPairs; j++) {
-      const int pr = blockIdx.x + j * gridDim.x;
-      if (pr >= n_pairs) break;
-      const AttnItem it = a.items[pr / a.H];
-      if (et == 0) sitems[j] = it;
-      if (et < it.row_count) sirows[j * XR + et] = a.item_rows[it.row_begin + et];
-    }
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
-                 "n"(kAcc * XR));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0) {
-    if (lane == 0) {
+  (void)warp; (void)lane; (void)G; (void)P;
       // ---------------- TMA producer
       const uint64_t wpol = policy_evict_first();  // weights are read once per tick
       int it = 0, n = 0;
@@ -655,9 +945,14 @@ __global__ void __launch_bounds__(kThreads, 1) decode_mk_kernel(const __grid_con
           flush();
         }
       }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
+}
+
+__device__ __noinline__ void role_mma(const Args& a, unsigned char* smem, uint32_t tmem) {
+  MK_SMEM_LAYOUT(smem);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = gridDim.x;
+  const int P = n_phases(a);
+  (void)warp; (void)lane; (void)G; (void)P;
       // ---------------- MMA issuer
       int it = 0, lu = 0, n = 0;
       for (int ph = 0; ph < P; ph++) {
@@ -696,8 +991,14 @@ __global__ void __launch_bounds__(kThreads, 1) decode_mk_kernel(const __grid_con
                        ::"r"(su32(&acc_full[acc])) : "memory");
         }
       }
-    }
-  } else {
+}
+
+__device__ __noinline__ void role_epilogue(const Args& a, unsigned char* smem, uint32_t tmem) {
+  MK_SMEM_LAYOUT(smem);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = gridDim.x;
+  const int P = n_phases(a);
+  (void)warp; (void)lane; (void)G; (void)P;
     // ---------------- epilogue / non-GEMM phases (128 threads)
     const int et = threadIdx.x - 64;
     const int r = 32 * (warp & 3) + lane;  // TMEM lane = weight row of the tile
@@ -716,222 +1017,12 @@ __global__ void __launch_bounds__(kThreads, 1) decode_mk_kernel(const __grid_con
       }
       epi_sync();
 
-      if (kind == K_EMBED) {
-        for (int ct = blockIdx.x; ct < n_ss; ct += G) {
-          const int col = ct * MT + et;
-          const float gw = __ldg(a.norms[0] + col);
-          int tok[XR];
-#pragma unroll
-          for (int b = 0; b < XR; b++)
-            tok[b] = b < B ? (srows[b].tok >= 0 ? srows[b].tok : __ldcg(a.out_tokens + srows[b].tok_src)) : 0;
-          float xv[XR], sq[XR];
-#pragma unroll
-          for (int b = 0; b < XR; b++) xv[b] = b < B ? __bfloat162float(a.embed[(size_t)tok[b] * d + col]) : 0.0f;
-#pragma unroll
-          for (int b = 0; b < XR; b++) {
-            sq[b] = xv[b] * xv[b];
-            if (b < B) {
-              a.x[(size_t)b * d + col] = xv[b];
-              a.xg[(size_t)b * d + col] = __float2bfloat16_rn(xv[b] * gw);
-            }
-          }
-          epi_sum16(sq, B, red, a.ss + ct, n_ss, et);
-          epi_sync();
-        }
-      } else if (kind == K_ATTN) {
-        // The ring is idle (the producer holds the next weights back until this
-        // phase ends): stage K and V of this CTA's (page, head) pairs into it with
-        // bulk copies, all in flight at once, then one warp per pair computes.
-        const int n_pairs = a.hdr[1] * a.H;
-        const __nv_bfloat16* pool_l = a.kv_pool + (size_t)l * 2 * a.H * FE_PAGE * HD;
-        if (a.trace && et == 0) a.trace[((size_t)ph * 6 + 2) * G + blockIdx.x] = gtimer();
-        for (int base = blockIdx.x, round = 0; base < n_pairs; base += kAttnSlots * G, round++) {
-          auto item_of = [&](int j, int pr) -> AttnItem { return round == 0 ? sitems[j] : a.items[pr / a.H]; };
-          if (et == 0) {
-            fence_proxy_async();  // K/V written by the QKV epilogues (generic) -> bulk-copy reads
-            for (int j = 0; j < kAttnSlots && base + j * G < n_pairs; j++) {
-              const int pr = base + j * G;
-              const AttnItem it = item_of(j, pr);
-              const uint32_t bytes = (uint32_t)it.valid_max * HD * 2;
-              const __nv_bfloat16* kg = pool_l + (size_t)it.page * a.page_elems + (size_t)(pr % a.H) * FE_PAGE * HD;
-              unsigned char* slot = sw + (size_t)j * kAttnSlotBytes;
-              mbar_expect_tx(&abar[j], 2 * bytes);
-              bulk_g2s(slot, kg, bytes, &abar[j]);
-              bulk_g2s(slot + kAttnSlotBytes / 2, kg + (size_t)a.H * FE_PAGE * HD, bytes, &abar[j]);
-            }
-          }
-          for (int j = et >> 5; j < kAttnSlots; j += 4) {
-            const int pr = base + j * G;
-            if (pr >= n_pairs) break;
-            const AttnItem it = item_of(j, pr);
-            const ItemRow* irows = round == 0 ? sirows + j * XR : a.item_rows + it.row_begin;
-            uint4 q0[4], q1[4];
-            attn_load_q(a, it, irows, pr % a.H, lane, q0, q1);  // overlaps the K/V staging
-            mbar_wait(&abar[j], (apar >> j) & 1u);
-            if (a.trace && et == 0 && round == 0) a.trace[((size_t)ph * 6 + 3) * G + blockIdx.x] = gtimer();
-            const unsigned char* slot = sw + (size_t)j * kAttnSlotBytes;
-            attn_pair(a, srows, it, irows, pr % a.H, slot, slot + kAttnSlotBytes / 2, q0, q1, lane);
-            if (a.trace && et == 0 && round == 0) a.trace[((size_t)ph * 6 + 4) * G + blockIdx.x] = gtimer();
-          }
-          if (a.trace && et == 0 && round == 0) a.trace[((size_t)ph * 6 + 5) * G + blockIdx.x] = gtimer();
-          for (int j = 0; j < kAttnSlots && base + j * G < n_pairs; j++) apar ^= 1u << j;
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem reads before async writes
-          epi_sync();  // slots reused by the next round
-        }
-      } else if (kind == K_AMERGE) {
-        if (a.trace && et == 0) a.trace[((size_t)ph * 6 + 2) * G + blockIdx.x] = gtimer();
-        for (int pr = blockIdx.x * 4 + (et >> 5); pr < B * a.H; pr += G * 4)
-          attn_merge(a, srows[pr / a.H], pr / a.H, pr % a.H, lane);
-        if (a.trace && et == 0) a.trace[((size_t)ph * 6 + 5) * G + blockIdx.x] = gtimer();
-      } else if (kind == K_FINAL) {
-        const int tiles = a.plan[MK_LM].tiles;
-        for (int b = blockIdx.x; b < B; b += G) {
-          unsigned long long k = 0ull;
-          for (int t = et; t < tiles; t += 128) k = max(k, __ldcg(&a.part_keys[(size_t)b * tiles + t]));
-#pragma unroll
-          for (int off = 16; off >= 1; off >>= 1) k = max(k, __shfl_xor_sync(0xffffffffu, k, off));
-          if (lane == 0) kred[et >> 5] = k;
-          epi_sync();
-          if (et == 0) {
-            const unsigned long long kk = max(max(kred[0], kred[1]), max(kred[2], kred[3]));
-            if (srows[b].out_idx >= 0) a.out_tokens[srows[b].out_idx] = argmax_index(kk);
-          }
-          epi_sync();
-        }
-      } else if (gemm_of(kind) >= 0) {
-        // ---- GEMM phase: drain each grabbed chunk's accumulator into its partial
-        // slot (no synchronisation; the grid barrier publishes them)
-        const MkPlan p = a.plan[gemm_of(kind)];
-        bool first_chunk = true;
-        for (;; lu++) {
-          const int q = queue_read(qseq, qval, n++);
-          if (q < 0) break;
-          int tl, j, kb0, kb1;
-          chunk_range(p, q, &tl, &j, &kb0, &kb1);
-          const int acc = lu % kAcc;
-          // residual GEMMs: chunk 0 of a tile folds the old x into its partial
-          // (loaded while the MMAs run), so the tile epilogue needs no x load
-          const bool fold_x = (kind == K_O || kind == K_DOWN) && j == 0;
-          float xo[XR];
-#pragma unroll
-          for (int b = 0; b < XR; b++) xo[b] = (fold_x && b < B) ? __ldcg(a.x + (size_t)b * d + tl * MT + r) : 0.0f;
-          mbar_wait(&acc_full[acc], (lu / kAcc) & 1);
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          if (a.trace && et == 0) {
-            const uint64_t tnow = gtimer();
-            if (first_chunk) a.trace[((size_t)ph * 6 + 3) * G + blockIdx.x] = tnow;
-            a.trace[((size_t)ph * 6 + 4) * G + blockIdx.x] = tnow;
-          }
-          first_chunk = false;
-          uint32_t raw[16];
-          asm volatile(
-              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-              : "=r"(raw[0]), "=r"(raw[1]), "=r"(raw[2]), "=r"(raw[3]), "=r"(raw[4]), "=r"(raw[5]), "=r"(raw[6]),
-                "=r"(raw[7]), "=r"(raw[8]), "=r"(raw[9]), "=r"(raw[10]), "=r"(raw[11]), "=r"(raw[12]),
-                "=r"(raw[13]), "=r"(raw[14]), "=r"(raw[15])
-              : "r"(tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(acc * XR)));
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-          epi_sync();
-          if (et == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&acc_empty[acc])) : "memory");
-          // partial layout [chunk][batch rows / 4][128 weight rows] float4: coalesced
-          float4* dst = reinterpret_cast<float4*>(a.partial) + (size_t)q * (XR / 4) * MT + r;
-#pragma unroll
-          for (int q4 = 0; q4 < XR / 4; q4++)
-            if (4 * q4 < B)
-              __stcg(dst + q4 * MT, make_float4(__uint_as_float(raw[4 * q4]) + xo[4 * q4],
-                                           __uint_as_float(raw[4 * q4 + 1]) + xo[4 * q4 + 1],
-                                           __uint_as_float(raw[4 * q4 + 2]) + xo[4 * q4 + 2],
-                                           __uint_as_float(raw[4 * q4 + 3]) + xo[4 * q4 + 3]));
-        }
-        if (a.trace && et == 0) a.trace[((size_t)ph * 6 + 5) * G + blockIdx.x] = gtimer();
-      } else {
-        // ---- reduction phase: the tiles t = cta (mod grid) of the GEMM just done:
-        // sum the nc chunk partials in chunk order (deterministic), then the fused
-        // epilogue (RoPE + q / paged K/V, residual + norm inputs, SiLU * up, argmax).
-        // The norm sums, gain column and partials are all requested in one round.
-        const int gk = gemm_kind_of_reduce(kind);
-        const MkPlan p = a.plan[gemm_of(gk)];
-        const bool scaled = gk == K_QKV || gk == K_GU || gk == K_LM;
-        const bool resid = gk == K_O || gk == K_DOWN;
-        const float* gnext = gk == K_O ? a.norms[2 * l + 1]
-                             : gk == K_DOWN ? (l + 1 < a.L ? a.norms[2 * (l + 1)] : a.norms[2 * a.L]) : nullptr;
-        if (a.trace && et == 0) a.trace[((size_t)ph * 6 + 2) * G + blockIdx.x] = gtimer();
-        float4 sv[8];
-        const bool need_ss = scaled && et < B && blockIdx.x < p.tiles;
-        if (need_ss) {
-          const float4* sr = reinterpret_cast<const float4*>(a.ss + (size_t)et * n_ss);
-#pragma unroll
-          for (int u = 0; u < 8; u++) sv[u] = 4 * u < n_ss ? __ldcg(sr + u) : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-        for (int tl = blockIdx.x; tl < p.tiles; tl += G) {
-          const float gw = resid ? __ldg(gnext + tl * MT + r) : 0.0f;
-          float4 acc4[XR / 4];
-#pragma unroll
-          for (int q4 = 0; q4 < XR / 4; q4++) acc4[q4] = make_float4(0.f, 0.f, 0.f, 0.f);
-          const size_t q0 = (size_t)tl * p.nc;
-          if (B <= 8) {  // 12 chunks x 2 float4 in flight
-            for (int c0 = 0; c0 < p.nc; c0 += 12) {
-              float4 v[12][2];
-#pragma unroll
-              for (int u = 0; u < 12; u++) {
-                const float4* src = reinterpret_cast<const float4*>(a.partial) + (q0 + c0 + u) * (XR / 4) * MT + r;
-                if (c0 + u < p.nc) {
-                  v[u][0] = __ldcg(src);
-                  v[u][1] = B > 4 ? __ldcg(src + MT) : make_float4(0.f, 0.f, 0.f, 0.f);
-                }
-              }
-#pragma unroll
-              for (int u = 0; u < 12; u++)
-                if (c0 + u < p.nc) {
-#pragma unroll
-                  for (int q4 = 0; q4 < 2; q4++) {
-                    acc4[q4].x += v[u][q4].x; acc4[q4].y += v[u][q4].y;
-                    acc4[q4].z += v[u][q4].z; acc4[q4].w += v[u][q4].w;
-                  }
-                }
-            }
-          } else {
-            for (int c0 = 0; c0 < p.nc; c0 += 4) {
-              float4 v[4][XR / 4];
-#pragma unroll
-              for (int u = 0; u < 4; u++)
-#pragma unroll
-                for (int q4 = 0; q4 < XR / 4; q4++)
-                  if (c0 + u < p.nc && 4 * q4 < B)
-                    v[u][q4] = __ldcg(reinterpret_cast<const float4*>(a.partial) + ((q0 + c0 + u) * (XR / 4) + q4) * MT + r);
-#pragma unroll
-              for (int u = 0; u < 4; u++)
-#pragma unroll
-                for (int q4 = 0; q4 < XR / 4; q4++)
-                  if (c0 + u < p.nc && 4 * q4 < B) {
-                    acc4[q4].x += v[u][q4].x; acc4[q4].y += v[u][q4].y;
-                    acc4[q4].z += v[u][q4].z; acc4[q4].w += v[u][q4].w;
-                  }
-            }
-          }
-          if (tl == blockIdx.x && need_ss) {
-            float sacc = 0.0f;
-#pragma unroll
-            for (int u = 0; u < 8; u++) sacc += (sv[u].x + sv[u].y) + (sv[u].z + sv[u].w);
-            for (int t4 = 32; t4 < n_ss; t4++) sacc += __ldcg(a.ss + (size_t)et * n_ss + t4);  // d > 4096 only
-            rn[et] = rsqrtf(sacc / (float)d + a.eps);
-          }
-#pragma unroll
-          for (int q4 = 0; q4 < XR / 4; q4++) {
-            tile[r * (XR + 1) + 4 * q4] = acc4[q4].x;
-            tile[r * (XR + 1) + 4 * q4 + 1] = acc4[q4].y;
-            tile[r * (XR + 1) + 4 * q4 + 2] = acc4[q4].z;
-            tile[r * (XR + 1) + 4 * q4 + 3] = acc4[q4].w;
-          }
-          epi_sync();  // tile and rn visible
-          if (a.trace && et == 0 && tl == blockIdx.x) a.trace[((size_t)ph * 6 + 3) * G + blockIdx.x] = gtimer();
-          tile_epilogue(a, gk, l, tl, tile, rn, red, kred, srows, srope, gw, et, warp, lane);
-          epi_sync();  // tile / reduction scratch reused by the next tile
-          if (a.trace && et == 0 && tl == blockIdx.x) a.trace[((size_t)ph * 6 + 4) * G + blockIdx.x] = gtimer();
-        }
-        if (a.trace && et == 0) a.trace[((size_t)ph * 6 + 5) * G + blockIdx.x] = gtimer();
-      }
+      if (kind == K_EMBED) epi_embed(a, smem, ph, l, kind);
+      else if (kind == K_ATTN) epi_attn(a, smem, ph, l, kind);
+      else if (kind == K_AMERGE) epi_amerge(a, smem, ph, l, kind);
+      else if (kind == K_FINAL) epi_final(a, smem, ph, l, kind);
+      else if (gemm_of(kind) >= 0) epi_gemm(a, smem, ph, l, kind, tmem, lu, n);
+      else epi_reduce(a, smem, ph, l, kind);
       // ---- phase done: publish and arrive at the grid barrier
       if (ph + 1 < P) {
         fence_proxy_async();  // generic-proxy writes read by the next phase's TMA / bulk loads
@@ -943,6 +1034,90 @@ __global__ void __launch_bounds__(kThreads, 1) decode_mk_kernel(const __grid_con
         }
       }
     }
+}
+
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads, 1) decode_mk_kernel(const __grid_constant__ CUtensorMap map_xg,
+                                                                const __grid_constant__ CUtensorMap map_attn,
+                                                                const __grid_constant__ CUtensorMap map_act,
+                                                                const __grid_constant__ Args a) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  __shared__ __align__(16) Args sargs[1];
+  unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  static_assert(sizeof(Args) % 4 == 0, "Args copy");
+  for (int i = threadIdx.x; i < (int)(sizeof(Args) / 4); i += blockDim.x)
+    reinterpret_cast<uint32_t*>(sargs)[i] = reinterpret_cast<const uint32_t*>(&a)[i];
+  unsigned char* sw = smem;                                  // [kStages][128 x 64] weights
+  unsigned char* sx = smem + kStages * kWBytes;              // [kStages][16 x 64] activations
+  float* tile = (float*)(sx + kStages * kXBytes);            // [128][17]
+  float* srope = tile + MT * (XR + 1);                       // [16][128] RoPE cos | sin of the rows' positions
+  uint64_t* full = (uint64_t*)(srope + XR * HD);
+  uint64_t* empty = full + kStages;
+  uint64_t* acc_full = empty + kStages;
+  uint64_t* acc_empty = acc_full + kAcc;
+  uint32_t* tmem_slot = (uint32_t*)(acc_empty + kAcc);
+  int* last_flag = (int*)(tmem_slot + 1);
+  float* rn = (float*)(tmem_slot + 4);                       // [16] row norms of the phase
+  float* red = rn + XR;                                      // [4][16] epilogue reductions
+  unsigned long long* kred = (unsigned long long*)(red + 4 * XR);  // [16][4]
+  volatile int* ready_ph = (volatile int*)(kred + 4 * XR);    // last phase whose grid barrier was passed
+  RowMeta* srows = (RowMeta*)(kred + 4 * XR + 2);            // [16] rows of the tick
+  uint64_t* abar = (uint64_t*)(srows + XR);                  // [kAttnSlots] K/V staging barriers
+  volatile int* qseq = (volatile int*)(abar + kAttnSlots);   // [kQueue] chunk queue: sequence numbers
+  volatile int* qval = qseq + kQueue;                        // [kQueue] chunk ids
+  AttnItem* sitems = (AttnItem*)(qval + kQueue);             // [kMaxPairs] items of this CTA's pairs
+  ItemRow* sirows = (ItemRow*)(sitems + kMaxPairs);          // [kMaxPairs][16] their query rows
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = gridDim.x;
+  const int P = n_phases(a);
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < kStages; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < kAcc; i++) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], 1);
+    }
+    for (int i = 0; i < kAttnSlots; i++) mbar_init(&abar[i], 1);
+    for (int i = 0; i < kQueue; i++) qseq[i] = -1;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    *ready_ph = -1;
+  }
+  if (threadIdx.x >= 64) {  // per-tick constants: rows, their RoPE rows, this CTA's attention items
+    const int et = threadIdx.x - 64;
+    if (et < a.B) srows[et] = a.rows[et];
+    for (int b = 0; b < a.B; b++) srope[b * HD + et] = __ldg(a.rope + (size_t)a.rows[b].pos * HD + et);
+    const int n_pairs = a.hdr[1] * a.H;
+    for (int j = 0; j < kMaxPairs; j++) {
+      const int pr = blockIdx.x + j * gridDim.x;
+      if (pr >= n_pairs) break;
+      const AttnItem it = a.items[pr / a.H];
+      if (et == 0) sitems[j] = it;
+      if (et < it.row_count) sirows[j * XR + et] = a.item_rows[it.row_begin + et];
+    }
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
+                 "n"(kAcc * XR));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  // the roles read their arguments from a shared-memory copy (fast, and it keeps
+  // kernel-parameter addresses out of the non-inlined role functions)
+  const Args& as = *sargs;
+  if (warp == 0) {
+    if (lane == 0) role_producer(as, smem, map_xg, map_attn, map_act);
+  } else if (warp == 1) {
+    if (lane == 0) role_mma(as, smem, tmem);
+  } else {
+    role_epilogue(as, smem, tmem);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();

@@ -795,7 +795,7 @@ void create_lane(fe_engine* e, Lane& ln, int id, int rows, int priority) {
   ln.ws.attn = e->dalloc(R * std::max(d, F) * el);
   ln.max_partials = (int)std::min<size_t>(R * (size_t)(m.max_pos / FE_PAGE), 65536);
   ln.max_items = ln.max_partials;
-  ln.ws.partial = (float*)e->dalloc((size_t)ln.max_partials * m.H * (m.hd + 2) * 4);
+  ln.ws.partial = (float*)e->dalloc((size_t)ln.max_partials * m.H * (m.hd + 4) * 4);  // decode_mk: hd + 4 records
   ln.ws.part_keys = (unsigned long long*)e->dalloc(R * (size_t)fe::lm_head_ctas(m) * 8);
   ln.ws.logits = id == 0 ? e->logits : nullptr;
   ln.attn_counters = (int*)e->dalloc(R * m.H * sizeof(int));

@@ -1,5 +1,9 @@
-"""Extract per-launch DRAM traffic of the decode GEMM from an ncu --set full
-report into profiles/ncu_decode_gemv.json (read by bench.py's roofline)."""
+"""Extract per-launch DRAM traffic of the dominant decode kernel from an ncu
+--set full report into profiles/ncu_decode_tick.json (persistent decode-tick
+kernel) or profiles/ncu_decode_gemv.json (kernel chain); read by bench.py's
+roofline `traffic`.
+
+    python tools/ncu_traffic.py gpurun_out/prof_tick.ncu-rep profiles/ncu_decode_tick.json"""
 import csv
 import io
 import json
@@ -12,9 +16,17 @@ rows = list(csv.reader(io.StringIO(raw)))
 hdr = rows[0]
 names = {12288: "qkv", 4096: "o/down", 22016: "gate_up", 32064: "lm_head"}
 launches = []
+units = dict(zip(hdr, rows[1]))
+SCALE = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3,            # -> MB
+         "nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6,
+         "ns": 1e-3, "us": 1.0, "ms": 1e3, "s": 1e6}                          # -> us
 for r in rows[2:]:
     d = dict(zip(hdr, r))
-    f = lambda k: float(d[k].replace(",", "")) if d.get(k) not in (None, "") else None
+
+    def f(k, d=d):
+        if d.get(k) in (None, ""):
+            return None
+        return float(d[k].replace(",", "")) * SCALE.get(units.get(k, ""), 1.0)
     rd, wr = f("dram__bytes_read.sum"), f("dram__bytes_write.sum")
     launches.append({
         "kernel": d["Kernel Name"].split("(")[0].split("::")[-1], "grid": d["Grid Size"],
