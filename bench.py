@@ -63,14 +63,8 @@ def parse():
 
 # --------------------------------------------------------------------------
 def dist_setup(backend: str):
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        import torch.distributed as dist
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group(backend=backend)
-    return rank, world, local
+    from paper_2506_07639_b200.distributed import init_from_env
+    return init_from_env(backend)
 
 
 def barrier(world):
@@ -90,12 +84,8 @@ def all_max(x: float, world: int) -> float:
 
 
 def gather_objects(obj, world):
-    if world == 1:
-        return [obj]
-    import torch.distributed as dist
-    out = [None] * world
-    dist.all_gather_object(out, obj)
-    return out
+    from paper_2506_07639_b200.distributed import gather_to_all
+    return gather_to_all(obj, world)
 
 
 class ClockSampler:
@@ -299,7 +289,8 @@ def run_engine(args, rank, world, local):
     stream = torch.cuda.ExternalStream(eng.stream_handle(), device=local)
     cfg_run = S.SchedulerConfig(mode=args.mode, slots=8, wall_clock=True)
     if args.episodes > 1:  # config 4: this rank's shard of the episodes, one batch per timestep
-        local_seeds = [e for e in range(args.episodes) if e % world == rank]
+        from paper_2506_07639_b200.distributed import shard_episodes
+        local_seeds = shard_episodes(list(range(args.episodes)), world, rank)
         runner = S.BatchedEpisodes(cfg_run, backend, schema, local_seeds)
     else:
         runner = S.make_runner(cfg_run, backend, schema)
