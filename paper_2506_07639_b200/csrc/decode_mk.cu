@@ -106,6 +106,7 @@ struct Args {
   float* logits;
   unsigned long long* bar;
   int flags;                  // diagnostics (engine option "mk_flags")
+  int pf_stages;              // weight stages prefetched ahead of a phase's grid barrier (<= kStages)
   int* grab;                  // [P] chunk counters of the GEMM phases (reset by the last CTA to exit)
   unsigned long long* trace;  // diagnostics: [P][6][G] globaltimer: barrier pass, phase done, last weight load issued,
                              // first / last accumulator ready, segments drained
@@ -568,6 +569,8 @@ __device__ __forceinline__ void tile_epilogue(const Args& a, int kind, int l, in
   volatile int* qval = qseq + kQueue; \
   AttnItem* sitems = (AttnItem*)(qval + kQueue); \
   ItemRow* sirows = (ItemRow*)(sitems + kMaxPairs); \
+  int* pend_slot = (int*)(sirows + kMaxPairs * XR); \
+  int* pend_kb = pend_slot + kStages; \
   (void)0
 
 __device__ __noinline__ void epi_embed(const Args& a, unsigned char* smem, int ph, int l, int kind) {
@@ -804,27 +807,21 @@ __device__ __noinline__ void epi_reduce(const Args& a, unsigned char* smem, int 
 #pragma unroll
         for (int q4 = 0; q4 < XR / 4; q4++) acc4[q4] = make_float4(0.f, 0.f, 0.f, 0.f);
         const size_t q0 = (size_t)tl * p.nc;
-        if (B <= 8) {  // 12 chunks x 2 float4 in flight
-          for (int c0 = 0; c0 < p.nc; c0 += 12) {
-            float4 v[12][2];
-#pragma unroll
-            for (int u = 0; u < 12; u++) {
-              const float4* src = reinterpret_cast<const float4*>(a.partial) + (q0 + c0 + u) * (XR / 4) * MT + r;
-              if (c0 + u < p.nc) {
-                v[u][0] = __ldcg(src);
-                v[u][1] = B > 4 ? __ldcg(src + MT) : make_float4(0.f, 0.f, 0.f, 0.f);
-              }
-            }
-#pragma unroll
-            for (int u = 0; u < 12; u++)
-              if (c0 + u < p.nc) {
-#pragma unroll
-                for (int q4 = 0; q4 < 2; q4++) {
-                  acc4[q4].x += v[u][q4].x; acc4[q4].y += v[u][q4].y;
-                  acc4[q4].z += v[u][q4].z; acc4[q4].w += v[u][q4].w;
-                }
-              }
-          }
+        if (B <= 8 && p.nc <= 16) {  // every chunk's 2 float4 requested together (straight-line registers)
+          const float4* src = reinterpret_cast<const float4*>(a.partial) + q0 * (XR / 4) * MT + r;
+          const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+          const int nc = p.nc;
+          const bool two = B > 4;
+#define MK_P(u) const float4 pa##u = u < nc ? __ldcg(src + (size_t)(u) * (XR / 4) * MT) : z; \
+                const float4 pb##u = (u < nc && two) ? __ldcg(src + (size_t)(u) * (XR / 4) * MT + MT) : z;
+          MK_P(0) MK_P(1) MK_P(2) MK_P(3) MK_P(4) MK_P(5) MK_P(6) MK_P(7)
+          MK_P(8) MK_P(9) MK_P(10) MK_P(11) MK_P(12) MK_P(13) MK_P(14) MK_P(15)
+#undef MK_P
+#define MK_S(u) acc4[0].x += pa##u.x; acc4[0].y += pa##u.y; acc4[0].z += pa##u.z; acc4[0].w += pa##u.w; \
+                acc4[1].x += pb##u.x; acc4[1].y += pb##u.y; acc4[1].z += pb##u.z; acc4[1].w += pb##u.w;
+          MK_S(0) MK_S(1) MK_S(2) MK_S(3) MK_S(4) MK_S(5) MK_S(6) MK_S(7)
+          MK_S(8) MK_S(9) MK_S(10) MK_S(11) MK_S(12) MK_S(13) MK_S(14) MK_S(15)
+#undef MK_S
         } else {
           for (int c0 = 0; c0 < p.nc; c0 += 4) {
             float4 v[4][XR / 4];
@@ -880,7 +877,6 @@ __device__ __noinline__ void role_producer(const Args& a, unsigned char* smem, c
       // ---------------- TMA producer
       const uint64_t wpol = policy_evict_first();  // weights are read once per tick
       int it = 0, n = 0;
-      int pend_slot[kStages], pend_kb[kStages];
       for (int ph = 0; ph < P; ph++) {
         int l;
         const int kind = phase_kind(a, ph, &l);
@@ -916,7 +912,7 @@ __device__ __noinline__ void role_producer(const Args& a, unsigned char* smem, c
           chunk_range(p, q, &tl, &j, &kb0, &kb1);
           for (int kb = kb0; kb < kb1; kb++, it++) {
             const int s = it % kStages;
-            if (!ready && npend == kStages) {  // the slot to refill is still waiting for its activations
+            if (!ready && npend == a.pf_stages) {  // prefetch depth reached (<= kStages: the slot to refill waits)
               wait_ready(ready_ph, ph);
               flush();
             }
@@ -1025,7 +1021,11 @@ __device__ __noinline__ void role_epilogue(const Args& a, unsigned char* smem, u
       else epi_reduce(a, smem, ph, l, kind);
       // ---- phase done: publish and arrive at the grid barrier
       if (ph + 1 < P) {
-        fence_proxy_async();  // generic-proxy writes read by the next phase's TMA / bulk loads
+        // (generic writes consumed by the next phase's TMA loads: the consumer
+        // side orders them -- the producer issues fence.proxy.async after it
+        // observes the barrier -- so no proxy fence here, which would also wait
+        // for this SM's in-flight weight prefetch)
+        if (a.flags & 16) fence_proxy_async();
         __threadfence();
         epi_sync();
         if (et == 0) {
@@ -1067,6 +1067,8 @@ __global__ void __launch_bounds__(kThreads, 1) decode_mk_kernel(const __grid_con
   volatile int* qval = qseq + kQueue;                        // [kQueue] chunk ids
   AttnItem* sitems = (AttnItem*)(qval + kQueue);             // [kMaxPairs] items of this CTA's pairs
   ItemRow* sirows = (ItemRow*)(sitems + kMaxPairs);          // [kMaxPairs][16] their query rows
+  int* pend_slot = (int*)(sirows + kMaxPairs * XR);          // [kStages] producer: stages awaiting activations
+  int* pend_kb = pend_slot + kStages;                        // [kStages] their k-blocks
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = gridDim.x;
@@ -1149,9 +1151,11 @@ int mk_grid() {
   return n_sm;
 }
 
-MkPlan mk_plan(int tiles, int kb_total) {
-  // ~8 k-blocks (128 KB of weights, ~3 us of one SM's HBM share) per chunk
-  const int nc = std::min(12, std::max(1, (kb_total + 4) / 8));  // <= 12: one load round in the reduction
+MkPlan mk_plan(int tiles, int kb_total, int grid) {
+  // enough chunks for ~4 per CTA (dynamic balance), at least 4 k-blocks each,
+  // at most 16 per tile (one load round in the reduction)
+  int nc = (4 * grid + tiles - 1) / tiles;
+  nc = std::max(1, std::min({nc, 16, std::max(1, kb_total / 4)}));
   return MkPlan{tiles, kb_total, nc, tiles * nc};
 }
 
@@ -1183,6 +1187,7 @@ void launch_decode_mk(const MkLaunch& l, cudaStream_t s) {
   a.part_keys = l.part_keys; a.logits = l.logits; a.bar = l.bar; a.trace = l.trace;
   a.grab = l.grab;
   a.flags = l.flags;
+  a.pf_stages = std::max(1, std::min(kStages, l.pf_stages > 0 ? l.pf_stages : kStages));
   decode_mk_kernel<<<l.grid, kThreads, kSmem, s>>>(*reinterpret_cast<const CUtensorMap*>(l.map_xg.bytes),
                                                    *reinterpret_cast<const CUtensorMap*>(l.map_attn.bytes),
                                                    *reinterpret_cast<const CUtensorMap*>(l.map_act.bytes), a);

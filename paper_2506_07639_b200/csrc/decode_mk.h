@@ -56,10 +56,11 @@ struct MkLaunch {
   unsigned long long* bar;       // [2]: grid barrier arrivals, exits (self-resetting)
   int* grab;                     // [phases] chunk counters (self-resetting)
   int flags;                     // diagnostics: 1 = no weight prefetch across grid barriers
+  int pf_stages;                 // weight stages prefetched ahead of a grid barrier (0 = whole ring)
   unsigned long long* trace;     // diagnostics (null): [phases][2][grid] globaltimer at barrier pass / phase end
 };
 
-MkPlan mk_plan(int tiles, int kb_total);
+MkPlan mk_plan(int tiles, int kb_total, int grid);
 size_t mk_partial_floats(const MkPlan* plans);
 void launch_decode_mk(const MkLaunch& l, cudaStream_t s);
 int mk_grid();

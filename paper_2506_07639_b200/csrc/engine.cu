@@ -191,6 +191,7 @@ struct fe_engine {
   size_t mk_trace_n = 0;
   bool mk_trace_on = false;
   int mk_flags = 0;
+  int mk_pf_stages = 0;  // 0 = the whole ring
   bool graphs_on = true;
   float* op_partial = nullptr;  // fe_op_skinny_tc scratch
   size_t op_bytes = 0;
@@ -394,6 +395,7 @@ void launch_layers(fe_engine* e, Lane& ln, const fe::Fwd& f, int n, bool decode,
     k.trace = e->mk_trace_on ? e->mk_trace : nullptr;
     k.grab = ln.mk_grab;
     k.flags = e->mk_flags;
+    k.pf_stages = e->mk_pf_stages;
     const int p = prof_begin(e, ln, PROF_TICK);
     fe::launch_decode_mk(k, st);
     // algorithmic bytes of the tick: every weight once, the K/V pages the
@@ -907,11 +909,11 @@ fe_engine* create(const fe_config* c, int device, const float* rope_host) {
     e->mk_on = e->use_tc && m.H * m.hd == m.d && m.d % 512 == 0;
     if (e->mk_on) {
       e->mk_grid = fe::mk_grid();
-      e->mk_plans[fe::MK_QKV] = fe::mk_plan(3 * m.d / 128, m.d / 64);
-      e->mk_plans[fe::MK_O] = fe::mk_plan(m.d / 128, m.d / 64);
-      e->mk_plans[fe::MK_GU] = fe::mk_plan(m.F / 64, m.d / 64);
-      e->mk_plans[fe::MK_DOWN] = fe::mk_plan(m.d / 128, m.F / 64);
-      e->mk_plans[fe::MK_LM] = fe::mk_plan((m.V + 127) / 128, m.d / 64);
+      e->mk_plans[fe::MK_QKV] = fe::mk_plan(3 * m.d / 128, m.d / 64, e->mk_grid);
+      e->mk_plans[fe::MK_O] = fe::mk_plan(m.d / 128, m.d / 64, e->mk_grid);
+      e->mk_plans[fe::MK_GU] = fe::mk_plan(m.F / 64, m.d / 64, e->mk_grid);
+      e->mk_plans[fe::MK_DOWN] = fe::mk_plan(m.d / 128, m.F / 64, e->mk_grid);
+      e->mk_plans[fe::MK_LM] = fe::mk_plan((m.V + 127) / 128, m.d / 64, e->mk_grid);
       std::vector<fe::TmaMap> maps(4 * m.L + 1);
       for (int l = 0; l < m.L; l++) {
         maps[4 * l + 0] = e->tc_maps[l].qkv;
@@ -1377,6 +1379,9 @@ int fe_set_option(fe_engine* e, const char* key, int64_t value) {
       clear_graphs(e);
     } else if (k == "mk_flags") {
       e->mk_flags = (int)value;
+      clear_graphs(e);
+    } else if (k == "mk_pf") {
+      e->mk_pf_stages = (int)value;
       clear_graphs(e);
     } else if (k == "mk") {
       e->mk_on = value != 0 && e->use_tc && e->mk_maps != nullptr;
