@@ -194,15 +194,25 @@ __device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, 128;" :::
 
 // out[b * ostride] = sum over the 128 tile rows of tile[c][b]^2 (b < B), fixed
 // order; the caller has synchronised the epilogue group after writing `tile`
-__device__ __forceinline__ void epi_sumsq_cols(const float* tile, int B, float* out, int ostride, int et) {
-  if (et < B) {
-    float acc = 0.0f;
-#pragma unroll 8
-    for (int c = 0; c < MT; c++) {
-      const float v = tile[c * (XR + 1) + et];
+__device__ __forceinline__ void epi_sumsq_cols(float* tile, float* red, int B, float* out, int ostride, int et) {
+  // 8 groups of 16 tile rows per column b (thread et: b = et & 15, group et >> 4),
+  // then the 8 group sums in order: short dependent chains, fixed order
+  const int b = et & 15, grp = et >> 4;
+  float acc = 0.0f;
+  if (b < B) {
+#pragma unroll
+    for (int c = 0; c < 16; c++) {
+      const float v = tile[(16 * grp + c) * (XR + 1) + b];
       acc = fmaf(v, v, acc);
     }
-    out[et * ostride] = acc;
+  }
+  red[grp * 16 + b] = acc;  // red: [8][16] scratch (rn / red / kred region)
+  epi_sync();
+  if (et < B) {
+    float t = 0.0f;
+#pragma unroll
+    for (int g2 = 0; g2 < 8; g2++) t += red[g2 * 16 + et];
+    out[et * ostride] = t;
   }
 }
 
@@ -522,13 +532,14 @@ __device__ __forceinline__ void tile_epilogue(const Args& a, int kind, int l, in
       a.x[(size_t)b * d + col] = xv;
       a.xg[(size_t)b * d + col] = __float2bfloat16_rn(xv * gw);
     }
-    epi_sumsq_cols(tile, B, a.ss + tl, a.d / MT, et);  // ss[row][tile]
+    epi_sumsq_cols(const_cast<float*>(tile), red, B, a.ss + tl, a.d / MT, et);  // ss[row][tile]
   } else if (kind == K_GU) {
     if (et < 64 && tl * 64 + et < a.F)
-#pragma unroll 1
-      for (int b = 0; b < B; b++)
-        a.attn[(size_t)b * a.F + tl * 64 + et] = __float2bfloat16_rn(
-            silu_mul(tile[et * (XR + 1) + b] * rn[b], tile[(et + 64) * (XR + 1) + b] * rn[b]));
+#pragma unroll 4
+      for (int b = 0; b < B; b++) {
+        const float gt = tile[et * (XR + 1) + b] * rn[b], up = tile[(et + 64) * (XR + 1) + b] * rn[b];
+        a.attn[(size_t)b * a.F + tl * 64 + et] = __float2bfloat16_rn(__fdividef(gt, 1.0f + __expf(-gt)) * up);
+      }
   } else {  // K_LM
     const int nrow = n0 + r;
     const bool row_ok = nrow < a.V;
@@ -561,7 +572,7 @@ __device__ __forceinline__ void tile_epilogue(const Args& a, int kind, int l, in
   int* last_flag = (int*)(tmem_slot + 1); \
   float* rn = (float*)(tmem_slot + 4); \
   float* red = rn + XR; \
-  unsigned long long* kred = (unsigned long long*)(red + 4 * XR); \
+  unsigned long long* kred = (unsigned long long*)(red + 8 * XR); \
   volatile int* ready_ph = (volatile int*)(kred + 4 * XR); \
   RowMeta* srows = (RowMeta*)(kred + 4 * XR + 2); \
   uint64_t* abar = (uint64_t*)(srows + XR); \
@@ -601,7 +612,7 @@ __device__ __noinline__ void epi_embed(const Args& a, unsigned char* smem, int p
           }
         }
         epi_sync();
-        epi_sumsq_cols(tile, B, a.ss + ct, n_ss, et);
+        epi_sumsq_cols(tile, red, B, a.ss + ct, n_ss, et);
         epi_sync();
       }
 }
@@ -623,16 +634,20 @@ __device__ __noinline__ void epi_attn(const Args& a, unsigned char* smem, int ph
       if (a.trace && et == 0) a.trace[((size_t)ph * 6 + 2) * G + blockIdx.x] = gtimer();
       for (int base = blockIdx.x, round = 0; base < n_pairs; base += kAttnSlots * G, round++) {
         auto item_of = [&](int j, int pr) -> AttnItem { return round == 0 ? sitems[j] : a.items[pr / a.H]; };
-        // all 128 threads stage K and V of every pair of the round with 16-byte
-        // cp.async (rows 256 B, 16-byte chunks XOR-swizzled by key & 7: the
-        // fragment reads below are bank-conflict free)
-        for (int j = 0; j < kAttnSlots && base + j * G < n_pairs; j++) {
+        // each warp stages K and V of its own pairs (j = warp, warp + 4) with
+        // 16-byte cp.async, one commit group per pair (rows 256 B, 16-byte chunks
+        // XOR-swizzled by key & 7: the fragment reads are bank-conflict free), and
+        // starts computing as soon as its first pair has landed
+        const int w = et >> 5;
+        int ngroups = 0;
+        for (int j = w; j < kAttnSlots; j += 4) {
           const int pr = base + j * G;
+          if (pr >= n_pairs) break;
           const AttnItem it = item_of(j, pr);
           const __nv_bfloat16* kg = pool_l + (size_t)it.page * a.page_elems + (size_t)(pr % a.H) * FE_PAGE * HD;
           const __nv_bfloat16* vg = kg + (size_t)a.H * FE_PAGE * HD;
           unsigned char* slot = sw + (size_t)j * kAttnSlotBytes;
-          for (int x = et; x < it.valid_max * 16; x += 128) {
+          for (int x = lane; x < it.valid_max * 16; x += 32) {
             const int key = x >> 4, c = x & 15;
             const uint32_t so = (uint32_t)(key * 256 + ((c ^ (key & 7)) << 4));
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(su32(slot + so)),
@@ -640,26 +655,21 @@ __device__ __noinline__ void epi_attn(const Args& a, unsigned char* smem, int ph
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(su32(slot + kAttnSlotBytes / 2 + so)),
                          "l"(vg + (size_t)key * HD + c * 8) : "memory");
           }
+          asm volatile("cp.async.commit_group;" ::: "memory");
+          ngroups++;
         }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-        // this warp's pairs j0, j0 + 4: the first one's Q is requested while K / V land
         uint4 q0[4], q1[4];
-        {
-          const int j0 = et >> 5, pr0 = base + j0 * G;
-          if (pr0 < n_pairs) {
-            const AttnItem it = item_of(j0, pr0);
-            attn_load_q(a, it, round == 0 ? sirows + j0 * XR : a.item_rows + it.row_begin, pr0 % a.H, lane, q0, q1);
-          }
-        }
-        asm volatile("cp.async.wait_all;" ::: "memory");
-        epi_sync();
-        if (a.trace && et == 0 && round == 0) a.trace[((size_t)ph * 6 + 3) * G + blockIdx.x] = gtimer();
-        for (int j = et >> 5; j < kAttnSlots; j += 4) {
+        int gi = 0;
+        for (int j = w; j < kAttnSlots; j += 4, gi++) {
           const int pr = base + j * G;
           if (pr >= n_pairs) break;
           const AttnItem it = item_of(j, pr);
           const ItemRow* irows = round == 0 ? sirows + j * XR : a.item_rows + it.row_begin;
-          if (j >= 4) attn_load_q(a, it, irows, pr % a.H, lane, q0, q1);
+          attn_load_q(a, it, irows, pr % a.H, lane, q0, q1);  // overlaps the K / V landing
+          if (ngroups - gi - 1 >= 1) asm volatile("cp.async.wait_group 1;" ::: "memory");
+          else asm volatile("cp.async.wait_group 0;" ::: "memory");
+          __syncwarp();
+          if (a.trace && et == 0 && round == 0 && gi == 0) a.trace[((size_t)ph * 6 + 3) * G + blockIdx.x] = gtimer();
           const unsigned char* slot = sw + (size_t)j * kAttnSlotBytes;
           unsigned long long* dbg = nullptr;  // diagnostics (flags & 4): sub-step times of CTA 0's first pair
           if ((a.flags & 4) && a.trace && blockIdx.x == 0 && et == 0 && j == 0 && round == 0)
@@ -1058,8 +1068,8 @@ __global__ void __launch_bounds__(kThreads, 1) decode_mk_kernel(const __grid_con
   uint32_t* tmem_slot = (uint32_t*)(acc_empty + kAcc);
   int* last_flag = (int*)(tmem_slot + 1);
   float* rn = (float*)(tmem_slot + 4);                       // [16] row norms of the phase
-  float* red = rn + XR;                                      // [4][16] epilogue reductions
-  unsigned long long* kred = (unsigned long long*)(red + 4 * XR);  // [16][4]
+  float* red = rn + XR;                                      // [8][16] epilogue reductions
+  unsigned long long* kred = (unsigned long long*)(red + 8 * XR);  // [16][4]
   volatile int* ready_ph = (volatile int*)(kred + 4 * XR);    // last phase whose grid barrier was passed
   RowMeta* srows = (RowMeta*)(kred + 4 * XR + 2);            // [16] rows of the tick
   uint64_t* abar = (uint64_t*)(srows + XR);                  // [kAttnSlots] K/V staging barriers
