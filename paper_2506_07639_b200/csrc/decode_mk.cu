@@ -387,6 +387,9 @@ __device__ void attn_pair(const Args& a, const RowMeta* srows, const AttnItem& i
   // o is transposed through the (no longer needed) K tile so each row leaves as one 512-byte store
   float* stg = reinterpret_cast<float*>(const_cast<unsigned char*>(ks));
   __syncwarp();
+  // V fragments by ldmatrix.x4.trans: matrices (keys 16kk + {0-7, 8-15}) x (dims 16np + {0-7, 8-15});
+  // lane L addresses row L & 7 of matrix L >> 3 (staged rows beyond valid_max are zero-filled)
+  const int lm = lane >> 3, lrow = lane & 7;
 #pragma unroll
   for (int half = 0; half < 2; half++) {
     float o[8][4];
@@ -395,31 +398,25 @@ __device__ void attn_pair(const Args& a, const RowMeta* srows, const AttnItem& i
 #pragma unroll
     for (int kk = 0; kk < 4; kk++) {
       if (16 * kk >= vmax) break;
-      // keys 16kk + 2t + {0, 1, 8, 9}, dims 16g + 8 half .. +7 (zero beyond the staged keys)
-      uint4 w[4];
+      const int key = 16 * kk + lrow + 8 * (lm & 1);
 #pragma unroll
-      for (int c = 0; c < 4; c++) {
-        const int key = 16 * kk + 2 * t + (c & 1) + 8 * (c >> 1);
-        w[c] = key < vmax ? *reinterpret_cast<const uint4*>(vs + (size_t)key * HD * 2 + (((2 * g + half) ^ (key & 7)) << 4))
-                          : make_uint4(0u, 0u, 0u, 0u);
-      }
-#pragma unroll
-      for (int nt = 0; nt < 8; nt++) {
-        const int k4 = nt >> 1;  // word of the 8-dim slice holding dim 16g + 8 half + nt
-        const uint32_t sel = (nt & 1) ? 0x7632u : 0x5410u;
-        auto word = [&](int c) -> uint32_t {
-          return k4 == 0 ? w[c].x : k4 == 1 ? w[c].y : k4 == 2 ? w[c].z : w[c].w;
-        };
-        mma_bf16(o[nt], pa[kk], __byte_perm(word(0), word(1), sel), __byte_perm(word(2), word(3), sel));
+      for (int q = 0; q < 4; q++) {
+        const int np = 4 * half + q;  // dims 16 np .. 16 np + 15 = n-tiles 2 np, 2 np + 1
+        const int c = 2 * np + (lm >> 1);
+        uint32_t b0, b1, b2, b3;
+        asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(b0), "=r"(b1), "=r"(b2), "=r"(b3)
+                     : "r"(su32(vs + (size_t)key * HD * 2 + ((c ^ (key & 7)) << 4))));
+        mma_bf16(o[2 * q], pa[kk], b0, b1);
+        mma_bf16(o[2 * q + 1], pa[kk], b2, b3);
       }
     }
-    // lane (g, t) holds dims 32t + 8 half + nt (c0/c2) and 32t + 16 + 8 half + nt (c1/c3) of rows g, g + 8
+    // n-tile nt of this half = dims 64 half + 8 nt .. +7; lane (g, t) holds columns 2t, 2t + 1 of rows g, g + 8
 #pragma unroll
     for (int nt = 0; nt < 8; nt++) {
-      stg[g * kStgStride + 32 * t + 8 * half + nt] = o[nt][0];
-      stg[g * kStgStride + 32 * t + 16 + 8 * half + nt] = o[nt][1];
-      stg[(g + 8) * kStgStride + 32 * t + 8 * half + nt] = o[nt][2];
-      stg[(g + 8) * kStgStride + 32 * t + 16 + 8 * half + nt] = o[nt][3];
+      const int dim = 64 * half + 8 * nt + 2 * t;
+      *reinterpret_cast<float2*>(stg + g * kStgStride + dim) = make_float2(o[nt][0], o[nt][1]);
+      *reinterpret_cast<float2*>(stg + (g + 8) * kStgStride + dim) = make_float2(o[nt][2], o[nt][3]);
     }
   }
   __syncwarp();
@@ -647,13 +644,17 @@ __device__ __noinline__ void epi_attn(const Args& a, unsigned char* smem, int ph
           const __nv_bfloat16* kg = pool_l + (size_t)it.page * a.page_elems + (size_t)(pr % a.H) * FE_PAGE * HD;
           const __nv_bfloat16* vg = kg + (size_t)a.H * FE_PAGE * HD;
           unsigned char* slot = sw + (size_t)j * kAttnSlotBytes;
-          for (int x = lane; x < it.valid_max * 16; x += 32) {
+          const int vpad = (it.valid_max + 15) & ~15;  // V rows up to the 16-key step: zero-filled
+          for (int x = lane; x < vpad * 16; x += 32) {
             const int key = x >> 4, c = x & 15;
             const uint32_t so = (uint32_t)(key * 256 + ((c ^ (key & 7)) << 4));
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(su32(slot + so)),
-                         "l"(kg + (size_t)key * HD + c * 8) : "memory");
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(su32(slot + kAttnSlotBytes / 2 + so)),
-                         "l"(vg + (size_t)key * HD + c * 8) : "memory");
+            const bool in = key < it.valid_max;
+            const int keyc = in ? key : 0;
+            if (in)
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(su32(slot + so)),
+                           "l"(kg + (size_t)keyc * HD + c * 8) : "memory");
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(su32(slot + kAttnSlotBytes / 2 + so)),
+                         "l"(vg + (size_t)keyc * HD + c * 8), "r"(in ? 16 : 0) : "memory");
           }
           asm volatile("cp.async.commit_group;" ::: "memory");
           ngroups++;
