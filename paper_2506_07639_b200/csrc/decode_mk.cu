@@ -62,13 +62,14 @@ constexpr int kStages = 11;
 constexpr int kAcc = 4;
 constexpr int kWBytes = MT * KBK * 2;      // 16 KB
 constexpr int kXBytes = XR * KBK * 2;      // 2 KB
-constexpr int kThreads = 192;
+constexpr int kThreads = 224;  // producer, MMA, 4 epilogue warps, helper
 constexpr int HD = 128;                    // head dim (7B shape)
 constexpr uint32_t kIdesc = idesc_bf16(MT, XR);
 // attention phase: the (idle) ring holds K and V of up to 6 (page, head) pairs
 constexpr int kAttnSlotBytes = 2 * FE_PAGE * HD * 2;  // 32 KB
 constexpr int kAttnSlots = kStages * (kWBytes + kXBytes) / kAttnSlotBytes;
 constexpr int kMaxPairs = kAttnSlots;
+constexpr int kRing = 64;            // event / task rings (entries in flight per CTA << 64)
 constexpr int kPartStride = HD + 4;  // attention chunk partial record: m, l, pad, pad, o[HD] (16-byte aligned)
 constexpr int kStgStride = HD + 4;   // o staging rows in shared memory  // (page, head) pairs per CTA whose items are cached in smem
 constexpr int kSmem = kStages * (kWBytes + kXBytes) + MT * (XR + 1) * 4 + XR * HD * 4 /* rope */ + 1024 /* align */ +
@@ -112,18 +113,32 @@ struct Args {
                              // first / last accumulator ready, segments drained
 };
 
-// per layer: QKV, RQKV, ATTN, AMERGE, O, RO, GU, RGU, DOWN, RDOWN (R* = split reduction + epilogue)
-constexpr int kLayerPhases = 10;
-__device__ __forceinline__ int n_phases(const Args& a) { return 4 + kLayerPhases * a.L; }
+// per layer: QKV, RQKV, ATTN, AMERGE, O, RO, GU, DOWN, RDOWN.  Gate/up and
+// lm_head (many tiles) finalise their tiles progressively inside the GEMM
+// phase (role_helper); QKV, O and down (few, long-K tiles whose chunks all
+// land at the end) reduce in a separate phase, which measured faster.
+constexpr int kLayerPhases = 9;
+__device__ __forceinline__ int n_phases(const Args& a) { return 3 + kLayerPhases * a.L; }
 __device__ __forceinline__ int phase_kind(const Args& a, int ph, int* layer) {
   *layer = 0;
   if (ph == 0) return K_EMBED;
   if (ph == 1 + kLayerPhases * a.L) return K_LM;
-  if (ph == 2 + kLayerPhases * a.L) return K_RLM;
-  if (ph == 3 + kLayerPhases * a.L) return K_FINAL;
+  if (ph == 2 + kLayerPhases * a.L) return K_FINAL;
   *layer = (ph - 1) / kLayerPhases;
-  return K_QKV + (ph - 1) % kLayerPhases;  // K_QKV .. K_RDOWN are consecutive
+  switch ((ph - 1) % kLayerPhases) {
+    case 0: return K_QKV;
+    case 1: return K_RQKV;
+    case 2: return K_ATTN;
+    case 3: return K_AMERGE;
+    case 4: return K_O;
+    case 5: return K_RO;
+    case 6: return K_GU;
+    case 7: return K_DOWN;
+    default: return K_RDOWN;
+  }
 }
+// GEMMs whose tiles are finalised inside their own phase
+__device__ __forceinline__ bool fused_reduce(int kind) { return kind == K_GU || kind == K_LM; }
 // the GEMM whose chunk partials a reduction phase finalises
 __device__ __forceinline__ int gemm_kind_of_reduce(int kind) {
   return kind == K_RQKV ? K_QKV : kind == K_RO ? K_O : kind == K_RGU ? K_GU : kind == K_RDOWN ? K_DOWN
@@ -579,6 +594,11 @@ __device__ __forceinline__ void tile_epilogue(const Args& a, int kind, int l, in
   ItemRow* sirows = (ItemRow*)(sitems + kMaxPairs); \
   int* pend_slot = (int*)(sirows + kMaxPairs * XR); \
   int* pend_kb = pend_slot + kStages; \
+  volatile int* evq = (volatile int*)(pend_kb + kStages); \
+  volatile int* taskq = evq + kRing; \
+  volatile int* ev_cnt = taskq + kRing; \
+  volatile int* task_cnt = ev_cnt + 1; \
+  volatile int* task_snap = ev_cnt + 2; \
   (void)0
 
 __device__ __noinline__ void epi_embed(const Args& a, unsigned char* smem, int ph, int l, int kind) {
@@ -728,7 +748,10 @@ __device__ __noinline__ void epi_final(const Args& a, unsigned char* smem, int p
       }
 }
 
-__device__ __noinline__ void epi_gemm(const Args& a, unsigned char* smem, int ph, int l, int kind, uint32_t tmem, int& lu, int& n) {
+__device__ __noinline__ void finalize_tile(const Args& a, unsigned char* smem, int l, int gk, int tl);
+
+__device__ __noinline__ void epi_gemm(const Args& a, unsigned char* smem, int ph, int l, int kind, uint32_t tmem, int& lu, int& n,
+                                      int& task_r) {
   MK_SMEM_LAYOUT(smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = gridDim.x;
@@ -740,6 +763,32 @@ __device__ __noinline__ void epi_gemm(const Args& a, unsigned char* smem, int ph
       // ---- GEMM phase: drain each grabbed chunk's accumulator into its partial
       // slot (no synchronisation; the grid barrier publishes them)
       const MkPlan p = a.plan[gemm_of(kind)];
+      const bool scaled = kind == K_QKV || kind == K_GU || kind == K_LM;
+      if (fused_reduce(kind) && scaled && et < B) {  // row norms r = rsqrt(sum x^2 / d + eps) of this GEMM's input
+        const float4* sr = reinterpret_cast<const float4*>(a.ss + (size_t)et * n_ss);
+        float sacc = 0.0f;
+        for (int u = 0; u < n_ss / 4; u++) {
+          const float4 v = __ldcg(sr + u);
+          sacc += (v.x + v.y) + (v.z + v.w);
+        }
+        rn[et] = rsqrtf(sacc / (float)d + a.eps);
+      }
+      const bool fused = fused_reduce(kind);
+      bool phase_tasks_done = false;
+      const int ev_w_base = 0;
+      (void)ev_w_base;
+      // tasks (tiles to finalise) are consumed in order; task_r: next to run
+      auto run_tasks = [&](int upto) {
+        while (task_r < upto) {
+          const int tl = taskq[task_r % kRing];
+          task_r++;
+          if (tl < 0) {
+            phase_tasks_done = true;
+            break;
+          }
+          finalize_tile(a, smem, l, kind, tl);
+        }
+      };
       bool first_chunk = true;
       for (;; lu++) {
         const int q = queue_read(qseq, qval, n++);
@@ -770,8 +819,10 @@ __device__ __noinline__ void epi_gemm(const Args& a, unsigned char* smem, int ph
             : "r"(tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(acc * XR)));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        if (et == 0) *task_snap = *task_cnt;
         epi_sync();
         if (et == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&acc_empty[acc])) : "memory");
+        const int tasks_now = *task_snap;
         // partial layout [chunk][batch rows / 4][128 weight rows] float4: coalesced
         float4* dst = reinterpret_cast<float4*>(a.partial) + (size_t)q * (XR / 4) * MT + r;
 #pragma unroll
@@ -781,98 +832,169 @@ __device__ __noinline__ void epi_gemm(const Args& a, unsigned char* smem, int ph
                                          __uint_as_float(raw[4 * q4 + 1]) + xo[4 * q4 + 1],
                                          __uint_as_float(raw[4 * q4 + 2]) + xo[4 * q4 + 2],
                                          __uint_as_float(raw[4 * q4 + 3]) + xo[4 * q4 + 3]));
+        if (fused) {
+          epi_sync();  // the chunk's partial is issued by every thread before the helper's release
+          if (et == 0) {
+            evq[*ev_cnt % kRing] = tl;
+            __threadfence_block();
+            *ev_cnt = *ev_cnt + 1;
+          }
+          run_tasks(tasks_now);  // tiles completed meanwhile (uniform: snapshot taken before the sync)
+        }
       }
       if (a.trace && et == 0) a.trace[((size_t)ph * 6 + 5) * G + blockIdx.x] = gtimer();
+      // no more chunks: tell the helper, then finalise the remaining tasks of this phase
+      if (!fused) return;
+      if (et == 0) {
+        evq[*ev_cnt % kRing] = -1;
+        __threadfence_block();
+        *ev_cnt = *ev_cnt + 1;
+      }
+      while (!phase_tasks_done) {
+        if (et == 0) {
+          const int seen = task_r;
+          if (*task_cnt <= seen) {
+            const uint64_t t0 = gtimer();
+            unsigned spins = 0;
+            while (*task_cnt <= seen)
+              if (++spins % 1024 == 0 && gtimer() - t0 > 2000000000ull) __trap();
+          }
+          __threadfence_block();
+          *task_snap = *task_cnt;
+        }
+        epi_sync();
+        const int upto = *task_snap;
+        epi_sync();  // task_snap may be rewritten next iteration
+        run_tasks(upto);
+      }
 }
 
-__device__ __noinline__ void epi_reduce(const Args& a, unsigned char* smem, int ph, int l, int kind) {
+// Reduction + fused epilogue of one tile whose nc chunk partials have all
+// landed: sum in chunk order (deterministic), then RoPE + q / paged K/V,
+// residual + norm inputs, SiLU * up or argmax keys (tile_epilogue).  rn holds
+// the phase's row norms.
+__device__ __noinline__ void finalize_tile(const Args& a, unsigned char* smem, int l, int gk, int tl) {
   MK_SMEM_LAYOUT(smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int G = gridDim.x;
   const int et = threadIdx.x - 64;
   const int r = 32 * (warp & 3) + lane;
-  const int d = a.d, B = a.B;
-  const int n_ss = d / MT;
-  (void)r; (void)d; (void)B; (void)n_ss; (void)G;
-      // ---- reduction phase: the tiles t = cta (mod grid) of the GEMM just done:
-      // sum the nc chunk partials in chunk order (deterministic), then the fused
-      // epilogue (RoPE + q / paged K/V, residual + norm inputs, SiLU * up, argmax).
-      // The norm sums, gain column and partials are all requested in one round.
-      const int gk = gemm_kind_of_reduce(kind);
-      const MkPlan p = a.plan[gemm_of(gk)];
-      const bool scaled = gk == K_QKV || gk == K_GU || gk == K_LM;
-      const bool resid = gk == K_O || gk == K_DOWN;
-      const float* gnext = gk == K_O ? a.norms[2 * l + 1]
-                           : gk == K_DOWN ? (l + 1 < a.L ? a.norms[2 * (l + 1)] : a.norms[2 * a.L]) : nullptr;
-      if (a.trace && et == 0) a.trace[((size_t)ph * 6 + 2) * G + blockIdx.x] = gtimer();
-      float4 sv[8];
-      const bool need_ss = scaled && et < B && blockIdx.x < p.tiles;
-      if (need_ss) {
-        const float4* sr = reinterpret_cast<const float4*>(a.ss + (size_t)et * n_ss);
-#pragma unroll
-        for (int u = 0; u < 8; u++) sv[u] = 4 * u < n_ss ? __ldcg(sr + u) : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-      for (int tl = blockIdx.x; tl < p.tiles; tl += G) {
+  const int B = a.B;
+  const MkPlan p = a.plan[gemm_of(gk)];
+  const bool resid = gk == K_O || gk == K_DOWN;
+  const float* gnext = gk == K_O ? a.norms[2 * l + 1]
+                       : gk == K_DOWN ? (l + 1 < a.L ? a.norms[2 * (l + 1)] : a.norms[2 * a.L]) : nullptr;
         const float gw = resid ? __ldg(gnext + tl * MT + r) : 0.0f;
-        float4 acc4[XR / 4];
+  float4 acc4[XR / 4];
 #pragma unroll
-        for (int q4 = 0; q4 < XR / 4; q4++) acc4[q4] = make_float4(0.f, 0.f, 0.f, 0.f);
-        const size_t q0 = (size_t)tl * p.nc;
-        if (B <= 8 && p.nc <= 16) {  // every chunk's 2 float4 requested together (straight-line registers)
-          const float4* src = reinterpret_cast<const float4*>(a.partial) + q0 * (XR / 4) * MT + r;
-          const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-          const int nc = p.nc;
-          const bool two = B > 4;
+  for (int q4 = 0; q4 < XR / 4; q4++) acc4[q4] = make_float4(0.f, 0.f, 0.f, 0.f);
+  const size_t q0 = (size_t)tl * p.nc;
+  if (B <= 8 && p.nc <= 16) {  // every chunk's 2 float4 requested together (straight-line registers)
+    const float4* src = reinterpret_cast<const float4*>(a.partial) + q0 * (XR / 4) * MT + r;
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int nc = p.nc;
+    const bool two = B > 4;
 #define MK_P(u) const float4 pa##u = u < nc ? __ldcg(src + (size_t)(u) * (XR / 4) * MT) : z; \
-                const float4 pb##u = (u < nc && two) ? __ldcg(src + (size_t)(u) * (XR / 4) * MT + MT) : z;
-          MK_P(0) MK_P(1) MK_P(2) MK_P(3) MK_P(4) MK_P(5) MK_P(6) MK_P(7)
-          MK_P(8) MK_P(9) MK_P(10) MK_P(11) MK_P(12) MK_P(13) MK_P(14) MK_P(15)
+          const float4 pb##u = (u < nc && two) ? __ldcg(src + (size_t)(u) * (XR / 4) * MT + MT) : z;
+    MK_P(0) MK_P(1) MK_P(2) MK_P(3) MK_P(4) MK_P(5) MK_P(6) MK_P(7)
+    MK_P(8) MK_P(9) MK_P(10) MK_P(11) MK_P(12) MK_P(13) MK_P(14) MK_P(15)
 #undef MK_P
 #define MK_S(u) acc4[0].x += pa##u.x; acc4[0].y += pa##u.y; acc4[0].z += pa##u.z; acc4[0].w += pa##u.w; \
-                acc4[1].x += pb##u.x; acc4[1].y += pb##u.y; acc4[1].z += pb##u.z; acc4[1].w += pb##u.w;
-          MK_S(0) MK_S(1) MK_S(2) MK_S(3) MK_S(4) MK_S(5) MK_S(6) MK_S(7)
-          MK_S(8) MK_S(9) MK_S(10) MK_S(11) MK_S(12) MK_S(13) MK_S(14) MK_S(15)
+          acc4[1].x += pb##u.x; acc4[1].y += pb##u.y; acc4[1].z += pb##u.z; acc4[1].w += pb##u.w;
+    MK_S(0) MK_S(1) MK_S(2) MK_S(3) MK_S(4) MK_S(5) MK_S(6) MK_S(7)
+    MK_S(8) MK_S(9) MK_S(10) MK_S(11) MK_S(12) MK_S(13) MK_S(14) MK_S(15)
 #undef MK_S
-        } else {
-          for (int c0 = 0; c0 < p.nc; c0 += 4) {
-            float4 v[4][XR / 4];
+  } else {
+    for (int c0 = 0; c0 < p.nc; c0 += 4) {
+      float4 v[4][XR / 4];
 #pragma unroll
-            for (int u = 0; u < 4; u++)
+      for (int u = 0; u < 4; u++)
 #pragma unroll
-              for (int q4 = 0; q4 < XR / 4; q4++)
-                if (c0 + u < p.nc && 4 * q4 < B)
-                  v[u][q4] = __ldcg(reinterpret_cast<const float4*>(a.partial) + ((q0 + c0 + u) * (XR / 4) + q4) * MT + r);
+        for (int q4 = 0; q4 < XR / 4; q4++)
+          if (c0 + u < p.nc && 4 * q4 < B)
+            v[u][q4] = __ldcg(reinterpret_cast<const float4*>(a.partial) + ((q0 + c0 + u) * (XR / 4) + q4) * MT + r);
 #pragma unroll
-            for (int u = 0; u < 4; u++)
+      for (int u = 0; u < 4; u++)
 #pragma unroll
-              for (int q4 = 0; q4 < XR / 4; q4++)
-                if (c0 + u < p.nc && 4 * q4 < B) {
-                  acc4[q4].x += v[u][q4].x; acc4[q4].y += v[u][q4].y;
-                  acc4[q4].z += v[u][q4].z; acc4[q4].w += v[u][q4].w;
-                }
+        for (int q4 = 0; q4 < XR / 4; q4++)
+          if (c0 + u < p.nc && 4 * q4 < B) {
+            acc4[q4].x += v[u][q4].x; acc4[q4].y += v[u][q4].y;
+            acc4[q4].z += v[u][q4].z; acc4[q4].w += v[u][q4].w;
           }
-        }
-        if (tl == blockIdx.x && need_ss) {
-          float sacc = 0.0f;
+    }
+  }
 #pragma unroll
-          for (int u = 0; u < 8; u++) sacc += (sv[u].x + sv[u].y) + (sv[u].z + sv[u].w);
-          for (int t4 = 32; t4 < n_ss; t4++) sacc += __ldcg(a.ss + (size_t)et * n_ss + t4);  // d > 4096 only
-          rn[et] = rsqrtf(sacc / (float)d + a.eps);
-        }
-#pragma unroll
-        for (int q4 = 0; q4 < XR / 4; q4++) {
-          tile[r * (XR + 1) + 4 * q4] = acc4[q4].x;
-          tile[r * (XR + 1) + 4 * q4 + 1] = acc4[q4].y;
-          tile[r * (XR + 1) + 4 * q4 + 2] = acc4[q4].z;
-          tile[r * (XR + 1) + 4 * q4 + 3] = acc4[q4].w;
-        }
-        epi_sync();  // tile and rn visible
-        if (a.trace && et == 0 && tl == blockIdx.x) a.trace[((size_t)ph * 6 + 3) * G + blockIdx.x] = gtimer();
-        tile_epilogue(a, gk, l, tl, tile, rn, red, kred, srows, srope, gw, et, warp, lane);
-        epi_sync();  // tile / reduction scratch reused by the next tile
-        if (a.trace && et == 0 && tl == blockIdx.x) a.trace[((size_t)ph * 6 + 4) * G + blockIdx.x] = gtimer();
+  for (int q4 = 0; q4 < XR / 4; q4++) {
+    tile[r * (XR + 1) + 4 * q4] = acc4[q4].x;
+    tile[r * (XR + 1) + 4 * q4 + 1] = acc4[q4].y;
+    tile[r * (XR + 1) + 4 * q4 + 2] = acc4[q4].z;
+    tile[r * (XR + 1) + 4 * q4 + 3] = acc4[q4].w;
+  }
+  epi_sync();  // tile visible
+  tile_epilogue(a, gk, l, tl, tile, rn, red, kred, srows, srope, gw, et, warp, lane);
+  epi_sync();  // tile / reduction scratch reused
+}
+
+// Separate reduction phase (QKV, O, down): tiles t = cta (mod grid).
+__device__ __noinline__ void epi_reduce(const Args& a, unsigned char* smem, int ph, int l, int kind) {
+  MK_SMEM_LAYOUT(smem);
+  const int G = gridDim.x;
+  const int et = threadIdx.x - 64;
+  const int d = a.d, B = a.B;
+  const int n_ss = d / MT;
+  const int gk = gemm_kind_of_reduce(kind);
+  const MkPlan p = a.plan[gemm_of(gk)];
+  if (blockIdx.x >= p.tiles) return;
+  if (gk == K_QKV && et < B) {  // row norms of the QKV input
+    const float4* sr = reinterpret_cast<const float4*>(a.ss + (size_t)et * n_ss);
+    float sacc = 0.0f;
+    for (int u = 0; u < n_ss / 4; u++) {
+      const float4 v = __ldcg(sr + u);
+      sacc += (v.x + v.y) + (v.z + v.w);
+    }
+    rn[et] = rsqrtf(sacc / (float)d + a.eps);
+  }
+  if (a.trace && et == 0) a.trace[((size_t)ph * 6 + 2) * G + blockIdx.x] = gtimer();
+  for (int tl = blockIdx.x; tl < p.tiles; tl += G) finalize_tile(a, smem, l, gk, tl);
+  if (a.trace && et == 0) a.trace[((size_t)ph * 6 + 5) * G + blockIdx.x] = gtimer();
+}
+
+// Helper warp (lane 0): for every chunk the epilogue drained it adds to the
+// tile's arrival counter (acquire-release); the arrival that completes a tile
+// queues it for finalisation by this CTA's epilogue warps.  Keeping these
+// round trips off the epilogue keeps the accumulator drain (and with it the
+// MMA and the weight stream) running; tiles are finalised progressively
+// through the phase instead of in a separate reduction phase.
+__device__ __noinline__ void role_helper(const Args& a, unsigned char* smem) {
+  MK_SMEM_LAYOUT(smem);
+  const int P = n_phases(a);
+  int ev_pos = 0, task_w = 0;
+  for (int ph = 0; ph < P; ph++) {
+    int l;
+    const int kind = phase_kind(a, ph, &l);
+    const int gi = gemm_of(kind);
+    if (gi < 0 || !fused_reduce(kind)) continue;
+    const MkPlan p = a.plan[gi];
+    while (true) {
+      if (*ev_cnt <= ev_pos) {
+        const uint64_t t0 = gtimer();
+        unsigned spins = 0;
+        while (*ev_cnt <= ev_pos)
+          if (++spins % 1024 == 0 && gtimer() - t0 > 2000000000ull) __trap();
       }
-      if (a.trace && et == 0) a.trace[((size_t)ph * 6 + 5) * G + blockIdx.x] = gtimer();
+      __threadfence_block();
+      const int tl = evq[ev_pos % kRing];
+      ev_pos++;
+      if (tl >= 0) {
+        const int prev = atom_add_acq_rel(&a.counters[tl], 1);  // releases this CTA's partial of the chunk
+        if (prev != p.nc - 1) continue;
+        a.counters[tl] = 0;  // next use is after a grid barrier
+      }
+      taskq[task_w % kRing] = tl;  // tile, or -1: no more tasks this phase
+      __threadfence_block();
+      *task_cnt = ++task_w;
+      if (tl < 0) break;
+    }
+  }
 }
 
 // The three warp roles are separate non-inlined functions so each gets its own
@@ -1011,7 +1133,7 @@ __device__ __noinline__ void role_epilogue(const Args& a, unsigned char* smem, u
     const int r = 32 * (warp & 3) + lane;  // TMEM lane = weight row of the tile
     const int d = a.d, B = a.B;
     const int n_ss = d / MT;
-    int lu = 0, n = 0;
+    int lu = 0, n = 0, task_r = 0;
     uint32_t apar = 0;  // phase parity of the attention staging barriers
     for (int ph = 0; ph < P; ph++) {
       int l;
@@ -1028,7 +1150,7 @@ __device__ __noinline__ void role_epilogue(const Args& a, unsigned char* smem, u
       else if (kind == K_ATTN) epi_attn(a, smem, ph, l, kind);
       else if (kind == K_AMERGE) epi_amerge(a, smem, ph, l, kind);
       else if (kind == K_FINAL) epi_final(a, smem, ph, l, kind);
-      else if (gemm_of(kind) >= 0) epi_gemm(a, smem, ph, l, kind, tmem, lu, n);
+      else if (gemm_of(kind) >= 0) epi_gemm(a, smem, ph, l, kind, tmem, lu, n, task_r);
       else epi_reduce(a, smem, ph, l, kind);
       // ---- phase done: publish and arrive at the grid barrier
       if (ph + 1 < P) {
@@ -1080,6 +1202,11 @@ __global__ void __launch_bounds__(kThreads, 1) decode_mk_kernel(const __grid_con
   ItemRow* sirows = (ItemRow*)(sitems + kMaxPairs);          // [kMaxPairs][16] their query rows
   int* pend_slot = (int*)(sirows + kMaxPairs * XR);          // [kStages] producer: stages awaiting activations
   int* pend_kb = pend_slot + kStages;                        // [kStages] their k-blocks
+  volatile int* evq = (volatile int*)(pend_kb + kStages);    // [kRing] epilogue -> helper: drained chunks' tiles
+  volatile int* taskq = evq + kRing;                         // [kRing] helper -> epilogue: tiles to finalise
+  volatile int* ev_cnt = taskq + kRing;                      // events posted (monotonic)
+  volatile int* task_cnt = ev_cnt + 1;                       // tasks posted (monotonic)
+  volatile int* task_snap = ev_cnt + 2;                      // epilogue-group broadcast of task_cnt
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = gridDim.x;
@@ -1096,10 +1223,12 @@ __global__ void __launch_bounds__(kThreads, 1) decode_mk_kernel(const __grid_con
     }
     for (int i = 0; i < kAttnSlots; i++) mbar_init(&abar[i], 1);
     for (int i = 0; i < kQueue; i++) qseq[i] = -1;
+    *ev_cnt = 0;
+    *task_cnt = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     *ready_ph = -1;
   }
-  if (threadIdx.x >= 64) {  // per-tick constants: rows, their RoPE rows, this CTA's attention items
+  if (threadIdx.x >= 64 && threadIdx.x < 192) {  // per-tick constants: rows, RoPE rows, attention items
     const int et = threadIdx.x - 64;
     if (et < a.B) srows[et] = a.rows[et];
     for (int b = 0; b < a.B; b++) srope[b * HD + et] = __ldg(a.rope + (size_t)a.rows[b].pos * HD + et);
@@ -1129,8 +1258,10 @@ __global__ void __launch_bounds__(kThreads, 1) decode_mk_kernel(const __grid_con
     if (lane == 0) role_producer(as, smem, map_xg, map_attn, map_act);
   } else if (warp == 1) {
     if (lane == 0) role_mma(as, smem, tmem);
-  } else {
+  } else if (warp < 6) {
     role_epilogue(as, smem, tmem);
+  } else {
+    if (lane == 0) role_helper(as, smem);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -1150,7 +1281,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_mk_kernel(const __grid_con
 
 }  // namespace
 
-int mk_phases(int L) { return 4 + 10 * L; }
+int mk_phases(int L) { return 3 + 9 * L; }
 
 int mk_grid() {
   static int n_sm = 0;

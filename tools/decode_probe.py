@@ -84,8 +84,8 @@ if args.trace:
     P = tr.shape[0]
     t0 = tr[0, 0].min()
     names = (["EMBED"] + [n for l in range(cfg.n_layers)
-                          for n in ("QKV", "RQKV", "ATTN", "AMERGE", "O", "RO", "GU", "RGU", "DOWN", "RDOWN")]
-             + ["LM", "RLM", "FINAL"])
+                          for n in ("QKV", "RQKV", "ATTN", "AMERGE", "O", "RO", "GU", "DOWN", "RDOWN")]
+             + ["LM", "FINAL"])
     agg = {}
     print("phase         start   span | W-issue end   1st acc      last acc     drained  (min/max us from phase start)")
     for ph in range(P):
