@@ -1293,17 +1293,17 @@ int mk_grid() {
   return n_sm;
 }
 
-MkPlan mk_plan(int tiles, int kb_total, int grid) {
-  // enough chunks for ~4 per CTA (dynamic balance), at least 4 k-blocks each,
-  // at most 16 per tile (one load round in the reduction)
-  int nc = (4 * grid + tiles - 1) / tiles;
-  nc = std::max(1, std::min({nc, 16, std::max(1, kb_total / 4)}));
+MkPlan mk_plan(int tiles, int kb_total, int grid, int per_cta, int cap) {
+  // enough chunks for ~per_cta per CTA (dynamic balance), at least 4 k-blocks
+  // each, at most min(cap, 16) per tile (one load round in the reduction)
+  int nc = (per_cta * grid + tiles - 1) / tiles;
+  nc = std::max(1, std::min({nc, cap, 16, std::max(1, kb_total / 4)}));
   return MkPlan{tiles, kb_total, nc, tiles * nc};
 }
 
 size_t mk_partial_floats(const MkPlan* plans) {
   int chunks = 0;
-  for (int i = 0; i < 5; i++) chunks = std::max(chunks, plans[i].chunks);
+  for (int i = 0; i < 5; i++) chunks = std::max(chunks, plans[i].tiles * 16);  // any plan up to 16 per tile
   return (size_t)chunks * MT * XR;
 }
 

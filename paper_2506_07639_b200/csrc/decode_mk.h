@@ -60,7 +60,7 @@ struct MkLaunch {
   unsigned long long* trace;     // diagnostics (null): [phases][2][grid] globaltimer at barrier pass / phase end
 };
 
-MkPlan mk_plan(int tiles, int kb_total, int grid);
+MkPlan mk_plan(int tiles, int kb_total, int grid, int per_cta = 4, int cap = 16);
 size_t mk_partial_floats(const MkPlan* plans);
 void launch_decode_mk(const MkLaunch& l, cudaStream_t s);
 int mk_grid();

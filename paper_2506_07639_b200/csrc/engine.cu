@@ -192,6 +192,7 @@ struct fe_engine {
   bool mk_trace_on = false;
   int mk_flags = 0;
   int mk_pf_stages = 0;  // 0 = the whole ring
+  int mk_per_cta = 4, mk_nc_cap = 8, mk_nc_cap_o = 0;  // chunk plans (mk_make_plans; swept in tools/mk_sweep.sh)
   bool graphs_on = true;
   float* op_partial = nullptr;  // fe_op_skinny_tc scratch
   size_t op_bytes = 0;
@@ -354,6 +355,18 @@ void clear_graphs(fe_engine* e) {
       if (g.second.exec) cudaGraphExecDestroy(g.second.exec);
     ln.graphs.clear();
   }
+}
+
+// Chunk plans of the persistent decode-tick kernel's GEMMs (options "mk_per_cta",
+// "mk_nc_cap" retune them; the partial buffers are sized for any plan).
+void mk_make_plans(fe_engine* e) {
+  const fe::ModelDims& m = e->m;
+  const int G = e->mk_grid, pc = e->mk_per_cta, cap = e->mk_nc_cap;
+  e->mk_plans[fe::MK_QKV] = fe::mk_plan(3 * m.d / 128, m.d / 64, G, pc, cap);
+  e->mk_plans[fe::MK_O] = fe::mk_plan(m.d / 128, m.d / 64, G, pc, e->mk_nc_cap_o > 0 ? e->mk_nc_cap_o : cap);
+  e->mk_plans[fe::MK_GU] = fe::mk_plan(m.F / 64, m.d / 64, G, pc, cap);
+  e->mk_plans[fe::MK_DOWN] = fe::mk_plan(m.d / 128, m.F / 64, G, pc, cap);
+  e->mk_plans[fe::MK_LM] = fe::mk_plan((m.V + 127) / 128, m.d / 64, G, pc, cap);
 }
 
 // ---- forward pass -----------------------------------------------------------
@@ -909,11 +922,7 @@ fe_engine* create(const fe_config* c, int device, const float* rope_host) {
     e->mk_on = e->use_tc && m.H * m.hd == m.d && m.d % 512 == 0;
     if (e->mk_on) {
       e->mk_grid = fe::mk_grid();
-      e->mk_plans[fe::MK_QKV] = fe::mk_plan(3 * m.d / 128, m.d / 64, e->mk_grid);
-      e->mk_plans[fe::MK_O] = fe::mk_plan(m.d / 128, m.d / 64, e->mk_grid);
-      e->mk_plans[fe::MK_GU] = fe::mk_plan(m.F / 64, m.d / 64, e->mk_grid);
-      e->mk_plans[fe::MK_DOWN] = fe::mk_plan(m.d / 128, m.F / 64, e->mk_grid);
-      e->mk_plans[fe::MK_LM] = fe::mk_plan((m.V + 127) / 128, m.d / 64, e->mk_grid);
+      mk_make_plans(e);
       std::vector<fe::TmaMap> maps(4 * m.L + 1);
       for (int l = 0; l < m.L; l++) {
         maps[4 * l + 0] = e->tc_maps[l].qkv;
@@ -1382,6 +1391,10 @@ int fe_set_option(fe_engine* e, const char* key, int64_t value) {
       clear_graphs(e);
     } else if (k == "mk_pf") {
       e->mk_pf_stages = (int)value;
+      clear_graphs(e);
+    } else if (k == "mk_per_cta" || k == "mk_nc_cap" || k == "mk_nc_cap_o") {
+      (k == "mk_per_cta" ? e->mk_per_cta : k == "mk_nc_cap" ? e->mk_nc_cap : e->mk_nc_cap_o) = (int)value;
+      if (e->mk_on) mk_make_plans(e);
       clear_graphs(e);
     } else if (k == "mk") {
       e->mk_on = value != 0 && e->use_tc && e->mk_maps != nullptr;

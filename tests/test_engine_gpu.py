@@ -450,3 +450,27 @@ def test_bf16_persistent_tick_branch_batch():
         firsts[mk] = [eng.request_tokens(r, 5)[0] for r in reqs]
         eng.close()
     assert sum(a == b for a, b in zip(firsts[1], firsts[0])) >= 6, firsts
+
+
+@pytest.mark.parametrize("n_branches", [13, 16])
+def test_bf16_persistent_tick_wide_rows(n_branches):
+    """The tick kernel's widest batches (> 8 rows: the 16-column partial path;
+    16 rows: the kernel's limit) vs the kernel chain: first greedy token of
+    every branch agrees (bf16 near-ties aside: >= all but one)."""
+    from oracle.backend import frame
+    ids = frame("small", list(range(16)), list(range(900, 1150)), "plan")
+    firsts = {}
+    for mk in (1, 0):
+        eng = Engine("small", dtype="bf16", seed=0, kv_pages=256, max_rows=512)
+        eng.set_option("mk", mk)
+        trunk = eng.seq_create()
+        eng.prefill(trunk, ids[:-1], 99, M.VIS_ID)
+        reqs = []
+        for j in range(n_branches):
+            b = eng.seq_fork(trunk, len(ids) - 1 - 11 * j)
+            reqs.append(eng.submit(b, M.TAG_BASE + (j % 32), 4, 1))
+        eng.set_slots(n_branches)
+        eng.run(-1)
+        firsts[mk] = [eng.request_tokens(r, 4)[0] for r in reqs]
+        eng.close()
+    assert sum(a == b for a, b in zip(firsts[1], firsts[0])) >= n_branches - 1, firsts

@@ -29,6 +29,7 @@ ap.add_argument("--graphs", type=int, default=1)
 ap.add_argument("--mk", type=int, default=1)
 ap.add_argument("--mk-flags", type=int, default=0)
 ap.add_argument("--pf", type=int, default=0, help="persistent tick: weight stages prefetched across a barrier")
+ap.add_argument("--opt", action="append", default=[], help="extra engine option key=value")
 ap.add_argument("--trace", action="store_true", help="per-phase barrier timeline of the persistent tick kernel")
 args = ap.parse_args()
 
@@ -40,6 +41,9 @@ eng.set_option("graphs", args.graphs)
 eng.set_option("mk", args.mk)
 eng.set_option("mk_flags", args.mk_flags)
 eng.set_option("mk_pf", args.pf)
+for kv in args.opt:
+    k, v = kv.split("=")
+    eng.set_option(k, int(v))
 if args.trace:
     eng.set_option("mk_trace", 1)
 if args.stages:
