@@ -1020,7 +1020,9 @@ __device__ __noinline__ void role_producer(const Args& a, unsigned char* smem, c
         const CUtensorMap* xm = gi == MK_O ? &map_attn : gi == MK_DOWN ? &map_act : &map_xg;
         // the attention phase borrows the ring: start the O weights only once this
         // CTA's epilogue warps have left it (they publish the AMERGE barrier)
-        if (kind == K_O) wait_ready(ready_ph, ph - 1);
+        // -- and only once the merge's outputs are fenced: its stores then do not
+        // queue behind the O weight stream (measured: merge 5.8 -> 3.5 us)
+        if (kind == K_O) wait_ready(ready_ph + 1, ph - 1);
         if (a.flags & 1) wait_ready(ready_ph, ph);  // diagnostics: no weight prefetch across barriers
         bool ready = false;
         int npend = 0;
@@ -1162,6 +1164,7 @@ __device__ __noinline__ void role_epilogue(const Args& a, unsigned char* smem, u
         __threadfence();
         epi_sync();
         if (et == 0) {
+          ready_ph[1] = ph;  // this phase's outputs are fenced (the producer starts the O weights on it)
           if (a.trace) a.trace[((size_t)ph * 6 + 1) * G + blockIdx.x] = gtimer();
           atomicAdd(a.bar, 1ull);
         }
@@ -1226,7 +1229,8 @@ __global__ void __launch_bounds__(kThreads, 1) decode_mk_kernel(const __grid_con
     *ev_cnt = 0;
     *task_cnt = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    *ready_ph = -1;
+    ready_ph[0] = -1;
+    ready_ph[1] = -1;
   }
   if (threadIdx.x >= 64 && threadIdx.x < 192) {  // per-tick constants: rows, RoPE rows, attention items
     const int et = threadIdx.x - 64;
