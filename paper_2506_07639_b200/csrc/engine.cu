@@ -26,6 +26,8 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <thread>
+#include <chrono>
 #include <stdexcept>
 #include <string>
 #include <unordered_map>
@@ -127,6 +129,7 @@ struct Lane {
   fe::TmaMap map_xn{}, map_attn{}, map_act{};        // 128-row boxes (tile GEMM A operand)
   fe::TmaMap map_xn16{}, map_attn16{}, map_act16{};  // 16-row boxes (skinny GEMM B operand)
   std::unordered_map<long, GraphSlot> graphs;       // key: rows * 4096 + attention item bucket
+  cudaEvent_t tick_ev[2] = {};                      // lane 1 pacing (run_lane)
   // continuous batcher
   int slots = 8;
   std::vector<int> slot_req;
@@ -191,9 +194,12 @@ struct fe_engine {
   size_t mk_trace_n = 0;
   bool mk_trace_on = false;
   int mk_flags = 0;
+  cudaEvent_t mk_ev[kLanes] = {};  // last persistent tick of each lane
+  bool mk_ev_used[kLanes] = {};
   int mk_pf_stages = 0;  // 0 = the whole ring
   int mk_per_cta = 4, mk_nc_cap = 8, mk_nc_cap_o = 0;  // chunk plans (mk_make_plans; swept in tools/mk_sweep.sh)
   bool graphs_on = true;
+  bool lane1_yields = true;  // option "lane1_yields": reasoning lane defers while the action lane has work
   float* op_partial = nullptr;  // fe_op_skinny_tc scratch
   size_t op_bytes = 0;
   int* op_counters = nullptr;
@@ -373,7 +379,8 @@ void mk_make_plans(fe_engine* e) {
 // The persistent decode-tick kernel takes bf16 decode ticks of <= 16 rows on
 // lane 0 where every row samples a token (it needs every SM: one lane only).
 bool mk_eligible(fe_engine* e, const Lane& ln, const fe::Fwd& f, int n) {
-  return e->mk_on && ln.id == 0 && n <= 16 && f.n_head_rows == n && e->debug_skip == 0;
+  (void)ln;
+  return e->mk_on && n <= 16 && f.n_head_rows == n && e->debug_skip == 0;
 }
 
 // The kernel sequence of one forward pass (eager or under graph capture).
@@ -644,6 +651,10 @@ void forward(fe_engine* e, Lane& ln, const std::vector<RowIn>& rows, uint64_t vi
   const bool graphable = decode && e->graphs_on && !(e->prof_on && ln.id == 0) && n <= kMaxGraphRows;
   const long key = (long)n * 4096 + item_bucket;
   auto it_g = ln.graphs.find(key);
+  // a persistent tick needs every SM: it never overlaps the other lane's
+  // persistent tick (grid-barrier deadlock); order them with events
+  const bool mk_tick = decode && mk_eligible(e, ln, f, n);
+  if (mk_tick && e->mk_ev_used[1 - ln.id]) CK(cudaStreamWaitEvent(ln.stream, e->mk_ev[1 - ln.id], 0));
   if (graphable && it_g != ln.graphs.end() && it_g->second.exec) {
     CK(cudaGraphLaunch(it_g->second.exec, ln.stream));
   } else if (graphable && it_g != ln.graphs.end() && it_g->second.seen) {
@@ -659,8 +670,12 @@ void forward(fe_engine* e, Lane& ln, const std::vector<RowIn>& rows, uint64_t vi
     launch_layers(e, ln, f, n, decode, kv_bytes, gemv_bytes);
   }
   CK(cudaGetLastError());
+  if (mk_tick) {
+    CK(cudaEventRecord(e->mk_ev[ln.id], ln.stream));
+    e->mk_ev_used[ln.id] = true;
+  }
   const int attn_kernels = e->dtype == FE_BF16 ? 1 : 2;  // bf16: merge fused into the attention kernel
-  if (decode && mk_eligible(e, ln, f, n)) e->n_launches += 1;
+  if (mk_tick) e->n_launches += 1;
   else e->n_launches += 1 + (6 + attn_kernels) * m.L + (decode ? 3 : 0) - (items.empty() ? m.L : 0);
   e->n_forwards++;
   e->n_rows_total += n;
@@ -815,7 +830,7 @@ void create_lane(fe_engine* e, Lane& ln, int id, int rows, int priority) {
   ln.ws.logits = id == 0 ? e->logits : nullptr;
   ln.attn_counters = (int*)e->dalloc(R * m.H * sizeof(int));
   CK(cudaMemset(ln.attn_counters, 0, R * m.H * sizeof(int)));
-  if (id == 0 && e->mk_on) {
+  if (e->mk_on) {
     ln.mk_ss = (float*)e->dalloc((size_t)(m.d / 128) * 16 * 4);
     ln.mk_bar = (unsigned long long*)e->dalloc(2 * sizeof(unsigned long long));
     CK(cudaMemset(ln.mk_bar, 0, 2 * sizeof(unsigned long long)));
@@ -839,6 +854,7 @@ void create_lane(fe_engine* e, Lane& ln, int id, int rows, int priority) {
     L.total = up16(L.o_heads + R * 4);
   }
   ln.ws.meta = e->dalloc(ln.layout.total);
+  for (int i = 0; i < 2; i++) CK(cudaEventCreateWithFlags(&ln.tick_ev[i], cudaEventDisableTiming));
   for (int i = 0; i < kMetaRing; i++) {
     CK(cudaMallocHost((void**)&ln.meta_host[i], ln.layout.total));
     CK(cudaEventCreateWithFlags(&ln.meta_ev[i], cudaEventDisableTiming));
@@ -949,6 +965,7 @@ fe_engine* create(const fe_config* c, int device, const float* rope_host) {
     create_lane(e, e->lanes[0], 0, max_rows, prio_high);
     create_lane(e, e->lanes[1], 1, std::min(max_rows, kLane1Rows), prio_low);
     CK(cudaEventCreateWithFlags(&e->lane0_ev, cudaEventDisableTiming));
+    for (int i = 0; i < kLanes; i++) CK(cudaEventCreateWithFlags(&e->mk_ev[i], cudaEventDisableTiming));
     CK(cudaEventRecord(e->lane0_ev, e->lanes[0].stream));
 
     // KV pool: 64-token pages [L][2][H][64][hd]
@@ -1042,7 +1059,18 @@ int run_lane(fe_engine* e, int lane, int32_t stop_req, int32_t max_ticks, int32_
   try {
     if (!e) throw Error("null engine");
     int t = 0, nc = 0;
+    bool yield = false, paced = false;
+    cudaEvent_t pace = nullptr;
     while (true) {
+      if (paced) {
+        CK(cudaEventSynchronize(pace));
+        paced = false;
+      }
+      if (yield) {  // lane 1 waiting for the action lane: outside the lock
+        std::this_thread::sleep_for(std::chrono::microseconds(50));
+        yield = false;
+        if (stop_req < 0 && max_ticks > 0) break;  // a bounded background call returns to its driver
+      }
       std::lock_guard<std::mutex> lk(e->mu);
       cudaSetDevice(e->device);
       Lane& ln = lane_at(e, lane);
@@ -1055,6 +1083,12 @@ int run_lane(fe_engine* e, int lane, int32_t stop_req, int32_t max_ticks, int32_
       }
       if (max_ticks > 0 && t >= max_ticks) break;
       if (!lane_busy(ln)) throw Error("run: stop request is not in flight");
+      if (lane == 1 && e->lane1_yields && lane_busy(e->lanes[0])) {
+        // the action lane has work: the reasoning lane does not add ticks
+        // (the action decodes on an uncontended GPU); retry shortly
+        yield = true;
+        continue;
+      }
       if (t >= cap) throw Error("run: tick capacity exceeded");
       std::vector<int> done;
       occupancy[t] = tick(e, ln, &done);
@@ -1063,6 +1097,11 @@ int run_lane(fe_engine* e, int lane, int32_t stop_req, int32_t max_ticks, int32_
         completed[nc] = r;
         completed_tick[nc] = t;
         nc++;
+      }
+      if (lane == 1 && e->lane1_yields) {  // keep <= 2 reasoning ticks queued on the device
+        CK(cudaEventRecord(ln.tick_ev[t & 1], ln.stream));
+        pace = ln.tick_ev[(t + 1) & 1];
+        paced = t > 0;
       }
       t++;
     }
@@ -1396,6 +1435,8 @@ int fe_set_option(fe_engine* e, const char* key, int64_t value) {
       (k == "mk_per_cta" ? e->mk_per_cta : k == "mk_nc_cap" ? e->mk_nc_cap : e->mk_nc_cap_o) = (int)value;
       if (e->mk_on) mk_make_plans(e);
       clear_graphs(e);
+    } else if (k == "lane1_yields") {
+      e->lane1_yields = value != 0;
     } else if (k == "mk") {
       e->mk_on = value != 0 && e->use_tc && e->mk_maps != nullptr;
       clear_graphs(e);
