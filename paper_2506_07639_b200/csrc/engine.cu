@@ -57,8 +57,8 @@ constexpr int kLanes = 2;
 constexpr int kLane1Rows = 64;      // background lane: decode rows only
 
 struct MetaLayout {
-  size_t o_rows, o_items, o_irows, o_heads, total;
-  int cap_rows, cap_items, cap_irows;
+  size_t o_rows, o_items, o_irows, o_heads, o_pages, total;
+  int cap_rows, cap_items, cap_irows, cap_pages;
 };
 
 struct Seq {
@@ -199,7 +199,8 @@ struct fe_engine {
   int mk_pf_stages = 0;  // 0 = the whole ring
   int mk_per_cta = 4, mk_nc_cap = 8, mk_nc_cap_o = 0;  // chunk plans (mk_make_plans; swept in tools/mk_sweep.sh)
   bool graphs_on = true;
-  bool lane1_yields = true;  // option "lane1_yields": reasoning lane defers while the action lane has work
+  bool lane1_yields = true;
+  bool prefill_fa = true;  // option "prefill_fa": tensor-core causal prefill attention (bf16)  // option "lane1_yields": reasoning lane defers while the action lane has work
   float* op_partial = nullptr;  // fe_op_skinny_tc scratch
   size_t op_bytes = 0;
   int* op_counters = nullptr;
@@ -475,7 +476,12 @@ void launch_layers(fe_engine* e, Lane& ln, const fe::Fwd& f, int n, bool decode,
     }
     prof_end(e, ln, p, gemv_bytes(3.0 * m.d, m.d, n));
     p = decode ? prof_begin(e, ln, PROF_ATTN) : -1;
-    if (!(e->debug_skip & 1)) fe::launch_attention(dt, f, m, ws.q, e->kv_pool, l, ws.partial, ws.attn, st);
+    if (e->debug_skip & 1) {
+    } else if (!decode && f.seq_pages && dt == FE_BF16 && m.hd == 128 && e->prefill_fa) {
+      fe::launch_prefill_attention(f, m, ws.q, e->kv_pool, l, ws.attn, st);
+    } else {
+      fe::launch_attention(dt, f, m, ws.q, e->kv_pool, l, ws.partial, ws.attn, st);
+    }
     prof_end(e, ln, p, kv_bytes);
     p = decode ? prof_begin(e, ln, PROF_GEMV) : -1;
     if (skip_gemm) {
@@ -619,6 +625,19 @@ void forward(fe_engine* e, Lane& ln, const std::vector<RowIn>& rows, uint64_t vi
   copy(L.o_items, sizeof(fe::AttnItem) * items.size());
   copy(L.o_irows, sizeof(fe::ItemRow) * irows.size());
   copy(L.o_heads, sizeof(int32_t) * head_rows.size());
+  // single-sequence prefill: the sequence's page table for the tensor-core attention
+  bool one_seq = head_rows.empty() && n > 1;
+  for (int i = 1; i < n && one_seq; i++) one_seq = rows[i].seq == rows[0].seq && rows[i].pos == rows[0].pos + i;
+  int n_seq_pages = 0;
+  if (one_seq) {
+    const Seq& sq = e->seqs[rows[0].seq];
+    n_seq_pages = (rows[n - 1].pos) / FE_PAGE + 1;
+    if (n_seq_pages > L.cap_pages) one_seq = false;
+    else {
+      std::memcpy(hbuf + L.o_pages, sq.pages.data(), sizeof(int32_t) * n_seq_pages);
+      copy(L.o_pages, sizeof(int32_t) * n_seq_pages);
+    }
+  }
   CK(cudaEventRecord(ln.meta_ev[mi], ln.stream));
   e->h2d_bytes += h2d;
 
@@ -638,6 +657,8 @@ void forward(fe_engine* e, Lane& ln, const std::vector<RowIn>& rows, uint64_t vi
   f.head_rows = (const int32_t*)(dbuf + L.o_heads);
   f.attn_counters = ln.attn_counters;
   f.vision_key = fe::tensor_key(vision_seed, 4 /* T_VISION */);
+  f.seq_pages = one_seq ? (const int32_t*)(dbuf + L.o_pages) : nullptr;
+  f.pos0 = one_seq ? rows[0].pos : 0;
 
   const bool decode = f.n_head_rows > 0;
   const double el = (double)e->elem;
@@ -851,7 +872,9 @@ void create_lane(fe_engine* e, Lane& ln, int id, int rows, int priority) {
     L.o_items = up16(L.o_rows + R * sizeof(fe::RowMeta));
     L.o_irows = up16(L.o_items + (size_t)L.cap_items * sizeof(fe::AttnItem));
     L.o_heads = up16(L.o_irows + (size_t)L.cap_irows * sizeof(fe::ItemRow));
-    L.total = up16(L.o_heads + R * 4);
+    L.cap_pages = m.max_pos / FE_PAGE + 1;
+    L.o_pages = up16(L.o_heads + R * 4);
+    L.total = up16(L.o_pages + (size_t)L.cap_pages * 4);
   }
   ln.ws.meta = e->dalloc(ln.layout.total);
   for (int i = 0; i < 2; i++) CK(cudaEventCreateWithFlags(&ln.tick_ev[i], cudaEventDisableTiming));
@@ -1435,6 +1458,8 @@ int fe_set_option(fe_engine* e, const char* key, int64_t value) {
       (k == "mk_per_cta" ? e->mk_per_cta : k == "mk_nc_cap" ? e->mk_nc_cap : e->mk_nc_cap_o) = (int)value;
       if (e->mk_on) mk_make_plans(e);
       clear_graphs(e);
+    } else if (k == "prefill_fa") {
+      e->prefill_fa = value != 0;
     } else if (k == "lane1_yields") {
       e->lane1_yields = value != 0;
     } else if (k == "mk") {

@@ -61,6 +61,10 @@ struct Fwd {
   int n_head_rows;         // rows that need the lm_head
   const int32_t* head_rows;  // row index of each lm_head row
   uint64_t vision_key;
+  // single-sequence prefill (rows = positions pos0 .. pos0 + n_rows - 1 of one
+  // sequence): its page table, for the tensor-core prefill attention; else null
+  const int32_t* seq_pages;
+  int pos0;
 };
 
 struct Weights {
@@ -119,6 +123,9 @@ void launch_qkv(int dtype, const Fwd& f, const ModelDims& m, const void* w, cons
                 void* kv_pool, int layer, const float* rope, cudaStream_t s);
 void launch_attention(int dtype, const Fwd& f, const ModelDims& m, const float* q, const void* kv_pool,
                       int layer, float* partial, void* attn_out, cudaStream_t s);
+// bf16, head_dim 128, f.seq_pages set (prefill_attn.cu)
+void launch_prefill_attention(const Fwd& f, const ModelDims& m, const float* q, const void* kv_pool, int layer,
+                              void* attn_out, cudaStream_t s);
 void launch_resid(int dtype, const Fwd& f, int N, int K, const void* w, const void* xin, float* x,
                   cudaStream_t s);
 void launch_swiglu(int dtype, const Fwd& f, int F, int K, const void* w, const void* xin, void* act,

@@ -474,3 +474,23 @@ def test_bf16_persistent_tick_wide_rows(n_branches):
         firsts[mk] = [eng.request_tokens(r, 4)[0] for r in reqs]
         eng.close()
     assert sum(a == b for a, b in zip(firsts[1], firsts[0])) >= n_branches - 1, firsts
+
+
+@pytest.mark.parametrize("config,plen", [("small", 180), ("small", 700), ("7b_2layer", 420)])
+def test_bf16_prefill_tensor_core_attention_matches_cascade(config, plen):
+    """Trunk prefill through the tensor-core causal attention (prefill_attn.cu:
+    mma.sync flash-style, paged K/V, multi-chunk prefill for > 512 rows) vs the
+    CUDA-core cascade kernel: first decode logits within bf16 tolerance, same
+    first greedy token."""
+    from oracle.backend import frame
+    ids = frame(config, list(range(16)), list(range(300, 300 + plen)), "plan")
+    out = {}
+    for fa in (1, 0):
+        eng = Engine(config, dtype="bf16", seed=0, kv_pages=128, max_rows=512)
+        eng.set_option("prefill_fa", fa)
+        out[fa] = _decode(eng, ids, 777, 3, capture=True)
+        eng.close()
+    (t1, l1), (t0, l0) = out[1], out[0]
+    rel = np.abs(l1[0] - l0[0]).max() / np.abs(l0[0]).max()
+    assert rel < 2e-2, rel
+    assert t1[0] == t0[0]
