@@ -110,7 +110,7 @@ class Engine:
     """One engine per GPU: weights, paged KV pool, continuous batcher."""
 
     def __init__(self, config: str | ModelConfig = "tiny", dtype: str = "f32", device: int = 0,
-                 seed: int = 0, max_rows: int = 512, kv_pages: int = 0, max_slots: int = 512):
+                 seed: int = 0, max_rows: int = 1024, kv_pages: int = 0, max_slots: int = 512):
         self.cfg = get_config(config)
         self.lib = load_library()
         self.dtype = dtype

@@ -18,6 +18,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="7b")
 ap.add_argument("--dtype", default="bf16")
 ap.add_argument("--rows", type=int, default=7)
+ap.add_argument("--max-rows", type=int, default=1024, help="engine rows per forward (prefill chunk)")
 ap.add_argument("--trunk", type=int, default=625)
 ap.add_argument("--ticks", type=int, default=8)
 ap.add_argument("--repeat", type=int, default=3)
@@ -33,7 +34,7 @@ ap.add_argument("--opt", action="append", default=[], help="extra engine option 
 ap.add_argument("--trace", action="store_true", help="per-phase barrier timeline of the persistent tick kernel")
 args = ap.parse_args()
 
-eng = Engine(args.config, dtype=args.dtype, seed=0, kv_pages=256)
+eng = Engine(args.config, dtype=args.dtype, seed=0, kv_pages=256, max_rows=args.max_rows)
 if args.skip:
     eng.set_option("debug_skip", args.skip)
 eng.set_option("pdl", args.pdl)
