@@ -107,6 +107,7 @@ struct Args {
   float* logits;
   unsigned long long* bar;
   int flags;                  // diagnostics (engine option "mk_flags")
+  int fused;                  // bit MK_*: GEMM finalised in-phase (option "mk_fused")
   int pf_stages;              // weight stages prefetched ahead of a phase's grid barrier (<= kStages)
   int* grab;                  // [P] chunk counters of the GEMM phases (reset by the last CTA to exit)
   unsigned long long* trace;  // diagnostics: [P][6][G] globaltimer: barrier pass, phase done, last weight load issued,
@@ -117,28 +118,32 @@ struct Args {
 // lm_head (many tiles) finalise their tiles progressively inside the GEMM
 // phase (role_helper); QKV, O and down (few, long-K tiles whose chunks all
 // land at the end) reduce in a separate phase, which measured faster.
-constexpr int kLayerPhases = 9;
-__device__ __forceinline__ int n_phases(const Args& a) { return 3 + kLayerPhases * a.L; }
+// a.fused: bit MK_* set = that GEMM finalises its tiles inside its own phase
+// (helper warp), else a reduction phase follows it
+__device__ __forceinline__ int layer_phases(const Args& a) {
+  return 6 + !(a.fused >> MK_QKV & 1) + !(a.fused >> MK_O & 1) + !(a.fused >> MK_GU & 1) + !(a.fused >> MK_DOWN & 1);
+}
+__device__ __forceinline__ int n_phases(const Args& a) { return 3 + layer_phases(a) * a.L; }
 __device__ __forceinline__ int phase_kind(const Args& a, int ph, int* layer) {
   *layer = 0;
+  const int lp = layer_phases(a);
   if (ph == 0) return K_EMBED;
-  if (ph == 1 + kLayerPhases * a.L) return K_LM;
-  if (ph == 2 + kLayerPhases * a.L) return K_FINAL;
-  *layer = (ph - 1) / kLayerPhases;
-  switch ((ph - 1) % kLayerPhases) {
-    case 0: return K_QKV;
-    case 1: return K_RQKV;
-    case 2: return K_ATTN;
-    case 3: return K_AMERGE;
-    case 4: return K_O;
-    case 5: return K_RO;
-    case 6: return K_GU;
-    case 7: return K_DOWN;
-    default: return K_RDOWN;
+  if (ph == 1 + lp * a.L) return K_LM;
+  if (ph == 2 + lp * a.L) return K_FINAL;
+  *layer = (ph - 1) / lp;
+  int k = (ph - 1) % lp;
+  // QKV [RQKV] ATTN AMERGE O [RO] GU [RGU] DOWN [RDOWN]
+  const int seq[10] = {K_QKV, K_RQKV, K_ATTN, K_AMERGE, K_O, K_RO, K_GU, K_RGU, K_DOWN, K_RDOWN};
+  const bool has[10] = {true, !(a.fused >> MK_QKV & 1), true, true, true, !(a.fused >> MK_O & 1),
+                        true, !(a.fused >> MK_GU & 1), true, !(a.fused >> MK_DOWN & 1)};
+#pragma unroll
+  for (int i = 0; i < 10; i++) {
+    if (!has[i]) continue;
+    if (k == 0) return seq[i];
+    k--;
   }
+  return K_FINAL;  // unreachable
 }
-// GEMMs whose tiles are finalised inside their own phase
-__device__ __forceinline__ bool fused_reduce(int kind) { return kind == K_GU || kind == K_LM; }
 // the GEMM whose chunk partials a reduction phase finalises
 __device__ __forceinline__ int gemm_kind_of_reduce(int kind) {
   return kind == K_RQKV ? K_QKV : kind == K_RO ? K_O : kind == K_RGU ? K_GU : kind == K_RDOWN ? K_DOWN
@@ -147,6 +152,10 @@ __device__ __forceinline__ int gemm_kind_of_reduce(int kind) {
 __device__ __forceinline__ int gemm_of(int kind) {
   return kind == K_QKV ? MK_QKV : kind == K_O ? MK_O : kind == K_GU ? MK_GU : kind == K_DOWN ? MK_DOWN
        : kind == K_LM ? MK_LM : -1;
+}
+__device__ __forceinline__ bool fused_reduce_a(const Args& a, int kind) {
+  const int gi = gemm_of(kind);
+  return gi >= 0 && (a.fused >> gi & 1);
 }
 __device__ __forceinline__ const CUtensorMap* wmap_of(const Args& a, int gi, int l) {
   return gi == MK_LM ? &a.wmaps[4 * a.L] : &a.wmaps[4 * l + gi];
@@ -764,7 +773,7 @@ __device__ __noinline__ void epi_gemm(const Args& a, unsigned char* smem, int ph
       // slot (no synchronisation; the grid barrier publishes them)
       const MkPlan p = a.plan[gemm_of(kind)];
       const bool scaled = kind == K_QKV || kind == K_GU || kind == K_LM;
-      if (fused_reduce(kind) && scaled && et < B) {  // row norms r = rsqrt(sum x^2 / d + eps) of this GEMM's input
+      if (fused_reduce_a(a, kind) && scaled && et < B) {  // row norms r = rsqrt(sum x^2 / d + eps) of this GEMM's input
         const float4* sr = reinterpret_cast<const float4*>(a.ss + (size_t)et * n_ss);
         float sacc = 0.0f;
         for (int u = 0; u < n_ss / 4; u++) {
@@ -773,7 +782,7 @@ __device__ __noinline__ void epi_gemm(const Args& a, unsigned char* smem, int ph
         }
         rn[et] = rsqrtf(sacc / (float)d + a.eps);
       }
-      const bool fused = fused_reduce(kind);
+      const bool fused = fused_reduce_a(a, kind);
       bool phase_tasks_done = false;
       const int ev_w_base = 0;
       (void)ev_w_base;
@@ -944,7 +953,7 @@ __device__ __noinline__ void epi_reduce(const Args& a, unsigned char* smem, int 
   const int gk = gemm_kind_of_reduce(kind);
   const MkPlan p = a.plan[gemm_of(gk)];
   if (blockIdx.x >= p.tiles) return;
-  if (gk == K_QKV && et < B) {  // row norms of the QKV input
+  if ((gk == K_QKV || gk == K_GU) && et < B) {  // row norms of the GEMM input
     const float4* sr = reinterpret_cast<const float4*>(a.ss + (size_t)et * n_ss);
     float sacc = 0.0f;
     for (int u = 0; u < n_ss / 4; u++) {
@@ -972,7 +981,7 @@ __device__ __noinline__ void role_helper(const Args& a, unsigned char* smem) {
     int l;
     const int kind = phase_kind(a, ph, &l);
     const int gi = gemm_of(kind);
-    if (gi < 0 || !fused_reduce(kind)) continue;
+    if (gi < 0 || !fused_reduce_a(a, kind)) continue;
     const MkPlan p = a.plan[gi];
     while (true) {
       if (*ev_cnt <= ev_pos) {
@@ -1285,7 +1294,10 @@ __global__ void __launch_bounds__(kThreads, 1) decode_mk_kernel(const __grid_con
 
 }  // namespace
 
-int mk_phases(int L) { return 3 + 9 * L; }
+int mk_phases(int L) { return 3 + 10 * L; }  // upper bound (any fused mask)
+int mk_phases(int L, int fused) {
+  return 3 + L * (6 + !(fused >> MK_QKV & 1) + !(fused >> MK_O & 1) + !(fused >> MK_GU & 1) + !(fused >> MK_DOWN & 1));
+}
 
 int mk_grid() {
   static int n_sm = 0;
@@ -1333,6 +1345,7 @@ void launch_decode_mk(const MkLaunch& l, cudaStream_t s) {
   a.part_keys = l.part_keys; a.logits = l.logits; a.bar = l.bar; a.trace = l.trace;
   a.grab = l.grab;
   a.flags = l.flags;
+  a.fused = l.fused | (1 << MK_LM);  // lm_head always finalises in-phase (FINAL follows)
   a.pf_stages = std::max(1, std::min(kStages, l.pf_stages > 0 ? l.pf_stages : kStages));
   decode_mk_kernel<<<l.grid, kThreads, kSmem, s>>>(*reinterpret_cast<const CUtensorMap*>(l.map_xg.bytes),
                                                    *reinterpret_cast<const CUtensorMap*>(l.map_attn.bytes),

@@ -56,6 +56,7 @@ struct MkLaunch {
   unsigned long long* bar;       // [2]: grid barrier arrivals, exits (self-resetting)
   int* grab;                     // [phases] chunk counters (self-resetting)
   int flags;                     // diagnostics: 1 = no weight prefetch across grid barriers
+  int fused;                     // bit MK_*: that GEMM's tiles are finalised inside its phase
   int pf_stages;                 // weight stages prefetched ahead of a grid barrier (0 = whole ring)
   unsigned long long* trace;     // diagnostics (null): [phases][2][grid] globaltimer at barrier pass / phase end
 };
@@ -64,6 +65,7 @@ MkPlan mk_plan(int tiles, int kb_total, int grid, int per_cta = 4, int cap = 16)
 size_t mk_partial_floats(const MkPlan* plans);
 void launch_decode_mk(const MkLaunch& l, cudaStream_t s);
 int mk_grid();
-int mk_phases(int L);
+int mk_phases(int L);             // upper bound over fused masks (buffer sizing)
+int mk_phases(int L, int fused);  // phases of a tick with that fused mask
 
 }  // namespace fe

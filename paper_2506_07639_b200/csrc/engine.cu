@@ -194,6 +194,7 @@ struct fe_engine {
   size_t mk_trace_n = 0;
   bool mk_trace_on = false;
   int mk_flags = 0;
+  int mk_fused = (1 << fe::MK_GU) | (1 << fe::MK_LM);  // option "mk_fused"
   cudaEvent_t mk_ev[kLanes] = {};  // last persistent tick of each lane
   bool mk_ev_used[kLanes] = {};
   int mk_pf_stages = 0;  // 0 = the whole ring
@@ -416,6 +417,7 @@ void launch_layers(fe_engine* e, Lane& ln, const fe::Fwd& f, int n, bool decode,
     k.trace = e->mk_trace_on ? e->mk_trace : nullptr;
     k.grab = ln.mk_grab;
     k.flags = e->mk_flags;
+    k.fused = e->mk_fused;
     k.pf_stages = e->mk_pf_stages;
     const int p = prof_begin(e, ln, PROF_TICK);
     fe::launch_decode_mk(k, st);
@@ -1448,6 +1450,9 @@ int fe_set_option(fe_engine* e, const char* key, int64_t value) {
       }
       e->mk_trace_on = value != 0 && e->mk_trace != nullptr;
       clear_graphs(e);
+    } else if (k == "mk_fused") {
+      e->mk_fused = (int)value;
+      clear_graphs(e);
     } else if (k == "mk_flags") {
       e->mk_flags = (int)value;
       clear_graphs(e);
@@ -1488,7 +1493,7 @@ int fe_debug_trace(fe_engine* e, uint64_t* out, int32_t n, int32_t* n_phases, in
     CK(cudaStreamSynchronize(e->lanes[0].stream));
     const size_t k = std::min<size_t>((size_t)std::max(n, 0), e->mk_trace_n);
     CK(cudaMemcpy(out, e->mk_trace, k * 8, cudaMemcpyDeviceToHost));
-    *n_phases = fe::mk_phases(e->m.L);
+    *n_phases = fe::mk_phases(e->m.L, e->mk_fused | (1 << fe::MK_LM));
     *grid = e->mk_grid;
   });
 }

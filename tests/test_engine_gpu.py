@@ -431,6 +431,25 @@ def test_bf16_persistent_tick_matches_kernel_chain(config, plen):
     assert t1[0] == t0[0]
 
 
+@pytest.mark.parametrize("fused", [0, 31])
+def test_bf16_persistent_tick_fused_masks(fused):
+    """Every GEMM finalised in a separate reduction phase (0) or inside its
+    own phase by the helper warp (31): same tokens / logits as the kernel chain."""
+    from oracle.backend import frame
+    ids = frame("small", list(range(16)), list(range(500, 780)), "plan")
+    out = {}
+    for mk in (1, 0):
+        eng = Engine("small", dtype="bf16", seed=0, kv_pages=64, max_rows=512)
+        eng.set_option("mk", mk)
+        eng.set_option("mk_fused", fused)
+        out[mk] = _decode(eng, ids, 4242, 6, capture=True)
+        eng.close()
+    (t1, l1), (t0, l0) = out[1], out[0]
+    rel = np.abs(l1[0] - l0[0]).max() / np.abs(l0[0]).max()
+    assert rel < 2e-2, rel
+    assert t1[0] == t0[0]
+
+
 def test_bf16_persistent_tick_branch_batch():
     """7 forked branches (shared trunk pages + private suffixes) decoded as one
     batch by the persistent tick kernel vs the kernel chain."""

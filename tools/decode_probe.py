@@ -88,9 +88,11 @@ if args.trace:
     tr = eng.debug_trace().astype(np.int64)  # [P][6][G]
     P = tr.shape[0]
     t0 = tr[0, 0].min()
-    names = (["EMBED"] + [n for l in range(cfg.n_layers)
-                          for n in ("QKV", "RQKV", "ATTN", "AMERGE", "O", "RO", "GU", "DOWN", "RDOWN")]
-             + ["LM", "FINAL"])
+    fused = int(dict(o.split("=") for o in args.opt).get("mk_fused", 20)) if args.opt else 20
+    seq = [("QKV", -1), ("RQKV", 0), ("ATTN", -1), ("AMERGE", -1), ("O", -1), ("RO", 1),
+           ("GU", -1), ("RGU", 2), ("DOWN", -1), ("RDOWN", 3)]  # reduction phases exist unless fused
+    layer = [n for n, bit in seq if bit < 0 or not (fused >> bit & 1)]
+    names = ["EMBED"] + layer * cfg.n_layers + ["LM", "FINAL"]
     agg = {}
     print("phase         start   span | W-issue end   1st acc      last acc     drained  (min/max us from phase start)")
     for ph in range(P):
