@@ -293,14 +293,16 @@ class Engine:
                                              ctypes.c_void_p(y_ptr)))
 
     def debug_trace(self) -> np.ndarray:
-        """Persistent-tick phase timestamps [phases][6][grid] (ns) of the last tick:
+        """Persistent-tick phase timestamps [phases][10][grid] (ns) of the last tick:
         barrier passed, phase done, last weight load issued, first / last
-        accumulator ready, segments drained."""
+        accumulator ready, segments drained, first stage landed, pending
+        input (X) loads issued, last stage of the first chunk landed, first
+        weight load issued."""
         n = 4 * 1024 * 1024
         out = np.zeros(n, dtype=np.uint64)
         ph, g = ctypes.c_int(), ctypes.c_int()
         self._check(self.lib.fe_debug_trace(self._h, _np_ptr(out), n, ctypes.byref(ph), ctypes.byref(g)))
-        return out[: ph.value * 6 * g.value].reshape(ph.value, 6, g.value)
+        return out[: ph.value * 10 * g.value].reshape(ph.value, 10, g.value)
 
     def set_option(self, key: str, value: int) -> None:
         self._check(self.lib.fe_set_option(self._h, key.encode(), int(value)))
