@@ -117,21 +117,16 @@ int fe_op_gemm_tc(fe_engine* e, const void* x, const void* w, int32_t M, int32_t
 /* bf16 tcgen05 swap-AB decode GEMM (M <= 16 rows): y[M][N] = x[M][K] . w[N][K]^T */
 int fe_op_skinny_tc(fe_engine* e, const void* x, const void* w, int32_t M, int32_t N, int32_t K, float* y);
 /* diagnostics of the persistent decode-tick kernel (option "mk_trace" = 1):
- * globaltimer ns of the last traced tick, out[(10 ph + k) * grid + cta]: k = 0
+ * globaltimer ns of the last traced tick, out[(6 ph + k) * grid + cta]: k = 0
  * barrier passed, 1 phase done, 2 last weight load issued, 3 / 4 first / last
- * accumulator ready, 5 segments drained, 6 first stage landed, 7 pending
- * input loads issued, 8 last stage of the first chunk landed, 9 last weight
- * prefetch issued before the barrier */
+ * accumulator ready, 5 segments drained */
 int fe_debug_trace(fe_engine* e, uint64_t* out, int32_t n, int32_t* n_phases, int32_t* grid);
 /* engine options: "tc_min_rows" (rows from which a forward uses the tcgen05
  * GEMMs, bf16 only), "use_tc" (0/1), "mk" (0/1: persistent decode-tick
  * kernel), "mk_trace", "graphs", "pdl", "sk_mask", "sk_stages", "op_reps",
- * "debug_skip"; tick tuning: "mk_per_cta", "mk_nc_cap", "mk_nc_cap_o",
- * "mk_tail", "mk_tail_nc" (chunk plans), "mk_pf" (weight stages prefetched
- * across a barrier), "mk_fused" (bit per GEMM: finalise tiles in-phase),
- * "mk_l2pf" (bit per GEMM: L2 prefetch of its weights), "mk_o_early",
- * "mk_tiled" (stream pre-tiled weight copies), "mk_xtiled" (swizzled GEMM
- * input blocks), "mk_flags" (diagnostics) */
+ * "debug_skip"; tick tuning: "mk_per_cta", "mk_nc_cap", "mk_nc_cap_o" (chunk
+ * plans), "mk_pf" (weight stages prefetched across a barrier), "mk_fused"
+ * (bit per GEMM: finalise its tiles in-phase), "mk_flags" (diagnostics) */
 int fe_set_option(fe_engine* e, const char* key, int64_t value);
 
 #ifdef __cplusplus

@@ -50,7 +50,6 @@
 
 #include <algorithm>
 #include <stdexcept>
-#include <string>
 
 namespace fe {
 namespace {
@@ -60,7 +59,6 @@ constexpr int MT = 128;                    // weight rows per tile (UMMA M)
 constexpr int KBK = 64;                    // K per ring stage
 constexpr int XR = 16;                     // batch rows (UMMA N)
 constexpr int kStages = 11;
-constexpr int kTr = 10;  // trace slots per (phase, CTA)
 constexpr int kAcc = 4;
 constexpr int kWBytes = MT * KBK * 2;      // 16 KB
 constexpr int kXBytes = XR * KBK * 2;      // 2 KB
@@ -110,15 +108,10 @@ struct Args {
   unsigned long long* bar;
   int flags;                  // diagnostics (engine option "mk_flags")
   int fused;                  // bit MK_*: GEMM finalised in-phase (option "mk_fused")
-  int l2pf;                   // bit MK_*: that GEMM's weights are prefetched into L2 ahead of its phase
-  int o_early;                // O weight stages issued while the attention merge runs
-  int xtiled;                 // GEMM inputs in swizzled [K / 64][16][64] blocks (bulk copies), else row-major
-  const unsigned char* const* wtiled;  // [4 L + 1] pre-tiled weights (null: 2-D TMA boxes of the row-major weights)
   int pf_stages;              // weight stages prefetched ahead of a phase's grid barrier (<= kStages)
   int* grab;                  // [P] chunk counters of the GEMM phases (reset by the last CTA to exit)
-  unsigned long long* trace;  // diagnostics: [P][10][G] globaltimer: barrier pass, phase done, last weight load issued,
-                             // first / last accumulator ready, segments drained, first stage landed (MMA warp),
-                             // pending X loads issued (producer), last stage of the first chunk landed, first weight load issued
+  unsigned long long* trace;  // diagnostics: [P][6][G] globaltimer: barrier pass, phase done, last weight load issued,
+                             // first / last accumulator ready, segments drained
 };
 
 // per layer: QKV, RQKV, ATTN, AMERGE, O, RO, GU, DOWN, RDOWN.  Gate/up and
@@ -164,15 +157,6 @@ __device__ __forceinline__ bool fused_reduce_a(const Args& a, int kind) {
   const int gi = gemm_of(kind);
   return gi >= 0 && (a.fused >> gi & 1);
 }
-// Element offset of (row, col) in a 16-row GEMM input buffer (xg, attention
-// output, SwiGLU activation).  a.xtiled: [K / 64][16][64] blocks holding the
-// 128B-swizzled shared-memory image of one ring stage's input (16-byte chunk c
-// of row r at c ^ (r & 7)), so the producer moves it with one 2 KB bulk copy;
-// else row-major [16][stride] behind a 2-D TMA box.
-__device__ __forceinline__ size_t xt_off(const Args& a, int row, int col, int stride) {
-  if (!a.xtiled) return (size_t)row * stride + col;
-  return (size_t)(col >> 6) * (XR * KBK) + row * KBK + ((((col >> 3) & 7) ^ (row & 7)) << 3) + (col & 7);
-}
 __device__ __forceinline__ const CUtensorMap* wmap_of(const Args& a, int gi, int l) {
   return gi == MK_LM ? &a.wmaps[4 * a.L] : &a.wmaps[4 * l + gi];
 }
@@ -180,23 +164,10 @@ __device__ __forceinline__ const CUtensorMap* wmap_of(const Args& a, int gi, int
 // ids q = t * nc + j from a per-phase counter (tile-major, so tiles complete
 // progressively through the phase and fast SMs simply take more chunks).
 __device__ __forceinline__ void chunk_range(const MkPlan& p, int q, int* t, int* j, int* kb0, int* kb1) {
-  const int qs = p.t2 * p.nc;  // tiles >= t2 (the phase's tail) use nc2 finer chunks
-  int nc = p.nc;
-  if (q < qs) {
-    *t = q / nc;
-    *j = q - *t * nc;
-  } else {
-    nc = p.nc2;
-    const int qq = q - qs;
-    *t = p.t2 + qq / nc;
-    *j = qq - (*t - p.t2) * nc;
-  }
-  *kb0 = *j * p.kb_total / nc;
-  *kb1 = (*j + 1) * p.kb_total / nc;
-}
-__device__ __forceinline__ int tile_nc(const MkPlan& p, int t) { return t < p.t2 ? p.nc : p.nc2; }
-__device__ __forceinline__ int tile_q0(const MkPlan& p, int t) {
-  return t < p.t2 ? t * p.nc : p.t2 * p.nc + (t - p.t2) * p.nc2;
+  *t = q / p.nc;
+  *j = q - *t * p.nc;
+  *kb0 = *j * p.kb_total / p.nc;
+  *kb1 = (*j + 1) * p.kb_total / p.nc;
 }
 // producer -> MMA / epilogue queue of grabbed chunk ids (-1 ends a phase)
 constexpr int kQueue = 32;
@@ -524,7 +495,7 @@ __device__ void attn_merge(const Args& a, const RowMeta& m, int row, int h, int 
   uint2 packed;
   packed.x = pack_bf16(acc0 * inv, acc1 * inv);
   packed.y = pack_bf16(acc2 * inv, acc3 * inv);
-  *reinterpret_cast<uint2*>(a.attn + xt_off(a, row, h * HD + 4 * lane, a.d)) = packed;
+  *reinterpret_cast<uint2*>(a.attn + (size_t)row * a.d + h * HD + 4 * lane) = packed;
 }
 
 __device__ __forceinline__ int ld_acquire_i32(const int* p) {
@@ -580,7 +551,7 @@ __device__ __forceinline__ void tile_epilogue(const Args& a, int kind, int l, in
     for (int b = 0; b < B; b++) {
       const float xv = tile[r * (XR + 1) + b];  // old x already folded into the sum
       a.x[(size_t)b * d + col] = xv;
-      a.xg[xt_off(a, b, col, d)] = __float2bfloat16_rn(xv * gw);
+      a.xg[(size_t)b * d + col] = __float2bfloat16_rn(xv * gw);
     }
     epi_sumsq_cols(const_cast<float*>(tile), red, B, a.ss + tl, a.d / MT, et);  // ss[row][tile]
   } else if (kind == K_GU) {
@@ -588,7 +559,7 @@ __device__ __forceinline__ void tile_epilogue(const Args& a, int kind, int l, in
 #pragma unroll 4
       for (int b = 0; b < B; b++) {
         const float gt = tile[et * (XR + 1) + b] * rn[b], up = tile[(et + 64) * (XR + 1) + b] * rn[b];
-        a.attn[xt_off(a, b, tl * 64 + et, a.F)] = __float2bfloat16_rn(__fdividef(gt, 1.0f + __expf(-gt)) * up);
+        a.attn[(size_t)b * a.F + tl * 64 + et] = __float2bfloat16_rn(__fdividef(gt, 1.0f + __expf(-gt)) * up);
       }
   } else {  // K_LM
     const int nrow = n0 + r;
@@ -663,7 +634,7 @@ __device__ __noinline__ void epi_embed(const Args& a, unsigned char* smem, int p
           tile[et * (XR + 1) + b] = xv[b];
           if (b < B) {
             a.x[(size_t)b * d + col] = xv[b];
-            a.xg[xt_off(a, b, col, d)] = __float2bfloat16_rn(xv[b] * gw);
+            a.xg[(size_t)b * d + col] = __float2bfloat16_rn(xv[b] * gw);
           }
         }
         epi_sync();
@@ -686,7 +657,7 @@ __device__ __noinline__ void epi_attn(const Args& a, unsigned char* smem, int ph
       // bulk copies, all in flight at once, then one warp per pair computes.
       const int n_pairs = a.hdr[1] * a.H;
       const __nv_bfloat16* pool_l = a.kv_pool + (size_t)l * 2 * a.H * FE_PAGE * HD;
-      if (a.trace && et == 0) a.trace[((size_t)ph * kTr + 2) * G + blockIdx.x] = gtimer();
+      if (a.trace && et == 0) a.trace[((size_t)ph * 6 + 2) * G + blockIdx.x] = gtimer();
       for (int base = blockIdx.x, round = 0; base < n_pairs; base += kAttnSlots * G, round++) {
         auto item_of = [&](int j, int pr) -> AttnItem { return round == 0 ? sitems[j] : a.items[pr / a.H]; };
         // each warp stages K and V of its own pairs (j = warp, warp + 4) with
@@ -728,17 +699,17 @@ __device__ __noinline__ void epi_attn(const Args& a, unsigned char* smem, int ph
           if (ngroups - gi - 1 >= 1) asm volatile("cp.async.wait_group 1;" ::: "memory");
           else asm volatile("cp.async.wait_group 0;" ::: "memory");
           __syncwarp();
-          if (a.trace && et == 0 && round == 0 && gi == 0) a.trace[((size_t)ph * kTr + 3) * G + blockIdx.x] = gtimer();
+          if (a.trace && et == 0 && round == 0 && gi == 0) a.trace[((size_t)ph * 6 + 3) * G + blockIdx.x] = gtimer();
           const unsigned char* slot = sw + (size_t)j * kAttnSlotBytes;
           unsigned long long* dbg = nullptr;  // diagnostics (flags & 4): sub-step times of CTA 0's first pair
           if ((a.flags & 4) && a.trace && blockIdx.x == 0 && et == 0 && j == 0 && round == 0)
-            dbg = a.trace + ((size_t)(n_phases(a) - 1) * kTr + 2) * G + 8 * l;  // FINAL phase slot 2, [layer][4]
+            dbg = a.trace + ((size_t)(n_phases(a) - 1) * 6 + 2) * G + 8 * l;  // FINAL phase slot 2, [layer][4]
           attn_pair(a, srows, it, irows, pr % a.H, slot, slot + kAttnSlotBytes / 2, q0, q1, lane, dbg);
         }
-        if (a.trace && et == 0 && round == 0) a.trace[((size_t)ph * kTr + 4) * G + blockIdx.x] = gtimer();
+        if (a.trace && et == 0 && round == 0) a.trace[((size_t)ph * 6 + 4) * G + blockIdx.x] = gtimer();
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem reads before async writes
         epi_sync();  // slots reused by the next round
-        if (a.trace && et == 0 && round == 0) a.trace[((size_t)ph * kTr + 5) * G + blockIdx.x] = gtimer();
+        if (a.trace && et == 0 && round == 0) a.trace[((size_t)ph * 6 + 5) * G + blockIdx.x] = gtimer();
       }
 }
 
@@ -751,14 +722,14 @@ __device__ __noinline__ void epi_amerge(const Args& a, unsigned char* smem, int 
   const int d = a.d, B = a.B;
   const int n_ss = d / MT;
   (void)r; (void)d; (void)B; (void)n_ss; (void)G;
-      if (a.trace && et == 0) a.trace[((size_t)ph * kTr + 2) * G + blockIdx.x] = gtimer();
+      if (a.trace && et == 0) a.trace[((size_t)ph * 6 + 2) * G + blockIdx.x] = gtimer();
       for (int pr = blockIdx.x * 4 + (et >> 5); pr < B * a.H; pr += G * 4) {
         attn_merge(a, srows[pr / a.H], pr / a.H, pr % a.H, lane);
-        if (a.trace && et == 0) a.trace[((size_t)ph * kTr + 3) * G + blockIdx.x] = gtimer();
+        if (a.trace && et == 0) a.trace[((size_t)ph * 6 + 3) * G + blockIdx.x] = gtimer();
       }
-      if (a.trace && et == 0) a.trace[((size_t)ph * kTr + 4) * G + blockIdx.x] = gtimer();
+      if (a.trace && et == 0) a.trace[((size_t)ph * 6 + 4) * G + blockIdx.x] = gtimer();
       epi_sync();
-      if (a.trace && et == 0) a.trace[((size_t)ph * kTr + 5) * G + blockIdx.x] = gtimer();
+      if (a.trace && et == 0) a.trace[((size_t)ph * 6 + 5) * G + blockIdx.x] = gtimer();
 }
 
 __device__ __noinline__ void epi_final(const Args& a, unsigned char* smem, int ph, int l, int kind) {
@@ -844,8 +815,8 @@ __device__ __noinline__ void epi_gemm(const Args& a, unsigned char* smem, int ph
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         if (a.trace && et == 0) {
           const uint64_t tnow = gtimer();
-          if (first_chunk) a.trace[((size_t)ph * kTr + 3) * G + blockIdx.x] = tnow;
-          a.trace[((size_t)ph * kTr + 4) * G + blockIdx.x] = tnow;
+          if (first_chunk) a.trace[((size_t)ph * 6 + 3) * G + blockIdx.x] = tnow;
+          a.trace[((size_t)ph * 6 + 4) * G + blockIdx.x] = tnow;
         }
         first_chunk = false;
         uint32_t raw[16];
@@ -880,7 +851,7 @@ __device__ __noinline__ void epi_gemm(const Args& a, unsigned char* smem, int ph
           run_tasks(tasks_now);  // tiles completed meanwhile (uniform: snapshot taken before the sync)
         }
       }
-      if (a.trace && et == 0) a.trace[((size_t)ph * kTr + 5) * G + blockIdx.x] = gtimer();
+      if (a.trace && et == 0) a.trace[((size_t)ph * 6 + 5) * G + blockIdx.x] = gtimer();
       // no more chunks: tell the helper, then finalise the remaining tasks of this phase
       if (!fused) return;
       if (et == 0) {
@@ -925,12 +896,11 @@ __device__ __noinline__ void finalize_tile(const Args& a, unsigned char* smem, i
   float4 acc4[XR / 4];
 #pragma unroll
   for (int q4 = 0; q4 < XR / 4; q4++) acc4[q4] = make_float4(0.f, 0.f, 0.f, 0.f);
-  const size_t q0 = (size_t)tile_q0(p, tl);
-  const int tnc = tile_nc(p, tl);
-  if (B <= 8) {  // nc <= 16  // every chunk's 2 float4 requested together (straight-line registers)
+  const size_t q0 = (size_t)tl * p.nc;
+  if (B <= 8 && p.nc <= 16) {  // every chunk's 2 float4 requested together (straight-line registers)
     const float4* src = reinterpret_cast<const float4*>(a.partial) + q0 * (XR / 4) * MT + r;
     const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-    const int nc = tnc;
+    const int nc = p.nc;
     const bool two = B > 4;
 #define MK_P(u) const float4 pa##u = u < nc ? __ldcg(src + (size_t)(u) * (XR / 4) * MT) : z; \
           const float4 pb##u = (u < nc && two) ? __ldcg(src + (size_t)(u) * (XR / 4) * MT + MT) : z;
@@ -943,19 +913,19 @@ __device__ __noinline__ void finalize_tile(const Args& a, unsigned char* smem, i
     MK_S(8) MK_S(9) MK_S(10) MK_S(11) MK_S(12) MK_S(13) MK_S(14) MK_S(15)
 #undef MK_S
   } else {
-    for (int c0 = 0; c0 < tnc; c0 += 4) {
+    for (int c0 = 0; c0 < p.nc; c0 += 4) {
       float4 v[4][XR / 4];
 #pragma unroll
       for (int u = 0; u < 4; u++)
 #pragma unroll
         for (int q4 = 0; q4 < XR / 4; q4++)
-          if (c0 + u < tnc && 4 * q4 < B)
+          if (c0 + u < p.nc && 4 * q4 < B)
             v[u][q4] = __ldcg(reinterpret_cast<const float4*>(a.partial) + ((q0 + c0 + u) * (XR / 4) + q4) * MT + r);
 #pragma unroll
       for (int u = 0; u < 4; u++)
 #pragma unroll
         for (int q4 = 0; q4 < XR / 4; q4++)
-          if (c0 + u < tnc && 4 * q4 < B) {
+          if (c0 + u < p.nc && 4 * q4 < B) {
             acc4[q4].x += v[u][q4].x; acc4[q4].y += v[u][q4].y;
             acc4[q4].z += v[u][q4].z; acc4[q4].w += v[u][q4].w;
           }
@@ -992,9 +962,9 @@ __device__ __noinline__ void epi_reduce(const Args& a, unsigned char* smem, int 
     }
     rn[et] = rsqrtf(sacc / (float)d + a.eps);
   }
-  if (a.trace && et == 0) a.trace[((size_t)ph * kTr + 2) * G + blockIdx.x] = gtimer();
+  if (a.trace && et == 0) a.trace[((size_t)ph * 6 + 2) * G + blockIdx.x] = gtimer();
   for (int tl = blockIdx.x; tl < p.tiles; tl += G) finalize_tile(a, smem, l, gk, tl);
-  if (a.trace && et == 0) a.trace[((size_t)ph * kTr + 5) * G + blockIdx.x] = gtimer();
+  if (a.trace && et == 0) a.trace[((size_t)ph * 6 + 5) * G + blockIdx.x] = gtimer();
 }
 
 // Helper warp (lane 0): for every chunk the epilogue drained it adds to the
@@ -1025,7 +995,7 @@ __device__ __noinline__ void role_helper(const Args& a, unsigned char* smem) {
       ev_pos++;
       if (tl >= 0) {
         const int prev = atom_add_acq_rel(&a.counters[tl], 1);  // releases this CTA's partial of the chunk
-        if (prev != tile_nc(p, tl) - 1) continue;
+        if (prev != p.nc - 1) continue;
         a.counters[tl] = 0;  // next use is after a grid barrier
       }
       taskq[task_w % kRing] = tl;  // tile, or -1: no more tasks this phase
@@ -1056,50 +1026,20 @@ __device__ __noinline__ void role_producer(const Args& a, unsigned char* smem, c
         if (gi < 0) continue;
         const MkPlan p = a.plan[gi];
         const CUtensorMap* wm = wmap_of(a, gi, l);
-        const unsigned char* wt = a.wtiled ? a.wtiled[gi == MK_LM ? 4 * a.L : 4 * l + gi] : nullptr;
         const CUtensorMap* xm = gi == MK_O ? &map_attn : gi == MK_DOWN ? &map_act : &map_xg;
-        const unsigned char* xt = !a.xtiled ? nullptr
-                                  : (const unsigned char*)(gi == MK_O || gi == MK_DOWN ? a.attn : a.xg);
-        auto load_x = [&](int slot, int kb) {
-          if (xt) bulk_g2s(sx + slot * kXBytes, xt + (size_t)kb * kXBytes, kXBytes, &full[slot]);
-          else tma_load_2d(sx + slot * kXBytes, xm, &full[slot], kb * KBK, 0);
-        };
         // the attention phase borrows the ring: start the O weights only once this
         // CTA's epilogue warps have left it (they publish the AMERGE barrier)
         // -- and only once the merge's outputs are fenced: its stores then do not
         // queue behind the O weight stream (measured: merge 5.8 -> 3.5 us)
-        if (kind == K_O && (a.l2pf >> MK_O & 1)) {
-          // HBM is idle once the attention phase starts (the QKV stream is
-          // over): pull this CTA's share of the O weights into L2 meanwhile
-          wait_ready(ready_ph, ph - 2);
-          const int boxes = p.tiles * p.kb_total;
-          for (int b = blockIdx.x; b < boxes; b += G) {
-            if (wt) bulk_prefetch_l2(wt + (size_t)b * kWBytes, kWBytes);
-            else tma_prefetch_l2(wm, (b % p.kb_total) * KBK, (b / p.kb_total) * MT);
-          }
-        }
-        // the first o_early O stages may go out as soon as this CTA's attention
-        // left the ring (AMERGE started), the rest once the merge is fenced
-        if (kind == K_O) wait_ready(ready_ph, ph - 1);
-        bool o_gate = kind == K_O;
-        int issued = 0;
+        if (kind == K_O) wait_ready(ready_ph + 1, ph - 1);
         if (a.flags & 1) wait_ready(ready_ph, ph);  // diagnostics: no weight prefetch across barriers
         bool ready = false;
         int npend = 0;
         auto flush = [&]() {
-          if (a.flags & 64) {  // diagnostics: hold the input loads back 3 us (do the prefetched weights land?)
-            const uint64_t t0 = gtimer();
-            while (gtimer() - t0 < 3000) {}
-          }
-          if (a.trace) a.trace[((size_t)ph * kTr + 7) * G + blockIdx.x] = gtimer();
           __threadfence_block();
           fence_proxy_async();
-          for (int i0 = 0; i0 < npend && !(a.flags & 512); i0++) {
-            const int i = (a.flags & 128) ? npend - 1 - i0 : i0;  // diagnostics: reverse issue order
-            load_x(pend_slot[i], pend_kb[i]);
-            if ((a.flags & 1024) && a.trace && ph == 10 && blockIdx.x < 4 && i < 24)
-              a.trace[blockIdx.x * 96 + 48 + i] = gtimer();
-          }
+          for (int i = 0; i < npend; i++)
+            tma_load_2d(sx + pend_slot[i] * kXBytes, xm, &full[pend_slot[i]], pend_kb[i] * KBK, 0);
           npend = 0;
           ready = true;
         };
@@ -1116,36 +1056,22 @@ __device__ __noinline__ void role_producer(const Args& a, unsigned char* smem, c
           chunk_range(p, q, &tl, &j, &kb0, &kb1);
           for (int kb = kb0; kb < kb1; kb++, it++) {
             const int s = it % kStages;
-            if (o_gate && issued >= a.o_early) {
-              wait_ready(ready_ph + 1, ph - 1);
-              o_gate = false;
-            }
-            issued++;
             if (!ready && npend == a.pf_stages) {  // prefetch depth reached (<= kStages: the slot to refill waits)
               wait_ready(ready_ph, ph);
               flush();
             }
             mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
-            const bool nox = a.flags & 512;  // diagnostics: no activation loads (are they the per-stage limit?)
-            mbar_expect_tx(&full[s], nox ? kWBytes : kWBytes + kXBytes);
-            if (wt) {  // pre-tiled weights: one contiguous 16 KB run per stage
-              bulk_g2s_hint(sw + s * kWBytes, wt + ((size_t)tl * p.kb_total + kb) * kWBytes, kWBytes, &full[s], wpol);
-            } else if (gi == MK_GU) {
+            mbar_expect_tx(&full[s], kWBytes + kXBytes);
+            if (gi == MK_GU) {
               tma_load_2d_hint(sw + s * kWBytes, wm, &full[s], kb * KBK, tl * (MT / 2), wpol);
               tma_load_2d_hint(sw + s * kWBytes + kWBytes / 2, wm, &full[s], kb * KBK, a.F + tl * (MT / 2), wpol);
             } else {
               tma_load_2d_hint(sw + s * kWBytes, wm, &full[s], kb * KBK, tl * MT, wpol);
             }
-            if ((a.flags & 1024) && a.trace && ph == 10 && blockIdx.x < 4 && issued - 1 < 24)
-              a.trace[blockIdx.x * 96 + 24 + issued - 1] = gtimer();
             if (!ready && *ready_ph >= ph) flush();
-            if (nox) {
-            } else if (ready) {
-              load_x(s, kb);
-              if ((a.flags & 1024) && a.trace && ph == 10 && blockIdx.x < 4 && issued - 1 < 24)
-                a.trace[blockIdx.x * 96 + 48 + issued - 1] = gtimer();
+            if (ready) {
+              tma_load_2d(sx + s * kXBytes, xm, &full[s], kb * KBK, 0);
             } else {
-              if (a.trace) a.trace[((size_t)ph * kTr + 9) * G + blockIdx.x] = gtimer();  // last prefetch issue
               pend_slot[npend] = s;
               pend_kb[npend] = kb;
               npend++;
@@ -1153,7 +1079,7 @@ __device__ __noinline__ void role_producer(const Args& a, unsigned char* smem, c
           }
           q = q_next;
         }
-        if (a.trace) a.trace[((size_t)ph * kTr + 2) * G + blockIdx.x] = gtimer();
+        if (a.trace) a.trace[((size_t)ph * 6 + 2) * G + blockIdx.x] = gtimer();
         if (!ready) {
           wait_ready(ready_ph, ph);
           flush();
@@ -1174,8 +1100,6 @@ __device__ __noinline__ void role_mma(const Args& a, unsigned char* smem, uint32
         const int gi = gemm_of(phase_kind(a, ph, &l));
         if (gi < 0) continue;
         const MkPlan p = a.plan[gi];
-        bool first = true;
-        int sidx = 0;
         for (;; lu++) {
           const int q = queue_read(qseq, qval, n++);
           if (q < 0) break;
@@ -1189,17 +1113,10 @@ __device__ __noinline__ void role_mma(const Args& a, unsigned char* smem, uint32
             const int s = it % kStages;
             mbar_wait(&full[s], (it / kStages) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            if (first && a.trace) a.trace[((size_t)ph * kTr + (kb == kb0 ? 6 : 8)) * G + blockIdx.x] = gtimer();
-            if ((a.flags & 1024) && a.trace && ph == 10 && blockIdx.x < 4 && sidx < 24)  // diagnostics: per-stage landing
-              a.trace[blockIdx.x * 96 + sidx] = gtimer();
-            sidx++;
-            if (kb == kb1 - 1) first = false;
             const uint64_t da = smem_desc(sw + s * kWBytes);
             const uint64_t db = smem_desc(sx + s * kXBytes);
 #pragma unroll
             for (int k = 0; k < KBK / 16; k++) {
-              if (a.flags & 256) break;  // diagnostics: no MMAs (is the tensor core the per-stage limit?)
-              if ((a.flags & 2048) && k > 0) break;  // diagnostics: one MMA per stage
               const uint64_t off = (uint64_t)((k * 32) >> 4);
               const uint32_t accum = (kb > kb0 || k > 0) ? 1u : 0u;
               asm volatile(
@@ -1234,7 +1151,7 @@ __device__ __noinline__ void role_epilogue(const Args& a, unsigned char* smem, u
       const int kind = phase_kind(a, ph, &l);
       if (et == 0) {
         spin_until(a.bar, (unsigned long long)ph * G);
-        if (a.trace) a.trace[((size_t)ph * kTr) * G + blockIdx.x] = gtimer();
+        if (a.trace) a.trace[((size_t)ph * 6) * G + blockIdx.x] = gtimer();
         __threadfence_block();
         *ready_ph = ph;  // lets the producer issue this phase's activation loads
       }
@@ -1257,7 +1174,7 @@ __device__ __noinline__ void role_epilogue(const Args& a, unsigned char* smem, u
         epi_sync();
         if (et == 0) {
           ready_ph[1] = ph;  // this phase's outputs are fenced (the producer starts the O weights on it)
-          if (a.trace) a.trace[((size_t)ph * kTr + 1) * G + blockIdx.x] = gtimer();
+          if (a.trace) a.trace[((size_t)ph * 6 + 1) * G + blockIdx.x] = gtimer();
           atomicAdd(a.bar, 1ull);
         }
       }
@@ -1382,34 +1299,6 @@ int mk_phases(int L, int fused) {
   return 3 + L * (6 + !(fused >> MK_QKV & 1) + !(fused >> MK_O & 1) + !(fused >> MK_GU & 1) + !(fused >> MK_DOWN & 1));
 }
 
-// Weight tiling for the tick's stream: block (tile t, k-block kb) of a
-// [rows][K] bf16 matrix becomes one contiguous 16 KB run holding exactly the
-// shared-memory image a 128B-swizzled TMA box [64 cols x 128 rows] would
-// produce (16-byte chunk c of row r at position c ^ (r & 7)), so the producer
-// moves it with one 1-D bulk copy (measured ~84 GB/s per SM vs ~57 for the
-// 2-D box, tools/tma_bw.cu).  gu_F > 0: gate/up interleave, rows 0-63 of the
-// block are gate rows t*64.., rows 64-127 up rows gu_F + t*64...  Rows past
-// `rows` are zero (the lm_head tail).
-__global__ void mk_tile_kernel(uint4* dst, const __nv_bfloat16* src, int rows, int K, int tiles, int gu_F) {
-  const int kbt = K / KBK;
-  const size_t n = (size_t)tiles * kbt * MT * 8;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-    const size_t blk = i >> 10;
-    const int within = (int)(i & 1023), r = within >> 3, cpos = within & 7, c = cpos ^ (r & 7);
-    const int t = (int)(blk / kbt), kb = (int)(blk % kbt);
-    const int row = gu_F > 0 ? (r < MT / 2 ? t * (MT / 2) + r : gu_F + t * (MT / 2) + r - MT / 2) : t * MT + r;
-    uint4 v = make_uint4(0u, 0u, 0u, 0u);
-    if (row < rows) v = *reinterpret_cast<const uint4*>(src + (size_t)row * K + kb * KBK + c * 8);
-    dst[i] = v;
-  }
-}
-
-void mk_tile_weights(void* dst, const void* src, int rows, int K, int tiles, int gu_F, cudaStream_t s) {
-  mk_tile_kernel<<<4 * mk_grid(), 256, 0, s>>>((uint4*)dst, (const __nv_bfloat16*)src, rows, K, tiles, gu_F);
-  const cudaError_t err = cudaGetLastError();
-  if (err != cudaSuccess) throw std::runtime_error(std::string("mk_tile_weights: ") + cudaGetErrorString(err));
-}
-
 int mk_grid() {
   static int n_sm = 0;
   if (!n_sm) {
@@ -1420,19 +1309,14 @@ int mk_grid() {
   return n_sm;
 }
 
-MkPlan mk_plan(int tiles, int kb_total, int grid, int per_cta, int cap, int tail_chunks, int tail_nc) {
+MkPlan mk_plan(int tiles, int kb_total, int grid, int per_cta, int cap) {
   // enough chunks for ~per_cta per CTA (dynamic balance), at least 4 k-blocks
   // each, at most min(cap, 16) per tile (one load round in the reduction)
   int nc = (per_cta * grid + tiles - 1) / tiles;
   nc = std::max(1, std::min({nc, cap, 16, std::max(1, kb_total / 4)}));
-  // the last tiles of the phase (grabbed last) are cut finer, ~tail_chunks
-  // chunks in all, so the CTAs finish the phase within a small chunk of each other
-  int nc2 = std::max(1, std::min({tail_nc, 16, std::max(1, kb_total / 2)}));
-  int t2 = tiles;
-  if (tail_chunks > 0 && nc2 > nc) t2 = std::max(0, tiles - (tail_chunks + nc2 - 1) / nc2);
-  if (t2 == tiles) nc2 = nc;
-  return MkPlan{tiles, kb_total, nc, t2 * nc + (tiles - t2) * nc2, t2, nc2};
+  return MkPlan{tiles, kb_total, nc, tiles * nc};
 }
+
 size_t mk_partial_floats(const MkPlan* plans) {
   int chunks = 0;
   for (int i = 0; i < 5; i++) chunks = std::max(chunks, plans[i].tiles * 16);  // any plan up to 16 per tile
@@ -1461,11 +1345,7 @@ void launch_decode_mk(const MkLaunch& l, cudaStream_t s) {
   a.part_keys = l.part_keys; a.logits = l.logits; a.bar = l.bar; a.trace = l.trace;
   a.grab = l.grab;
   a.flags = l.flags;
-  a.fused = l.fused | (1 << MK_LM);
-  a.l2pf = l.l2pf;
-  a.o_early = l.o_early;
-  a.xtiled = l.xtiled;
-  a.wtiled = (const unsigned char* const*)l.wtiled;  // lm_head always finalises in-phase (FINAL follows)
+  a.fused = l.fused | (1 << MK_LM);  // lm_head always finalises in-phase (FINAL follows)
   a.pf_stages = std::max(1, std::min(kStages, l.pf_stages > 0 ? l.pf_stages : kStages));
   decode_mk_kernel<<<l.grid, kThreads, kSmem, s>>>(*reinterpret_cast<const CUtensorMap*>(l.map_xg.bytes),
                                                    *reinterpret_cast<const CUtensorMap*>(l.map_attn.bytes),

@@ -16,10 +16,9 @@ struct Fwd;
 struct ModelDims;
 
 // One GEMM of the tick: `tiles` tiles of 128 weight rows; the k-blocks of a
-// tile are cut into `nc` chunks that CTAs grab dynamically, tile-major; tiles
-// t >= t2 (the phase's tail) are cut into nc2 >= nc finer chunks.
+// tile are cut into `nc` chunks that CTAs grab dynamically (chunks = tiles * nc).
 struct MkPlan {
-  int tiles, kb_total, nc, chunks, t2, nc2;
+  int tiles, kb_total, nc, chunks;
 };
 enum MkGemm { MK_QKV = 0, MK_O = 1, MK_GU = 2, MK_DOWN = 3, MK_LM = 4 };
 
@@ -58,22 +57,14 @@ struct MkLaunch {
   int* grab;                     // [phases] chunk counters (self-resetting)
   int flags;                     // diagnostics: 1 = no weight prefetch across grid barriers
   int fused;                     // bit MK_*: that GEMM's tiles are finalised inside its phase
-  int l2pf;                      // bit MK_*: that GEMM's weights are prefetched into L2 while HBM idles
-  int o_early;                   // O weight stages issued during the attention merge (option "mk_o_early")
-  int xtiled;                    // GEMM inputs kept as swizzled 2 KB stage blocks (option "mk_xtiled")
-  const void* wtiled;            // device pointer[4 L + 1] to pre-tiled weights (mk_tile_weights), or null
   int pf_stages;                 // weight stages prefetched ahead of a grid barrier (0 = whole ring)
   unsigned long long* trace;     // diagnostics (null): [phases][2][grid] globaltimer at barrier pass / phase end
 };
 
-MkPlan mk_plan(int tiles, int kb_total, int grid, int per_cta = 4, int cap = 16, int tail_chunks = 0,
-               int tail_nc = 16);
+MkPlan mk_plan(int tiles, int kb_total, int grid, int per_cta = 4, int cap = 16);
 size_t mk_partial_floats(const MkPlan* plans);
 void launch_decode_mk(const MkLaunch& l, cudaStream_t s);
 int mk_grid();
-// contiguous 16 KB stage blocks of a weight matrix for the tick's bulk copies
-// (gu_F > 0: the gate/up matrix [2F][K], gate and up rows interleaved per block)
-void mk_tile_weights(void* dst, const void* src, int rows, int K, int tiles, int gu_F, cudaStream_t s);
 int mk_phases(int L);             // upper bound over fused masks (buffer sizing)
 int mk_phases(int L, int fused);  // phases of a tick with that fused mask
 

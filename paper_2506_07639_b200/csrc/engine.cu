@@ -195,18 +195,10 @@ struct fe_engine {
   bool mk_trace_on = false;
   int mk_flags = 0;
   int mk_fused = (1 << fe::MK_GU) | (1 << fe::MK_LM);  // option "mk_fused"
-  int mk_l2pf = 0;                                      // option "mk_l2pf"
-  int mk_o_early = 0;                                   // option "mk_o_early"
-  int mk_xtiled = 1;                                    // option "mk_xtiled"
-  int mk_tiled = 0;                 // option "mk_tiled": stream pre-tiled weights with 1-D bulk copies
-  void* mk_wt_base = nullptr;       // pre-tiled copies of every tick weight (mk_tile_weights)
-  void* mk_wt = nullptr;            // device pointer[4 L + 1] into mk_wt_base
-  bool mk_wt_dirty = true;          // weights changed since the last tiling
   cudaEvent_t mk_ev[kLanes] = {};  // last persistent tick of each lane
   bool mk_ev_used[kLanes] = {};
   int mk_pf_stages = 0;  // 0 = the whole ring
   int mk_per_cta = 4, mk_nc_cap = 8, mk_nc_cap_o = 0;  // chunk plans (mk_make_plans; swept in tools/mk_sweep.sh)
-  int mk_tail = 0, mk_tail_nc = 16;                      // fine-chunk tail of each GEMM phase
   bool graphs_on = true;
   bool lane1_yields = true;
   bool prefill_fa = true;  // option "prefill_fa": tensor-core causal prefill attention (bf16)  // option "lane1_yields": reasoning lane defers while the action lane has work
@@ -377,12 +369,12 @@ void clear_graphs(fe_engine* e) {
 // "mk_nc_cap" retune them; the partial buffers are sized for any plan).
 void mk_make_plans(fe_engine* e) {
   const fe::ModelDims& m = e->m;
-  const int G = e->mk_grid, pc = e->mk_per_cta, cap = e->mk_nc_cap, tc = e->mk_tail, tn = e->mk_tail_nc;
-  e->mk_plans[fe::MK_QKV] = fe::mk_plan(3 * m.d / 128, m.d / 64, G, pc, cap, tc, tn);
-  e->mk_plans[fe::MK_O] = fe::mk_plan(m.d / 128, m.d / 64, G, pc, e->mk_nc_cap_o > 0 ? e->mk_nc_cap_o : cap, tc, tn);
-  e->mk_plans[fe::MK_GU] = fe::mk_plan(m.F / 64, m.d / 64, G, pc, cap, tc, tn);
-  e->mk_plans[fe::MK_DOWN] = fe::mk_plan(m.d / 128, m.F / 64, G, pc, cap, tc, tn);
-  e->mk_plans[fe::MK_LM] = fe::mk_plan((m.V + 127) / 128, m.d / 64, G, pc, cap, tc, tn);
+  const int G = e->mk_grid, pc = e->mk_per_cta, cap = e->mk_nc_cap;
+  e->mk_plans[fe::MK_QKV] = fe::mk_plan(3 * m.d / 128, m.d / 64, G, pc, cap);
+  e->mk_plans[fe::MK_O] = fe::mk_plan(m.d / 128, m.d / 64, G, pc, e->mk_nc_cap_o > 0 ? e->mk_nc_cap_o : cap);
+  e->mk_plans[fe::MK_GU] = fe::mk_plan(m.F / 64, m.d / 64, G, pc, cap);
+  e->mk_plans[fe::MK_DOWN] = fe::mk_plan(m.d / 128, m.F / 64, G, pc, cap);
+  e->mk_plans[fe::MK_LM] = fe::mk_plan((m.V + 127) / 128, m.d / 64, G, pc, cap);
 }
 
 // ---- forward pass -----------------------------------------------------------
@@ -426,10 +418,6 @@ void launch_layers(fe_engine* e, Lane& ln, const fe::Fwd& f, int n, bool decode,
     k.grab = ln.mk_grab;
     k.flags = e->mk_flags;
     k.fused = e->mk_fused;
-    k.l2pf = e->mk_l2pf;
-    k.o_early = e->mk_o_early;
-    k.xtiled = e->mk_xtiled;
-    k.wtiled = e->mk_tiled ? e->mk_wt : nullptr;
     k.pf_stages = e->mk_pf_stages;
     const int p = prof_begin(e, ln, PROF_TICK);
     fe::launch_decode_mk(k, st);
@@ -1091,51 +1079,10 @@ int submit(fe_engine* e, int lane, int32_t seq, int32_t first_id, int32_t length
 // Tick a lane until `stop_req` completes (-1: until idle) or `max_ticks`
 // (<= 0: unbounded).  The engine lock is held per tick, so the two lanes can
 // be driven by two host threads concurrently.
-// Pre-tiled weight copies for the persistent tick (one contiguous 16 KB run
-// per ring stage): allocated on first use, rebuilt after the weights changed
-// (fe_weights_init_random / fe_weight_ptr).  Runs before any tick is enqueued
-// (never inside a graph capture) and waits for the copies.
-void mk_retile(fe_engine* e) {
-  if (!e->mk_on || !e->mk_tiled || !e->mk_wt_dirty) return;
-  std::lock_guard<std::mutex> lk(e->mu);
-  if (!e->mk_wt_dirty) return;
-  const fe::ModelDims& m = e->m;
-  const size_t d = m.d, F = m.F, lm_rows = (size_t)(m.V + 127) / 128 * 128;
-  const size_t per_layer = (4 * d * d + 3 * F * d) * 2;
-  if (!e->mk_wt_base) {
-    e->mk_wt_base = e->dalloc(per_layer * m.L + lm_rows * d * 2);
-    std::vector<const void*> ptrs(4 * m.L + 1);
-    for (int l = 0; l < m.L; l++) {
-      const char* b = (const char*)e->mk_wt_base + per_layer * l;
-      ptrs[4 * l + 0] = b;
-      ptrs[4 * l + 1] = b + 3 * d * d * 2;
-      ptrs[4 * l + 2] = b + 4 * d * d * 2;
-      ptrs[4 * l + 3] = b + (4 * d * d + 2 * F * d) * 2;
-    }
-    ptrs[4 * m.L] = (const char*)e->mk_wt_base + per_layer * m.L;
-    e->mk_wt = e->dalloc(ptrs.size() * sizeof(void*));
-    CK(cudaMemcpy(e->mk_wt, ptrs.data(), ptrs.size() * sizeof(void*), cudaMemcpyHostToDevice));
-  }
-  cudaStream_t st = e->lanes[0].stream;
-  CK(cudaDeviceSynchronize());  // no tick of either lane reads the copies meanwhile
-  for (int l = 0; l < m.L; l++) {
-    char* b = (char*)e->mk_wt_base + per_layer * l;
-    const auto& ly = e->layers[l];
-    fe::mk_tile_weights(b, ly.wqkv, 3 * m.d, m.d, 3 * m.d / 128, 0, st);
-    fe::mk_tile_weights(b + 3 * d * d * 2, ly.wo, m.d, m.d, m.d / 128, 0, st);
-    fe::mk_tile_weights(b + 4 * d * d * 2, ly.wgu, 2 * m.F, m.d, m.F / 64, m.F, st);
-    fe::mk_tile_weights(b + (4 * d * d + 2 * F * d) * 2, ly.wdown, m.d, m.F, m.d / 128, 0, st);
-  }
-  fe::mk_tile_weights((char*)e->mk_wt_base + per_layer * m.L, e->w.lm_head, m.V, m.d, (m.V + 127) / 128, 0, st);
-  CK(cudaStreamSynchronize(st));
-  e->mk_wt_dirty = false;
-}
-
 int run_lane(fe_engine* e, int lane, int32_t stop_req, int32_t max_ticks, int32_t cap, int32_t* n_ticks,
              int32_t* occupancy, int32_t* completed, int32_t* completed_tick, int32_t* n_completed) {
   try {
     if (!e) throw Error("null engine");
-    mk_retile(e);
     int t = 0, nc = 0;
     bool yield = false, paced = false;
     cudaEvent_t pace = nullptr;
@@ -1216,10 +1163,7 @@ int fe_engine_destroy(fe_engine* e) {
 }
 
 int fe_weights_init_random(fe_engine* e, uint64_t seed) {
-  return guarded(e, [&] {
-    init_weights(e, seed);
-    e->mk_wt_dirty = true;
-  });
+  return guarded(e, [&] { init_weights(e, seed); });
 }
 
 int fe_seq_create(fe_engine* e, int32_t* seq) {
@@ -1418,7 +1362,6 @@ int fe_stats(fe_engine* e, int64_t* out, int32_t n) {
 
 int fe_weight_ptr(fe_engine* e, int32_t tensor, int32_t layer, void** ptr, size_t* bytes) {
   return guarded(e, [&] {
-    e->mk_wt_dirty = true;  // the caller may write through the pointer: re-tile before the next tick
     const size_t d = e->m.d, F = e->m.F, V = e->m.V, el = e->elem;
     if (tensor == 1) { *ptr = e->w.embed; *bytes = V * d * el; return; }
     if (tensor == 2) { *ptr = e->w.lm_head; *bytes = V * d * el; return; }
@@ -1501,23 +1444,11 @@ int fe_set_option(fe_engine* e, const char* key, int64_t value) {
       clear_graphs(e);
     } else if (k == "mk_trace") {
       if (value && !e->mk_trace && e->mk_on) {
-        e->mk_trace_n = (size_t)fe::mk_phases(e->m.L) * 10 * e->mk_grid;
+        e->mk_trace_n = (size_t)fe::mk_phases(e->m.L) * 6 * e->mk_grid;
         e->mk_trace = (unsigned long long*)e->dalloc(e->mk_trace_n * 8);
         CK(cudaMemset(e->mk_trace, 0, e->mk_trace_n * 8));
       }
       e->mk_trace_on = value != 0 && e->mk_trace != nullptr;
-      clear_graphs(e);
-    } else if (k == "mk_tiled") {
-      e->mk_tiled = value != 0;
-      clear_graphs(e);
-    } else if (k == "mk_xtiled") {
-      e->mk_xtiled = value != 0;
-      clear_graphs(e);
-    } else if (k == "mk_o_early") {
-      e->mk_o_early = (int)value;
-      clear_graphs(e);
-    } else if (k == "mk_l2pf") {
-      e->mk_l2pf = (int)value;
       clear_graphs(e);
     } else if (k == "mk_fused") {
       e->mk_fused = (int)value;
@@ -1528,9 +1459,8 @@ int fe_set_option(fe_engine* e, const char* key, int64_t value) {
     } else if (k == "mk_pf") {
       e->mk_pf_stages = (int)value;
       clear_graphs(e);
-    } else if (k == "mk_per_cta" || k == "mk_nc_cap" || k == "mk_nc_cap_o" || k == "mk_tail" || k == "mk_tail_nc") {
-      (k == "mk_per_cta" ? e->mk_per_cta : k == "mk_nc_cap" ? e->mk_nc_cap : k == "mk_nc_cap_o" ? e->mk_nc_cap_o
-       : k == "mk_tail" ? e->mk_tail : e->mk_tail_nc) = (int)value;
+    } else if (k == "mk_per_cta" || k == "mk_nc_cap" || k == "mk_nc_cap_o") {
+      (k == "mk_per_cta" ? e->mk_per_cta : k == "mk_nc_cap" ? e->mk_nc_cap : e->mk_nc_cap_o) = (int)value;
       if (e->mk_on) mk_make_plans(e);
       clear_graphs(e);
     } else if (k == "prefill_fa") {

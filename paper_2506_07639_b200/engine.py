@@ -9,6 +9,7 @@ path.
 from __future__ import annotations
 
 import ctypes
+import os
 from pathlib import Path
 
 import numpy as np
@@ -16,7 +17,8 @@ import numpy as np
 from .backends import EngineError
 from .model import ModelConfig, ROPE_MAX_POS, TEXT_VOCAB, get_config, rope_table
 
-LIB_PATH = Path(__file__).resolve().parent / "_build" / "libfastecot.so"
+# FASTECOT_LIB: another build of the library (A/B timing of two builds on one box)
+LIB_PATH = Path(os.environ.get("FASTECOT_LIB", Path(__file__).resolve().parent / "_build" / "libfastecot.so"))
 
 F32, BF16 = 0, 1
 PRIO_ACTION, PRIO_REASONING = 0, 1
@@ -293,16 +295,14 @@ class Engine:
                                              ctypes.c_void_p(y_ptr)))
 
     def debug_trace(self) -> np.ndarray:
-        """Persistent-tick phase timestamps [phases][10][grid] (ns) of the last tick:
+        """Persistent-tick phase timestamps [phases][6][grid] (ns) of the last tick:
         barrier passed, phase done, last weight load issued, first / last
-        accumulator ready, segments drained, first stage landed, pending
-        input (X) loads issued, last stage of the first chunk landed, first
-        weight load issued."""
+        accumulator ready, segments drained."""
         n = 4 * 1024 * 1024
         out = np.zeros(n, dtype=np.uint64)
         ph, g = ctypes.c_int(), ctypes.c_int()
         self._check(self.lib.fe_debug_trace(self._h, _np_ptr(out), n, ctypes.byref(ph), ctypes.byref(g)))
-        return out[: ph.value * 10 * g.value].reshape(ph.value, 10, g.value)
+        return out[: ph.value * 6 * g.value].reshape(ph.value, 6, g.value)
 
     def set_option(self, key: str, value: int) -> None:
         self._check(self.lib.fe_set_option(self._h, key.encode(), int(value)))

@@ -310,6 +310,7 @@ class TwoStreamAsyncEngine:
         backend._slots = slots
         self._lock = threading.Lock()
         self._inflight: dict[int, EngineRequest] = {}
+        self._landing = 0  # completed requests the background thread is still landing
         self._now = 0
         self._errors: list[BaseException] = []
         self._stop = threading.Event()
@@ -342,7 +343,7 @@ class TwoStreamAsyncEngine:
 
     def idle(self) -> bool:
         with self._lock:
-            return not self._inflight
+            return not self._inflight and not self._landing
 
     def run_until_complete(self, h: EngineRequest, timestep: int) -> list[int]:
         self._raise_background_error()
@@ -372,17 +373,22 @@ class TwoStreamAsyncEngine:
             try:
                 _, done = eng.run(-1, lane=1, max_ticks=4)
                 for req, _tick in done:
+                    # take the handle out before the id is released: a submit on
+                    # the runner thread may reuse the id right after the release
                     with self._lock:
-                        h = self._inflight.get(req)
-                    h.tokens = tuple(eng.request_tokens(req, h.length))
-                    h.done = True
-                    eng.request_release(req)
-                    eng.seq_free(h.branch)
-                    self.backend._log(h)
-                    if h.on_complete is not None:
-                        h.on_complete(h, self._now)
-                    with self._lock:
-                        self._inflight.pop(req, None)
+                        h = self._inflight.pop(req)
+                        self._landing += 1
+                    try:
+                        h.tokens = tuple(eng.request_tokens(req, h.length))
+                        h.done = True
+                        eng.request_release(req)
+                        eng.seq_free(h.branch)
+                        self.backend._log(h)
+                        if h.on_complete is not None:
+                            h.on_complete(h, self._now)
+                    finally:
+                        with self._lock:
+                            self._landing -= 1
             except BaseException as exc:  # surfaced on the runner thread
                 self._errors.append(exc)
                 self._stop.set()

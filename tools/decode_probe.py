@@ -85,7 +85,7 @@ for rep in range(args.repeat):
           f"({dev/args.ticks:.3f} ms/tick), host enqueue {host*1e3:.2f} ms  {prof}", flush=True)
 if args.trace:
     import numpy as np
-    tr = eng.debug_trace().astype(np.int64)  # [P][10][G]
+    tr = eng.debug_trace().astype(np.int64)  # [P][6][G]
     P = tr.shape[0]
     t0 = tr[0, 0].min()
     fused = int(dict(o.split("=") for o in args.opt).get("mk_fused", 20)) if args.opt else 20

@@ -7,7 +7,7 @@ import numpy as np
 
 tr = np.load(sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/mk_trace.npy").astype(np.int64)
 first, last = (int(sys.argv[2]), int(sys.argv[3])) if len(sys.argv) > 3 else (1, 12)
-slots = ["bar", "done", "Wiss", "acc1", "accL", "drain", "land1", "Xiss", "landC", "Wst"]
+slots = ["bar", "done", "Wiss", "acc1", "accL", "drain"][: tr.shape[1]]
 for ph in range(first, min(last, tr.shape[0])):
     t0 = tr[ph, 0].min()
     row = []
