@@ -51,6 +51,11 @@
 #include <algorithm>
 #include <stdexcept>
 
+#ifndef MK_TRACE
+#define MK_TRACE 0  // decode_mk_trace.cu builds the instrumented variant
+#endif
+#define MKTR(a) (MK_TRACE ? (a).trace : (unsigned long long*)nullptr)
+
 namespace fe {
 namespace {
 using namespace tc;
@@ -657,7 +662,7 @@ __device__ __noinline__ void epi_attn(const Args& a, unsigned char* smem, int ph
       // bulk copies, all in flight at once, then one warp per pair computes.
       const int n_pairs = a.hdr[1] * a.H;
       const __nv_bfloat16* pool_l = a.kv_pool + (size_t)l * 2 * a.H * FE_PAGE * HD;
-      if (a.trace && et == 0) a.trace[((size_t)ph * 6 + 2) * G + blockIdx.x] = gtimer();
+      if (MKTR(a) && et == 0) MKTR(a)[((size_t)ph * 6 + 2) * G + blockIdx.x] = gtimer();
       for (int base = blockIdx.x, round = 0; base < n_pairs; base += kAttnSlots * G, round++) {
         auto item_of = [&](int j, int pr) -> AttnItem { return round == 0 ? sitems[j] : a.items[pr / a.H]; };
         // each warp stages K and V of its own pairs (j = warp, warp + 4) with
@@ -699,17 +704,17 @@ __device__ __noinline__ void epi_attn(const Args& a, unsigned char* smem, int ph
           if (ngroups - gi - 1 >= 1) asm volatile("cp.async.wait_group 1;" ::: "memory");
           else asm volatile("cp.async.wait_group 0;" ::: "memory");
           __syncwarp();
-          if (a.trace && et == 0 && round == 0 && gi == 0) a.trace[((size_t)ph * 6 + 3) * G + blockIdx.x] = gtimer();
+          if (MKTR(a) && et == 0 && round == 0 && gi == 0) MKTR(a)[((size_t)ph * 6 + 3) * G + blockIdx.x] = gtimer();
           const unsigned char* slot = sw + (size_t)j * kAttnSlotBytes;
           unsigned long long* dbg = nullptr;  // diagnostics (flags & 4): sub-step times of CTA 0's first pair
-          if ((a.flags & 4) && a.trace && blockIdx.x == 0 && et == 0 && j == 0 && round == 0)
-            dbg = a.trace + ((size_t)(n_phases(a) - 1) * 6 + 2) * G + 8 * l;  // FINAL phase slot 2, [layer][4]
+          if ((MK_TRACE && (a.flags & 4)) && MKTR(a) && blockIdx.x == 0 && et == 0 && j == 0 && round == 0)
+            dbg = MKTR(a) + ((size_t)(n_phases(a) - 1) * 6 + 2) * G + 8 * l;  // FINAL phase slot 2, [layer][4]
           attn_pair(a, srows, it, irows, pr % a.H, slot, slot + kAttnSlotBytes / 2, q0, q1, lane, dbg);
         }
-        if (a.trace && et == 0 && round == 0) a.trace[((size_t)ph * 6 + 4) * G + blockIdx.x] = gtimer();
+        if (MKTR(a) && et == 0 && round == 0) MKTR(a)[((size_t)ph * 6 + 4) * G + blockIdx.x] = gtimer();
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem reads before async writes
         epi_sync();  // slots reused by the next round
-        if (a.trace && et == 0 && round == 0) a.trace[((size_t)ph * 6 + 5) * G + blockIdx.x] = gtimer();
+        if (MKTR(a) && et == 0 && round == 0) MKTR(a)[((size_t)ph * 6 + 5) * G + blockIdx.x] = gtimer();
       }
 }
 
@@ -722,14 +727,14 @@ __device__ __noinline__ void epi_amerge(const Args& a, unsigned char* smem, int 
   const int d = a.d, B = a.B;
   const int n_ss = d / MT;
   (void)r; (void)d; (void)B; (void)n_ss; (void)G;
-      if (a.trace && et == 0) a.trace[((size_t)ph * 6 + 2) * G + blockIdx.x] = gtimer();
+      if (MKTR(a) && et == 0) MKTR(a)[((size_t)ph * 6 + 2) * G + blockIdx.x] = gtimer();
       for (int pr = blockIdx.x * 4 + (et >> 5); pr < B * a.H; pr += G * 4) {
         attn_merge(a, srows[pr / a.H], pr / a.H, pr % a.H, lane);
-        if (a.trace && et == 0) a.trace[((size_t)ph * 6 + 3) * G + blockIdx.x] = gtimer();
+        if (MKTR(a) && et == 0) MKTR(a)[((size_t)ph * 6 + 3) * G + blockIdx.x] = gtimer();
       }
-      if (a.trace && et == 0) a.trace[((size_t)ph * 6 + 4) * G + blockIdx.x] = gtimer();
+      if (MKTR(a) && et == 0) MKTR(a)[((size_t)ph * 6 + 4) * G + blockIdx.x] = gtimer();
       epi_sync();
-      if (a.trace && et == 0) a.trace[((size_t)ph * 6 + 5) * G + blockIdx.x] = gtimer();
+      if (MKTR(a) && et == 0) MKTR(a)[((size_t)ph * 6 + 5) * G + blockIdx.x] = gtimer();
 }
 
 __device__ __noinline__ void epi_final(const Args& a, unsigned char* smem, int ph, int l, int kind) {
@@ -813,10 +818,10 @@ __device__ __noinline__ void epi_gemm(const Args& a, unsigned char* smem, int ph
         for (int b = 0; b < XR; b++) xo[b] = (fold_x && b < B) ? __ldcg(a.x + (size_t)b * d + tl * MT + r) : 0.0f;
         mbar_wait(&acc_full[acc], (lu / kAcc) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        if (a.trace && et == 0) {
+        if (MKTR(a) && et == 0) {
           const uint64_t tnow = gtimer();
-          if (first_chunk) a.trace[((size_t)ph * 6 + 3) * G + blockIdx.x] = tnow;
-          a.trace[((size_t)ph * 6 + 4) * G + blockIdx.x] = tnow;
+          if (first_chunk) MKTR(a)[((size_t)ph * 6 + 3) * G + blockIdx.x] = tnow;
+          MKTR(a)[((size_t)ph * 6 + 4) * G + blockIdx.x] = tnow;
         }
         first_chunk = false;
         uint32_t raw[16];
@@ -851,7 +856,7 @@ __device__ __noinline__ void epi_gemm(const Args& a, unsigned char* smem, int ph
           run_tasks(tasks_now);  // tiles completed meanwhile (uniform: snapshot taken before the sync)
         }
       }
-      if (a.trace && et == 0) a.trace[((size_t)ph * 6 + 5) * G + blockIdx.x] = gtimer();
+      if (MKTR(a) && et == 0) MKTR(a)[((size_t)ph * 6 + 5) * G + blockIdx.x] = gtimer();
       // no more chunks: tell the helper, then finalise the remaining tasks of this phase
       if (!fused) return;
       if (et == 0) {
@@ -962,9 +967,9 @@ __device__ __noinline__ void epi_reduce(const Args& a, unsigned char* smem, int 
     }
     rn[et] = rsqrtf(sacc / (float)d + a.eps);
   }
-  if (a.trace && et == 0) a.trace[((size_t)ph * 6 + 2) * G + blockIdx.x] = gtimer();
+  if (MKTR(a) && et == 0) MKTR(a)[((size_t)ph * 6 + 2) * G + blockIdx.x] = gtimer();
   for (int tl = blockIdx.x; tl < p.tiles; tl += G) finalize_tile(a, smem, l, gk, tl);
-  if (a.trace && et == 0) a.trace[((size_t)ph * 6 + 5) * G + blockIdx.x] = gtimer();
+  if (MKTR(a) && et == 0) MKTR(a)[((size_t)ph * 6 + 5) * G + blockIdx.x] = gtimer();
 }
 
 // Helper warp (lane 0): for every chunk the epilogue drained it adds to the
@@ -1032,7 +1037,7 @@ __device__ __noinline__ void role_producer(const Args& a, unsigned char* smem, c
         // -- and only once the merge's outputs are fenced: its stores then do not
         // queue behind the O weight stream (measured: merge 5.8 -> 3.5 us)
         if (kind == K_O) wait_ready(ready_ph + 1, ph - 1);
-        if (a.flags & 1) wait_ready(ready_ph, ph);  // diagnostics: no weight prefetch across barriers
+        if (MK_TRACE && (a.flags & 1)) wait_ready(ready_ph, ph);  // diagnostics: no weight prefetch across barriers
         bool ready = false;
         int npend = 0;
         auto flush = [&]() {
@@ -1079,7 +1084,7 @@ __device__ __noinline__ void role_producer(const Args& a, unsigned char* smem, c
           }
           q = q_next;
         }
-        if (a.trace) a.trace[((size_t)ph * 6 + 2) * G + blockIdx.x] = gtimer();
+        if (MKTR(a)) MKTR(a)[((size_t)ph * 6 + 2) * G + blockIdx.x] = gtimer();
         if (!ready) {
           wait_ready(ready_ph, ph);
           flush();
@@ -1151,7 +1156,7 @@ __device__ __noinline__ void role_epilogue(const Args& a, unsigned char* smem, u
       const int kind = phase_kind(a, ph, &l);
       if (et == 0) {
         spin_until(a.bar, (unsigned long long)ph * G);
-        if (a.trace) a.trace[((size_t)ph * 6) * G + blockIdx.x] = gtimer();
+        if (MKTR(a)) MKTR(a)[((size_t)ph * 6) * G + blockIdx.x] = gtimer();
         __threadfence_block();
         *ready_ph = ph;  // lets the producer issue this phase's activation loads
       }
@@ -1169,12 +1174,12 @@ __device__ __noinline__ void role_epilogue(const Args& a, unsigned char* smem, u
         // side orders them -- the producer issues fence.proxy.async after it
         // observes the barrier -- so no proxy fence here, which would also wait
         // for this SM's in-flight weight prefetch)
-        if (a.flags & 16) fence_proxy_async();
+        if (MK_TRACE && (a.flags & 16)) fence_proxy_async();
         __threadfence();
         epi_sync();
         if (et == 0) {
           ready_ph[1] = ph;  // this phase's outputs are fenced (the producer starts the O weights on it)
-          if (a.trace) a.trace[((size_t)ph * 6 + 1) * G + blockIdx.x] = gtimer();
+          if (MKTR(a)) MKTR(a)[((size_t)ph * 6 + 1) * G + blockIdx.x] = gtimer();
           atomicAdd(a.bar, 1ull);
         }
       }
@@ -1292,8 +1297,41 @@ __global__ void __launch_bounds__(kThreads, 1) decode_mk_kernel(const __grid_con
   }
 }
 
+
+void launch_impl(const MkLaunch& l, cudaStream_t s) {
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(decode_mk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    configured = true;
+  }
+  if (l.B < 1 || l.B > XR) throw std::runtime_error("decode_mk: 1..16 rows");
+  if (l.d % (4 * MT) || l.F % 64 || l.H * HD != l.d) throw std::runtime_error("decode_mk: unsupported shape");
+  Args a{};
+  for (int i = 0; i < 5; i++) a.plan[i] = l.plan[i];
+  a.wmaps = (const CUtensorMap*)l.wmaps;
+  a.norms = l.norms;
+  a.d = l.d; a.F = l.F; a.H = l.H; a.L = l.L; a.V = l.V; a.n_text = l.n_text;
+  a.eps = l.eps; a.scale_log2 = l.scale_log2;
+  a.hdr = l.hdr; a.rows = (const RowMeta*)l.rows; a.items = (const AttnItem*)l.items;
+  a.item_rows = (const ItemRow*)l.item_rows; a.B = l.B;
+  a.embed = l.embed; a.out_tokens = l.out_tokens; a.x = l.x; a.xg = l.xg; a.ss = l.ss; a.q = l.q;
+  a.attn = l.attn; a.kv_pool = l.kv_pool; a.page_elems = l.page_elems; a.rope = l.rope;
+  a.partial = l.partial; a.counters = l.counters; a.apartial = l.apartial; a.acounters = l.acounters;
+  a.part_keys = l.part_keys; a.logits = l.logits; a.bar = l.bar; a.trace = l.trace;
+  a.grab = l.grab;
+  a.flags = l.flags;
+  a.fused = l.fused | (1 << MK_LM);  // lm_head always finalises in-phase (FINAL follows)
+  a.pf_stages = std::max(1, std::min(kStages, l.pf_stages > 0 ? l.pf_stages : kStages));
+  decode_mk_kernel<<<l.grid, kThreads, kSmem, s>>>(*reinterpret_cast<const CUtensorMap*>(l.map_xg.bytes),
+                                                   *reinterpret_cast<const CUtensorMap*>(l.map_attn.bytes),
+                                                   *reinterpret_cast<const CUtensorMap*>(l.map_act.bytes), a);
+}
+
 }  // namespace
 
+#if MK_TRACE
+void launch_decode_mk_traced(const MkLaunch& l, cudaStream_t s) { launch_impl(l, s); }
+#else
 int mk_phases(int L) { return 3 + 10 * L; }  // upper bound (any fused mask)
 int mk_phases(int L, int fused) {
   return 3 + L * (6 + !(fused >> MK_QKV & 1) + !(fused >> MK_O & 1) + !(fused >> MK_GU & 1) + !(fused >> MK_DOWN & 1));
@@ -1323,33 +1361,12 @@ size_t mk_partial_floats(const MkPlan* plans) {
   return (size_t)chunks * MT * XR;
 }
 
+// the lean kernel unless a trace or a diagnostic flag is requested: the
+// instrumented one (decode_mk_trace.cu) is measurably slower (larger hot loops)
 void launch_decode_mk(const MkLaunch& l, cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(decode_mk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-    configured = true;
-  }
-  if (l.B < 1 || l.B > XR) throw std::runtime_error("decode_mk: 1..16 rows");
-  if (l.d % (4 * MT) || l.F % 64 || l.H * HD != l.d) throw std::runtime_error("decode_mk: unsupported shape");
-  Args a{};
-  for (int i = 0; i < 5; i++) a.plan[i] = l.plan[i];
-  a.wmaps = (const CUtensorMap*)l.wmaps;
-  a.norms = l.norms;
-  a.d = l.d; a.F = l.F; a.H = l.H; a.L = l.L; a.V = l.V; a.n_text = l.n_text;
-  a.eps = l.eps; a.scale_log2 = l.scale_log2;
-  a.hdr = l.hdr; a.rows = (const RowMeta*)l.rows; a.items = (const AttnItem*)l.items;
-  a.item_rows = (const ItemRow*)l.item_rows; a.B = l.B;
-  a.embed = l.embed; a.out_tokens = l.out_tokens; a.x = l.x; a.xg = l.xg; a.ss = l.ss; a.q = l.q;
-  a.attn = l.attn; a.kv_pool = l.kv_pool; a.page_elems = l.page_elems; a.rope = l.rope;
-  a.partial = l.partial; a.counters = l.counters; a.apartial = l.apartial; a.acounters = l.acounters;
-  a.part_keys = l.part_keys; a.logits = l.logits; a.bar = l.bar; a.trace = l.trace;
-  a.grab = l.grab;
-  a.flags = l.flags;
-  a.fused = l.fused | (1 << MK_LM);  // lm_head always finalises in-phase (FINAL follows)
-  a.pf_stages = std::max(1, std::min(kStages, l.pf_stages > 0 ? l.pf_stages : kStages));
-  decode_mk_kernel<<<l.grid, kThreads, kSmem, s>>>(*reinterpret_cast<const CUtensorMap*>(l.map_xg.bytes),
-                                                   *reinterpret_cast<const CUtensorMap*>(l.map_attn.bytes),
-                                                   *reinterpret_cast<const CUtensorMap*>(l.map_act.bytes), a);
+  if (l.trace || l.flags) launch_decode_mk_traced(l, s);
+  else launch_impl(l, s);
 }
+#endif
 
 }  // namespace fe

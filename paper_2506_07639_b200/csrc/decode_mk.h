@@ -64,6 +64,7 @@ struct MkLaunch {
 MkPlan mk_plan(int tiles, int kb_total, int grid, int per_cta = 4, int cap = 16);
 size_t mk_partial_floats(const MkPlan* plans);
 void launch_decode_mk(const MkLaunch& l, cudaStream_t s);
+void launch_decode_mk_traced(const MkLaunch& l, cudaStream_t s);  // decode_mk_trace.cu
 int mk_grid();
 int mk_phases(int L);             // upper bound over fused masks (buffer sizing)
 int mk_phases(int L, int fused);  // phases of a tick with that fused mask
