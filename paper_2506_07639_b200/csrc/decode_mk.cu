@@ -77,8 +77,9 @@ constexpr int kMaxPairs = kAttnSlots;
 constexpr int kRing = 64;            // event / task rings (entries in flight per CTA << 64)
 constexpr int kPartStride = HD + 4;  // attention chunk partial record: m, l, pad, pad, o[HD] (16-byte aligned)
 constexpr int kStgStride = HD + 4;   // o staging rows in shared memory  // (page, head) pairs per CTA whose items are cached in smem
-constexpr int kSmem = kStages * (kWBytes + kXBytes) + MT * (XR + 1) * 4 + XR * HD * 4 /* rope */ + 1024 /* align */ +
-                      4096 /* barriers, scratch, rows, items */;
+constexpr int kPtabOff = kStages * (kWBytes + kXBytes) + MT * (XR + 1) * 4 + XR * HD * 4 /* rope */ +
+                         4096 /* barriers, scratch, rows, items */;
+constexpr int kSmem = kPtabOff + 1024 /* phase table */ + 1024 /* align */;
 static_assert(kAttnSlots >= 4, "attention staging needs >= 4 slots");
 
 enum Kind { K_EMBED, K_QKV, K_RQKV, K_ATTN, K_AMERGE, K_O, K_RO, K_GU, K_RGU, K_DOWN, K_RDOWN, K_LM, K_RLM, K_FINAL };
@@ -157,6 +158,12 @@ __device__ __forceinline__ int gemm_kind_of_reduce(int kind) {
 __device__ __forceinline__ int gemm_of(int kind) {
   return kind == K_QKV ? MK_QKV : kind == K_O ? MK_O : kind == K_GU ? MK_GU : kind == K_DOWN ? MK_DOWN
        : kind == K_LM ? MK_LM : -1;
+}
+// phase -> (kind, layer) from the table every CTA builds at launch
+// (phase_kind's fused-mask walk stays out of the roles' code)
+__device__ __forceinline__ int pkind(const unsigned char* ptab, int ph, int* layer) {
+  *layer = ptab[512 + ph];
+  return ptab[ph];
 }
 __device__ __forceinline__ bool fused_reduce_a(const Args& a, int kind) {
   const int gi = gemm_of(kind);
@@ -587,6 +594,7 @@ __device__ __forceinline__ void tile_epilogue(const Args& a, int kind, int l, in
 
 #define MK_SMEM_LAYOUT(smem) \
   unsigned char* sw = smem; \
+  const unsigned char* ptab = smem + kPtabOff; \
   unsigned char* sx = smem + kStages * kWBytes; \
   float* tile = (float*)(sx + kStages * kXBytes); \
   float* srope = tile + MT * (XR + 1); \
@@ -902,7 +910,7 @@ __device__ __noinline__ void finalize_tile(const Args& a, unsigned char* smem, i
 #pragma unroll
   for (int q4 = 0; q4 < XR / 4; q4++) acc4[q4] = make_float4(0.f, 0.f, 0.f, 0.f);
   const size_t q0 = (size_t)tl * p.nc;
-  if (B <= 8 && p.nc <= 16) {  // every chunk's 2 float4 requested together (straight-line registers)
+  if (B <= 8 && p.nc <= 8) {  // every chunk's 2 float4 requested together (straight-line registers)
     const float4* src = reinterpret_cast<const float4*>(a.partial) + q0 * (XR / 4) * MT + r;
     const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
     const int nc = p.nc;
@@ -910,12 +918,10 @@ __device__ __noinline__ void finalize_tile(const Args& a, unsigned char* smem, i
 #define MK_P(u) const float4 pa##u = u < nc ? __ldcg(src + (size_t)(u) * (XR / 4) * MT) : z; \
           const float4 pb##u = (u < nc && two) ? __ldcg(src + (size_t)(u) * (XR / 4) * MT + MT) : z;
     MK_P(0) MK_P(1) MK_P(2) MK_P(3) MK_P(4) MK_P(5) MK_P(6) MK_P(7)
-    MK_P(8) MK_P(9) MK_P(10) MK_P(11) MK_P(12) MK_P(13) MK_P(14) MK_P(15)
 #undef MK_P
 #define MK_S(u) acc4[0].x += pa##u.x; acc4[0].y += pa##u.y; acc4[0].z += pa##u.z; acc4[0].w += pa##u.w; \
           acc4[1].x += pb##u.x; acc4[1].y += pb##u.y; acc4[1].z += pb##u.z; acc4[1].w += pb##u.w;
     MK_S(0) MK_S(1) MK_S(2) MK_S(3) MK_S(4) MK_S(5) MK_S(6) MK_S(7)
-    MK_S(8) MK_S(9) MK_S(10) MK_S(11) MK_S(12) MK_S(13) MK_S(14) MK_S(15)
 #undef MK_S
   } else {
     for (int c0 = 0; c0 < p.nc; c0 += 4) {
@@ -984,7 +990,7 @@ __device__ __noinline__ void role_helper(const Args& a, unsigned char* smem) {
   int ev_pos = 0, task_w = 0;
   for (int ph = 0; ph < P; ph++) {
     int l;
-    const int kind = phase_kind(a, ph, &l);
+    const int kind = pkind(ptab, ph, &l);
     const int gi = gemm_of(kind);
     if (gi < 0 || !fused_reduce_a(a, kind)) continue;
     const MkPlan p = a.plan[gi];
@@ -1026,7 +1032,7 @@ __device__ __noinline__ void role_producer(const Args& a, unsigned char* smem, c
       int it = 0, n = 0;
       for (int ph = 0; ph < P; ph++) {
         int l;
-        const int kind = phase_kind(a, ph, &l);
+        const int kind = pkind(ptab, ph, &l);
         const int gi = gemm_of(kind);
         if (gi < 0) continue;
         const MkPlan p = a.plan[gi];
@@ -1102,7 +1108,7 @@ __device__ __noinline__ void role_mma(const Args& a, unsigned char* smem, uint32
       int it = 0, lu = 0, n = 0;
       for (int ph = 0; ph < P; ph++) {
         int l;
-        const int gi = gemm_of(phase_kind(a, ph, &l));
+        const int gi = gemm_of(pkind(ptab, ph, &l));
         if (gi < 0) continue;
         const MkPlan p = a.plan[gi];
         for (;; lu++) {
@@ -1153,7 +1159,7 @@ __device__ __noinline__ void role_epilogue(const Args& a, unsigned char* smem, u
     uint32_t apar = 0;  // phase parity of the attention staging barriers
     for (int ph = 0; ph < P; ph++) {
       int l;
-      const int kind = phase_kind(a, ph, &l);
+      const int kind = pkind(ptab, ph, &l);
       if (et == 0) {
         spin_until(a.bar, (unsigned long long)ph * G);
         if (MKTR(a)) MKTR(a)[((size_t)ph * 6) * G + blockIdx.x] = gtimer();
@@ -1198,6 +1204,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_mk_kernel(const __grid_con
   for (int i = threadIdx.x; i < (int)(sizeof(Args) / 4); i += blockDim.x)
     reinterpret_cast<uint32_t*>(sargs)[i] = reinterpret_cast<const uint32_t*>(&a)[i];
   unsigned char* sw = smem;                                  // [kStages][128 x 64] weights
+  const unsigned char* ptab = smem + kPtabOff;               // phase -> kind [512], layer [512]
   unsigned char* sx = smem + kStages * kWBytes;              // [kStages][16 x 64] activations
   float* tile = (float*)(sx + kStages * kXBytes);            // [128][17]
   float* srope = tile + MT * (XR + 1);                       // [16][128] RoPE cos | sin of the rows' positions
@@ -1240,11 +1247,18 @@ __global__ void __launch_bounds__(kThreads, 1) decode_mk_kernel(const __grid_con
     }
     for (int i = 0; i < kAttnSlots; i++) mbar_init(&abar[i], 1);
     for (int i = 0; i < kQueue; i++) qseq[i] = -1;
+    if ((const unsigned char*)(task_snap + 1) > ptab) __trap();  // scratch region overflows into the phase table
     *ev_cnt = 0;
     *task_cnt = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     ready_ph[0] = -1;
     ready_ph[1] = -1;
+  }
+  for (int ph = threadIdx.x; ph < P; ph += blockDim.x) {
+    int l;
+    const int k = phase_kind(a, ph, &l);
+    smem[kPtabOff + ph] = (unsigned char)k;
+    smem[kPtabOff + 512 + ph] = (unsigned char)l;
   }
   if (threadIdx.x >= 64 && threadIdx.x < 192) {  // per-tick constants: rows, RoPE rows, attention items
     const int et = threadIdx.x - 64;
@@ -1305,6 +1319,7 @@ void launch_impl(const MkLaunch& l, cudaStream_t s) {
     configured = true;
   }
   if (l.B < 1 || l.B > XR) throw std::runtime_error("decode_mk: 1..16 rows");
+  if (mk_phases(l.L) > 512 || l.L > 255) throw std::runtime_error("decode_mk: too many layers for the phase table");
   if (l.d % (4 * MT) || l.F % 64 || l.H * HD != l.d) throw std::runtime_error("decode_mk: unsupported shape");
   Args a{};
   for (int i = 0; i < 5; i++) a.plan[i] = l.plan[i];
