@@ -1049,6 +1049,7 @@ __device__ __noinline__ void role_producer(const Args& a, unsigned char* smem, c
         auto flush = [&]() {
           __threadfence_block();
           fence_proxy_async();
+#pragma unroll 1
           for (int i = 0; i < npend; i++)
             tma_load_2d(sx + pend_slot[i] * kXBytes, xm, &full[pend_slot[i]], pend_kb[i] * KBK, 0);
           npend = 0;
