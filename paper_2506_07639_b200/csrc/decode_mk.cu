@@ -770,7 +770,7 @@ __device__ __noinline__ void epi_final(const Args& a, unsigned char* smem, int p
       }
 }
 
-__device__ __noinline__ void finalize_tile(const Args& a, unsigned char* smem, int l, int gk, int tl);
+__device__ __noinline__ void finalize_tile(const Args& a, unsigned char* smem, int l, int gk, int tl, bool with_rn);
 
 __device__ __noinline__ void epi_gemm(const Args& a, unsigned char* smem, int ph, int l, int kind, uint32_t tmem, int& lu, int& n,
                                       int& task_r) {
@@ -808,7 +808,7 @@ __device__ __noinline__ void epi_gemm(const Args& a, unsigned char* smem, int ph
             phase_tasks_done = true;
             break;
           }
-          finalize_tile(a, smem, l, kind, tl);
+          finalize_tile(a, smem, l, kind, tl, false);
         }
       };
       bool first_chunk = true;
@@ -895,12 +895,20 @@ __device__ __noinline__ void epi_gemm(const Args& a, unsigned char* smem, int ph
 // landed: sum in chunk order (deterministic), then RoPE + q / paged K/V,
 // residual + norm inputs, SiLU * up or argmax keys (tile_epilogue).  rn holds
 // the phase's row norms.
-__device__ __noinline__ void finalize_tile(const Args& a, unsigned char* smem, int l, int gk, int tl) {
+__device__ __noinline__ void finalize_tile(const Args& a, unsigned char* smem, int l, int gk, int tl, bool with_rn) {
   MK_SMEM_LAYOUT(smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int et = threadIdx.x - 64;
   const int r = 32 * (warp & 3) + lane;
   const int B = a.B;
+  // with_rn: this reduction phase also derives the row norms of the GEMM
+  // input (r = rsqrt(sum x^2 / d + eps)); their loads go out with the partials'
+  const bool do_rn = with_rn && et < B;
+  const int nq = a.d / MT / 4;
+  const float4* sr = reinterpret_cast<const float4*>(a.ss + (size_t)(do_rn ? et : 0) * (a.d / MT));
+  float4 sv[8];
+#pragma unroll
+  for (int u = 0; u < 8; u++) sv[u] = (do_rn && u < nq) ? __ldcg(sr + u) : make_float4(0.f, 0.f, 0.f, 0.f);
   const MkPlan p = a.plan[gemm_of(gk)];
   const bool resid = gk == K_O || gk == K_DOWN;
   const float* gnext = gk == K_O ? a.norms[2 * l + 1]
@@ -942,6 +950,17 @@ __device__ __noinline__ void finalize_tile(const Args& a, unsigned char* smem, i
           }
     }
   }
+  if (do_rn) {
+    float sacc = 0.0f;
+#pragma unroll
+    for (int u = 0; u < 8; u++)
+      if (u < nq) sacc += (sv[u].x + sv[u].y) + (sv[u].z + sv[u].w);
+    for (int u = 8; u < nq; u++) {
+      const float4 v = __ldcg(sr + u);
+      sacc += (v.x + v.y) + (v.z + v.w);
+    }
+    rn[et] = rsqrtf(sacc / (float)a.d + a.eps);
+  }
 #pragma unroll
   for (int q4 = 0; q4 < XR / 4; q4++) {
     tile[r * (XR + 1) + 4 * q4] = acc4[q4].x;
@@ -964,17 +983,10 @@ __device__ __noinline__ void epi_reduce(const Args& a, unsigned char* smem, int 
   const int gk = gemm_kind_of_reduce(kind);
   const MkPlan p = a.plan[gemm_of(gk)];
   if (blockIdx.x >= p.tiles) return;
-  if ((gk == K_QKV || gk == K_GU) && et < B) {  // row norms of the GEMM input
-    const float4* sr = reinterpret_cast<const float4*>(a.ss + (size_t)et * n_ss);
-    float sacc = 0.0f;
-    for (int u = 0; u < n_ss / 4; u++) {
-      const float4 v = __ldcg(sr + u);
-      sacc += (v.x + v.y) + (v.z + v.w);
-    }
-    rn[et] = rsqrtf(sacc / (float)d + a.eps);
-  }
+  (void)d; (void)B; (void)n_ss; (void)et;
   if (MKTR(a) && et == 0) MKTR(a)[((size_t)ph * 6 + 2) * G + blockIdx.x] = gtimer();
-  for (int tl = blockIdx.x; tl < p.tiles; tl += G) finalize_tile(a, smem, l, gk, tl);
+  const bool scaled = gk == K_QKV || gk == K_GU;  // row norms computed with the first tile's partials
+  for (int tl = blockIdx.x; tl < p.tiles; tl += G) finalize_tile(a, smem, l, gk, tl, scaled);
   if (MKTR(a) && et == 0) MKTR(a)[((size_t)ph * 6 + 5) * G + blockIdx.x] = gtimer();
 }
 
