@@ -770,7 +770,8 @@ __device__ __noinline__ void epi_final(const Args& a, unsigned char* smem, int p
       }
 }
 
-__device__ __noinline__ void finalize_tile(const Args& a, unsigned char* smem, int l, int gk, int tl, bool with_rn);
+__device__ __noinline__ void finalize_tile(const Args& a, unsigned char* smem, int l, int gk, int tl, bool with_rn,
+                                          int ph);
 
 __device__ __noinline__ void epi_gemm(const Args& a, unsigned char* smem, int ph, int l, int kind, uint32_t tmem, int& lu, int& n,
                                       int& task_r) {
@@ -808,7 +809,7 @@ __device__ __noinline__ void epi_gemm(const Args& a, unsigned char* smem, int ph
             phase_tasks_done = true;
             break;
           }
-          finalize_tile(a, smem, l, kind, tl, false);
+          finalize_tile(a, smem, l, kind, tl, false, -1);
         }
       };
       bool first_chunk = true;
@@ -895,7 +896,8 @@ __device__ __noinline__ void epi_gemm(const Args& a, unsigned char* smem, int ph
 // landed: sum in chunk order (deterministic), then RoPE + q / paged K/V,
 // residual + norm inputs, SiLU * up or argmax keys (tile_epilogue).  rn holds
 // the phase's row norms.
-__device__ __noinline__ void finalize_tile(const Args& a, unsigned char* smem, int l, int gk, int tl, bool with_rn) {
+__device__ __noinline__ void finalize_tile(const Args& a, unsigned char* smem, int l, int gk, int tl, bool with_rn,
+                                          int ph) {
   MK_SMEM_LAYOUT(smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int et = threadIdx.x - 64;
@@ -968,9 +970,12 @@ __device__ __noinline__ void finalize_tile(const Args& a, unsigned char* smem, i
     tile[r * (XR + 1) + 4 * q4 + 2] = acc4[q4].z;
     tile[r * (XR + 1) + 4 * q4 + 3] = acc4[q4].w;
   }
+  // trace (reduction phases): slot 3 = partials summed, slot 4 = epilogue done
+  if (MKTR(a) && ph >= 0 && et == 0) MKTR(a)[((size_t)ph * 6 + 3) * gridDim.x + blockIdx.x] = gtimer();
   epi_sync();  // tile visible
   tile_epilogue(a, gk, l, tl, tile, rn, red, kred, srows, srope, gw, et, warp, lane);
   epi_sync();  // tile / reduction scratch reused
+  if (MKTR(a) && ph >= 0 && et == 0) MKTR(a)[((size_t)ph * 6 + 4) * gridDim.x + blockIdx.x] = gtimer();
 }
 
 // Separate reduction phase (QKV, O, down): tiles t = cta (mod grid).
@@ -986,7 +991,7 @@ __device__ __noinline__ void epi_reduce(const Args& a, unsigned char* smem, int 
   (void)d; (void)B; (void)n_ss; (void)et;
   if (MKTR(a) && et == 0) MKTR(a)[((size_t)ph * 6 + 2) * G + blockIdx.x] = gtimer();
   const bool scaled = gk == K_QKV || gk == K_GU;  // row norms computed with the first tile's partials
-  for (int tl = blockIdx.x; tl < p.tiles; tl += G) finalize_tile(a, smem, l, gk, tl, scaled);
+  for (int tl = blockIdx.x; tl < p.tiles; tl += G) finalize_tile(a, smem, l, gk, tl, scaled, ph);
   if (MKTR(a) && et == 0) MKTR(a)[((size_t)ph * 6 + 5) * G + blockIdx.x] = gtimer();
 }
 
