@@ -335,11 +335,9 @@ __device__ void attn_pair(const Args& a, const RowMeta* srows, const AttnItem& i
     for (int nt = 0; nt < 8; nt++)  // key 8nt + g (swizzle key & 7 = g), dims 32i + 8t .. +7
       kv[nt] = *reinterpret_cast<const uint4*>(ks + (size_t)(8 * nt + g) * HD * 2 + (((4 * i + t) ^ g) << 4));
 #pragma unroll
-    for (int nt = 0; nt < 8; nt++)
-      if (8 * nt < vmax) mma_bf16(s[nt], qa[2 * i], kv[nt].x, kv[nt].y);
+    for (int nt = 0; nt < 8; nt++) mma_bf16(s[nt], qa[2 * i], kv[nt].x, kv[nt].y);  // keys past vmax masked below
 #pragma unroll
-    for (int nt = 0; nt < 8; nt++)
-      if (8 * nt < vmax) mma_bf16(s[nt], qa[2 * i + 1], kv[nt].z, kv[nt].w);
+    for (int nt = 0; nt < 8; nt++) mma_bf16(s[nt], qa[2 * i + 1], kv[nt].z, kv[nt].w);
   }
   if (dbg) { uint64_t t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t) :: "memory"); dbg[1] = t + (s[0][0] == 1234.5f); }
   // masked softmax (exp2 domain) per row; rows g (c0, c1) and g + 8 (c2, c3); tree reductions
@@ -432,8 +430,7 @@ __device__ void attn_pair(const Args& a, const RowMeta* srows, const AttnItem& i
 #pragma unroll
     for (int nt = 0; nt < 8; nt++) o[nt][0] = o[nt][1] = o[nt][2] = o[nt][3] = 0.0f;
 #pragma unroll
-    for (int kk = 0; kk < 4; kk++) {
-      if (16 * kk >= vmax) break;
+    for (int kk = 0; kk < 4; kk++) {  // P = 0 and V = 0 past vmax
       const int key = 16 * kk + lrow + 8 * (lm & 1);
 #pragma unroll
       for (int q = 0; q < 4; q++) {
@@ -686,7 +683,10 @@ __device__ __noinline__ void epi_attn(const Args& a, unsigned char* smem, int ph
           const __nv_bfloat16* kg = pool_l + (size_t)it.page * a.page_elems + (size_t)(pr % a.H) * FE_PAGE * HD;
           const __nv_bfloat16* vg = kg + (size_t)a.H * FE_PAGE * HD;
           unsigned char* slot = sw + (size_t)j * kAttnSlotBytes;
-          const int vpad = (it.valid_max + 15) & ~15;  // V rows up to the 16-key step: zero-filled
+          // every V row of the page is staged (rows past valid_max zero-filled):
+          // the MMAs then run over all 64 keys without data-dependent branches
+          // around mma.sync (which cost a warp re-convergence each)
+          const int vpad = FE_PAGE;
           for (int x = lane; x < vpad * 16; x += 32) {
             const int key = x >> 4, c = x & 15;
             const uint32_t so = (uint32_t)(key * 256 + ((c ^ (key & 7)) << 4));
