@@ -67,7 +67,8 @@ constexpr int kStages = 11;
 constexpr int kAcc = 4;
 constexpr int kWBytes = MT * KBK * 2;      // 16 KB
 constexpr int kXBytes = XR * KBK * 2;      // 2 KB
-constexpr int kThreads = 224;  // producer, MMA, 4 epilogue warps, helper
+constexpr int kThreads = 256;  // producer, MMA, 4 epilogue warps, helper, attention warp
+constexpr int kAttnWarps = 5;   // the 4 epilogue warps + warp 7 stage and compute attention pairs
 constexpr int HD = 128;                    // head dim (7B shape)
 constexpr uint32_t kIdesc = idesc_bf16(MT, XR);
 // attention phase: the (idle) ring holds K and V of up to 6 (page, head) pairs
@@ -227,6 +228,8 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 
 // ---- epilogue-group (warps 2-5) helpers
 __device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+// the attention phase's group: the 4 epilogue warps and warp 7
+__device__ __forceinline__ void attn_sync() { asm volatile("bar.sync 2, 160;" ::: "memory"); }
 
 // out[b * ostride] = sum over the 128 tile rows of tile[c][b]^2 (b < B), fixed
 // order; the caller has synchronised the epilogue group after writing `tile`
@@ -674,9 +677,9 @@ __device__ __noinline__ void epi_attn(const Args& a, unsigned char* smem, int ph
         // 16-byte cp.async, one commit group per pair (rows 256 B, 16-byte chunks
         // XOR-swizzled by key & 7: the fragment reads are bank-conflict free), and
         // starts computing as soon as its first pair has landed
-        const int w = et >> 5;
+        const int w = warp == 7 ? 4 : warp - 2;  // attention warp 0..4
         int ngroups = 0;
-        for (int j = w; j < kAttnSlots; j += 4) {
+        for (int j = w; j < kAttnSlots; j += kAttnWarps) {
           const int pr = base + j * G;
           if (pr >= n_pairs) break;
           const AttnItem it = item_of(j, pr);
@@ -703,7 +706,7 @@ __device__ __noinline__ void epi_attn(const Args& a, unsigned char* smem, int ph
         }
         uint4 q0[4], q1[4];
         int gi = 0;
-        for (int j = w; j < kAttnSlots; j += 4, gi++) {
+        for (int j = w; j < kAttnSlots; j += kAttnWarps, gi++) {
           const int pr = base + j * G;
           if (pr >= n_pairs) break;
           const AttnItem it = item_of(j, pr);
@@ -721,7 +724,8 @@ __device__ __noinline__ void epi_attn(const Args& a, unsigned char* smem, int ph
         }
         if (MKTR(a) && et == 0 && round == 0) MKTR(a)[((size_t)ph * 6 + 4) * G + blockIdx.x] = gtimer();
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem reads before async writes
-        epi_sync();  // slots reused by the next round
+        if (warp == 7) __threadfence();  // its partials, before the epilogue warps' barrier arrival
+        attn_sync();  // slots reused by the next round
         if (MKTR(a) && et == 0 && round == 0) MKTR(a)[((size_t)ph * 6 + 5) * G + blockIdx.x] = gtimer();
       }
 }
@@ -1210,6 +1214,21 @@ __device__ __noinline__ void role_epilogue(const Args& a, unsigned char* smem, u
     }
 }
 
+// Warp 7: a fifth attention warp (the attention phase is latency-bound, one
+// pair per warp halves the CTAs' critical path); idle in every other phase.
+__device__ __noinline__ void role_attn(const Args& a, unsigned char* smem) {
+  MK_SMEM_LAYOUT(smem);
+  const int P = n_phases(a);
+  for (int ph = 0; ph < P; ph++) {
+    int l;
+    const int kind = pkind(ptab, ph, &l);
+    if (kind != K_ATTN) continue;
+    wait_ready(ready_ph, ph);  // the epilogue warps passed this phase's grid barrier
+    __syncwarp();
+    epi_attn(a, smem, ph, l, kind);
+  }
+}
+
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads, 1) decode_mk_kernel(const __grid_constant__ CUtensorMap map_xg,
                                                                 const __grid_constant__ CUtensorMap map_attn,
@@ -1310,8 +1329,10 @@ __global__ void __launch_bounds__(kThreads, 1) decode_mk_kernel(const __grid_con
     if (lane == 0) role_mma(as, smem, tmem);
   } else if (warp < 6) {
     role_epilogue(as, smem, tmem);
-  } else {
+  } else if (warp == 6) {
     if (lane == 0) role_helper(as, smem);
+  } else {
+    role_attn(as, smem);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
