@@ -470,17 +470,16 @@ __device__ void attn_merge(const Args& a, const RowMeta& m, int row, int h, int 
   const float4* base = reinterpret_cast<const float4*>(mbase + 4) + lane;
   const int nch = m.n_chunks;
   float M = -INFINITY, L = 0.0f, acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
-  // batches of 8 chunks: (m, l) lane-parallel plus this lane's 4 dims of each
-  // chunk, all requested together; running-max rescale across batches
-  for (int c0 = 0; c0 < nch; c0 += 8) {
-    const int nb = min(8, nch - c0);
+  // batches of 16 chunks: (m, l) lane-parallel plus this lane's 4 dims of each
+  // chunk, all requested together (a trunk row has ~10-20 chunks: one or two
+  // L2 round trips); running-max rescale across batches
+  for (int c0 = 0; c0 < nch; c0 += 16) {
+    const int nb = min(16, nch - c0);
     const float mc = lane < nb ? __ldcg(mbase + (c0 + lane) * cs) : -INFINITY;
     const float lc = lane < nb ? __ldcg(mbase + (c0 + lane) * cs + 1) : 0.0f;
-    float4 x0 = make_float4(0.f, 0.f, 0.f, 0.f), x1 = x0, x2 = x0, x3 = x0, x4 = x0, x5 = x0, x6 = x0, x7 = x0;
-#define MK_LD(u, X) \
-    if (u < nb) X = __ldcg(base + (c0 + u) * (cs / 4));
-    MK_LD(0, x0) MK_LD(1, x1) MK_LD(2, x2) MK_LD(3, x3) MK_LD(4, x4) MK_LD(5, x5) MK_LD(6, x6) MK_LD(7, x7)
-#undef MK_LD
+    float4 x[16];
+#pragma unroll
+    for (int u = 0; u < 16; u++) x[u] = u < nb ? __ldcg(base + (c0 + u) * (cs / 4)) : make_float4(0.f, 0.f, 0.f, 0.f);
     float Mb = mc;
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) Mb = fmaxf(Mb, __shfl_xor_sync(0xffffffffu, Mb, off));
@@ -493,14 +492,12 @@ __device__ void attn_merge(const Args& a, const RowMeta& m, int row, int h, int 
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) ls += __shfl_xor_sync(0xffffffffu, ls, off);
     L += ls;
-#define MK_ACC(u, X)                                                                      \
-    {                                                                                      \
-      const float wt = __shfl_sync(0xffffffffu, wl, u);                                    \
-      acc0 = fmaf(wt, X.x, acc0); acc1 = fmaf(wt, X.y, acc1);                              \
-      acc2 = fmaf(wt, X.z, acc2); acc3 = fmaf(wt, X.w, acc3);                              \
+#pragma unroll
+    for (int u = 0; u < 16; u++) {
+      const float wt = __shfl_sync(0xffffffffu, wl, u);
+      acc0 = fmaf(wt, x[u].x, acc0); acc1 = fmaf(wt, x[u].y, acc1);
+      acc2 = fmaf(wt, x[u].z, acc2); acc3 = fmaf(wt, x[u].w, acc3);
     }
-    MK_ACC(0, x0) MK_ACC(1, x1) MK_ACC(2, x2) MK_ACC(3, x3) MK_ACC(4, x4) MK_ACC(5, x5) MK_ACC(6, x6) MK_ACC(7, x7)
-#undef MK_ACC
     M = Mn;
   }
   const float inv = 1.0f / L;
