@@ -1061,14 +1061,14 @@ __device__ __noinline__ void role_producer(const Args& a, unsigned char* smem, c
         // -- and only once the merge's outputs are fenced: its stores then do not
         // queue behind the O weight stream (measured: merge 5.8 -> 3.5 us)
         if (kind == K_O) {
-          // HBM idles through the QKV reduction: pull this CTA's round-0
-          // attention K/V blocks into L2 so the attention phase stages them from L2
+          // HBM idles through the QKV reduction: pull this CTA's attention K/V
+          // blocks into L2 so the attention phase stages them from L2
           const int n_pairs = a.hdr[1] * a.H;
           const __nv_bfloat16* pool_l = a.kv_pool + (size_t)l * 2 * a.H * FE_PAGE * HD;
-          for (int j = 0; j < kAttnSlots; j++) {
+          for (int j = 0;; j++) {  // every round's pairs (round 0's items are in shared memory)
             const int pr = blockIdx.x + j * G;
             if (pr >= n_pairs) break;
-            const AttnItem it = sitems[j];
+            const AttnItem it = j < kAttnSlots ? sitems[j] : a.items[pr / a.H];
             const __nv_bfloat16* kg = pool_l + (size_t)it.page * a.page_elems + (size_t)(pr % a.H) * FE_PAGE * HD;
             const uint32_t bytes = (uint32_t)it.valid_max * HD * 2;
             bulk_prefetch_l2(kg, bytes);
