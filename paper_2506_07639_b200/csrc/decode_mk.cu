@@ -1074,6 +1074,10 @@ __device__ __noinline__ void role_producer(const Args& a, unsigned char* smem, c
             bulk_prefetch_l2(kg, bytes);
             bulk_prefetch_l2(kg + (size_t)a.H * FE_PAGE * HD, bytes);
           }
+          {  // then this CTA's share of the O weights (the ring is the attention's until the merge ends)
+            const int boxes = p.tiles * p.kb_total;
+            for (int b = blockIdx.x; b < boxes; b += G) tma_prefetch_l2(wm, (b % p.kb_total) * KBK, (b / p.kb_total) * MT);
+          }
         }
         if (kind == K_O) wait_ready(ready_ph + 1, ph - 1);
         if (MK_TRACE && (a.flags & 1)) wait_ready(ready_ph, ph);  // diagnostics: no weight prefetch across barriers
