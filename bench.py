@@ -6,29 +6,33 @@
 Workload (BASELINE.json config 2, 1 GPU): Llama-2-7B-shaped decoder + 256
 vision tokens, random-init bf16 weights, synthetic LIBERO-shaped
 observations (`observation_for(seed, t)`), default ECoT schema/profile; one
-episode per GPU driven by the Fast-ECoT runner (`parallel_sync`: trunk
-prefill + 7 forked branches decoded as one batch).  A *step* is one control
-timestep.  `value` = policy steps/s over all ranks (device time, CUDA events
-on the engine stream, max over ranks); `e2e` = the same through the public
-runner API with host wall clock (all H2D/D2H inside).  Sequential ECoT and
-async action latency are reported alongside.  Every decode iteration streams
-13.2 GB of weights (> L2), so no L2 flush is needed between steps.
+episode driven by the reference's own Fast-ECoT runner (`ecot_sched`
+`parallel_sync`: trunk prefill + N+1 forked branches decoded as one batch).
+A *step* is one control timestep.  `value` = policy steps/s (device time,
+CUDA events on the engine stream, max over ranks); `e2e` = the same through
+the public runner API with host wall clock (all H2D/D2H inside).  Sequential
+ECoT and async action latency (config 3) are reported alongside.  Every
+decode iteration streams 13.2 GB of weights (> L2), so no L2 flush is needed
+between steps.
 
-Multi-GPU: one process per GPU (torchrun); each rank runs an independent
-episode (seed = rank) on its own engine; NCCL is used only to gather the
-per-rank results at the end ("scaling": "weak").
+Multi-GPU (config 4): `--gpus N` launches N processes (torchrun; one per GPU)
+unless already running under one; the episodes (`--episodes`, default 64
+when N > 1) are sharded round-robin over the ranks, every rank steps its
+shard as one batch per timestep on its own engine, and NCCL gathers the
+per-episode token sequences at the end -- no collective on the hot path.
 """
 
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
 import tempfile
-import threading
 import time
 from pathlib import Path
 
@@ -50,15 +54,34 @@ def parse():
     ap.add_argument("--mode", default="parallel_sync")
     ap.add_argument("--workload", choices=("config2", "stress"), default="config2",
                     help="config2: default ECoT schema; stress: config 5 (8-way fan-out, ~2k-token cached prefix)")
-    ap.add_argument("--episodes", type=int, default=1,
-                    help="total episodes (config 4: >1 shards them over ranks, batched per timestep)")
-    ap.add_argument("--seq-steps", type=int, default=2)
-    ap.add_argument("--async-steps", type=int, default=10)
+    ap.add_argument("--episodes", type=int, default=None,
+                    help="total episodes (config 4; default 1 on one GPU, 64 on several): sharded over "
+                         "ranks, each rank's shard batched per timestep")
+    ap.add_argument("--seq-steps", type=int, default=4)
+    ap.add_argument("--async-steps", type=int, default=50)
     ap.add_argument("--no-extras", action="store_true", help="skip sequential/async side measurements")
     ap.add_argument("--profile-steps", type=int, default=3, help="eager timesteps timed per kernel after the run")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-config", default="7b_2layer",
+                    help="oracle model of the reference arm (7B width; depth-scaled to 32 layers in the line)")
+    ap.add_argument("--ref-budget-s", type=float, default=150.0,
+                    help="reference arm: stop after this much CPU wall time (at least one timed step)")
     ap.add_argument("--out", default=None, help="also write the JSON line here")
-    return ap.parse_args()
+    args = ap.parse_args()
+    if args.episodes is None:
+        args.episodes = 64 if args.gpus > 1 else 1
+    return args
+
+
+def self_launch(args) -> int:
+    """`--gpus N` outside torchrun: re-run this script under torchrun with N
+    local ranks (rendezvous on 127.0.0.1)."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
 
 
 # --------------------------------------------------------------------------
@@ -83,9 +106,9 @@ def all_max(x: float, world: int) -> float:
     return float(t.item())
 
 
-def gather_objects(obj, world):
-    from paper_2506_07639_b200.distributed import gather_to_all
-    return gather_to_all(obj, world)
+def percentile(xs, q: float) -> float:
+    import numpy as np
+    return float(np.percentile(np.asarray(xs, dtype=np.float64), q))
 
 
 class ClockSampler:
@@ -139,124 +162,112 @@ def measured_peaks() -> dict:
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "source": "fallback"}
 
 
-def ncu_traffic(name: str = "ncu_decode_gemv.json") -> float | None:
-    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
+def profile_json(name: str) -> dict | None:
     p = REPO / "profiles" / name
     if p.exists():
         try:
-            return json.loads(p.read_text()).get("dram_bytes_per_launch")
+            return json.loads(p.read_text())
         except (ValueError, OSError):
             return None
     return None
 
 
 # --------------------------------------------------------------------------
-def workload_shapes(config: str, seed: int, warmup: int, steps: int, mode: str = "parallel_sync"):
-    """Per timed step: (trunk tokens to prefill, decode tokens) of the ECoT
-    workload.  Lengths come from the synthetic length oracle only, so the
-    shape is known without running the model (it equals the engine's)."""
-    from paper_2506_07639_b200 import schedulers as S
-    from paper_2506_07639_b200.backends import SyntheticBackend, default_profile
+# CPU side: the reference runners over the CPU oracle model
+# --------------------------------------------------------------------------
+def oracle_steps(args, budget_s: float, min_timed: int = 1) -> dict:
+    """The reference's CPU path for this workload: the reference's own runner
+    (`ecot_sched.schedulers.make_runner`, unmodified, `wall_clock=True` so each
+    step's latency is the reference's own timer) over the CPU oracle model
+    (fp32, canonical arithmetic, every host thread).  Runs the warm-up
+    timestep(s) then timed timesteps until `budget_s` of wall time is spent
+    (at least `min_timed`).  The 7B width at reduced depth (`--ref-config`)
+    keeps a step within seconds; the line states the depth scale."""
+    import ecot_sched
+    from ecot_sched import schedulers as RS
+
+    from oracle.backend import SHAPES, OracleBackend
     from paper_2506_07639_b200.model import get_config
-    from paper_2506_07639_b200.trace import default_schema
-    cfg = get_config(config)
-    ctx_len = 1 + cfg.n_vision + 16
-    schema = default_schema()
-    be = SyntheticBackend(default_profile(seed))
-    runner = S.make_runner(S.SchedulerConfig(mode=mode, slots=8), be, schema)
-    shapes, prev = [], None
-    for t in range(warmup + steps):
-        r = runner.step(be.encode(INSTRUCTION, S.observation_for(seed, t)), t)
-        if t >= warmup:
-            lens = [len(toks) for _, toks in r.trace.steps]
-            if mode == "parallel_sync" and prev is not None:
-                trunk = ctx_len + sum(len(toks) for _, toks in prev.steps[:-1])
-            else:  # sequential chain: context + every step but the last is prefilled
-                trunk = ctx_len + sum(lens[:-1])
-            shapes.append((trunk, sum(lens)))
-        prev = r.trace
-    return shapes
+    from paper_2506_07639_b200.workloads import WORKLOADS
+    make_schema, make_profile = WORKLOADS[args.workload]
+    schema = make_schema()
+    threads = os.cpu_count() or 1
+    be = OracleBackend(args.ref_config, seed=0, profile=make_profile(0), threads=threads)
+    runner = RS.make_runner(RS.SchedulerConfig(mode=args.mode, slots=8, wall_clock=True), be, schema)
+    warm = 1 if args.mode != "sequential" else 0     # t=0: the reference warm-up (sequential pass)
+    t_start = time.perf_counter()
+    lat, t = [], 0
+    while True:
+        r = runner.step(be.encode(INSTRUCTION, RS.observation_for(0, t)), t)
+        if t >= warm:
+            lat.append(r.latency_ms)
+        t += 1
+        spent = time.perf_counter() - t_start
+        if len(lat) >= args.steps or (len(lat) >= min_timed and spent > budget_s):
+            break
+    full, used = get_config(args.config), get_config(args.ref_config)
+    scale = full.linear_params / used.linear_params
+    return {"ms": lat, "warmup_run": warm, "wall_s": time.perf_counter() - t_start, "threads": threads,
+            "model": args.ref_config, "depth_scale": scale, "layers": SHAPES[args.ref_config][1],
+            "runner": f"ecot_sched {ecot_sched.__file__}"}
 
 
-def cpu_sample(config: str, threads: int) -> dict:
-    """Time the CPU oracle (fp32, canonical arithmetic, all host threads) on a
-    bounded sample of the same model shape: one 48-token prefill and 3 decode
-    tokens.  Falls back to the 2-layer 7B shape scaled by depth when host RAM
-    cannot hold the 26 GB fp32 7B model."""
-    from oracle.backend import OracleModel, SHAPES
-    mem_gb = 0.0
-    try:
-        for line in open("/proc/meminfo"):
-            if line.startswith("MemAvailable"):
-                mem_gb = int(line.split()[1]) / 1e6
-    except OSError:
-        pass
-    use, scale = config, 1.0
-    if config == "7b" and mem_gb < 80:
-        use, scale = "7b_2layer", SHAPES["7b"][1] / SHAPES["7b_2layer"][1]
-    t0 = time.perf_counter()
-    om = OracleModel(use, seed=0, threads=threads)
-    init_s = time.perf_counter() - t0
-    ids = [32000] + [32001] * 16 + list(range(100, 131))       # 48 ids
-    t0 = time.perf_counter()
-    om.generate(ids, 1, 1)                                      # prefill 48 + 1 head
-    t_pre = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    om.generate(ids, 1, 4)                                      # cached prefix: 1 row + 3 decode tokens
-    t_dec = (time.perf_counter() - t0) / 4.0
-    per_prefill = (t_pre - t_dec) / 47.0
-    return {"model": use, "depth_scale": scale, "prefill_s_per_token": per_prefill * scale,
-            "decode_s_per_token": t_dec * scale, "init_s": init_s, "threads": threads, "mem_gb": mem_gb}
+def synthetic_path(args) -> dict:
+    """The reference CPU path as shipped: reference runners over the
+    reference `SyntheticBackend`, wall clock (`schedulers.py:317-323`)."""
+    import ecot_sched
+    from ecot_sched import schedulers as RS
+
+    from paper_2506_07639_b200.workloads import WORKLOADS
+    make_schema, make_profile = WORKLOADS[args.workload]
+    schema = make_schema()
+    be = ecot_sched.SyntheticBackend(make_profile(0))
+    res, _ = ecot_sched.run_episode(RS.SchedulerConfig(mode=args.mode, slots=8, wall_clock=True),
+                                    args.warmup + args.steps, be, schema, seed=0)
+    ms = [r.latency_ms for r in res[args.warmup:]]
+    return {"p50_ms": statistics.median(ms), "mean_ms": statistics.mean(ms), "steps": len(ms)}
 
 
-def extrapolate_ms(sample: dict, shape) -> float:
-    trunk, dec = shape
-    return 1000.0 * (trunk * sample["prefill_s_per_token"] + dec * sample["decode_s_per_token"])
+def run_reference(args, rank, world):
+    """Reference arm: the reference runners over the CPU oracle model, timed on
+    the host cores (rank 0 only), plus the shipped SyntheticBackend path."""
+    if rank != 0:
+        return None
+    o = oracle_steps(args, args.ref_budget_s)
+    syn = synthetic_path(args)
+    ms = statistics.mean(o["ms"])
+    value = 1000.0 / ms
+    sample = (f"reference ParallelSyncRunner (ecot_sched, unmodified, wall_clock) over the CPU oracle "
+              f"({o['model']}: 7B width, {o['layers']} layers, fp32, {o['threads']} threads); "
+              f"{len(o['ms'])} timed timestep(s) after {o['warmup_run']} warm-up, {o['wall_s']:.0f} s total")
+    return {
+        "metric": METRIC, "impl": "reference", "value": value, "unit": "steps/s", "n_gpus": world,
+        "steps": len(o["ms"]), "warmup": o["warmup_run"], "steps_requested": args.steps,
+        "ms_per_step": ms, "p50_ms": statistics.median(o["ms"]), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"config 2 shape at reduced depth ({o['model']}), single episode, "
+                               f"Fast ECoT {args.mode}", "model": o["model"], "mode": args.mode},
+        "cpu_baseline": {"value": value, "unit": "steps/s", "cores": o["threads"], "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "depth_scaled_7b": {"ms_per_step": ms * o["depth_scale"], "value": value / o["depth_scale"],
+                            "scale": o["depth_scale"],
+                            "how": "x (7b linear params / sample linear params); CPU time ~ weight traffic"},
+        "reference_synthetic_backend": syn,
+    }
 
 
 # --------------------------------------------------------------------------
-def run_reference(args, rank, world):
-    """Reference arm: the reference's CPU path for this workload -- the
-    reference runners (baseline/_ref when installed, else the mirror) over
-    the CPU oracle model -- timed on the host cores in a bounded sample."""
-    if rank != 0:
-        return None
-    threads = os.cpu_count() or 1
-    ref_runner = "mirror"
-    try:
-        sys.path.insert(0, str(REPO / "baseline" / "_ref"))
-        os.environ.setdefault("NUMBA_CACHE_DIR", tempfile.mkdtemp(prefix="numba_"))
-        import ecot_sched  # noqa: F401
-        ref_runner = "reference (baseline/_ref)"
-    except Exception:
-        pass
-    sample = cpu_sample(args.config, threads)
-    shapes = workload_shapes(args.config, 0, args.warmup, args.steps, args.mode)
-    ms = [extrapolate_ms(sample, s) for s in shapes]
-    value = 1000.0 / statistics.mean(ms)
-    line = {
-        "metric": METRIC, "impl": "reference", "value": value, "unit": "steps/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": statistics.mean(ms),
-        "p50_ms": statistics.median(ms), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "config 2: 7B-shaped ECoT VLA, single episode, Fast ECoT parallel_sync",
-                   "model": args.config, "mode": args.mode},
-        "cpu_baseline": {"value": value, "unit": "steps/s", "cores": threads, "kind": "port",
-                         "sample": (f"CPU oracle ({sample['model']}, fp32, {threads} threads): 47-token prefill "
-                                    f"+ 4 decode tokens timed, extrapolated to each step's trunk and branch "
-                                    f"lengths (depth x{sample['depth_scale']:.0f}); runners: {ref_runner}")},
-        "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "detail": sample,
-    }
-    return line
-
-
+# GPU side
+# --------------------------------------------------------------------------
 def time_mode(backend, runner, seed, t0, n, stream):
     """Run n timesteps from t0; returns per-step (device ms, host ms, results).
-    `runner` is a reference-style runner (one episode, `seed`) or a
-    `BatchedEpisodes` driver (all its episodes per step)."""
+    `runner` is a reference runner (one episode, `seed`) or a `BatchedEpisodes`
+    driver (all its episodes per step)."""
     import torch
-    from paper_2506_07639_b200.schedulers import BatchedEpisodes, observation_for
+    from ecot_sched.schedulers import observation_for
+
+    from paper_2506_07639_b200 import BatchedEpisodes
     dev, host, results = [], [], []
     for t in range(t0, t0 + n):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -273,31 +284,73 @@ def time_mode(backend, runner, seed, t0, n, stream):
     return dev, host, results
 
 
+def episode_token_shards(results, seeds) -> dict:
+    """{episode seed: per-timestep [(step, tokens)]} of this rank's results."""
+    from paper_2506_07639_b200.distributed import episode_tokens
+    if results and isinstance(results[0], list):      # BatchedEpisodes: [timestep][episode]
+        return {s: episode_tokens([step[i] for step in results]) for i, s in enumerate(seeds)}
+    return {seeds[0]: episode_tokens(results)}
+
+
+def run_extras(args, backend, schema, make_profile, seed, stream, local):
+    """Sequential ECoT and config 3 (async action latency) on the same engine."""
+    from ecot_sched import schedulers as RS
+
+    from paper_2506_07639_b200 import summarize
+    from paper_2506_07639_b200.engine_backend import EngineBackend
+    seq_runner = RS.make_runner(RS.SchedulerConfig(mode="sequential", slots=8, wall_clock=True), backend, schema)
+    sdev, _, _ = time_mode(backend, seq_runner, 1000 + seed, 0, 1 + args.seq_steps, stream)
+    asy = RS.make_runner(RS.SchedulerConfig(mode="parallel_async", slots=8, wall_clock=True), backend, schema)
+    adev, _, ares = time_mode(backend, asy, 2000 + seed, 0, 1 + args.async_steps, stream)
+    asy.engine.drain()   # land the lockstep runner's in-flight reasoning before the engine is reused
+    asy.close()
+    # config 3 proper: two CUDA streams, reasoning refresh free-running on the
+    # low-priority lane between and during control steps
+    backend2 = EngineBackend(args.config, dtype=args.dtype, seed=0, device=local, profile=make_profile(0),
+                             engine=backend.engine, async_streams=2)
+    asy2 = RS.make_runner(RS.SchedulerConfig(mode="parallel_async", slots=8, wall_clock=True), backend2, schema)
+    _, a2host, a2res = time_mode(backend2, asy2, 3000 + seed, 0, 1 + args.async_steps, stream)
+    asy2.engine.drain()
+    asy2.close()
+    s_lock = summarize("parallel_async", ares[1:], schema)
+    s_two = summarize("parallel_async", a2res[1:], schema)
+    return {
+        "sequential_ms": {"p50": statistics.median(sdev[1:]), "p99": percentile(sdev[1:], 99),
+                          "steps": len(sdev) - 1},
+        "parallel_async_action_ms": {"p50": statistics.median(adev[1:]), "p99": percentile(adev[1:], 99),
+                                     "steps": len(adev) - 1, "scheduler": "lockstep (reference landing order)",
+                                     "staleness_histogram": s_lock["staleness_histogram"]},
+        "parallel_async_2stream_action_ms": {"p50": statistics.median(a2host[1:]), "p99": percentile(a2host[1:], 99),
+                                             "steps": len(a2host) - 1,
+                                             "scheduler": "two CUDA streams, host wall clock per action",
+                                             "staleness_histogram": s_two["staleness_histogram"]},
+    }
+
+
 def run_engine(args, rank, world, local):
     import torch
-    from paper_2506_07639_b200 import schedulers as S
-    from paper_2506_07639_b200.engine_backend import EngineBackend
-    from paper_2506_07639_b200.trace import default_schema
+    from ecot_sched import schedulers as RS
 
+    from paper_2506_07639_b200 import BatchedEpisodes
+    from paper_2506_07639_b200.distributed import gather_to_all, shard_episodes
+    from paper_2506_07639_b200.engine_backend import EngineBackend
     from paper_2506_07639_b200.workloads import WORKLOADS
     torch.cuda.set_device(local)
     make_schema, make_profile = WORKLOADS[args.workload]
     schema = make_schema()
-    seed = rank
+    seeds = shard_episodes(list(range(args.episodes)), world, rank) if args.episodes > 1 else [rank]
     backend = EngineBackend(args.config, dtype=args.dtype, seed=0, device=local, profile=make_profile(0))
     eng = backend.engine
     stream = torch.cuda.ExternalStream(eng.stream_handle(), device=local)
-    cfg_run = S.SchedulerConfig(mode=args.mode, slots=8, wall_clock=True)
+    cfg_run = RS.SchedulerConfig(mode=args.mode, slots=8, wall_clock=True)
     if args.episodes > 1:  # config 4: this rank's shard of the episodes, one batch per timestep
-        from paper_2506_07639_b200.distributed import shard_episodes
-        local_seeds = shard_episodes(list(range(args.episodes)), world, rank)
-        runner = S.BatchedEpisodes(cfg_run, backend, schema, local_seeds)
+        runner = BatchedEpisodes(cfg_run, backend, schema, seeds)
     else:
-        runner = S.make_runner(cfg_run, backend, schema)
+        runner = RS.make_runner(cfg_run, backend, schema)
 
     # warm-up (t=0 is the reference's sequential warm-up pass); decode ticks
     # of each row count are captured into CUDA graphs during warm-up
-    time_mode(backend, runner, seed, 0, args.warmup, stream)
+    time_mode(backend, runner, seeds[0], 0, args.warmup, stream)
     eng.synchronize()
     torch.cuda.synchronize()
     barrier(world)
@@ -308,7 +361,7 @@ def run_engine(args, rank, world, local):
     torch.cuda.synchronize()
     start.record(stream)
     h0 = time.perf_counter()
-    dev, host, results = time_mode(backend, runner, seed, args.warmup, args.steps, stream)
+    dev, host, results = time_mode(backend, runner, seeds[0], args.warmup, args.steps, stream)
     host_total = time.perf_counter() - h0
     end.record(stream)
     eng.synchronize()
@@ -320,10 +373,13 @@ def run_engine(args, rank, world, local):
     total_max = all_max(total_s, world)
     host_max = all_max(host_total, world)
 
+    # results: every rank's episode token sequences gathered over NCCL
+    # (the only collective; after the timed region)
+    shards = gather_to_all(episode_token_shards(results, seeds), world)
     # per-kernel CUDA-event timing (eager launches, events around every decode
-    # GEMM / attention launch on the engine stream) over the next timesteps
+    # launch on the engine stream) over the next timesteps
     eng.profile(True)
-    pdev, _, _ = time_mode(backend, runner, seed, args.warmup + args.steps, args.profile_steps, stream)
+    pdev, _, _ = time_mode(backend, runner, seeds[0], args.warmup + args.steps, args.profile_steps, stream)
     prof = eng.profile_read()
     eng.profile(False)
     prof["steps"] = args.profile_steps
@@ -331,39 +387,31 @@ def run_engine(args, rank, world, local):
 
     extras = {}
     if world == 1 and not args.no_extras and args.episodes <= 1:
-        seq_runner = S.make_runner(S.SchedulerConfig(mode="sequential", slots=8, wall_clock=True), backend, schema)
-        sdev, shost, _ = time_mode(backend, seq_runner, 1000 + seed, 0, 1 + args.seq_steps, stream)
-        asy = S.make_runner(S.SchedulerConfig(mode="parallel_async", slots=8, wall_clock=True), backend, schema)
-        adev, ahost, ares = time_mode(backend, asy, 2000 + seed, 0, 1 + args.async_steps, stream)
-        asy.engine.drain()  # land the lockstep runner's in-flight reasoning before the engine is reused
-        # config 3 proper: two CUDA streams, reasoning refresh free-running on the
-        # low-priority lane between and during control steps
-        backend2 = EngineBackend(args.config, dtype=args.dtype, seed=0, device=local, profile=make_profile(0),
-                                 engine=backend.engine, async_streams=2)
-        asy2 = S.make_runner(S.SchedulerConfig(mode="parallel_async", slots=8, wall_clock=True), backend2, schema)
-        a2dev, a2host, a2res = time_mode(backend2, asy2, 3000 + seed, 0, 1 + args.async_steps, stream)
-        asy2.engine.drain()
-        asy2.engine.close()
-        stal = [max(v for k, v in r.staleness.items() if k != schema.action_step.name) for r in a2res[1:]]
-        extras = {
-            "sequential_ms": {"p50": statistics.median(sdev[1:]), "steps": len(sdev) - 1,
-                              "all": [round(x, 2) for x in sdev[1:]]},
-            "parallel_async_action_ms": {"p50": statistics.median(adev[1:]),
-                                         "p99": sorted(adev[1:])[max(0, int(0.99 * (len(adev) - 1)) - 1)],
-                                         "steps": len(adev) - 1, "scheduler": "lockstep (reference landing order)"},
-            "parallel_async_2stream_action_ms": {"p50": statistics.median(a2host[1:]),
-                                                 "p99": sorted(a2host[1:])[max(0, int(0.99 * (len(a2host) - 1)) - 1)],
-                                                 "steps": len(a2host) - 1,
-                                                 "max_reasoning_staleness_p50": statistics.median(stal),
-                                                 "scheduler": "two CUDA streams, host wall clock per action"},
-        }
-    gathered = gather_objects({"rank": rank, "dev_ms": dev, "host_ms": host}, world)
-    return backend, dict(dev=dev, host=host, results=results, total_max=total_max, host_max=host_max,
+        extras = run_extras(args, backend, schema, make_profile, seeds[0], stream, local)
+    gathered = gather_to_all({"rank": rank, "dev_ms": dev, "host_ms": host}, world)
+    return backend, dict(dev=dev, host=host, total_max=total_max, host_max=host_max, shards=shards,
                          prof=prof, clocks=clk, stats0=stats0, stats1=stats1, extras=extras, gathered=gathered)
+
+
+def token_summary(shards) -> dict:
+    from paper_2506_07639_b200.distributed import merge_shards
+    eps = sorted(e for s in shards for e in s)
+    merged = merge_shards(shards, eps)
+    h = hashlib.blake2b(digest_size=8)
+    n = 0
+    for ep in merged:
+        for step in ep:
+            for name, toks in step:
+                h.update(name.encode())
+                h.update(repr(toks).encode())
+                n += len(toks)
+    return {"episodes": len(eps), "tokens": n, "digest": h.hexdigest(), "via": "all_gather_object (NCCL)"}
 
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     if args.impl == "reference":
         rank, world, local = dist_setup("gloo")
         line = run_reference(args, rank, world)
@@ -373,7 +421,6 @@ def main():
                 Path(args.out).write_text(json.dumps(line) + "\n")
         return
 
-    import torch
     rank, world, local = dist_setup("nccl")
     backend, r = run_engine(args, rank, world, local)
     K = args.steps
@@ -388,29 +435,30 @@ def main():
     achieved = (g["bytes"] / 1e9) / (g["ms"] / 1e3) if g["ms"] > 0 else None
     steps_prof = prof.pop("steps")
     step_ms_prof = prof.pop("step_ms")
-    dev_sorted = sorted(d for gr in r["gathered"] for d in gr["dev_ms"])
-    p50 = statistics.median(dev_sorted)
-    p99 = dev_sorted[min(len(dev_sorted) - 1, int(round(0.99 * (len(dev_sorted) - 1))))]
+    dev_all = [d for gr in r["gathered"] for d in gr["dev_ms"]]
     s0, s1 = r["stats0"], r["stats1"]
-    eps = max(1, args.episodes) if args.episodes > 1 else world  # episodes across all ranks
+    eps = args.episodes if args.episodes > 1 else world  # episodes across all ranks
     value = eps * K / r["total_max"]
     e2e = eps * K / r["host_max"]
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.episodes <= 1:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            threads = os.cpu_count() or 1
-            sample = cpu_sample(args.config, threads)
-            shapes = workload_shapes(args.config, 0, args.warmup, K, args.mode)
-            ms = statistics.mean(extrapolate_ms(sample, s) for s in shapes)
-            cpu = {"value": 1000.0 / ms, "unit": "steps/s", "cores": threads, "kind": "port",
-                   "sample": (f"CPU oracle ({sample['model']}, fp32, {threads} threads): 47-token prefill + 4 "
-                              f"decode tokens timed, extrapolated to the timed steps' trunk/branch lengths "
-                              f"(depth x{sample['depth_scale']:.0f}); {ms:.0f} ms/step")}
+            o = oracle_steps(args, budget_s=20.0)
+            ms = statistics.mean(o["ms"])
+            cpu = {"value": 1000.0 / ms, "unit": "steps/s", "cores": o["threads"], "kind": "port",
+                   "sample": (f"reference ParallelSyncRunner (ecot_sched, wall clock) over the CPU oracle "
+                              f"({o['model']}: 7B width, {o['layers']} layers, fp32); {len(o['ms'])} timed "
+                              f"timestep(s) after {o['warmup_run']} warm-up; {ms:.0f} ms/step at this depth, "
+                              f"~{ms * o['depth_scale'] / 1000:.0f} s/step depth-scaled to 32 layers "
+                              f"(x{o['depth_scale']:.1f})"),
+                   "depth_scaled_7b_value": 1000.0 / (ms * o["depth_scale"])}
         except Exception as exc:  # the baseline must never sink the GPU line
             cpu = {"value": None, "unit": "steps/s", "cores": os.cpu_count(), "kind": "port",
                    "sample": f"failed: {exc!r}"}
     if rank != 0:
         return
+    tick_ncu = profile_json("ncu_decode_tick.json") or {}
+    parity = profile_json("bf16_parity.json")
     line = {
         "metric": METRIC,
         "value": value,
@@ -419,8 +467,8 @@ def main():
         "steps": K,
         "warmup": args.warmup,
         "ms_per_step": 1000.0 * r["total_max"] / K,
-        "p50_ms": p50,
-        "p99_ms": p99,
+        "p50_ms": statistics.median(dev_all),
+        "p99_ms": percentile(dev_all, 99),
         "higher_is_better": True,
         "scaling": "weak" if args.episodes <= 1 else "strong",
         "vs_baseline": None,
@@ -433,19 +481,19 @@ def main():
                                 f"over {world} GPU(s), 7B-shaped, Fast ECoT parallel_sync, one decode batch "
                                 f"per timestep per GPU"),
                    "model": args.config, "mode": args.mode, "schema": args.workload,
-                   "episodes": args.episodes if args.episodes > 1 else world,
-                   "episodes_per_gpu": (args.episodes / world) if args.episodes > 1 else 1, "slots": 8,
+                   "episodes": eps, "episodes_per_gpu": eps / world, "slots": 8,
                    "l2": "no flush: every decode iteration streams 13.2 GB of weights (> 126 MB L2)"},
-        "e2e": {"value": e2e, "unit": "steps/s",
+        "e2e": {"value": e2e, "unit": "steps/s" if args.episodes <= 1 else "episode-steps/s",
                 "h2d_bytes_per_step": (s1["h2d_bytes"] - s0["h2d_bytes"]) / K,
                 "d2h_bytes_per_step": (s1["d2h_bytes"] - s0["d2h_bytes"]) / K},
         "gpu_launches": s1["launches"] - s0["launches"],
         "roofline": {"bound": "hbm",
                      "kernel": ("persistent decode-tick kernel (decode_mk_kernel: every layer's QKV/O/gate-up/down "
                                 "+ lm_head weights and the cascade-attention KV pages, one launch per tick)")
-                               if use_tick else "decode GEMV (QKV/O/gate-up/down/lm_head, bf16 weights)",
+                               if use_tick else "decode GEMMs of the kernel chain (skinny tcgen05, bf16 weights)",
                      "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                     "frac": (achieved / peaks["hbm_gbs"]) if achieved else None, "traffic": ncu_traffic("ncu_decode_tick.json" if use_tick else "ncu_decode_gemv.json"),
+                     "frac": (achieved / peaks["hbm_gbs"]) if achieved else None,
+                     "traffic": tick_ncu.get("dram_bytes_per_launch") if use_tick else None,
                      "peak_source": peaks["source"],
                      "launches": g["launches"], "ms_total": g["ms"],
                      "share_of_step": g["ms"] / step_ms_prof,
@@ -457,6 +505,8 @@ def main():
         "clocks": r["clocks"],
         "breakdown_ms_per_step_eager": {k: v["ms"] / steps_prof for k, v in prof.items()},
         "decode_ticks_per_step": (s1["ticks"] - s0["ticks"]) / K,
+        "results_gathered": token_summary(r["shards"]),
+        "bf16_token_match": parity.get("summary") if parity else None,
         **r["extras"],
     }
     print(json.dumps(line), flush=True)

@@ -155,21 +155,24 @@ class OracleBackend:
 
     def __init__(self, config: str = "tiny", seed: int = 0, profile=None, threads: int = 0,
                  model: OracleModel | None = None):
-        from paper_2506_07639_b200.backends import default_profile  # profile is data
+        from paper_2506_07639_b200.refapi import backends as rb  # the reference API (profile is data)
+        default_profile = rb.default_profile
         self.model = model or OracleModel(config, seed, threads)
         self.config = config
         self.profile = profile or default_profile(seed)
         self.requests = 0
 
     def encode(self, instruction: str, observation: bytes):
-        from paper_2506_07639_b200.trace import Context
+        from paper_2506_07639_b200.refapi import trace as rt
+        Context = rt.Context
         if not instruction and not observation:
             return Context(instruction, observation, ())
         rng = np.random.default_rng(_digest("encode", instruction, observation))
         return Context(instruction, observation, tuple(int(t) for t in rng.integers(0, 2**32, size=16)))
 
     def begin_step(self, context, prefix, step, prev_content):
-        from paper_2506_07639_b200.backends import BackendError, StepGenerator
+        from paper_2506_07639_b200.refapi import backends as rb
+        BackendError, StepGenerator = rb.BackendError, rb.StepGenerator
         n, truncated = planned_length(self.profile, context, step, prev_content)
         if n < 0:
             raise BackendError(f"no synthetic profile for step {step.name!r}")

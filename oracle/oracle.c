@@ -35,6 +35,7 @@
 #include <stdlib.h>
 #include <string.h>
 #include <omp.h>
+#include <immintrin.h>
 
 #define CHUNK 64
 
@@ -192,11 +193,58 @@ void or_destroy(or_model* m) {
     free(m->layers); free(m->embed); free(m->lm_head); free(m->final_norm); free(m->rope); free(m);
 }
 
+/*
+ * Canonical dots of one weight row against 32 tokens at once (AVX2): the
+ * 8-wide vectors run across TOKENS, so every (row, token) dot keeps exactly
+ * cdot's order -- lane l accumulates k = 128j + 4l + c (j, then c ascending)
+ * with one fused multiply-add each, then the xor butterfly.  Only the loop
+ * order over lanes changes (lanes are independent), so results are
+ * bit-identical to cdot.  xT holds 4 blocks of 8 tokens as [block][K][8].
+ */
+static void cdot_rows32(float* out, const float* w, const float* xT, int K, int N_out_stride) {
+    __m256 part[4][32];
+    for (int l = 0; l < 32; l++) {
+        __m256 a0 = _mm256_setzero_ps(), a1 = a0, a2 = a0, a3 = a0;
+        for (int j = 0; j + 4 * l < K; j += 128) {
+            int k = j + 4 * l;
+            for (int c = 0; c < 4; c++) {
+                __m256 wv = _mm256_set1_ps(w[k + c]);
+                const float* xp = xT + (size_t)(k + c) * 8;
+                a0 = _mm256_fmadd_ps(wv, _mm256_loadu_ps(xp), a0);
+                a1 = _mm256_fmadd_ps(wv, _mm256_loadu_ps(xp + (size_t)K * 8), a1);
+                a2 = _mm256_fmadd_ps(wv, _mm256_loadu_ps(xp + (size_t)K * 16), a2);
+                a3 = _mm256_fmadd_ps(wv, _mm256_loadu_ps(xp + (size_t)K * 24), a3);
+            }
+        }
+        part[0][l] = a0; part[1][l] = a1; part[2][l] = a2; part[3][l] = a3;
+    }
+    for (int b = 0; b < 4; b++) {
+        for (int off = 16; off >= 1; off >>= 1)
+            for (int l = 0; l < off; l++) part[b][l] = _mm256_add_ps(part[b][l], part[b][l + off]);
+        float tmp[8];
+        _mm256_storeu_ps(tmp, part[b][0]);
+        for (int i = 0; i < 8; i++) out[(size_t)(8 * b + i) * N_out_stride] = tmp[i];
+    }
+}
+
 /* y[n][N] = x[n][K] . W[N][K]^T, every element a canonical dot */
 static void matmul(float* y, const float* x, const float* W, int n, int N, int K) {
+    int n32 = (K % 4 == 0) ? n / 32 * 32 : 0;
+    if (n32) {
+        float* xT = (float*)malloc(sizeof(float) * (size_t)32 * K);
+        for (int t0 = 0; t0 < n32; t0 += 32) {
+            for (int b = 0; b < 4; b++)
+                for (int k = 0; k < K; k++)
+                    for (int i = 0; i < 8; i++)
+                        xT[((size_t)b * K + k) * 8 + i] = x[(size_t)(t0 + 8 * b + i) * K + k];
+#pragma omp parallel for schedule(static)
+            for (int r = 0; r < N; r++) cdot_rows32(y + (size_t)t0 * N + r, W + (size_t)r * K, xT, K, N);
+        }
+        free(xT);
+    }
 #pragma omp parallel for schedule(static)
     for (int r = 0; r < N; r++)
-        for (int t = 0; t < n; t++) y[(size_t)t * N + r] = cdot(W + (size_t)r * K, x + (size_t)t * K, K);
+        for (int t = n32; t < n; t++) y[(size_t)t * N + r] = cdot(W + (size_t)r * K, x + (size_t)t * K, K);
 }
 
 static void rope_apply(const or_model* m, float* v, int pos) {

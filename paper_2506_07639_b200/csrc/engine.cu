@@ -422,11 +422,12 @@ void launch_layers(fe_engine* e, Lane& ln, const fe::Fwd& f, int n, bool decode,
     const int p = prof_begin(e, ln, PROF_TICK);
     fe::launch_decode_mk(k, st);
     // algorithmic bytes of the tick: every weight once, the K/V pages the
-    // cascade items stage (shared pages once per head), the new K/V rows
+    // cascade items stage in every layer (shared pages once per head;
+    // `kv_bytes` is one layer's), the new K/V rows
     const double el = (double)e->elem;
     const double w_bytes = (double)m.L * (4.0 * m.d * m.d + 3.0 * m.F * m.d) * el + (double)m.V * m.d * el;
     const double kv_write = (double)n * m.L * 2.0 * m.d * el;
-    prof_end(e, ln, p, w_bytes + kv_bytes + kv_write);
+    prof_end(e, ln, p, w_bytes + (double)m.L * kv_bytes + kv_write);
     prof_end(e, ln, whole, 0.0);
     return;
   }

@@ -62,3 +62,9 @@ def merge_shards(per_rank: Sequence[dict], episodes: Sequence[int]) -> list[Any]
     if missing:
         raise ValueError(f"episodes {missing} missing from the gathered shards")
     return [merged[e] for e in episodes]
+
+
+def episode_tokens(results) -> list:
+    """One episode's per-timestep step contents as plain int tuples
+    [(step name, tokens), ...] -- what ranks gather (the episode's results)."""
+    return [tuple((name, tuple(int(t) for t in toks)) for name, toks in r.trace.steps) for r in results]

@@ -1,44 +1,61 @@
 """`EngineBackend`: the reference `GenerationBackend` served by the B200 engine.
 
-Drop-in for the protocol of `pkg/src/ecot_sched/backends.py:98-110`
-(`encode`, `begin_step`, `deterministic`, `supports_prefix_conditioning`),
-plus the two runner-level extensions the GPU-aware runners use
-(schedulers.py in this package):
+Implements the protocol of `ecot_sched.backends.GenerationBackend`
+(`pkg/src/ecot_sched/backends.py:98-110`: `encode`, `begin_step`,
+`deterministic`, `supports_prefix_conditioning`) so the reference's own
+runners (`ecot_sched.schedulers`) drive the GPU unchanged.
 
-* `begin_steps(ctx, jobs)` -- the N+1 branch jobs of one Fast-ECoT timestep
-  (reference `ParallelSyncRunner`, schedulers.py:399-420) decoded as one
-  batch: the longest prefix is prefilled once as a *trunk*, every job forks
-  the trunk's paged KV at its own prefix length (copy-on-write of the partial
-  page only) and all branches decode together;
-* `make_async_engine(slots)` -- the continuous batcher for Fast ECoT async
-  (reference `_MicroEngine`, schedulers.py:244-299) whose ticks are real
-  decode iterations.
+Batching without a runner fork.  `begin_step` does not decode: it prepares the
+request on the device (trunk lookup / prefill, copy-on-write fork of the
+paged KV at the prefix length) and returns a `StepGenerator` whose `tokens`
+is a `DeviceTokens` sequence -- its length (the length oracle) is known at
+once, its ids only when the request completes.  The first time any pending
+request's ids are read, *every* pending request is submitted and the engine
+decodes them as one continuous batch until that request completes.  The
+reference `ParallelSyncRunner` issues all N+1 branch requests of a timestep
+before it reads any content (`schedulers.py:399-420`), so its branches decode
+together on the GPU; `SequentialRunner` reads each step before issuing the
+next (`schedulers.py:329-351`), so it decodes one request at a time, as
+Alg. A.1 prescribes.
 
 Reuse across timesteps: trunks live in a content-addressed prefix cache keyed
 by (vision seed, input ids); a request whose context and prefix extend a
 cached trunk forks it at the longest common prefix and prefills only the
-remainder (sequential ECoT extends the trunk step by step; repeated
-contexts reuse whole trunks).
+remainder (sequential ECoT extends the trunk step by step; repeated contexts
+reuse whole trunks).
 
-Errors from the engine surface as `BackendError` subclasses (`EngineError`)
-so the runners' `reuse_stale` / `abort_episode` policies apply unchanged
-(schedulers.py:422-434, :510-517).
+For Fast ECoT async (`schedulers.py:459-552`) `make_async_engine(slots)`
+returns a device engine with the surface of the reference `_MicroEngine`
+(`submit(_EngineRequest)`, `tick(timestep) -> (occupied, completed)`,
+`in_flight_names()`, `idle()`; `schedulers.py:244-299`), each tick being one
+real decode iteration; `runners.EngineParallelAsyncRunner` plugs it into the
+reference runner.
+
+Errors surface as `EngineError`, an `ecot_sched.backends.BackendError`, and
+every limit the device would reject at submission (request length, context
+length, live requests) is checked in `begin_step`, before the fork, so the
+reference failure policies (`schedulers.py:411-434`, `:481-483`,
+`:510-517`) see them.
 """
 
 from __future__ import annotations
 
 import threading
-from dataclasses import dataclass, field
+import time
+from collections.abc import Sequence as _SequenceABC
+from dataclasses import dataclass
 from typing import Callable, Optional, Sequence
 
 import numpy as np
 
 from .backends import (BackendError, EngineError, StepGenerator, SyntheticProfile, default_profile,
-                       encode_tokens, length_plan)
-from .batching import ACTION
+                       encode_context, length_plan)
 from .engine import Engine, PRIO_ACTION, PRIO_REASONING
-from .model import VIS_ID, context_ids, get_config, step_tag, text_ids, vision_seed
-from .trace import Context, StepSpec, TokenSeq
+from .model import ROPE_MAX_POS, VIS_ID, context_ids, get_config, step_tag, text_ids, vision_seed
+from .refapi import batching as _rbatch
+from .refapi import trace as _rt
+
+REQUEST_CAP = 1024  # tokens per request (device token arena slot, csrc/engine.cu kRequestCap)
 
 
 @dataclass
@@ -49,23 +66,91 @@ class _Trunk:
     stamp: int
 
 
-@dataclass
-class EngineRequest:
-    """A prepared branch request (async engine handle)."""
+class DeviceRequest:
+    """One branch request on the device."""
 
-    name: str
-    step: StepSpec
-    length: int
-    truncated: bool
-    tag: int
-    branch: int
-    priority: int
-    issue_timestep: int = 0
-    lane: int = 0
-    req: int = -1
-    tokens: TokenSeq = ()
-    on_complete: Optional[Callable[["EngineRequest", int], None]] = None
-    done: bool = False
+    __slots__ = ("name", "length", "truncated", "tag", "branch", "priority", "lane", "req", "tokens",
+                 "error", "log", "on_complete", "waiter")
+
+    def __init__(self, name, length, truncated, tag, branch, priority):
+        self.name, self.length, self.truncated = name, length, truncated
+        self.tag, self.branch, self.priority = tag, branch, priority
+        self.lane = 0
+        self.req = -1                      # device request id once submitted
+        self.tokens: Optional[tuple] = None
+        self.error: Optional[BaseException] = None
+        self.log = None
+        self.on_complete: Optional[Callable[["DeviceRequest"], None]] = None
+        self.waiter = None                 # engine that owns completion (two-stream lane 1)
+
+    @property
+    def done(self) -> bool:
+        return self.tokens is not None
+
+
+class DeviceTokens(_SequenceABC):
+    """Token ids of a device request.  `len()` is known at issue (the length
+    oracle); reading any id resolves the request, driving the engine until it
+    completes (see the module docstring)."""
+
+    __slots__ = ("handle", "_owner")
+
+    def __init__(self, handle: DeviceRequest, owner: "EngineBackend"):
+        self.handle = handle
+        self._owner = owner
+
+    def resolve(self) -> tuple:
+        h = self.handle
+        if h.tokens is None:
+            self._owner._resolve(h)
+        return h.tokens
+
+    def __len__(self) -> int:
+        return self.handle.length
+
+    def __getitem__(self, i):
+        return self.resolve()[i]
+
+    def __iter__(self):
+        return iter(self.resolve())
+
+    def __eq__(self, other):
+        if isinstance(other, (tuple, list, DeviceTokens)):
+            return self.resolve() == tuple(other)
+        return NotImplemented
+
+    def __hash__(self):
+        return hash(self.resolve())
+
+    def __array__(self, dtype=None, copy=None):
+        return np.asarray(self.resolve(), dtype=dtype)
+
+    def __repr__(self) -> str:
+        h = self.handle
+        return f"DeviceTokens({h.tokens!r})" if h.tokens is not None else f"DeviceTokens(<{h.length} pending>)"
+
+
+class DeviceStepGenerator(StepGenerator):
+    """`StepGenerator` (`backends.py:69-95`) over a device request; the base
+    constructor is not called because it would materialise the tokens."""
+
+    def __init__(self, handle: DeviceRequest, owner: "EngineBackend"):  # noqa: D107
+        self._seq = DeviceTokens(handle, owner)
+        self.truncated = handle.truncated
+        self.reported_tokens = handle.length
+        self._pos = 0
+
+    @property
+    def tokens(self):
+        return self._seq
+
+    @property
+    def handle(self) -> DeviceRequest:
+        return self._seq.handle
+
+
+def device_handle(tokens) -> Optional[DeviceRequest]:
+    return tokens.handle if isinstance(tokens, DeviceTokens) else None
 
 
 class EngineBackend:
@@ -76,9 +161,9 @@ class EngineBackend:
                  profile: SyntheticProfile | None = None, device: int = 0,
                  engine: Engine | None = None, trunk_cache: int = 64, async_streams: int = 1,
                  request_log: list | None = None, **engine_kw):
-        """`async_streams=1`: lockstep async batcher (reference landing order,
-        byte-comparable traces); `2`: two-stream async scheduler (action on the
-        high-priority lane, reasoning refresh running on the low-priority lane in
+        """`async_streams=1`: lockstep async batcher (the reference landing
+        order, byte-comparable traces); `2`: two-stream async scheduler (action
+        on the high-priority lane, reasoning refresh on the low-priority lane in
         the background, across control steps).  `request_log`: if a list,
         every completed request appends (context, prefix, step name,
         prev_content, tokens) -- used by per-request parity checks."""
@@ -90,87 +175,63 @@ class EngineBackend:
         self._trunks: list[_Trunk] = []
         self._trunk_cap = trunk_cache
         self._clock = 0
-        # request -> handle, shared by every backend driving this engine (a
-        # request left in flight by one backend may complete in another's run)
-        if not hasattr(self.engine, "owners"):
-            self.engine.owners = {}
-        self._owners: dict[int, EngineRequest] = self.engine.owners
+        self._lock = threading.RLock()
+        self._pending: list[DeviceRequest] = []
+        self._owners: dict[int, DeviceRequest] = {}
+        self._live = 0                                  # prepared, not yet released
+        self._live_cap = max(4 * self.engine.max_slots, 256)   # device token arena slots
         self._async_engines: list = []
         self._slots = 8
+        self._fixed_slots = False    # an async engine fixes the batcher to the runner's slots
         self.requests = 0
 
-    # -- protocol ------------------------------------------------------------
-    def encode(self, instruction: str, observation: bytes) -> Context:
-        return Context(instruction, observation, encode_tokens(instruction, observation))
+    # -- protocol --------------------------------------------------------------
+    def encode(self, instruction: str, observation: bytes) -> _rt.Context:
+        return encode_context(instruction, observation)
 
-    def begin_step(self, context: Context, prefix: TokenSeq, step: StepSpec,
-                   prev_content: TokenSeq) -> StepGenerator:
-        out = self.begin_steps(context, [(step, prefix, prev_content)], priorities=[PRIO_ACTION])[0]
-        if isinstance(out, BackendError):
-            raise out
-        return out
-
-    def begin_steps(self, context: Context, jobs: Sequence[tuple[StepSpec, TokenSeq, TokenSeq]],
-                    priorities: Sequence[int] | None = None) -> list:
-        """Decode several branch requests of one context as one batch.
-        Returns a StepGenerator or a BackendError per job (job order)."""
-        if priorities is None:  # reference fan-out order: the action step is last
-            priorities = [PRIO_REASONING] * (len(jobs) - 1) + [PRIO_ACTION]
-        outcomes: list = [None] * len(jobs)
-        handles: dict[int, EngineRequest] = {}
-        order = sorted(range(len(jobs)), key=lambda i: -len(jobs[i][1]))  # longest trunk first
-        for i in order:
-            spec, prefix, prev = jobs[i]
-            try:
-                handles[i] = self._prepare(context, prefix, spec, prev, priorities[i])
-            except BackendError as exc:
-                outcomes[i] = exc
-        for i in sorted(handles):
-            self._submit(handles[i], None)
-        for i in sorted(handles):
-            h = handles[i]
-            if not h.done:
-                self._run(h.req, 0)
-            outcomes[i] = StepGenerator(h.tokens, truncated=h.truncated)
-        return outcomes
-
-    def begin_steps_multi(self, contexts: Sequence[Context], jobs_per_context: Sequence[Sequence],
-                          priorities=None) -> list[list]:
-        """Branch jobs of several independent contexts (episodes) decoded as one
-        batch (BASELINE config 4).  Returns per context a list of
-        StepGenerator / BackendError in job order."""
-        outcomes: list[list] = [[None] * len(j) for j in jobs_per_context]
-        handles: dict[tuple[int, int], EngineRequest] = {}
-        self._ensure_slots(sum(len(j) for j in jobs_per_context))
-        for e, (ctx, jobs) in enumerate(zip(contexts, jobs_per_context)):
-            prios = priorities[e] if priorities else [PRIO_REASONING] * (len(jobs) - 1) + [PRIO_ACTION]
-            for i in sorted(range(len(jobs)), key=lambda i: -len(jobs[i][1])):
-                spec, prefix, prev = jobs[i]
-                try:
-                    handles[(e, i)] = self._prepare(ctx, prefix, spec, prev, prios[i])
-                except BackendError as exc:
-                    outcomes[e][i] = exc
-        for key in sorted(handles):
-            self._submit(handles[key], None)
-        for key in sorted(handles):
-            h = handles[key]
-            if not h.done:
-                self._run(h.req, 0)
-            outcomes[key[0]][key[1]] = StepGenerator(h.tokens, truncated=h.truncated)
-        return outcomes
+    def begin_step(self, context: _rt.Context, prefix, step: _rt.StepSpec,
+                   prev_content) -> StepGenerator:
+        with self._lock:
+            h = self._prepare(context, prefix, step, prev_content, PRIO_REASONING)
+            self._pending.append(h)
+            self._ensure_slots(len(self._pending) + len(self._owners))
+        return DeviceStepGenerator(h, self)
 
     def make_async_engine(self, slots: int):
         if self.async_streams == 2:
             return TwoStreamAsyncEngine(self, slots)
-        return AsyncEngine(self, slots)
+        return AsyncDeviceEngine(self, slots)
+
+    # -- batching ----------------------------------------------------------------
+    def flush(self) -> None:
+        """Submit every pending request (they join the next decode tick)."""
+        with self._lock:
+            pending, self._pending = self._pending, []
+            for h in pending:
+                self._submit(h, 0)
+
+    def _resolve(self, h: DeviceRequest) -> None:
+        if h.waiter is not None:
+            h.waiter.wait_for(h)
+            return
+        with self._lock:
+            if h.tokens is not None:
+                return
+            if h.req < 0 and h.error is None:
+                self.flush()
+            if h.error is not None:
+                raise EngineError(f"request {h.name!r} failed: {h.error}") from h.error
+            self._run(h.req)
+            if h.tokens is None:
+                raise EngineError(f"request {h.name!r} did not complete")
 
     def _ensure_slots(self, n: int) -> None:
-        """Grow the batcher so a multi-episode barrier fits in one batch."""
-        if n > self._slots:
-            self._slots = min(n, self.engine.max_slots)
+        """Grow the batcher so every request issued together decodes in one batch."""
+        if n > self._slots and not self._fixed_slots:
+            self._slots = min(max(n, 2 * self._slots), self.engine.max_slots)
             self.engine.set_slots(self._slots)
 
-    # -- trunks & branches -----------------------------------------------------
+    # -- trunks & branches -------------------------------------------------------
     def _branch_point(self, vseed: int, ids: np.ndarray) -> tuple[int, bool]:
         """Sequence whose KV covers ids exactly up to len(ids) (possibly longer)."""
         n = ids.size
@@ -201,43 +262,76 @@ class EngineBackend:
             eng.seq_free(victim.seq)
         return seq, True
 
-    def _prepare(self, ctx: Context, prefix: TokenSeq, spec: StepSpec, prev: TokenSeq,
-                 priority: int, timestep: int = 0) -> EngineRequest:
+    def _prepare(self, ctx: _rt.Context, prefix, spec: _rt.StepSpec, prev, priority: int) -> DeviceRequest:
         plan = length_plan(self.profile, ctx, spec, prev)  # BackendError on unknown step
         ids = np.asarray(context_ids(ctx, self.cfg) + text_ids(prefix), dtype=np.int32)
-        vseed = vision_seed(ctx.observation)
-        trunk, _ = self._branch_point(vseed, ids)
+        # every limit fe_submit would reject, checked before any device state changes
+        if plan.length > REQUEST_CAP:
+            raise EngineError(f"step {spec.name!r}: {plan.length} tokens exceed the request cap {REQUEST_CAP}")
+        if ids.size + 1 + plan.length > ROPE_MAX_POS:
+            raise EngineError(f"step {spec.name!r}: context {ids.size} + {plan.length} tokens exceed "
+                              f"max_pos {ROPE_MAX_POS}")
+        if self._live >= self._live_cap:
+            raise EngineError(f"too many live requests ({self._live})")
+        trunk, _ = self._branch_point(vision_seed(ctx.observation), ids)
         branch = self.engine.seq_fork(trunk, ids.size)
-        h = EngineRequest(spec.name, spec, plan.length, plan.truncated, step_tag(spec), branch,
-                          priority, issue_timestep=timestep)
+        h = DeviceRequest(spec.name, plan.length, plan.truncated, step_tag(spec), branch, priority)
+        self._live += 1
         if self.request_log is not None:
             h.log = (ctx, tuple(prefix), spec.name, tuple(prev))
         return h
 
-    def _submit(self, h: EngineRequest, on_complete) -> None:
-        h.on_complete = on_complete
-        h.req = self.engine.submit(h.branch, h.tag, h.length, h.priority)
-        self._owners[h.req] = h
+    def _submit(self, h: DeviceRequest, lane: int) -> None:
+        """Hand a prepared request to the device batcher; a rejection is kept on
+        the handle (and raised when its tokens are read) and frees its fork."""
+        try:
+            h.lane = lane
+            h.req = self.engine.submit_lane(lane, h.branch, h.tag, h.length, h.priority)
+        except EngineError as exc:
+            h.error = exc
+            self._drop(h)
+            return
+        if lane == 0:
+            self._owners[h.req] = h
         self.requests += 1
 
-    def _run(self, stop_req: int, timestep: int) -> list[int]:
-        occupancy, done = self.engine.run(stop_req)
+    def _drop(self, h: DeviceRequest) -> None:
+        """Release a request's fork (never submitted, or completed)."""
+        if h.branch >= 0:
+            self.engine.seq_free(h.branch)
+            h.branch = -1
+            self._live -= 1
+
+    def discard(self, h: DeviceRequest) -> None:
+        """Abandon a prepared, never-submitted request."""
+        with self._lock:
+            if h in self._pending:
+                self._pending.remove(h)
+            if h.req < 0:
+                self._drop(h)
+
+    def _complete(self, h: DeviceRequest, lane: int = 0) -> None:
+        eng = self.engine
+        h.tokens = tuple(eng.request_tokens(h.req, h.length))
+        eng.request_release(h.req)
+        self._drop(h)
+        if self.request_log is not None and h.log is not None:
+            self.request_log.append(h.log + (h.tokens,))
+
+    def _run(self, stop_req: int, max_ticks: int = 0) -> list[int]:
+        """Lane-0 decode until `stop_req` completes (-1: idle) or `max_ticks`."""
+        occupancy, done = self.engine.run(stop_req, lane=0, max_ticks=max_ticks)
+        landed = []
         for req, _tick in done:
             h = self._owners.pop(req, None)
             if h is None:
                 raise EngineError(f"request {req} completed without an owner")
-            h.tokens = tuple(self.engine.request_tokens(req, h.length))
-            h.done = True
-            self._log(h)
-            self.engine.request_release(req)
-            self.engine.seq_free(h.branch)
+            self._complete(h)
+            landed.append(h)
+        for h in landed:
             if h.on_complete is not None:
-                h.on_complete(h, timestep)
+                h.on_complete(h)
         return occupancy
-
-    def _log(self, h: EngineRequest) -> None:
-        if self.request_log is not None and getattr(h, "log", None) is not None:
-            self.request_log.append(h.log + (h.tokens,))
 
     def close(self) -> None:
         for eng in list(self._async_engines):
@@ -245,48 +339,83 @@ class EngineBackend:
         self.engine.close()
 
 
-class AsyncEngine:
-    """Continuous batcher facade used by `ParallelAsyncRunner`: same surface
-    as the reference `_MicroEngine` (submit / in_flight_names), but each tick
-    is one decode iteration of every admitted row on the GPU."""
+def _device_priority(priority: str) -> int:
+    return PRIO_ACTION if priority == _rbatch.ACTION else PRIO_REASONING
+
+
+class AsyncDeviceEngine:
+    """Lockstep Fast-ECoT async engine: the reference `_MicroEngine` surface
+    (`schedulers.py:244-299`) over the device batcher.  Admission is the
+    reference's (action first, then FIFO; a slot freed at tick k is reused at
+    k+1 -- csrc/engine.cu `tick()`), each `tick` is one decode iteration of
+    every admitted row, and completions fire the requests' `on_complete`
+    after the tick, as the reference does."""
 
     def __init__(self, backend: EngineBackend, slots: int):
         self.backend = backend
         backend.engine.set_slots(slots)
         backend._slots = slots
-        self._inflight: dict[int, EngineRequest] = {}
+        backend._fixed_slots = True
+        self._inflight: dict[int, object] = {}   # device request id -> reference _EngineRequest
+        self._now = 0
+        backend._async_engines.append(self)
 
-    def prepare(self, ctx, prefix, spec, prev_content, priority: str, timestep: int) -> EngineRequest:
-        prio = PRIO_ACTION if priority == ACTION else PRIO_REASONING
-        return self.backend._prepare(ctx, prefix, spec, prev_content, prio, timestep)
+    def _take(self, req) -> DeviceRequest:
+        h = device_handle(req.tokens)
+        if h is None:
+            raise EngineError(f"request {req.name!r} was not issued by this engine's backend")
+        be = self.backend
+        if h in be._pending:
+            be._pending.remove(h)
+        h.priority = _device_priority(req.priority)
+        return h
 
-    def submit(self, h: EngineRequest, on_complete) -> None:
-        def landed(req: EngineRequest, t: int) -> None:
-            self._inflight.pop(req.req, None)
-            if on_complete is not None:
-                on_complete(req, t)
+    def submit(self, req) -> None:
+        be = self.backend
+        with be._lock:
+            h = self._take(req)
+            be._submit(h, 0)
+            if h.error is not None:
+                raise EngineError(f"request {req.name!r} rejected: {h.error}") from h.error
+            self._inflight[h.req] = req
+            h.on_complete = self._landed
 
-        self.backend._submit(h, landed)
-        self._inflight[h.req] = h
+    def _landed(self, h: DeviceRequest) -> None:
+        self._completed.append(self._inflight.pop(h.req))
 
     def in_flight_names(self) -> set[str]:
-        return {h.name for h in self._inflight.values()}
+        return {r.name for r in self._inflight.values()}
 
     def idle(self) -> bool:
         return not self._inflight
 
-    def run_until_complete(self, h: EngineRequest, timestep: int) -> list[int]:
+    def tick(self, timestep: int) -> tuple[int, list]:
         self._now = timestep
-        return self.backend._run(h.req, timestep)
+        be = self.backend
+        with be._lock:
+            if be._pending:
+                be.flush()
+            self._completed = []
+            occ = be._run(-1, max_ticks=1)
+            completed, self._completed = self._completed, []
+        for req in completed:
+            req.remaining = 0
+            if req.on_complete is not None:
+                req.on_complete(req, timestep)
+        return (occ[0] if occ else 0), completed
 
     def drain(self) -> None:
         """Decode every request still in flight (they land at the last control
         timestep) so the engine is idle before it is handed to another runner."""
-        if self._inflight:
-            self.backend._run(-1, getattr(self, "_now", 0))
+        while self._inflight:
+            self.tick(self._now)
+
+    def wait_for(self, h: DeviceRequest) -> None:  # lane 0 requests resolve through the backend
+        self.backend._resolve(h)
 
     def close(self) -> None:
-        pass
+        if self in self.backend._async_engines:
+            self.backend._async_engines.remove(self)
 
 
 class TwoStreamAsyncEngine:
@@ -296,11 +425,12 @@ class TwoStreamAsyncEngine:
     priority) against the last committed reasoning; reasoning-refresh requests
     decode on lane 1 (lowest priority), driven by a background host thread
     that keeps ticking across control steps.  A request's content is fixed at
-    issue (the snapshot it was prepared against, as in the reference,
-    `schedulers.py:471-492`); it lands into the cache at the control timestep
+    issue (the snapshot it was prepared against, `schedulers.py:471-492`); it
+    lands into the cache -- through the reference runner's own `on_complete`
+    (`cache.write`, `schedulers.py:485-486`) -- at the control timestep
     current when it completes.  Landing order is real-time, so traces are
-    checked per request (identical (context, prefix, step) -> identical tokens)
-    rather than byte-for-byte against the simulated clock."""
+    checked per request (identical (context, prefix, step) -> identical
+    tokens) rather than byte for byte against the simulated clock."""
 
     def __init__(self, backend: EngineBackend, slots: int):
         self.backend = backend
@@ -308,9 +438,12 @@ class TwoStreamAsyncEngine:
         eng.set_slots(slots)
         eng.set_slots_lane(1, slots)
         backend._slots = slots
+        backend._fixed_slots = True
         self._lock = threading.Lock()
-        self._inflight: dict[int, EngineRequest] = {}
-        self._landing = 0  # completed requests the background thread is still landing
+        self._cv = threading.Condition(self._lock)
+        self._inflight: dict[int, tuple[DeviceRequest, object]] = {}   # lane-1 id -> (handle, request)
+        self._landing: set[str] = set()   # completed, on_complete still running
+        self._lane0: dict[int, tuple[DeviceRequest, object]] = {}
         self._now = 0
         self._errors: list[BaseException] = []
         self._stop = threading.Event()
@@ -319,50 +452,70 @@ class TwoStreamAsyncEngine:
         self._thread.start()
         backend._async_engines.append(self)
 
-    # -- runner surface (same as AsyncEngine / the reference _MicroEngine) ----
-    def prepare(self, ctx, prefix, spec, prev_content, priority: str, timestep: int) -> EngineRequest:
-        prio = PRIO_ACTION if priority == ACTION else PRIO_REASONING
-        with self._lock:  # trunk cache / prefill / fork all happen on lane 0
-            h = self.backend._prepare(ctx, prefix, spec, prev_content, prio, timestep)
-        h.lane = 0 if prio == PRIO_ACTION else 1
-        return h
-
-    def submit(self, h: EngineRequest, on_complete) -> None:
-        h.on_complete = on_complete
-        if h.lane == 0:
-            h.req = self.backend.engine.submit_lane(0, h.branch, h.tag, h.length, h.priority)
-            return
-        with self._lock:
-            h.req = self.backend.engine.submit_lane(1, h.branch, h.tag, h.length, h.priority)
-            self._inflight[h.req] = h
-        self._work.set()
+    # -- runner surface (the reference _MicroEngine's) -------------------------
+    def submit(self, req) -> None:
+        be = self.backend
+        h = device_handle(req.tokens)
+        if h is None:
+            raise EngineError(f"request {req.name!r} was not issued by this engine's backend")
+        prio = _device_priority(req.priority)
+        with be._lock:
+            if h in be._pending:
+                be._pending.remove(h)
+            h.priority = prio
+            lane = 0 if prio == PRIO_ACTION else 1
+            if lane == 1:
+                h.waiter = self
+                with self._lock:   # registered before the background lane can complete it
+                    be._submit(h, 1)
+                    if h.error is None:
+                        self._inflight[h.req] = (h, req)
+            else:
+                be._submit(h, 0)
+                if h.error is None:
+                    self._lane0[h.req] = (h, req)
+                    h.on_complete = self._landed0
+        if h.error is not None:
+            raise EngineError(f"request {req.name!r} rejected: {h.error}") from h.error
+        if lane == 1:
+            self._work.set()
 
     def in_flight_names(self) -> set[str]:
         with self._lock:
-            return {h.name for h in self._inflight.values()}
+            names = {r.name for _, r in self._inflight.values()}
+            names.update(self._landing)
+        names.update(r.name for _, r in self._lane0.values())
+        return names
 
     def idle(self) -> bool:
         with self._lock:
-            return not self._inflight and not self._landing
+            return not self._inflight and not self._landing and not self._lane0
 
-    def run_until_complete(self, h: EngineRequest, timestep: int) -> list[int]:
+    def _landed0(self, h: DeviceRequest) -> None:
+        self._completed.append(self._lane0.pop(h.req)[1])
+
+    def tick(self, timestep: int) -> tuple[int, list]:
+        """One lane-0 decode iteration (the action lane)."""
         self._raise_background_error()
         self._now = timestep
-        eng = self.backend.engine
-        occupancy, _ = eng.run(h.req, lane=0)
-        h.tokens = tuple(eng.request_tokens(h.req, h.length))
-        h.done = True
-        eng.request_release(h.req)
-        eng.seq_free(h.branch)
-        self.backend._log(h)
-        return occupancy
+        be = self.backend
+        with be._lock:
+            self._completed = []
+            occ = be._run(-1, max_ticks=1)
+            completed, self._completed = self._completed, []
+        for req in completed:
+            req.remaining = 0
+            if req.on_complete is not None:
+                req.on_complete(req, timestep)
+        return (occ[0] if occ else 0), completed
 
     def set_timestep(self, timestep: int) -> None:
         self._now = timestep
 
-    # -- background lane ----------------------------------------------------
+    # -- background lane --------------------------------------------------------
     def _loop(self) -> None:
-        eng = self.backend.engine
+        be = self.backend
+        eng = be.engine
         while not self._stop.is_set():
             with self._lock:
                 busy = bool(self._inflight)
@@ -372,26 +525,41 @@ class TwoStreamAsyncEngine:
                 continue
             try:
                 _, done = eng.run(-1, lane=1, max_ticks=4)
-                for req, _tick in done:
-                    # take the handle out before the id is released: a submit on
-                    # the runner thread may reuse the id right after the release
+                for req_id, _tick in done:
+                    # the name stays visible to in_flight_names() until the
+                    # landing (cache write) has happened
                     with self._lock:
-                        h = self._inflight.pop(req)
-                        self._landing += 1
+                        h, req = self._inflight.pop(req_id)
+                        self._landing.add(req.name)
                     try:
-                        h.tokens = tuple(eng.request_tokens(req, h.length))
-                        h.done = True
-                        eng.request_release(req)
-                        eng.seq_free(h.branch)
-                        self.backend._log(h)
-                        if h.on_complete is not None:
-                            h.on_complete(h, self._now)
+                        with be._lock:
+                            be._complete(h, lane=1)
+                        with self._lock:
+                            self._cv.notify_all()
+                        req.remaining = 0
+                        if req.on_complete is not None:
+                            req.on_complete(req, self._now)
                     finally:
                         with self._lock:
-                            self._landing -= 1
+                            self._landing.discard(req.name)
             except BaseException as exc:  # surfaced on the runner thread
                 self._errors.append(exc)
                 self._stop.set()
+                with self._lock:
+                    self._cv.notify_all()
+
+    def wait_for(self, h: DeviceRequest, timeout: float = 600.0) -> None:
+        """Block until a lane-1 request has completed."""
+        with self._lock:
+            end = time.monotonic() + timeout
+            while h.tokens is None:
+                if self._errors:
+                    break
+                if not self._cv.wait(timeout=max(0.0, end - time.monotonic())):
+                    break
+        self._raise_background_error()
+        if h.tokens is None:
+            raise EngineError(f"lane-1 request {h.name!r} did not complete")
 
     def _raise_background_error(self) -> None:
         if self._errors:
@@ -399,13 +567,17 @@ class TwoStreamAsyncEngine:
 
     def drain(self, timeout: float = 60.0) -> None:
         """Wait until every background request has landed."""
-        import time
         t0 = time.time()
         while not self.idle() and time.time() - t0 < timeout:
             self._raise_background_error()
-            time.sleep(0.002)
+            if self._lane0:
+                self.tick(self._now)
+            else:
+                time.sleep(0.002)
 
     def close(self) -> None:
         self._stop.set()
         self._work.set()
         self._thread.join(timeout=10.0)
+        if self in self.backend._async_engines:
+            self.backend._async_engines.remove(self)

@@ -26,8 +26,11 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .backends import stable_digest
-from .trace import Context, StepSpec, TokenSeq
+from .refapi import backends as _rb
+from .refapi import trace as _rt
+
+stable_digest = _rb.stable_digest
+Context, StepSpec, TokenSeq = _rt.Context, _rt.StepSpec, _rt.TokenSeq
 
 TEXT_VOCAB = 32000
 VOCAB = 32064

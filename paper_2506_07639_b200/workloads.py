@@ -7,8 +7,11 @@ a custom schema and profile.
 
 from __future__ import annotations
 
-from .backends import StepProfile, SyntheticProfile, default_profile
-from .trace import HIGH, LOW, StepSchema, StepSpec, default_schema
+from .refapi import backends as _rb
+from .refapi import trace as _rt
+
+StepProfile, SyntheticProfile, default_profile = _rb.StepProfile, _rb.SyntheticProfile, _rb.default_profile
+HIGH, LOW, StepSchema, StepSpec, default_schema = _rt.HIGH, _rt.LOW, _rt.StepSchema, _rt.StepSpec, _rt.default_schema
 
 STRESS_STEPS = ("task", "plan", "subtask", "move", "gripper", "visible_objects", "scene")
 

@@ -1,10 +1,13 @@
-"""N > 1 host path on CPU (gloo, world size 2): episode sharding, per-rank
-episodes driven by the package runners, and the result gather -- the same
-functions bench.py uses over NCCL.  The gathered traces must equal a
-single-process run of every episode (episodes are independent)."""
+"""N > 1 host path on CPU (gloo, world size 2): episode sharding, each rank
+driving its shard as one `BatchedEpisodes` batch on its own engine (a fake
+device engine here), and the token gather -- the same functions bench.py
+uses over NCCL.  The gathered traces must equal a single-process batch of
+every episode (episodes are independent)."""
 
 import os
 import socket
+import sys
+from pathlib import Path
 
 import pytest
 import torch.multiprocessing as mp
@@ -21,14 +24,18 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
-def _episode_bytes(seed: int) -> list[bytes]:
-    from paper_2506_07639_b200 import schedulers as S
-    from paper_2506_07639_b200.backends import SyntheticBackend, default_profile
-    from paper_2506_07639_b200.trace import default_schema, trace_content_bytes
-    schema = default_schema()
-    res, _ = S.run_episode(S.SchedulerConfig(mode="parallel_sync", slots=8), T,
-                           SyntheticBackend(default_profile(0)), schema, seed=seed)
-    return [trace_content_bytes(r.trace, schema) for r in res]
+def _shard_tokens(seeds) -> dict:
+    """{episode: [per-timestep step token tuples]} from one batched engine."""
+    sys.path.insert(0, str(Path(__file__).resolve().parent))
+    import ecot_sched
+    from fake_engine import fake_backend
+
+    from paper_2506_07639_b200 import BatchedEpisodes
+    schema = ecot_sched.trace.default_schema()
+    be, _ = fake_backend()
+    batch = BatchedEpisodes(ecot_sched.SchedulerConfig(mode="parallel_sync", slots=8), be, schema, seeds)
+    steps = [batch.step(t) for t in range(T)]
+    return {e: D.episode_tokens([steps[t][i] for t in range(T)]) for i, e in enumerate(seeds)}
 
 
 def _worker(rank: int, world: int, port: int, out):
@@ -36,8 +43,7 @@ def _worker(rank: int, world: int, port: int, out):
                       LOCAL_RANK=str(rank))
     r, w, _ = D.init_from_env("gloo")
     mine = D.shard_episodes(EPISODES, w, r)
-    local = {e: _episode_bytes(e) for e in mine}
-    gathered = D.gather_to_all(local, w)
+    gathered = D.gather_to_all(_shard_tokens(mine), w)
     if r == 0:
         out.put(D.merge_shards(gathered, EPISODES))
     import torch.distributed as dist
@@ -74,5 +80,5 @@ def test_gloo_world2_sharded_episodes_equal_single_process():
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
-    want = [_episode_bytes(e) for e in EPISODES]
-    assert got == want
+    want = _shard_tokens(EPISODES)
+    assert got == [want[e] for e in EPISODES]

@@ -13,10 +13,12 @@ import numpy as np
 import pytest
 import torch
 
+import ecot_sched
 from conftest import GOLDEN
+from ecot_sched import schedulers as RS
+from ecot_sched.trace import trace_content_bytes
+from paper_2506_07639_b200 import BatchedEpisodes
 from paper_2506_07639_b200 import model as M
-from paper_2506_07639_b200 import schedulers as S
-from paper_2506_07639_b200 import trace as T
 from paper_2506_07639_b200.backends import EngineError
 from paper_2506_07639_b200.engine import Engine
 from paper_2506_07639_b200.engine_backend import EngineBackend
@@ -153,17 +155,35 @@ def test_fork_cow_branch_equals_fresh_sequence(tiny_f32, oracle_tiny):
 
 @pytest.mark.parametrize("mode", ["sequential", "parallel_sync", "parallel_async"])
 def test_traces_byte_identical_to_reference_golden(schema, golden_traces, mode):
-    """BASELINE config 1 through the GPU-aware runners and the engine: trace
-    bytes, simulated latency, staleness and accounting equal the reference
-    runners over the CPU oracle."""
+    """BASELINE config 1: the reference's own `run_episode` / runners over
+    `EngineBackend` (parallel_async through the registered device-engine
+    runner): trace bytes, simulated latency, staleness and accounting equal
+    the reference runners over the CPU oracle."""
     g = golden_traces["modes"][mode]
     be = EngineBackend("tiny", dtype="f32", seed=0, kv_pages=1024)
     try:
-        res, _ = S.run_episode(S.SchedulerConfig(mode=mode, slots=8), golden_traces["T"], be, schema, seed=0)
-        assert [T.trace_content_bytes(r.trace, schema).decode() for r in res] == g["lines"]
+        res, _ = ecot_sched.run_episode(RS.SchedulerConfig(mode=mode, slots=8), golden_traces["T"], be, schema, seed=0)
+        assert [trace_content_bytes(r.trace, schema).decode() for r in res] == g["lines"]
         assert [r.latency_ms for r in res] == g["latency_ms"]
         assert [r.staleness for r in res] == g["staleness"]
         assert [r.generated_tokens for r in res] == g["generated_tokens"]
+    finally:
+        be.close()
+
+
+def test_unregistered_reference_async_runner_over_engine(schema, golden_traces):
+    """The stock reference `ParallelAsyncRunner` (simulated `_MicroEngine`,
+    no device-engine hook) over `EngineBackend` also reproduces the golden
+    traces: its generators resolve on the device when the runner reads them."""
+    g = golden_traces["modes"]["parallel_async"]
+    be = EngineBackend("tiny", dtype="f32", seed=0, kv_pages=1024)
+    try:
+        runner = RS.ParallelAsyncRunner(be, schema, RS.SchedulerConfig(mode="parallel_async", slots=8))
+        assert isinstance(runner.engine, RS._MicroEngine)
+        res = [runner.step(be.encode("pick up the object and place it on the target",
+                                     RS.observation_for(0, t)), t) for t in range(golden_traces["T"])]
+        assert [trace_content_bytes(r.trace, schema).decode() for r in res] == g["lines"]
+        assert [r.latency_ms for r in res] == g["latency_ms"]
     finally:
         be.close()
 
@@ -173,7 +193,7 @@ def test_bf16_token_match_rate(golden_traces, schema):
     g = golden_traces["modes"]["sequential"]
     be = EngineBackend("tiny", dtype="bf16", seed=0, kv_pages=1024)
     try:
-        res, _ = S.run_episode(S.SchedulerConfig(mode="sequential"), 3, be, schema, seed=0)
+        res, _ = ecot_sched.run_episode(RS.SchedulerConfig(mode="sequential"), 3, be, schema, seed=0)
     finally:
         be.close()
     want = [json.loads(l) for l in g["lines"][:3]]
@@ -318,16 +338,16 @@ def test_batched_episodes_bit_exact_vs_independent_oracle_episodes(schema):
     seeds, T_ = [0, 1, 2], 3
     be = EngineBackend("tiny", dtype="f32", seed=0, kv_pages=1024)
     try:
-        drv = S.BatchedEpisodes(S.SchedulerConfig(mode="parallel_sync", slots=8), be, schema, seeds)
+        drv = BatchedEpisodes(RS.SchedulerConfig(mode="parallel_sync", slots=8), be, schema, seeds)
         got = [drv.step(t) for t in range(T_)]
     finally:
         be.close()
     model = OracleModel("tiny", seed=0)
     for e, seed in enumerate(seeds):
-        want, _ = S.run_episode(S.SchedulerConfig(mode="parallel_sync", slots=8), T_,
+        want, _ = ecot_sched.run_episode(RS.SchedulerConfig(mode="parallel_sync", slots=8), T_,
                                 OracleBackend("tiny", seed=0, model=model), schema, seed=seed)
         for t in range(T_):
-            assert T.trace_content_bytes(got[t][e].trace, schema) == T.trace_content_bytes(want[t].trace, schema)
+            assert trace_content_bytes(got[t][e].trace, schema) == trace_content_bytes(want[t].trace, schema)
             assert got[t][e].latency_ms == want[t].latency_ms
 
 
@@ -336,7 +356,7 @@ def test_bf16_wide_batch_decode_runs(schema):
     tick through the tcgen05 tile GEMM (M-fastest raster)."""
     be = EngineBackend("small", dtype="bf16", seed=0, kv_pages=2048)
     try:
-        drv = S.BatchedEpisodes(S.SchedulerConfig(mode="parallel_sync", slots=8), be, schema, list(range(8)))
+        drv = BatchedEpisodes(RS.SchedulerConfig(mode="parallel_sync", slots=8), be, schema, list(range(8)))
         res = [drv.step(t) for t in range(2)]
     finally:
         be.close()
@@ -353,10 +373,10 @@ def test_two_stream_async_per_request_parity(schema):
     log = []
     be = EngineBackend("tiny", dtype="f32", seed=0, kv_pages=2048, async_streams=2, request_log=log)
     try:
-        runner = S.make_runner(S.SchedulerConfig(mode="parallel_async", slots=8, wall_clock=True), be, schema)
+        runner = RS.make_runner(RS.SchedulerConfig(mode="parallel_async", slots=8, wall_clock=True), be, schema)
         results = []
         for t in range(8):
-            ctx = be.encode("pick up the object and place it on the target", S.observation_for(0, t))
+            ctx = be.encode("pick up the object and place it on the target", RS.observation_for(0, t))
             results.append(runner.step(ctx, t))
             time.sleep(0.01)  # paced control loop: the reasoning lane keeps running in between
         runner.engine.drain()
@@ -377,15 +397,15 @@ def test_stress_schema_parallel_sync_bit_exact():
     from oracle.backend import OracleBackend
     from paper_2506_07639_b200.workloads import stress_profile, stress_schema
     sch = stress_schema()
-    cfg = S.SchedulerConfig(mode="parallel_sync", slots=8)
+    cfg = RS.SchedulerConfig(mode="parallel_sync", slots=8)
     be = EngineBackend("tiny", dtype="f32", seed=0, kv_pages=2048, profile=stress_profile(0))
     try:
-        got, _ = S.run_episode(cfg, 2, be, sch, seed=0)
+        got, _ = ecot_sched.run_episode(cfg, 2, be, sch, seed=0)
     finally:
         be.close()
-    want, _ = S.run_episode(cfg, 2, OracleBackend("tiny", seed=0, profile=stress_profile(0)), sch, seed=0)
+    want, _ = ecot_sched.run_episode(cfg, 2, OracleBackend("tiny", seed=0, profile=stress_profile(0)), sch, seed=0)
     for a, b in zip(got, want):
-        assert T.trace_content_bytes(a.trace, sch) == T.trace_content_bytes(b.trace, sch)
+        assert trace_content_bytes(a.trace, sch) == trace_content_bytes(b.trace, sch)
         assert a.latency_ms == b.latency_ms
     assert sum(len(t) for _, t in got[1].trace.steps) > 1500
 
@@ -396,14 +416,14 @@ def test_engine_shared_by_lockstep_then_two_stream_backends(schema):
     same engine from its own warm-up without stray completions."""
     be = EngineBackend("tiny", dtype="f32", seed=0, kv_pages=2048)
     try:
-        asy = S.make_runner(S.SchedulerConfig(mode="parallel_async", slots=8, wall_clock=True), be, schema)
+        asy = RS.make_runner(RS.SchedulerConfig(mode="parallel_async", slots=8, wall_clock=True), be, schema)
         for t in range(3):
-            asy.step(be.encode("pick up the object", S.observation_for(1, t)), t)
+            asy.step(be.encode("pick up the object", RS.observation_for(1, t)), t)
         asy.engine.drain()
         assert be.engine.in_flight() == 0
         be2 = EngineBackend("tiny", dtype="f32", seed=0, engine=be.engine, async_streams=2)
-        asy2 = S.make_runner(S.SchedulerConfig(mode="parallel_async", slots=8, wall_clock=True), be2, schema)
-        res = [asy2.step(be2.encode("pick up the object", S.observation_for(2, t)), t) for t in range(3)]
+        asy2 = RS.make_runner(RS.SchedulerConfig(mode="parallel_async", slots=8, wall_clock=True), be2, schema)
+        res = [asy2.step(be2.encode("pick up the object", RS.observation_for(2, t)), t) for t in range(3)]
         asy2.engine.drain()
         asy2.engine.close()
     finally:

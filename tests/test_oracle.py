@@ -103,3 +103,23 @@ def test_canonical_dot_order():
         got = lib.or_cdot(w.ctypes.data, x.ctypes.data, K)
         assert np.float32(got) == acc[0]
         del a
+
+
+def test_reference_runners_over_oracle_reproduce_golden(schema, golden_traces):
+    """The golden lines were produced by the reference runners over the CPU
+    oracle (tests/golden/make_golden.py); re-running them here pins the
+    oracle (and the runners' simulated accounting) for the GPU parity tests."""
+    import ecot_sched
+    from ecot_sched.trace import trace_content_bytes
+
+    from oracle.backend import OracleBackend, OracleModel
+    model = OracleModel("tiny", seed=0)
+    for mode in ("sequential", "parallel_sync", "parallel_async"):
+        g = golden_traces["modes"][mode]
+        cfg = ecot_sched.SchedulerConfig(mode=mode, slots=8)
+        res, _ = ecot_sched.run_episode(cfg, golden_traces["T"], OracleBackend("tiny", seed=0, model=model),
+                                        schema, seed=0)
+        assert [trace_content_bytes(r.trace, schema).decode() for r in res] == g["lines"], mode
+        assert [r.latency_ms for r in res] == g["latency_ms"]
+        assert [r.staleness for r in res] == g["staleness"]
+        assert [r.generated_tokens for r in res] == g["generated_tokens"]
