@@ -50,6 +50,7 @@
 
 #include <algorithm>
 #include <stdexcept>
+#include <string>
 
 #ifndef MK_TRACE
 #define MK_TRACE 0  // decode_mk_trace.cu builds the instrumented variant
@@ -1392,9 +1393,24 @@ void launch_impl(const MkLaunch& l, cudaStream_t s) {
   a.flags = l.flags;
   a.fused = l.fused | (1 << MK_LM);  // lm_head always finalises in-phase (FINAL follows)
   a.pf_stages = std::max(1, std::min(kStages, l.pf_stages > 0 ? l.pf_stages : kStages));
-  decode_mk_kernel<<<l.grid, kThreads, kSmem, s>>>(*reinterpret_cast<const CUtensorMap*>(l.map_xg.bytes),
-                                                   *reinterpret_cast<const CUtensorMap*>(l.map_attn.bytes),
-                                                   *reinterpret_cast<const CUtensorMap*>(l.map_act.bytes), a);
+  // cooperative launch: the grid barriers need every CTA resident, which the
+  // runtime then guarantees (or rejects the launch) instead of a spin timeout
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(l.grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t err = cudaLaunchKernelEx(&cfg, decode_mk_kernel,
+                                             *reinterpret_cast<const CUtensorMap*>(l.map_xg.bytes),
+                                             *reinterpret_cast<const CUtensorMap*>(l.map_attn.bytes),
+                                             *reinterpret_cast<const CUtensorMap*>(l.map_act.bytes), a);
+  if (err != cudaSuccess)
+    throw std::runtime_error(std::string("decode tick: cooperative launch failed: ") + cudaGetErrorString(err));
 }
 
 }  // namespace

@@ -25,6 +25,8 @@
 #include <algorithm>
 #include <cstring>
 #include <map>
+#include <tuple>
+#include <unordered_map>
 #include <mutex>
 #include <thread>
 #include <chrono>
@@ -254,6 +256,20 @@ void reclaim_pages(fe_engine* e) {
       i++;
     }
   }
+}
+
+// Make `need` pages allocatable (waiting for in-flight frees if necessary);
+// throws before anything is allocated when the pool cannot supply them.
+void ensure_free_pages(fe_engine* e, int need) {
+  if (need <= 0 || (int)e->free_pages.size() >= need) return;
+  reclaim_pages(e);
+  if ((int)e->free_pages.size() < need && !e->pending_pages.empty()) {
+    for (int l = 0; l < kLanes; l++) CK(cudaStreamSynchronize(e->lanes[l].stream));
+    reclaim_pages(e);
+  }
+  if ((int)e->free_pages.size() < need)
+    throw Error("KV pool exhausted (" + std::to_string(e->n_pages) + " pages, " + std::to_string(need) +
+                " needed, " + std::to_string(e->free_pages.size()) + " free)");
 }
 
 int alloc_page(fe_engine* e) {
@@ -533,17 +549,56 @@ void forward(fe_engine* e, Lane& ln, const std::vector<RowIn>& rows, uint64_t vi
   if (e->prof_on && e->prof_used > 8192) flush_profile(e);  // only between forwards: all records closed
   if (ln.id != 0) CK(cudaStreamWaitEvent(ln.stream, e->lane0_ev, 0));  // trunks prefilled / forked on lane 0
 
+  // Pass 1: validate every row and count the pages this forward appends,
+  // without touching any sequence -- a rejected forward (bad position, shared
+  // page, pool exhausted, workspace too small) leaves the engine unchanged.
+  std::unordered_map<int, std::pair<int, int>> vlen;  // seq -> (length, pages) as the rows extend it
+  int new_pages = 0, chunk_need = 0;
+  for (int i = 0; i < n; i++) {
+    const RowIn& r = rows[i];
+    const Seq& s = seq_at(e, r.seq);
+    auto it = vlen.find(r.seq);
+    const int len = it == vlen.end() ? s.len : it->second.first;
+    int np = it == vlen.end() ? (int)s.pages.size() : it->second.second;
+    if (r.pos != len) throw Error("forward: non-contiguous append");
+    if (r.pos >= m.max_pos) throw Error("forward: position beyond max_pos");
+    const int pg = r.pos / FE_PAGE;
+    if (pg == np) {
+      np++;
+      new_pages++;
+    } else if (pg < (int)s.pages.size() && e->page_ref[s.pages[pg]] != 1) {
+      throw Error("forward: write into a shared page");
+    }
+    vlen[r.seq] = {r.pos + 1, np};
+    chunk_need += pg + 1;
+  }
+  if (chunk_need > ln.max_partials) throw Error("forward: partial workspace too small");
+  ensure_free_pages(e, new_pages);
+
+  // Pass 2: commit (cannot fail); undone below if a later check rejects.
+  std::vector<std::tuple<int, int, int>> undo;  // seq, length, pages before this forward
+  for (const auto& kv : vlen) {
+    const Seq& s = e->seqs[kv.first];
+    undo.emplace_back(kv.first, s.len, (int)s.pages.size());
+  }
+  auto rollback = [&]() {
+    for (const auto& u : undo) {
+      Seq& s = e->seqs[std::get<0>(u)];
+      while ((int)s.pages.size() > std::get<2>(u)) {
+        release_page(e, s.pages.back());
+        s.pages.pop_back();
+      }
+      s.len = std::get<1>(u);
+    }
+  };
   std::vector<fe::RowMeta> meta(n);
   std::vector<int32_t> head_rows;
   int chunk_total = 0;
   for (int i = 0; i < n; i++) {
     const RowIn& r = rows[i];
-    Seq& s = seq_at(e, r.seq);
-    if (r.pos != s.len) throw Error("forward: non-contiguous append");
-    if (r.pos >= m.max_pos) throw Error("forward: position beyond max_pos");
+    Seq& s = e->seqs[r.seq];
     const int pg = r.pos / FE_PAGE;
     if (pg == (int)s.pages.size()) s.pages.push_back(alloc_page(e));
-    if (e->page_ref[s.pages[pg]] != 1) throw Error("forward: write into a shared page");
     s.len = r.pos + 1;
     fe::RowMeta& mm = meta[i];
     mm.pos = r.pos;
@@ -564,7 +619,6 @@ void forward(fe_engine* e, Lane& ln, const std::vector<RowIn>& rows, uint64_t vi
       head_rows.push_back(i);
     }
   }
-  if (chunk_total > ln.max_partials) throw Error("forward: partial workspace too small");
 
   // cascade work list: group rows by the physical page their chunk maps to.
   // Rows sharing a trunk point at the same pages, so each shared page is
@@ -604,8 +658,10 @@ void forward(fe_engine* e, Lane& ln, const std::vector<RowIn>& rows, uint64_t vi
   // items, item rows, head rows) so a captured decode graph can be replayed
   // with new contents: counts that vary per tick are read on device.
   const MetaLayout& L = ln.layout;
-  if (n > L.cap_rows || (int)items.size() > L.cap_items || (int)irows.size() > L.cap_irows)
+  if (n > L.cap_rows || (int)items.size() > L.cap_items || (int)irows.size() > L.cap_irows) {
+    rollback();
     throw Error("forward: metadata capacity exceeded");
+  }
   int mi;
   unsigned char* hbuf = next_meta(ln, &mi);
   int32_t* hdr = reinterpret_cast<int32_t*>(hbuf);
@@ -1438,8 +1494,12 @@ int fe_op_skinny_tc(fe_engine* e, const void* x, const void* w, int32_t M, int32
 int fe_set_option(fe_engine* e, const char* key, int64_t value) {
   return guarded(e, [&] {
     const std::string k = key ? key : "";
-    if (k == "tc_min_rows") e->tc_min_rows = (int)value;
-    else if (k == "use_tc") {
+    // every option that changes the kernel selection baked into captured
+    // decode graphs drops them (a graphed tick would keep the old choice)
+    if (k == "tc_min_rows") {
+      e->tc_min_rows = (int)value;
+      clear_graphs(e);
+    } else if (k == "use_tc") {
       e->use_tc = value != 0 && !e->tc_maps.empty();
       e->mk_on = e->use_tc && e->mk_maps != nullptr;
       clear_graphs(e);
@@ -1472,9 +1532,14 @@ int fe_set_option(fe_engine* e, const char* key, int64_t value) {
       e->mk_on = value != 0 && e->use_tc && e->mk_maps != nullptr;
       clear_graphs(e);
     }
-    else if (k == "sk_mask") e->sk_mask = (int)value;
-    else if (k == "graphs") e->graphs_on = value != 0;
-    else if (k == "pdl") fe::g_pdl = value != 0;
+    else if (k == "sk_mask") {
+      e->sk_mask = (int)value;
+      clear_graphs(e);
+    } else if (k == "graphs") e->graphs_on = value != 0;
+    else if (k == "pdl") {
+      fe::g_pdl = value != 0;
+      clear_graphs(e);
+    }
     else if (k == "op_reps") e->op_reps = (int)std::max<int64_t>(1, value);
     else if (k == "sk_stages") {
       fe::g_sk_stages = (int)value;

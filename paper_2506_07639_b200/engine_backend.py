@@ -51,7 +51,7 @@ import numpy as np
 from .backends import (BackendError, EngineError, StepGenerator, SyntheticProfile, default_profile,
                        encode_context, length_plan)
 from .engine import Engine, PRIO_ACTION, PRIO_REASONING
-from .model import ROPE_MAX_POS, VIS_ID, context_ids, get_config, step_tag, text_ids, vision_seed
+from .model import PAGE_TOKENS, ROPE_MAX_POS, VIS_ID, context_ids, get_config, step_tag, text_ids, vision_seed
 from .refapi import batching as _rbatch
 from .refapi import trace as _rt
 
@@ -70,11 +70,14 @@ class DeviceRequest:
     """One branch request on the device."""
 
     __slots__ = ("name", "length", "truncated", "tag", "branch", "priority", "lane", "req", "tokens",
-                 "error", "log", "on_complete", "waiter")
+                 "error", "log", "on_complete", "waiter", "ids", "vseed", "reserve")
 
-    def __init__(self, name, length, truncated, tag, branch, priority):
+    def __init__(self, name, length, truncated, tag, priority, ids, vseed):
         self.name, self.length, self.truncated = name, length, truncated
-        self.tag, self.branch, self.priority = tag, branch, priority
+        self.tag, self.priority = tag, priority
+        self.ids, self.vseed = ids, vseed  # framed input; forked off a trunk when materialised
+        self.branch = -1                   # device sequence once materialised
+        self.reserve = 0                   # KV pages held for it until it completes
         self.lane = 0
         self.req = -1                      # device request id once submitted
         self.tokens: Optional[tuple] = None
@@ -179,6 +182,7 @@ class EngineBackend:
         self._pending: list[DeviceRequest] = []
         self._owners: dict[int, DeviceRequest] = {}
         self._live = 0                                  # prepared, not yet released
+        self._reserved = 0                              # KV pages held by live requests
         self._live_cap = max(4 * self.engine.max_slots, 256)   # device token arena slots
         self._async_engines: list = []
         self._slots = 8
@@ -204,8 +208,10 @@ class EngineBackend:
 
     # -- batching ----------------------------------------------------------------
     def flush(self) -> None:
-        """Submit every pending request (they join the next decode tick)."""
+        """Materialise and submit every pending request, in issue order (they
+        join the next decode tick)."""
         with self._lock:
+            self._materialize()
             pending, self._pending = self._pending, []
             for h in pending:
                 self._submit(h, 0)
@@ -263,9 +269,12 @@ class EngineBackend:
         return seq, True
 
     def _prepare(self, ctx: _rt.Context, prefix, spec: _rt.StepSpec, prev, priority: int) -> DeviceRequest:
+        """Plan a request and check every limit the device could reject later
+        (request cap, max_pos, live requests, KV pages); nothing on the device
+        changes yet -- the trunk prefill and the fork happen when the request
+        is materialised (`_materialize`), longest input first."""
         plan = length_plan(self.profile, ctx, spec, prev)  # BackendError on unknown step
         ids = np.asarray(context_ids(ctx, self.cfg) + text_ids(prefix), dtype=np.int32)
-        # every limit fe_submit would reject, checked before any device state changes
         if plan.length > REQUEST_CAP:
             raise EngineError(f"step {spec.name!r}: {plan.length} tokens exceed the request cap {REQUEST_CAP}")
         if ids.size + 1 + plan.length > ROPE_MAX_POS:
@@ -273,33 +282,86 @@ class EngineBackend:
                               f"max_pos {ROPE_MAX_POS}")
         if self._live >= self._live_cap:
             raise EngineError(f"too many live requests ({self._live})")
-        trunk, _ = self._branch_point(vision_seed(ctx.observation), ids)
-        branch = self.engine.seq_fork(trunk, ids.size)
-        h = DeviceRequest(spec.name, plan.length, plan.truncated, step_tag(spec), branch, priority)
+        h = DeviceRequest(spec.name, plan.length, plan.truncated, step_tag(spec), priority, ids,
+                          vision_seed(ctx.observation))
+        self._reserve_pages(h)
         self._live += 1
         if self.request_log is not None:
             h.log = (ctx, tuple(prefix), spec.name, tuple(prev))
         return h
 
+    def _covered(self, vseed: int, ids: np.ndarray) -> int:
+        """Longest prefix of `ids` whose KV exists (a cached trunk) or will
+        exist once the pending requests are materialised."""
+        best = 0
+        cands = [t.ids for t in self._trunks if t.vseed == vseed]
+        cands += [h.ids for h in self._pending if h.branch < 0 and h.vseed == vseed]
+        for other in cands:
+            m = min(ids.size, other.size)
+            neq = np.flatnonzero(other[:m] != ids[:m])
+            best = max(best, int(neq[0]) if neq.size else m)
+        return best
+
+    def _reserve_pages(self, h: DeviceRequest) -> None:
+        """Hold the KV pages the request can need (trunk extension beyond what
+        is cached or pending, the copy-on-write page, its decode pages) so
+        that materialising and decoding it cannot exhaust the pool; LRU trunks
+        are evicted to make room.  EngineError (a BackendError) otherwise."""
+        new_trunk = h.ids.size - self._covered(h.vseed, h.ids)
+        need = -(-max(0, new_trunk) // PAGE_TOKENS) + 1 + -(-(h.length + 1) // PAGE_TOKENS) + 1
+        while True:
+            st = self.engine.stats()
+            free = st["pages_total"] - st["pages_used"] - self._reserved
+            if free >= need or not self._trunks:
+                break
+            victim = min(self._trunks, key=lambda t: t.stamp)
+            self._trunks.remove(victim)
+            self.engine.seq_free(victim.seq)
+        if free < need:
+            raise EngineError(f"KV pool exhausted: step {h.name!r} needs {need} pages, {free} free")
+        h.reserve = need
+        self._reserved += need
+
+    def _materialize(self, extra=()) -> None:
+        """Fork every pending request (and `extra`) off its trunk, prefilling
+        trunks longest input first so nested branch prefixes share one prefill."""
+        todo = [h for h in [*self._pending, *extra] if h.branch < 0 and h.error is None and h.ids is not None]
+        for h in sorted(todo, key=lambda h: -h.ids.size):
+            try:
+                trunk, _ = self._branch_point(h.vseed, h.ids)
+                h.branch = self.engine.seq_fork(trunk, h.ids.size)
+            except EngineError as exc:
+                h.error = exc
+                self._release(h)
+
     def _submit(self, h: DeviceRequest, lane: int) -> None:
-        """Hand a prepared request to the device batcher; a rejection is kept on
-        the handle (and raised when its tokens are read) and frees its fork."""
+        """Hand a materialised request to the device batcher; a rejection is
+        kept on the handle (raised when its tokens are read) and frees it."""
+        if h.error is None and h.branch < 0:
+            self._materialize(extra=(h,))
+        if h.error is not None:
+            return
         try:
             h.lane = lane
             h.req = self.engine.submit_lane(lane, h.branch, h.tag, h.length, h.priority)
         except EngineError as exc:
             h.error = exc
-            self._drop(h)
+            self._release(h)
             return
         if lane == 0:
             self._owners[h.req] = h
         self.requests += 1
 
-    def _drop(self, h: DeviceRequest) -> None:
-        """Release a request's fork (never submitted, or completed)."""
+    def _release(self, h: DeviceRequest) -> None:
+        """Free a request's fork and its page reservation (failed or done)."""
         if h.branch >= 0:
             self.engine.seq_free(h.branch)
             h.branch = -1
+        if h.reserve:
+            self._reserved -= h.reserve
+            h.reserve = 0
+        if h.ids is not None:
+            h.ids = None
             self._live -= 1
 
     def discard(self, h: DeviceRequest) -> None:
@@ -308,13 +370,13 @@ class EngineBackend:
             if h in self._pending:
                 self._pending.remove(h)
             if h.req < 0:
-                self._drop(h)
+                self._release(h)
 
     def _complete(self, h: DeviceRequest, lane: int = 0) -> None:
         eng = self.engine
         h.tokens = tuple(eng.request_tokens(h.req, h.length))
         eng.request_release(h.req)
-        self._drop(h)
+        self._release(h)
         if self.request_log is not None and h.log is not None:
             self.request_log.append(h.log + (h.tokens,))
 
@@ -365,6 +427,7 @@ class AsyncDeviceEngine:
         if h is None:
             raise EngineError(f"request {req.name!r} was not issued by this engine's backend")
         be = self.backend
+        be._materialize()            # every request issued so far: one trunk prefill, longest first
         if h in be._pending:
             be._pending.remove(h)
         h.priority = _device_priority(req.priority)
@@ -460,6 +523,7 @@ class TwoStreamAsyncEngine:
             raise EngineError(f"request {req.name!r} was not issued by this engine's backend")
         prio = _device_priority(req.priority)
         with be._lock:
+            be._materialize()        # every request issued so far: one trunk prefill, longest first
             if h in be._pending:
                 be._pending.remove(h)
             h.priority = prio

@@ -54,7 +54,9 @@ class FakeEngine:
         self._seqno = 0
         self.occupancy_log: list[tuple[int, int]] = []  # (lane, occupied) per tick
         self.prefilled_tokens = 0
+        self.prefill_calls = 0
         self.on_release = None                          # hook run inside request_release
+        self.pages_total = 1 << 20
 
     # sequences
     def seq_create(self) -> int:
@@ -82,6 +84,7 @@ class FakeEngine:
             _, cur = self.seqs[seq]
             self.seqs[seq] = (vision_seed, cur + [int(i) for i in ids])
             self.prefilled_tokens += len(ids)
+            self.prefill_calls += 1
 
     # batcher
     def set_slots(self, n: int) -> None:
@@ -165,6 +168,11 @@ class FakeEngine:
         if self.on_release is not None:
             hook, self.on_release = self.on_release, None
             hook()
+
+    def stats(self) -> dict:
+        with self.lock:
+            used = sum(-(-len(ids) // M.PAGE_TOKENS) for _, ids in self.seqs.values())
+        return {"pages_total": self.pages_total, "pages_used": used}
 
     def close(self) -> None:
         pass

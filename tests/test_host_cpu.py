@@ -82,13 +82,13 @@ def test_trunk_prefix_is_prefilled_once_per_timestep():
     schema = default_schema()
     be, eng = fake_backend()
     res, _ = episode("parallel_sync", be, schema, 2)
-    before = eng.prefilled_tokens
-    RS.ParallelSyncRunner  # noqa: B018 - the reference runner is what run_episode used
+    before, calls = eng.prefilled_tokens, eng.prefill_calls
     runner = RS.ParallelSyncRunner(be, schema, RS.SchedulerConfig(mode="parallel_sync"))
     runner._prev_trace = res[-1].trace
     runner.step(be.encode("pick up the object and place it on the target", b"obs-x"), 2)
     ctx_len = 1 + be.cfg.n_vision + 16
     assert eng.prefilled_tokens - before == ctx_len + sum(len(t) for _, t in res[-1].trace.steps[:-1])
+    assert eng.prefill_calls - calls == 1   # longest branch first: one prefill, every other branch forks it
 
 
 def test_generators_are_lazy_until_read():
@@ -282,3 +282,19 @@ def test_summary_adds_percentiles():
     s = runners.summarize("parallel_sync", res, schema)
     assert s["latency_p50_ms"] <= s["latency_p99_ms"]
     assert s["latency_mean_ms"] == pytest.approx(float(np.mean([r.latency_ms for r in res])))
+
+
+def test_kv_pool_exhaustion_is_a_policy_error():
+    """Page reservations fail in begin_step (a BackendError) when the pool
+    cannot hold the request, so the reference reuse_stale policy applies
+    instead of a device allocation failing mid-tick."""
+    schema = default_schema()
+    be, eng = fake_backend(trunk_cache=1)
+    runner = RS.make_runner(RS.SchedulerConfig(mode="parallel_sync", slots=8), be, schema)
+    for t in range(2):
+        runner.step(be.encode("i", RS.observation_for(0, t)), t)
+    eng.pages_total = eng.stats()["pages_used"] + 16
+    r = runner.step(be.encode("i", RS.observation_for(0, 2)), 2)
+    assert r.failures                       # some branches could not reserve their pages
+    assert len(r.failures) < len(schema.steps)
+    assert be._live == 0 and be._reserved == 0
