@@ -80,6 +80,7 @@ struct Request {
   int lane = 0;
   int state = 0;      // 0 waiting, 1 running, 2 done
   bool capture = false;
+  int logit_base = 0;  // first row of its logits in the capture buffer
   bool live = false;
 };
 
@@ -173,7 +174,8 @@ struct fe_engine {
   std::vector<int> free_arena;
   int32_t* out_tokens = nullptr;
   float* logits = nullptr;  // lane 0 capture buffer
-  int capture_req = -1;
+  int logit_next = 0;    // next free row of the logit capture buffer
+  int capture_live = 0;  // live requests holding capture rows
 
   Lane lanes[kLanes];
 
@@ -846,7 +848,7 @@ int tick(fe_engine* e, Lane& ln, std::vector<int>* completed) {
     r.tok_src = q.produced == 0 ? -1 : q.arena * kRequestCap + q.produced - 1;
     r.vis_row = -1;
     r.out_idx = q.arena * kRequestCap + q.produced;
-    r.logit_row = (q.capture && q.produced < kLogitRows) ? q.produced : -1;
+    r.logit_row = (q.capture && q.produced < q.length) ? q.logit_base + q.produced : -1;
     r.head = true;
     rows.push_back(r);
   }
@@ -1334,7 +1336,7 @@ int fe_request_release(fe_engine* e, int32_t req) {
     Request& q = req_at(e, req);
     if (q.state == 0 || q.state == 1) throw Error("request still in flight");
     e->free_arena.push_back(q.arena);
-    if (e->capture_req == req) e->capture_req = -1;
+    if (q.capture && --e->capture_live == 0) e->logit_next = 0;  // buffer rows recycled when none is held
     q = Request();
     e->free_reqs.push_back(req);
   });
@@ -1344,9 +1346,13 @@ int fe_request_capture_logits(fe_engine* e, int32_t req) {
   return guarded(e, [&] {
     Request& q = req_at(e, req);
     if (q.lane != 0) throw Error("logit capture is a lane-0 feature");
-    if (e->capture_req >= 0 && e->capture_req != req) throw Error("another request is capturing logits");
+    if (q.capture) return;
+    if (q.state != 0 || q.produced != 0) throw Error("logit capture must be requested before decoding starts");
+    if (e->logit_next + q.length > kLogitRows) throw Error("logit capture buffer full (" + std::to_string(kLogitRows) + " rows)");
     q.capture = true;
-    e->capture_req = req;
+    q.logit_base = e->logit_next;
+    e->logit_next += q.length;
+    e->capture_live++;
   });
 }
 
@@ -1354,9 +1360,10 @@ int fe_request_logits(fe_engine* e, int32_t req, float* out, int32_t rows) {
   return guarded(e, [&] {
     Request& q = req_at(e, req);
     if (!q.capture) throw Error("request did not capture logits");
-    if (rows > std::min(q.produced, kLogitRows)) throw Error("more logit rows than captured");
+    if (rows > q.produced) throw Error("more logit rows than captured");
     CK(cudaStreamSynchronize(e->lanes[0].stream));
-    CK(cudaMemcpy(out, e->logits, sizeof(float) * (size_t)rows * e->m.V, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(out, e->logits + (size_t)q.logit_base * e->m.V, sizeof(float) * (size_t)rows * e->m.V,
+                  cudaMemcpyDeviceToHost));
   });
 }
 

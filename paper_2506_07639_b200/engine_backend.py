@@ -162,16 +162,20 @@ class EngineBackend:
 
     def __init__(self, config="tiny", dtype: str = "f32", seed: int = 0,
                  profile: SyntheticProfile | None = None, device: int = 0,
-                 engine: Engine | None = None, trunk_cache: int = 64, async_streams: int = 1,
+                 engine: Engine | None = None, trunk_cache: int = 64, async_mode: str = "lockstep",
                  request_log: list | None = None, **engine_kw):
-        """`async_streams=1`: lockstep async batcher (the reference landing
-        order, byte-comparable traces); `2`: two-stream async scheduler (action
-        on the high-priority lane, reasoning refresh on the low-priority lane in
-        the background, across control steps).  `request_log`: if a list,
+        """`async_mode="lockstep"`: the async runner's device engine advances
+        exactly as many decode iterations as each control step's action needs
+        (the reference landing order, byte-comparable traces);
+        `"background"`: a background ticker keeps the reasoning refresh decoding
+        between and during control steps, the action joins its ticks at high
+        priority (`BackgroundAsyncEngine`).  `request_log`: if a list,
         every completed request appends (context, prefix, step name,
         prev_content, tokens) -- used by per-request parity checks."""
         self.cfg = get_config(config)
-        self.async_streams = async_streams
+        if async_mode not in ("lockstep", "background"):
+            raise ValueError(f"async_mode must be 'lockstep' or 'background', got {async_mode!r}")
+        self.async_mode = async_mode
         self.request_log = request_log
         self.engine = engine or Engine(self.cfg, dtype=dtype, device=device, seed=seed, **engine_kw)
         self.profile = profile or default_profile(seed)
@@ -202,8 +206,8 @@ class EngineBackend:
         return DeviceStepGenerator(h, self)
 
     def make_async_engine(self, slots: int):
-        if self.async_streams == 2:
-            return TwoStreamAsyncEngine(self, slots)
+        if self.async_mode == "background":
+            return BackgroundAsyncEngine(self, slots)
         return AsyncDeviceEngine(self, slots)
 
     # -- batching ----------------------------------------------------------------
@@ -372,27 +376,25 @@ class EngineBackend:
             if h.req < 0:
                 self._release(h)
 
-    def _complete(self, h: DeviceRequest, lane: int = 0) -> None:
-        eng = self.engine
-        h.tokens = tuple(eng.request_tokens(h.req, h.length))
-        eng.request_release(h.req)
-        self._release(h)
-        if self.request_log is not None and h.log is not None:
-            self.request_log.append(h.log + (h.tokens,))
-
     def _run(self, stop_req: int, max_ticks: int = 0) -> list[int]:
-        """Lane-0 decode until `stop_req` completes (-1: idle) or `max_ticks`."""
+        """Lane-0 decode until `stop_req` completes (-1: idle) or `max_ticks`.
+        Per completed request: read its tokens, notify its owner (`on_complete`:
+        bookkeeping only, no user callbacks), then release the device id -- in
+        that order, because a released id can be reused by the very next
+        submit (e.g. from a landing callback)."""
         occupancy, done = self.engine.run(stop_req, lane=0, max_ticks=max_ticks)
-        landed = []
+        eng = self.engine
         for req, _tick in done:
             h = self._owners.pop(req, None)
             if h is None:
                 raise EngineError(f"request {req} completed without an owner")
-            self._complete(h)
-            landed.append(h)
-        for h in landed:
+            h.tokens = tuple(eng.request_tokens(h.req, h.length))
+            if self.request_log is not None and h.log is not None:
+                self.request_log.append(h.log + (h.tokens,))
             if h.on_complete is not None:
                 h.on_complete(h)
+            eng.request_release(h.req)
+            self._release(h)
         return occupancy
 
     def close(self) -> None:
@@ -481,37 +483,39 @@ class AsyncDeviceEngine:
             self.backend._async_engines.remove(self)
 
 
-class TwoStreamAsyncEngine:
-    """Fast ECoT async as two CUDA streams (north_star item 4).
+class BackgroundAsyncEngine:
+    """Fast ECoT async with the reasoning refresh running in the background
+    (north_star item 4; reference `ParallelAsyncRunner`, Alg. 1).
 
-    The action request of each control step decodes on lane 0 (highest stream
-    priority) against the last committed reasoning; reasoning-refresh requests
-    decode on lane 1 (lowest priority), driven by a background host thread
-    that keeps ticking across control steps.  A request's content is fixed at
-    issue (the snapshot it was prepared against, `schedulers.py:471-492`); it
-    lands into the cache -- through the reference runner's own `on_complete`
-    (`cache.write`, `schedulers.py:485-486`) -- at the control timestep
-    current when it completes.  Landing order is real-time, so traces are
-    checked per request (identical (context, prefix, step) -> identical
-    tokens) rather than byte for byte against the simulated clock."""
+    A host thread ticks the device batcher whenever anything is in flight, so
+    reasoning requests keep decoding between and during control steps.  The
+    action of a control step is a high-priority request on the same batcher:
+    it is admitted ahead of queued reasoning (the reference's admission,
+    `schedulers.py:263-273`) and decodes in the same ticks as the in-flight
+    reasoning rows.  A decode tick streams every weight once whatever its row
+    count, so merging costs the action nothing, whereas a second stream with
+    its own ticks would stream the weights twice (measured in round 1: the
+    two-lane variant's action p50 was 11 % above lockstep).
+    Requests land through the reference runner's own `on_complete`
+    (`cache.write`, `schedulers.py:485-486`) at the control timestep current
+    when they complete; landing order is real-time, so parity is checked per
+    request (identical (context, prefix, step) -> identical tokens)."""
 
     def __init__(self, backend: EngineBackend, slots: int):
         self.backend = backend
-        eng = backend.engine
-        eng.set_slots(slots)
-        eng.set_slots_lane(1, slots)
+        backend.engine.set_slots(slots)
         backend._slots = slots
         backend._fixed_slots = True
-        self._lock = threading.Lock()
-        self._cv = threading.Condition(self._lock)
-        self._inflight: dict[int, tuple[DeviceRequest, object]] = {}   # lane-1 id -> (handle, request)
+        self._cv = threading.Condition()
+        self._inflight: dict[int, tuple[DeviceRequest, object]] = {}   # device id -> (handle, request)
         self._landing: set[str] = set()   # completed, on_complete still running
-        self._lane0: dict[int, tuple[DeviceRequest, object]] = {}
+        self._landed: list = []
+        self._ticks = 0
+        self._last_occ = 0
         self._now = 0
         self._errors: list[BaseException] = []
-        self._stop = threading.Event()
-        self._work = threading.Event()
-        self._thread = threading.Thread(target=self._loop, name="fastecot-reasoning-lane", daemon=True)
+        self._stop = False
+        self._thread = threading.Thread(target=self._loop, name="fastecot-background-ticker", daemon=True)
         self._thread.start()
         backend._async_engines.append(self)
 
@@ -521,127 +525,104 @@ class TwoStreamAsyncEngine:
         h = device_handle(req.tokens)
         if h is None:
             raise EngineError(f"request {req.name!r} was not issued by this engine's backend")
-        prio = _device_priority(req.priority)
         with be._lock:
             be._materialize()        # every request issued so far: one trunk prefill, longest first
             if h in be._pending:
                 be._pending.remove(h)
-            h.priority = prio
-            lane = 0 if prio == PRIO_ACTION else 1
-            if lane == 1:
-                h.waiter = self
-                with self._lock:   # registered before the background lane can complete it
-                    be._submit(h, 1)
-                    if h.error is None:
-                        self._inflight[h.req] = (h, req)
-            else:
-                be._submit(h, 0)
-                if h.error is None:
-                    self._lane0[h.req] = (h, req)
-                    h.on_complete = self._landed0
+            h.priority = _device_priority(req.priority)
+            be._submit(h, 0)
+            if h.error is None:
+                h.on_complete = self._on_device_complete
+                with self._cv:
+                    self._inflight[h.req] = (h, req)
+                    self._cv.notify_all()
         if h.error is not None:
             raise EngineError(f"request {req.name!r} rejected: {h.error}") from h.error
-        if lane == 1:
-            self._work.set()
+
+    def _on_device_complete(self, h: DeviceRequest) -> None:   # under the backend lock
+        with self._cv:
+            _, req = self._inflight.pop(h.req)
+            self._landing.add(req.name)
+            self._landed.append(req)
 
     def in_flight_names(self) -> set[str]:
-        with self._lock:
+        with self._cv:
             names = {r.name for _, r in self._inflight.values()}
             names.update(self._landing)
-        names.update(r.name for _, r in self._lane0.values())
         return names
 
     def idle(self) -> bool:
-        with self._lock:
-            return not self._inflight and not self._landing and not self._lane0
-
-    def _landed0(self, h: DeviceRequest) -> None:
-        self._completed.append(self._lane0.pop(h.req)[1])
+        with self._cv:
+            return not self._inflight and not self._landing
 
     def tick(self, timestep: int) -> tuple[int, list]:
-        """One lane-0 decode iteration (the action lane)."""
+        """Wait for the background ticker's next decode iteration (returns its
+        occupancy); completions have already landed through their callbacks."""
         self._raise_background_error()
         self._now = timestep
-        be = self.backend
-        with be._lock:
-            self._completed = []
-            occ = be._run(-1, max_ticks=1)
-            completed, self._completed = self._completed, []
-        for req in completed:
-            req.remaining = 0
-            if req.on_complete is not None:
-                req.on_complete(req, timestep)
-        return (occ[0] if occ else 0), completed
+        with self._cv:
+            start = self._ticks
+            while self._ticks == start and (self._inflight or self._landing) and not self._errors:
+                self._cv.wait(1.0)
+            occ = self._last_occ if self._ticks != start else 0
+        self._raise_background_error()
+        return occ, []
 
     def set_timestep(self, timestep: int) -> None:
         self._now = timestep
 
-    # -- background lane --------------------------------------------------------
+    # -- background ticker ---------------------------------------------------------
     def _loop(self) -> None:
         be = self.backend
-        eng = be.engine
-        while not self._stop.is_set():
-            with self._lock:
-                busy = bool(self._inflight)
-            if not busy:
-                self._work.wait(0.05)
-                self._work.clear()
-                continue
+        while True:
+            with self._cv:
+                while not self._inflight and not self._stop:
+                    self._cv.wait(0.05)
+                if self._stop:
+                    return
             try:
-                _, done = eng.run(-1, lane=1, max_ticks=4)
-                for req_id, _tick in done:
-                    # the name stays visible to in_flight_names() until the
-                    # landing (cache write) has happened
-                    with self._lock:
-                        h, req = self._inflight.pop(req_id)
-                        self._landing.add(req.name)
+                with be._lock:   # one tick at a time; the runner's prefill / forks interleave between ticks
+                    occ = be._run(-1, max_ticks=1)
+                with self._cv:
+                    landed, self._landed = self._landed, []
+                for req in landed:
                     try:
-                        with be._lock:
-                            be._complete(h, lane=1)
-                        with self._lock:
-                            self._cv.notify_all()
                         req.remaining = 0
                         if req.on_complete is not None:
                             req.on_complete(req, self._now)
                     finally:
-                        with self._lock:
+                        with self._cv:
                             self._landing.discard(req.name)
-            except BaseException as exc:  # surfaced on the runner thread
-                self._errors.append(exc)
-                self._stop.set()
-                with self._lock:
+                with self._cv:
+                    self._ticks += 1
+                    self._last_occ = occ[0] if occ else 0
                     self._cv.notify_all()
+            except BaseException as exc:  # surfaced on the runner thread
+                with self._cv:
+                    self._errors.append(exc)
+                    self._stop = True
+                    self._cv.notify_all()
+                return
 
-    def wait_for(self, h: DeviceRequest, timeout: float = 600.0) -> None:
-        """Block until a lane-1 request has completed."""
-        with self._lock:
-            end = time.monotonic() + timeout
-            while h.tokens is None:
-                if self._errors:
-                    break
-                if not self._cv.wait(timeout=max(0.0, end - time.monotonic())):
-                    break
-        self._raise_background_error()
-        if h.tokens is None:
-            raise EngineError(f"lane-1 request {h.name!r} did not complete")
+    def wait_for(self, h: DeviceRequest) -> None:
+        self.backend._resolve(h)
 
     def _raise_background_error(self) -> None:
         if self._errors:
-            raise EngineError(f"background reasoning lane failed: {self._errors[0]!r}")
+            raise EngineError(f"background decode ticker failed: {self._errors[0]!r}")
 
-    def drain(self, timeout: float = 60.0) -> None:
-        """Wait until every background request has landed."""
-        t0 = time.time()
-        while not self.idle() and time.time() - t0 < timeout:
-            self._raise_background_error()
-            if self._lane0:
-                self.tick(self._now)
-            else:
-                time.sleep(0.002)
+    def drain(self, timeout: float = 120.0) -> None:
+        """Wait until every in-flight request has landed."""
+        end = time.monotonic() + timeout
+        with self._cv:
+            while (self._inflight or self._landing) and not self._errors and time.monotonic() < end:
+                self._cv.wait(0.05)
+        self._raise_background_error()
 
     def close(self) -> None:
-        self._stop.set()
-        self._work.set()
+        with self._cv:
+            self._stop = True
+            self._cv.notify_all()
         self._thread.join(timeout=10.0)
         if self in self.backend._async_engines:
             self.backend._async_engines.remove(self)

@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import hashlib
 import threading
+import time
 
 import numpy as np
 
@@ -57,6 +58,7 @@ class FakeEngine:
         self.prefill_calls = 0
         self.on_release = None                          # hook run inside request_release
         self.pages_total = 1 << 20
+        self.tick_delay = 0.0
 
     # sequences
     def seq_create(self) -> int:
@@ -150,6 +152,8 @@ class FakeEngine:
                 if max_ticks and len(occ) >= max_ticks:
                     break
                 o, d = self._tick(lane)
+            if self.tick_delay:
+                time.sleep(self.tick_delay)   # a device tick takes time (background-ticker tests)
             occ.append(o)
             done.extend((r, len(occ) - 1) for r in d)
         return occ, done

@@ -38,6 +38,8 @@ pytestmark = pytest.mark.gpu
 # bounds (set from the measured values below with margin)
 TF_LOGIT_RTOL = 3e-2        # max |dlogit| / max |logit| over the stored columns
 TF_ARGMAX_MIN = 0.85        # teacher-forced greedy agreement, all positions
+TF_EPISODE_MIN = 0.90       # teacher-forced agreement over every golden-episode position
+FREE_RUN_MIN = 0.04         # free-running whole-episode token match (chaotic after the first near-tie)
 RESULTS: dict = {}
 
 
@@ -127,13 +129,17 @@ def test_bf16_teacher_forced_vs_fp32_oracle(config, path):
 
 
 def _token_match(got_lines, want_lines):
+    """(matching tokens, total tokens, first-divergence index per request)."""
     same = total = 0
+    first_div = []
     for a, b in zip(got_lines, want_lines):
         ja, jb = json.loads(a), json.loads(b)
         for sa, sb in zip(ja["steps"], jb["steps"]):
             total += len(sb["tokens"])
-            same += sum(x == y for x, y in zip(sa["tokens"], sb["tokens"]))
-    return same, total
+            eq = [x == y for x, y in zip(sa["tokens"], sb["tokens"])]
+            same += sum(eq)
+            first_div.append(eq.index(False) if False in eq else len(eq))
+    return same, total, first_div
 
 
 def _traces():
@@ -143,14 +149,89 @@ def _traces():
     return json.loads(p.read_text())
 
 
+def _golden_requests(g):
+    """Every request of the golden episodes, rebuilt the way the reference
+    runners issued it: (framed ids, vision seed, oracle tokens).  t = 0 is
+    the sequential warm-up (prefix = this timestep's earlier steps,
+    schedulers.py:329-351); t >= 1 are Fast-ECoT branches (prefix = the
+    previous trace's earlier steps, schedulers.py:399-404)."""
+    from ecot_sched.backends import SyntheticBackend, default_profile, stable_digest
+
+    from oracle.backend import frame
+    enc = SyntheticBackend(default_profile(0))
+    out = []
+    for seed, lines in g["episodes"].items():
+        traces = [json.loads(l) for l in lines]
+        for t, tr in enumerate(traces):
+            obs = RS.observation_for(int(seed), t)
+            ctx = enc.encode("pick up the object and place it on the target", obs)
+            src = tr if t == 0 else traces[t - 1]
+            prefix = []
+            for i, st in enumerate(tr["steps"]):
+                out.append((frame(g["config"], ctx.encoded, prefix, st["name"]), stable_digest("vision", obs),
+                            st["tokens"]))
+                prefix = prefix + src["steps"][i]["tokens"]
+    return out
+
+
+def _teacher_force_all(eng, reqs, max_rows):
+    """Greedy token at every position of every request given the oracle's
+    own prefix: the positions of a request are forked off one trunk and
+    decoded as one-token branches, `max_rows` per tick."""
+    agree = total = 0
+    for ids, vseed, toks in reqs:
+        full = list(ids) + list(toks)
+        n0 = len(ids) - 1
+        trunk = eng.seq_create()
+        eng.prefill(trunk, full[: n0 + len(toks) - 1], vseed, M.VIS_ID)
+        for c0 in range(0, len(toks), max_rows):
+            pos = range(c0, min(len(toks), c0 + max_rows))
+            forks = [eng.seq_fork(trunk, n0 + i) for i in pos]
+            reqs_ = [eng.submit(b, full[n0 + i], 1, 1) for b, i in zip(forks, pos)]
+            eng.set_slots(max(8, len(reqs_)))
+            eng.run(-1)
+            for r, i in zip(reqs_, pos):
+                agree += eng.request_tokens(r, 1)[0] == toks[i]
+                total += 1
+                eng.request_release(r)
+            for b in forks:
+                eng.seq_free(b)
+        eng.seq_free(trunk)
+    return agree, total
+
+
+@pytest.mark.parametrize("path", ["tick", "chain"])
+def test_bf16_teacher_forced_golden_episodes(path):
+    """bf16 token-match rate, teacher-forced, over every token of the golden
+    7b_2layer episodes (~3k positions): the tick kernel (16 rows per tick)
+    and the kernel chain (a request's positions in one wide tick)."""
+    g = _traces()
+    reqs = _golden_requests(g)
+    eng = Engine("7b_2layer", dtype="bf16", seed=0, kv_pages=1024, max_rows=512)
+    try:
+        eng.set_option("mk", 1 if path == "tick" else 0)
+        agree, total = _teacher_force_all(eng, reqs, 16 if path == "tick" else 128)
+    finally:
+        eng.close()
+    rate = agree / total
+    _record(f"teacher_forced_7b_2layer_episodes_{path}", {"positions": total, "argmax_agreement": rate})
+    print("bf16 teacher-forced token-match", path, rate, total)
+    assert rate >= TF_EPISODE_MIN, rate
+
+
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
 def test_7b_2layer_episodes_vs_oracle_traces(schema, dtype):
     """Reference `run_episode` (parallel_sync) over the engine vs the reference
-    runners over the fp32 oracle: fp32 bit-exact; bf16 token-match rate."""
+    runners over the fp32 oracle: fp32 bit-exact; bf16 free-running
+    token-match rate (greedy decode of a random-init model diverges at the
+    first near-tie and never re-converges, so this rate is dominated by where
+    the first divergence falls; the teacher-forced rate above is the
+    per-position agreement)."""
     from ecot_sched.trace import trace_content_bytes
     g = _traces()
     be = EngineBackend("7b_2layer", dtype=dtype, seed=0, kv_pages=1024)
     same = total = 0
+    first = []
     try:
         for seed, want in g["episodes"].items():
             res, _ = ecot_sched.run_episode(RS.SchedulerConfig(mode="parallel_sync", slots=8), g["T"], be,
@@ -158,15 +239,17 @@ def test_7b_2layer_episodes_vs_oracle_traces(schema, dtype):
             got = [trace_content_bytes(r.trace, schema).decode() for r in res]
             if dtype == "f32":
                 assert got == want, seed
-            s, t = _token_match(got, want)
-            same, total = same + s, total + t
+            s, t, fd = _token_match(got, want)
+            same, total, first = same + s, total + t, first + fd
     finally:
         be.close()
     if dtype == "bf16":
         rate = same / total
-        _record("free_running_7b_2layer_episodes", {"tokens": total, "match_rate": rate, "rows_per_tick": "<= 7"})
-        print("bf16 free-running token-match rate", rate, total)
-        assert rate > 0.25
+        _record("free_running_7b_2layer_episodes", {"tokens": total, "match_rate": rate, "rows_per_tick": "<= 7",
+                                                      "median_first_divergence": float(np.median(first)),
+                                                      "requests": len(first)})
+        print("bf16 free-running token-match rate", rate, total, "median first divergence", np.median(first))
+        assert rate >= FREE_RUN_MIN
 
 
 def test_7b_2layer_batched_episodes_wide_rows_vs_oracle_traces(schema):
@@ -182,11 +265,13 @@ def test_7b_2layer_batched_episodes_wide_rows_vs_oracle_traces(schema):
     finally:
         be.close()
     same = total = 0
+    first = []
     for e, seed in enumerate(seeds):
         got = [trace_content_bytes(steps[t][e].trace, schema).decode() for t in range(g["T"])]
-        s, t = _token_match(got, g["episodes"][seed])
-        same, total = same + s, total + t
+        s, t, fd = _token_match(got, g["episodes"][seed])
+        same, total, first = same + s, total + t, first + fd
     rate = same / total
-    _record("free_running_7b_2layer_batched", {"tokens": total, "match_rate": rate, "rows_per_tick": len(seeds) * 7})
+    _record("free_running_7b_2layer_batched", {"tokens": total, "match_rate": rate, "rows_per_tick": len(seeds) * 7,
+                                               "median_first_divergence": float(np.median(first))})
     print("bf16 batched free-running token-match rate", rate, total)
-    assert rate > 0.25
+    assert rate >= FREE_RUN_MIN

@@ -363,25 +363,40 @@ def test_bf16_wide_batch_decode_runs(schema):
     assert all(len(r.trace.steps) == len(schema.steps) for step in res for r in step)
 
 
-def test_two_stream_async_per_request_parity(schema):
-    """Two-stream async (action on the high-priority lane, reasoning refresh on
-    the low-priority lane in a background thread): landing order is real-time,
-    so parity is per request -- every request's tokens equal the CPU oracle's
-    greedy decode of the same framed (context, prefix, step)."""
+def test_background_async_per_request_parity_and_coherence(schema):
+    """Background-ticker async (reasoning refresh decoding between and during
+    control steps, the action merged into its ticks at high priority) under
+    the reference runner: landing order is real-time, so parity is per request
+    -- every request's tokens equal the CPU oracle's greedy decode of the same
+    framed (context, prefix, step) -- and every snapshot the runner took was an
+    atomic cache state (recorder audit, reference tests/test_schedulers.py:397-429)."""
     import time
     from oracle.backend import OracleModel, frame
     log = []
-    be = EngineBackend("tiny", dtype="f32", seed=0, kv_pages=2048, async_streams=2, request_log=log)
+    be = EngineBackend("tiny", dtype="f32", seed=0, kv_pages=2048, async_mode="background", request_log=log)
+    registry, torn = {}, []
     try:
         runner = RS.make_runner(RS.SchedulerConfig(mode="parallel_async", slots=8, wall_clock=True), be, schema)
+        runner.cache.recorder = lambda v, fp: registry.__setitem__(v, fp)
+        snapshot = runner.cache.snapshot
+
+        def audited():
+            snap = snapshot()
+            if snap.version and RS.snapshot_fingerprint(snap.steps) != registry.get(snap.version):
+                torn.append(snap.version)
+            return snap
+
+        runner.cache.snapshot = audited
         results = []
         for t in range(8):
             ctx = be.encode("pick up the object and place it on the target", RS.observation_for(0, t))
             results.append(runner.step(ctx, t))
-            time.sleep(0.01)  # paced control loop: the reasoning lane keeps running in between
+            time.sleep(0.01)  # paced control loop: the reasoning refresh keeps decoding in between
         runner.engine.drain()
+        runner.close()
     finally:
         be.close()
+    assert torn == []
     assert all(len(r.trace.steps) == len(schema.steps) for r in results)
     assert len(log) >= 7 + 7  # warm-up chain + at least one action per step
     model = OracleModel("tiny", seed=0)
@@ -421,11 +436,11 @@ def test_engine_shared_by_lockstep_then_two_stream_backends(schema):
             asy.step(be.encode("pick up the object", RS.observation_for(1, t)), t)
         asy.engine.drain()
         assert be.engine.in_flight() == 0
-        be2 = EngineBackend("tiny", dtype="f32", seed=0, engine=be.engine, async_streams=2)
+        be2 = EngineBackend("tiny", dtype="f32", seed=0, engine=be.engine, async_mode="background")
         asy2 = RS.make_runner(RS.SchedulerConfig(mode="parallel_async", slots=8, wall_clock=True), be2, schema)
         res = [asy2.step(be2.encode("pick up the object", RS.observation_for(2, t)), t) for t in range(3)]
         asy2.engine.drain()
-        asy2.engine.close()
+        asy2.close()
     finally:
         be.close()
     assert all(len(r.trace.steps) == len(schema.steps) for r in res)
