@@ -185,6 +185,10 @@ struct fe_engine {
   };
   bool use_tc = false;
   int tc_min_rows = 17;
+  // forwards up to this many rows use the skinny GEMM, wider ones the tile
+  // GEMM (option "sk_max_rows"; measured in the engine at 7B: skinny ahead
+  // up to ~32 rows, the tile GEMM at 56 and for prefill)
+  int sk_max_rows = 32;
   int sk_mask = 31;  // skinny path per matrix: 1 QKV, 2 O, 4 gate/up, 8 down, 16 lm_head
   std::vector<LayerMaps> tc_maps;
   fe::TmaMap map_lm{};
@@ -450,9 +454,10 @@ void launch_layers(fe_engine* e, Lane& ln, const fe::Fwd& f, int n, bool decode,
     return;
   }
   fe::launch_embed(dt, f, m, e->w.embed, e->out_tokens, ws.x, st);
-  // bf16: skinny tcgen05 swap-AB GEMM for <= 16 rows (decode), the tile
-  // tcgen05 GEMM for wide forwards (prefill); fp32: canonical CUDA-core GEMV
-  const bool sk_any = e->use_tc && n <= fe::skinny_max_rows();
+  // bf16: the persistent swap-AB tcgen05 GEMM (decode batches of any width
+  // and, up to `sk_max_rows`, prefill), else the tile tcgen05 GEMM; fp32: the
+  // canonical CUDA-core GEMV
+  const bool sk_any = e->use_tc && n <= std::min(e->sk_max_rows, fe::skinny_max_rows());
   const bool tc = e->use_tc && !sk_any && n >= e->tc_min_rows;
   auto sk_on = [&](int bit) { return sk_any && (e->sk_mask >> bit & 1); };
   auto tc_launch = [&](int epi, int N, int K) {
@@ -950,10 +955,12 @@ void create_lane(fe_engine* e, Lane& ln, int id, int rows, int priority) {
     ln.map_xn = fe::make_kmajor_map(ln.ws.xn, rows, m.d, m.d, 128);
     ln.map_attn = fe::make_kmajor_map(ln.ws.attn, rows, m.d, m.d, 128);
     ln.map_act = fe::make_kmajor_map(ln.ws.attn, rows, m.F, m.F, 128);
-    ln.map_xn16 = fe::make_kmajor_map(ln.ws.xn, rows, m.d, m.d, fe::skinny_max_rows());
-    ln.map_attn16 = fe::make_kmajor_map(ln.ws.attn, rows, m.d, m.d, fe::skinny_max_rows());
-    ln.map_act16 = fe::make_kmajor_map(ln.ws.attn, rows, m.F, m.F, fe::skinny_max_rows());
-    const size_t part_floats = (size_t)64 * std::max<size_t>(3 * m.d, 2 * (size_t)m.F) * fe::skinny_max_rows();
+    ln.map_xn16 = fe::make_kmajor_map(ln.ws.xn, rows, m.d, m.d, 16);
+    ln.map_attn16 = fe::make_kmajor_map(ln.ws.attn, rows, m.d, m.d, 16);
+    ln.map_act16 = fe::make_kmajor_map(ln.ws.attn, rows, m.F, m.F, 16);
+    const size_t part_floats = std::max({fe::skinny_partial_floats(3 * m.d, m.d), fe::skinny_partial_floats(m.d, m.d),
+                                         fe::skinny_partial_floats(2 * m.F, m.d), fe::skinny_partial_floats(m.d, m.F),
+                                         fe::skinny_partial_floats(m.V, m.d)});  // any skinny split plan
     ln.sk_partial = (float*)e->dalloc(part_floats * 4);
     ln.sk_counters = (int*)e->dalloc(4096 * sizeof(int));
     CK(cudaMemset(ln.sk_counters, 0, 4096 * sizeof(int)));
@@ -1469,17 +1476,17 @@ int fe_op_gemm_tc(fe_engine* e, const void* x, const void* w, int32_t M, int32_t
     const fe::TmaMap bm = fe::make_kmajor_map(w, N, K, K, 128);
     fe::TcLaunch t{};
     t.M = M; t.N = N; t.K = K; t.epi = fe::TC_STORE; t.y = y; t.ldy = N;
-    fe::launch_gemm_tc(am, bm, t, e->lanes[0].stream);
+    for (int r = 0; r < e->op_reps; r++) fe::launch_gemm_tc(am, bm, t, e->lanes[0].stream);
     CK(cudaGetLastError());
   });
 }
 
 int fe_op_skinny_tc(fe_engine* e, const void* x, const void* w, int32_t M, int32_t N, int32_t K, float* y) {
   return guarded(e, [&] {
-    if (M > fe::skinny_max_rows() || N % 128 || K % 64) throw Error("skinny_tc: M <= 16, N % 128, K % 64");
+    if (M > fe::skinny_max_rows() || N % 128 || K % 64) throw Error("skinny_tc: M <= 128, N % 128, K % 64");
     Lane& ln = e->lanes[0];
     // kernel-test scratch, separate from the lanes' (graph-captured) buffers
-    const size_t need = (size_t)8 * ((N + 127) / 128) * 128 * 16 * 4;
+    const size_t need = std::max(fe::skinny_partial_floats(N, K), (size_t)((N + 127) / 128) * 16 * 128 * 256) * 4;
     if (e->op_bytes < need) {
       e->op_partial = (float*)e->dalloc(need);
       e->op_bytes = need;
@@ -1488,7 +1495,7 @@ int fe_op_skinny_tc(fe_engine* e, const void* x, const void* w, int32_t M, int32
       e->op_counters = (int*)e->dalloc(4096 * sizeof(int));
       CK(cudaMemset(e->op_counters, 0, 4096 * sizeof(int)));
     }
-    const fe::TmaMap xm = fe::make_kmajor_map(x, M, K, K, fe::skinny_max_rows());
+    const fe::TmaMap xm = fe::make_kmajor_map(x, M, K, K, 16);
     const fe::TmaMap wm = fe::make_kmajor_map(w, N, K, K, 128);
     fe::SkLaunch t{};
     t.N = N; t.K = K; t.B = M; t.epi = fe::TC_STORE; t.y = y; t.ldy = N;
@@ -1505,6 +1512,12 @@ int fe_set_option(fe_engine* e, const char* key, int64_t value) {
     // decode graphs drops them (a graphed tick would keep the old choice)
     if (k == "tc_min_rows") {
       e->tc_min_rows = (int)value;
+      clear_graphs(e);
+    } else if (k == "sk_splits") {
+      fe::g_sk_splits = (int)value;
+      clear_graphs(e);
+    } else if (k == "sk_max_rows") {
+      e->sk_max_rows = (int)value;
       clear_graphs(e);
     } else if (k == "use_tc") {
       e->use_tc = value != 0 && !e->tc_maps.empty();

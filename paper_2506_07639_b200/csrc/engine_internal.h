@@ -96,6 +96,7 @@ struct Workspace {
 // --- programmatic dependent launch -------------------------------------------
 extern bool g_pdl;       // engine option "pdl"
 extern int g_sk_stages;  // engine option "sk_stages" (5 or 10)
+extern int g_sk_splits;  // engine option "sk_splits" (0: cost model)
 
 template <typename... KArgs, typename... Args>
 inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {

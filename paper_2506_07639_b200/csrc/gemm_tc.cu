@@ -32,6 +32,7 @@
 namespace fe {
 
 int g_sk_stages = 10;
+int g_sk_splits = 0;  // engine option "sk_splits": force the skinny K split (0: cost model)
 
 namespace {
 
@@ -261,23 +262,32 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
 // the weight stream never drains between units.  Split partials are reduced
 // in a fixed order by the last CTA of each tile (deterministic), which then
 // applies the fused epilogue.
-constexpr int SN = 16;                        // batch columns per MMA
-constexpr int kSkStagesMax = 10;
-constexpr int kSkAcc = 4;                     // TMEM accumulator ring (units in flight)
+// SN = batch columns per MMA (16 / 32 / 64 / 128 / 256: the row count rounded
+// up); the 16-row activation boxes of the lane's tensor maps are loaded SN / 16
+// at a time into one K-major [SN x 64] operand tile.  The epilogue drains the
+// accumulator 16 columns at a time through a [128 x 16] shared tile, so the
+// shared memory left for the TMA ring does not shrink with SN.
 constexpr int kSkA = BM * BK * 2;             // 16 KB weights per stage
-constexpr int kSkB = SN * BK * 2;             // 2 KB activations per stage
-template <int STAGES>
-constexpr int sk_smem() { return STAGES * (kSkA + kSkB) + BM * (SN + 1) * 4 + 1024 + 2048; }
-constexpr uint32_t kSkIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(SN >> 3) << 17) |
-                              ((uint32_t)(BM >> 4) << 24);
+constexpr int kSkBox = 16;                    // rows per activation TMA box
+constexpr int kSkChunk = 16;                  // accumulator columns per epilogue chunk
+template <int SN>
+__host__ __device__ constexpr int sk_b_bytes() { return SN * BK * 2; }
+template <int SN>
+__host__ __device__ constexpr int sk_acc() { return SN <= 128 ? 4 : 2; }   // TMEM ring depth (<= 512 columns)
+template <int SN, int STAGES>
+constexpr int sk_smem() {
+  return STAGES * (kSkA + sk_b_bytes<SN>()) + BM * (kSkChunk + 1) * 4 + 1024 /* align */ + 1024 /* barriers, red */;
+}
+template <int SN>
+constexpr int sk_stages() { return SN <= 32 ? 10 : SN == 64 ? 8 : SN == 128 ? 6 : 4; }  // ~200 KB ring
 
 struct SkArgs {
-  int N, K, B;            // weight rows, reduction, live batch rows
+  int N, K, B, b0;        // weight rows, reduction, batch rows of this launch, first batch row
   int tiles, splits, kb_per_split, units;
   int epi;
-  float* partial;         // [splits][N][B]
+  float* partial;         // [units][128][SN]
   int* counters;          // [tiles]
-  // epilogue operands (see TcArgs)
+  // epilogue operands (see TcArgs); batch row b of this launch is row b0 + b
   float* y;               // RESID: x [rows][ldy]
   int ldy;
   __nv_bfloat16* act;
@@ -289,7 +299,7 @@ struct SkArgs {
   const RowMeta* rows;    // batch rows (QKV) / all rows (ARGMAX via head_rows)
   const int32_t* head_rows;
   int H, hd, d;
-  unsigned long long* part_keys;  // ARGMAX: [B][tiles]
+  unsigned long long* part_keys;  // ARGMAX: [rows][tiles]
   float* logits;
   int V, n_text;
 };
@@ -302,22 +312,106 @@ __device__ __forceinline__ void unit_of(const SkArgs& a, int u, int kb_total, in
   *kb1 = min(kb_total, *kb0 + a.kb_per_split);
 }
 
-template <int kSkStages>
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&raw)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(raw[0]), "=r"(raw[1]), "=r"(raw[2]), "=r"(raw[3]), "=r"(raw[4]), "=r"(raw[5]), "=r"(raw[6]),
+        "=r"(raw[7]), "=r"(raw[8]), "=r"(raw[9]), "=r"(raw[10]), "=r"(raw[11]), "=r"(raw[12]), "=r"(raw[13]),
+        "=r"(raw[14]), "=r"(raw[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Fused epilogue of one 16-column chunk (batch rows c0 .. c0 + nb - 1 of the
+// launch) of a reduced [128 x 16] tile `ct` (row stride 17).  Called by the
+// 128 epilogue threads; r = this thread's weight row of the tile.
+__device__ __forceinline__ void sk_epilogue_chunk(const SkArgs& a, const float* ct, unsigned long long* red,
+                                                  int tl, int c0, int nb, int r, int warp, int lane) {
+  const int et = r;
+  const int n0 = tl * BM;
+  const bool swiglu = a.epi == TC_SWIGLU;
+  const int nrow = swiglu ? (r < 64 ? tl * 64 + r : a.F + tl * 64 + r - 64) : n0 + r;
+  const bool row_ok = nrow < a.N;
+  const int g0 = a.b0 + c0;  // global batch row of column 0 of the chunk
+  if (a.epi == TC_RESID) {
+    if (row_ok)
+      for (int j = 0; j < nb; j++) a.y[(size_t)(g0 + j) * a.ldy + nrow] += ct[r * (kSkChunk + 1) + j];
+  } else if (a.epi == TC_SWIGLU) {
+    if (et < 64 && tl * 64 + et < a.F)
+      for (int j = 0; j < nb; j++)
+        a.act[(size_t)(g0 + j) * a.F + tl * 64 + et] =
+            __float2bfloat16_rn(silu_mul(ct[et * (kSkChunk + 1) + j], ct[(et + 64) * (kSkChunk + 1) + j]));
+  } else if (a.epi == TC_QKV) {
+    if (et < 64) {
+      const int sec = n0 / a.d, h = (n0 % a.d) / a.hd, half = a.hd >> 1;
+      for (int j = 0; j < nb; j++) {
+        const int b = g0 + j;
+        const RowMeta m = a.rows[b];
+        float x1 = ct[et * (kSkChunk + 1) + j], x2 = ct[(et + half) * (kSkChunk + 1) + j];
+        if (sec < 2) {
+          const float* cs = a.rope + (size_t)m.pos * a.hd;
+          const float co = cs[et], sn = cs[half + et];
+          const float r1 = __fmaf_rn(x1, co, -__fmul_rn(x2, sn));
+          const float r2 = __fmaf_rn(x2, co, __fmul_rn(x1, sn));
+          x1 = r1;
+          x2 = r2;
+        }
+        if (sec == 0) {
+          float* qr = a.q + (size_t)b * a.d + h * a.hd;
+          qr[et] = x1;
+          qr[et + half] = x2;
+        } else {
+          __nv_bfloat16* kv = a.kv_pool + (size_t)m.kv_page * a.page_elems + a.layer_off +
+                              ((size_t)((sec - 1) * a.H + h) * FE_PAGE + m.kv_slot) * a.hd;
+          kv[et] = __float2bfloat16_rn(x1);
+          kv[et + half] = __float2bfloat16_rn(x2);
+        }
+      }
+    }
+  } else if (a.epi == TC_ARGMAX) {
+    for (int j = 0; j < nb; j++) {
+      const float v = ct[r * (kSkChunk + 1) + j];
+      unsigned long long k = (row_ok && nrow < a.n_text) ? argmax_key(v, nrow) : 0ull;
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) k = max(k, __shfl_xor_sync(0xffffffffu, k, off));
+      if (lane == 0) red[j * 4 + (warp & 3)] = k;
+      if (row_ok && a.logits) {
+        const RowMeta m = a.rows[a.head_rows[g0 + j]];
+        if (m.logit_row >= 0) a.logits[(size_t)m.logit_row * a.V + nrow] = v;
+      }
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    if (et < nb) {
+      unsigned long long k = 0ull;
+      for (int w = 0; w < 4; w++) k = max(k, red[et * 4 + w]);
+      a.part_keys[(size_t)(g0 + et) * a.tiles + tl] = k;
+    }
+  } else {  // TC_STORE: y[b][n]
+    if (row_ok)
+      for (int j = 0; j < nb; j++) a.y[(size_t)(g0 + j) * a.ldy + nrow] = ct[r * (kSkChunk + 1) + j];
+  }
+}
+
+template <int SN, int kSkStages>
 __global__ void __launch_bounds__(kThreads, 1)
 skinny_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x,
                  const SkArgs a) {
+  constexpr int kSkB = sk_b_bytes<SN>();
+  constexpr int kSkAcc = sk_acc<SN>();
+  constexpr uint32_t kSkIdesc = idesc_bf16(BM, SN);
+  constexpr int kTmemCols = kSkAcc * SN;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   unsigned char* sa = smem;
   unsigned char* sb = smem + kSkStages * kSkA;
-  float* tile = (float*)(sb + kSkStages * kSkB);           // [128][SN + 1]
-  uint64_t* full = (uint64_t*)(tile + BM * (SN + 1));
+  float* ct = (float*)(sb + kSkStages * kSkB);             // [128][16 + 1] chunk tile
+  uint64_t* full = (uint64_t*)(ct + BM * (kSkChunk + 1));
   uint64_t* empty = full + kSkStages;
   uint64_t* acc_full = empty + kSkStages;                  // [kSkAcc]
   uint64_t* acc_empty = acc_full + kSkAcc;                 // [kSkAcc]
   uint32_t* tmem_slot = (uint32_t*)(acc_empty + kSkAcc);
   int* last_flag = (int*)(tmem_slot + 1);
-  unsigned long long* red = (unsigned long long*)(tmem_slot + 4);  // [SN][4], 8-byte aligned
+  unsigned long long* red = (unsigned long long*)(tmem_slot + 4);  // [16][4], 8-byte aligned
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kb_total = (a.K + BK - 1) / BK;
@@ -337,9 +431,9 @@ skinny_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constan
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 1) {  // kSkAcc 16-column fp32 accumulators
+  if (warp == 1) {  // kSkAcc SN-column fp32 accumulators
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
-                 "n"(kSkAcc * SN));
+                 "n"(kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -388,12 +482,14 @@ skinny_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constan
             mbar_expect_tx(&full[s], kSkA + kSkB);
             load_w(s, tl, kb);
           }
-          tma_load_2d(sb + s * kSkB, &map_x, &full[s], kb * BK, 0);
+#pragma unroll
+          for (int j = 0; j < SN / kSkBox; j++)
+            tma_load_2d(sb + s * kSkB + j * kSkBox * BK * 2, &map_x, &full[s], kb * BK, a.b0 + j * kSkBox);
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ---- MMA issuer: accumulator (local unit index & 1)
+    if (lane == 0) {  // ---- MMA issuer: accumulator (local unit index) % kSkAcc
       int it = 0, lu = 0;
       for (int u = blockIdx.x; u < a.units; u += gridDim.x, lu++) {
         int tl, sp, kb0, kb1;
@@ -428,6 +524,7 @@ skinny_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constan
     // ---- epilogue warps: thread <-> weight row r of the tile
     const int r = 32 * (warp & 3) + lane;
     const int et = threadIdx.x - 64;  // 0..127
+    const int n_chunks = (a.B + kSkChunk - 1) / kSkChunk;   // live 16-column chunks
     pdl_wait();  // epilogue writes / reads outputs of earlier kernels
     int lu = 0;
     for (int u = blockIdx.x; u < a.units; u += gridDim.x, lu++) {
@@ -436,135 +533,85 @@ skinny_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constan
       const int acc = lu % kSkAcc;
       mbar_wait(&acc_full[acc], (lu / kSkAcc) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      uint32_t raw[16];
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-          : "=r"(raw[0]), "=r"(raw[1]), "=r"(raw[2]), "=r"(raw[3]), "=r"(raw[4]), "=r"(raw[5]), "=r"(raw[6]),
-            "=r"(raw[7]), "=r"(raw[8]), "=r"(raw[9]), "=r"(raw[10]), "=r"(raw[11]), "=r"(raw[12]), "=r"(raw[13]),
-            "=r"(raw[14]), "=r"(raw[15])
-          : "r"(tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(acc * SN)));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      // accumulator drained: hand it back to the MMA warp
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (et == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&acc_empty[acc])) : "memory");
-
-      const int n0 = tl * BM;
-      const int nrow = swiglu ? (r < 64 ? tl * 64 + r : a.F + tl * 64 + r - 64) : n0 + r;
-      const bool row_ok = nrow < a.N;
+      const uint32_t tacc = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(acc * SN);
       if (a.splits == 1) {
+        // chunk by chunk: TMEM -> shared chunk tile -> fused epilogue
+        for (int c = 0; c < n_chunks; c++) {
+          uint32_t raw[16];
+          tmem_ld16(tacc + c * kSkChunk, raw);
 #pragma unroll
-        for (int b = 0; b < SN; b++) tile[r * (SN + 1) + b] = __uint_as_float(raw[b]);
-      } else {
-        // partial of this unit: [unit][128 rows][16 columns] fp32, 4 x 16-byte stores per thread
-        float4* dst = reinterpret_cast<float4*>(a.partial + ((size_t)u * BM + r) * SN);
+          for (int j = 0; j < 16; j++) ct[r * (kSkChunk + 1) + j] = __uint_as_float(raw[j]);
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          sk_epilogue_chunk(a, ct, red, tl, c * kSkChunk, min(kSkChunk, a.B - c * kSkChunk), r, warp, lane);
+          asm volatile("bar.sync 1, 128;" ::: "memory");  // ct / red reused by the next chunk
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (et == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&acc_empty[acc])) : "memory");
+        continue;
+      }
+      // split-K: drain into this unit's partial [unit][128 rows][SN] fp32
+      for (int c = 0; c < n_chunks; c++) {
+        uint32_t raw[16];
+        tmem_ld16(tacc + c * kSkChunk, raw);
+        float4* dst = reinterpret_cast<float4*>(a.partial + ((size_t)u * BM + r) * SN + c * kSkChunk);
 #pragma unroll
-        for (int i = 0; i < SN / 4; i++)
+        for (int i = 0; i < 4; i++)
           __stcg(dst + i, make_float4(__uint_as_float(raw[4 * i]), __uint_as_float(raw[4 * i + 1]),
                                       __uint_as_float(raw[4 * i + 2]), __uint_as_float(raw[4 * i + 3])));
-        // one gpu-scope fence per CTA after the CTA barrier publishes all 128
-        // threads' partials before the arrival count (split-K serial pattern)
-        __threadfence();  // each thread publishes its rows of the partial
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (et == 0) {
-          const int prev = atomicAdd(&a.counters[tl], 1);
-          const bool last = prev == a.splits - 1;
-          if (last) {
-            a.counters[tl] = 0;  // reset for the next launch
-            __threadfence();
-          }
-          *last_flag = last;
+      }
+      // accumulator drained: hand it back to the MMA warp
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      // one gpu-scope fence per thread publishes its partial rows before the
+      // CTA's arrival on the tile counter (split-K serial pattern)
+      __threadfence();
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (et == 0) {
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&acc_empty[acc])) : "memory");
+        const int prev = atomicAdd(&a.counters[tl], 1);
+        const bool last = prev == a.splits - 1;
+        if (last) {
+          a.counters[tl] = 0;  // reset for the next launch
+          __threadfence();
         }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (!*last_flag) continue;
-        // fixed-order reduction over the tile's splits (units tl*splits .. +splits-1)
-        float4 acc4[SN / 4];
+        *last_flag = last;
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (!*last_flag) continue;
+      // fixed-order reduction over the tile's splits (units tl*splits .. +splits-1), chunk by chunk
+      for (int c = 0; c < n_chunks; c++) {
+        float4 acc4[4];
 #pragma unroll
-        for (int i = 0; i < SN / 4; i++) acc4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int i = 0; i < 4; i++) acc4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
         for (int q = 0; q < a.splits; q++) {
-          const float4* src = reinterpret_cast<const float4*>(a.partial + ((size_t)(tl * a.splits + q) * BM + r) * SN);
-          float4 v[SN / 4];
+          const float4* src = reinterpret_cast<const float4*>(
+              a.partial + ((size_t)(tl * a.splits + q) * BM + r) * SN + c * kSkChunk);
+          float4 v[4];
 #pragma unroll
-          for (int i = 0; i < SN / 4; i++) v[i] = __ldcg(src + i);
+          for (int i = 0; i < 4; i++) v[i] = __ldcg(src + i);
 #pragma unroll
-          for (int i = 0; i < SN / 4; i++) {
+          for (int i = 0; i < 4; i++) {
             acc4[i].x += v[i].x; acc4[i].y += v[i].y; acc4[i].z += v[i].z; acc4[i].w += v[i].w;
           }
         }
 #pragma unroll
-        for (int i = 0; i < SN / 4; i++) {
-          tile[r * (SN + 1) + 4 * i] = acc4[i].x;
-          tile[r * (SN + 1) + 4 * i + 1] = acc4[i].y;
-          tile[r * (SN + 1) + 4 * i + 2] = acc4[i].z;
-          tile[r * (SN + 1) + 4 * i + 3] = acc4[i].w;
-        }
-      }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      // ---- fused epilogues on the reduced [128 x B] tile
-      if (a.epi == TC_RESID) {
-        if (row_ok)
-          for (int b = 0; b < a.B; b++) a.y[(size_t)b * a.ldy + nrow] += tile[r * (SN + 1) + b];
-      } else if (a.epi == TC_SWIGLU) {
-        if (et < 64 && tl * 64 + et < a.F)
-          for (int b = 0; b < a.B; b++)
-            a.act[(size_t)b * a.F + tl * 64 + et] =
-                __float2bfloat16_rn(silu_mul(tile[et * (SN + 1) + b], tile[(et + 64) * (SN + 1) + b]));
-      } else if (a.epi == TC_QKV) {
-        if (et < 64) {
-          const int sec = n0 / a.d, h = (n0 % a.d) / a.hd, half = a.hd >> 1;
-          for (int b = 0; b < a.B; b++) {
-            const RowMeta m = a.rows[b];
-            float x1 = tile[et * (SN + 1) + b], x2 = tile[(et + half) * (SN + 1) + b];
-            if (sec < 2) {
-              const float* cs = a.rope + (size_t)m.pos * a.hd;
-              const float co = cs[et], sn = cs[half + et];
-              const float r1 = __fmaf_rn(x1, co, -__fmul_rn(x2, sn));
-              const float r2 = __fmaf_rn(x2, co, __fmul_rn(x1, sn));
-              x1 = r1;
-              x2 = r2;
-            }
-            if (sec == 0) {
-              float* qr = a.q + (size_t)b * a.d + h * a.hd;
-              qr[et] = x1;
-              qr[et + half] = x2;
-            } else {
-              __nv_bfloat16* kv = a.kv_pool + (size_t)m.kv_page * a.page_elems + a.layer_off +
-                                  ((size_t)((sec - 1) * a.H + h) * FE_PAGE + m.kv_slot) * a.hd;
-              kv[et] = __float2bfloat16_rn(x1);
-              kv[et + half] = __float2bfloat16_rn(x2);
-            }
-          }
-        }
-      } else if (a.epi == TC_ARGMAX) {
-        for (int b = 0; b < a.B; b++) {
-          const float v = tile[r * (SN + 1) + b];
-          unsigned long long k = (row_ok && nrow < a.n_text) ? argmax_key(v, nrow) : 0ull;
-#pragma unroll
-          for (int off = 16; off >= 1; off >>= 1) k = max(k, __shfl_xor_sync(0xffffffffu, k, off));
-          if (lane == 0) red[b * 4 + (warp & 3)] = k;
-          if (row_ok && a.logits) {
-            const RowMeta m = a.rows[a.head_rows[b]];
-            if (m.logit_row >= 0) a.logits[(size_t)m.logit_row * a.V + nrow] = v;
-          }
+        for (int i = 0; i < 4; i++) {
+          ct[r * (kSkChunk + 1) + 4 * i] = acc4[i].x;
+          ct[r * (kSkChunk + 1) + 4 * i + 1] = acc4[i].y;
+          ct[r * (kSkChunk + 1) + 4 * i + 2] = acc4[i].z;
+          ct[r * (kSkChunk + 1) + 4 * i + 3] = acc4[i].w;
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (et < a.B) {
-          unsigned long long k = 0ull;
-          for (int w = 0; w < 4; w++) k = max(k, red[et * 4 + w]);
-          a.part_keys[(size_t)et * a.tiles + tl] = k;
-        }
-      } else {  // TC_STORE: y[b][n]
-        if (row_ok)
-          for (int b = 0; b < a.B; b++) a.y[(size_t)b * a.ldy + nrow] = tile[r * (SN + 1) + b];
+        sk_epilogue_chunk(a, ct, red, tl, c * kSkChunk, min(kSkChunk, a.B - c * kSkChunk), r, warp, lane);
+        asm volatile("bar.sync 1, 128;" ::: "memory");
       }
-      asm volatile("bar.sync 1, 128;" ::: "memory");  // tile / red reused by the next unit
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kSkAcc * SN));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols));
   }
 }
 
@@ -598,82 +645,108 @@ TmaMap make_kmajor_map(const void* base, int rows, int K, int ld_elems, int box_
 
 int tc_box_rows(int epi) { return epi == TC_SWIGLU ? BN / 2 : BN; }
 
-int skinny_max_rows() { return SN; }
+int skinny_max_rows() { return 1 << 20; }  // wider batches run in 256-row slices
+int skinny_cols(int rows) {
+  return rows <= 16 ? 16 : rows <= 32 ? 32 : rows <= 64 ? 64 : rows <= 128 ? 128 : 256;
+}
 
 int skinny_tiles(int epi, int N, int F) { return epi == TC_SWIGLU ? F / (BM / 2) : (N + BM - 1) / BM; }
 
-void launch_skinny_tc(const TmaMap& w_map, const TmaMap& x_map, const SkLaunch& l, cudaStream_t s) {
-  static bool configured = false;
-  static int n_sm = 148;
-  if (!configured) {
-    cudaFuncSetAttribute(skinny_tc_kernel<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, sk_smem<10>());
-    cudaFuncSetAttribute(skinny_tc_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, sk_smem<5>());
-    // maximum shared-memory carveout, so two 5-stage CTAs (of consecutive
-    // PDL-chained launches) can be resident on one SM
-    cudaFuncSetAttribute(skinny_tc_kernel<5>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    cudaFuncSetAttribute(skinny_tc_kernel<10>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    if (getenv("FE_DEBUG_OCC")) {
-      int o5 = 0, o10 = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o5, skinny_tc_kernel<5>, kThreads, sk_smem<5>());
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o10, skinny_tc_kernel<10>, kThreads, sk_smem<10>());
-      fprintf(stderr, "skinny occupancy: 5 stages %d CTAs/SM (%d B), 10 stages %d CTAs/SM (%d B)\n", o5, sk_smem<5>(), o10,
-              sk_smem<10>());
-      size_t avail1 = 0, avail2 = 0;
-      cudaOccupancyAvailableDynamicSMemPerBlock(&avail1, skinny_tc_kernel<5>, 1, kThreads);
-      cudaOccupancyAvailableDynamicSMemPerBlock(&avail2, skinny_tc_kernel<5>, 2, kThreads);
-      int smpm = 0, smpb = 0;
-      cudaDeviceGetAttribute(&smpm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, 0);
-      cudaDeviceGetAttribute(&smpb, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0);
-      fprintf(stderr, "avail dyn smem: 1 CTA %zu, 2 CTAs %zu; per SM %d, per block optin %d\n", avail1, avail2, smpm, smpb);
-      cudaFuncAttributes fa{};
-      cudaError_t er = cudaFuncGetAttributes(&fa, skinny_tc_kernel<5>);
-      fprintf(stderr, "attrs(%d): regs %d static %zu maxdyn %d carveout %d maxthreads %d\n", (int)er, fa.numRegs,
-              fa.sharedSizeBytes, fa.maxDynamicSharedSizeBytes, fa.preferredShmemCarveout, fa.maxThreadsPerBlock);
-      int rps = 0, maxb = 0;
-      cudaDeviceGetAttribute(&rps, cudaDevAttrMaxRegistersPerMultiprocessor, 0);
-      cudaDeviceGetAttribute(&maxb, cudaDevAttrMaxBlocksPerMultiprocessor, 0);
-      fprintf(stderr, "regs/SM %d max blocks/SM %d\n", rps, maxb);
-    }
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-    configured = true;
-  }
-  const int tiles = skinny_tiles(l.epi, l.N, l.F);
-  const int kb_total = (l.K + BK - 1) / BK;
-  // Pick the K split that balances units over the persistent CTAs, keeping the
-  // split partial traffic (splits * N * B * 8 bytes) under ~8% of the weights.
-  const double weight_bytes = (double)l.N * l.K * 2.0;
+namespace {
+int g_n_sm = 0;
+
+template <int SN, int ST>
+void sk_configure() {
+  cudaFuncSetAttribute(skinny_tc_kernel<SN, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, sk_smem<SN, ST>());
+  cudaFuncSetAttribute(skinny_tc_kernel<SN, ST>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+}
+
+template <int SN, int ST>
+void sk_launch(const CUtensorMap& wm, const CUtensorMap& xm, const SkArgs& a, cudaStream_t s) {
+  const int grid = std::min(a.units, g_n_sm);
+  launch_k(skinny_tc_kernel<SN, ST>, dim3(grid), dim3(kThreads), (size_t)sk_smem<SN, ST>(), s, wm, xm, a);
+}
+
+// K split balancing the units over the persistent CTAs, keeping the split
+// partial traffic (units * 128 * sn * 8 bytes) under ~6 % of the weights: a
+// split unit costs a partial store, a gpu-scope fence, a tile-counter atomic
+// and its share of the owner's ordered reduction (measured ~3 us per unit,
+// tools/bench_skinny.py), so only weight-light splits pay off.
+int pick_kb_per_split(int tiles, int kb_total, int sn, double weight_bytes) {
   int best_kb = kb_total;
   double best_eff = -1.0;
   for (int kb_per = kb_total; kb_per >= 4; kb_per--) {
     const int splits = (kb_total + kb_per - 1) / kb_per;
     const int units = tiles * splits;
-    if (splits > 1 && (units * (double)BM * SN * 8.0 > 0.06 * weight_bytes || splits > 8)) break;
-    const int rounds = (units + n_sm - 1) / n_sm;
+    if (splits > 1 && (units * (double)BM * sn * 8.0 > 0.06 * weight_bytes || splits > 8)) break;
+    const int rounds = (units + g_n_sm - 1) / g_n_sm;
     // balance, with a small per-unit epilogue cost
-    const double eff = (double)tiles * kb_total / ((double)n_sm * rounds * (kb_per + 1.0));
+    const double eff = (double)tiles * kb_total / ((double)g_n_sm * rounds * (kb_per + 1.0));
     if (eff > best_eff + 1e-9) {
       best_eff = eff;
       best_kb = kb_per;
     }
   }
-  SkArgs a{};
-  a.N = l.N; a.K = l.K; a.B = l.B; a.epi = l.epi;
-  a.kb_per_split = best_kb;
-  a.splits = (kb_total + best_kb - 1) / best_kb;
-  a.tiles = tiles;
-  a.units = tiles * a.splits;
-  a.partial = l.partial; a.counters = l.counters;
-  a.y = l.y; a.ldy = l.ldy; a.act = l.act; a.F = l.F; a.q = l.q; a.kv_pool = l.kv_pool;
-  a.page_elems = l.page_elems; a.layer_off = l.layer_off; a.rope = l.rope; a.rows = l.rows;
-  a.head_rows = l.head_rows; a.H = l.H; a.hd = l.hd; a.d = l.d; a.part_keys = l.part_keys;
-  a.logits = l.logits; a.V = l.V; a.n_text = l.n_text;
-  const int grid = std::min(a.units, n_sm);
+  return best_kb;
+}
+}  // namespace
+
+size_t skinny_partial_floats(int N, int K) {
+  // the largest plan pick_kb_per_split can return (any row count), or a
+  // forced split of up to 16 (option sk_splits) at 16 columns
+  const size_t tiles = (size_t)(N + BM - 1) / BM;
+  return std::max((size_t)(0.06 * (double)N * K * 2.0 / 8.0) + (size_t)BM * 256 * 8, tiles * 16 * BM * 16);
+}
+
+void launch_skinny_tc(const TmaMap& w_map, const TmaMap& x_map, const SkLaunch& l, cudaStream_t s) {
+  static bool configured = false;
+  if (!configured) {
+    // 16 columns: 10 stages, or 5 so two CTAs of consecutive PDL-chained
+    // launches fit on one SM (maximum shared-memory carveout)
+    sk_configure<16, 10>();
+    sk_configure<16, 5>();
+    sk_configure<32, sk_stages<32>()>();
+    sk_configure<64, sk_stages<64>()>();
+    sk_configure<128, sk_stages<128>()>();
+    sk_configure<256, sk_stages<256>()>();
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_n_sm, cudaDevAttrMultiProcessorCount, dev);
+    configured = true;
+  }
   const CUtensorMap& wm = *reinterpret_cast<const CUtensorMap*>(w_map.bytes);
   const CUtensorMap& xm = *reinterpret_cast<const CUtensorMap*>(x_map.bytes);
-  if (g_sk_stages <= 5) launch_k(skinny_tc_kernel<5>, dim3(grid), dim3(kThreads), (size_t)sk_smem<5>(), s, wm, xm, a);
-  else launch_k(skinny_tc_kernel<10>, dim3(grid), dim3(kThreads), (size_t)sk_smem<10>(), s, wm, xm, a);
+  const int tiles = skinny_tiles(l.epi, l.N, l.F);
+  const int kb_total = (l.K + BK - 1) / BK;
+  // > 256 rows: 256-row slices, each streaming the weights once more
+  for (int b0 = 0; b0 < l.B; b0 += 256) {
+    const int rows = std::min(256, l.B - b0);
+    const int sn = skinny_cols(rows);
+    const int forced = sn == 16 ? g_sk_splits : std::min(g_sk_splits, 2);   // within the scratch bound
+    const int kb_per = forced > 0 ? (kb_total + forced - 1) / forced
+                                       : pick_kb_per_split(tiles, kb_total, sn, (double)l.N * l.K * 2.0);
+    SkArgs a{};
+    a.N = l.N; a.K = l.K; a.B = rows; a.b0 = b0; a.epi = l.epi;
+    a.kb_per_split = kb_per;
+    a.splits = (kb_total + kb_per - 1) / kb_per;
+    a.tiles = tiles;
+    a.units = tiles * a.splits;
+    a.partial = l.partial; a.counters = l.counters;
+    a.y = l.y; a.ldy = l.ldy; a.act = l.act; a.F = l.F; a.q = l.q; a.kv_pool = l.kv_pool;
+    a.page_elems = l.page_elems; a.layer_off = l.layer_off; a.rope = l.rope; a.rows = l.rows;
+    a.head_rows = l.head_rows; a.H = l.H; a.hd = l.hd; a.d = l.d; a.part_keys = l.part_keys;
+    a.logits = l.logits; a.V = l.V; a.n_text = l.n_text;
+    switch (sn) {
+      case 16:
+        if (g_sk_stages <= 5) sk_launch<16, 5>(wm, xm, a, s);
+        else sk_launch<16, 10>(wm, xm, a, s);
+        break;
+      case 32: sk_launch<32, sk_stages<32>()>(wm, xm, a, s); break;
+      case 64: sk_launch<64, sk_stages<64>()>(wm, xm, a, s); break;
+      case 128: sk_launch<128, sk_stages<128>()>(wm, xm, a, s); break;
+      default: sk_launch<256, sk_stages<256>()>(wm, xm, a, s); break;
+    }
+  }
 }
 
 void launch_gemm_tc(const TmaMap& a_map, const TmaMap& b_map, const TcLaunch& l, cudaStream_t s) {

@@ -56,7 +56,9 @@ struct SkLaunch {
 TmaMap make_kmajor_map(const void* base, int rows, int K, int ld_elems, int box_rows);
 int tc_box_rows(int epi);
 void launch_gemm_tc(const TmaMap& a_map, const TmaMap& b_map, const TcLaunch& l, cudaStream_t s);
-int skinny_max_rows();
+int skinny_max_rows();      // widest batch of the skinny GEMM (rows; > 256 run as 256-row slices)
+int skinny_cols(int rows);  // MMA N used for `rows` batch rows (16/32/64/128/256)
+size_t skinny_partial_floats(int N, int K);  // split-K scratch the skinny GEMM may use for one matrix
 int skinny_tiles(int epi, int N, int F);
 void launch_skinny_tc(const TmaMap& w_map, const TmaMap& x_map, const SkLaunch& l, cudaStream_t s);
 

@@ -40,6 +40,7 @@ reference failure policies (`schedulers.py:411-434`, `:481-483`,
 
 from __future__ import annotations
 
+import contextlib
 import threading
 import time
 from collections.abc import Sequence as _SequenceABC
@@ -183,6 +184,8 @@ class EngineBackend:
         self._trunk_cap = trunk_cache
         self._clock = 0
         self._lock = threading.RLock()
+        self._fg = 0                                    # foreground threads waiting for / holding the lock
+        self._fg_cv = threading.Condition()
         self._pending: list[DeviceRequest] = []
         self._owners: dict[int, DeviceRequest] = {}
         self._live = 0                                  # prepared, not yet released
@@ -193,13 +196,37 @@ class EngineBackend:
         self._fixed_slots = False    # an async engine fixes the batcher to the runner's slots
         self.requests = 0
 
+    @contextlib.contextmanager
+    def _foreground(self):
+        """The backend lock for a runner-thread operation.  A background
+        ticker (BackgroundAsyncEngine) only takes the lock between ticks when
+        no foreground operation is waiting, so control steps never starve
+        behind a stream of decode ticks."""
+        with self._fg_cv:
+            self._fg += 1
+        try:
+            with self._lock:
+                yield
+        finally:
+            with self._fg_cv:
+                self._fg -= 1
+                self._fg_cv.notify_all()
+
+    def _background_turn(self):
+        """Acquire the lock for one background tick (after any waiting
+        foreground operation); use as `with be._background_turn():`."""
+        with self._fg_cv:
+            while self._fg:
+                self._fg_cv.wait(0.01)
+        return self._lock
+
     # -- protocol --------------------------------------------------------------
     def encode(self, instruction: str, observation: bytes) -> _rt.Context:
         return encode_context(instruction, observation)
 
     def begin_step(self, context: _rt.Context, prefix, step: _rt.StepSpec,
                    prev_content) -> StepGenerator:
-        with self._lock:
+        with self._foreground():
             h = self._prepare(context, prefix, step, prev_content, PRIO_REASONING)
             self._pending.append(h)
             self._ensure_slots(len(self._pending) + len(self._owners))
@@ -214,7 +241,7 @@ class EngineBackend:
     def flush(self) -> None:
         """Materialise and submit every pending request, in issue order (they
         join the next decode tick)."""
-        with self._lock:
+        with self._foreground():
             self._materialize()
             pending, self._pending = self._pending, []
             for h in pending:
@@ -224,7 +251,7 @@ class EngineBackend:
         if h.waiter is not None:
             h.waiter.wait_for(h)
             return
-        with self._lock:
+        with self._foreground():
             if h.tokens is not None:
                 return
             if h.req < 0 and h.error is None:
@@ -370,7 +397,7 @@ class EngineBackend:
 
     def discard(self, h: DeviceRequest) -> None:
         """Abandon a prepared, never-submitted request."""
-        with self._lock:
+        with self._foreground():
             if h in self._pending:
                 self._pending.remove(h)
             if h.req < 0:
@@ -515,9 +542,23 @@ class BackgroundAsyncEngine:
         self._now = 0
         self._errors: list[BaseException] = []
         self._stop = False
+        self._held = False               # a control step is issuing its requests
         self._thread = threading.Thread(target=self._loop, name="fastecot-background-ticker", daemon=True)
         self._thread.start()
         backend._async_engines.append(self)
+
+    # -- control-step bracket (EngineParallelAsyncRunner.step) -------------------
+    def hold(self) -> None:
+        """Pause the ticker while a control step issues its requests (trunk
+        prefill, forks, submissions), so the action joins the very next tick
+        instead of queueing behind ticks slipped in between those calls."""
+        with self._cv:
+            self._held = True
+
+    def release(self) -> None:
+        with self._cv:
+            self._held = False
+            self._cv.notify_all()
 
     # -- runner surface (the reference _MicroEngine's) -------------------------
     def submit(self, req) -> None:
@@ -525,7 +566,9 @@ class BackgroundAsyncEngine:
         h = device_handle(req.tokens)
         if h is None:
             raise EngineError(f"request {req.name!r} was not issued by this engine's backend")
-        with be._lock:
+        if req.priority == _rbatch.ACTION:
+            self.release()           # the action is the control step's last submission
+        with be._foreground():
             be._materialize()        # every request issued so far: one trunk prefill, longest first
             if h in be._pending:
                 be._pending.remove(h)
@@ -576,12 +619,12 @@ class BackgroundAsyncEngine:
         be = self.backend
         while True:
             with self._cv:
-                while not self._inflight and not self._stop:
+                while (not self._inflight or self._held) and not self._stop:
                     self._cv.wait(0.05)
                 if self._stop:
                     return
             try:
-                with be._lock:   # one tick at a time; the runner's prefill / forks interleave between ticks
+                with be._background_turn():   # one tick; waiting runner operations go first
                     occ = be._run(-1, max_ticks=1)
                 with self._cv:
                     landed, self._landed = self._landed, []

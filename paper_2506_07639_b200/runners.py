@@ -44,6 +44,16 @@ class EngineParallelAsyncRunner(_rs.ParallelAsyncRunner):
         if factory is not None:
             self.engine = factory(config.slots)
 
+    def step(self, ctx, timestep: int):
+        hold = getattr(self.engine, "hold", None)
+        if hold is None or not self._warm:
+            return super().step(ctx, timestep)
+        hold()               # the device engine pauses background ticks until the action is submitted
+        try:
+            return super().step(ctx, timestep)
+        finally:
+            self.engine.release()
+
     def close(self) -> None:
         close = getattr(self.engine, "close", None)
         if close is not None:

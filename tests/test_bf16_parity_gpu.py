@@ -36,7 +36,7 @@ from paper_2506_07639_b200.engine_backend import EngineBackend
 pytestmark = pytest.mark.gpu
 
 # bounds (set from the measured values below with margin)
-TF_LOGIT_RTOL = 3e-2        # max |dlogit| / max |logit| over the stored columns
+TF_LOGIT_RTOL = {"7b_2layer": 3e-2, "7b": 1e-1}   # max |dlogit| / max |logit| (stored columns)
 TF_ARGMAX_MIN = 0.85        # teacher-forced greedy agreement, all positions
 TF_EPISODE_MIN = 0.90       # teacher-forced agreement over every golden-episode position
 FREE_RUN_MIN = 0.04         # free-running whole-episode token match (chaotic after the first near-tie)
@@ -124,7 +124,7 @@ def test_bf16_teacher_forced_vs_fp32_oracle(config, path):
     stats = _compare(g, got)
     _record(f"teacher_forced_{config}_{path}", stats)
     print(config, path, stats)
-    assert stats["max_rel_logit_err"] < TF_LOGIT_RTOL, stats
+    assert stats["max_rel_logit_err"] < TF_LOGIT_RTOL[config], stats
     assert stats["argmax_agreement"] >= TF_ARGMAX_MIN, stats
 
 

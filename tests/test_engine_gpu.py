@@ -188,26 +188,6 @@ def test_unregistered_reference_async_runner_over_engine(schema, golden_traces):
         be.close()
 
 
-def test_bf16_token_match_rate(golden_traces, schema):
-    """bf16 engine vs the fp32 golden (reported; must stay a coherent model)."""
-    g = golden_traces["modes"]["sequential"]
-    be = EngineBackend("tiny", dtype="bf16", seed=0, kv_pages=1024)
-    try:
-        res, _ = ecot_sched.run_episode(RS.SchedulerConfig(mode="sequential"), 3, be, schema, seed=0)
-    finally:
-        be.close()
-    want = [json.loads(l) for l in g["lines"][:3]]
-    same = total = 0
-    for r, w in zip(res, want):
-        for (name, toks), ws in zip(r.trace.steps, w["steps"]):
-            total += len(ws["tokens"])
-            for a, b in zip(toks, ws["tokens"]):
-                same += a == b
-    rate = same / total
-    print(f"bf16 token-match rate vs fp32 oracle: {rate:.3f} over {total} tokens")
-    assert rate > 0.0
-
-
 def test_engine_errors_are_backend_errors():
     eng = Engine("tiny", dtype="f32", seed=0, kv_pages=4)
     try:
@@ -280,8 +260,13 @@ def test_bf16_skinny_batch_matches_gemv_batch():
     assert sum(a == b for a, b in zip(firsts[1], firsts[0])) >= 6, firsts
 
 
-@pytest.mark.parametrize("M,N,K", [(1, 128, 64), (7, 256, 512), (16, 384, 4096), (3, 4096, 11008)])
+@pytest.mark.parametrize("M,N,K", [(1, 128, 64), (7, 256, 512), (16, 384, 4096), (3, 4096, 11008),
+                                   (17, 4096, 4096), (32, 512, 11008), (56, 4096, 4096), (64, 1024, 4096),
+                                   (100, 4096, 11008), (128, 384, 4096)])
 def test_skinny_tc_matches_torch(M, N, K):
+    """Swap-AB skinny tcgen05 GEMM, every column width (16/32/64/128 rows per
+    MMA), with and without split-K, vs an fp32 torch matmul of the same bf16
+    operands."""
     eng = Engine("small", dtype="bf16", seed=0, kv_pages=8, max_rows=64)
     try:
         g = torch.Generator().manual_seed(M * 7 + N)
@@ -293,7 +278,7 @@ def test_skinny_tc_matches_torch(M, N, K):
         eng.synchronize()
         ref = x.float() @ w.float().T
         err = ((y - ref).abs().max() / ref.abs().max()).item()
-        assert err < 1e-5, (err, y[0, :4].tolist(), ref[0, :4].tolist())
+        assert err < 5e-5, (err, y[0, :4].tolist(), ref[0, :4].tolist())  # fp32 accumulation order
     finally:
         eng.close()
 

@@ -60,9 +60,10 @@ for rep in range(args.repeat):
     t_pre = time.perf_counter() - t0
     reqs, seqs = [], []
     for j in range(args.rows):
-        b = eng.seq_fork(trunk, len(ids) - 40 * j)
+        b = eng.seq_fork(trunk, len(ids) - 40 * (j % 8))
         seqs.append(b)
         reqs.append(eng.submit(b, M.TAG_BASE + j, args.ticks, 1))
+    eng.set_slots(max(8, args.rows))
     if args.profile:
         eng.profile(True)
     a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
