@@ -181,9 +181,11 @@ struct fe_engine {
 
   // tcgen05 path (bf16)
   struct LayerMaps {
-    fe::TmaMap qkv, wo, wgu, wdown;
+    fe::TmaMap qkv, wo, wgu, wdown;   // 128-row boxes (wgu: 64), skinny A operand / v1 tile GEMM
+    fe::TmaMap qkv64, wo64, wdown64;  // 64-row boxes: B operand of the CTA-pair GEMM (wgu shared)
   };
   bool use_tc = false;
+  bool tc_pair = true;  // option "tc_pair": CTA-pair persistent GEMM (0: round-1 128x128 tile GEMM)
   int tc_min_rows = 17;
   // forwards up to this many rows use the skinny GEMM, wider ones the tile
   // GEMM (option "sk_max_rows"; measured in the engine at 7B: skinny ahead
@@ -496,7 +498,8 @@ void launch_layers(fe_engine* e, Lane& ln, const fe::Fwd& f, int n, bool decode,
     } else if (tc) {
       fe::TcLaunch t = tc_launch(fe::TC_QKV, 3 * m.d, m.d);
       t.layer_off = layer_off;
-      fe::launch_gemm_tc(ln.map_xn, mp.qkv, t, st);
+      if (e->tc_pair) fe::launch_gemm_tc(ln.map_xn, mp.qkv64, t, st);
+      else fe::launch_gemm_tc_v1(ln.map_xn, mp.qkv, t, st);
     } else {
       fe::launch_qkv(dt, f, m, ly.wqkv, ws.xn, ws.q, e->kv_pool, l, e->rope, st);
     }
@@ -512,20 +515,23 @@ void launch_layers(fe_engine* e, Lane& ln, const fe::Fwd& f, int n, bool decode,
     p = decode ? prof_begin(e, ln, PROF_GEMV) : -1;
     if (skip_gemm) {
     } else if (sk_on(1)) fe::launch_skinny_tc(mp.wo, ln.map_attn16, sk_launch(fe::TC_RESID, m.d, m.d), st);
-    else if (tc) fe::launch_gemm_tc(ln.map_attn, mp.wo, tc_launch(fe::TC_RESID, m.d, m.d), st);
+    else if (tc && e->tc_pair) fe::launch_gemm_tc(ln.map_attn, mp.wo64, tc_launch(fe::TC_RESID, m.d, m.d), st);
+    else if (tc) fe::launch_gemm_tc_v1(ln.map_attn, mp.wo, tc_launch(fe::TC_RESID, m.d, m.d), st);
     else fe::launch_resid(dt, f, m.d, m.d, ly.wo, ws.attn, ws.x, st);
     prof_end(e, ln, p, gemv_bytes(m.d, m.d, n));
     if (!skip_norm) fe::launch_rmsnorm(dt, ws.x, ly.ffn_norm, ws.xn, n, m.d, m.d, m.eps, nullptr, st);
     p = decode ? prof_begin(e, ln, PROF_GEMV) : -1;
     if (skip_gemm) {
     } else if (sk_on(2)) fe::launch_skinny_tc(mp.wgu, ln.map_xn16, sk_launch(fe::TC_SWIGLU, 2 * m.F, m.d), st);
-    else if (tc) fe::launch_gemm_tc(ln.map_xn, mp.wgu, tc_launch(fe::TC_SWIGLU, 2 * m.F, m.d), st);
+    else if (tc && e->tc_pair) fe::launch_gemm_tc(ln.map_xn, mp.wgu, tc_launch(fe::TC_SWIGLU, 2 * m.F, m.d), st);
+    else if (tc) fe::launch_gemm_tc_v1(ln.map_xn, mp.wgu, tc_launch(fe::TC_SWIGLU, 2 * m.F, m.d), st);
     else fe::launch_swiglu(dt, f, m.F, m.d, ly.wgu, ws.xn, ws.attn /* reused as the SwiGLU activation */, st);
     prof_end(e, ln, p, gemv_bytes(2.0 * m.F, m.d, n));
     p = decode ? prof_begin(e, ln, PROF_GEMV) : -1;
     if (skip_gemm) {
     } else if (sk_on(3)) fe::launch_skinny_tc(mp.wdown, ln.map_act16, sk_launch(fe::TC_RESID, m.d, m.F), st);
-    else if (tc) fe::launch_gemm_tc(ln.map_act, mp.wdown, tc_launch(fe::TC_RESID, m.d, m.F), st);
+    else if (tc && e->tc_pair) fe::launch_gemm_tc(ln.map_act, mp.wdown64, tc_launch(fe::TC_RESID, m.d, m.F), st);
+    else if (tc) fe::launch_gemm_tc_v1(ln.map_act, mp.wdown, tc_launch(fe::TC_RESID, m.d, m.F), st);
     else fe::launch_resid(dt, f, m.d, m.F, ly.wdown, ws.attn, ws.x, st);
     prof_end(e, ln, p, gemv_bytes(m.d, m.F, n));
   }
@@ -1021,6 +1027,9 @@ fe_engine* create(const fe_config* c, int device, const float* rope_host) {
         e->tc_maps[l].wo = fe::make_kmajor_map(ly.wo, m.d, m.d, m.d, 128);
         e->tc_maps[l].wgu = fe::make_kmajor_map(ly.wgu, 2 * m.F, m.d, m.d, fe::tc_box_rows(fe::TC_SWIGLU));
         e->tc_maps[l].wdown = fe::make_kmajor_map(ly.wdown, m.d, m.F, m.F, 128);
+        e->tc_maps[l].qkv64 = fe::make_kmajor_map(ly.wqkv, 3 * m.d, m.d, m.d, 64);
+        e->tc_maps[l].wo64 = fe::make_kmajor_map(ly.wo, m.d, m.d, m.d, 64);
+        e->tc_maps[l].wdown64 = fe::make_kmajor_map(ly.wdown, m.d, m.F, m.F, 64);
       }
     }
 
@@ -1473,10 +1482,13 @@ int fe_op_gemm_tc(fe_engine* e, const void* x, const void* w, int32_t M, int32_t
   return guarded(e, [&] {
     if (N % 128 || K % 64) throw Error("gemm_tc: N % 128 and K % 64 must be 0");
     const fe::TmaMap am = fe::make_kmajor_map(x, M, K, K, 128);
-    const fe::TmaMap bm = fe::make_kmajor_map(w, N, K, K, 128);
+    const fe::TmaMap bm = fe::make_kmajor_map(w, N, K, K, e->tc_pair ? 64 : 128);
     fe::TcLaunch t{};
     t.M = M; t.N = N; t.K = K; t.epi = fe::TC_STORE; t.y = y; t.ldy = N;
-    for (int r = 0; r < e->op_reps; r++) fe::launch_gemm_tc(am, bm, t, e->lanes[0].stream);
+    for (int r = 0; r < e->op_reps; r++) {
+      if (e->tc_pair) fe::launch_gemm_tc(am, bm, t, e->lanes[0].stream);
+      else fe::launch_gemm_tc_v1(am, bm, t, e->lanes[0].stream);
+    }
     CK(cudaGetLastError());
   });
 }
@@ -1543,6 +1555,12 @@ int fe_set_option(fe_engine* e, const char* key, int64_t value) {
     } else if (k == "mk_per_cta" || k == "mk_nc_cap" || k == "mk_nc_cap_o") {
       (k == "mk_per_cta" ? e->mk_per_cta : k == "mk_nc_cap" ? e->mk_nc_cap : e->mk_nc_cap_o) = (int)value;
       if (e->mk_on) mk_make_plans(e);
+      clear_graphs(e);
+    } else if (k == "tc_pair") {
+      e->tc_pair = value != 0;
+      clear_graphs(e);
+    } else if (k == "tc_bn") {
+      fe::g_pair_bn = (int)value;
       clear_graphs(e);
     } else if (k == "prefill_fa") {
       e->prefill_fa = value != 0;

@@ -250,6 +250,313 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
 }
 
 // ----------------------------------------------------------------------------
+// CTA-pair persistent GEMM (the dense-contraction path: trunk prefill and
+// wide decode batches).  A cluster of two CTAs on one TPC computes a
+// 256 x BN output tile with tcgen05.mma.cta_group::2 (M = 256): CTA rank r
+// stages A rows [m0 + 128 r, +128) and B rows [n0 + BN/2 r, +BN/2) of every
+// 64-wide k-block, so each SM streams half the operand bytes of a 1-CTA
+// 128 x BN tile of the same MMA rate (L2 -> SM traffic per flop: 128x128
+// 1-CTA tiles 1, this kernel 1/2 at BN = 256).  The leader CTA (rank 0)
+// issues every MMA; both CTAs' TMA loads complete on the leader's `full`
+// barrier, the MMA commit multicasts to both CTAs' `empty` / `tfull`
+// barriers, and each CTA's epilogue drains its own 128 TMEM lanes (= its 128
+// tile rows x BN columns).  Two TMEM accumulators (2 x BN columns) let the
+// epilogue of tile i overlap the mainloop of tile i + 1; tiles are walked
+// persistently (m fastest, so concurrently running pairs share weight tiles
+// in L2).
+//
+// B tile columns: rank 0's BN/2 rows then rank 1's; for SwiGLU rank 0 loads
+// gate rows [f0, f0 + BN/2) and rank 1 the up rows [F + f0, ...), so columns
+// [0, BN/2) are gate and [BN/2, BN) up of the same BN/2 features.  B tensor
+// maps use 64-row boxes (BN/2 = 64 or 128 -> 1 or 2 boxes per stage).
+// ----------------------------------------------------------------------------
+constexpr int kPairThreads = 192;
+
+template <int BN>
+__host__ __device__ constexpr int pair_stages() { return BN == 256 ? 6 : 8; }
+template <int BN>
+__host__ __device__ constexpr int pair_stage_bytes() { return BM * BK * 2 + (BN / 2) * BK * 2; }
+template <int BN>
+constexpr int pair_smem() { return pair_stages<BN>() * pair_stage_bytes<BN>() + 1024 + 256; }
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t saddr, uint32_t rank) {
+  uint32_t out;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(saddr), "r"(rank));
+  return out;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* b, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done) : "r"(su32(b)), "r"(parity) : "memory");
+}
+// TMA 2-D load into this CTA's shared memory, completing on the pair
+// leader's mbarrier (`bar_cluster`: a shared::cluster address)
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int x, int y,
+                                                 uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;"
+      ::"r"(su32(dst)), "l"(map), "r"(x), "r"(y), "r"(bar_cluster), "l"(policy) : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+struct PairArgs {
+  TcArgs t;
+  int m_tiles, n_tiles;
+};
+
+// Fused epilogue for 32 accumulator columns [c, c + 32) of one tile row
+// (`v`; for SwiGLU `v` = gate, `u` = up of the same features).
+template <int BN>
+__device__ __forceinline__ void pair_epilogue_row(const TcArgs& a, int row, int n_tile, uint32_t tacc) {
+  const int n0 = n_tile * BN;
+  if (a.epi == TC_STORE || a.epi == TC_RESID) {
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      float v[32];
+      tmem_ld32(tacc + c, v);
+      if (row >= a.M) continue;
+      float* dst = a.y + (size_t)row * a.ldy + n0 + c;
+      if (a.epi == TC_STORE) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+          float4 o = *reinterpret_cast<float4*>(dst + i);
+          o.x += v[i]; o.y += v[i + 1]; o.z += v[i + 2]; o.w += v[i + 3];
+          *reinterpret_cast<float4*>(dst + i) = o;
+        }
+      }
+    }
+  } else if (a.epi == TC_SWIGLU) {
+    const int f0 = n_tile * (BN / 2);
+#pragma unroll 1
+    for (int c = 0; c < BN / 2; c += 32) {
+      float g[32], u[32];
+      tmem_ld32(tacc + c, g);
+      tmem_ld32(tacc + BN / 2 + c, u);
+      if (row >= a.M) continue;
+      __nv_bfloat16* dst = a.act + (size_t)row * a.F + f0 + c;
+#pragma unroll
+      for (int i = 0; i < 32; i += 8) {
+        uint4 pk;
+        uint32_t w[4];
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+          __nv_bfloat162 p;
+          p.x = __float2bfloat16_rn(silu_mul(g[i + 2 * j], u[i + 2 * j]));
+          p.y = __float2bfloat16_rn(silu_mul(g[i + 2 * j + 1], u[i + 2 * j + 1]));
+          w[j] = *reinterpret_cast<uint32_t*>(&p);
+        }
+        pk.x = w[0]; pk.y = w[1]; pk.z = w[2]; pk.w = w[3];
+        *reinterpret_cast<uint4*>(dst + i) = pk;
+      }
+    }
+  } else {  // TC_QKV: BN / 128 heads of the q, k or v section (head_dim 128)
+    RowMeta m{};
+    if (row < a.M) m = a.rows[row];
+#pragma unroll 1
+    for (int hh = 0; hh < BN / 128; hh++) {
+      const int nh = n0 + hh * 128;
+      const int sec = nh / a.d, h = (nh % a.d) / 128;
+#pragma unroll 1
+      for (int c = 0; c < 64; c += 32) {
+        float x1[32], x2[32];
+        tmem_ld32(tacc + hh * 128 + c, x1);
+        tmem_ld32(tacc + hh * 128 + 64 + c, x2);
+        if (row >= a.M) continue;
+        if (sec < 2) {
+          const float* cs = a.rope + (size_t)m.pos * 128;
+#pragma unroll
+          for (int i = 0; i < 32; i++) {
+            const float co = cs[c + i], sn = cs[64 + c + i];
+            const float r1 = __fmaf_rn(x1[i], co, -__fmul_rn(x2[i], sn));
+            const float r2 = __fmaf_rn(x2[i], co, __fmul_rn(x1[i], sn));
+            x1[i] = r1;
+            x2[i] = r2;
+          }
+        }
+        if (sec == 0) {
+          float* qr = a.q + (size_t)row * a.d + h * 128;
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            *reinterpret_cast<float4*>(qr + c + i) = make_float4(x1[i], x1[i + 1], x1[i + 2], x1[i + 3]);
+            *reinterpret_cast<float4*>(qr + 64 + c + i) = make_float4(x2[i], x2[i + 1], x2[i + 2], x2[i + 3]);
+          }
+        } else {
+          __nv_bfloat16* kv = a.kv_pool + (size_t)m.kv_page * a.page_elems + a.layer_off +
+                              ((size_t)((sec - 1) * a.H + h) * FE_PAGE + m.kv_slot) * 128;
+#pragma unroll
+          for (int i = 0; i < 32; i += 8) {
+            uint32_t w1[4], w2[4];
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+              __nv_bfloat162 p1, p2;
+              p1.x = __float2bfloat16_rn(x1[i + 2 * j]); p1.y = __float2bfloat16_rn(x1[i + 2 * j + 1]);
+              p2.x = __float2bfloat16_rn(x2[i + 2 * j]); p2.y = __float2bfloat16_rn(x2[i + 2 * j + 1]);
+              w1[j] = *reinterpret_cast<uint32_t*>(&p1);
+              w2[j] = *reinterpret_cast<uint32_t*>(&p2);
+            }
+            *reinterpret_cast<uint4*>(kv + c + i) = make_uint4(w1[0], w1[1], w1[2], w1[3]);
+            *reinterpret_cast<uint4*>(kv + 64 + c + i) = make_uint4(w2[0], w2[1], w2[2], w2[3]);
+          }
+        }
+      }
+    }
+  }
+}
+
+template <int BN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
+gemm_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                 const PairArgs p) {
+  constexpr int ST = pair_stages<BN>();
+  constexpr int kA = BM * BK * 2;               // 16 KB: this CTA's 128 A rows
+  constexpr int kB = (BN / 2) * BK * 2;          // this CTA's BN/2 B rows
+  constexpr int kBoxB = 64 * BK * 2;             // one 64-row B box
+  constexpr uint32_t kIdesc2 = idesc_bf16(256, BN);
+  constexpr int kCols = 2 * BN;                  // two accumulators
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  unsigned char* sa = smem;
+  unsigned char* sb = smem + ST * kA;
+  uint64_t* full = (uint64_t*)(sb + ST * kB);
+  uint64_t* empty = full + ST;
+  uint64_t* tfull = empty + ST;   // [2]
+  uint64_t* tempty = tfull + 2;   // [2] (leader's: arrivals from both CTAs' epilogues)
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+
+  const TcArgs& a = p.t;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
+  const int tiles = p.m_tiles * p.n_tiles;
+  const int kblocks = (a.K + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_b) : "memory");
+    for (int s = 0; s < ST; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 2; i++) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 2);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {  // same warp in both CTAs: the pair's accumulator columns
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
+                 "n"(kCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();  // barriers of both CTAs initialised before any remote arrival
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer (both CTAs)
+      const uint64_t pol_b = policy_evict_last();   // weight tiles are re-read by the other m tiles
+      const uint64_t pol_a = policy_evict_last();
+      const uint32_t full0 = map_to_rank(su32(full), 0);
+      int it = 0;
+      for (int t = pair; t < tiles; t += n_pairs) {
+        const int m_tile = t % p.m_tiles, n_tile = t / p.m_tiles;
+        const int arow = m_tile * 256 + (int)rank * 128;
+        int brow;
+        if (a.epi == TC_SWIGLU) brow = (rank == 0 ? 0 : a.F) + n_tile * (BN / 2);
+        else brow = n_tile * BN + (int)rank * (BN / 2);
+        for (int kb = 0; kb < kblocks; kb++, it++) {
+          const int s = it % ST;
+          mbar_wait(&empty[s], ((it / ST) & 1) ^ 1);
+          if (rank == 0) mbar_expect_tx(&full[s], 2 * (kA + kB));
+          const uint32_t fb = full0 + (uint32_t)s * 8u;
+          tma_load_2d_pair(sa + s * kA, &map_a, fb, kb * BK, arow, pol_a);
+#pragma unroll
+          for (int j = 0; j < BN / 128; j++)
+            tma_load_2d_pair(sb + s * kB + j * kBoxB, &map_b, fb, kb * BK, brow + 64 * j, pol_b);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {  // ---- MMA issuer (leader only)
+      int it = 0, lt = 0;
+      for (int t = pair; t < tiles; t += n_pairs, lt++) {
+        const int acc = lt & 1;
+        mbar_wait_cluster(&tempty[acc], ((lt >> 1) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t dst = tmem + (uint32_t)(acc * BN);
+        for (int kb = 0; kb < kblocks; kb++, it++) {
+          const int s = it % ST;
+          mbar_wait(&full[s], (it / ST) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint64_t da = smem_desc(sa + s * kA);
+          const uint64_t db = smem_desc(sb + s * kB);
+#pragma unroll
+          for (int k = 0; k < BK / 16; k++) {
+            const uint64_t off = (uint64_t)((k * 32) >> 4);
+            const uint32_t accum = (kb > 0 || k > 0) ? 1u : 0u;
+            asm volatile(
+                "{ .reg .pred p; setp.ne.b32 p, %4, 0;"
+                " tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p; }"
+                ::"r"(dst), "l"(da + off), "l"(db + off), "r"(kIdesc2), "r"(accum));
+          }
+          asm volatile(
+              "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+              ::"r"(su32(&empty[s])), "h"((uint16_t)3) : "memory");
+        }
+        asm volatile(
+            "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+            ::"r"(su32(&tfull[acc])), "h"((uint16_t)3) : "memory");
+      }
+    }
+  } else {
+    // ---- epilogue warps 2..5 (both CTAs): TMEM lanes 32*(warp%4) .. +31 = tile rows
+    const int lane_base = 32 * (warp & 3);
+    const uint32_t tempty0 = map_to_rank(su32(tempty), 0);
+    int lt = 0;
+    for (int t = pair; t < tiles; t += n_pairs, lt++) {
+      const int m_tile = t % p.m_tiles, n_tile = t / p.m_tiles;
+      const int acc = lt & 1;
+      mbar_wait(&tfull[acc], (lt >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int row = m_tile * 256 + (int)rank * 128 + lane_base + lane;
+      const uint32_t tacc = tmem + ((uint32_t)lane_base << 16) + (uint32_t)(acc * BN);
+      pair_epilogue_row<BN>(a, row, n_tile, tacc);
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (warp == 2 && lane == 0)
+        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(tempty0 + (uint32_t)acc * 8u)
+                     : "memory");
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();  // the peer's TMEM / shared memory is in use until the pair is done
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kCols));
+  }
+}
+
+// ----------------------------------------------------------------------------
 // Skinny decode GEMM (swap-AB): D[n, b] = sum_k W[n, k] * X[b, k] for up to 16
 // batch rows.  A = weights (M = 128 weight rows per tile), B = staged rows
 // (N = 16), so every weight byte is streamed from HBM exactly once per
@@ -749,21 +1056,68 @@ void launch_skinny_tc(const TmaMap& w_map, const TmaMap& x_map, const SkLaunch& 
   }
 }
 
-void launch_gemm_tc(const TmaMap& a_map, const TmaMap& b_map, const TcLaunch& l, cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-    configured = true;
-  }
+namespace {
+TcArgs tc_args(const TcLaunch& l) {
   TcArgs a{};
   a.M = l.M; a.N = l.N; a.K = l.K; a.epi = l.epi;
   a.y = l.y; a.ldy = l.ldy; a.act = l.act; a.F = l.F;
   a.q = l.q; a.kv_pool = l.kv_pool; a.page_elems = l.page_elems; a.layer_off = l.layer_off;
   a.rope = l.rope; a.rows = l.rows; a.H = l.H; a.hd = l.hd; a.d = l.d;
+  return a;
+}
+}  // namespace
+
+void launch_gemm_tc_v1(const TmaMap& a_map, const TmaMap& b_map, const TcLaunch& l, cudaStream_t s) {
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    configured = true;
+  }
+  const TcArgs a = tc_args(l);
   const int n_tiles = l.epi == TC_SWIGLU ? (l.F / (BN / 2)) : (l.N / BN);
   dim3 grid((l.M + BM - 1) / BM, n_tiles);
   gemm_tc_kernel<<<grid, kThreads, kSmem, s>>>(*reinterpret_cast<const CUtensorMap*>(a_map.bytes),
                                                *reinterpret_cast<const CUtensorMap*>(b_map.bytes), a);
+}
+
+int g_pair_bn = 0;  // engine option "tc_bn": force the pair tile width (0: wave model)
+
+int pair_tile_n(int M, int N, int epi, int F) {
+  (void)M;
+  if (g_pair_bn == 128 || g_pair_bn == 256) return g_pair_bn;
+  // 256 wherever it divides: measured faster than 128 at every 7B shape and
+  // row count (tools/bench_gemm.py, profiles/r2_gemm_pair.json), including
+  // those where 128 needs fewer waves -- a 128-wide pair tile streams 1.5x
+  // the operand bytes per flop and is L2-bandwidth bound
+  const int cols = epi == TC_SWIGLU ? 2 * F : N;
+  return cols % 256 == 0 ? 256 : 128;
+}
+
+void launch_gemm_tc(const TmaMap& a_map, const TmaMap& b_map64, const TcLaunch& l, cudaStream_t s) {
+  static bool configured = false;
+  static int n_sm = 0;
+  if (!configured) {
+    cudaFuncSetAttribute(gemm_pair_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, pair_smem<128>());
+    cudaFuncSetAttribute(gemm_pair_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, pair_smem<256>());
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    configured = true;
+  }
+  if (l.epi == TC_QKV && l.hd != 128) throw std::runtime_error("gemm_tc: QKV epilogue needs head_dim 128");
+  PairArgs p{};
+  p.t = tc_args(l);
+  const int bn = pair_tile_n(l.M, l.N, l.epi, l.F);
+  const int cols = l.epi == TC_SWIGLU ? 2 * l.F : l.N;
+  if (cols % bn || l.K % BK) throw std::runtime_error("gemm_tc: N % tile and K % 64 must be 0");
+  p.m_tiles = (l.M + 255) / 256;
+  p.n_tiles = cols / bn;
+  const int tiles = p.m_tiles * p.n_tiles;
+  const int grid = 2 * std::min(tiles, n_sm / 2);
+  const CUtensorMap& am = *reinterpret_cast<const CUtensorMap*>(a_map.bytes);
+  const CUtensorMap& bm = *reinterpret_cast<const CUtensorMap*>(b_map64.bytes);
+  if (bn == 256) gemm_pair_kernel<256><<<grid, kPairThreads, pair_smem<256>(), s>>>(am, bm, p);
+  else gemm_pair_kernel<128><<<grid, kPairThreads, pair_smem<128>(), s>>>(am, bm, p);
 }
 
 }  // namespace fe

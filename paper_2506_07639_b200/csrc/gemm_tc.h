@@ -55,7 +55,11 @@ struct SkLaunch {
 // 2-D K-major bf16 tensor [rows][K] with row stride ld_elems, box [box_rows x 64], 128B swizzle
 TmaMap make_kmajor_map(const void* base, int rows, int K, int ld_elems, int box_rows);
 int tc_box_rows(int epi);
-void launch_gemm_tc(const TmaMap& a_map, const TmaMap& b_map, const TcLaunch& l, cudaStream_t s);
+// CTA-pair persistent tcgen05 GEMM (B map: 64-row boxes)
+void launch_gemm_tc(const TmaMap& a_map, const TmaMap& b_map64, const TcLaunch& l, cudaStream_t s);
+// round-1 1-CTA 128 x 128 tile GEMM (B map: 128-row boxes, SwiGLU 64), kept for A/B (option "tc_pair" 0)
+void launch_gemm_tc_v1(const TmaMap& a_map, const TmaMap& b_map, const TcLaunch& l, cudaStream_t s);
+extern int g_pair_bn;
 int skinny_max_rows();      // widest batch of the skinny GEMM (rows; > 256 run as 256-row slices)
 int skinny_cols(int rows);  // MMA N used for `rows` batch rows (16/32/64/128/256)
 size_t skinny_partial_floats(int N, int K);  // split-K scratch the skinny GEMM may use for one matrix
