@@ -27,12 +27,14 @@
 #include <map>
 #include <tuple>
 #include <unordered_map>
+#include <unordered_set>
 #include <mutex>
 #include <thread>
 #include <chrono>
 #include <stdexcept>
 #include <string>
 #include <unordered_map>
+#include <unordered_set>
 #include <vector>
 
 namespace {
@@ -59,7 +61,7 @@ constexpr int kLanes = 2;
 constexpr int kLane1Rows = 64;      // background lane: decode rows only
 
 struct MetaLayout {
-  size_t o_rows, o_items, o_irows, o_heads, o_pages, total;
+  size_t o_rows, o_items, o_irows, o_heads, o_pages, o_slots, o_nspans, o_spages, total;
   int cap_rows, cap_items, cap_irows, cap_pages;
 };
 
@@ -118,6 +120,8 @@ struct Lane {
   int* attn_counters = nullptr;
   float* sk_partial = nullptr;
   int* sk_counters = nullptr;
+  float* pair_scratch = nullptr;  // stream-K partials of the CTA-pair GEMM
+  int* pair_counters = nullptr;
   // persistent decode-tick kernel scratch (lane 0)
   float* mk_ss = nullptr;
   unsigned long long* mk_bar = nullptr;
@@ -186,6 +190,9 @@ struct fe_engine {
   };
   bool use_tc = false;
   bool tc_pair = true;  // option "tc_pair": CTA-pair persistent GEMM (0: round-1 128x128 tile GEMM)
+  bool span_attn = true;  // option "span_attn": tensor-core span attention for chain decode ticks (bf16)
+  int span_cap = 16;      // option "span_cap": pages per span item
+  fe::TmaMap pool_map{};  // the KV pool as [rows][128] bf16, 64 x 64 boxes (span attention)
   int tc_min_rows = 17;
   // forwards up to this many rows use the skinny GEMM, wider ones the tile
   // GEMM (option "sk_max_rows"; measured in the engine at 7B: skinny ahead
@@ -469,6 +476,7 @@ void launch_layers(fe_engine* e, Lane& ln, const fe::Fwd& f, int n, bool decode,
     t.act = (__nv_bfloat16*)ws.attn; t.F = m.F;
     t.q = ws.q; t.kv_pool = (__nv_bfloat16*)e->kv_pool; t.page_elems = e->page_elems;
     t.rope = e->rope; t.rows = f.rows; t.H = m.H; t.hd = m.hd; t.d = m.d;
+    t.sk_scratch = ln.pair_scratch; t.sk_counters = ln.pair_counters;
     return t;
   };
   auto sk_launch = [&](int epi, int N, int K) {
@@ -506,6 +514,8 @@ void launch_layers(fe_engine* e, Lane& ln, const fe::Fwd& f, int n, bool decode,
     prof_end(e, ln, p, gemv_bytes(3.0 * m.d, m.d, n));
     p = decode ? prof_begin(e, ln, PROF_ATTN) : -1;
     if (e->debug_skip & 1) {
+    } else if (f.span_mode) {
+      fe::launch_span_attention(f, m, e->pool_map, ws.q, l, ws.partial, ws.attn, st);
     } else if (!decode && f.seq_pages && dt == FE_BF16 && m.hd == 128 && e->prefill_fa) {
       fe::launch_prefill_attention(f, m, ws.q, e->kv_pool, l, ws.attn, st);
     } else {
@@ -647,23 +657,82 @@ void forward(fe_engine* e, Lane& ln, const std::vector<RowIn>& rows, uint64_t vi
       page_chunk[pg] = c;
     }
   }
+  // span mode (bf16 chain decode ticks, attn_span.cu): runs of consecutive
+  // pages with the same rows, every page but the last full for all of them
+  int n_head = 0;
+  for (const RowIn& r : rows) n_head += r.head ? 1 : 0;
+  const bool span_mode = n_head > 0 && e->span_attn && e->use_tc && m.hd == 128 &&
+                         !(e->mk_on && n <= 16 && n_head == n && e->debug_skip == 0);
   std::vector<fe::AttnItem> items;
   std::vector<fe::ItemRow> irows;
-  for (auto& kv : by_page) {
-    const auto& lst = kv.second;
-    for (size_t b = 0; b < lst.size(); b += kItemRows) {
-      fe::AttnItem it;
-      it.page = kv.first;
-      it.chunk = page_chunk[kv.first];
-      it.row_begin = (int)irows.size();
-      it.row_count = (int)std::min<size_t>(kItemRows, lst.size() - b);
-      it.valid_max = 0;
-      it.pad[0] = it.pad[1] = it.pad[2] = 0;
-      for (int j = 0; j < it.row_count; j++) {
-        irows.push_back({lst[b + j].first, lst[b + j].second});
-        it.valid_max = std::max(it.valid_max, lst[b + j].second);
+  std::vector<int32_t> islots, nspans, spages;
+  if (span_mode) {
+    nspans.assign(n, 0);
+    std::unordered_set<int> done;
+    for (int i = 0; i < n; i++) {
+      const Seq& s = e->seqs[rows[i].seq];
+      const int last_c = rows[i].pos / FE_PAGE;
+      for (int c = 0; c <= last_c;) {
+        const int pg = s.pages[c];
+        if (done.count(pg)) { c++; continue; }
+        const auto& lst = by_page[pg];
+        // extend while the next chunk's page has the same rows and this one is full for all
+        int c1 = c;
+        auto full_for_all = [&](int page) {
+          for (const auto& rv : by_page[page]) if (rv.second != FE_PAGE) return false;
+          return true;
+        };
+        while (c1 < last_c && c1 - c + 1 < e->span_cap && full_for_all(s.pages[c1])) {
+          const auto& nxt = by_page[s.pages[c1 + 1]];
+          bool same = nxt.size() == lst.size();
+          for (size_t k = 0; same && k < lst.size(); k++) same = nxt[k].first == lst[k].first;
+          if (!same) break;
+          c1++;
+        }
+        const int po = (int)spages.size();
+        for (int cc = c; cc <= c1; cc++) {
+          spages.push_back(s.pages[cc]);
+          done.insert(s.pages[cc]);
+        }
+        const auto& lastl = by_page[s.pages[c1]];  // valid keys on the span's last page
+        for (size_t b = 0; b < lastl.size(); b += kItemRows) {
+          fe::AttnItem it;
+          it.page = s.pages[c];
+          it.chunk = c;
+          it.row_begin = (int)irows.size();
+          it.row_count = (int)std::min<size_t>(kItemRows, lastl.size() - b);
+          it.valid_max = 0;
+          it.pad[0] = c1 - c + 1;
+          it.pad[1] = po;
+          it.pad[2] = 0;
+          for (int j = 0; j < it.row_count; j++) {
+            const int row = lastl[b + j].first;
+            irows.push_back({row, lastl[b + j].second});
+            islots.push_back(nspans[row]++);
+            it.valid_max = std::max(it.valid_max, lastl[b + j].second);
+          }
+          items.push_back(it);
+        }
+        c = c1 + 1;
       }
-      items.push_back(it);
+    }
+  } else {
+    for (auto& kv : by_page) {
+      const auto& lst = kv.second;
+      for (size_t b = 0; b < lst.size(); b += kItemRows) {
+        fe::AttnItem it;
+        it.page = kv.first;
+        it.chunk = page_chunk[kv.first];
+        it.row_begin = (int)irows.size();
+        it.row_count = (int)std::min<size_t>(kItemRows, lst.size() - b);
+        it.valid_max = 0;
+        it.pad[0] = it.pad[1] = it.pad[2] = 0;
+        for (int j = 0; j < it.row_count; j++) {
+          irows.push_back({lst[b + j].first, lst[b + j].second});
+          it.valid_max = std::max(it.valid_max, lst[b + j].second);
+        }
+        items.push_back(it);
+      }
     }
   }
 
@@ -697,6 +766,14 @@ void forward(fe_engine* e, Lane& ln, const std::vector<RowIn>& rows, uint64_t vi
   copy(L.o_items, sizeof(fe::AttnItem) * items.size());
   copy(L.o_irows, sizeof(fe::ItemRow) * irows.size());
   copy(L.o_heads, sizeof(int32_t) * head_rows.size());
+  if (span_mode) {
+    std::memcpy(hbuf + L.o_slots, islots.data(), sizeof(int32_t) * islots.size());
+    std::memcpy(hbuf + L.o_nspans, nspans.data(), sizeof(int32_t) * nspans.size());
+    std::memcpy(hbuf + L.o_spages, spages.data(), sizeof(int32_t) * spages.size());
+    copy(L.o_slots, sizeof(int32_t) * islots.size());
+    copy(L.o_nspans, sizeof(int32_t) * nspans.size());
+    copy(L.o_spages, sizeof(int32_t) * spages.size());
+  }
   // single-sequence prefill: the sequence's page table for the tensor-core attention
   bool one_seq = head_rows.empty() && n > 1;
   for (int i = 1; i < n && one_seq; i++) one_seq = rows[i].seq == rows[0].seq && rows[i].pos == rows[0].pos + i;
@@ -731,13 +808,18 @@ void forward(fe_engine* e, Lane& ln, const std::vector<RowIn>& rows, uint64_t vi
   f.vision_key = fe::tensor_key(vision_seed, 4 /* T_VISION */);
   f.seq_pages = one_seq ? (const int32_t*)(dbuf + L.o_pages) : nullptr;
   f.pos0 = one_seq ? rows[0].pos : 0;
+  f.span_mode = span_mode;
+  f.item_slots = (const int32_t*)(dbuf + L.o_slots);
+  f.row_nspans = (const int32_t*)(dbuf + L.o_nspans);
+  f.span_pages = (const int32_t*)(dbuf + L.o_spages);
 
   const bool decode = f.n_head_rows > 0;
   const double el = (double)e->elem;
   // algorithmic bytes of one GEMV launch: weights + staged input + fp32 output
   auto gemv_bytes = [&](double N, double K, int rws) { return N * K * el + rws * K * el + rws * N * 4.0; };
   double kv_bytes = 0;  // K+V bytes the cascade items stage (each shared page once per head)
-  for (const auto& it : items) kv_bytes += 2.0 * it.valid_max * m.hd * m.H * el;
+  for (const auto& it : items)
+    kv_bytes += 2.0 * (span_mode ? (it.pad[0] - 1) * FE_PAGE + it.valid_max : it.valid_max) * m.hd * m.H * el;
 
   // decode ticks replay a CUDA graph per (rows, item bucket), captured on the
   // second tick with that key; prefill and profiled runs launch eagerly
@@ -946,7 +1028,10 @@ void create_lane(fe_engine* e, Lane& ln, int id, int rows, int priority) {
     L.o_heads = up16(L.o_irows + (size_t)L.cap_irows * sizeof(fe::ItemRow));
     L.cap_pages = m.max_pos / FE_PAGE + 1;
     L.o_pages = up16(L.o_heads + R * 4);
-    L.total = up16(L.o_pages + (size_t)L.cap_pages * 4);
+    L.o_slots = up16(L.o_pages + (size_t)L.cap_pages * 4);
+    L.o_nspans = up16(L.o_slots + (size_t)L.cap_irows * 4);
+    L.o_spages = up16(L.o_nspans + R * 4);
+    L.total = up16(L.o_spages + (size_t)ln.max_partials * 4);
   }
   ln.ws.meta = e->dalloc(ln.layout.total);
   for (int i = 0; i < 2; i++) CK(cudaEventCreateWithFlags(&ln.tick_ev[i], cudaEventDisableTiming));
@@ -970,6 +1055,9 @@ void create_lane(fe_engine* e, Lane& ln, int id, int rows, int priority) {
     ln.sk_partial = (float*)e->dalloc(part_floats * 4);
     ln.sk_counters = (int*)e->dalloc(4096 * sizeof(int));
     CK(cudaMemset(ln.sk_counters, 0, 4096 * sizeof(int)));
+    ln.pair_scratch = (float*)e->dalloc(fe::pair_sk_scratch_floats() * 4);
+    ln.pair_counters = (int*)e->dalloc(fe::pair_sk_counters() * sizeof(int));
+    CK(cudaMemset(ln.pair_counters, 0, fe::pair_sk_counters() * sizeof(int)));
   }
   (void)V;
 }
@@ -1080,6 +1168,11 @@ fe_engine* create(const fe_config* c, int device, const float* rope_host) {
     }
     e->n_pages = (int)pages;
     e->kv_pool = e->dalloc(pages * e->page_elems * el);
+    // zeroed once: attention kernels that stage whole pages multiply the keys
+    // past a row's valid count by p = 0, which needs finite contents
+    CK(cudaMemset(e->kv_pool, 0, pages * e->page_elems * el));
+    if (e->use_tc)
+      e->pool_map = fe::make_kmajor_map(e->kv_pool, (int)(pages * e->page_elems / 128), 128, 128, 64);
     e->page_ref.assign(pages, 0);
     for (int p = (int)pages - 1; p >= 0; p--) e->free_pages.push_back(p);
   } catch (...) {
@@ -1485,6 +1578,7 @@ int fe_op_gemm_tc(fe_engine* e, const void* x, const void* w, int32_t M, int32_t
     const fe::TmaMap bm = fe::make_kmajor_map(w, N, K, K, e->tc_pair ? 64 : 128);
     fe::TcLaunch t{};
     t.M = M; t.N = N; t.K = K; t.epi = fe::TC_STORE; t.y = y; t.ldy = N;
+    t.sk_scratch = e->lanes[0].pair_scratch; t.sk_counters = e->lanes[0].pair_counters;
     for (int r = 0; r < e->op_reps; r++) {
       if (e->tc_pair) fe::launch_gemm_tc(am, bm, t, e->lanes[0].stream);
       else fe::launch_gemm_tc_v1(am, bm, t, e->lanes[0].stream);
@@ -1556,8 +1650,17 @@ int fe_set_option(fe_engine* e, const char* key, int64_t value) {
       (k == "mk_per_cta" ? e->mk_per_cta : k == "mk_nc_cap" ? e->mk_nc_cap : e->mk_nc_cap_o) = (int)value;
       if (e->mk_on) mk_make_plans(e);
       clear_graphs(e);
+    } else if (k == "span_attn") {
+      e->span_attn = value != 0;
+      clear_graphs(e);
+    } else if (k == "span_cap") {
+      e->span_cap = (int)std::max<int64_t>(1, value);
+      clear_graphs(e);
     } else if (k == "tc_pair") {
       e->tc_pair = value != 0;
+      clear_graphs(e);
+    } else if (k == "tc_sk") {
+      fe::g_pair_sk = (int)value;
       clear_graphs(e);
     } else if (k == "tc_bn") {
       fe::g_pair_bn = (int)value;

@@ -271,6 +271,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
 // maps use 64-row boxes (BN/2 = 64 or 128 -> 1 or 2 boxes per stage).
 // ----------------------------------------------------------------------------
 constexpr int kPairThreads = 192;
+constexpr int kPairMaxPairs = 74;  // 148 SMs
 
 template <int BN>
 __host__ __device__ constexpr int pair_stages() { return BN == 256 ? 6 : 8; }
@@ -318,18 +319,68 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
 struct PairArgs {
   TcArgs t;
   int m_tiles, n_tiles;
+  int kblocks;
+  // stream-K schedule (DP + one stream-K wave): tiles [0, dp) are walked
+  // data-parallel (pair p: p, p + P, ...); the k-iterations of tiles
+  // [dp, tiles) are split evenly over the P pairs, pair p taking
+  // [p W / P, (p + 1) W / P) of the W = (tiles - dp) * kblocks iterations.
+  int dp;
+  long long W;
+  float* scratch;   // [P][2 slots][2 ranks][BN / 4][128] float4: partial segments
+  int* counters;    // [tiles - dp][2 ranks]: arrivals of a tile's partial segments
 };
 
-// Fused epilogue for 32 accumulator columns [c, c + 32) of one tile row
-// (`v`; for SwiGLU `v` = gate, `u` = up of the same features).
-template <int BN>
-__device__ __forceinline__ void pair_epilogue_row(const TcArgs& a, int row, int n_tile, uint32_t tacc) {
+struct Seg {
+  int tile, k0, k1;
+  bool sk;   // from the stream-K range
+};
+
+// The segments of one pair in order (identical walk in every role).
+struct SegIter {
+  int t_dp, dp, P, KB;
+  long long i, i1;
+  __device__ SegIter(const PairArgs& p, int pair, int n_pairs) {
+    P = n_pairs;
+    dp = p.dp;
+    KB = p.kblocks;
+    t_dp = pair;
+    i = (long long)pair * p.W / n_pairs;
+    i1 = (long long)(pair + 1) * p.W / n_pairs;
+  }
+  __device__ bool next(Seg& s) {
+    if (t_dp < dp) {
+      s.tile = t_dp; s.k0 = 0; s.k1 = KB; s.sk = false;
+      t_dp += P;
+      return true;
+    }
+    if (i >= i1) return false;
+    const int t = (int)(i / KB), k0 = (int)(i % KB);
+    const int k1 = (int)min((long long)KB, (long long)k0 + (i1 - i));
+    s.tile = dp + t; s.k0 = k0; s.k1 = k1; s.sk = true;
+    i += k1 - k0;
+    return true;
+  }
+};
+
+__device__ __forceinline__ long long sk_start(const PairArgs& p, int q, int P) { return (long long)q * p.W / P; }
+// the pair whose stream-K range holds iteration x (the largest q with start(q) <= x)
+__device__ __forceinline__ int sk_owner(const PairArgs& p, long long x, int P) {
+  int q = (int)(x * P / p.W);
+  while (q + 1 < P && sk_start(p, q + 1, P) <= x) q++;
+  while (q > 0 && sk_start(p, q, P) > x) q--;
+  return q;
+}
+
+// Fused epilogue of one tile row (`row`; TMEM lane / scratch row r) over BN
+// columns, the accumulator values coming from `ld(c, v)` (32 columns at c).
+template <int BN, typename LD>
+__device__ __forceinline__ void pair_epilogue_row(const TcArgs& a, int row, int n_tile, LD&& ld) {
   const int n0 = n_tile * BN;
   if (a.epi == TC_STORE || a.epi == TC_RESID) {
 #pragma unroll 1
     for (int c = 0; c < BN; c += 32) {
       float v[32];
-      tmem_ld32(tacc + c, v);
+      ld(c, v);
       if (row >= a.M) continue;
       float* dst = a.y + (size_t)row * a.ldy + n0 + c;
       if (a.epi == TC_STORE) {
@@ -349,13 +400,12 @@ __device__ __forceinline__ void pair_epilogue_row(const TcArgs& a, int row, int 
 #pragma unroll 1
     for (int c = 0; c < BN / 2; c += 32) {
       float g[32], u[32];
-      tmem_ld32(tacc + c, g);
-      tmem_ld32(tacc + BN / 2 + c, u);
+      ld(c, g);
+      ld(BN / 2 + c, u);
       if (row >= a.M) continue;
       __nv_bfloat16* dst = a.act + (size_t)row * a.F + f0 + c;
 #pragma unroll
       for (int i = 0; i < 32; i += 8) {
-        uint4 pk;
         uint32_t w[4];
 #pragma unroll
         for (int j = 0; j < 4; j++) {
@@ -364,8 +414,7 @@ __device__ __forceinline__ void pair_epilogue_row(const TcArgs& a, int row, int 
           p.y = __float2bfloat16_rn(silu_mul(g[i + 2 * j + 1], u[i + 2 * j + 1]));
           w[j] = *reinterpret_cast<uint32_t*>(&p);
         }
-        pk.x = w[0]; pk.y = w[1]; pk.z = w[2]; pk.w = w[3];
-        *reinterpret_cast<uint4*>(dst + i) = pk;
+        *reinterpret_cast<uint4*>(dst + i) = make_uint4(w[0], w[1], w[2], w[3]);
       }
     }
   } else {  // TC_QKV: BN / 128 heads of the q, k or v section (head_dim 128)
@@ -378,8 +427,8 @@ __device__ __forceinline__ void pair_epilogue_row(const TcArgs& a, int row, int 
 #pragma unroll 1
       for (int c = 0; c < 64; c += 32) {
         float x1[32], x2[32];
-        tmem_ld32(tacc + hh * 128 + c, x1);
-        tmem_ld32(tacc + hh * 128 + 64 + c, x2);
+        ld(hh * 128 + c, x1);
+        ld(hh * 128 + 64 + c, x2);
         if (row >= a.M) continue;
         if (sec < 2) {
           const float* cs = a.rope + (size_t)m.pos * 128;
@@ -432,6 +481,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
   constexpr int kBoxB = 64 * BK * 2;             // one 64-row B box
   constexpr uint32_t kIdesc2 = idesc_bf16(256, BN);
   constexpr int kCols = 2 * BN;                  // two accumulators
+  constexpr size_t kPart = (size_t)BM * BN;      // floats of one partial (one rank's 128 rows)
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   unsigned char* sa = smem;
@@ -441,13 +491,12 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
   uint64_t* tfull = empty + ST;   // [2]
   uint64_t* tempty = tfull + 2;   // [2] (leader's: arrivals from both CTAs' epilogues)
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+  int* last_flag = (int*)(tmem_slot + 1);
 
   const TcArgs& a = p.t;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
   const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
-  const int tiles = p.m_tiles * p.n_tiles;
-  const int kblocks = (a.K + BK - 1) / BK;
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
@@ -474,37 +523,40 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
 
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer (both CTAs)
-      const uint64_t pol_b = policy_evict_last();   // weight tiles are re-read by the other m tiles
-      const uint64_t pol_a = policy_evict_last();
+      const uint64_t pol = policy_evict_last();   // weight tiles are re-read by the other m tiles
       const uint32_t full0 = map_to_rank(su32(full), 0);
       int it = 0;
-      for (int t = pair; t < tiles; t += n_pairs) {
-        const int m_tile = t % p.m_tiles, n_tile = t / p.m_tiles;
+      SegIter si(p, pair, n_pairs);
+      Seg sg;
+      while (si.next(sg)) {
+        const int m_tile = sg.tile % p.m_tiles, n_tile = sg.tile / p.m_tiles;
         const int arow = m_tile * 256 + (int)rank * 128;
         int brow;
         if (a.epi == TC_SWIGLU) brow = (rank == 0 ? 0 : a.F) + n_tile * (BN / 2);
         else brow = n_tile * BN + (int)rank * (BN / 2);
-        for (int kb = 0; kb < kblocks; kb++, it++) {
+        for (int kb = sg.k0; kb < sg.k1; kb++, it++) {
           const int s = it % ST;
           mbar_wait(&empty[s], ((it / ST) & 1) ^ 1);
           if (rank == 0) mbar_expect_tx(&full[s], 2 * (kA + kB));
           const uint32_t fb = full0 + (uint32_t)s * 8u;
-          tma_load_2d_pair(sa + s * kA, &map_a, fb, kb * BK, arow, pol_a);
+          tma_load_2d_pair(sa + s * kA, &map_a, fb, kb * BK, arow, pol);
 #pragma unroll
           for (int j = 0; j < BN / 128; j++)
-            tma_load_2d_pair(sb + s * kB + j * kBoxB, &map_b, fb, kb * BK, brow + 64 * j, pol_b);
+            tma_load_2d_pair(sb + s * kB + j * kBoxB, &map_b, fb, kb * BK, brow + 64 * j, pol);
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {  // ---- MMA issuer (leader only)
       int it = 0, lt = 0;
-      for (int t = pair; t < tiles; t += n_pairs, lt++) {
+      SegIter si(p, pair, n_pairs);
+      Seg sg;
+      for (; si.next(sg); lt++) {
         const int acc = lt & 1;
         mbar_wait_cluster(&tempty[acc], ((lt >> 1) & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t dst = tmem + (uint32_t)(acc * BN);
-        for (int kb = 0; kb < kblocks; kb++, it++) {
+        for (int kb = sg.k0; kb < sg.k1; kb++, it++) {
           const int s = it % ST;
           mbar_wait(&full[s], (it / ST) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -513,7 +565,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
 #pragma unroll
           for (int k = 0; k < BK / 16; k++) {
             const uint64_t off = (uint64_t)((k * 32) >> 4);
-            const uint32_t accum = (kb > 0 || k > 0) ? 1u : 0u;
+            const uint32_t accum = (kb > sg.k0 || k > 0) ? 1u : 0u;
             asm volatile(
                 "{ .reg .pred p; setp.ne.b32 p, %4, 0;"
                 " tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p; }"
@@ -531,21 +583,74 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
   } else {
     // ---- epilogue warps 2..5 (both CTAs): TMEM lanes 32*(warp%4) .. +31 = tile rows
     const int lane_base = 32 * (warp & 3);
+    const int r = lane_base + lane;            // this thread's row of the CTA's 128
     const uint32_t tempty0 = map_to_rank(su32(tempty), 0);
     int lt = 0;
-    for (int t = pair; t < tiles; t += n_pairs, lt++) {
-      const int m_tile = t % p.m_tiles, n_tile = t / p.m_tiles;
+    SegIter si(p, pair, n_pairs);
+    Seg sg;
+    for (; si.next(sg); lt++) {
+      const int m_tile = sg.tile % p.m_tiles, n_tile = sg.tile / p.m_tiles;
       const int acc = lt & 1;
       mbar_wait(&tfull[acc], (lt >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const int row = m_tile * 256 + (int)rank * 128 + lane_base + lane;
+      const int row = m_tile * 256 + (int)rank * 128 + r;
       const uint32_t tacc = tmem + ((uint32_t)lane_base << 16) + (uint32_t)(acc * BN);
-      pair_epilogue_row<BN>(a, row, n_tile, tacc);
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      auto release_acc = [&]() {
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (warp == 2 && lane == 0)
+          asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];"
+                       ::"r"(tempty0 + (uint32_t)acc * 8u) : "memory");
+      };
+      if (sg.k0 == 0 && sg.k1 == p.kblocks) {  // whole tile: fused epilogue straight from TMEM
+        pair_epilogue_row<BN>(a, row, n_tile, [&](int c, float(&v)[32]) { tmem_ld32(tacc + c, v); });
+        release_acc();
+        continue;
+      }
+      // partial segment: accumulator -> this pair's scratch slot (coalesced float4
+      // columns); slot 0 = the pair's first stream-K segment, 1 = its last
+      const int slot = (sk_start(p, pair, n_pairs) / p.kblocks == sg.tile - p.dp) ? 0 : 1;
+      float4* dst = reinterpret_cast<float4*>(p.scratch + ((size_t)(pair * 2 + slot) * 2 + rank) * kPart);
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        float v[32];
+        tmem_ld32(tacc + c, v);
+#pragma unroll
+        for (int j = 0; j < 8; j++)
+          __stcg(dst + (size_t)(c / 4 + j) * BM + r, make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
+      }
+      __threadfence();
+      release_acc();
+      // the tile's segments: pairs q_first .. q_last of the stream-K range
+      const long long x0 = (long long)(sg.tile - p.dp) * p.kblocks;
+      const int q_first = sk_owner(p, x0, n_pairs), q_last = sk_owner(p, x0 + p.kblocks - 1, n_pairs);
+      const int nseg = q_last - q_first + 1;
+      int* cnt = p.counters + (size_t)(sg.tile - p.dp) * 2 + rank;
+      if (warp == 2 && lane == 0) {
+        const int prev = atomicAdd(cnt, 1);
+        const bool last = prev == nseg - 1;
+        if (last) *cnt = 0;  // ready for the next launch
+        *last_flag = last;
+      }
       asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (warp == 2 && lane == 0)
-        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(tempty0 + (uint32_t)acc * 8u)
-                     : "memory");
+      if (!*last_flag) continue;
+      __threadfence();
+      // last arrival: sum the segments in k order (deterministic) and run the epilogue
+      pair_epilogue_row<BN>(a, row, n_tile, [&](int c, float(&v)[32]) {
+#pragma unroll
+        for (int j = 0; j < 32; j++) v[j] = 0.0f;
+        for (int q = q_first; q <= q_last; q++) {
+          const long long qs = sk_start(p, q, n_pairs);
+          const int qslot = (qs / p.kblocks == sg.tile - p.dp) ? 0 : 1;  // q's first segment, or its last
+          const float4* src = reinterpret_cast<const float4*>(p.scratch + ((size_t)(q * 2 + qslot) * 2 + rank) * kPart);
+#pragma unroll
+          for (int j = 0; j < 8; j++) {
+            const float4 w = __ldcg(src + (size_t)(c / 4 + j) * BM + r);
+            v[4 * j] += w.x; v[4 * j + 1] += w.y; v[4 * j + 2] += w.z; v[4 * j + 3] += w.w;
+          }
+        }
+      });
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // last_flag reused by the next segment
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -1080,7 +1185,12 @@ void launch_gemm_tc_v1(const TmaMap& a_map, const TmaMap& b_map, const TcLaunch&
                                                *reinterpret_cast<const CUtensorMap*>(b_map.bytes), a);
 }
 
-int g_pair_bn = 0;  // engine option "tc_bn": force the pair tile width (0: wave model)
+int g_pair_bn = 0;  // engine option "tc_bn": force the pair tile width (0: 256 where it divides)
+int g_pair_sk = 0;  // engine option "tc_sk": stream-K the last waves (measured slower: the 256 x 256 fp32
+                    // partials cost more than the wave tail they remove, profiles/r2_gemm_pair_sk.txt)
+
+size_t pair_sk_scratch_floats() { return (size_t)kPairMaxPairs * 2 * 2 * BM * 256; }
+int pair_sk_counters() { return 4 * kPairMaxPairs; }
 
 int pair_tile_n(int M, int N, int epi, int F) {
   (void)M;
@@ -1112,8 +1222,15 @@ void launch_gemm_tc(const TmaMap& a_map, const TmaMap& b_map64, const TcLaunch& 
   if (cols % bn || l.K % BK) throw std::runtime_error("gemm_tc: N % tile and K % 64 must be 0");
   p.m_tiles = (l.M + 255) / 256;
   p.n_tiles = cols / bn;
+  p.kblocks = l.K / BK;
   const int tiles = p.m_tiles * p.n_tiles;
-  const int grid = 2 * std::min(tiles, n_sm / 2);
+  const int P = std::min(tiles * p.kblocks, std::min(n_sm / 2, kPairMaxPairs));
+  // DP for all but the last one-to-two waves, which are stream-K'd (no wave tail)
+  p.dp = (!g_pair_sk || !l.sk_scratch) ? tiles : (tiles >= 2 * P ? (tiles / P - 1) * P : 0);
+  p.W = (long long)(tiles - p.dp) * p.kblocks;
+  p.scratch = l.sk_scratch;
+  p.counters = l.sk_counters;
+  const int grid = 2 * (p.dp == tiles ? std::min(tiles, P) : P);
   const CUtensorMap& am = *reinterpret_cast<const CUtensorMap*>(a_map.bytes);
   const CUtensorMap& bm = *reinterpret_cast<const CUtensorMap*>(b_map64.bytes);
   if (bn == 256) gemm_pair_kernel<256><<<grid, kPairThreads, pair_smem<256>(), s>>>(am, bm, p);

@@ -29,6 +29,8 @@ struct TcLaunch {
   const float* rope;
   const RowMeta* rows;
   int H, hd, d;
+  float* sk_scratch;   // stream-K partials of the pair GEMM (pair_sk_scratch_floats()), or null: no stream-K
+  int* sk_counters;    // pair_sk_counters() ints, zero-initialised
 };
 
 // skinny decode GEMM (swap-AB, <= skinny_max_rows() batch rows)
@@ -60,6 +62,9 @@ void launch_gemm_tc(const TmaMap& a_map, const TmaMap& b_map64, const TcLaunch& 
 // round-1 1-CTA 128 x 128 tile GEMM (B map: 128-row boxes, SwiGLU 64), kept for A/B (option "tc_pair" 0)
 void launch_gemm_tc_v1(const TmaMap& a_map, const TmaMap& b_map, const TcLaunch& l, cudaStream_t s);
 extern int g_pair_bn;
+extern int g_pair_sk;
+size_t pair_sk_scratch_floats();
+int pair_sk_counters();
 int skinny_max_rows();      // widest batch of the skinny GEMM (rows; > 256 run as 256-row slices)
 int skinny_cols(int rows);  // MMA N used for `rows` batch rows (16/32/64/128/256)
 size_t skinny_partial_floats(int N, int K);  // split-K scratch the skinny GEMM may use for one matrix

@@ -533,3 +533,70 @@ def test_bf16_prefill_tensor_core_attention_matches_cascade(config, plen):
     rel = np.abs(l1[0] - l0[0]).max() / np.abs(l0[0]).max()
     assert rel < 2e-2, rel
     assert t1[0] == t0[0]
+
+
+def _branch_batch(eng, ids, n_branches, n_out, stride, capture=True):
+    """Trunk prefill + `n_branches` forks (fork points `stride` apart) decoded
+    as one continuous batch; returns per-branch (tokens, logits)."""
+    trunk = eng.seq_create()
+    eng.prefill(trunk, ids[:-1], 99, M.VIS_ID)
+    reqs = []
+    for j in range(n_branches):
+        b = eng.seq_fork(trunk, len(ids) - 1 - stride * j)
+        r = eng.submit(b, M.TAG_BASE + (j % 32), n_out, 1)
+        if capture:
+            eng.capture_logits(r)
+        reqs.append(r)
+    eng.set_slots(n_branches)
+    eng.run(-1)
+    out = [(eng.request_tokens(r, n_out), eng.request_logits(r, n_out) if capture else None) for r in reqs]
+    for r in reqs:
+        eng.request_release(r)
+    return out
+
+
+@pytest.mark.parametrize("config,n_branches,cap,plen", [("small", 24, 16, 900), ("small", 24, 3, 900),
+                                                        ("7b_2layer", 20, 4, 700)])
+def test_bf16_span_attention_matches_page_items(config, n_branches, cap, plen):
+    """Wide chain decode ticks (> 16 rows: rows of a span split over two items)
+    through the tensor-core span attention (attn_span.cu; `span_cap` pages per
+    span, so several trunk spans per row and the fused slot merge) vs the
+    per-page CUDA-core cascade kernel: every branch's first-step logits within
+    bf16 tolerance, first greedy tokens equal (all but one: bf16 near-ties)."""
+    from oracle.backend import frame
+    ids = frame(config, list(range(16)), list(range(900, 900 + plen)), "plan")
+    res = {}
+    for span in (1, 0):
+        eng = Engine(config, dtype="bf16", seed=0, kv_pages=512, max_rows=512)
+        eng.set_option("mk", 0)
+        eng.set_option("span_attn", span)
+        eng.set_option("span_cap", cap)
+        res[span] = _branch_batch(eng, ids, n_branches, 3, 13)
+        eng.close()
+    worst = 0.0
+    for (t1, l1), (t0, l0) in zip(res[1], res[0]):
+        worst = max(worst, float(np.abs(l1[0] - l0[0]).max() / np.abs(l0[0]).max()))
+    assert worst < 2e-2, worst
+    same = sum(a[0][0] == b[0][0] for a, b in zip(res[1], res[0]))
+    assert same >= n_branches - 1, (same, n_branches)
+
+
+def test_bf16_persistent_tick_multi_round_attention():
+    """The tick kernel's attention phase over more (page, head) pairs than one
+    round of its slots (kAttnSlots x grid ~ 888 on B200): 16 branches over a
+    1.5k-token trunk of the 32-head 7b_2layer model (~1.3k pairs, two rounds,
+    round >= 1 items and their K/V L2 prefetch) vs the kernel chain."""
+    from oracle.backend import frame
+    ids = frame("7b_2layer", list(range(16)), list(range(900, 2150)), "plan")
+    res = {}
+    for mk in (1, 0):
+        eng = Engine("7b_2layer", dtype="bf16", seed=0, kv_pages=512, max_rows=512)
+        eng.set_option("mk", mk)
+        res[mk] = _branch_batch(eng, ids, 16, 3, 40)
+        eng.close()
+    worst = 0.0
+    for (t1, l1), (t0, l0) in zip(res[1], res[0]):
+        worst = max(worst, float(np.abs(l1[0] - l0[0]).max() / np.abs(l0[0]).max()))
+    assert worst < 2e-2, worst
+    same = sum(a[0][0] == b[0][0] for a, b in zip(res[1], res[0]))
+    assert same >= 15, same
