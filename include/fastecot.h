@@ -71,6 +71,16 @@ int fe_seq_len(fe_engine* e, int32_t seq, int32_t* len);
  * `vis_id` take row (pos-1) of the vision embedding seeded by `vision_seed` */
 int fe_prefill(fe_engine* e, int32_t seq, const int32_t* ids, int32_t n, uint64_t vision_seed, int32_t vis_id);
 
+/* reuse-as-draft verification (replaces nothing in the reference: the
+ * SyntheticBackend's reuse draw, backends.py:202-204, returns prev_content
+ * verbatim; here prev_content is checked as a greedy draft): one batched
+ * forward extends seqs[i] by counts[i] ids (concatenated in `ids`); out[k] =
+ * greedy token after input k.  Then keep the accepted prefix: */
+int fe_verify(fe_engine* e, int32_t n_seqs, const int32_t* seqs, const int32_t* counts, const int32_t* ids,
+              int32_t* out);
+/* drop positions >= len (pages past the end are released) */
+int fe_seq_truncate(fe_engine* e, int32_t seq, int32_t len);
+
 /* continuous batcher: a request decodes `length` greedy tokens on `seq`,
  * the first iteration consuming `first_id` */
 int fe_set_slots(fe_engine* e, int32_t slots);

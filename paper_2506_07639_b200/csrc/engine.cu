@@ -1375,6 +1375,84 @@ int fe_seq_len(fe_engine* e, int32_t seq, int32_t* len) {
   return guarded(e, [&] { *len = seq_at(e, seq).len; });
 }
 
+// Draft verification (reuse-as-draft): every listed
+// sequence is extended by counts[i] input ids in ONE batched forward whose
+// rows all run the lm_head; the greedy token after each input lands in
+// out[] (same order as ids).  The caller keeps the verified prefix and
+// truncates the rest (fe_seq_truncate).  Rows beyond the lane's capacity run
+// as further forwards (each sequence's rows stay in order).
+int fe_verify(fe_engine* e, int32_t n_seqs, const int32_t* seqs, const int32_t* counts, const int32_t* ids,
+              int32_t* out) {
+  return guarded(e, [&] {
+    Lane& ln = e->lanes[0];
+    int total = 0;
+    for (int i = 0; i < n_seqs; i++) {
+      if (counts[i] < 1) throw Error("verify: every sequence needs >= 1 input");
+      seq_at(e, seqs[i]);
+      total += counts[i];
+    }
+    const int n_slots = (total + kRequestCap - 1) / kRequestCap;
+    if ((int)e->free_arena.size() < n_slots) throw Error("verify: token arena exhausted");
+    std::vector<int> arena(e->free_arena.end() - n_slots, e->free_arena.end());
+    e->free_arena.resize(e->free_arena.size() - n_slots);
+    auto give_back = [&]() { for (int a : arena) e->free_arena.push_back(a); };
+    try {
+      std::vector<RowIn> rows;
+      int chunks = 0, k = 0;
+      for (int i = 0; i < n_seqs; i++) {
+        int pos = e->seqs[seqs[i]].len;
+        for (int j = 0; j < counts[i]; j++, k++, pos++) {
+          const int c = pos / FE_PAGE + 1;
+          if (!rows.empty() && ((int)rows.size() >= ln.max_rows || chunks + c > ln.max_partials)) {
+            forward(e, ln, rows, 0);
+            rows.clear();
+            chunks = 0;
+          }
+          if (ids[k] < 0 || ids[k] >= e->m.V) throw Error("verify: token id out of range");
+          RowIn r{};
+          r.seq = seqs[i];
+          r.pos = pos;
+          r.tok = ids[k];
+          r.tok_src = -1;
+          r.vis_row = -1;
+          r.out_idx = arena[k / kRequestCap] * kRequestCap + k % kRequestCap;
+          r.logit_row = -1;
+          r.head = true;
+          rows.push_back(r);
+          chunks += c;
+        }
+      }
+      if (!rows.empty()) forward(e, ln, rows, 0);
+      CK(cudaStreamSynchronize(ln.stream));
+      for (int a = 0; a < n_slots; a++) {
+        const int n = std::min(kRequestCap, total - a * kRequestCap);
+        CK(cudaMemcpy(out + (size_t)a * kRequestCap, e->out_tokens + (size_t)arena[a] * kRequestCap,
+                      sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
+      }
+      e->d2h_bytes += (int64_t)sizeof(int32_t) * total;
+      e->h2d_bytes += 0;
+    } catch (...) {
+      give_back();
+      throw;
+    }
+    give_back();
+  });
+}
+
+// Drop positions >= len of a sequence (its pages past the new end are released).
+int fe_seq_truncate(fe_engine* e, int32_t seq, int32_t len) {
+  return guarded(e, [&] {
+    Seq& s = seq_at(e, seq);
+    if (len < 0 || len > s.len) throw Error("truncate: length outside the sequence");
+    const int keep = (len + FE_PAGE - 1) / FE_PAGE;
+    while ((int)s.pages.size() > keep) {
+      release_page(e, s.pages.back());
+      s.pages.pop_back();
+    }
+    s.len = len;
+  });
+}
+
 int fe_prefill(fe_engine* e, int32_t seq, const int32_t* ids, int32_t n, uint64_t vision_seed, int32_t vis_id) {
   return guarded(e, [&] { prefill(e, seq, ids, n, vision_seed, vis_id); });
 }

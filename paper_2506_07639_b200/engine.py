@@ -38,7 +38,8 @@ class FeConfig(ctypes.Structure):
 
 EXPORTS = (
     "fe_engine_create", "fe_engine_destroy", "fe_weights_init_random", "fe_last_error",
-    "fe_seq_create", "fe_seq_fork", "fe_seq_free", "fe_seq_len", "fe_prefill", "fe_set_slots",
+    "fe_seq_create", "fe_seq_fork", "fe_seq_free", "fe_seq_len", "fe_prefill", "fe_verify", "fe_seq_truncate",
+    "fe_set_slots",
     "fe_set_slots_lane", "fe_submit_lane", "fe_run_lane", "fe_stream_lane",
     "fe_submit", "fe_run", "fe_request_tokens", "fe_request_release", "fe_request_capture_logits",
     "fe_request_logits", "fe_in_flight", "fe_synchronize", "fe_stream", "fe_stats", "fe_profile",
@@ -68,6 +69,8 @@ def load_library(path: Path = LIB_PATH) -> ctypes.CDLL:
         "fe_seq_free": [vp, i32],
         "fe_seq_len": [vp, i32, _c_int_p],
         "fe_prefill": [vp, i32, vp, i32, u64, i32],
+        "fe_verify": [vp, i32, vp, vp, vp, vp],
+        "fe_seq_truncate": [vp, i32, i32],
         "fe_set_slots": [vp, i32],
         "fe_set_slots_lane": [vp, i32, i32],
         "fe_submit_lane": [vp, i32, i32, i32, i32, i32, _c_int_p],
@@ -173,6 +176,21 @@ class Engine:
         if a.size:
             self._check(self.lib.fe_prefill(self._h, seq, _np_ptr(a), int(a.size),
                                             ctypes.c_uint64(vision_seed & 0xFFFFFFFFFFFFFFFF), vis_id))
+
+    def verify(self, seqs, inputs) -> list[np.ndarray]:
+        """Reuse-as-draft verification: extend every `seqs[i]` by `inputs[i]`
+        in one batched forward; returns, per sequence, the greedy token after
+        each input (the caller truncates what it rejects)."""
+        counts = np.asarray([len(x) for x in inputs], dtype=np.int32)
+        flat = np.ascontiguousarray(np.concatenate([np.asarray(x, dtype=np.int32) for x in inputs]))
+        sq = np.ascontiguousarray(np.asarray(seqs, dtype=np.int32))
+        out = np.empty(flat.size, dtype=np.int32)
+        self._check(self.lib.fe_verify(self._h, int(sq.size), _np_ptr(sq), _np_ptr(counts), _np_ptr(flat),
+                                       _np_ptr(out)))
+        return np.split(out, np.cumsum(counts)[:-1])
+
+    def seq_truncate(self, seq: int, length: int) -> None:
+        self._check(self.lib.fe_seq_truncate(self._h, seq, length))
 
     # -- batcher -------------------------------------------------------------
     def set_slots(self, slots: int) -> None:

@@ -71,7 +71,7 @@ class DeviceRequest:
     """One branch request on the device."""
 
     __slots__ = ("name", "length", "truncated", "tag", "branch", "priority", "lane", "req", "tokens",
-                 "error", "log", "on_complete", "waiter", "ids", "vseed", "reserve")
+                 "error", "log", "on_complete", "waiter", "ids", "vseed", "reserve", "draft", "prefix")
 
     def __init__(self, name, length, truncated, tag, priority, ids, vseed):
         self.name, self.length, self.truncated = name, length, truncated
@@ -86,6 +86,8 @@ class DeviceRequest:
         self.log = None
         self.on_complete: Optional[Callable[["DeviceRequest"], None]] = None
         self.waiter = None                 # engine that owns completion (two-stream lane 1)
+        self.draft: tuple = ()             # prev_content to verify as a greedy draft (draft_reuse)
+        self.prefix: tuple = ()            # tokens already produced by the draft verification
 
     @property
     def done(self) -> bool:
@@ -164,7 +166,7 @@ class EngineBackend:
     def __init__(self, config="tiny", dtype: str = "f32", seed: int = 0,
                  profile: SyntheticProfile | None = None, device: int = 0,
                  engine: Engine | None = None, trunk_cache: int = 64, async_mode: str = "lockstep",
-                 request_log: list | None = None, **engine_kw):
+                 request_log: list | None = None, draft_reuse: bool = False, **engine_kw):
         """`async_mode="lockstep"`: the async runner's device engine advances
         exactly as many decode iterations as each control step's action needs
         (the reference landing order, byte-comparable traces);
@@ -172,7 +174,12 @@ class EngineBackend:
         between and during control steps, the action joins its ticks at high
         priority (`BackgroundAsyncEngine`).  `request_log`: if a list,
         every completed request appends (context, prefix, step name,
-        prev_content, tokens) -- used by per-request parity checks."""
+        prev_content, tokens) -- used by per-request parity checks.
+        `draft_reuse`: verify each synchronous request's `prev_content` as a
+        greedy draft in one batched forward before decoding (SURVEY §8(f)
+        rank 1; `_verify_drafts`); the tokens are those of plain greedy
+        decoding, only the decode iterations for the accepted prefix are
+        skipped."""
         self.cfg = get_config(config)
         if async_mode not in ("lockstep", "background"):
             raise ValueError(f"async_mode must be 'lockstep' or 'background', got {async_mode!r}")
@@ -195,6 +202,10 @@ class EngineBackend:
         self._slots = 8
         self._fixed_slots = False    # an async engine fixes the batcher to the runner's slots
         self.requests = 0
+        self.draft_reuse = draft_reuse
+        self.draft_stats = {"requests": 0, "drafted": 0, "draft_tokens": 0, "accepted_tokens": 0,
+                            "verified_tokens": 0, "resolved_by_verify": 0, "verify_forwards": 0,
+                            "verify_rows": 0}
 
     @contextlib.contextmanager
     def _foreground(self):
@@ -244,8 +255,69 @@ class EngineBackend:
         with self._foreground():
             self._materialize()
             pending, self._pending = self._pending, []
+            if self.draft_reuse:
+                self._verify_drafts(pending)
             for h in pending:
-                self._submit(h, 0)
+                if h.tokens is None:
+                    self._submit(h, 0)
+
+    def _verify_drafts(self, hs: list[DeviceRequest]) -> None:
+        """Reuse-as-draft (anchor: the reference's reuse
+        draw returns prev_content verbatim, `backends.py:202-204`, and the
+        runners pass it at `schedulers.py:404`, `:478`).  For every request
+        with a draft d (its prev_content, cut to length - 1): one batched
+        forward over all of them feeds [TAG, d_0 .. d_m-1] after the branch
+        and returns the greedy tokens g_0 .. g_m; the accepted prefix is the
+        longest a with g_i == d_i (i < a), so g_0 .. g_a are exactly the
+        tokens greedy decoding would emit (each was computed from the true
+        prefix).  The branch keeps the KV of those a + 1 inputs (the rest is
+        truncated) and decodes only the remaining length - a - 1 tokens,
+        starting from g_a -- or completes with no decode at all."""
+        st = self.draft_stats
+        todo = []
+        for h in hs:
+            if h.error is not None or h.tokens is not None or h.branch < 0:
+                continue
+            st["requests"] += 1
+            d = h.draft[: max(0, h.length - 1)]
+            if not d:
+                continue
+            todo.append((h, d))
+        if not todo:
+            return
+        inputs = [[h.tag] + text_ids(d) for h, d in todo]
+        eng = self.engine
+        try:
+            outs = eng.verify([h.branch for h, _ in todo], inputs)
+        except EngineError as exc:
+            for h, _ in todo:
+                h.error = exc
+                self._release(h)
+            return
+        st["verify_forwards"] += 1
+        st["verify_rows"] += sum(len(x) for x in inputs)
+        for (h, d), g in zip(todo, outs):
+            g = [int(x) for x in g]
+            a = 0
+            while a < len(d) and g[a] == int(d[a]):
+                a += 1
+            verified = tuple(g[: a + 1])
+            base = h.ids.size
+            eng.seq_truncate(h.branch, base + len(verified))
+            st["drafted"] += 1
+            st["draft_tokens"] += len(d)
+            st["accepted_tokens"] += a
+            st["verified_tokens"] += len(verified)
+            if len(verified) >= h.length:
+                h.tokens = verified[: h.length]
+                st["resolved_by_verify"] += 1
+                if self.request_log is not None and h.log is not None:
+                    self.request_log.append(h.log + (h.tokens,))
+                if h.on_complete is not None:
+                    h.on_complete(h)
+                self._release(h)
+            else:
+                h.prefix = verified
 
     def _resolve(self, h: DeviceRequest) -> None:
         if h.waiter is not None:
@@ -315,6 +387,8 @@ class EngineBackend:
             raise EngineError(f"too many live requests ({self._live})")
         h = DeviceRequest(spec.name, plan.length, plan.truncated, step_tag(spec), priority, ids,
                           vision_seed(ctx.observation))
+        if self.draft_reuse and priority == PRIO_REASONING:
+            h.draft = tuple(int(x) for x in prev)
         self._reserve_pages(h)
         self._live += 1
         if self.request_log is not None:
@@ -374,7 +448,8 @@ class EngineBackend:
             return
         try:
             h.lane = lane
-            h.req = self.engine.submit_lane(lane, h.branch, h.tag, h.length, h.priority)
+            first = h.prefix[-1] if h.prefix else h.tag
+            h.req = self.engine.submit_lane(lane, h.branch, first, h.length - len(h.prefix), h.priority)
         except EngineError as exc:
             h.error = exc
             self._release(h)
@@ -415,7 +490,7 @@ class EngineBackend:
             h = self._owners.pop(req, None)
             if h is None:
                 raise EngineError(f"request {req} completed without an owner")
-            h.tokens = tuple(eng.request_tokens(h.req, h.length))
+            h.tokens = h.prefix + tuple(eng.request_tokens(h.req, h.length - len(h.prefix)))
             if self.request_log is not None and h.log is not None:
                 self.request_log.append(h.log + (h.tokens,))
             if h.on_complete is not None:

@@ -36,6 +36,25 @@ def hash_tokens(vseed: int, ids, first_id: int, n: int) -> tuple:
     return tuple(int(t) for t in rng.integers(0, M.TEXT_VOCAB, size=n))
 
 
+def ar_token(vseed: int, ids) -> int:
+    """Autoregressive stand-in for one greedy step: the next token is a hash
+    of everything the sequence holds (vision seed + every input so far)."""
+    h = hashlib.blake2b(digest_size=8)
+    h.update(int(vseed).to_bytes(8, "little"))
+    h.update(np.asarray(ids, dtype=np.int32).tobytes())
+    return int.from_bytes(h.digest(), "little") % M.TEXT_VOCAB
+
+
+def ar_tokens(vseed: int, ids, first_id: int, n: int) -> tuple:
+    seq = [int(i) for i in ids] + [int(first_id)]
+    out = []
+    for _ in range(n):
+        t = ar_token(vseed, seq)
+        out.append(t)
+        seq.append(t)
+    return tuple(out)
+
+
 class _Lane:
     def __init__(self):
         self.slots: list = [None] * 8
@@ -43,8 +62,10 @@ class _Lane:
 
 
 class FakeEngine:
-    def __init__(self, cfg="tiny", max_slots: int = 512):
+    def __init__(self, cfg="tiny", max_slots: int = 512, autoregressive: bool = False):
         self.cfg = M.get_config(cfg)
+        self.autoregressive = autoregressive   # outputs from ar_tokens (draft verification tests)
+        self.verify_calls = 0
         self.max_slots = max_slots
         self.lock = threading.RLock()
         self.seqs: dict[int, tuple[int, list]] = {}     # seq -> (vseed, ids)
@@ -88,6 +109,29 @@ class FakeEngine:
             self.prefilled_tokens += len(ids)
             self.prefill_calls += 1
 
+    def verify(self, seqs, inputs) -> list:
+        """fe_verify: extend each sequence by its inputs; the token after each."""
+        if not self.autoregressive:
+            raise B.EngineError("verify needs the autoregressive fake engine")
+        with self.lock:
+            self.verify_calls += 1
+            outs = []
+            for s, xs in zip(seqs, inputs):
+                vseed, ids = self.seqs[s]
+                g = []
+                for x in xs:
+                    ids.append(int(x))
+                    g.append(ar_token(vseed, ids))
+                outs.append(np.asarray(g, dtype=np.int32))
+            return outs
+
+    def seq_truncate(self, seq: int, n: int) -> None:
+        with self.lock:
+            vseed, ids = self.seqs[seq]
+            if n > len(ids):
+                raise B.EngineError("truncate beyond the sequence")
+            self.seqs[seq] = (vseed, ids[:n])
+
     # batcher
     def set_slots(self, n: int) -> None:
         self.set_slots_lane(0, n)
@@ -107,7 +151,8 @@ class FakeEngine:
             r = self.free_ids.pop(0)
             self.reqs[r] = dict(lane=lane, remaining=length, state=0, seqno=self._seqno,
                                 prio=0 if priority == PRIO_ACTION else 1,
-                                out=hash_tokens(vseed, ids, first_id, length))
+                                out=(ar_tokens if self.autoregressive else hash_tokens)(vseed, ids, first_id,
+                                                                                       length))
             self._seqno += 1
             self.lanes[lane].waiting.append(r)
             return r
@@ -203,7 +248,7 @@ class HashBackend:
         return B.StepGenerator(toks, truncated=plan.truncated)
 
 
-def fake_backend(profile=None, **kw):
+def fake_backend(profile=None, autoregressive=False, **kw):
     from paper_2506_07639_b200.engine_backend import EngineBackend
-    eng = FakeEngine()
+    eng = FakeEngine(autoregressive=autoregressive)
     return EngineBackend("tiny", engine=eng, profile=profile, **kw), eng

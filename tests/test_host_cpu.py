@@ -304,3 +304,50 @@ def test_kv_pool_exhaustion_is_a_policy_error():
     assert r.failures                       # some branches could not reserve their pages
     assert len(r.failures) < len(schema.steps)
     assert be._live == 0 and be._reserved == 0
+
+
+# ------------------------------------------------------- reuse-as-draft ----
+def _fixed_obs_episode(mode, backend, schema, T, obs=b"same-frame"):
+    """Episode whose observation never changes (repeated control steps on one
+    frame): the reasoning a branch emits at t equals the content it was
+    conditioned on at t - 1, so prev_content is a correct greedy draft."""
+    runner = RS.make_runner(RS.SchedulerConfig(mode=mode, slots=8, latency=MODEL), backend, schema)
+    ctx_instr = "pick up the object and place it on the target"
+    return [runner.step(backend.encode(ctx_instr, obs), t) for t in range(T)]
+
+
+@pytest.mark.parametrize("mode", ("sequential", "parallel_sync"))
+@pytest.mark.parametrize("fixed", (True, False))
+def test_draft_reuse_is_exactly_greedy(mode, fixed):
+    """Reuse-as-draft changes how tokens are produced,
+    not which: traces are byte-identical with and without it, over an
+    autoregressive stand-in model.  On a fixed frame the drafts are accepted
+    (decode iterations skipped); with a new frame every step they are not."""
+    schema = default_schema()
+    runs = {}
+    for draft in (False, True):
+        be, eng = fake_backend(autoregressive=True, draft_reuse=draft)
+        if fixed:
+            res = _fixed_obs_episode(mode, be, schema, 6)
+        else:
+            res, _ = episode(mode, be, schema, 6, seed=5)
+        runs[draft] = (lines(res, schema), be.draft_stats, eng)
+    assert runs[True][0] == runs[False][0]
+    st = runs[True][1]
+    assert st["drafted"] > 0 and runs[True][2].verify_calls > 0
+    if fixed:
+        assert st["accepted_tokens"] > 0.9 * st["draft_tokens"], st
+        assert st["resolved_by_verify"] > 0, st
+    else:
+        assert st["accepted_tokens"] < 0.05 * st["draft_tokens"], st
+    assert runs[False][1]["drafted"] == 0
+
+
+def test_draft_reuse_skips_decode_ticks_on_a_fixed_frame():
+    schema = default_schema()
+    ticks = {}
+    for draft in (False, True):
+        be, eng = fake_backend(autoregressive=True, draft_reuse=draft)
+        _fixed_obs_episode("parallel_sync", be, schema, 5)
+        ticks[draft] = len(eng.occupancy_log)
+    assert ticks[True] < 0.5 * ticks[False], ticks
