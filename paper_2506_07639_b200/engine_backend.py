@@ -377,23 +377,40 @@ class EngineBackend:
         changes yet -- the trunk prefill and the fork happen when the request
         is materialised (`_materialize`), longest input first."""
         plan = length_plan(self.profile, ctx, spec, prev)  # BackendError on unknown step
-        ids = np.asarray(context_ids(ctx, self.cfg) + text_ids(prefix), dtype=np.int32)
-        if plan.length > REQUEST_CAP:
-            raise EngineError(f"step {spec.name!r}: {plan.length} tokens exceed the request cap {REQUEST_CAP}")
-        if ids.size + 1 + plan.length > ROPE_MAX_POS:
-            raise EngineError(f"step {spec.name!r}: context {ids.size} + {plan.length} tokens exceed "
-                              f"max_pos {ROPE_MAX_POS}")
-        if self._live >= self._live_cap:
-            raise EngineError(f"too many live requests ({self._live})")
-        h = DeviceRequest(spec.name, plan.length, plan.truncated, step_tag(spec), priority, ids,
-                          vision_seed(ctx.observation))
+        h = self._new_request(ctx, prefix, spec, plan.length, plan.truncated, priority)
         if self.draft_reuse and priority == PRIO_REASONING:
             h.draft = tuple(int(x) for x in prev)
-        self._reserve_pages(h)
-        self._live += 1
         if self.request_log is not None:
             h.log = (ctx, tuple(prefix), spec.name, tuple(prev))
         return h
+
+    def _new_request(self, ctx: _rt.Context, prefix, spec: _rt.StepSpec, length: int, truncated: bool,
+                     priority: int) -> DeviceRequest:
+        ids = np.asarray(context_ids(ctx, self.cfg) + text_ids(prefix), dtype=np.int32)
+        if not 1 <= length <= REQUEST_CAP:
+            raise EngineError(f"step {spec.name!r}: {length} tokens outside the request cap [1, {REQUEST_CAP}]")
+        if ids.size + 1 + length > ROPE_MAX_POS:
+            raise EngineError(f"step {spec.name!r}: context {ids.size} + {length} tokens exceed "
+                              f"max_pos {ROPE_MAX_POS}")
+        if self._live >= self._live_cap:
+            raise EngineError(f"too many live requests ({self._live})")
+        h = DeviceRequest(spec.name, length, truncated, step_tag(spec), priority, ids,
+                          vision_seed(ctx.observation))
+        self._reserve_pages(h)
+        self._live += 1
+        return h
+
+    def begin_completion(self, context: _rt.Context, prefix, step_name: str, length: int) -> StepGenerator:
+        """A plain completion of exactly `length` greedy tokens (no length
+        oracle, no draft): the request the `/v1/completions` front serves
+        (server.py).  Deferred like `begin_step`: requests prepared together
+        decode as one batch when the first is read."""
+        spec = _rt.StepSpec(step_name, _rt.LOW, max(1, int(length)))
+        with self._foreground():
+            h = self._new_request(context, prefix, spec, int(length), False, PRIO_REASONING)
+            self._pending.append(h)
+            self._ensure_slots(len(self._pending) + len(self._owners))
+        return DeviceStepGenerator(h, self)
 
     def _covered(self, vseed: int, ids: np.ndarray) -> int:
         """Longest prefix of `ids` whose KV exists (a cached trunk) or will

@@ -646,3 +646,28 @@ def test_draft_reuse_accepts_on_a_fixed_frame(schema, config, dtype):
     assert runs[True][2] < runs[False][2]
     if dtype == "f32":
         assert runs[True][0] == runs[False][0]
+
+
+# ------------------------------------------------------ /v1/completions ----
+def test_completions_server_tokens_equal_the_oracle(schema, oracle_tiny):
+    """The reference client (`remote_complete`, backends.py:285-326) against
+    the engine's /v1/completions front (server.py), tiny fp32: the reply's
+    token ids are the CPU oracle's greedy continuation of the parsed request
+    (reference default prompt -> context + prefix framing + step tag)."""
+    from ecot_sched.backends import RemoteEndpoint, default_prompt_builder, remote_complete
+
+    from oracle.backend import frame
+    from paper_2506_07639_b200.backends import encode_context
+    from paper_2506_07639_b200.server import CompletionServer
+    be = EngineBackend("tiny", dtype="f32", seed=0, kv_pages=512)
+    try:
+        with CompletionServer(be, observation=b"frame-7") as srv:
+            step = schema.steps[3]
+            ctx = encode_context("put the block in the bowl", b"frame-7")
+            res = remote_complete(RemoteEndpoint(srv.url), default_prompt_builder(ctx, (11, 22, 33), step), 9)
+        got = [int(t) for t in res.text.split()]
+        ids = frame("tiny", ctx.encoded, (11, 22, 33), step.name)
+        want, _ = oracle_tiny.generate(ids, M.vision_seed(b"frame-7"), 9)
+        assert got == list(want)
+    finally:
+        be.close()
