@@ -512,6 +512,8 @@ def main():
         "cpu_baseline": cpu,
         "clocks": r["clocks"],
         "breakdown_ms_per_step_eager": {k: v["ms"] / steps_prof for k, v in prof.items()},
+        "breakdown_gbs_eager": {k: (v["bytes"] / 1e9) / (v["ms"] / 1e3) for k, v in prof.items()
+                                if v["ms"] > 0 and v["bytes"] > 0},
         "decode_ticks_per_step": (s1["ticks"] - s0["ticks"]) / K,
         "results_gathered": token_summary(r["shards"]),
         "bf16_token_match": parity.get("summary") if parity else None,

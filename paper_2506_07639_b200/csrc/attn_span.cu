@@ -1,25 +1,26 @@
-// Span cascade decode attention on tensor cores (bf16 path, head_dim 128):
-// the attention of the wide decode ticks that run the per-matrix kernel chain
-// (> 16 rows: config 4's batched episodes, the background lane).
+// Row-group cascade decode attention on tensor cores (bf16 path, head_dim
+// 128): the attention of the decode ticks that run the per-matrix kernel
+// chain (> 16 rows: config 4's batched episodes, the background lane).
 //
-// Work item = (span, head).  A span is a run of consecutive KV pages whose
-// rows are identical for every page (a trunk shared by the branches forked
-// from it, or one branch's own pages), with <= 16 query rows; all pages but
-// the last are full for every row.  The CTA (4 warps) streams the span's
-// K/V page tiles through an NST-stage TMA ring -- a 2-D tensor map over the
-// whole pool viewed as [rows][128] bf16, 64 x 64 boxes with 128-byte swizzle,
-// so every fragment load is bank-conflict free -- and each warp owns 16 of
-// the 64 keys of every page: S = Q K^T and O += P V on mma.sync m16n8k16
-// (rows padded to 16), online softmax in the exp2 domain.  The four warps'
-// (m, l, o) states are combined in shared memory; a row whose attention is
-// this one span writes its bf16 output directly, otherwise the span's partial
-// goes to the row's slot and the CTA completing the row's last span merges the
-// slots in slot order (deterministic) -- no separate merge launch.
+// Work item = (row group, page range, head).  A row group is <= 16 query rows
+// connected through shared KV pages (a trunk and the branches forked off it,
+// engine.cu forward()); its item walks the union of the rows' pages in chunk
+// order -- every page staged ONCE per head, whichever rows share it -- with
+// one online-softmax state per row and a per-page row mask (rows that do not
+// hold the page see no key of it; a row's last page is cut at its valid
+// count).  So a row's whole attention is normally one item and its output is
+// written directly: no partials, no merge.  Only when the groups alone do not
+// fill the GPU are a group's pages split into ranges ("parts"); then each part
+// writes a per-row partial and the CTA completing a row's last part merges
+// the parts in part order (deterministic).
 //
-// Versus the per-page item kernel (one CUDA-core warp per row per page, a
-// partial per page): every K/V byte is still staged exactly once per head,
-// but the dot products run on the tensor pipe and the partial traffic drops
-// by the span length.
+// Staging: an NST-stage TMA ring over the pool viewed as [rows][128] bf16,
+// 64 x 64 boxes with 128-byte swizzle (bank-conflict-free ldmatrix); a
+// partially filled page loads only its 16-key blocks that hold valid keys.
+// Each of the 4 warps owns 16 keys of every page: S = Q K^T and O += P V on
+// mma.sync m16n8k16 (rows padded to 16), softmax in the exp2 domain, and a
+// warp whose keys no row can see skips the page (so unloaded rows are never
+// read).  The four warps' states are combined in shared memory.
 #include "common.cuh"
 #include "engine_internal.h"
 #include "gemm_tc.h"
@@ -59,9 +60,11 @@ __device__ __forceinline__ uint32_t swz(int key, int c16) {
 }
 
 __global__ void __launch_bounds__(128)
-attn_span_kernel(const __grid_constant__ CUtensorMap pool_map, const int32_t* __restrict__ hdr,
+attn_span_kernel(const __grid_constant__ CUtensorMap pool_map, const __grid_constant__ CUtensorMap pool_map16,
+                 const int32_t* __restrict__ hdr,
                  const AttnItem* __restrict__ items, const ItemRow* __restrict__ item_rows,
                  const int32_t* __restrict__ item_slots, const int32_t* __restrict__ span_pages,
+                 const int32_t* __restrict__ span_masks,
                  const RowMeta* __restrict__ rows, const int32_t* __restrict__ row_nspans,
                  const float* __restrict__ q, int L, int layer, int H, int d, float scale_log2,
                  float* __restrict__ partial, int* __restrict__ counters, __nv_bfloat16* __restrict__ out) {
@@ -75,6 +78,7 @@ attn_span_kernel(const __grid_constant__ CUtensorMap pool_map, const int32_t* __
   const int h = blockIdx.y;
   if (tid == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&pool_map) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&pool_map16) : "memory");
     for (int s = 0; s < NST; s++) mbar_init(&full[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -93,20 +97,42 @@ attn_span_kernel(const __grid_constant__ CUtensorMap pool_map, const int32_t* __
     const int rk = (((page * L + layer) * 2 + 0) * H + h) * 64;
     const int rv = rk + H * 64;
     unsigned char* st = smem + s * kStage;
-    mbar_expect_tx(&full[s], kStage);
-    tma_load_2d(st, &pool_map, &full[s], 0, rk);
-    tma_load_2d(st + kBox, &pool_map, &full[s], 64, rk);
-    tma_load_2d(st + 2 * kBox, &pool_map, &full[s], 0, rv);
-    tma_load_2d(st + 3 * kBox, &pool_map, &full[s], 64, rv);
+    const int vmax = (int)((uint32_t)span_masks[it.pad[1] + j] >> 16);
+    if (vmax == 64) {
+      mbar_expect_tx(&full[s], kStage);
+      tma_load_2d(st, &pool_map, &full[s], 0, rk);
+      tma_load_2d(st + kBox, &pool_map, &full[s], 64, rk);
+      tma_load_2d(st + 2 * kBox, &pool_map, &full[s], 0, rv);
+      tma_load_2d(st + 3 * kBox, &pool_map, &full[s], 64, rv);
+    } else {
+      // partially filled last page: only the 16-key blocks holding valid
+      // keys; a warp whose 16 keys are past every row's valid count skips
+      // the page, so the rows never loaded are never read
+      const int nb = (vmax + 15) >> 4;
+      mbar_expect_tx(&full[s], nb * 4 * 16 * 128);
+      for (int b = 0; b < nb; b++) {
+        const int o = b * 16 * 128;
+        tma_load_2d(st + o, &pool_map16, &full[s], 0, rk + 16 * b);
+        tma_load_2d(st + kBox + o, &pool_map16, &full[s], 64, rk + 16 * b);
+        tma_load_2d(st + 2 * kBox + o, &pool_map16, &full[s], 0, rv + 16 * b);
+        tma_load_2d(st + 3 * kBox + o, &pool_map16, &full[s], 64, rv + 16 * b);
+      }
+    }
   };
   if (tid == 0)
     for (int j = 0; j < min(NST, n_pages); j++) issue(j);
 
   // this lane's rows (g, g + 8) of the item and their keys on the last page
   const int ra = g, rb = g + 8;
-  int rowa = -1, rowb = -1, va = 0, vb = 0;
-  if (ra < nr) { const ItemRow ir = item_rows[it.row_begin + ra]; rowa = ir.row; va = ir.valid; }
-  if (rb < nr) { const ItemRow ir = item_rows[it.row_begin + rb]; rowb = ir.row; vb = ir.valid; }
+  int rowa = -1, rowb = -1, va = 0, vb = 0, lpa = -1, lpb = -1;  // last-page position in this item
+  if (ra < nr) {
+    const ItemRow ir = item_rows[it.row_begin + ra];
+    rowa = ir.row; va = ir.valid; lpa = item_slots[it.row_begin + ra] >> 16;
+  }
+  if (rb < nr) {
+    const ItemRow ir = item_rows[it.row_begin + rb];
+    rowb = ir.row; vb = ir.valid; lpb = item_slots[it.row_begin + rb] >> 16;
+  }
   // Q fragments (A operand, k-step ks: dims 16 ks + 2t + {0,1} | + 8), exp2 domain
   uint32_t qa[8][4];
 #pragma unroll
@@ -141,84 +167,88 @@ attn_span_kernel(const __grid_constant__ CUtensorMap pool_map, const int32_t* __
     mbar_wait(&full[s], (j / NST) & 1);
     const unsigned char* ks_ = smem + s * kStage;
     const unsigned char* vs_ = ks_ + 2 * kBox;
-    // S = Q K^T over keys kw .. kw + 15 (two n-tiles of 8)
-    float sc[2][4];
+    // keys visible per row: none if the row does not hold the page, its valid
+    // count on its last page, else the whole page (padded rows see nothing)
+    const uint32_t pmask = (uint32_t)span_masks[it.pad[1] + j] & 0xffffu;
+    const int lima = (pmask >> ra & 1) ? (j == lpa ? va : 64) : 0;
+    const int limb = (pmask >> rb & 1) ? (j == lpb ? vb : 64) : 0;
+    if (__any_sync(0xffffffffu, kw < max(lima, limb))) {  // keys of this warp visible to some row (warp-uniform)
+      // S = Q K^T over keys kw .. kw + 15 (two n-tiles of 8)
+      float sc[2][4];
 #pragma unroll
-    for (int nt = 0; nt < 2; nt++) sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.0f;
+      for (int nt = 0; nt < 2; nt++) sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.0f;
 #pragma unroll
-    for (int kk = 0; kk < 8; kk++) {
-      // matrices: (keys +0-7, dims lo8), (keys +0-7, dims hi8), (keys +8-15, lo8), (keys +8-15, hi8)
-      const int key = kw + 8 * (lm >> 1) + lrow;
-      const int c16 = 2 * kk + (lm & 1);
-      uint32_t b0, b1, b2, b3;
-      asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-                   : "=r"(b0), "=r"(b1), "=r"(b2), "=r"(b3)
-                   : "r"(su32(ks_ + swz(key, c16))));
-      mma16816(sc[0], qa[kk], b0, b1);
-      mma16816(sc[1], qa[kk], b2, b3);
-    }
-    // mask: the last page is partial per row; padded rows see nothing
-    const bool last = j == n_pages - 1;
-    const int lima = rowa < 0 ? 0 : (last ? va : 64), limb = rowb < 0 ? 0 : (last ? vb : 64);
-    float mxa = -INFINITY, mxb = -INFINITY;
+      for (int kk = 0; kk < 8; kk++) {
+        // matrices: (keys +0-7, dims lo8), (keys +0-7, dims hi8), (keys +8-15, lo8), (keys +8-15, hi8)
+        const int key = kw + 8 * (lm >> 1) + lrow;
+        const int c16 = 2 * kk + (lm & 1);
+        uint32_t b0, b1, b2, b3;
+        asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(b0), "=r"(b1), "=r"(b2), "=r"(b3)
+                     : "r"(su32(ks_ + swz(key, c16))));
+        mma16816(sc[0], qa[kk], b0, b1);
+        mma16816(sc[1], qa[kk], b2, b3);
+      }
+      float mxa = -INFINITY, mxb = -INFINITY;
 #pragma unroll
-    for (int nt = 0; nt < 2; nt++) {
-      const int kp = kw + 8 * nt + 2 * t;
-      sc[nt][0] = kp < lima ? sc[nt][0] : -INFINITY;
-      sc[nt][1] = kp + 1 < lima ? sc[nt][1] : -INFINITY;
-      sc[nt][2] = kp < limb ? sc[nt][2] : -INFINITY;
-      sc[nt][3] = kp + 1 < limb ? sc[nt][3] : -INFINITY;
-      mxa = fmaxf(mxa, fmaxf(sc[nt][0], sc[nt][1]));
-      mxb = fmaxf(mxb, fmaxf(sc[nt][2], sc[nt][3]));
-    }
-    mxa = fmaxf(mxa, __shfl_xor_sync(0xffffffffu, mxa, 1));
-    mxa = fmaxf(mxa, __shfl_xor_sync(0xffffffffu, mxa, 2));
-    mxb = fmaxf(mxb, __shfl_xor_sync(0xffffffffu, mxb, 1));
-    mxb = fmaxf(mxb, __shfl_xor_sync(0xffffffffu, mxb, 2));
-    const float na = fmaxf(m0, mxa), nb = fmaxf(m1, mxb);
-    const float ua = na == -INFINITY ? 0.0f : na, ub = nb == -INFINITY ? 0.0f : nb;
-    const float ca = exp2f(m0 - ua), cb = exp2f(m1 - ub);
-    float sa = 0.0f, sb = 0.0f;
+      for (int nt = 0; nt < 2; nt++) {
+        const int kp = kw + 8 * nt + 2 * t;
+        sc[nt][0] = kp < lima ? sc[nt][0] : -INFINITY;
+        sc[nt][1] = kp + 1 < lima ? sc[nt][1] : -INFINITY;
+        sc[nt][2] = kp < limb ? sc[nt][2] : -INFINITY;
+        sc[nt][3] = kp + 1 < limb ? sc[nt][3] : -INFINITY;
+        mxa = fmaxf(mxa, fmaxf(sc[nt][0], sc[nt][1]));
+        mxb = fmaxf(mxb, fmaxf(sc[nt][2], sc[nt][3]));
+      }
+      mxa = fmaxf(mxa, __shfl_xor_sync(0xffffffffu, mxa, 1));
+      mxa = fmaxf(mxa, __shfl_xor_sync(0xffffffffu, mxa, 2));
+      mxb = fmaxf(mxb, __shfl_xor_sync(0xffffffffu, mxb, 1));
+      mxb = fmaxf(mxb, __shfl_xor_sync(0xffffffffu, mxb, 2));
+      const float na = fmaxf(m0, mxa), nb = fmaxf(m1, mxb);
+      const float ua = na == -INFINITY ? 0.0f : na, ub = nb == -INFINITY ? 0.0f : nb;
+      const float ca = exp2f(m0 - ua), cb = exp2f(m1 - ub);
+      float sa = 0.0f, sb = 0.0f;
 #pragma unroll
-    for (int nt = 0; nt < 2; nt++) {
-      sc[nt][0] = exp2f(sc[nt][0] - ua);
-      sc[nt][1] = exp2f(sc[nt][1] - ua);
-      sc[nt][2] = exp2f(sc[nt][2] - ub);
-      sc[nt][3] = exp2f(sc[nt][3] - ub);
-      sa += sc[nt][0] + sc[nt][1];
-      sb += sc[nt][2] + sc[nt][3];
-    }
-    sa += __shfl_xor_sync(0xffffffffu, sa, 1);
-    sa += __shfl_xor_sync(0xffffffffu, sa, 2);
-    sb += __shfl_xor_sync(0xffffffffu, sb, 1);
-    sb += __shfl_xor_sync(0xffffffffu, sb, 2);
-    l0 = l0 * ca + sa;
-    l1 = l1 * cb + sb;
-    m0 = na;
-    m1 = nb;
+      for (int nt = 0; nt < 2; nt++) {
+        sc[nt][0] = exp2f(sc[nt][0] - ua);
+        sc[nt][1] = exp2f(sc[nt][1] - ua);
+        sc[nt][2] = exp2f(sc[nt][2] - ub);
+        sc[nt][3] = exp2f(sc[nt][3] - ub);
+        sa += sc[nt][0] + sc[nt][1];
+        sb += sc[nt][2] + sc[nt][3];
+      }
+      sa += __shfl_xor_sync(0xffffffffu, sa, 1);
+      sa += __shfl_xor_sync(0xffffffffu, sa, 2);
+      sb += __shfl_xor_sync(0xffffffffu, sb, 1);
+      sb += __shfl_xor_sync(0xffffffffu, sb, 2);
+      l0 = l0 * ca + sa;
+      l1 = l1 * cb + sb;
+      m0 = na;
+      m1 = nb;
 #pragma unroll
-    for (int nt = 0; nt < 16; nt++) {
-      o[nt][0] *= ca;
-      o[nt][1] *= ca;
-      o[nt][2] *= cb;
-      o[nt][3] *= cb;
-    }
-    // O += P V over the warp's 16 keys: V^T fragments by ldmatrix.x4.trans
-    uint32_t pa4[4];
-    pa4[0] = pack2(sc[0][0], sc[0][1]);
-    pa4[1] = pack2(sc[0][2], sc[0][3]);
-    pa4[2] = pack2(sc[1][0], sc[1][1]);
-    pa4[3] = pack2(sc[1][2], sc[1][3]);
-    const int vkey = kw + lrow + 8 * (lm & 1);
+      for (int nt = 0; nt < 16; nt++) {
+        o[nt][0] *= ca;
+        o[nt][1] *= ca;
+        o[nt][2] *= cb;
+        o[nt][3] *= cb;
+      }
+      // O += P V over the warp's 16 keys: V^T fragments by ldmatrix.x4.trans
+      uint32_t pa4[4];
+      pa4[0] = pack2(sc[0][0], sc[0][1]);
+      pa4[1] = pack2(sc[0][2], sc[0][3]);
+      pa4[2] = pack2(sc[1][0], sc[1][1]);
+      pa4[3] = pack2(sc[1][2], sc[1][3]);
+      const int vkey = kw + lrow + 8 * (lm & 1);
 #pragma unroll
-    for (int np = 0; np < 8; np++) {
-      const int c16 = 2 * np + (lm >> 1);
-      uint32_t b0, b1, b2, b3;
-      asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
-                   : "=r"(b0), "=r"(b1), "=r"(b2), "=r"(b3)
-                   : "r"(su32(vs_ + swz(vkey, c16))));
-      mma16816(o[2 * np], pa4, b0, b1);
-      mma16816(o[2 * np + 1], pa4, b2, b3);
+      for (int np = 0; np < 8; np++) {
+        const int c16 = 2 * np + (lm >> 1);
+        uint32_t b0, b1, b2, b3;
+        asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(b0), "=r"(b1), "=r"(b2), "=r"(b3)
+                     : "r"(su32(vs_ + swz(vkey, c16))));
+        mma16816(o[2 * np], pa4, b0, b1);
+        mma16816(o[2 * np + 1], pa4, b2, b3);
+      }
     }
     __syncthreads();  // every warp is done with stage s
     if (tid == 0 && j + NST < n_pages) issue(j + NST);
@@ -258,7 +288,8 @@ attn_span_kernel(const __grid_constant__ CUtensorMap pool_map, const int32_t* __
       for (int w = 0; w < 4; w++) M = fmaxf(M, ml[(w * 16 + r) * 2]);
       float Lr = 0.0f;
 #pragma unroll
-      for (int w = 0; w < 4; w++) Lr += ml[(w * 16 + r) * 2 + 1] * exp2f(ml[(w * 16 + r) * 2] - M);
+      for (int w = 0; w < 4; w++)  // a warp (or the whole part) that saw no key of the row has m = -inf, l = 0
+        if (ml[(w * 16 + r) * 2 + 1] > 0.0f) Lr += ml[(w * 16 + r) * 2 + 1] * exp2f(ml[(w * 16 + r) * 2] - M);
       float acc[16];
 #pragma unroll
       for (int e = 0; e < 16; e++) acc[e] = 0.0f;
@@ -280,7 +311,7 @@ attn_span_kernel(const __grid_constant__ CUtensorMap pool_map, const int32_t* __
         *reinterpret_cast<uint4*>(dst + 8) = make_uint4(w4[4], w4[5], w4[6], w4[7]);
       } else {
         const RowMeta m = rows[ir.row];
-        float* pp = partial + ((size_t)(m.chunk_base + item_slots[it.row_begin + r]) * H + h) * (HD + 2);
+        float* pp = partial + ((size_t)(m.chunk_base + (item_slots[it.row_begin + r] & 0xffff)) * H + h) * (HD + 2);
         if ((tid & 7) == 0) { pp[0] = M; pp[1] = Lr; }
 #pragma unroll
         for (int e = 0; e < 16; e++) pp[2 + d0 + e] = acc[e];
@@ -307,7 +338,9 @@ attn_span_kernel(const __grid_constant__ CUtensorMap pool_map, const int32_t* __
     for (int c = 0; c < ns; c++) M = fmaxf(M, __ldcg(base + c * stride));
     float Lr = 0.0f, acc[4] = {0.f, 0.f, 0.f, 0.f};
     for (int c = 0; c < ns; c++) {
-      const float wgt = exp2f(__ldcg(base + c * stride) - M);
+      const float mc = __ldcg(base + c * stride);
+      if (mc == -INFINITY) continue;  // a part holding none of the row's pages
+      const float wgt = exp2f(mc - M);
       Lr += wgt * __ldcg(base + c * stride + 1);
       const float2 v0 = __ldcg(reinterpret_cast<const float2*>(base + c * stride + 2 + 4 * lane));
       const float2 v1 = __ldcg(reinterpret_cast<const float2*>(base + c * stride + 4 + 4 * lane));
@@ -321,8 +354,10 @@ attn_span_kernel(const __grid_constant__ CUtensorMap pool_map, const int32_t* __
 
 }  // namespace
 
-void launch_span_attention(const Fwd& f, const ModelDims& m, const TmaMap& pool_map, const float* q, int layer,
-                           float* partial, void* out, cudaStream_t s) {
+int g_span_dbg = 0;  // engine option "span_dbg" (unused: diagnostics hook)
+
+void launch_span_attention(const Fwd& f, const ModelDims& m, const TmaMap& pool_map, const TmaMap& pool_map16,
+                           const float* q, int layer, float* partial, void* out, cudaStream_t s) {
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(attn_span_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
@@ -330,8 +365,9 @@ void launch_span_attention(const Fwd& f, const ModelDims& m, const TmaMap& pool_
   }
   if (f.item_cap <= 0) return;
   launch_k(attn_span_kernel, dim3(f.item_cap, m.H), dim3(128), (size_t)kSmem, s,
-           *reinterpret_cast<const CUtensorMap*>(pool_map.bytes), f.hdr, f.items, f.item_rows, f.item_slots,
-           f.span_pages, f.rows, f.row_nspans, q, m.L, layer, m.H, m.d, m.attn_scale * 1.4426950408889634f,
+           *reinterpret_cast<const CUtensorMap*>(pool_map.bytes),
+           *reinterpret_cast<const CUtensorMap*>(pool_map16.bytes), f.hdr, f.items, f.item_rows, f.item_slots,
+           f.span_pages, f.span_masks, f.rows, f.row_nspans, q, m.L, layer, m.H, m.d, m.attn_scale * 1.4426950408889634f,
            partial, f.attn_counters, (__nv_bfloat16*)out);
 }
 

@@ -28,6 +28,7 @@
 #include <tuple>
 #include <unordered_map>
 #include <unordered_set>
+#include <functional>
 #include <mutex>
 #include <thread>
 #include <chrono>
@@ -35,6 +36,7 @@
 #include <string>
 #include <unordered_map>
 #include <unordered_set>
+#include <functional>
 #include <vector>
 
 namespace {
@@ -61,7 +63,7 @@ constexpr int kLanes = 2;
 constexpr int kLane1Rows = 64;      // background lane: decode rows only
 
 struct MetaLayout {
-  size_t o_rows, o_items, o_irows, o_heads, o_pages, o_slots, o_nspans, o_spages, total;
+  size_t o_rows, o_items, o_irows, o_heads, o_pages, o_slots, o_nspans, o_spages, o_smasks, total;
   int cap_rows, cap_items, cap_irows, cap_pages;
 };
 
@@ -191,8 +193,10 @@ struct fe_engine {
   bool use_tc = false;
   bool tc_pair = true;  // option "tc_pair": CTA-pair persistent GEMM (0: round-1 128x128 tile GEMM)
   bool span_attn = true;  // option "span_attn": tensor-core span attention for chain decode ticks (bf16)
-  int span_cap = 16;      // option "span_cap": pages per span item
-  fe::TmaMap pool_map{};  // the KV pool as [rows][128] bf16, 64 x 64 boxes (span attention)
+  int span_cap = 8;       // option "span_cap": most page-range parts per row group (1: never split)
+  int n_sm = 148;
+  fe::TmaMap pool_map{};    // the KV pool as [rows][128] bf16, 64 x 64 boxes (span attention)
+  fe::TmaMap pool_map16{};  // same, 64 x 16 boxes (partially filled last pages)
   int tc_min_rows = 17;
   // forwards up to this many rows use the skinny GEMM, wider ones the tile
   // GEMM (option "sk_max_rows"; measured in the engine at 7B: skinny ahead
@@ -515,7 +519,7 @@ void launch_layers(fe_engine* e, Lane& ln, const fe::Fwd& f, int n, bool decode,
     p = decode ? prof_begin(e, ln, PROF_ATTN) : -1;
     if (e->debug_skip & 1) {
     } else if (f.span_mode) {
-      fe::launch_span_attention(f, m, e->pool_map, ws.q, l, ws.partial, ws.attn, st);
+      fe::launch_span_attention(f, m, e->pool_map, e->pool_map16, ws.q, l, ws.partial, ws.attn, st);
     } else if (!decode && f.seq_pages && dt == FE_BF16 && m.hd == 128 && e->prefill_fa) {
       fe::launch_prefill_attention(f, m, ws.q, e->kv_pool, l, ws.attn, st);
     } else {
@@ -665,56 +669,83 @@ void forward(fe_engine* e, Lane& ln, const std::vector<RowIn>& rows, uint64_t vi
                          !(e->mk_on && n <= 16 && n_head == n && e->debug_skip == 0);
   std::vector<fe::AttnItem> items;
   std::vector<fe::ItemRow> irows;
-  std::vector<int32_t> islots, nspans, spages;
+  std::vector<int32_t> islots, nspans, spages, smasks;
   if (span_mode) {
-    nspans.assign(n, 0);
-    std::unordered_set<int> done;
-    for (int i = 0; i < n; i++) {
-      const Seq& s = e->seqs[rows[i].seq];
-      const int last_c = rows[i].pos / FE_PAGE;
-      for (int c = 0; c <= last_c;) {
-        const int pg = s.pages[c];
-        if (done.count(pg)) { c++; continue; }
-        const auto& lst = by_page[pg];
-        // extend while the next chunk's page has the same rows and this one is full for all
-        int c1 = c;
-        auto full_for_all = [&](int page) {
-          for (const auto& rv : by_page[page]) if (rv.second != FE_PAGE) return false;
-          return true;
-        };
-        while (c1 < last_c && c1 - c + 1 < e->span_cap && full_for_all(s.pages[c1])) {
-          const auto& nxt = by_page[s.pages[c1 + 1]];
-          bool same = nxt.size() == lst.size();
-          for (size_t k = 0; same && k < lst.size(); k++) same = nxt[k].first == lst[k].first;
-          if (!same) break;
-          c1++;
-        }
-        const int po = (int)spages.size();
-        for (int cc = c; cc <= c1; cc++) {
-          spages.push_back(s.pages[cc]);
-          done.insert(s.pages[cc]);
-        }
-        const auto& lastl = by_page[s.pages[c1]];  // valid keys on the span's last page
-        for (size_t b = 0; b < lastl.size(); b += kItemRows) {
-          fe::AttnItem it;
-          it.page = s.pages[c];
-          it.chunk = c;
-          it.row_begin = (int)irows.size();
-          it.row_count = (int)std::min<size_t>(kItemRows, lastl.size() - b);
-          it.valid_max = 0;
-          it.pad[0] = c1 - c + 1;
-          it.pad[1] = po;
-          it.pad[2] = 0;
-          for (int j = 0; j < it.row_count; j++) {
-            const int row = lastl[b + j].first;
-            irows.push_back({row, lastl[b + j].second});
-            islots.push_back(nspans[row]++);
-            it.valid_max = std::max(it.valid_max, lastl[b + j].second);
-          }
-          items.push_back(it);
-        }
-        c = c1 + 1;
+    // Row groups (attn_span.cu): rows connected through shared pages (a trunk
+    // and the branches forked off it), <= 16 per group; a group's unit walks
+    // the union of its rows' pages once per head with one softmax state per
+    // row, so a row's whole attention is one unit -- no partials -- unless
+    // the group's pages are split into `parts` ranges to fill the GPU.
+    std::vector<int> parent(n);
+    for (int i = 0; i < n; i++) parent[i] = i;
+    std::function<int(int)> find = [&](int x) { return parent[x] == x ? x : parent[x] = find(parent[x]); };
+    for (auto& kv : by_page)
+      for (size_t k = 1; k < kv.second.size(); k++) {
+        const int ra = find(kv.second[0].first), rb = find(kv.second[k].first);
+        if (ra != rb) parent[std::max(ra, rb)] = std::min(ra, rb);
       }
+    std::map<int, std::vector<int>> comps;  // root -> rows (ascending)
+    for (int i = 0; i < n; i++) comps[find(i)].push_back(i);
+    std::vector<std::vector<int>> groups;
+    for (auto& kv : comps)
+      for (size_t b = 0; b < kv.second.size(); b += kItemRows)
+        groups.emplace_back(kv.second.begin() + b, kv.second.begin() + std::min(kv.second.size(), b + kItemRows));
+    // page-range splits: enough units for ~4 CTAs per SM
+    const int target = 4 * e->n_sm;
+    const int base_units = (int)groups.size() * m.H;
+    const int want_parts = std::max(1, std::min(e->span_cap, (target + base_units - 1) / base_units));
+    nspans.assign(n, 0);
+    for (const auto& grp : groups) {
+      // the union of the group's pages in chunk order, with per page the rows that see it
+      std::map<std::pair<int, int>, std::pair<uint32_t, int>> pg;  // (chunk, page) -> (row mask, valid max)
+      std::vector<int> last_chunk(grp.size());
+      for (size_t k = 0; k < grp.size(); k++) {
+        const Seq& sq = e->seqs[rows[grp[k]].seq];
+        const int pos = rows[grp[k]].pos;
+        last_chunk[k] = pos / FE_PAGE;
+        for (int c = 0; c <= last_chunk[k]; c++) {
+          auto& ent = pg[{c, sq.pages[c]}];
+          ent.first |= 1u << k;
+          ent.second = std::max(ent.second, std::min(FE_PAGE, pos + 1 - c * FE_PAGE));
+        }
+      }
+      std::vector<std::pair<int, int>> plist;  // (chunk, page)
+      for (auto& kv : pg) plist.push_back(kv.first);
+      const int np = (int)plist.size();
+      const int parts = std::min(want_parts, np);
+      for (int part = 0; part < parts; part++) {
+        const int p0 = (int)((long)np * part / parts), p1 = (int)((long)np * (part + 1) / parts);
+        fe::AttnItem it;
+        it.page = plist[p0].second;
+        it.chunk = plist[p0].first;
+        it.row_begin = (int)irows.size();
+        it.row_count = (int)grp.size();
+        it.valid_max = 0;
+        it.pad[0] = p1 - p0;
+        it.pad[1] = (int)spages.size();
+        it.pad[2] = 0;
+        for (int j = p0; j < p1; j++) {
+          const auto& ent = pg[plist[j]];
+          spages.push_back(plist[j].second);
+          smasks.push_back((int32_t)(ent.first | ((uint32_t)ent.second << 16)));
+          it.valid_max = std::max(it.valid_max, ent.second);
+        }
+        for (size_t k = 0; k < grp.size(); k++) {
+          const int row = grp[k];
+          // the row's last page inside this part (position in the part's list), else -1
+          int lastpos = -1, valid = FE_PAGE;
+          const Seq& sq = e->seqs[rows[row].seq];
+          for (int j = p0; j < p1; j++)
+            if (plist[j].first == last_chunk[k] && plist[j].second == sq.pages[last_chunk[k]]) {
+              lastpos = j - p0;
+              valid = rows[row].pos + 1 - last_chunk[k] * FE_PAGE;
+            }
+          irows.push_back({row, valid});
+          islots.push_back(part | (lastpos << 16));
+        }
+        items.push_back(it);
+      }
+      for (int row : grp) nspans[row] = parts;
     }
   } else {
     for (auto& kv : by_page) {
@@ -770,6 +801,8 @@ void forward(fe_engine* e, Lane& ln, const std::vector<RowIn>& rows, uint64_t vi
     std::memcpy(hbuf + L.o_slots, islots.data(), sizeof(int32_t) * islots.size());
     std::memcpy(hbuf + L.o_nspans, nspans.data(), sizeof(int32_t) * nspans.size());
     std::memcpy(hbuf + L.o_spages, spages.data(), sizeof(int32_t) * spages.size());
+    std::memcpy(hbuf + L.o_smasks, smasks.data(), sizeof(int32_t) * smasks.size());
+    copy(L.o_smasks, sizeof(int32_t) * smasks.size());
     copy(L.o_slots, sizeof(int32_t) * islots.size());
     copy(L.o_nspans, sizeof(int32_t) * nspans.size());
     copy(L.o_spages, sizeof(int32_t) * spages.size());
@@ -812,6 +845,7 @@ void forward(fe_engine* e, Lane& ln, const std::vector<RowIn>& rows, uint64_t vi
   f.item_slots = (const int32_t*)(dbuf + L.o_slots);
   f.row_nspans = (const int32_t*)(dbuf + L.o_nspans);
   f.span_pages = (const int32_t*)(dbuf + L.o_spages);
+  f.span_masks = (const int32_t*)(dbuf + L.o_smasks);
 
   const bool decode = f.n_head_rows > 0;
   const double el = (double)e->elem;
@@ -819,7 +853,8 @@ void forward(fe_engine* e, Lane& ln, const std::vector<RowIn>& rows, uint64_t vi
   auto gemv_bytes = [&](double N, double K, int rws) { return N * K * el + rws * K * el + rws * N * 4.0; };
   double kv_bytes = 0;  // K+V bytes the cascade items stage (each shared page once per head)
   for (const auto& it : items)
-    kv_bytes += 2.0 * (span_mode ? (it.pad[0] - 1) * FE_PAGE + it.valid_max : it.valid_max) * m.hd * m.H * el;
+    if (!span_mode) kv_bytes += 2.0 * it.valid_max * m.hd * m.H * el;
+  for (size_t j = 0; j < smasks.size(); j++) kv_bytes += 2.0 * ((uint32_t)smasks[j] >> 16) * m.hd * m.H * el;
 
   // decode ticks replay a CUDA graph per (rows, item bucket), captured on the
   // second tick with that key; prefill and profiled runs launch eagerly
@@ -1031,7 +1066,8 @@ void create_lane(fe_engine* e, Lane& ln, int id, int rows, int priority) {
     L.o_slots = up16(L.o_pages + (size_t)L.cap_pages * 4);
     L.o_nspans = up16(L.o_slots + (size_t)L.cap_irows * 4);
     L.o_spages = up16(L.o_nspans + R * 4);
-    L.total = up16(L.o_spages + (size_t)ln.max_partials * 4);
+    L.o_smasks = up16(L.o_spages + (size_t)ln.max_partials * 4);
+    L.total = up16(L.o_smasks + (size_t)ln.max_partials * 4);
   }
   ln.ws.meta = e->dalloc(ln.layout.total);
   for (int i = 0; i < 2; i++) CK(cudaEventCreateWithFlags(&ln.tick_ev[i], cudaEventDisableTiming));
@@ -1158,6 +1194,7 @@ fe_engine* create(const fe_config* c, int device, const float* rope_host) {
 
     // KV pool: 64-token pages [L][2][H][64][hd]
     e->page_elems = fe::kv_page_elems(m);
+    CK(cudaDeviceGetAttribute(&e->n_sm, cudaDevAttrMultiProcessorCount, device));
     size_t pages = c->kv_pages;
     if (pages == 0) {
       size_t free_b = 0, total_b = 0;
@@ -1172,7 +1209,10 @@ fe_engine* create(const fe_config* c, int device, const float* rope_host) {
     // past a row's valid count by p = 0, which needs finite contents
     CK(cudaMemset(e->kv_pool, 0, pages * e->page_elems * el));
     if (e->use_tc)
+    {
       e->pool_map = fe::make_kmajor_map(e->kv_pool, (int)(pages * e->page_elems / 128), 128, 128, 64);
+      e->pool_map16 = fe::make_kmajor_map(e->kv_pool, (int)(pages * e->page_elems / 128), 128, 128, 16);
+    }
     e->page_ref.assign(pages, 0);
     for (int p = (int)pages - 1; p >= 0; p--) e->free_pages.push_back(p);
   } catch (...) {
@@ -1730,6 +1770,9 @@ int fe_set_option(fe_engine* e, const char* key, int64_t value) {
       clear_graphs(e);
     } else if (k == "span_attn") {
       e->span_attn = value != 0;
+      clear_graphs(e);
+    } else if (k == "span_dbg") {
+      fe::g_span_dbg = (int)value;
       clear_graphs(e);
     } else if (k == "span_cap") {
       e->span_cap = (int)std::max<int64_t>(1, value);

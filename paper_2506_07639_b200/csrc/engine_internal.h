@@ -65,12 +65,16 @@ struct Fwd {
   // sequence): its page table, for the tensor-core prefill attention; else null
   const int32_t* seq_pages;
   int pos0;
-  // span attention (bf16 wide decode ticks; attn_span.cu): items are spans of
-  // pages (AttnItem.pad[0] pages listed from span_pages[pad[1]]), each item
-  // row carries the row's slot (its span index), rows their span count
+  // span attention (bf16 chain decode ticks; attn_span.cu): an item is a
+  // row group (<= 16 rows sharing pages) and a range of its pages
+  // (AttnItem.pad[0] pages listed from span_pages[pad[1]], span_masks: per
+  // page the group-local rows that see it | valid-key max << 16); each item
+  // row carries (part | last-page position << 16) in item_slots, rows their
+  // part count in row_nspans (1: the item writes the attention output)
   bool span_mode;
   const int32_t* item_slots;   // parallel to item_rows
   const int32_t* span_pages;
+  const int32_t* span_masks;   // parallel to span_pages
   const int32_t* row_nspans;   // [n_rows]
 };
 
@@ -136,8 +140,9 @@ void launch_prefill_attention(const Fwd& f, const ModelDims& m, const float* q, 
                               void* attn_out, cudaStream_t s);
 struct TmaMap;
 // bf16, head_dim 128, f.span_mode (attn_span.cu); pool_map: the KV pool as [rows][128] bf16, 64 x 64 boxes
-void launch_span_attention(const Fwd& f, const ModelDims& m, const TmaMap& pool_map, const float* q, int layer,
-                           float* partial, void* attn_out, cudaStream_t s);
+extern int g_span_dbg;
+void launch_span_attention(const Fwd& f, const ModelDims& m, const TmaMap& pool_map, const TmaMap& pool_map16,
+                           const float* q, int layer, float* partial, void* attn_out, cudaStream_t s);
 void launch_resid(int dtype, const Fwd& f, int N, int K, const void* w, const void* xin, float* x,
                   cudaStream_t s);
 void launch_swiglu(int dtype, const Fwd& f, int F, int K, const void* w, const void* xin, void* act,
