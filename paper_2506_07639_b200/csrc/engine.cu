@@ -124,6 +124,8 @@ struct Lane {
   int* sk_counters = nullptr;
   float* pair_scratch = nullptr;  // stream-K partials of the CTA-pair GEMM
   int* pair_counters = nullptr;
+  float* split_scratch = nullptr;  // split-K planes of the CTA-pair GEMM
+  size_t split_floats = 0;
   // persistent decode-tick kernel scratch (lane 0)
   float* mk_ss = nullptr;
   unsigned long long* mk_bar = nullptr;
@@ -481,6 +483,7 @@ void launch_layers(fe_engine* e, Lane& ln, const fe::Fwd& f, int n, bool decode,
     t.q = ws.q; t.kv_pool = (__nv_bfloat16*)e->kv_pool; t.page_elems = e->page_elems;
     t.rope = e->rope; t.rows = f.rows; t.H = m.H; t.hd = m.hd; t.d = m.d;
     t.sk_scratch = ln.pair_scratch; t.sk_counters = ln.pair_counters;
+    t.split_scratch = ln.split_scratch; t.split_floats = ln.split_floats;
     return t;
   };
   auto sk_launch = [&](int epi, int N, int K) {
@@ -712,7 +715,9 @@ void forward(fe_engine* e, Lane& ln, const std::vector<RowIn>& rows, uint64_t vi
       std::vector<std::pair<int, int>> plist;  // (chunk, page)
       for (auto& kv : pg) plist.push_back(kv.first);
       const int np = (int)plist.size();
-      const int parts = std::min(want_parts, np);
+      // a row's partial slots are its n_chunks (chunk_base ..): parts <= every row's chunk count
+      int parts = std::min(want_parts, np);
+      for (size_t k = 0; k < grp.size(); k++) parts = std::min(parts, last_chunk[k] + 1);
       for (int part = 0; part < parts; part++) {
         const int p0 = (int)((long)np * part / parts), p1 = (int)((long)np * (part + 1) / parts);
         fe::AttnItem it;
@@ -1094,6 +1099,9 @@ void create_lane(fe_engine* e, Lane& ln, int id, int rows, int priority) {
     ln.pair_scratch = (float*)e->dalloc(fe::pair_sk_scratch_floats() * 4);
     ln.pair_counters = (int*)e->dalloc(fe::pair_sk_counters() * sizeof(int));
     CK(cudaMemset(ln.pair_counters, 0, fe::pair_sk_counters() * sizeof(int)));
+    // split-K planes: 4 splits of a 256-row gate/up output
+    ln.split_floats = (size_t)4 * 256 * std::max<size_t>(2 * F, 3 * d);
+    ln.split_scratch = (float*)e->dalloc(ln.split_floats * 4);
   }
   (void)V;
 }
@@ -1697,6 +1705,7 @@ int fe_op_gemm_tc(fe_engine* e, const void* x, const void* w, int32_t M, int32_t
     fe::TcLaunch t{};
     t.M = M; t.N = N; t.K = K; t.epi = fe::TC_STORE; t.y = y; t.ldy = N;
     t.sk_scratch = e->lanes[0].pair_scratch; t.sk_counters = e->lanes[0].pair_counters;
+    t.split_scratch = e->lanes[0].split_scratch; t.split_floats = e->lanes[0].split_floats;
     for (int r = 0; r < e->op_reps; r++) {
       if (e->tc_pair) fe::launch_gemm_tc(am, bm, t, e->lanes[0].stream);
       else fe::launch_gemm_tc_v1(am, bm, t, e->lanes[0].stream);
@@ -1779,6 +1788,9 @@ int fe_set_option(fe_engine* e, const char* key, int64_t value) {
       clear_graphs(e);
     } else if (k == "tc_pair") {
       e->tc_pair = value != 0;
+      clear_graphs(e);
+    } else if (k == "tc_split") {
+      fe::g_pair_split = (int)value;
       clear_graphs(e);
     } else if (k == "tc_sk") {
       fe::g_pair_sk = (int)value;

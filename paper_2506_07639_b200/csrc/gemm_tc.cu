@@ -328,35 +328,48 @@ struct PairArgs {
   long long W;
   float* scratch;   // [P][2 slots][2 ranks][BN / 4][128] float4: partial segments
   int* counters;    // [tiles - dp][2 ranks]: arrivals of a tile's partial segments
+  // split-K (one m tile, few n tiles: the decode-width regime): data-parallel
+  // units (tile, split) over k-ranges of kbs blocks; each unit stores its raw
+  // fp32 tile to split_out[split][M][N] and launch_splitk_reduce sums the
+  // splits in order and runs the fused epilogue
+  int splits, kbs, tiles;
+  float* split_out;
 };
 
 struct Seg {
   int tile, k0, k1;
+  int split;
   bool sk;   // from the stream-K range
 };
 
 // The segments of one pair in order (identical walk in every role).
 struct SegIter {
-  int t_dp, dp, P, KB;
+  int t_dp, dp, P, KB, tiles, kbs;
   long long i, i1;
   __device__ SegIter(const PairArgs& p, int pair, int n_pairs) {
     P = n_pairs;
     dp = p.dp;
     KB = p.kblocks;
+    tiles = p.tiles;
+    kbs = p.kbs;
     t_dp = pair;
     i = (long long)pair * p.W / n_pairs;
     i1 = (long long)(pair + 1) * p.W / n_pairs;
   }
   __device__ bool next(Seg& s) {
-    if (t_dp < dp) {
-      s.tile = t_dp; s.k0 = 0; s.k1 = KB; s.sk = false;
+    if (t_dp < dp) {  // unit t_dp = (tile, split)
+      s.tile = t_dp % tiles;
+      s.split = t_dp / tiles;
+      s.k0 = s.split * kbs;
+      s.k1 = min(KB, s.k0 + kbs);
+      s.sk = false;
       t_dp += P;
       return true;
     }
     if (i >= i1) return false;
     const int t = (int)(i / KB), k0 = (int)(i % KB);
     const int k1 = (int)min((long long)KB, (long long)k0 + (i1 - i));
-    s.tile = dp + t; s.k0 = k0; s.k1 = k1; s.sk = true;
+    s.tile = dp + t; s.k0 = k0; s.k1 = k1; s.split = 0; s.sk = true;
     i += k1 - k0;
     return true;
   }
@@ -602,6 +615,22 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
           asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];"
                        ::"r"(tempty0 + (uint32_t)acc * 8u) : "memory");
       };
+      if (p.split_out) {  // split-K unit: raw fp32 tile -> split_out[split] (logical columns)
+        float* dst = p.split_out + ((size_t)sg.split * a.M + row) * a.N;
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          float v[32];
+          tmem_ld32(tacc + c, v);  // warp-collective: every lane, rows past M discard
+          if (row >= a.M) continue;
+          const int col = a.epi == TC_SWIGLU ? (c < BN / 2 ? n_tile * (BN / 2) + c : a.F + n_tile * (BN / 2) + c - BN / 2)
+                                             : n_tile * BN + c;
+#pragma unroll
+          for (int i = 0; i < 32; i += 4)
+            __stcg(reinterpret_cast<float4*>(dst + col + i), make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]));
+        }
+        release_acc();
+        continue;
+      }
       if (sg.k0 == 0 && sg.k1 == p.kblocks) {  // whole tile: fused epilogue straight from TMEM
         pair_epilogue_row<BN>(a, row, n_tile, [&](int c, float(&v)[32]) { tmem_ld32(tacc + c, v); });
         release_acc();
@@ -1027,6 +1056,101 @@ skinny_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constan
   }
 }
 
+// Split-K reduction with the fused epilogue (the pair GEMM's split mode):
+// sums split_out[0 .. S-1][row][col] in split order (deterministic) and
+// applies the GEMM's epilogue -- STORE / RESID (float4 per thread), SwiGLU
+// (gate col j, up col F + j), QKV (RoPE pairs c, c + 64 of a head; q rows or
+// the paged K/V append).
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restrict__ part, int S, TcArgs a) {
+  pdl_trigger();
+  pdl_wait();
+  const size_t plane = (size_t)a.M * a.N;
+  if (a.epi == TC_STORE || a.epi == TC_RESID) {
+    const size_t n4 = plane / 4;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
+      float4 acc = __ldcg(reinterpret_cast<const float4*>(part) + i);
+      for (int sp = 1; sp < S; sp++) {
+        const float4 v = __ldcg(reinterpret_cast<const float4*>(part + sp * plane) + i);
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+      }
+      const size_t row = i * 4 / a.N, col = i * 4 % a.N;
+      float4* dst = reinterpret_cast<float4*>(a.y + row * a.ldy + col);
+      if (a.epi == TC_RESID) {
+        const float4 o = *dst;
+        acc.x += o.x; acc.y += o.y; acc.z += o.z; acc.w += o.w;
+      }
+      *dst = acc;
+    }
+  } else if (a.epi == TC_SWIGLU) {
+    const size_t n4 = (size_t)a.M * a.F / 4;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
+      const size_t row = i * 4 / a.F, j = i * 4 % a.F;
+      const float* g0 = part + row * a.N + j;
+      float4 g = __ldcg(reinterpret_cast<const float4*>(g0)), u = __ldcg(reinterpret_cast<const float4*>(g0 + a.F));
+      for (int sp = 1; sp < S; sp++) {
+        const float4 vg = __ldcg(reinterpret_cast<const float4*>(g0 + sp * plane));
+        const float4 vu = __ldcg(reinterpret_cast<const float4*>(g0 + sp * plane + a.F));
+        g.x += vg.x; g.y += vg.y; g.z += vg.z; g.w += vg.w;
+        u.x += vu.x; u.y += vu.y; u.z += vu.z; u.w += vu.w;
+      }
+      __nv_bfloat162 p0, p1;
+      p0.x = __float2bfloat16_rn(silu_mul(g.x, u.x)); p0.y = __float2bfloat16_rn(silu_mul(g.y, u.y));
+      p1.x = __float2bfloat16_rn(silu_mul(g.z, u.z)); p1.y = __float2bfloat16_rn(silu_mul(g.w, u.w));
+      __nv_bfloat162* dst = reinterpret_cast<__nv_bfloat162*>(a.act + row * a.F + j);
+      dst[0] = p0;
+      dst[1] = p1;
+    }
+  } else {  // TC_QKV: thread = (row, head section, 4 rotary pairs)
+    const int heads = a.N / 128;
+    const size_t n = (size_t)a.M * heads * 16;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+      const int c = (int)(i % 16) * 4;
+      const size_t rh = i / 16;
+      const int hs = (int)(rh % heads);
+      const size_t row = rh / heads;
+      const int nh = hs * 128, sec = nh / a.d, h = (nh % a.d) / 128;
+      const float* p1 = part + row * a.N + nh + c;
+      float4 x1 = __ldcg(reinterpret_cast<const float4*>(p1)), x2 = __ldcg(reinterpret_cast<const float4*>(p1 + 64));
+      for (int sp = 1; sp < S; sp++) {
+        const float4 v1 = __ldcg(reinterpret_cast<const float4*>(p1 + sp * plane));
+        const float4 v2 = __ldcg(reinterpret_cast<const float4*>(p1 + sp * plane + 64));
+        x1.x += v1.x; x1.y += v1.y; x1.z += v1.z; x1.w += v1.w;
+        x2.x += v2.x; x2.y += v2.y; x2.z += v2.z; x2.w += v2.w;
+      }
+      float a1[4] = {x1.x, x1.y, x1.z, x1.w}, a2[4] = {x2.x, x2.y, x2.z, x2.w};
+      const RowMeta m = a.rows[row];
+      if (sec < 2) {
+        const float* cs = a.rope + (size_t)m.pos * 128;
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+          const float co = cs[c + e], sn = cs[64 + c + e];
+          const float r1 = __fmaf_rn(a1[e], co, -__fmul_rn(a2[e], sn));
+          const float r2 = __fmaf_rn(a2[e], co, __fmul_rn(a1[e], sn));
+          a1[e] = r1;
+          a2[e] = r2;
+        }
+      }
+      if (sec == 0) {
+        float* qr = a.q + row * a.d + h * 128;
+        *reinterpret_cast<float4*>(qr + c) = make_float4(a1[0], a1[1], a1[2], a1[3]);
+        *reinterpret_cast<float4*>(qr + 64 + c) = make_float4(a2[0], a2[1], a2[2], a2[3]);
+      } else {
+        __nv_bfloat16* kv = a.kv_pool + (size_t)m.kv_page * a.page_elems + a.layer_off +
+                            ((size_t)((sec - 1) * a.H + h) * FE_PAGE + m.kv_slot) * 128;
+        __nv_bfloat162 q0, q1, q2, q3;
+        q0.x = __float2bfloat16_rn(a1[0]); q0.y = __float2bfloat16_rn(a1[1]);
+        q1.x = __float2bfloat16_rn(a1[2]); q1.y = __float2bfloat16_rn(a1[3]);
+        q2.x = __float2bfloat16_rn(a2[0]); q2.y = __float2bfloat16_rn(a2[1]);
+        q3.x = __float2bfloat16_rn(a2[2]); q3.y = __float2bfloat16_rn(a2[3]);
+        reinterpret_cast<__nv_bfloat162*>(kv + c)[0] = q0;
+        reinterpret_cast<__nv_bfloat162*>(kv + c)[1] = q1;
+        reinterpret_cast<__nv_bfloat162*>(kv + 64 + c)[0] = q2;
+        reinterpret_cast<__nv_bfloat162*>(kv + 64 + c)[1] = q3;
+      }
+    }
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -1186,6 +1310,7 @@ void launch_gemm_tc_v1(const TmaMap& a_map, const TmaMap& b_map, const TcLaunch&
 }
 
 int g_pair_bn = 0;  // engine option "tc_bn": force the pair tile width (0: 256 where it divides)
+int g_pair_split = 1;  // engine option "tc_split": split-K for decode-width batches
 int g_pair_sk = 0;  // engine option "tc_sk": stream-K the last waves (measured slower: the 256 x 256 fp32
                     // partials cost more than the wave tail they remove, profiles/r2_gemm_pair_sk.txt)
 
@@ -1226,15 +1351,40 @@ void launch_gemm_tc(const TmaMap& a_map, const TmaMap& b_map64, const TcLaunch& 
   const int tiles = p.m_tiles * p.n_tiles;
   const int P = std::min(tiles * p.kblocks, std::min(n_sm / 2, kPairMaxPairs));
   // DP for all but the last one-to-two waves, which are stream-K'd (no wave tail)
-  p.dp = (!g_pair_sk || !l.sk_scratch) ? tiles : (tiles >= 2 * P ? (tiles / P - 1) * P : 0);
-  p.W = (long long)(tiles - p.dp) * p.kblocks;
+  // split-K for one m tile over few n tiles (decode-width batches): the
+  // split count minimising waves x k-blocks per unit + a per-split cost for
+  // the partial traffic (~4 k-block wave-times per 168 x 4096 fp32 plane)
+  int S = 1;
+  if (g_pair_split && l.split_scratch && p.m_tiles == 1 && tiles < P) {
+    double best = 1e30;
+    const double plane = (double)l.M * cols / (168.0 * 4096.0);
+    for (int sp = 1; sp <= 8; sp++) {
+      if ((size_t)sp * l.M * cols > l.split_floats || (sp > 1 && p.kblocks / sp < 4)) break;
+      const int units = tiles * sp;
+      const double t = (double)((units + P - 1) / P) * ((p.kblocks + sp - 1) / sp) + (sp > 1 ? 4.0 * sp * plane : 0.0);
+      if (t < best - 1e-9) { best = t; S = sp; }
+    }
+  }
+  p.tiles = tiles;
+  p.splits = S;
+  p.kbs = (p.kblocks + S - 1) / S;
+  p.split_out = S > 1 ? l.split_scratch : nullptr;
+  const int units = tiles * S;
+  p.dp = (S > 1 || !g_pair_sk || !l.sk_scratch) ? units : (tiles >= 2 * P ? (tiles / P - 1) * P : 0);
+  p.W = (long long)(tiles - std::min(p.dp, tiles)) * p.kblocks;
   p.scratch = l.sk_scratch;
   p.counters = l.sk_counters;
-  const int grid = 2 * (p.dp == tiles ? std::min(tiles, P) : P);
+  const int grid = 2 * (p.dp == units ? std::min(units, P) : P);
   const CUtensorMap& am = *reinterpret_cast<const CUtensorMap*>(a_map.bytes);
   const CUtensorMap& bm = *reinterpret_cast<const CUtensorMap*>(b_map64.bytes);
   if (bn == 256) gemm_pair_kernel<256><<<grid, kPairThreads, pair_smem<256>(), s>>>(am, bm, p);
   else gemm_pair_kernel<128><<<grid, kPairThreads, pair_smem<128>(), s>>>(am, bm, p);
+  if (S > 1) {
+    const size_t work = l.epi == TC_SWIGLU ? (size_t)l.M * l.F / 4 : l.epi == TC_QKV ? (size_t)l.M * (l.N / 128) * 16
+                                                                                   : (size_t)l.M * l.N / 4;
+    const int blocks = (int)std::min<size_t>((work + 255) / 256, (size_t)n_sm * 8);
+    launch_k(splitk_reduce_kernel, dim3(blocks), dim3(256), 0, s, (const float*)l.split_scratch, S, p.t);
+  }
 }
 
 }  // namespace fe

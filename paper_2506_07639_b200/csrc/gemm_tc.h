@@ -31,6 +31,8 @@ struct TcLaunch {
   int H, hd, d;
   float* sk_scratch;   // stream-K partials of the pair GEMM (pair_sk_scratch_floats()), or null: no stream-K
   int* sk_counters;    // pair_sk_counters() ints, zero-initialised
+  float* split_scratch;  // split-K partial planes (split_floats floats), or null: no split-K
+  size_t split_floats;
 };
 
 // skinny decode GEMM (swap-AB, <= skinny_max_rows() batch rows)
@@ -63,6 +65,7 @@ void launch_gemm_tc(const TmaMap& a_map, const TmaMap& b_map64, const TcLaunch& 
 void launch_gemm_tc_v1(const TmaMap& a_map, const TmaMap& b_map, const TcLaunch& l, cudaStream_t s);
 extern int g_pair_bn;
 extern int g_pair_sk;
+extern int g_pair_split;
 size_t pair_sk_scratch_floats();
 int pair_sk_counters();
 int skinny_max_rows();      // widest batch of the skinny GEMM (rows; > 256 run as 256-row slices)

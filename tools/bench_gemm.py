@@ -1,7 +1,7 @@
 """Micro-benchmark of the dense-contraction tcgen05 GEMMs on 7B shapes (warm,
 back-to-back launches inside one call, CUDA events on the engine stream):
-the CTA-pair persistent GEMM (data-parallel tiles only, and with the
-stream-K last waves)
+the CTA-pair persistent GEMM (with and without split-K for one-m-tile
+batches)
 against the round-1 1-CTA 128 x 128 tile GEMM, per row count.
 
     python tools/bench_gemm.py [ROWS...] [--shapes qkv,o,gate_up,down]
@@ -17,7 +17,7 @@ import torch  # noqa: E402
 from paper_2506_07639_b200.engine import Engine  # noqa: E402
 
 ap = argparse.ArgumentParser()
-ap.add_argument("rows", nargs="*", type=int, default=[48, 96, 168, 256, 448, 625, 1024, 2500, 8192])
+ap.add_argument("rows", nargs="*", type=int, default=[33, 48, 96, 168, 256, 448, 625, 1024, 8192])
 ap.add_argument("--shapes", default="qkv,o,gate_up,down")
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--out", default=None)
@@ -52,9 +52,9 @@ for rows in args.rows:
         torch.cuda.synchronize()
         line = f"rows {rows:5d} {name:8s} N={N:6d} K={K:6d}:"
         rec = {"rows": rows, "shape": name, "N": N, "K": K}
-        for label, pair, sk in (("v1", 0, 0), ("pair_dp", 1, 0), ("pair_sk", 1, 1)):
+        for label, pair, split in (("v1", 0, 0), ("pair_nosplit", 1, 0), ("pair", 1, 1)):
             eng.set_option("tc_pair", pair)
-            eng.set_option("tc_sk", sk)
+            eng.set_option("tc_split", split)
             y.fill_(float("nan"))
             us = timed(lambda: eng.op_gemm_tc(x.data_ptr(), w.data_ptr(), rows, N, K, y.data_ptr()), args.reps)
             err = ((y - ref).abs().max() / ref.abs().max()).item()
@@ -63,7 +63,7 @@ for rows in args.rows:
             rec[label] = {"us": us, "tflops": tf}
             line += f"  {label}: {us:8.1f}us {tf:6.0f}TF/s"
         eng.set_option("tc_pair", 1)
-        eng.set_option("tc_sk", 0)
+        eng.set_option("tc_split", 1)
         print(line, flush=True)
         results.append(rec)
         del w, ref
