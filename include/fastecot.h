@@ -71,6 +71,13 @@ int fe_seq_len(fe_engine* e, int32_t seq, int32_t* len);
  * `vis_id` take row (pos-1) of the vision embedding seeded by `vision_seed` */
 int fe_prefill(fe_engine* e, int32_t seq, const int32_t* ids, int32_t n, uint64_t vision_seed, int32_t vis_id);
 
+/* batched prefill: seqs[i] gets counts[i] ids (concatenated in `ids`),
+ * vision placeholders seeded by vision_seeds[i]; rows of all sequences are
+ * packed into as few forwards as the engine holds (one GEMM pass per
+ * forward for every trunk of a batched-episode timestep) */
+int fe_prefill_batch(fe_engine* e, int32_t n_seqs, const int32_t* seqs, const int32_t* counts, const int32_t* ids,
+                     const uint64_t* vision_seeds, int32_t vis_id);
+
 /* reuse-as-draft verification (replaces nothing in the reference: the
  * SyntheticBackend's reuse draw, backends.py:202-204, returns prev_content
  * verbatim; here prev_content is checked as a greedy draft): one batched

@@ -63,7 +63,8 @@ constexpr int kLanes = 2;
 constexpr int kLane1Rows = 64;      // background lane: decode rows only
 
 struct MetaLayout {
-  size_t o_rows, o_items, o_irows, o_heads, o_pages, o_slots, o_nspans, o_spages, o_smasks, total;
+  size_t o_rows, o_items, o_irows, o_heads, o_pages, o_slots, o_nspans, o_spages, o_smasks, o_ptiles, o_vkeys,
+      total;
   int cap_rows, cap_items, cap_irows, cap_pages;
 };
 
@@ -91,6 +92,7 @@ struct Request {
 struct RowIn {
   int seq, pos, tok, tok_src, vis_row, out_idx, logit_row;
   bool head;
+  int vk;  // index into the forward's vision seeds (multi-sequence prefill)
 };
 
 enum ProfCat { PROF_GEMV = 0, PROF_ATTN = 1, PROF_DECODE_FWD = 2, PROF_PREFILL_FWD = 3, PROF_TICK = 4, PROF_NCAT = 5 };
@@ -523,7 +525,7 @@ void launch_layers(fe_engine* e, Lane& ln, const fe::Fwd& f, int n, bool decode,
     if (e->debug_skip & 1) {
     } else if (f.span_mode) {
       fe::launch_span_attention(f, m, e->pool_map, e->pool_map16, ws.q, l, ws.partial, ws.attn, st);
-    } else if (!decode && f.seq_pages && dt == FE_BF16 && m.hd == 128 && e->prefill_fa) {
+    } else if (!decode && f.ptiles && dt == FE_BF16 && m.hd == 128 && e->prefill_fa) {
       fe::launch_prefill_attention(f, m, ws.q, e->kv_pool, l, ws.attn, st);
     } else {
       fe::launch_attention(dt, f, m, ws.q, e->kv_pool, l, ws.partial, ws.attn, st);
@@ -571,7 +573,8 @@ void launch_layers(fe_engine* e, Lane& ln, const fe::Fwd& f, int n, bool decode,
 // One forward pass over `rows` on a lane (positions must extend each
 // sequence contiguously, in order).  Builds row metadata and the cascade work
 // list, then launches the layer stack (or replays the lane's decode graph).
-void forward(fe_engine* e, Lane& ln, const std::vector<RowIn>& rows, uint64_t vision_seed) {
+void forward(fe_engine* e, Lane& ln, const std::vector<RowIn>& rows, uint64_t vision_seed,
+             const std::vector<uint64_t>* vseeds = nullptr) {
   const fe::ModelDims& m = e->m;
   const int n = (int)rows.size();
   if (n == 0) return;
@@ -642,7 +645,7 @@ void forward(fe_engine* e, Lane& ln, const std::vector<RowIn>& rows, uint64_t vi
     mm.n_chunks = pg + 1;
     mm.logit_row = r.logit_row;
     mm.head_row = -1;
-    mm.pad = 0;
+    mm.pad = vseeds ? r.vk : 0;
     chunk_total += pg + 1;
     if (r.head) {
       mm.head_row = (int)head_rows.size();
@@ -812,18 +815,36 @@ void forward(fe_engine* e, Lane& ln, const std::vector<RowIn>& rows, uint64_t vi
     copy(L.o_nspans, sizeof(int32_t) * nspans.size());
     copy(L.o_spages, sizeof(int32_t) * spages.size());
   }
-  // single-sequence prefill: the sequence's page table for the tensor-core attention
-  bool one_seq = head_rows.empty() && n > 1;
-  for (int i = 1; i < n && one_seq; i++) one_seq = rows[i].seq == rows[0].seq && rows[i].pos == rows[0].pos + i;
-  int n_seq_pages = 0;
-  if (one_seq) {
-    const Seq& sq = e->seqs[rows[0].seq];
-    n_seq_pages = (rows[n - 1].pos) / FE_PAGE + 1;
-    if (n_seq_pages > L.cap_pages) one_seq = false;
-    else {
-      std::memcpy(hbuf + L.o_pages, sq.pages.data(), sizeof(int32_t) * n_seq_pages);
-      copy(L.o_pages, sizeof(int32_t) * n_seq_pages);
+  // prefill forwards (no lm_head rows): runs of consecutive positions of one
+  // sequence, cut into 64-row query tiles with their sequence's page table,
+  // for the tensor-core causal attention (prefill_attn.cu; several trunks per
+  // forward in a batched prefill)
+  std::vector<fe::PrefillTile> ptiles;
+  std::vector<int32_t> ptab;
+  if (head_rows.empty() && !span_mode) {
+    for (int i = 0; i < n;) {
+      int j = i + 1;
+      while (j < n && rows[j].seq == rows[i].seq && rows[j].pos == rows[j - 1].pos + 1) j++;
+      const Seq& sq = e->seqs[rows[i].seq];
+      const int np = rows[j - 1].pos / FE_PAGE + 1;
+      const int off = (int)ptab.size();
+      ptab.insert(ptab.end(), sq.pages.begin(), sq.pages.begin() + np);
+      for (int t = i; t < j; t += 64) ptiles.push_back({t, std::min(64, j - t), rows[t].pos, off});
+      i = j;
     }
+    if ((int)ptab.size() > ln.max_partials) ptiles.clear();  // table does not fit: cascade kernel
+    else {
+      std::memcpy(hbuf + L.o_spages, ptab.data(), sizeof(int32_t) * ptab.size());
+      std::memcpy(hbuf + L.o_ptiles, ptiles.data(), sizeof(fe::PrefillTile) * ptiles.size());
+      copy(L.o_spages, sizeof(int32_t) * ptab.size());
+      copy(L.o_ptiles, sizeof(fe::PrefillTile) * ptiles.size());
+    }
+  }
+  if (vseeds) {
+    std::vector<uint64_t> keys(vseeds->size());
+    for (size_t k = 0; k < keys.size(); k++) keys[k] = fe::tensor_key((*vseeds)[k], 4 /* T_VISION */);
+    std::memcpy(hbuf + L.o_vkeys, keys.data(), 8 * keys.size());
+    copy(L.o_vkeys, 8 * keys.size());
   }
   CK(cudaEventRecord(ln.meta_ev[mi], ln.stream));
   e->h2d_bytes += h2d;
@@ -844,8 +865,10 @@ void forward(fe_engine* e, Lane& ln, const std::vector<RowIn>& rows, uint64_t vi
   f.head_rows = (const int32_t*)(dbuf + L.o_heads);
   f.attn_counters = ln.attn_counters;
   f.vision_key = fe::tensor_key(vision_seed, 4 /* T_VISION */);
-  f.seq_pages = one_seq ? (const int32_t*)(dbuf + L.o_pages) : nullptr;
-  f.pos0 = one_seq ? rows[0].pos : 0;
+  f.ptiles = ptiles.empty() ? nullptr : (const fe::PrefillTile*)(dbuf + L.o_ptiles);
+  f.n_ptiles = (int)ptiles.size();
+  f.ptab = (const int32_t*)(dbuf + L.o_spages);
+  f.vision_keys = vseeds ? (const uint64_t*)(dbuf + L.o_vkeys) : nullptr;
   f.span_mode = span_mode;
   f.item_slots = (const int32_t*)(dbuf + L.o_slots);
   f.row_nspans = (const int32_t*)(dbuf + L.o_nspans);
@@ -896,36 +919,70 @@ void forward(fe_engine* e, Lane& ln, const std::vector<RowIn>& rows, uint64_t vi
   e->n_rows_total += n;
 }
 
-void prefill(fe_engine* e, int seq, const int32_t* ids, int n, uint64_t vseed, int vis_id) {
+// Append ids to one or more sequences (positions len .. len + n - 1 each),
+// packing the rows of all of them into as few forwards as the lane holds:
+// a batched trunk prefill runs its GEMMs at M = the packed row count.
+struct PrefillSeg {
+  int seq;
+  const int32_t* ids;
+  int n;
+  uint64_t vseed;
+};
+
+void prefill_multi(fe_engine* e, const std::vector<PrefillSeg>& segs, int vis_id) {
   Lane& ln = e->lanes[0];
-  Seq& s = seq_at(e, seq);
-  int pos = s.len;
-  int i = 0;
-  while (i < n) {
-    std::vector<RowIn> rows;
-    int chunks = 0;
-    while (i < n && (int)rows.size() < ln.max_rows) {
+  for (const auto& sg : segs) {
+    seq_at(e, sg.seq);
+    for (int i = 0; i < sg.n; i++) {
+      if (sg.ids[i] == vis_id && e->seqs[sg.seq].len + i < 1) throw Error("prefill: vision placeholder at position 0");
+      if (sg.ids[i] != vis_id && (sg.ids[i] < 0 || sg.ids[i] >= e->m.V)) throw Error("prefill: token id out of range");
+    }
+    for (const auto& o : segs)
+      if (&o != &sg && o.seq == sg.seq) throw Error("prefill: a sequence listed twice");
+  }
+  std::vector<RowIn> rows;
+  std::vector<uint64_t> vseeds;
+  int chunks = 0;
+  auto flush = [&]() {
+    if (rows.empty()) return;
+    forward(e, ln, rows, 0, &vseeds);
+    rows.clear();
+    vseeds.clear();
+    chunks = 0;
+  };
+  for (const auto& sg : segs) {
+    int pos = e->seqs[sg.seq].len;
+    int vk = -1;
+    for (int i = 0; i < sg.n; i++, pos++) {
       const int c = pos / FE_PAGE + 1;
-      if (chunks + c > ln.max_partials && !rows.empty()) break;
+      if (!rows.empty() && ((int)rows.size() >= ln.max_rows || chunks + c > ln.max_partials)) {
+        flush();
+        vk = -1;
+      }
+      if (vk < 0) {
+        vk = (int)vseeds.size();
+        vseeds.push_back(sg.vseed);
+      }
       RowIn r{};
-      r.seq = seq;
+      r.seq = sg.seq;
       r.pos = pos;
-      r.tok = ids[i] == vis_id ? -1 : ids[i];
+      r.tok = sg.ids[i] == vis_id ? -1 : sg.ids[i];
       r.tok_src = -1;
-      r.vis_row = ids[i] == vis_id ? pos - 1 : -1;
-      if (ids[i] == vis_id && pos < 1) throw Error("prefill: vision placeholder at position 0");
-      if (ids[i] != vis_id && (ids[i] < 0 || ids[i] >= e->m.V)) throw Error("prefill: token id out of range");
+      r.vis_row = sg.ids[i] == vis_id ? pos - 1 : -1;
       r.out_idx = -1;
       r.logit_row = -1;
       r.head = false;
+      r.vk = vk;
       rows.push_back(r);
       chunks += c;
-      pos++;
-      i++;
     }
-    forward(e, ln, rows, vseed);
   }
+  flush();
   CK(cudaEventRecord(e->lane0_ev, ln.stream));
+}
+
+void prefill(fe_engine* e, int seq, const int32_t* ids, int n, uint64_t vseed, int vis_id) {
+  prefill_multi(e, {PrefillSeg{seq, ids, n, vseed}}, vis_id);
 }
 
 int new_request_slot(fe_engine* e) {
@@ -1072,7 +1129,9 @@ void create_lane(fe_engine* e, Lane& ln, int id, int rows, int priority) {
     L.o_nspans = up16(L.o_slots + (size_t)L.cap_irows * 4);
     L.o_spages = up16(L.o_nspans + R * 4);
     L.o_smasks = up16(L.o_spages + (size_t)ln.max_partials * 4);
-    L.total = up16(L.o_smasks + (size_t)ln.max_partials * 4);
+    L.o_ptiles = up16(L.o_smasks + (size_t)ln.max_partials * 4);
+    L.o_vkeys = up16(L.o_ptiles + R * sizeof(fe::PrefillTile));
+    L.total = up16(L.o_vkeys + R * 8);
   }
   ln.ws.meta = e->dalloc(ln.layout.total);
   for (int i = 0; i < 2; i++) CK(cudaEventCreateWithFlags(&ln.tick_ev[i], cudaEventDisableTiming));
@@ -1503,6 +1562,20 @@ int fe_seq_truncate(fe_engine* e, int32_t seq, int32_t len) {
 
 int fe_prefill(fe_engine* e, int32_t seq, const int32_t* ids, int32_t n, uint64_t vision_seed, int32_t vis_id) {
   return guarded(e, [&] { prefill(e, seq, ids, n, vision_seed, vis_id); });
+}
+
+int fe_prefill_batch(fe_engine* e, int32_t n_seqs, const int32_t* seqs, const int32_t* counts, const int32_t* ids,
+                     const uint64_t* vision_seeds, int32_t vis_id) {
+  return guarded(e, [&] {
+    std::vector<PrefillSeg> segs;
+    size_t off = 0;
+    for (int i = 0; i < n_seqs; i++) {
+      if (counts[i] < 0) throw Error("prefill_batch: negative count");
+      if (counts[i]) segs.push_back({seqs[i], ids + off, counts[i], vision_seeds[i]});
+      off += counts[i];
+    }
+    prefill_multi(e, segs, vis_id);
+  });
 }
 
 int fe_set_slots(fe_engine* e, int32_t slots) { return fe_set_slots_lane(e, 0, slots); }

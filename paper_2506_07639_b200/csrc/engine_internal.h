@@ -48,6 +48,13 @@ struct ModelDims {
   float eps, attn_scale;
 };
 
+// A query tile of the tensor-core prefill attention: rows [row0, row0 + n) of
+// the forward are consecutive positions pos0 .. of one sequence whose page
+// table starts at ptab[pages].
+struct PrefillTile {
+  int32_t row0, n, pos0, pages;
+};
+
 // Device-side view of a forward pass.
 struct Fwd {
   const int32_t* hdr;      // device header: [n_rows, n_items, n_head_rows, 0]
@@ -61,10 +68,12 @@ struct Fwd {
   int n_head_rows;         // rows that need the lm_head
   const int32_t* head_rows;  // row index of each lm_head row
   uint64_t vision_key;
-  // single-sequence prefill (rows = positions pos0 .. pos0 + n_rows - 1 of one
-  // sequence): its page table, for the tensor-core prefill attention; else null
-  const int32_t* seq_pages;
-  int pos0;
+  const uint64_t* vision_keys;  // per-row vision keys (RowMeta.pad indexes them), or null: vision_key
+  // prefill forwards: 64-row query tiles of consecutive positions of one
+  // sequence each (several sequences per forward), their page tables; else null
+  const PrefillTile* ptiles;
+  int n_ptiles;
+  const int32_t* ptab;
   // span attention (bf16 chain decode ticks; attn_span.cu): an item is a
   // row group (<= 16 rows sharing pages) and a range of its pages
   // (AttnItem.pad[0] pages listed from span_pages[pad[1]], span_masks: per

@@ -53,8 +53,9 @@ __global__ void embed_kernel(Fwd f, int d, const WT* embed, const int32_t* out_t
   float* xr = x + (size_t)blockIdx.x * d;
   if (m.vis_row >= 0) {
     const uint64_t base = (uint64_t)m.vis_row * d;
+    const uint64_t key = f.vision_keys ? f.vision_keys[m.pad] : f.vision_key;
     for (int k = threadIdx.x; k < d; k += blockDim.x)
-      xr[k] = __fmul_rn(centered(f.vision_key, base + k), kVisionMult);
+      xr[k] = __fmul_rn(centered(key, base + k), kVisionMult);
   } else {
     const int tok = m.tok >= 0 ? m.tok : out_tokens[m.tok_src];
     const WT* e = embed + (size_t)tok * d;

@@ -1,8 +1,10 @@
-// Causal prefill attention on tensor cores (bf16 path): the rows of one
-// forward are consecutive positions pos0 .. pos0 + n - 1 of one sequence
-// (trunk prefill), attending over that sequence's paged K/V.
+// Causal prefill attention on tensor cores (bf16 path): the rows of a
+// prefill forward are runs of consecutive positions of one or more sequences
+// (a trunk prefill, or every trunk of a batched-episode timestep), cut into
+// 64-row query tiles (engine.cu forward(): PrefillTile) attending over their
+// sequence's paged K/V.
 //
-// Grid (query tiles of 64 rows, heads); 4 warps, 16 query rows each.  Per KV
+// Grid (query tiles, heads); 4 warps, 16 query rows each.  Per KV
 // page (64 keys): K and V staged by cp.async into a double buffer (rows 256 B,
 // 16-byte chunks XOR-swizzled by key & 7), S = Q K^T on mma.sync m16n8k16
 // (Q scaled to the exp2 domain, head dims permuted identically in Q and K so a
@@ -58,7 +60,8 @@ __device__ __forceinline__ void stage(unsigned char* buf, const __nv_bfloat16* k
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
-__global__ void __launch_bounds__(128) prefill_attn_kernel(const int32_t* __restrict__ pages, int pos0, int n_rows,
+__global__ void __launch_bounds__(128) prefill_attn_kernel(const PrefillTile* __restrict__ tiles,
+                                                           const int32_t* __restrict__ ptab,
                                                            const float* __restrict__ q,
                                                            const __nv_bfloat16* __restrict__ pool, size_t page_elems,
                                                            size_t layer_off, int H, int d, float scale_log2,
@@ -69,13 +72,15 @@ __global__ void __launch_bounds__(128) prefill_attn_kernel(const int32_t* __rest
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
   const int h = blockIdx.y;
-  const int row0 = blockIdx.x * QT;                 // first query row of the CTA
-  const int wrow0 = row0 + 16 * warp;                // first query row of the warp
-  const int last_row = min(n_rows, row0 + QT) - 1;
-  const int seq_len = pos0 + n_rows;                 // keys written before this kernel
-  const int n_pages = (pos0 + last_row) / FE_PAGE + 1;
-  const int ra = wrow0 + g, rb = wrow0 + g + 8;      // this lane's rows
+  const PrefillTile tile = tiles[blockIdx.x];
+  const int32_t* pages = ptab + tile.pages;          // the tile's sequence page table
+  const int pos0 = tile.pos0, n_rows = tile.n;       // tile rows: forward rows row0 .., positions pos0 ..
+  const int wrow0 = 16 * warp;                       // first tile-local query row of the warp
+  const int seq_len = pos0 + n_rows;                 // keys any row of the tile can see
+  const int n_pages = (seq_len - 1) / FE_PAGE + 1;
+  const int ra = wrow0 + g, rb = wrow0 + g + 8;      // this lane's tile-local rows
   const int pa = pos0 + ra, pb = pos0 + rb;          // their positions
+  const size_t fra = (size_t)(tile.row0 + ra), frb = (size_t)(tile.row0 + rb);  // forward rows
 
   auto kv_src = [&](int c, const __nv_bfloat16** kg, const __nv_bfloat16** vg, int* fill) {
     *kg = pool + (size_t)pages[c] * page_elems + layer_off + (size_t)h * FE_PAGE * HD;
@@ -97,12 +102,12 @@ __global__ void __launch_bounds__(128) prefill_attn_kernel(const int32_t* __rest
 #pragma unroll
     for (int u = 0; u < 4; u++) f[u] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (ra < n_rows) {
-      const float* qp = q + (size_t)ra * d + h * HD + 32 * i + 8 * t;
+      const float* qp = q + fra * d + h * HD + 32 * i + 8 * t;
       f[0] = *reinterpret_cast<const float4*>(qp);
       f[1] = *reinterpret_cast<const float4*>(qp + 4);
     }
     if (rb < n_rows) {
-      const float* qp = q + (size_t)rb * d + h * HD + 32 * i + 8 * t;
+      const float* qp = q + frb * d + h * HD + 32 * i + 8 * t;
       f[2] = *reinterpret_cast<const float4*>(qp);
       f[3] = *reinterpret_cast<const float4*>(qp + 4);
     }
@@ -228,9 +233,9 @@ __global__ void __launch_bounds__(128) prefill_attn_kernel(const int32_t* __rest
   for (int nt = 0; nt < 16; nt++) {
     const int dim = 8 * nt + 2 * t;
     if (ra < n_rows)
-      *reinterpret_cast<uint32_t*>(out + (size_t)ra * d + h * HD + dim) = pack2(o[nt][0] * ia, o[nt][1] * ia);
+      *reinterpret_cast<uint32_t*>(out + fra * d + h * HD + dim) = pack2(o[nt][0] * ia, o[nt][1] * ia);
     if (rb < n_rows)
-      *reinterpret_cast<uint32_t*>(out + (size_t)rb * d + h * HD + dim) = pack2(o[nt][2] * ib, o[nt][3] * ib);
+      *reinterpret_cast<uint32_t*>(out + frb * d + h * HD + dim) = pack2(o[nt][2] * ib, o[nt][3] * ib);
   }
 }
 
@@ -245,8 +250,8 @@ void launch_prefill_attention(const Fwd& f, const ModelDims& m, const float* q, 
   }
   const size_t pe = kv_page_elems(m);
   const size_t lo = (size_t)layer * 2 * m.H * FE_PAGE * m.hd;
-  const dim3 grid((f.n_rows + QT - 1) / QT, m.H);
-  launch_k(prefill_attn_kernel, grid, dim3(128), (size_t)kSmem, s, f.seq_pages, f.pos0, f.n_rows, q,
+  const dim3 grid(f.n_ptiles, m.H);
+  launch_k(prefill_attn_kernel, grid, dim3(128), (size_t)kSmem, s, f.ptiles, f.ptab, q,
            (const __nv_bfloat16*)pool, pe, lo, m.H, m.d, m.attn_scale * 1.4426950408889634f, (__nv_bfloat16*)out);
 }
 

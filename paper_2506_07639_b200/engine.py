@@ -38,7 +38,7 @@ class FeConfig(ctypes.Structure):
 
 EXPORTS = (
     "fe_engine_create", "fe_engine_destroy", "fe_weights_init_random", "fe_last_error",
-    "fe_seq_create", "fe_seq_fork", "fe_seq_free", "fe_seq_len", "fe_prefill", "fe_verify", "fe_seq_truncate",
+    "fe_seq_create", "fe_seq_fork", "fe_seq_free", "fe_seq_len", "fe_prefill", "fe_prefill_batch", "fe_verify", "fe_seq_truncate",
     "fe_set_slots",
     "fe_set_slots_lane", "fe_submit_lane", "fe_run_lane", "fe_stream_lane",
     "fe_submit", "fe_run", "fe_request_tokens", "fe_request_release", "fe_request_capture_logits",
@@ -70,6 +70,7 @@ def load_library(path: Path = LIB_PATH) -> ctypes.CDLL:
         "fe_seq_len": [vp, i32, _c_int_p],
         "fe_prefill": [vp, i32, vp, i32, u64, i32],
         "fe_verify": [vp, i32, vp, vp, vp, vp],
+        "fe_prefill_batch": [vp, i32, vp, vp, vp, vp, i32],
         "fe_seq_truncate": [vp, i32, i32],
         "fe_set_slots": [vp, i32],
         "fe_set_slots_lane": [vp, i32, i32],
@@ -176,6 +177,18 @@ class Engine:
         if a.size:
             self._check(self.lib.fe_prefill(self._h, seq, _np_ptr(a), int(a.size),
                                             ctypes.c_uint64(vision_seed & 0xFFFFFFFFFFFFFFFF), vis_id))
+
+    def prefill_batch(self, seqs, ids_list, vision_seeds, vis_id: int) -> None:
+        """Prefill several sequences in as few forwards as the engine holds
+        (rows of all of them packed; one GEMM pass per forward)."""
+        counts = np.asarray([len(x) for x in ids_list], dtype=np.int32)
+        if counts.sum() == 0:
+            return
+        flat = np.ascontiguousarray(np.concatenate([np.asarray(x, dtype=np.int32) for x in ids_list]))
+        sq = np.ascontiguousarray(np.asarray(seqs, dtype=np.int32))
+        vs = np.ascontiguousarray(np.asarray([v & 0xFFFFFFFFFFFFFFFF for v in vision_seeds], dtype=np.uint64))
+        self._check(self.lib.fe_prefill_batch(self._h, int(sq.size), _np_ptr(sq), _np_ptr(counts), _np_ptr(flat),
+                                              _np_ptr(vs), vis_id))
 
     def verify(self, seqs, inputs) -> list[np.ndarray]:
         """Reuse-as-draft verification: extend every `seqs[i]` by `inputs[i]`

@@ -341,36 +341,6 @@ class EngineBackend:
             self.engine.set_slots(self._slots)
 
     # -- trunks & branches -------------------------------------------------------
-    def _branch_point(self, vseed: int, ids: np.ndarray) -> tuple[int, bool]:
-        """Sequence whose KV covers ids exactly up to len(ids) (possibly longer)."""
-        n = ids.size
-        best, best_lcp = None, 0
-        for tr in self._trunks:
-            if tr.vseed != vseed:
-                continue
-            m = min(n, tr.ids.size)
-            neq = np.flatnonzero(tr.ids[:m] != ids[:m])
-            lcp = int(neq[0]) if neq.size else m
-            if lcp > best_lcp or (lcp == best_lcp and best is not None and tr.ids.size < best.ids.size):
-                best, best_lcp = tr, lcp
-        self._clock += 1
-        if best is not None and best_lcp == n:
-            best.stamp = self._clock
-            return best.seq, False
-        eng = self.engine
-        seq = eng.seq_fork(best.seq, best_lcp) if best is not None and best_lcp > 0 else eng.seq_create()
-        try:
-            eng.prefill(seq, ids[best_lcp:], vseed, VIS_ID)
-        except EngineError:
-            eng.seq_free(seq)
-            raise
-        self._trunks.append(_Trunk(vseed, ids.copy(), seq, self._clock))
-        if len(self._trunks) > self._trunk_cap:
-            victim = min(self._trunks, key=lambda t: t.stamp)
-            self._trunks.remove(victim)
-            eng.seq_free(victim.seq)
-        return seq, True
-
     def _prepare(self, ctx: _rt.Context, prefix, spec: _rt.StepSpec, prev, priority: int) -> DeviceRequest:
         """Plan a request and check every limit the device could reject later
         (request cap, max_pos, live requests, KV pages); nothing on the device
@@ -445,16 +415,78 @@ class EngineBackend:
         self._reserved += need
 
     def _materialize(self, extra=()) -> None:
-        """Fork every pending request (and `extra`) off its trunk, prefilling
-        trunks longest input first so nested branch prefixes share one prefill."""
+        """Fork every pending request (and `extra`) off its trunk.  Trunks are
+        planned longest input first, so nested branch prefixes share one
+        prefill; every new trunk of the group (e.g. one per episode of a
+        batched-episode timestep) is then prefilled by ONE batched engine call
+        whose forwards pack the rows of all of them."""
         todo = [h for h in [*self._pending, *extra] if h.branch < 0 and h.error is None and h.ids is not None]
-        for h in sorted(todo, key=lambda h: -h.ids.size):
+        if not todo:
+            return
+        todo.sort(key=lambda h: -h.ids.size)
+        eng = self.engine
+        planned: list[tuple[_Trunk, int]] = []   # new trunk, prefilled from position lcp
+        for h in todo:
+            if self._covering(h.vseed, h.ids, [t for t, _ in planned]) is not None:
+                continue
+            best, lcp = self._best_trunk(h.vseed, h.ids)
             try:
-                trunk, _ = self._branch_point(h.vseed, h.ids)
-                h.branch = self.engine.seq_fork(trunk, h.ids.size)
+                seq = eng.seq_fork(best.seq, lcp) if best is not None and lcp > 0 else eng.seq_create()
             except EngineError as exc:
                 h.error = exc
                 self._release(h)
+                continue
+            self._clock += 1
+            planned.append((_Trunk(h.vseed, h.ids.copy(), seq, self._clock), lcp))
+        if planned:
+            try:
+                eng.prefill_batch([t.seq for t, _ in planned], [t.ids[lcp:] for t, lcp in planned],
+                                  [t.vseed for t, _ in planned], VIS_ID)
+            except EngineError as exc:
+                for t, _ in planned:
+                    eng.seq_free(t.seq)
+                for h in todo:
+                    if h.error is None and self._covering(h.vseed, h.ids, []) is None:
+                        h.error = exc
+                        self._release(h)
+                planned = []
+            self._trunks.extend(t for t, _ in planned)
+        for h in todo:
+            if h.error is not None:
+                continue
+            tr = self._covering(h.vseed, h.ids, [])
+            try:
+                if tr is None:
+                    raise EngineError(f"no trunk covers request {h.name!r}")
+                tr.stamp = self._clock
+                h.branch = eng.seq_fork(tr.seq, h.ids.size)
+            except EngineError as exc:
+                h.error = exc
+                self._release(h)
+        while len(self._trunks) > self._trunk_cap:
+            victim = min(self._trunks, key=lambda t: t.stamp)
+            self._trunks.remove(victim)
+            eng.seq_free(victim.seq)
+
+    def _best_trunk(self, vseed: int, ids: np.ndarray):
+        """Cached trunk with the longest common prefix with ids (ties: the shorter trunk)."""
+        best, best_lcp = None, 0
+        for tr in self._trunks:
+            if tr.vseed != vseed:
+                continue
+            m = min(ids.size, tr.ids.size)
+            neq = np.flatnonzero(tr.ids[:m] != ids[:m])
+            lcp = int(neq[0]) if neq.size else m
+            if lcp > best_lcp or (lcp == best_lcp and best is not None and tr.ids.size < best.ids.size):
+                best, best_lcp = tr, lcp
+        return best, best_lcp
+
+    def _covering(self, vseed: int, ids: np.ndarray, extra) -> Optional[_Trunk]:
+        """A cached (or `extra`) trunk whose ids start with all of ids."""
+        for tr in [*self._trunks, *extra]:
+            if tr.vseed == vseed and tr.ids.size >= ids.size and np.array_equal(tr.ids[: ids.size], ids):
+                return tr
+        return None
 
     def _submit(self, h: DeviceRequest, lane: int) -> None:
         """Hand a materialised request to the device batcher; a rejection is

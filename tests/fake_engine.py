@@ -132,6 +132,13 @@ class FakeEngine:
                 raise B.EngineError("truncate beyond the sequence")
             self.seqs[seq] = (vseed, ids[:n])
 
+    def prefill_batch(self, seqs, ids_list, vision_seeds, vis_id: int) -> None:
+        with self.lock:
+            self.prefill_batch_calls = getattr(self, "prefill_batch_calls", 0) + 1
+        for s, ids, v in zip(seqs, ids_list, vision_seeds):
+            if len(ids):
+                self.prefill(s, ids, v, vis_id)
+
     # batcher
     def set_slots(self, n: int) -> None:
         self.set_slots_lane(0, n)

@@ -671,3 +671,42 @@ def test_completions_server_tokens_equal_the_oracle(schema, oracle_tiny):
         assert got == list(want)
     finally:
         be.close()
+
+
+# ------------------------------------------------------- batched prefill ----
+@pytest.mark.parametrize("config,dtype", [("tiny", "f32"), ("small", "bf16"), ("7b_2layer", "bf16")])
+def test_batched_prefill_equals_separate_prefills(config, dtype):
+    """fe_prefill_batch (rows of several trunks with different observations
+    packed into shared forwards: multi-sequence prefill attention tiles,
+    per-row vision keys) vs one fe_prefill per trunk: the decoded
+    continuations are identical (fp32: logits bit-equal; bf16: within bf16
+    tolerance -- the GEMM M differs -- and the same first token)."""
+    from oracle.backend import frame
+    cfg = M.get_config(config)
+    trunks = [frame(config, list(range(16 + k)), list(range(300 + 40 * k, 300 + 40 * k + 90 + 37 * k)), "plan")
+              for k in range(3)]
+    res = {}
+    for batched in (1, 0):
+        eng = Engine(config, dtype=dtype, seed=0, kv_pages=256, max_rows=512)
+        seqs = [eng.seq_create() for _ in trunks]
+        if batched:
+            eng.prefill_batch(seqs, [t[:-1] for t in trunks], [1000 + k for k in range(3)], M.VIS_ID)
+        else:
+            for k, (s, t) in enumerate(zip(seqs, trunks)):
+                eng.prefill(s, t[:-1], 1000 + k, M.VIS_ID)
+        out = []
+        for s, t in zip(seqs, trunks):
+            r = eng.submit(s, t[-1], 4, 1)
+            eng.capture_logits(r)
+            eng.run(r)
+            out.append((eng.request_tokens(r, 4), eng.request_logits(r, 4)))
+            eng.request_release(r)
+        res[batched] = out
+        eng.close()
+    for (t1, l1), (t0, l0) in zip(res[1], res[0]):
+        if dtype == "f32":
+            assert t1 == t0
+            assert np.array_equal(l1, l0)
+        else:
+            assert np.abs(l1[0] - l0[0]).max() / np.abs(l0[0]).max() < 2e-2
+            assert t1[0] == t0[0]
