@@ -58,6 +58,8 @@ def parse():
                     help="total episodes (config 4; default 1 on one GPU, 64 on several): sharded over "
                          "ranks, each rank's shard batched per timestep")
     ap.add_argument("--seq-steps", type=int, default=4)
+    ap.add_argument("--max-rows", type=int, default=4096,
+                    help="engine rows per forward (a batched trunk prefill packs this many rows per GEMM pass)")
     ap.add_argument("--async-steps", type=int, default=50)
     ap.add_argument("--no-extras", action="store_true", help="skip sequential/async side measurements")
     ap.add_argument("--profile-steps", type=int, default=3, help="eager timesteps timed per kernel after the run")
@@ -340,7 +342,8 @@ def run_engine(args, rank, world, local):
     make_schema, make_profile = WORKLOADS[args.workload]
     schema = make_schema()
     seeds = shard_episodes(list(range(args.episodes)), world, rank) if args.episodes > 1 else [rank]
-    backend = EngineBackend(args.config, dtype=args.dtype, seed=0, device=local, profile=make_profile(0))
+    backend = EngineBackend(args.config, dtype=args.dtype, seed=0, device=local, profile=make_profile(0),
+                            max_rows=args.max_rows)
     eng = backend.engine
     stream = torch.cuda.ExternalStream(eng.stream_handle(), device=local)
     cfg_run = RS.SchedulerConfig(mode=args.mode, slots=8, wall_clock=True)

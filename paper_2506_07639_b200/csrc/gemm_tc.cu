@@ -1351,11 +1351,15 @@ void launch_gemm_tc(const TmaMap& a_map, const TmaMap& b_map64, const TcLaunch& 
   const int tiles = p.m_tiles * p.n_tiles;
   const int P = std::min(tiles * p.kblocks, std::min(n_sm / 2, kPairMaxPairs));
   // DP for all but the last one-to-two waves, which are stream-K'd (no wave tail)
-  // split-K for one m tile over few n tiles (decode-width batches): the
-  // split count minimising waves x k-blocks per unit + a per-split cost for
-  // the partial traffic (~4 k-block wave-times per 168 x 4096 fp32 plane)
+  // split-K when the tiles do not fill the pairs (decode-width batches, O and
+  // down projections): the split count minimising waves x k-blocks per unit
+  // + a per-split cost for the partial traffic (~4 k-block wave-times per
+  // 168 x 4096 fp32 plane; measured, profiles/r2_gemm_pair_split.txt)
   int S = 1;
-  if (g_pair_split && l.split_scratch && p.m_tiles == 1 && tiles < P) {
+  if (g_pair_split > 1 && l.split_scratch && (size_t)g_pair_split * l.M * cols <= l.split_floats &&
+      p.kblocks / g_pair_split >= 4) {
+    S = g_pair_split;  // forced (option tc_split = S > 1; measurement only)
+  } else if (g_pair_split && l.split_scratch && tiles < P) {
     double best = 1e30;
     const double plane = (double)l.M * cols / (168.0 * 4096.0);
     for (int sp = 1; sp <= 8; sp++) {

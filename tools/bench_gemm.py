@@ -21,6 +21,7 @@ ap.add_argument("rows", nargs="*", type=int, default=[33, 48, 96, 168, 256, 448,
 ap.add_argument("--shapes", default="qkv,o,gate_up,down")
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--out", default=None)
+ap.add_argument("--force-splits", type=lambda v: [int(x) for x in v.split(",") if x], default=[])
 args = ap.parse_args()
 
 eng = Engine("small", dtype="bf16", seed=0, kv_pages=8, max_rows=64)
@@ -52,7 +53,9 @@ for rows in args.rows:
         torch.cuda.synchronize()
         line = f"rows {rows:5d} {name:8s} N={N:6d} K={K:6d}:"
         rec = {"rows": rows, "shape": name, "N": N, "K": K}
-        for label, pair, split in (("v1", 0, 0), ("pair_nosplit", 1, 0), ("pair", 1, 1)):
+        variants = [("v1", 0, 0), ("pair_nosplit", 1, 0), ("pair", 1, 1)]
+        variants += [(f"split{k}", 1, k) for k in args.force_splits]
+        for label, pair, split in variants:
             eng.set_option("tc_pair", pair)
             eng.set_option("tc_split", split)
             y.fill_(float("nan"))
