@@ -223,10 +223,12 @@ struct fe_engine {
   cudaEvent_t mk_ev[kLanes] = {};  // last persistent tick of each lane
   bool mk_ev_used[kLanes] = {};
   int mk_pf_stages = 0;  // 0 = the whole ring
+  int mk_gu_pf = 0;      // option "mk_gu_pf": per-mille of gate/up weights L2-prefetched in the QKV reduction
   int mk_per_cta = 4, mk_nc_cap = 8, mk_nc_cap_o = 0;  // chunk plans (mk_make_plans; swept in tools/mk_sweep.sh)
   bool graphs_on = true;
   bool lane1_yields = true;
-  bool prefill_fa = true;  // option "prefill_fa": tensor-core causal prefill attention (bf16)  // option "lane1_yields": reasoning lane defers while the action lane has work
+  bool prefill_fa = true;  // option "prefill_fa": tensor-core causal prefill attention (bf16)
+  bool prefill_tc = true;  // option "prefill_tc": its tcgen05 kernel (prefill_attn_tc.cu), else mma.sync
   float* op_partial = nullptr;  // fe_op_skinny_tc scratch
   size_t op_bytes = 0;
   int* op_counters = nullptr;
@@ -458,6 +460,7 @@ void launch_layers(fe_engine* e, Lane& ln, const fe::Fwd& f, int n, bool decode,
     k.flags = e->mk_flags;
     k.fused = e->mk_fused;
     k.pf_stages = e->mk_pf_stages;
+    k.gu_pf = e->mk_gu_pf;
     const int p = prof_begin(e, ln, PROF_TICK);
     fe::launch_decode_mk(k, st);
     // algorithmic bytes of the tick: every weight once, the K/V pages the
@@ -526,7 +529,8 @@ void launch_layers(fe_engine* e, Lane& ln, const fe::Fwd& f, int n, bool decode,
     } else if (f.span_mode) {
       fe::launch_span_attention(f, m, e->pool_map, e->pool_map16, ws.q, l, ws.partial, ws.attn, st);
     } else if (!decode && f.ptiles && dt == FE_BF16 && m.hd == 128 && e->prefill_fa) {
-      fe::launch_prefill_attention(f, m, ws.q, e->kv_pool, l, ws.attn, st);
+      if (e->prefill_tc && e->use_tc) fe::launch_prefill_attention_tc(f, m, e->pool_map, ws.q, l, ws.attn, st);
+      else fe::launch_prefill_attention(f, m, ws.q, e->kv_pool, l, ws.attn, st);
     } else {
       fe::launch_attention(dt, f, m, ws.q, e->kv_pool, l, ws.partial, ws.attn, st);
     }
@@ -829,7 +833,8 @@ void forward(fe_engine* e, Lane& ln, const std::vector<RowIn>& rows, uint64_t vi
       const int np = rows[j - 1].pos / FE_PAGE + 1;
       const int off = (int)ptab.size();
       ptab.insert(ptab.end(), sq.pages.begin(), sq.pages.begin() + np);
-      for (int t = i; t < j; t += 64) ptiles.push_back({t, std::min(64, j - t), rows[t].pos, off});
+      const int tr = e->prefill_tc && e->use_tc ? 128 : 64;  // query rows per attention tile
+      for (int t = i; t < j; t += tr) ptiles.push_back({t, std::min(tr, j - t), rows[t].pos, off});
       i = j;
     }
     if ((int)ptab.size() > ln.max_partials) ptiles.clear();  // table does not fit: cascade kernel
@@ -1843,6 +1848,9 @@ int fe_set_option(fe_engine* e, const char* key, int64_t value) {
     } else if (k == "mk_flags") {
       e->mk_flags = (int)value;
       clear_graphs(e);
+    } else if (k == "mk_gu_pf") {
+      e->mk_gu_pf = (int)value;
+      clear_graphs(e);
     } else if (k == "mk_pf") {
       e->mk_pf_stages = (int)value;
       clear_graphs(e);
@@ -1871,6 +1879,8 @@ int fe_set_option(fe_engine* e, const char* key, int64_t value) {
     } else if (k == "tc_bn") {
       fe::g_pair_bn = (int)value;
       clear_graphs(e);
+    } else if (k == "prefill_tc") {
+      e->prefill_tc = value != 0 && e->use_tc;
     } else if (k == "prefill_fa") {
       e->prefill_fa = value != 0;
     } else if (k == "lane1_yields") {

@@ -150,6 +150,9 @@ void launch_prefill_attention(const Fwd& f, const ModelDims& m, const float* q, 
 struct TmaMap;
 // bf16, head_dim 128, f.span_mode (attn_span.cu); pool_map: the KV pool as [rows][128] bf16, 64 x 64 boxes
 extern int g_span_dbg;
+// bf16, head_dim 128, f.ptiles of <= 128 rows (prefill_attn_tc.cu: tcgen05 + TMEM + TMA)
+void launch_prefill_attention_tc(const Fwd& f, const ModelDims& m, const TmaMap& pool_map, const float* q, int layer,
+                                 void* attn_out, cudaStream_t s);
 void launch_span_attention(const Fwd& f, const ModelDims& m, const TmaMap& pool_map, const TmaMap& pool_map16,
                            const float* q, int layer, float* partial, void* attn_out, cudaStream_t s);
 void launch_resid(int dtype, const Fwd& f, int N, int K, const void* w, const void* xin, float* x,
