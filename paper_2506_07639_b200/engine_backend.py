@@ -59,7 +59,7 @@ from .refapi import trace as _rt
 REQUEST_CAP = 1024  # tokens per request (device token arena slot, csrc/engine.cu kRequestCap)
 
 
-@dataclass
+@dataclass(eq=False)   # identity: list.remove must not compare the id arrays
 class _Trunk:
     vseed: int
     ids: np.ndarray

@@ -43,6 +43,6 @@ except ImportError:
             "the reference scheduler API `ecot_sched` is required (pip install the reference "
             f"package, or install it into {_CANDIDATES[0]})") from exc
 
-from ecot_sched import backends, batching, schedulers, trace  # noqa: E402,F401
+from ecot_sched import backends, batching, experiments, schedulers, trace  # noqa: E402,F401
 
 REFERENCE_PATH = Path(ecot_sched.__file__).resolve().parent

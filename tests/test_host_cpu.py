@@ -351,3 +351,29 @@ def test_draft_reuse_skips_decode_ticks_on_a_fixed_frame():
         _fixed_obs_episode("parallel_sync", be, schema, 5)
         ticks[draft] = len(eng.occupancy_log)
     assert ticks[True] < 0.5 * ticks[False], ticks
+
+
+# --------------------------------------------------- experiments harness ----
+def test_reference_experiment_harness_runs_on_the_engine(tmp_path):
+    """The unmodified reference `run_experiment` (every mode cell, traces.jsonl,
+    comparison rows) with its backend factory served by EngineBackend
+    (paper_2506_07639_b200.experiments): the cell traces equal the same
+    harness over the synchronous HashBackend stand-in."""
+    from ecot_sched.experiments import spec_from_dict
+    from fake_engine import HashBackend
+
+    from paper_2506_07639_b200.experiments import engine_backends, run_engine_experiment
+    spec = spec_from_dict({"name": "eng", "modes": [{"mode": "sequential"}, {"mode": "parallel_sync"},
+                                                    {"mode": "parallel_async"}],
+                           "episode_len": 4, "repetitions": 2, "seed": 3, "slots": 8})
+    be, _ = fake_backend(profile=spec.profile)
+    out = run_engine_experiment(spec, tmp_path / "engine", backend=be)
+    with engine_backends(lambda sp, rep: HashBackend(profile=sp.profile.with_seed(sp.profile.seed + rep))):
+        ref = ecot_sched.experiments.run_experiment(spec, tmp_path / "hash")
+    assert not out.aborted and len(out.cell_summaries) == len(spec.modes) * spec.repetitions
+    for cell in sorted((tmp_path / "engine" / "eng").rglob("traces.jsonl")):
+        other = tmp_path / "hash" / "eng" / cell.relative_to(tmp_path / "engine" / "eng")
+        a = [line.split(b'"wall_ms"')[0] for line in cell.read_bytes().splitlines()]
+        b = [line.split(b'"wall_ms"')[0] for line in other.read_bytes().splitlines()]
+        assert a == b, cell
+    assert ecot_sched.experiments._make_backend.__module__ == "ecot_sched.experiments"
