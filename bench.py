@@ -62,6 +62,8 @@ def parse():
                     help="engine rows per forward (a batched trunk prefill packs this many rows per GEMM pass)")
     ap.add_argument("--async-steps", type=int, default=50)
     ap.add_argument("--no-extras", action="store_true", help="skip sequential/async side measurements")
+    ap.add_argument("--background-depth", type=int, default=1,
+                    help="decode ticks the background async ticker keeps queued (1 or 2)")
     ap.add_argument("--profile-steps", type=int, default=3, help="eager timesteps timed per kernel after the run")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-config", default="7b_2layer",
@@ -309,7 +311,8 @@ def run_extras(args, backend, schema, make_profile, seed, stream, local):
     # config 3 proper: the reasoning refresh free-running in the background
     # (background ticker), the action merged into its ticks at high priority
     backend2 = EngineBackend(args.config, dtype=args.dtype, seed=0, device=local, profile=make_profile(0),
-                             engine=backend.engine, async_mode="background")
+                             engine=backend.engine, async_mode="background",
+                             background_depth=args.background_depth)
     asy2 = RS.make_runner(RS.SchedulerConfig(mode="parallel_async", slots=8, wall_clock=True), backend2, schema)
     _, a2host, a2res = time_mode(backend2, asy2, 3000 + seed, 0, 1 + args.async_steps, stream)
     asy2.engine.drain()

@@ -142,7 +142,8 @@ struct Lane {
   fe::TmaMap map_xn{}, map_attn{}, map_act{};        // 128-row boxes (tile GEMM A operand)
   fe::TmaMap map_xn16{}, map_attn16{}, map_act16{};  // 16-row boxes (skinny GEMM B operand)
   std::unordered_map<long, GraphSlot> graphs;       // key: rows * 4096 + attention item bucket
-  cudaEvent_t tick_ev[2] = {};                      // lane 1 pacing (run_lane)
+  cudaEvent_t tick_ev[2] = {};                      // tick pacing (run_lane)
+  long pace_n = 0;                                  // ticks recorded for pacing (across run calls)
   // continuous batcher
   int slots = 8;
   std::vector<int> slot_req;
@@ -227,6 +228,7 @@ struct fe_engine {
   int mk_per_cta = 4, mk_nc_cap = 8, mk_nc_cap_o = 0;  // chunk plans (mk_make_plans; swept in tools/mk_sweep.sh)
   bool graphs_on = true;
   bool lane1_yields = true;
+  int lane0_pace = 0;  // option "lane0_pace": lane-0 ticks kept queued (1 or 2; 0: unpaced)
   bool prefill_fa = true;  // option "prefill_fa": tensor-core causal prefill attention (bf16)
   bool prefill_tc = true;  // option "prefill_tc": its tcgen05 kernel (prefill_attn_tc.cu), else mma.sync
   float* op_partial = nullptr;  // fe_op_skinny_tc scratch
@@ -1403,10 +1405,16 @@ int run_lane(fe_engine* e, int lane, int32_t stop_req, int32_t max_ticks, int32_
         completed_tick[nc] = t;
         nc++;
       }
-      if (lane == 1 && e->lane1_yields) {  // keep <= 2 reasoning ticks queued on the device
-        CK(cudaEventRecord(ln.tick_ev[t & 1], ln.stream));
-        pace = ln.tick_ev[(t + 1) & 1];
-        paced = t > 0;
+      if ((lane == 1 && e->lane1_yields) || (lane == 0 && e->lane0_pace)) {
+        // keep <= 2 ticks queued on the device: a background ticker (lane 0,
+        // option "lane0_pace") or the reasoning lane would otherwise run
+        // arbitrarily far ahead of the GPU, and a later action would queue
+        // behind all of those ticks
+        CK(cudaEventRecord(ln.tick_ev[ln.pace_n & 1], ln.stream));
+        const bool one = lane == 0 && e->lane0_pace == 1;  // depth 1: this tick done before returning
+        pace = ln.tick_ev[(ln.pace_n + (one ? 0 : 1)) & 1];
+        paced = one || ln.pace_n > 0;
+        ln.pace_n++;
       }
       t++;
     }
@@ -1883,6 +1891,8 @@ int fe_set_option(fe_engine* e, const char* key, int64_t value) {
       e->prefill_tc = value != 0 && e->use_tc;
     } else if (k == "prefill_fa") {
       e->prefill_fa = value != 0;
+    } else if (k == "lane0_pace") {
+      e->lane0_pace = (int)std::max<int64_t>(0, std::min<int64_t>(2, value));
     } else if (k == "lane1_yields") {
       e->lane1_yields = value != 0;
     } else if (k == "mk") {

@@ -166,7 +166,8 @@ class EngineBackend:
     def __init__(self, config="tiny", dtype: str = "f32", seed: int = 0,
                  profile: SyntheticProfile | None = None, device: int = 0,
                  engine: Engine | None = None, trunk_cache: int = 64, async_mode: str = "lockstep",
-                 request_log: list | None = None, draft_reuse: bool = False, **engine_kw):
+                 request_log: list | None = None, draft_reuse: bool = False, background_depth: int = 1,
+                 **engine_kw):
         """`async_mode="lockstep"`: the async runner's device engine advances
         exactly as many decode iterations as each control step's action needs
         (the reference landing order, byte-comparable traces);
@@ -203,6 +204,7 @@ class EngineBackend:
         self._fixed_slots = False    # an async engine fixes the batcher to the runner's slots
         self.requests = 0
         self.draft_reuse = draft_reuse
+        self.background_depth = background_depth   # decode ticks the background ticker keeps queued
         self.draft_stats = {"requests": 0, "drafted": 0, "draft_tokens": 0, "accepted_tokens": 0,
                             "verified_tokens": 0, "resolved_by_verify": 0, "verify_forwards": 0,
                             "verify_rows": 0}
@@ -667,6 +669,10 @@ class BackgroundAsyncEngine:
         self._errors: list[BaseException] = []
         self._stop = False
         self._held = False               # a control step is issuing its requests
+        # the ticker enqueues one tick per call and would run arbitrarily far
+        # ahead of the GPU; pacing keeps <= 2 ticks queued, so an action waits
+        # behind at most those
+        self._set_pace(backend.background_depth)
         self._thread = threading.Thread(target=self._loop, name="fastecot-background-ticker", daemon=True)
         self._thread.start()
         backend._async_engines.append(self)
@@ -786,10 +792,16 @@ class BackgroundAsyncEngine:
                 self._cv.wait(0.05)
         self._raise_background_error()
 
+    def _set_pace(self, on: int) -> None:
+        setter = getattr(self.backend.engine, "set_option", None)
+        if setter is not None:   # (the CPU stand-in engine has no options)
+            setter("lane0_pace", on)
+
     def close(self) -> None:
         with self._cv:
             self._stop = True
             self._cv.notify_all()
         self._thread.join(timeout=10.0)
+        self._set_pace(0)
         if self in self.backend._async_engines:
             self.backend._async_engines.remove(self)
