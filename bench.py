@@ -62,6 +62,9 @@ def parse():
                     help="engine rows per forward (a batched trunk prefill packs this many rows per GEMM pass)")
     ap.add_argument("--async-steps", type=int, default=50)
     ap.add_argument("--no-extras", action="store_true", help="skip sequential/async side measurements")
+    ap.add_argument("--vision", action="store_true",
+                    help="VIS rows from the vision tower + projector (DINOv2-L/14-shaped, 224 px) instead of "
+                         "synthetic embeddings")
     ap.add_argument("--background-depth", type=int, default=1,
                     help="decode ticks the background async ticker keeps queued (1 or 2)")
     ap.add_argument("--profile-steps", type=int, default=3, help="eager timesteps timed per kernel after the run")
@@ -346,7 +349,7 @@ def run_engine(args, rank, world, local):
     schema = make_schema()
     seeds = shard_episodes(list(range(args.episodes)), world, rank) if args.episodes > 1 else [rank]
     backend = EngineBackend(args.config, dtype=args.dtype, seed=0, device=local, profile=make_profile(0),
-                            max_rows=args.max_rows)
+                            max_rows=args.max_rows, vision=True if args.vision else None)
     eng = backend.engine
     stream = torch.cuda.ExternalStream(eng.stream_handle(), device=local)
     cfg_run = RS.SchedulerConfig(mode=args.mode, slots=8, wall_clock=True)
@@ -495,6 +498,7 @@ def main():
                                 f"per timestep per GPU"),
                    "model": args.config, "mode": args.mode, "schema": args.workload,
                    "episodes": eps, "episodes_per_gpu": eps / world, "slots": 8,
+                   "vision": "ViT tower + projector (vit_l14 preset)" if args.vision else "synthetic VIS embeddings",
                    "l2": "no flush: every decode iteration streams 13.2 GB of weights (> 126 MB L2)"},
         "e2e": {"value": e2e, "unit": "steps/s" if args.episodes <= 1 else "episode-steps/s",
                 "h2d_bytes_per_step": (s1["h2d_bytes"] - s0["h2d_bytes"]) / K,

@@ -71,6 +71,18 @@ int fe_seq_len(fe_engine* e, int32_t seq, int32_t* len);
  * `vis_id` take row (pos-1) of the vision embedding seeded by `vision_seed` */
 int fe_prefill(fe_engine* e, int32_t seq, const int32_t* ids, int32_t n, uint64_t vision_seed, int32_t vis_id);
 
+/* vision tower + projector: VIS placeholders take the
+ * rows a ViT (pre-LayerNorm, `layers` x `heads`, patch `patch` over an
+ * img x img synthetic image of the observation) and a 2-layer GELU projector
+ * produce, instead of the synthetic embeddings; the patch count must equal
+ * the framing's VIS count.  `slots` observations stay cached. */
+typedef struct {
+  int32_t img, patch, d, layers, heads, mlp, proj_hidden;
+  float eps;
+} fe_vision_config;
+int fe_vision_enable(fe_engine* e, const fe_vision_config* vc, uint64_t seed, int32_t slots);
+int fe_vision_encode(fe_engine* e, uint64_t vision_seed, float* out_host);  /* [P][d_model] rows (tests) */
+
 /* batched prefill: seqs[i] gets counts[i] ids (concatenated in `ids`),
  * vision placeholders seeded by vision_seeds[i]; rows of all sequences are
  * packed into as few forwards as the engine holds (one GEMM pass per

@@ -78,6 +78,13 @@ def load_library() -> ctypes.CDLL:
     lib.or_rmsnorm.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_float]
     lib.or_matmul.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_int] * 3
     lib.or_attention.argtypes = [ctypes.c_void_p] * 6 + [ctypes.c_int]
+    lib.or_vision_create.restype = ctypes.c_void_p
+    lib.or_vision_create.argtypes = [ctypes.c_int] * 8 + [ctypes.c_float, ctypes.c_uint64]
+    lib.or_vision_destroy.argtypes = [ctypes.c_void_p]
+    lib.or_vision_encode.restype = ctypes.c_int
+    lib.or_vision_encode.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p]
+    lib.or_set_vision.restype = ctypes.c_int
+    lib.or_set_vision.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
     lib.or_tensor.restype = ctypes.c_void_p
     lib.or_tensor.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
     return lib
@@ -90,8 +97,10 @@ def _ptr(a: np.ndarray) -> ctypes.c_void_p:
 class OracleModel:
     """Handle on the C model; weights are generated at construction."""
 
-    def __init__(self, config: str = "tiny", seed: int = 0, threads: int = 0, max_pos: int = 8192):
+    def __init__(self, config: str = "tiny", seed: int = 0, threads: int = 0, max_pos: int = 8192,
+                 vision=None):
         self.lib = load_library()
+        self._vh = None
         self.config = config
         d, L, H, hd, F, nv = SHAPES[config]
         self.d, self.L, self.H, self.hd, self.F, self.n_vision = d, L, H, hd, F, nv
@@ -104,12 +113,30 @@ class OracleModel:
                                      _ptr(self.rope), max_pos, threads or (os.cpu_count() or 1))
         if not self._h:
             raise RuntimeError("or_create failed")
+        self.vision = None
+        if vision:   # VIS rows from the vision tower + projector (oracle.c or_vision_encode)
+            from paper_2506_07639_b200.model import get_vision
+            v = get_vision(vision, config)
+            self._vh = self.lib.or_vision_create(v.img, v.patch, v.d, v.layers, v.heads, v.mlp, v.proj_hidden, d,
+                                                 ctypes.c_float(v.eps), ctypes.c_uint64(seed))
+            if not self._vh or self.lib.or_set_vision(self._h, self._vh) != 0:
+                raise RuntimeError("or_vision_create / or_set_vision failed")
+            self.vision = v
+
+    def vision_encode(self, vseed: int) -> np.ndarray:
+        out = np.empty((self.vision.patches, self.d), dtype=np.float32)
+        self.lib.or_vision_encode(self._vh, ctypes.c_uint64(vseed & 0xFFFFFFFFFFFFFFFF), _ptr(out))
+        return out
 
     def __del__(self):
         h = getattr(self, "_h", None)
         if h:
             self.lib.or_destroy(h)
             self._h = None
+        vh = getattr(self, "_vh", None)
+        if vh:
+            self.lib.or_vision_destroy(vh)
+            self._vh = None
 
     def generate(self, ids, vseed: int, n_out: int, want_logits: bool = False):
         ids = np.ascontiguousarray(np.asarray(ids, dtype=np.int32))
@@ -154,10 +181,10 @@ class OracleBackend:
     supports_prefix_conditioning = True
 
     def __init__(self, config: str = "tiny", seed: int = 0, profile=None, threads: int = 0,
-                 model: OracleModel | None = None):
+                 model: OracleModel | None = None, vision=None):
         from paper_2506_07639_b200.refapi import backends as rb  # the reference API (profile is data)
         default_profile = rb.default_profile
-        self.model = model or OracleModel(config, seed, threads)
+        self.model = model or OracleModel(config, seed, threads, vision=vision)
         self.config = config
         self.profile = profile or default_profile(seed)
         self.requests = 0

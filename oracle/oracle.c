@@ -139,7 +139,11 @@ typedef struct {
     float* rope;      /* [max_pos][2][hd/2] */
     entry_t cache[N_ENTRIES];
     uint64_t clock;
+    struct or_vision* vision;   /* optional vision tower: VIS rows take its output */
 } or_model;
+
+typedef struct or_vision or_vision;
+static const float* vision_rows(or_vision* v, uint64_t vseed);
 
 or_model* or_create(int d, int L, int H, int hd, int F, int V, int n_text, float eps,
                     float attn_scale, uint64_t seed, const float* rope, int max_pos, int n_threads) {
@@ -308,10 +312,13 @@ static void attend(const or_model* m, float* out, const float* q, const float* k
 static void embed_rows(const or_model* m, float* x, const int32_t* ids, int p0, int n, uint64_t vseed,
                        int vis_id) {
     uint64_t vkey = tensor_key(vseed, T_VISION);
+    const float* vis = m->vision ? vision_rows(m->vision, vseed) : NULL;
     for (int t = 0; t < n; t++) {
         int pos = p0 + t;
         float* row = x + (size_t)t * m->d;
-        if (ids[pos] == vis_id) {
+        if (ids[pos] == vis_id && vis) {
+            memcpy(row, vis + (size_t)(pos - 1) * m->d, sizeof(float) * m->d);
+        } else if (ids[pos] == vis_id) {
             uint64_t base = (uint64_t)(pos - 1) * m->d;
             for (int k = 0; k < m->d; k++) row[k] = centered(vkey, base + k) * VISION_MULT;
         } else {
@@ -463,4 +470,210 @@ const float* or_tensor(const or_model* m, int which, int layer) {
         case L_WDOWN: return ly->wd;
     }
     return NULL;
+}
+
+/* ================= vision tower + projector ===========
+ * A pre-LayerNorm ViT over a synthetic image of the observation, then a
+ * 2-layer MLP projector into the LLM width: the 256 (n_vision) VIS rows.
+ * Restated by csrc/vision.cu in the same canonical arithmetic (fp32 mode
+ * bit-exact).  Definition:
+ *   pixel(c, y, x)  = 2 * centered(key(vseed, T_IMAGE), (c * img + y) * img + x)
+ *   patch p (row-major grid), feature f = (c * P + dy) * P + dx, zero-padded to kp
+ *   x = cdot(pe_w, patch) ; x = x + pe_b ; x = x + pos[p]
+ *   layer: x += O(attn(LN1 x)) ; x += fc2(gelu(fc1(LN2 x)))   (linears add their bias after the dot)
+ *   LN(x) = ((x - mean) * r) * g + b, mean = cdot(x, 1) / d, r = 1 / sqrt(cdot(xc, xc) / d + eps)
+ *   attn: non-causal over all P patches, s = cdot(q, k) * hd^-1/2, fe_exp softmax, in order
+ *   gelu(z) = z / (1 + fe_exp(-1.702 z))
+ *   out = p2(gelu(p1(LN_f x)))
+ */
+enum { T_IMAGE = 5, T_VB = 1 << 20 };
+enum { V_PE_W, V_PE_B, V_POS, V_LNF_G, V_LNF_B, V_P1_W, V_P1_B, V_P2_W, V_P2_B };
+enum { VL_LN1_G, VL_LN1_B, VL_QKV_W, VL_QKV_B, VL_O_W, VL_O_B, VL_LN2_G, VL_LN2_B, VL_FC1_W, VL_FC1_B,
+       VL_FC2_W, VL_FC2_B };
+
+typedef struct {
+    float *ln1_g, *ln1_b, *qkv_w, *qkv_b, *o_w, *o_b, *ln2_g, *ln2_b, *fc1_w, *fc1_b, *fc2_w, *fc2_b;
+} vlayer_t;
+
+#define V_CACHE 8
+struct or_vision {
+    int img, patch, grid, P, d, L, H, hd, mlp, ph, out, kp;
+    float eps;
+    uint64_t seed;
+    float *pe_w, *pe_b, *pos, *lnf_g, *lnf_b, *p1_w, *p1_b, *p2_w, *p2_b;
+    vlayer_t* layers;
+    uint64_t cache_seed[V_CACHE];
+    float* cache_out[V_CACHE];
+    int cache_next;
+};
+
+static float* vfill(uint64_t seed, uint64_t tid, size_t n, int norm) {
+    float* w = (float*)malloc(sizeof(float) * n);
+    if (norm) fill_norm(w, seed, tid, n);
+    else fill_linear(w, seed, tid, n);
+    return w;
+}
+
+or_vision* or_vision_create(int img, int patch, int d, int L, int H, int mlp, int ph, int out, float eps,
+                            uint64_t seed) {
+    or_vision* v = (or_vision*)calloc(1, sizeof(or_vision));
+    v->img = img; v->patch = patch; v->grid = img / patch; v->P = v->grid * v->grid;
+    v->d = d; v->L = L; v->H = H; v->hd = d / H; v->mlp = mlp; v->ph = ph; v->out = out; v->eps = eps;
+    v->kp = (3 * patch * patch + 127) / 128 * 128;
+    v->seed = seed;
+    v->pe_w = vfill(seed, T_VB + V_PE_W, (size_t)d * v->kp, 0);
+    v->pe_b = vfill(seed, T_VB + V_PE_B, d, 0);
+    v->pos = vfill(seed, T_VB + V_POS, (size_t)v->P * d, 0);
+    v->lnf_g = vfill(seed, T_VB + V_LNF_G, d, 1);
+    v->lnf_b = vfill(seed, T_VB + V_LNF_B, d, 0);
+    v->p1_w = vfill(seed, T_VB + V_P1_W, (size_t)ph * d, 0);
+    v->p1_b = vfill(seed, T_VB + V_P1_B, ph, 0);
+    v->p2_w = vfill(seed, T_VB + V_P2_W, (size_t)out * ph, 0);
+    v->p2_b = vfill(seed, T_VB + V_P2_B, out, 0);
+    v->layers = (vlayer_t*)calloc(L, sizeof(vlayer_t));
+    for (int l = 0; l < L; l++) {
+        vlayer_t* y = &v->layers[l];
+        uint64_t b = T_VB + 16 + 16 * (uint64_t)l;
+        y->ln1_g = vfill(seed, b + VL_LN1_G, d, 1);
+        y->ln1_b = vfill(seed, b + VL_LN1_B, d, 0);
+        y->qkv_w = vfill(seed, b + VL_QKV_W, (size_t)3 * d * d, 0);
+        y->qkv_b = vfill(seed, b + VL_QKV_B, (size_t)3 * d, 0);
+        y->o_w = vfill(seed, b + VL_O_W, (size_t)d * d, 0);
+        y->o_b = vfill(seed, b + VL_O_B, d, 0);
+        y->ln2_g = vfill(seed, b + VL_LN2_G, d, 1);
+        y->ln2_b = vfill(seed, b + VL_LN2_B, d, 0);
+        y->fc1_w = vfill(seed, b + VL_FC1_W, (size_t)mlp * d, 0);
+        y->fc1_b = vfill(seed, b + VL_FC1_B, mlp, 0);
+        y->fc2_w = vfill(seed, b + VL_FC2_W, (size_t)d * mlp, 0);
+        y->fc2_b = vfill(seed, b + VL_FC2_B, d, 0);
+    }
+    return v;
+}
+
+void or_vision_destroy(or_vision* v) {
+    if (!v) return;
+    for (int l = 0; l < v->L; l++) {
+        vlayer_t* y = &v->layers[l];
+        free(y->ln1_g); free(y->ln1_b); free(y->qkv_w); free(y->qkv_b); free(y->o_w); free(y->o_b);
+        free(y->ln2_g); free(y->ln2_b); free(y->fc1_w); free(y->fc1_b); free(y->fc2_w); free(y->fc2_b);
+    }
+    for (int i = 0; i < V_CACHE; i++) free(v->cache_out[i]);
+    free(v->layers); free(v->pe_w); free(v->pe_b); free(v->pos); free(v->lnf_g); free(v->lnf_b);
+    free(v->p1_w); free(v->p1_b); free(v->p2_w); free(v->p2_b); free(v);
+}
+
+static void vlinear(float* y, const float* x, const float* W, const float* b, int n, int N, int K) {
+    matmul(y, x, W, n, N, K);
+    for (size_t i = 0; i < (size_t)n * N; i++) y[i] = y[i] + b[i % N];
+}
+
+static void vlayernorm(float* y, const float* x, const float* g, const float* b, int n, int d, float eps) {
+    float* ones = (float*)malloc(sizeof(float) * d);
+    float* xc = (float*)malloc(sizeof(float) * d);
+    for (int k = 0; k < d; k++) ones[k] = 1.0f;
+    for (int t = 0; t < n; t++) {
+        const float* xr = x + (size_t)t * d;
+        float mean = cdot(xr, ones, d) / (float)d;
+        for (int k = 0; k < d; k++) xc[k] = xr[k] - mean;
+        float var = cdot(xc, xc, d) / (float)d;
+        float r = 1.0f / sqrtf(var + eps);
+        for (int k = 0; k < d; k++) {
+            float u = xc[k] * r;
+            u = u * g[k];
+            y[(size_t)t * d + k] = u + b[k];
+        }
+    }
+    free(ones); free(xc);
+}
+
+static inline float vgelu(float z) { return z / (1.0f + fe_exp(-1.702f * z)); }
+
+static void vattention(const or_vision* v, float* out, const float* qkv) {
+    const int P = v->P, d = v->d, hd = v->hd;
+    const float scale = 1.0f / sqrtf((float)hd);
+#pragma omp parallel for schedule(static)
+    for (int t = 0; t < P * v->H; t++) {
+        int p = t / v->H, h = t % v->H;
+        const float* q = qkv + (size_t)p * 3 * d + h * hd;
+        float* s = (float*)malloc(sizeof(float) * P);
+        float m = -INFINITY;
+        for (int j = 0; j < P; j++) {
+            s[j] = cdot(q, qkv + (size_t)j * 3 * d + d + h * hd, hd) * scale;
+            if (s[j] > m) m = s[j];
+        }
+        float l = 0.0f;
+        float o[256];
+        for (int i = 0; i < hd; i++) o[i] = 0.0f;
+        for (int j = 0; j < P; j++) {
+            float pj = fe_exp(s[j] - m);
+            l = l + pj;
+            const float* vj = qkv + (size_t)j * 3 * d + 2 * d + h * hd;
+            for (int i = 0; i < hd; i++) o[i] = fmaf(pj, vj[i], o[i]);
+        }
+        for (int i = 0; i < hd; i++) out[(size_t)p * d + h * hd + i] = o[i] / l;
+        free(s);
+    }
+}
+
+/* out[P][out] = vision rows of the observation seeded vseed */
+int or_vision_encode(or_vision* v, uint64_t vseed, float* out) {
+    const int P = v->P, d = v->d, kp = v->kp, ps = v->patch, img = v->img;
+    float* patches = (float*)calloc((size_t)P * kp, sizeof(float));
+    uint64_t ikey = tensor_key(vseed, T_IMAGE);
+    for (int p = 0; p < P; p++) {
+        int gy = p / v->grid, gx = p % v->grid;
+        for (int c = 0; c < 3; c++)
+            for (int dy = 0; dy < ps; dy++)
+                for (int dx = 0; dx < ps; dx++) {
+                    int y = gy * ps + dy, xx = gx * ps + dx;
+                    patches[(size_t)p * kp + (c * ps + dy) * ps + dx] =
+                        centered(ikey, (uint64_t)((c * img + y) * img + xx)) * 2.0f;
+                }
+    }
+    float* x = (float*)malloc(sizeof(float) * (size_t)P * d);
+    float* ln = (float*)malloc(sizeof(float) * (size_t)P * d);
+    float* qkv = (float*)malloc(sizeof(float) * (size_t)P * 3 * d);
+    float* att = (float*)malloc(sizeof(float) * (size_t)P * d);
+    float* tmp = (float*)malloc(sizeof(float) * (size_t)P * d);
+    float* hid = (float*)malloc(sizeof(float) * (size_t)P * (v->mlp > v->ph ? v->mlp : v->ph));
+    vlinear(x, patches, v->pe_w, v->pe_b, P, d, kp);
+    for (size_t i = 0; i < (size_t)P * d; i++) x[i] = x[i] + v->pos[i];
+    for (int l = 0; l < v->L; l++) {
+        const vlayer_t* y = &v->layers[l];
+        vlayernorm(ln, x, y->ln1_g, y->ln1_b, P, d, v->eps);
+        vlinear(qkv, ln, y->qkv_w, y->qkv_b, P, 3 * d, d);
+        vattention(v, att, qkv);
+        vlinear(tmp, att, y->o_w, y->o_b, P, d, d);
+        for (size_t i = 0; i < (size_t)P * d; i++) x[i] = x[i] + tmp[i];
+        vlayernorm(ln, x, y->ln2_g, y->ln2_b, P, d, v->eps);
+        vlinear(hid, ln, y->fc1_w, y->fc1_b, P, v->mlp, d);
+        for (size_t i = 0; i < (size_t)P * v->mlp; i++) hid[i] = vgelu(hid[i]);
+        vlinear(tmp, hid, y->fc2_w, y->fc2_b, P, d, v->mlp);
+        for (size_t i = 0; i < (size_t)P * d; i++) x[i] = x[i] + tmp[i];
+    }
+    vlayernorm(ln, x, v->lnf_g, v->lnf_b, P, d, v->eps);
+    vlinear(hid, ln, v->p1_w, v->p1_b, P, v->ph, d);
+    for (size_t i = 0; i < (size_t)P * v->ph; i++) hid[i] = vgelu(hid[i]);
+    vlinear(out, hid, v->p2_w, v->p2_b, P, v->out, v->ph);
+    free(patches); free(x); free(ln); free(qkv); free(att); free(tmp); free(hid);
+    return 0;
+}
+
+static const float* vision_rows(or_vision* v, uint64_t vseed) {
+    for (int i = 0; i < V_CACHE; i++)
+        if (v->cache_out[i] && v->cache_seed[i] == vseed) return v->cache_out[i];
+    int i = v->cache_next;
+    v->cache_next = (v->cache_next + 1) % V_CACHE;
+    if (!v->cache_out[i]) v->cache_out[i] = (float*)malloc(sizeof(float) * (size_t)v->P * v->out);
+    or_vision_encode(v, vseed, v->cache_out[i]);
+    v->cache_seed[i] = vseed;
+    return v->cache_out[i];
+}
+
+/* VIS rows of every later generate take the tower's output (n_vision == P) */
+int or_set_vision(or_model* m, or_vision* v) {
+    if (v && v->out != m->d) return 1;
+    m->vision = v;
+    for (int e = 0; e < N_ENTRIES; e++) m->cache[e].n = 0;   /* KV cached under the old embeddings */
+    return 0;
 }

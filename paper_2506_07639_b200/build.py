@@ -17,7 +17,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 OUT = PKG / "_build" / "libfastecot.so"
-SOURCES = ["kernels.cu", "gemm_tc.cu", "decode_mk.cu", "decode_mk_trace.cu", "prefill_attn.cu", "prefill_attn_tc.cu", "attn_span.cu", "engine.cu"]
+SOURCES = ["kernels.cu", "gemm_tc.cu", "decode_mk.cu", "decode_mk_trace.cu", "prefill_attn.cu", "prefill_attn_tc.cu", "attn_span.cu", "vision.cu", "engine.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "--fmad=false", "-std=c++17",
          "-Xcompiler", "-fPIC", "-diag-suppress", "1886,177"]

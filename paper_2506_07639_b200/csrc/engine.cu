@@ -19,6 +19,7 @@
 #include "common.cuh"
 #include "engine_internal.h"
 #include "gemm_tc.h"
+#include "vision.h"
 #include "decode_mk.h"
 #include "../../include/fastecot.h"
 
@@ -202,6 +203,13 @@ struct fe_engine {
   int n_sm = 148;
   fe::TmaMap pool_map{};    // the KV pool as [rows][128] bf16, 64 x 64 boxes (span attention)
   fe::TmaMap pool_map16{};  // same, 64 x 16 boxes (partially filled last pages)
+  // vision tower (fe_vision_enable): VIS rows from the observation's image
+  std::unique_ptr<fe::Vision> vis;
+  std::vector<float*> vis_buf;       // [slots] P x d fp32
+  std::vector<uint64_t> vis_seed;
+  std::vector<int64_t> vis_stamp;
+  int64_t vis_clock = 0;
+  int64_t vis_encodes = 0;
   int tc_min_rows = 17;
   // forwards up to this many rows use the skinny GEMM, wider ones the tile
   // GEMM (option "sk_max_rows"; measured in the engine at 7B: skinny ahead
@@ -580,7 +588,7 @@ void launch_layers(fe_engine* e, Lane& ln, const fe::Fwd& f, int n, bool decode,
 // sequence contiguously, in order).  Builds row metadata and the cascade work
 // list, then launches the layer stack (or replays the lane's decode graph).
 void forward(fe_engine* e, Lane& ln, const std::vector<RowIn>& rows, uint64_t vision_seed,
-             const std::vector<uint64_t>* vseeds = nullptr) {
+             const std::vector<uint64_t>* vseeds = nullptr, bool vis_ptrs = false) {
   const fe::ModelDims& m = e->m;
   const int n = (int)rows.size();
   if (n == 0) return;
@@ -849,7 +857,8 @@ void forward(fe_engine* e, Lane& ln, const std::vector<RowIn>& rows, uint64_t vi
   }
   if (vseeds) {
     std::vector<uint64_t> keys(vseeds->size());
-    for (size_t k = 0; k < keys.size(); k++) keys[k] = fe::tensor_key((*vseeds)[k], 4 /* T_VISION */);
+    for (size_t k = 0; k < keys.size(); k++)
+      keys[k] = vis_ptrs ? (*vseeds)[k] : fe::tensor_key((*vseeds)[k], 4 /* T_VISION */);
     std::memcpy(hbuf + L.o_vkeys, keys.data(), 8 * keys.size());
     copy(L.o_vkeys, 8 * keys.size());
   }
@@ -876,6 +885,7 @@ void forward(fe_engine* e, Lane& ln, const std::vector<RowIn>& rows, uint64_t vi
   f.n_ptiles = (int)ptiles.size();
   f.ptab = (const int32_t*)(dbuf + L.o_spages);
   f.vision_keys = vseeds ? (const uint64_t*)(dbuf + L.o_vkeys) : nullptr;
+  f.vis_ptrs = vis_ptrs;
   f.span_mode = span_mode;
   f.item_slots = (const int32_t*)(dbuf + L.o_slots);
   f.row_nspans = (const int32_t*)(dbuf + L.o_nspans);
@@ -948,14 +958,39 @@ void prefill_multi(fe_engine* e, const std::vector<PrefillSeg>& segs, int vis_id
       if (&o != &sg && o.seq == sg.seq) throw Error("prefill: a sequence listed twice");
   }
   std::vector<RowIn> rows;
-  std::vector<uint64_t> vseeds;
+  std::vector<uint64_t> vseeds;  // per-forward table: vision seeds, or (tower on) VIS-row buffer pointers
+  std::vector<int> pinned;       // tower slots the pending forward reads
   int chunks = 0;
   auto flush = [&]() {
     if (rows.empty()) return;
-    forward(e, ln, rows, 0, &vseeds);
+    forward(e, ln, rows, 0, &vseeds, e->vis != nullptr);
     rows.clear();
     vseeds.clear();
+    pinned.clear();
     chunks = 0;
+  };
+  // VIS rows of an observation: the tower's output, encoded once per seed
+  // (LRU slots; a slot the pending forward reads is never recycled)
+  auto vis_rows = [&](uint64_t vseed) -> uint64_t {
+    int slot = -1;
+    for (size_t i = 0; i < e->vis_seed.size(); i++)
+      if (e->vis_stamp[i] >= 0 && e->vis_seed[i] == vseed) slot = (int)i;
+    if (slot < 0) {
+      for (size_t i = 0; i < e->vis_seed.size(); i++) {
+        if (std::find(pinned.begin(), pinned.end(), (int)i) != pinned.end()) continue;
+        if (slot < 0 || e->vis_stamp[i] < e->vis_stamp[slot]) slot = (int)i;
+      }
+      if (slot < 0) {  // every slot feeds the pending forward
+        flush();
+        slot = 0;
+      }
+      e->vis->encode(vseed, e->vis_buf[slot], ln.stream);
+      e->vis_seed[slot] = vseed;
+      e->vis_encodes++;
+    }
+    e->vis_stamp[slot] = ++e->vis_clock;
+    pinned.push_back(slot);
+    return (uint64_t)(uintptr_t)e->vis_buf[slot];
   };
   for (const auto& sg : segs) {
     int pos = e->seqs[sg.seq].len;
@@ -967,8 +1002,9 @@ void prefill_multi(fe_engine* e, const std::vector<PrefillSeg>& segs, int vis_id
         vk = -1;
       }
       if (vk < 0) {
+        const uint64_t tag = e->vis ? vis_rows(sg.vseed) : sg.vseed;  // (may flush the pending forward)
         vk = (int)vseeds.size();
-        vseeds.push_back(sg.vseed);
+        vseeds.push_back(tag);
       }
       RowIn r{};
       r.seq = sg.seq;
@@ -1575,6 +1611,37 @@ int fe_seq_truncate(fe_engine* e, int32_t seq, int32_t len) {
 
 int fe_prefill(fe_engine* e, int32_t seq, const int32_t* ids, int32_t n, uint64_t vision_seed, int32_t vis_id) {
   return guarded(e, [&] { prefill(e, seq, ids, n, vision_seed, vis_id); });
+}
+
+int fe_vision_enable(fe_engine* e, const fe_vision_config* vc, uint64_t seed, int32_t slots) {
+  return guarded(e, [&] {
+    if (!vc) throw Error("null vision config");
+    if (vc->img % vc->patch || vc->d % vc->heads || (vc->d / vc->heads) > 256 || vc->d % 128 || vc->d > 2048)
+      throw Error("bad vision shape (d a multiple of 128, <= 2048; head_dim <= 256)");
+    fe::VisionDims vd{vc->img, vc->patch, vc->d, vc->layers, vc->heads, vc->mlp, vc->proj_hidden, vc->eps};
+    cudaStream_t st = e->lanes[0].stream;
+    e->vis = std::make_unique<fe::Vision>(vd, e->dtype, e->m.d, seed, st, [&](size_t b) { return e->dalloc(b); });
+    const int P = e->vis->patches_count();
+    const int n = std::max(2, (int)slots);
+    e->vis_buf.assign(n, nullptr);
+    for (int i = 0; i < n; i++) e->vis_buf[i] = (float*)e->dalloc((size_t)P * e->m.d * 4);
+    e->vis_seed.assign(n, 0);
+    e->vis_stamp.assign(n, -1);
+    CK(cudaStreamSynchronize(st));
+  });
+}
+
+int fe_vision_encode(fe_engine* e, uint64_t vision_seed, float* out_host) {
+  return guarded(e, [&] {
+    if (!e->vis) throw Error("vision tower not enabled");
+    Lane& ln = e->lanes[0];
+    float* tmp = (float*)e->dalloc((size_t)e->vis->patches_count() * e->m.d * 4);
+    e->vis->encode(vision_seed, tmp, ln.stream);
+    CK(cudaStreamSynchronize(ln.stream));
+    CK(cudaMemcpy(out_host, tmp, (size_t)e->vis->patches_count() * e->m.d * 4, cudaMemcpyDeviceToHost));
+    e->allocs.pop_back();
+    CK(cudaFree(tmp));
+  });
 }
 
 int fe_prefill_batch(fe_engine* e, int32_t n_seqs, const int32_t* seqs, const int32_t* counts, const int32_t* ids,

@@ -69,6 +69,7 @@ struct Fwd {
   const int32_t* head_rows;  // row index of each lm_head row
   uint64_t vision_key;
   const uint64_t* vision_keys;  // per-row vision keys (RowMeta.pad indexes them), or null: vision_key
+  bool vis_ptrs;                // vision_keys hold device pointers to VIS rows (the vision tower's output)
   // prefill forwards: 64-row query tiles of consecutive positions of one
   // sequence each (several sequences per forward), their page tables; else null
   const PrefillTile* ptiles;

@@ -54,8 +54,13 @@ __global__ void embed_kernel(Fwd f, int d, const WT* embed, const int32_t* out_t
   if (m.vis_row >= 0) {
     const uint64_t base = (uint64_t)m.vis_row * d;
     const uint64_t key = f.vision_keys ? f.vision_keys[m.pad] : f.vision_key;
-    for (int k = threadIdx.x; k < d; k += blockDim.x)
-      xr[k] = __fmul_rn(centered(key, base + k), kVisionMult);
+    if (f.vis_ptrs) {  // the vision tower's rows
+      const float* src = reinterpret_cast<const float*>(key) + base;
+      for (int k = threadIdx.x; k < d; k += blockDim.x) xr[k] = src[k];
+    } else {
+      for (int k = threadIdx.x; k < d; k += blockDim.x)
+        xr[k] = __fmul_rn(centered(key, base + k), kVisionMult);
+    }
   } else {
     const int tok = m.tok >= 0 ? m.tok : out_tokens[m.tok_src];
     const WT* e = embed + (size_t)tok * d;

@@ -26,6 +26,12 @@ PRIO_ACTION, PRIO_REASONING = 0, 1
 _c_int_p = ctypes.POINTER(ctypes.c_int32)
 
 
+class FeVisionConfig(ctypes.Structure):
+    _fields_ = [("img", ctypes.c_int32), ("patch", ctypes.c_int32), ("d", ctypes.c_int32), ("layers", ctypes.c_int32),
+                ("heads", ctypes.c_int32), ("mlp", ctypes.c_int32), ("proj_hidden", ctypes.c_int32),
+                ("eps", ctypes.c_float)]
+
+
 class FeConfig(ctypes.Structure):
     _fields_ = [
         ("d_model", ctypes.c_int32), ("n_layers", ctypes.c_int32), ("n_heads", ctypes.c_int32),
@@ -38,7 +44,7 @@ class FeConfig(ctypes.Structure):
 
 EXPORTS = (
     "fe_engine_create", "fe_engine_destroy", "fe_weights_init_random", "fe_last_error",
-    "fe_seq_create", "fe_seq_fork", "fe_seq_free", "fe_seq_len", "fe_prefill", "fe_prefill_batch", "fe_verify", "fe_seq_truncate",
+    "fe_seq_create", "fe_seq_fork", "fe_seq_free", "fe_seq_len", "fe_prefill", "fe_prefill_batch", "fe_vision_enable", "fe_vision_encode", "fe_verify", "fe_seq_truncate",
     "fe_set_slots",
     "fe_set_slots_lane", "fe_submit_lane", "fe_run_lane", "fe_stream_lane",
     "fe_submit", "fe_run", "fe_request_tokens", "fe_request_release", "fe_request_capture_logits",
@@ -71,6 +77,8 @@ def load_library(path: Path = LIB_PATH) -> ctypes.CDLL:
         "fe_prefill": [vp, i32, vp, i32, u64, i32],
         "fe_verify": [vp, i32, vp, vp, vp, vp],
         "fe_prefill_batch": [vp, i32, vp, vp, vp, vp, i32],
+        "fe_vision_enable": [vp, vp, u64, i32],
+        "fe_vision_encode": [vp, u64, vp],
         "fe_seq_truncate": [vp, i32, i32],
         "fe_set_slots": [vp, i32],
         "fe_set_slots_lane": [vp, i32, i32],
@@ -116,8 +124,12 @@ class Engine:
     """One engine per GPU: weights, paged KV pool, continuous batcher."""
 
     def __init__(self, config: str | ModelConfig = "tiny", dtype: str = "f32", device: int = 0,
-                 seed: int = 0, max_rows: int = 1024, kv_pages: int = 0, max_slots: int = 512):
+                 seed: int = 0, max_rows: int = 1024, kv_pages: int = 0, max_slots: int = 512,
+                 vision=None):
+        """`vision`: None (synthetic VIS embeddings), True (the LLM's default
+        tower, model.DEFAULT_VISION) or a tower preset / VisionConfig."""
         self.cfg = get_config(config)
+        self.vision = None
         self.lib = load_library()
         self.dtype = dtype
         self.max_slots = max_slots
@@ -136,6 +148,8 @@ class Engine:
         self._occ = np.zeros(self._cap, dtype=np.int32)
         self._done = np.zeros(self._cap, dtype=np.int32)
         self._done_tick = np.zeros(self._cap, dtype=np.int32)
+        if vision:
+            self.enable_vision(vision)
 
     # -- plumbing ----------------------------------------------------------
     def _check(self, rc: int) -> None:
@@ -177,6 +191,22 @@ class Engine:
         if a.size:
             self._check(self.lib.fe_prefill(self._h, seq, _np_ptr(a), int(a.size),
                                             ctypes.c_uint64(vision_seed & 0xFFFFFFFFFFFFFFFF), vis_id))
+
+    def enable_vision(self, vision=True, seed: int | None = None, slots: int = 64) -> None:
+        """VIS rows from the vision tower + projector (csrc/vision.cu) instead of
+        the synthetic embeddings; `vision`: preset name, VisionConfig or True."""
+        from .model import get_vision
+        v = get_vision(vision, self.cfg)
+        vc = FeVisionConfig(v.img, v.patch, v.d, v.layers, v.heads, v.mlp, v.proj_hidden, v.eps)
+        self._check(self.lib.fe_vision_enable(self._h, ctypes.byref(vc),
+                                              ctypes.c_uint64(self.seed if seed is None else seed), slots))
+        self.vision = v
+
+    def vision_encode(self, vision_seed: int) -> np.ndarray:
+        out = np.empty((self.vision.patches, self.cfg.d_model), dtype=np.float32)
+        self._check(self.lib.fe_vision_encode(self._h, ctypes.c_uint64(vision_seed & 0xFFFFFFFFFFFFFFFF),
+                                              _np_ptr(out)))
+        return out
 
     def prefill_batch(self, seqs, ids_list, vision_seeds, vis_id: int) -> None:
         """Prefill several sequences in as few forwards as the engine holds

@@ -90,6 +90,49 @@ PRESETS = {
 }
 
 
+@dataclass(frozen=True)
+class VisionConfig:
+    """Vision tower + projector (csrc/vision.cu; oracle `or_vision_encode`):
+    a pre-LayerNorm ViT over an img x img synthetic image, patch `patch`, then
+    a 2-layer GELU projector into the LLM width; img / patch squared must be
+    the LLM's n_vision."""
+    name: str
+    img: int
+    patch: int
+    d: int
+    layers: int
+    heads: int
+    mlp: int
+    proj_hidden: int
+    eps: float = 1e-6
+
+    @property
+    def patches(self) -> int:
+        return (self.img // self.patch) ** 2
+
+
+VISION_PRESETS = {
+    # DINOv2-L/14-shaped tower at 224 px: 256 patches (OpenVLA's VIS count)
+    "vit_l14": VisionConfig("vit_l14", 224, 14, 1024, 24, 16, 4096, 4096),
+    "vit_l14_2layer": VisionConfig("vit_l14_2layer", 224, 14, 1024, 2, 16, 4096, 4096),
+    # small towers for the tiny / small LLMs (16 / 64 patches)
+    "vit_tiny": VisionConfig("vit_tiny", 56, 14, 128, 2, 2, 256, 256),
+    "vit_small": VisionConfig("vit_small", 112, 14, 256, 2, 4, 512, 512),
+}
+DEFAULT_VISION = {"tiny": "vit_tiny", "small": "vit_small", "7b_2layer": "vit_l14_2layer", "7b": "vit_l14"}
+
+
+def get_vision(name_or_cfg, llm) -> VisionConfig:
+    """The tower for an LLM config: a preset name, a VisionConfig, or True
+    (the LLM's default tower)."""
+    llm = get_config(llm)
+    v = VISION_PRESETS[DEFAULT_VISION[llm.name]] if name_or_cfg is True else (
+        name_or_cfg if isinstance(name_or_cfg, VisionConfig) else VISION_PRESETS[name_or_cfg])
+    if v.patches != llm.n_vision:
+        raise ValueError(f"vision tower {v.name} makes {v.patches} rows, {llm.name} frames {llm.n_vision}")
+    return v
+
+
 def get_config(name_or_cfg) -> ModelConfig:
     return name_or_cfg if isinstance(name_or_cfg, ModelConfig) else PRESETS[name_or_cfg]
 

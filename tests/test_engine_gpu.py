@@ -710,3 +710,48 @@ def test_batched_prefill_equals_separate_prefills(config, dtype):
         else:
             assert np.abs(l1[0] - l0[0]).max() / np.abs(l0[0]).max() < 2e-2
             assert t1[0] == t0[0]
+
+
+# ----------------------------------------------------------- vision tower ----
+def test_vision_rows_bit_exact_fp32():
+    """The vision tower + projector (csrc/vision.cu) in fp32 mode: VIS rows
+    bit-identical to the CPU oracle's or_vision_encode."""
+    from oracle.backend import OracleModel
+    eng = Engine("tiny", dtype="f32", seed=0, kv_pages=64, vision="vit_tiny")
+    orc = OracleModel("tiny", seed=0, vision="vit_tiny")
+    try:
+        for vs in (7, 123456789):
+            assert np.array_equal(eng.vision_encode(vs), orc.vision_encode(vs))
+    finally:
+        eng.close()
+
+
+@pytest.mark.parametrize("config", ["small", "7b_2layer"])
+def test_vision_rows_bf16_vs_oracle(config):
+    """bf16 tower (tcgen05 pair-GEMM linears, fp32 LayerNorm / attention): VIS
+    rows within bf16 tolerance of the fp32 oracle (7b_2layer: the 224-px
+    DINOv2-L/14-shaped tower, 256 patches, 2 layers)."""
+    from oracle.backend import OracleModel
+    eng = Engine(config, dtype="bf16", seed=0, kv_pages=64, max_rows=512, vision=True)
+    orc = OracleModel(config, seed=0, vision=True)
+    try:
+        got, want = eng.vision_encode(99), orc.vision_encode(99)
+        rel = np.abs(got - want).max() / np.abs(want).max()
+        assert rel < 3e-2, rel
+    finally:
+        eng.close()
+
+
+@pytest.mark.parametrize("mode", ["sequential", "parallel_sync"])
+def test_vision_traces_byte_identical_to_oracle(schema, mode):
+    """Reference runners over the engine with the vision tower (fp32) vs the
+    same runners over the CPU oracle with the same tower: identical traces."""
+    from oracle.backend import OracleBackend
+    cfg = RS.SchedulerConfig(mode=mode, slots=8)
+    be = EngineBackend("tiny", dtype="f32", seed=0, kv_pages=1024, vision="vit_tiny")
+    try:
+        got, _ = ecot_sched.run_episode(cfg, 3, be, schema, seed=4)
+    finally:
+        be.close()
+    want, _ = ecot_sched.run_episode(cfg, 3, OracleBackend("tiny", seed=0, vision="vit_tiny"), schema, seed=4)
+    assert [trace_content_bytes(r.trace, schema) for r in got] == [trace_content_bytes(r.trace, schema) for r in want]

@@ -123,3 +123,31 @@ def test_reference_runners_over_oracle_reproduce_golden(schema, golden_traces):
         assert [r.latency_ms for r in res] == g["latency_ms"]
         assert [r.staleness for r in res] == g["staleness"]
         assert [r.generated_tokens for r in res] == g["generated_tokens"]
+
+
+def test_vision_oracle_matches_float64_restatement():
+    """oracle/oracle.c's vision tower + projector (canonical fp32) against an
+    independent float64 numpy restatement of the same definition."""
+    from vision_ref import vision_rows
+
+    from oracle.backend import OracleModel
+    m = OracleModel("tiny", seed=3, vision="vit_tiny")
+    for vseed in (1, 987654321):
+        got = m.vision_encode(vseed)
+        want = vision_rows("tiny", "vit_tiny", 3, vseed)
+        assert got.shape == want.shape == (16, 256)
+        rel = np.abs(got - want).max() / np.abs(want).max()
+        assert rel < 1e-4, rel
+
+
+def test_vision_rows_feed_the_oracle_model():
+    """With a tower, the oracle's VIS rows are the tower's output: the greedy
+    continuation changes with the observation's image."""
+    from oracle.backend import OracleModel, frame
+    m = OracleModel("tiny", seed=0, vision="vit_tiny")
+    ids = frame("tiny", list(range(16)), [5, 6, 7], "plan")
+    a, _ = m.generate(ids, 11, 6)
+    b, _ = m.generate(ids, 12, 6)
+    plain = OracleModel("tiny", seed=0)
+    c, _ = plain.generate(ids, 11, 6)
+    assert a != b and a != c
