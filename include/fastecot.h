@@ -90,6 +90,13 @@ int fe_vision_encode(fe_engine* e, uint64_t vision_seed, float* out_host);  /* [
 int fe_prefill_batch(fe_engine* e, int32_t n_seqs, const int32_t* seqs, const int32_t* counts, const int32_t* ids,
                      const uint64_t* vision_seeds, int32_t vis_id);
 
+/* the same, and every sequence with want[i] != 0 runs the lm_head on its
+ * last row (a branch TAG riding along with its trunk prefill): out[i] = the
+ * greedy token after it (synchronous; -1 where want[i] == 0) */
+int fe_prefill_batch_heads(fe_engine* e, int32_t n_seqs, const int32_t* seqs, const int32_t* counts,
+                           const int32_t* ids, const uint64_t* vision_seeds, int32_t vis_id, const int32_t* want,
+                           int32_t* out);
+
 /* reuse-as-draft verification (replaces nothing in the reference: the
  * SyntheticBackend's reuse draw, backends.py:202-204, returns prev_content
  * verbatim; here prev_content is checked as a greedy draft): one batched

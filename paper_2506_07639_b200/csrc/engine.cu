@@ -538,7 +538,7 @@ void launch_layers(fe_engine* e, Lane& ln, const fe::Fwd& f, int n, bool decode,
     if (e->debug_skip & 1) {
     } else if (f.span_mode) {
       fe::launch_span_attention(f, m, e->pool_map, e->pool_map16, ws.q, l, ws.partial, ws.attn, st);
-    } else if (!decode && f.ptiles && dt == FE_BF16 && m.hd == 128 && e->prefill_fa) {
+    } else if (f.ptiles && dt == FE_BF16 && m.hd == 128 && e->prefill_fa) {
       if (e->prefill_tc && e->use_tc) fe::launch_prefill_attention_tc(f, m, e->pool_map, ws.q, l, ws.attn, st);
       else fe::launch_prefill_attention(f, m, ws.q, e->kv_pool, l, ws.attn, st);
     } else {
@@ -568,7 +568,7 @@ void launch_layers(fe_engine* e, Lane& ln, const fe::Fwd& f, int n, bool decode,
     else fe::launch_resid(dt, f, m.d, m.F, ly.wdown, ws.attn, ws.x, st);
     prof_end(e, ln, p, gemv_bytes(m.d, m.F, n));
   }
-  if (decode && !(e->debug_skip & 8)) {
+  if (f.n_head_rows > 0 && !(e->debug_skip & 8)) {
     fe::launch_rmsnorm(dt, ws.x, e->w.final_norm, ws.xn, f.n_head_rows, m.d, m.d, m.eps, f.head_rows, st);
     const int p = prof_begin(e, ln, PROF_GEMV);
     if (e->use_tc && (e->sk_mask >> 4 & 1) && f.n_head_rows <= fe::skinny_max_rows()) {
@@ -588,7 +588,7 @@ void launch_layers(fe_engine* e, Lane& ln, const fe::Fwd& f, int n, bool decode,
 // sequence contiguously, in order).  Builds row metadata and the cascade work
 // list, then launches the layer stack (or replays the lane's decode graph).
 void forward(fe_engine* e, Lane& ln, const std::vector<RowIn>& rows, uint64_t vision_seed,
-             const std::vector<uint64_t>* vseeds = nullptr, bool vis_ptrs = false) {
+             const std::vector<uint64_t>* vseeds = nullptr, bool vis_ptrs = false, bool prefill_rows = false) {
   const fe::ModelDims& m = e->m;
   const int n = (int)rows.size();
   if (n == 0) return;
@@ -685,7 +685,7 @@ void forward(fe_engine* e, Lane& ln, const std::vector<RowIn>& rows, uint64_t vi
   // pages with the same rows, every page but the last full for all of them
   int n_head = 0;
   for (const RowIn& r : rows) n_head += r.head ? 1 : 0;
-  const bool span_mode = n_head > 0 && e->span_attn && e->use_tc && m.hd == 128 &&
+  const bool span_mode = !prefill_rows && n_head > 0 && e->span_attn && e->use_tc && m.hd == 128 &&
                          !(e->mk_on && n <= 16 && n_head == n && e->debug_skip == 0);
   std::vector<fe::AttnItem> items;
   std::vector<fe::ItemRow> irows;
@@ -835,7 +835,7 @@ void forward(fe_engine* e, Lane& ln, const std::vector<RowIn>& rows, uint64_t vi
   // forward in a batched prefill)
   std::vector<fe::PrefillTile> ptiles;
   std::vector<int32_t> ptab;
-  if (head_rows.empty() && !span_mode) {
+  if ((head_rows.empty() || prefill_rows) && !span_mode) {
     for (int i = 0; i < n;) {
       int j = i + 1;
       while (j < n && rows[j].seq == rows[i].seq && rows[j].pos == rows[j - 1].pos + 1) j++;
@@ -892,7 +892,9 @@ void forward(fe_engine* e, Lane& ln, const std::vector<RowIn>& rows, uint64_t vi
   f.span_pages = (const int32_t*)(dbuf + L.o_spages);
   f.span_masks = (const int32_t*)(dbuf + L.o_smasks);
 
-  const bool decode = f.n_head_rows > 0;
+  // a prefill forward may carry lm_head rows (a branch's TAG riding along with
+  // its trunk): it is still a prefill (prefill attention tiles, no graph)
+  const bool decode = f.n_head_rows > 0 && !prefill_rows;
   const double el = (double)e->elem;
   // algorithmic bytes of one GEMV launch: weights + staged input + fp32 output
   auto gemv_bytes = [&](double N, double K, int rws) { return N * K * el + rws * K * el + rws * N * 4.0; };
@@ -944,6 +946,7 @@ struct PrefillSeg {
   const int32_t* ids;
   int n;
   uint64_t vseed;
+  int out_idx = -1;  // >= 0: the last row runs the lm_head, greedy token -> out_tokens[out_idx]
 };
 
 void prefill_multi(fe_engine* e, const std::vector<PrefillSeg>& segs, int vis_id) {
@@ -963,7 +966,7 @@ void prefill_multi(fe_engine* e, const std::vector<PrefillSeg>& segs, int vis_id
   int chunks = 0;
   auto flush = [&]() {
     if (rows.empty()) return;
-    forward(e, ln, rows, 0, &vseeds, e->vis != nullptr);
+    forward(e, ln, rows, 0, &vseeds, e->vis != nullptr, /*prefill_rows=*/true);
     rows.clear();
     vseeds.clear();
     pinned.clear();
@@ -1014,7 +1017,8 @@ void prefill_multi(fe_engine* e, const std::vector<PrefillSeg>& segs, int vis_id
       r.vis_row = sg.ids[i] == vis_id ? pos - 1 : -1;
       r.out_idx = -1;
       r.logit_row = -1;
-      r.head = false;
+      r.head = sg.out_idx >= 0 && i == sg.n - 1;
+      r.out_idx = r.head ? sg.out_idx : -1;
       r.vk = vk;
       rows.push_back(r);
       chunks += c;
@@ -1641,6 +1645,39 @@ int fe_vision_encode(fe_engine* e, uint64_t vision_seed, float* out_host) {
     CK(cudaMemcpy(out_host, tmp, (size_t)e->vis->patches_count() * e->m.d * 4, cudaMemcpyDeviceToHost));
     e->allocs.pop_back();
     CK(cudaFree(tmp));
+  });
+}
+
+int fe_prefill_batch_heads(fe_engine* e, int32_t n_seqs, const int32_t* seqs, const int32_t* counts,
+                           const int32_t* ids, const uint64_t* vision_seeds, int32_t vis_id, const int32_t* want,
+                           int32_t* out) {
+  return guarded(e, [&] {
+    if ((int)e->free_arena.empty()) throw Error("prefill_batch_heads: token arena exhausted");
+    if (n_seqs > kRequestCap) throw Error("prefill_batch_heads: too many sequences");
+    const int slot = e->free_arena.back();
+    e->free_arena.pop_back();
+    try {
+      std::vector<PrefillSeg> segs;
+      size_t off = 0;
+      for (int i = 0; i < n_seqs; i++) {
+        if (counts[i] < 0 || (want[i] && counts[i] < 1)) throw Error("prefill_batch_heads: bad count");
+        if (counts[i]) segs.push_back({seqs[i], ids + off, counts[i], vision_seeds[i],
+                                       want[i] ? slot * kRequestCap + i : -1});
+        off += counts[i];
+      }
+      prefill_multi(e, segs, vis_id);
+      Lane& ln = e->lanes[0];
+      CK(cudaStreamSynchronize(ln.stream));
+      std::vector<int32_t> tok(n_seqs);
+      CK(cudaMemcpy(tok.data(), e->out_tokens + (size_t)slot * kRequestCap, sizeof(int32_t) * n_seqs,
+                    cudaMemcpyDeviceToHost));
+      for (int i = 0; i < n_seqs; i++) out[i] = want[i] ? tok[i] : -1;
+      e->d2h_bytes += (int64_t)sizeof(int32_t) * n_seqs;
+    } catch (...) {
+      e->free_arena.push_back(slot);
+      throw;
+    }
+    e->free_arena.push_back(slot);
   });
 }
 

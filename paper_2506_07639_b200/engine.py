@@ -44,7 +44,7 @@ class FeConfig(ctypes.Structure):
 
 EXPORTS = (
     "fe_engine_create", "fe_engine_destroy", "fe_weights_init_random", "fe_last_error",
-    "fe_seq_create", "fe_seq_fork", "fe_seq_free", "fe_seq_len", "fe_prefill", "fe_prefill_batch", "fe_vision_enable", "fe_vision_encode", "fe_verify", "fe_seq_truncate",
+    "fe_seq_create", "fe_seq_fork", "fe_seq_free", "fe_seq_len", "fe_prefill", "fe_prefill_batch", "fe_prefill_batch_heads", "fe_vision_enable", "fe_vision_encode", "fe_verify", "fe_seq_truncate",
     "fe_set_slots",
     "fe_set_slots_lane", "fe_submit_lane", "fe_run_lane", "fe_stream_lane",
     "fe_submit", "fe_run", "fe_request_tokens", "fe_request_release", "fe_request_capture_logits",
@@ -77,6 +77,7 @@ def load_library(path: Path = LIB_PATH) -> ctypes.CDLL:
         "fe_prefill": [vp, i32, vp, i32, u64, i32],
         "fe_verify": [vp, i32, vp, vp, vp, vp],
         "fe_prefill_batch": [vp, i32, vp, vp, vp, vp, i32],
+        "fe_prefill_batch_heads": [vp, i32, vp, vp, vp, vp, i32, vp, vp],
         "fe_vision_enable": [vp, vp, u64, i32],
         "fe_vision_encode": [vp, u64, vp],
         "fe_seq_truncate": [vp, i32, i32],
@@ -208,17 +209,27 @@ class Engine:
                                               _np_ptr(out)))
         return out
 
-    def prefill_batch(self, seqs, ids_list, vision_seeds, vis_id: int) -> None:
+    def prefill_batch(self, seqs, ids_list, vision_seeds, vis_id: int, want=None):
         """Prefill several sequences in as few forwards as the engine holds
-        (rows of all of them packed; one GEMM pass per forward)."""
+        (rows of all of them packed; one GEMM pass per forward).  `want`: per
+        sequence, run the lm_head on its last row and return the greedy token
+        after it (list, -1 where not wanted); else None."""
         counts = np.asarray([len(x) for x in ids_list], dtype=np.int32)
-        if counts.sum() == 0:
-            return
-        flat = np.ascontiguousarray(np.concatenate([np.asarray(x, dtype=np.int32) for x in ids_list]))
+        if counts.sum() == 0 and not want:
+            return None
+        flat = np.ascontiguousarray(np.concatenate([np.asarray(x, dtype=np.int32) for x in ids_list]
+                                                   + [np.zeros(0, np.int32)]))
         sq = np.ascontiguousarray(np.asarray(seqs, dtype=np.int32))
         vs = np.ascontiguousarray(np.asarray([v & 0xFFFFFFFFFFFFFFFF for v in vision_seeds], dtype=np.uint64))
-        self._check(self.lib.fe_prefill_batch(self._h, int(sq.size), _np_ptr(sq), _np_ptr(counts), _np_ptr(flat),
-                                              _np_ptr(vs), vis_id))
+        if want is None:
+            self._check(self.lib.fe_prefill_batch(self._h, int(sq.size), _np_ptr(sq), _np_ptr(counts),
+                                                  _np_ptr(flat), _np_ptr(vs), vis_id))
+            return None
+        w = np.ascontiguousarray(np.asarray([1 if x else 0 for x in want], dtype=np.int32))
+        out = np.empty(sq.size, dtype=np.int32)
+        self._check(self.lib.fe_prefill_batch_heads(self._h, int(sq.size), _np_ptr(sq), _np_ptr(counts),
+                                                    _np_ptr(flat), _np_ptr(vs), vis_id, _np_ptr(w), _np_ptr(out)))
+        return out.tolist()
 
     def verify(self, seqs, inputs) -> list[np.ndarray]:
         """Reuse-as-draft verification: extend every `seqs[i]` by `inputs[i]`

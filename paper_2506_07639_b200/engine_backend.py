@@ -167,7 +167,7 @@ class EngineBackend:
                  profile: SyntheticProfile | None = None, device: int = 0,
                  engine: Engine | None = None, trunk_cache: int = 64, async_mode: str = "lockstep",
                  request_log: list | None = None, draft_reuse: bool = False, background_depth: int = 1,
-                 **engine_kw):
+                 tag_in_prefill: bool | None = None, **engine_kw):
         """`async_mode="lockstep"`: the async runner's device engine advances
         exactly as many decode iterations as each control step's action needs
         (the reference landing order, byte-comparable traces);
@@ -205,6 +205,13 @@ class EngineBackend:
         self.requests = 0
         self.draft_reuse = draft_reuse
         self.background_depth = background_depth   # decode ticks the background ticker keeps queued
+        # the request owning a new trunk (the longest: an async action) gets its
+        # first token from the trunk prefill itself -- its TAG row rides along
+        # with the trunk rows -- saving one decode tick; exact greedy (same
+        # token), but it moves completions one tick earlier, so the lockstep
+        # mode (the reference landing order) keeps it off
+        self.tag_in_prefill = (async_mode == "background") if tag_in_prefill is None else tag_in_prefill
+        self.tag_in_prefill &= getattr(self.engine, "supports_prefill_heads", True)
         self.draft_stats = {"requests": 0, "drafted": 0, "draft_tokens": 0, "accepted_tokens": 0,
                             "verified_tokens": 0, "resolved_by_verify": 0, "verify_forwards": 0,
                             "verify_rows": 0}
@@ -427,9 +434,9 @@ class EngineBackend:
             return
         todo.sort(key=lambda h: -h.ids.size)
         eng = self.engine
-        planned: list[tuple[_Trunk, int]] = []   # new trunk, prefilled from position lcp
+        planned: list[tuple[_Trunk, int, DeviceRequest]] = []   # new trunk, prefilled from lcp, its owner
         for h in todo:
-            if self._covering(h.vseed, h.ids, [t for t, _ in planned]) is not None:
+            if self._covering(h.vseed, h.ids, [t for t, _, _ in planned]) is not None:
                 continue
             best, lcp = self._best_trunk(h.vseed, h.ids)
             try:
@@ -439,20 +446,28 @@ class EngineBackend:
                 self._release(h)
                 continue
             self._clock += 1
-            planned.append((_Trunk(h.vseed, h.ids.copy(), seq, self._clock), lcp))
+            planned.append((_Trunk(h.vseed, h.ids.copy(), seq, self._clock), lcp, h))
+        first: dict[int, int] = {}   # id(owner) -> its first token, computed by the trunk prefill
         if planned:
+            want = [self.tag_in_prefill and not h.draft and not h.prefix and h.length >= 2 for _, _, h in planned]
+            ids_list = [np.concatenate([t.ids[lcp:], np.asarray([h.tag] if w else [], np.int32)])
+                        for (t, lcp, h), w in zip(planned, want)]
             try:
-                eng.prefill_batch([t.seq for t, _ in planned], [t.ids[lcp:] for t, lcp in planned],
-                                  [t.vseed for t, _ in planned], VIS_ID)
+                toks = eng.prefill_batch([t.seq for t, _, _ in planned], ids_list,
+                                         [t.vseed for t, _, _ in planned], VIS_ID, want=want if any(want) else None)
             except EngineError as exc:
-                for t, _ in planned:
+                for t, _, _ in planned:
                     eng.seq_free(t.seq)
                 for h in todo:
                     if h.error is None and self._covering(h.vseed, h.ids, []) is None:
                         h.error = exc
                         self._release(h)
-                planned = []
-            self._trunks.extend(t for t, _ in planned)
+                planned, toks = [], None
+            if toks is not None:
+                for (t, _, h), w, tok in zip(planned, want, toks):
+                    if w:
+                        first[id(h)] = int(tok)
+            self._trunks.extend(t for t, _, _ in planned)
         for h in todo:
             if h.error is not None:
                 continue
@@ -461,7 +476,11 @@ class EngineBackend:
                 if tr is None:
                     raise EngineError(f"no trunk covers request {h.name!r}")
                 tr.stamp = self._clock
-                h.branch = eng.seq_fork(tr.seq, h.ids.size)
+                if id(h) in first:   # its TAG row is in the trunk: fork past it, decode from token 1
+                    h.branch = eng.seq_fork(tr.seq, h.ids.size + 1)
+                    h.prefix = (first[id(h)],)
+                else:
+                    h.branch = eng.seq_fork(tr.seq, h.ids.size)
             except EngineError as exc:
                 h.error = exc
                 self._release(h)

@@ -132,12 +132,22 @@ class FakeEngine:
                 raise B.EngineError("truncate beyond the sequence")
             self.seqs[seq] = (vseed, ids[:n])
 
-    def prefill_batch(self, seqs, ids_list, vision_seeds, vis_id: int) -> None:
+    def prefill_batch(self, seqs, ids_list, vision_seeds, vis_id: int, want=None):
         with self.lock:
             self.prefill_batch_calls = getattr(self, "prefill_batch_calls", 0) + 1
-        for s, ids, v in zip(seqs, ids_list, vision_seeds):
+        out = []
+        for i, (s, ids, v) in enumerate(zip(seqs, ids_list, vision_seeds)):
             if len(ids):
                 self.prefill(s, ids, v, vis_id)
+            if want is not None:   # greedy token after the last id (autoregressive mode only)
+                if want[i] and not self.autoregressive:
+                    raise B.EngineError("prefill heads need the autoregressive fake engine")
+                out.append(ar_token(self.seqs[s][0], self.seqs[s][1]) if want[i] else -1)
+        return out if want is not None else None
+
+    @property
+    def supports_prefill_heads(self) -> bool:
+        return self.autoregressive
 
     # batcher
     def set_slots(self, n: int) -> None:

@@ -755,3 +755,17 @@ def test_vision_traces_byte_identical_to_oracle(schema, mode):
         be.close()
     want, _ = ecot_sched.run_episode(cfg, 3, OracleBackend("tiny", seed=0, vision="vit_tiny"), schema, seed=4)
     assert [trace_content_bytes(r.trace, schema) for r in got] == [trace_content_bytes(r.trace, schema) for r in want]
+
+
+@pytest.mark.parametrize("mode", ["sequential", "parallel_sync"])
+def test_tag_in_prefill_reproduces_reference_golden(schema, golden_traces, mode):
+    """fe_prefill_batch_heads: the trunk owner's TAG row runs with its trunk
+    prefill and returns its first token (fp32: the same bits as a decode
+    tick) -- the golden traces are unchanged."""
+    g = golden_traces["modes"][mode]
+    be = EngineBackend("tiny", dtype="f32", seed=0, kv_pages=1024, tag_in_prefill=True)
+    try:
+        res, _ = ecot_sched.run_episode(RS.SchedulerConfig(mode=mode, slots=8), golden_traces["T"], be, schema, seed=0)
+        assert [trace_content_bytes(r.trace, schema).decode() for r in res] == g["lines"]
+    finally:
+        be.close()

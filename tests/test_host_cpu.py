@@ -377,3 +377,17 @@ def test_reference_experiment_harness_runs_on_the_engine(tmp_path):
         b = [line.split(b'"wall_ms"')[0] for line in other.read_bytes().splitlines()]
         assert a == b, cell
     assert ecot_sched.experiments._make_backend.__module__ == "ecot_sched.experiments"
+
+
+@pytest.mark.parametrize("mode", ("sequential", "parallel_sync"))
+def test_tag_in_prefill_is_exactly_greedy(mode):
+    """The trunk owner's first token computed by the trunk prefill (its TAG row
+    riding along) instead of a decode tick: identical traces, fewer ticks."""
+    schema = default_schema()
+    runs = {}
+    for tag in (False, True):
+        be, eng = fake_backend(autoregressive=True, tag_in_prefill=tag)
+        res, _ = episode(mode, be, schema, 5, seed=2)
+        runs[tag] = (lines(res, schema), len(eng.occupancy_log))
+    assert runs[True][0] == runs[False][0]
+    assert runs[True][1] < runs[False][1]
