@@ -215,6 +215,12 @@ struct fe_engine {
   // GEMM (option "sk_max_rows"; measured in the engine at 7B: skinny ahead
   // up to ~32 rows, the tile GEMM at 56 and for prefill)
   int sk_max_rows = 32;
+  // per matrix (QKV, O, gate/up, down; options "sk_rows_*"): rows up to which
+  // the skinny swap-AB GEMM is used instead of the CTA-pair GEMM.  The
+  // isolated sweeps favour skinny QKV up to 128 rows and gate/up up to 64,
+  // but inside config-4 ticks that measured 795 vs 765 ms of decode GEMMs per
+  // step, so every matrix switches at 32
+  int sk_rows[4] = {32, 32, 32, 32};
   int sk_mask = 31;  // skinny path per matrix: 1 QKV, 2 O, 4 gate/up, 8 down, 16 lm_head
   std::vector<LayerMaps> tc_maps;
   fe::TmaMap map_lm{};
@@ -487,9 +493,11 @@ void launch_layers(fe_engine* e, Lane& ln, const fe::Fwd& f, int n, bool decode,
   // bf16: the persistent swap-AB tcgen05 GEMM (decode batches of any width
   // and, up to `sk_max_rows`, prefill), else the tile tcgen05 GEMM; fp32: the
   // canonical CUDA-core GEMV
-  const bool sk_any = e->use_tc && n <= std::min(e->sk_max_rows, fe::skinny_max_rows());
-  const bool tc = e->use_tc && !sk_any && n >= e->tc_min_rows;
-  auto sk_on = [&](int bit) { return sk_any && (e->sk_mask >> bit & 1); };
+  const int sk_cap = std::min(e->sk_max_rows, fe::skinny_max_rows());
+  auto sk_on = [&](int bit) {
+    return e->use_tc && n <= std::min(sk_cap, e->sk_rows[bit]) && (e->sk_mask >> bit & 1);
+  };
+  auto tc_on = [&](int bit) { return e->use_tc && !sk_on(bit) && n >= e->tc_min_rows; };
   auto tc_launch = [&](int epi, int N, int K) {
     fe::TcLaunch t{};
     t.M = n; t.N = N; t.K = K; t.epi = epi;
@@ -525,7 +533,7 @@ void launch_layers(fe_engine* e, Lane& ln, const fe::Fwd& f, int n, bool decode,
       fe::SkLaunch t = sk_launch(fe::TC_QKV, 3 * m.d, m.d);
       t.layer_off = layer_off;
       fe::launch_skinny_tc(mp.qkv, ln.map_xn16, t, st);
-    } else if (tc) {
+    } else if (tc_on(0)) {
       fe::TcLaunch t = tc_launch(fe::TC_QKV, 3 * m.d, m.d);
       t.layer_off = layer_off;
       if (e->tc_pair) fe::launch_gemm_tc(ln.map_xn, mp.qkv64, t, st);
@@ -548,23 +556,23 @@ void launch_layers(fe_engine* e, Lane& ln, const fe::Fwd& f, int n, bool decode,
     p = decode ? prof_begin(e, ln, PROF_GEMV) : -1;
     if (skip_gemm) {
     } else if (sk_on(1)) fe::launch_skinny_tc(mp.wo, ln.map_attn16, sk_launch(fe::TC_RESID, m.d, m.d), st);
-    else if (tc && e->tc_pair) fe::launch_gemm_tc(ln.map_attn, mp.wo64, tc_launch(fe::TC_RESID, m.d, m.d), st);
-    else if (tc) fe::launch_gemm_tc_v1(ln.map_attn, mp.wo, tc_launch(fe::TC_RESID, m.d, m.d), st);
+    else if (tc_on(1) && e->tc_pair) fe::launch_gemm_tc(ln.map_attn, mp.wo64, tc_launch(fe::TC_RESID, m.d, m.d), st);
+    else if (tc_on(1)) fe::launch_gemm_tc_v1(ln.map_attn, mp.wo, tc_launch(fe::TC_RESID, m.d, m.d), st);
     else fe::launch_resid(dt, f, m.d, m.d, ly.wo, ws.attn, ws.x, st);
     prof_end(e, ln, p, gemv_bytes(m.d, m.d, n));
     if (!skip_norm) fe::launch_rmsnorm(dt, ws.x, ly.ffn_norm, ws.xn, n, m.d, m.d, m.eps, nullptr, st);
     p = decode ? prof_begin(e, ln, PROF_GEMV) : -1;
     if (skip_gemm) {
     } else if (sk_on(2)) fe::launch_skinny_tc(mp.wgu, ln.map_xn16, sk_launch(fe::TC_SWIGLU, 2 * m.F, m.d), st);
-    else if (tc && e->tc_pair) fe::launch_gemm_tc(ln.map_xn, mp.wgu, tc_launch(fe::TC_SWIGLU, 2 * m.F, m.d), st);
-    else if (tc) fe::launch_gemm_tc_v1(ln.map_xn, mp.wgu, tc_launch(fe::TC_SWIGLU, 2 * m.F, m.d), st);
+    else if (tc_on(2) && e->tc_pair) fe::launch_gemm_tc(ln.map_xn, mp.wgu, tc_launch(fe::TC_SWIGLU, 2 * m.F, m.d), st);
+    else if (tc_on(2)) fe::launch_gemm_tc_v1(ln.map_xn, mp.wgu, tc_launch(fe::TC_SWIGLU, 2 * m.F, m.d), st);
     else fe::launch_swiglu(dt, f, m.F, m.d, ly.wgu, ws.xn, ws.attn /* reused as the SwiGLU activation */, st);
     prof_end(e, ln, p, gemv_bytes(2.0 * m.F, m.d, n));
     p = decode ? prof_begin(e, ln, PROF_GEMV) : -1;
     if (skip_gemm) {
     } else if (sk_on(3)) fe::launch_skinny_tc(mp.wdown, ln.map_act16, sk_launch(fe::TC_RESID, m.d, m.F), st);
-    else if (tc && e->tc_pair) fe::launch_gemm_tc(ln.map_act, mp.wdown64, tc_launch(fe::TC_RESID, m.d, m.F), st);
-    else if (tc) fe::launch_gemm_tc_v1(ln.map_act, mp.wdown, tc_launch(fe::TC_RESID, m.d, m.F), st);
+    else if (tc_on(3) && e->tc_pair) fe::launch_gemm_tc(ln.map_act, mp.wdown64, tc_launch(fe::TC_RESID, m.d, m.F), st);
+    else if (tc_on(3)) fe::launch_gemm_tc_v1(ln.map_act, mp.wdown, tc_launch(fe::TC_RESID, m.d, m.F), st);
     else fe::launch_resid(dt, f, m.d, m.F, ly.wdown, ws.attn, ws.x, st);
     prof_end(e, ln, p, gemv_bytes(m.d, m.F, n));
   }
@@ -1938,6 +1946,9 @@ int fe_set_option(fe_engine* e, const char* key, int64_t value) {
       clear_graphs(e);
     } else if (k == "sk_splits") {
       fe::g_sk_splits = (int)value;
+      clear_graphs(e);
+    } else if (k == "sk_rows_qkv" || k == "sk_rows_o" || k == "sk_rows_gu" || k == "sk_rows_down") {
+      e->sk_rows[k == "sk_rows_qkv" ? 0 : k == "sk_rows_o" ? 1 : k == "sk_rows_gu" ? 2 : 3] = (int)value;
       clear_graphs(e);
     } else if (k == "sk_max_rows") {
       e->sk_max_rows = (int)value;
