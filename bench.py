@@ -523,7 +523,16 @@ def main():
         "clocks": r["clocks"],
         "breakdown_ms_per_step_eager": {k: v["ms"] / steps_prof for k, v in prof.items()},
         "breakdown_gbs_eager": {k: (v["bytes"] / 1e9) / (v["ms"] / 1e3) for k, v in prof.items()
-                                if v["ms"] > 0 and v["bytes"] > 0},
+                                if v["ms"] > 0 and v["bytes"] > 0 and k != "prefill_forward"},
+        # trunk prefill (tensor-bound): algorithmic FLOPs over the prefill forwards' event time
+        "prefill_roofline": ({"bound": "tensor", "achieved": prof["prefill_forward"]["bytes"] / 1e12
+                              / (prof["prefill_forward"]["ms"] / 1e3),
+                              "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                              "frac": prof["prefill_forward"]["bytes"] / 1e12 / (prof["prefill_forward"]["ms"] / 1e3)
+                              / peaks["bf16_tflops"],
+                              "tflop_per_step": prof["prefill_forward"]["bytes"] / 1e12 / steps_prof,
+                              "peak_source": peaks["source"] + " (sustained cuBLAS bf16)"}
+                             if prof["prefill_forward"]["ms"] > 0 else None),
         "decode_ticks_per_step": (s1["ticks"] - s0["ticks"]) / K,
         "results_gathered": token_summary(r["shards"]),
         "bf16_token_match": parity.get("summary") if parity else None,

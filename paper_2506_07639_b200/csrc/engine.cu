@@ -444,7 +444,8 @@ bool mk_eligible(fe_engine* e, const Lane& ln, const fe::Fwd& f, int n) {
 
 // The kernel sequence of one forward pass (eager or under graph capture).
 template <typename GB>
-void launch_layers(fe_engine* e, Lane& ln, const fe::Fwd& f, int n, bool decode, double kv_bytes, GB gemv_bytes) {
+void launch_layers(fe_engine* e, Lane& ln, const fe::Fwd& f, int n, bool decode, double kv_bytes, GB gemv_bytes,
+                   double flops = 0.0) {
   const fe::ModelDims& m = e->m;
   cudaStream_t st = ln.stream;
   const int dt = e->dtype;
@@ -589,7 +590,7 @@ void launch_layers(fe_engine* e, Lane& ln, const fe::Fwd& f, int n, bool decode,
     }
     prof_end(e, ln, p, gemv_bytes(m.V, m.d, f.n_head_rows));
   }
-  prof_end(e, ln, whole, 0.0);
+  prof_end(e, ln, whole, decode ? 0.0 : flops);  // prefill: algorithmic FLOPs (the profile's "bytes" slot)
 }
 
 // One forward pass over `rows` on a lane (positions must extend each
@@ -903,6 +904,14 @@ void forward(fe_engine* e, Lane& ln, const std::vector<RowIn>& rows, uint64_t vi
   // a prefill forward may carry lm_head rows (a branch's TAG riding along with
   // its trunk): it is still a prefill (prefill attention tiles, no graph)
   const bool decode = f.n_head_rows > 0 && !prefill_rows;
+  // algorithmic FLOPs of the forward (prefill roofline): every row through
+  // every linear, causal attention over its own prefix, lm_head rows
+  double fwd_flops = 0.0;
+  {
+    const double lin = (double)m.L * (4.0 * m.d * m.d + 3.0 * m.d * m.F);
+    fwd_flops = 2.0 * n * lin + 2.0 * f.n_head_rows * (double)m.V * m.d;
+    for (const RowIn& r : rows) fwd_flops += 4.0 * (r.pos + 1) * (double)m.d * m.L;
+  }
   const double el = (double)e->elem;
   // algorithmic bytes of one GEMV launch: weights + staged input + fp32 output
   auto gemv_bytes = [&](double N, double K, int rws) { return N * K * el + rws * K * el + rws * N * 4.0; };
@@ -925,14 +934,14 @@ void forward(fe_engine* e, Lane& ln, const std::vector<RowIn>& rows, uint64_t vi
   } else if (graphable && it_g != ln.graphs.end() && it_g->second.seen) {
     cudaGraph_t g = nullptr;
     CK(cudaStreamBeginCapture(ln.stream, cudaStreamCaptureModeThreadLocal));
-    launch_layers(e, ln, f, n, decode, kv_bytes, gemv_bytes);
+    launch_layers(e, ln, f, n, decode, kv_bytes, gemv_bytes, fwd_flops);
     CK(cudaStreamEndCapture(ln.stream, &g));
     CK(cudaGraphInstantiate(&it_g->second.exec, g, 0));
     CK(cudaGraphDestroy(g));
     CK(cudaGraphLaunch(it_g->second.exec, ln.stream));
   } else {
     if (graphable) ln.graphs[key].seen = true;
-    launch_layers(e, ln, f, n, decode, kv_bytes, gemv_bytes);
+    launch_layers(e, ln, f, n, decode, kv_bytes, gemv_bytes, fwd_flops);
   }
   CK(cudaGetLastError());
   if (mk_tick) {
