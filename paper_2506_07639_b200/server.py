@@ -186,27 +186,36 @@ class CompletionServer:
                     break
             self.stats["batches"] += 1
             self.stats["max_batch"] = max(self.stats["max_batch"], len(batch))
-            gens = []
-            for job in batch:   # prepare all (deferred): they decode as one batch
-                try:
-                    ctx = encode_context(job.instruction, job.observation)
-                    gens.append((job, be.begin_completion(ctx, job.prefix, job.step, job.max_tokens)))
-                except BackendError as exc:
-                    self.stats["errors"] += 1
-                    job.finish(503, {"error": str(exc)})
-            for job, gen in gens:
-                try:
-                    toks = tuple(gen.tokens)
-                except BackendError as exc:
-                    self.stats["errors"] += 1
-                    job.finish(503, {"error": str(exc)})
-                    continue
-                self.stats["requests"] += 1
-                self.stats["tokens"] += len(toks)
-                job.finish(200, {"object": "text_completion",
-                                 "choices": [{"index": 0, "text": " ".join(str(t) for t in toks),
-                                              "finish_reason": "length"}],
-                                 "usage": {"completion_tokens": len(toks)}})
+            try:
+                self._serve_batch(be, batch)
+            except Exception as exc:  # never leave a client waiting on a dead worker
+                self.stats["errors"] += 1
+                for job in batch:
+                    if not job.done.is_set():
+                        job.finish(500, {"error": f"internal error: {exc!r}"})
+
+    def _serve_batch(self, be, batch) -> None:
+        gens = []
+        for job in batch:   # prepare all (deferred): they decode as one batch
+            try:
+                ctx = encode_context(job.instruction, job.observation)
+                gens.append((job, be.begin_completion(ctx, job.prefix, job.step, job.max_tokens)))
+            except BackendError as exc:
+                self.stats["errors"] += 1
+                job.finish(503, {"error": str(exc)})
+        for job, gen in gens:
+            try:
+                toks = tuple(gen.tokens)
+            except BackendError as exc:
+                self.stats["errors"] += 1
+                job.finish(503, {"error": str(exc)})
+                continue
+            self.stats["requests"] += 1
+            self.stats["tokens"] += len(toks)
+            job.finish(200, {"object": "text_completion",
+                             "choices": [{"index": 0, "text": " ".join(str(t) for t in toks),
+                                          "finish_reason": "length"}],
+                             "usage": {"completion_tokens": len(toks)}})
 
     # -- lifetime -----------------------------------------------------------------
     @property
