@@ -117,7 +117,6 @@ struct Args {
   int flags;                  // diagnostics (engine option "mk_flags")
   int fused;                  // bit MK_*: GEMM finalised in-phase (option "mk_fused")
   int pf_stages;              // weight stages prefetched ahead of a phase's grid barrier (<= kStages)
-  int gu_pf;                  // per-mille of the gate/up weights pulled into L2 during the QKV reduction
   int* grab;                  // [P] chunk counters of the GEMM phases (reset by the last CTA to exit)
   unsigned long long* trace;  // diagnostics: [P][6][G] globaltimer: barrier pass, phase done, last weight load issued,
                              // first / last accumulator ready, segments drained
@@ -1080,16 +1079,6 @@ __device__ __noinline__ void role_producer(const Args& a, unsigned char* smem, c
             const int boxes = p.tiles * p.kb_total;
             for (int b = blockIdx.x; b < boxes; b += G) tma_prefetch_l2(wm, (b % p.kb_total) * KBK, (b / p.kb_total) * MT);
           }
-          if (a.gu_pf > 0) {  // and the first gate/up tiles (grabbed first: tile-major chunks)
-            const MkPlan pg = a.plan[MK_GU];
-            const CUtensorMap* gm = wmap_of(a, MK_GU, l);
-            const int nb = (int)((long long)pg.tiles * pg.kb_total * a.gu_pf / 1000);
-            for (int b = blockIdx.x; b < nb; b += G) {
-              const int tl = b / pg.kb_total, kb = b % pg.kb_total;
-              tma_prefetch_l2(gm, kb * KBK, tl * (MT / 2));
-              tma_prefetch_l2(gm, kb * KBK, a.F + tl * (MT / 2));
-            }
-          }
         }
         if (kind == K_O) wait_ready(ready_ph + 1, ph - 1);
         if (MK_TRACE && (a.flags & 1)) wait_ready(ready_ph, ph);  // diagnostics: no weight prefetch across barriers
@@ -1404,7 +1393,6 @@ void launch_impl(const MkLaunch& l, cudaStream_t s) {
   a.flags = l.flags;
   a.fused = l.fused | (1 << MK_LM);  // lm_head always finalises in-phase (FINAL follows)
   a.pf_stages = std::max(1, std::min(kStages, l.pf_stages > 0 ? l.pf_stages : kStages));
-  a.gu_pf = std::max(0, std::min(1000, l.gu_pf));
   // cooperative launch: the grid barriers need every CTA resident, which the
   // runtime then guarantees (or rejects the launch) instead of a spin timeout
   cudaLaunchConfig_t cfg{};

@@ -58,7 +58,6 @@ struct MkLaunch {
   int flags;                     // diagnostics: 1 = no weight prefetch across grid barriers
   int fused;                     // bit MK_*: that GEMM's tiles are finalised inside its phase
   int pf_stages;                 // weight stages prefetched ahead of a grid barrier (0 = whole ring)
-  int gu_pf;                     // per-mille of gate/up weights pulled into L2 during the QKV reduction
   unsigned long long* trace;     // diagnostics (null): [phases][2][grid] globaltimer at barrier pass / phase end
 };
 

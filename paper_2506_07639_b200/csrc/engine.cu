@@ -238,7 +238,6 @@ struct fe_engine {
   cudaEvent_t mk_ev[kLanes] = {};  // last persistent tick of each lane
   bool mk_ev_used[kLanes] = {};
   int mk_pf_stages = 0;  // 0 = the whole ring
-  int mk_gu_pf = 0;      // option "mk_gu_pf": per-mille of gate/up weights L2-prefetched in the QKV reduction
   int mk_per_cta = 4, mk_nc_cap = 8, mk_nc_cap_o = 0;  // chunk plans (mk_make_plans; swept in tools/mk_sweep.sh)
   bool graphs_on = true;
   bool lane1_yields = true;
@@ -477,7 +476,6 @@ void launch_layers(fe_engine* e, Lane& ln, const fe::Fwd& f, int n, bool decode,
     k.flags = e->mk_flags;
     k.fused = e->mk_fused;
     k.pf_stages = e->mk_pf_stages;
-    k.gu_pf = e->mk_gu_pf;
     const int p = prof_begin(e, ln, PROF_TICK);
     fe::launch_decode_mk(k, st);
     // algorithmic bytes of the tick: every weight once, the K/V pages the
@@ -1979,9 +1977,6 @@ int fe_set_option(fe_engine* e, const char* key, int64_t value) {
       clear_graphs(e);
     } else if (k == "mk_flags") {
       e->mk_flags = (int)value;
-      clear_graphs(e);
-    } else if (k == "mk_gu_pf") {
-      e->mk_gu_pf = (int)value;
       clear_graphs(e);
     } else if (k == "mk_pf") {
       e->mk_pf_stages = (int)value;
