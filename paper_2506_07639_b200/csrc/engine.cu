@@ -233,6 +233,7 @@ struct fe_engine {
   unsigned long long* mk_trace = nullptr;  // diagnostics: per-phase barrier timestamps of the last tick
   size_t mk_trace_n = 0;
   bool mk_trace_on = false;
+  bool pattn_trace_on = false;  // diagnostics: prefill attention stamps into mk_trace (option "pattn_trace")
   int mk_flags = 0;
   int mk_fused = (1 << fe::MK_GU) | (1 << fe::MK_LM);  // option "mk_fused"
   cudaEvent_t mk_ev[kLanes] = {};  // last persistent tick of each lane
@@ -546,7 +547,8 @@ void launch_layers(fe_engine* e, Lane& ln, const fe::Fwd& f, int n, bool decode,
     } else if (f.span_mode) {
       fe::launch_span_attention(f, m, e->pool_map, e->pool_map16, ws.q, l, ws.partial, ws.attn, st);
     } else if (f.ptiles && dt == FE_BF16 && m.hd == 128 && e->prefill_fa) {
-      if (e->prefill_tc && e->use_tc) fe::launch_prefill_attention_tc(f, m, e->pool_map, ws.q, l, ws.attn, st);
+      if (e->prefill_tc && e->use_tc) fe::launch_prefill_attention_tc(f, m, e->pool_map, ws.q, l, ws.attn, st,
+                                                                        e->pattn_trace_on ? e->mk_trace : nullptr);
       else fe::launch_prefill_attention(f, m, ws.q, e->kv_pool, l, ws.attn, st);
     } else {
       fe::launch_attention(dt, f, m, ws.q, e->kv_pool, l, ws.partial, ws.attn, st);
@@ -1971,6 +1973,14 @@ int fe_set_option(fe_engine* e, const char* key, int64_t value) {
         CK(cudaMemset(e->mk_trace, 0, e->mk_trace_n * 8));
       }
       e->mk_trace_on = value != 0 && e->mk_trace != nullptr;
+      clear_graphs(e);
+    } else if (k == "pattn_trace") {
+      if (value && !e->mk_trace) {
+        e->mk_trace_n = 1 << 14;
+        e->mk_trace = (unsigned long long*)e->dalloc(e->mk_trace_n * 8);
+        CK(cudaMemset(e->mk_trace, 0, e->mk_trace_n * 8));
+      }
+      e->pattn_trace_on = value != 0 && e->mk_trace != nullptr;
       clear_graphs(e);
     } else if (k == "mk_fused") {
       e->mk_fused = (int)value;

@@ -153,7 +153,8 @@ struct TmaMap;
 extern int g_span_dbg;
 // bf16, head_dim 128, f.ptiles of <= 128 rows (prefill_attn_tc.cu: tcgen05 + TMEM + TMA)
 void launch_prefill_attention_tc(const Fwd& f, const ModelDims& m, const TmaMap& pool_map, const float* q, int layer,
-                                 void* attn_out, cudaStream_t s);
+                                 void* attn_out, cudaStream_t s,
+                                 unsigned long long* trace = nullptr);
 void launch_span_attention(const Fwd& f, const ModelDims& m, const TmaMap& pool_map, const TmaMap& pool_map16,
                            const float* q, int layer, float* partial, void* attn_out, cudaStream_t s);
 void launch_resid(int dtype, const Fwd& f, int N, int K, const void* w, const void* xin, float* x,

@@ -19,7 +19,8 @@
 //     when a row's new scores exceed it by more than 2^8, so the usual page
 //     needs no O traffic at all; exp2 of scores against the stale max stays
 //     <= 256 and the final O / l is exact.
-//   * one elected thread issues TMA and MMA; tcgen05.commit -> mbarriers.
+//   * a dedicated issuer warp (one lane) drives TMA and MMA two pages ahead of
+//     the softmax warps; tcgen05.commit and warp arrivals -> mbarriers.
 #include "common.cuh"
 #include "engine_internal.h"
 #include "gemm_tc.h"
@@ -36,17 +37,25 @@ using namespace tc;
 constexpr int HD = 128;
 constexpr int QR = 128;                       // query rows per CTA (UMMA M)
 constexpr int kBox = 64 * 64 * 2;             // 8 KB: 64 rows x 64 dims
-constexpr int kKV = 4 * kBox;                 // K lo, K hi, V lo, V hi of one page
+constexpr int kHalf = 2 * kBox;               // 16 KB: K (or V) of one page, dims 0-63 | 64-127
 constexpr int kQ = QR * HD * 2;               // 32 KB: Q tile (two 128 x 64 boxes)
 constexpr int kP = QR * 64 * 2;               // 16 KB: P tile [128 x 64 keys]
-constexpr int NKV = 4;                        // K/V pages in flight
-constexpr int kSmem = NKV * kKV + kQ + 2 * kP + 1024 + 256;
+constexpr int NK = 4, NV = 4;                 // K and V pages in flight (separate rings)
+constexpr int NS = 3;                         // S (TMEM) and P (smem) buffers
+constexpr int kSmem = (NK + NV) * kHalf + kQ + NS * kP + 3072 + 1024 + 256;
 constexpr float kRescale = 8.0f;              // log2 headroom before the running max is raised
-constexpr int kTmemCols = 256;                // S0 [0,64) S1 [64,128) O [128,256)
+constexpr int kTmemCols = 512;                // S0-2 [0,192), O [256,384)
 
 __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<const uint32_t*>(&v);
+}
+
+// 2^x on the SFU, flush-to-zero (x <= kRescale here: scores minus the stale running max)
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
@@ -109,38 +118,78 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
 
 constexpr uint32_t kIdS = idesc_bf16(QR, 64);                       // S = Q K^T
 constexpr uint32_t kIdPV = idesc_bf16(QR, HD) | (1u << 16);         // O += P V, V MN-major
+constexpr int kSoftWarps = 8;                                       // 2 per 32-row TMEM lane group
+constexpr int kIssuer = kSoftWarps;                                 // warp index of the TMA/MMA issuer
+constexpr int kThreads = 32 * (kSoftWarps + 1);
+// diagnostics (option "pattn_trace"): clock64 stamps of head 0's CTAs, 512 per tile
+#define PT_STAMP(slot) \
+  do {                                                                                   \
+    if (trace && blockIdx.y == 0 && (slot) < 512) trace[blockIdx.x * 512 + (slot)] = clock64(); \
+  } while (0)
 
-__global__ void __launch_bounds__(128, 1)
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void pair_sync(int id) {  // the two softmax warps of one lane group
+  asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory");
+}
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p;
+  asm volatile("{ .reg .pred P; elect.sync _|P, 0xffffffff; selp.b32 %0, 1, 0, P; }" : "=r"(p));
+  return p != 0;
+}
+
+// Warps 0-7: softmax.  Warp w owns query rows 32 (w & 3) .. + 31 (its TMEM
+// lane group) and key half w >> 2 (32 of a page's 64 keys); the two warps of
+// a lane group swap their row maxima through shared memory once per page.
+// Warp 8: TMA + MMA issue (the whole warp runs the schedule, one elected lane
+// issues), three pages of S ahead of the softmax so the issue latency of the
+// next S never sits on the softmax's critical path.  K and V have separate
+// rings: a K stage frees when its S completes, a V stage when its P V does.
+// Handshakes, all mbarriers:
+//   full_k/full_v[st]  TMA -> issuer        K (V) of a page landed
+//   s_full[b]          issuer -> softmax    S_j complete in TMEM buffer j % 3
+//   p_full[b]          softmax -> issuer    P_j written (and any O rescale stored)
+//   pv_done[b]         issuer -> both       P_j V_j complete: O stable, P buffer free
+__global__ void __launch_bounds__(kThreads, 1)
 prefill_attn_tc_kernel(const __grid_constant__ CUtensorMap pool_map, const PrefillTile* __restrict__ tiles,
                        const int32_t* __restrict__ ptab, const float* __restrict__ q, int L, int layer, int H, int d,
-                       float scale_log2, __nv_bfloat16* __restrict__ out) {
+                       float scale_log2, __nv_bfloat16* __restrict__ out, unsigned long long* trace) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  unsigned char* skv = smem;                       // [NKV][K lo, K hi, V lo, V hi]
-  unsigned char* sq = smem + NKV * kKV;            // Q: [dims 0-63 | dims 64-127] x 128 rows
-  unsigned char* sp = sq + kQ;                     // P: [2][128 x 64]
-  uint64_t* full = (uint64_t*)(sp + 2 * kP);       // [NKV] K/V landed
-  uint64_t* s_done = full + NKV;                   // [2] S MMAs of a page complete
-  uint64_t* pv_done = s_done + 2;                  // [2] P V MMAs complete (P buffer + K/V stage free)
-  uint32_t* tmem_slot = (uint32_t*)(pv_done + 2);
+  unsigned char* sk = smem;                        // [NK][K lo, K hi]
+  unsigned char* sv = sk + NK * kHalf;             // [NV][V lo, V hi]
+  unsigned char* sq = sv + NV * kHalf;             // Q: [dims 0-63 | dims 64-127] x 128 rows
+  unsigned char* sp = sq + kQ;                     // P: [NS][128 x 64]
+  float* red = (float*)(sp + NS * kP);             // [2 pages][2 halves][128 rows] maxima, then [2][128] sums
+  uint64_t* full_k = (uint64_t*)(red + 768);       // [NK]
+  uint64_t* full_v = full_k + NK;                  // [NV]
+  uint64_t* s_full = full_v + NV;                  // [NS]
+  uint64_t* p_full = s_full + NS;                  // [NS]
+  uint64_t* pv_done = p_full + NS;                 // [NS]
+  uint32_t* tmem_slot = (uint32_t*)(pv_done + NS);
 
   pdl_trigger();
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int h = blockIdx.y;
-  if (tid == 0) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&pool_map) : "memory");
-    for (int i = 0; i < NKV; i++) mbar_init(&full[i], 1);
-    for (int i = 0; i < 2; i++) {
-      mbar_init(&s_done[i], 1);
-      mbar_init(&pv_done[i], 1);
+  if (warp == kIssuer) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&pool_map) : "memory");
+      for (int i = 0; i < NK; i++) mbar_init(&full_k[i], 1);
+      for (int i = 0; i < NV; i++) mbar_init(&full_v[i], 1);
+      for (int i = 0; i < NS; i++) {
+        mbar_init(&s_full[i], 1);
+        mbar_init(&p_full[i], kSoftWarps);
+        mbar_init(&pv_done[i], 1);
+      }
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 0) {
+    __syncwarp();
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
                  "n"(kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
+  if (tid == 0) PT_STAMP(0);
   pdl_wait();  // q and the K/V of this forward's rows come from the QKV GEMM
   // heaviest tiles first: a tile's pages grow with its position, so the CTAs
   // that spill into a second wave are the short ones
@@ -149,37 +198,33 @@ prefill_attn_tc_kernel(const __grid_constant__ CUtensorMap pool_map, const Prefi
   const int pos0 = tile.pos0, n_rows = tile.n;
   const int n_pages = (pos0 + n_rows - 1) / FE_PAGE + 1;
 
-  auto issue_kv = [&](int j) {  // page j -> stage j % NKV (thread 0)
-    const int st = j % NKV;
-    const int rk = (((pages[j] * L + layer) * 2 + 0) * H + h) * 64;
-    const int rv = rk + H * 64;
-    unsigned char* b = skv + st * kKV;
-    mbar_expect_tx(&full[st], kKV);
-    tma_load_2d(b, &pool_map, &full[st], 0, rk);
-    tma_load_2d(b + kBox, &pool_map, &full[st], 64, rk);
-    tma_load_2d(b + 2 * kBox, &pool_map, &full[st], 0, rv);
-    tma_load_2d(b + 3 * kBox, &pool_map, &full[st], 64, rv);
+  // K (kv = 0) or V (kv = 1) of page j -> its ring stage (elected issuer lane)
+  auto issue_load = [&](int j, int kv) {
+    const int st = j % (kv ? NV : NK);
+    const int row = ((((pages[j] * L + layer) * 2 + kv) * H + h) * 64);
+    unsigned char* b = (kv ? sv : sk) + st * kHalf;
+    uint64_t* bar = kv ? &full_v[st] : &full_k[st];
+    mbar_expect_tx(bar, kHalf);
+    tma_load_2d(b, &pool_map, bar, 0, row);
+    tma_load_2d(b + kBox, &pool_map, bar, 64, row);
   };
-  if (tid == 0)
-    for (int j = 0; j < min(NKV, n_pages); j++) issue_kv(j);
+  if (warp == kIssuer && lane == 0) {  // barriers were initialised by this thread
+    for (int j = 0; j < min(NK, n_pages); j++) issue_load(j, 0);
+    for (int j = 0; j < min(NV, n_pages); j++) issue_load(j, 1);
+  }
 
-  // Q row `tid` -> bf16 (exp2 domain), 128B-swizzled K-major
-  const int r = tid;                       // query row of the tile = TMEM lane
-  const int pos = pos0 + r;
-  const bool live = r < n_rows;
-  {
-    const float* qr = q + (size_t)(tile.row0 + (live ? r : 0)) * d + h * HD;
-#pragma unroll
-    for (int c = 0; c < 16; c++) {  // 16-byte chunk c = dims 8c .. 8c + 7
-      float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
-      if (live) {
-        a = *reinterpret_cast<const float4*>(qr + 8 * c);
-        b = *reinterpret_cast<const float4*>(qr + 8 * c + 4);
-      }
-      const float s = scale_log2;
-      const uint4 v = make_uint4(pack2(a.x * s, a.y * s), pack2(a.z * s, a.w * s), pack2(b.x * s, b.y * s),
-                                 pack2(b.z * s, b.w * s));
-      *reinterpret_cast<uint4*>(sq + (c >> 3) * (QR * 128) + r * 128 + (((c & 7) ^ (r & 7)) << 4)) = v;
+  // Q -> bf16 (exp2 domain), 128B-swizzled K-major: softmax warp w stages rows
+  // 16 w .. 16 w + 15, one coalesced 512-byte row per load (lane = 4 dims)
+  if (warp < kSoftWarps) {
+    const int c = lane >> 1;               // 16-byte chunk = dims 8c .. 8c + 7
+#pragma unroll 8
+    for (int i = 0; i < 16; i++) {
+      const int row = 16 * warp + i;
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (row < n_rows) a = *reinterpret_cast<const float4*>(q + (size_t)(tile.row0 + row) * d + h * HD + 4 * lane);
+      const float sc = scale_log2;
+      *reinterpret_cast<uint2*>(sq + (c >> 3) * (QR * 128) + row * 128 + (((c & 7) ^ (row & 7)) << 4) +
+                                ((lane & 1) << 3)) = make_uint2(pack2(a.x * sc, a.y * sc), pack2(a.z * sc, a.w * sc));
     }
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -187,123 +232,179 @@ prefill_attn_tc_kernel(const __grid_constant__ CUtensorMap pool_map, const Prefi
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
-  const uint32_t t_lane = tmem + ((uint32_t)(32 * warp) << 16);
-  const uint32_t t_o = 128;  // O accumulator columns
+  const uint32_t t_o = 256;  // O accumulator columns
+  if (tid == 0) PT_STAMP(1);
 
-  auto issue_s = [&](int j) {  // S_j = Q K_j^T -> TMEM cols (j & 1) * 64 (thread 0)
-    const int st = j & 1, kst = j % NKV;
-    mbar_wait(&full[kst], (j / NKV) & 1);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const unsigned char* kb = skv + kst * kKV;
-#pragma unroll
-    for (int ks = 0; ks < 8; ks++) {
-      const uint64_t off = (uint64_t)(((ks & 3) * 32) >> 4);
-      mma_f16(tmem + (uint32_t)(st * 64), smem_desc(sq + (ks >> 2) * (QR * 128)) + off,
-              smem_desc(kb + (ks >> 2) * kBox) + off, kIdS, ks > 0 ? 1u : 0u);
-    }
-    mma_commit(&s_done[st]);
-  };
-  if (tid == 0) issue_s(0);
-
-  float m_used = -INFINITY, l = 0.0f;  // running (stale) max, sum -- this thread's row
-  for (int j = 0; j < n_pages; j++) {
-    const int st = j & 1;
-    // S of the next page while this page's softmax runs (its K stage and S
-    // buffer are free once the P V of page j - 1 completed)
-    // (S buffer (j + 1) & 1 was read by every thread before the last
-    // iteration's barrier; page j + 1's K/V stage was issued NKV - 1 pages ago)
-    if (tid == 0 && j + 1 < n_pages) issue_s(j + 1);
-    mbar_wait(&s_done[st], (j >> 1) & 1);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    float s[64];
-    {
-      float a[32], b[32];
-      tmem_ld32(t_lane + (uint32_t)(st * 64), a);
-      tmem_ld32(t_lane + (uint32_t)(st * 64 + 32), b);
-#pragma unroll
-      for (int i = 0; i < 32; i++) { s[i] = a[i]; s[32 + i] = b[i]; }
-    }
-    const int kbase = j * FE_PAGE;
-    float mx = -INFINITY;
-#pragma unroll
-    for (int i = 0; i < 64; i++) {
-      s[i] = (live && kbase + i <= pos) ? s[i] : -INFINITY;
-      mx = fmaxf(mx, s[i]);
-    }
-    // raise the running max only when the new scores would overflow the headroom
-    const bool raise = mx > m_used + kRescale;
-    if (__any_sync(0xffffffffu, raise && j > 0)) {
-      // the P V of page j - 1 must have landed in O before O is rescaled
-      mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
+  if (warp == kIssuer) {
+    // descriptors as base + (byte offset >> 4): the start-address field is the
+    // low 14 bits and every operand lies below 256 KB, so plain adds are exact
+    const uint64_t dq = smem_desc(sq), dk = smem_desc(sk), dp = smem_desc(sp), dv = smem_desc_mn(sv, kBox);
+    auto mma_s = [&](int j) {  // S_j = Q K_j^T -> TMEM cols (j % NS) * 64
+      const int kst = j % NK;
+      mbar_wait(&full_k[kst], (j / NK) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const float f = raise ? exp2f(m_used - mx) : 1.0f;  // m_used = -inf -> 0 (O is still 0)
+      if (elect_one()) {
+        const uint32_t dst = tmem + (uint32_t)((j % NS) * 64);
+        const uint64_t kb = dk + (uint64_t)((kst * kHalf) >> 4);
+#pragma unroll
+        for (int ks = 0; ks < 8; ks++) {
+          const uint64_t off = (uint64_t)((ks & 3) * 2 + (ks >> 2) * ((QR * 128) >> 4));
+          const uint64_t koff = (uint64_t)((ks & 3) * 2 + (ks >> 2) * (kBox >> 4));
+          mma_f16(dst, dq + off, kb + koff, kIdS, ks > 0 ? 1u : 0u);
+        }
+        mma_commit(&s_full[j % NS]);
+      }
+      __syncwarp();
+    };
+    for (int j = 0; j < min(NS, n_pages); j++) mma_s(j);
+    for (int m = 0; m < 2 && m + NK < n_pages; m++) {  // K stages of pages 0, 1 free once their S completed
+      mbar_wait(&s_full[m % NS], (m / NS) & 1);
+      if (elect_one()) issue_load(m + NK, 0);
+      __syncwarp();
+    }
+    for (int j = 0; j < n_pages; j++) {
+      const int b = j % NS, vst = j % NV;
+      mbar_wait(&p_full[b], (j / NS) & 1);
+      if (lane == 0) PT_STAMP(16 + 16 * j + 12);
+      mbar_wait(&full_v[vst], (j / NV) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (elect_one()) {
+        const uint64_t pb = dp + (uint64_t)((b * kP) >> 4);
+        const uint64_t vb = dv + (uint64_t)((vst * kHalf) >> 4);
+#pragma unroll
+        for (int kk = 0; kk < 4; kk++)  // 16 keys per MMA
+          mma_f16(tmem + t_o, pb + (uint64_t)(kk * 2), vb + (uint64_t)(kk * (2048 >> 4)), kIdPV,
+                  (j > 0 || kk > 0) ? 1u : 0u);
+        mma_commit(&pv_done[b]);
+      }
+      __syncwarp();
+      if (lane == 0) PT_STAMP(16 + 16 * j + 13);
+      // S buffer b was read by the softmax before p_full[b]
+      if (j + NS < n_pages) mma_s(j + NS);
+      if (lane == 0) PT_STAMP(16 + 16 * j + 14);
+      // refills: page j + 2's K stage (its S was issued an iteration ago) and
+      // page j - 1's V stage (its P V likewise) -- both all but certainly done
+      if (j + 2 + NK < n_pages) {
+        mbar_wait(&s_full[(j + 2) % NS], ((j + 2) / NS) & 1);
+        if (elect_one()) issue_load(j + 2 + NK, 0);
+        __syncwarp();
+      }
+      if (j >= 1 && j - 1 + NV < n_pages) {
+        mbar_wait(&pv_done[(j - 1) % NS], ((j - 1) / NS) & 1);
+        if (elect_one()) issue_load(j - 1 + NV, 1);
+        __syncwarp();
+      }
+    }
+  } else {
+    const int grp = warp & 3, hf = warp >> 2;     // lane group, key half
+    const int r = 32 * grp + lane;                // query row of the tile = TMEM lane
+    const int pos = pos0 + r;
+    const bool live = r < n_rows;
+    const uint32_t t_lane = tmem + ((uint32_t)(32 * grp) << 16);
+    float m_used = -INFINITY, l = 0.0f;  // running (stale) max, partial sum over this half's keys
+    for (int j = 0; j < n_pages; j++) {
+      const int b = j % NS;
+      mbar_wait(&s_full[b], (j / NS) & 1);
+      if (tid == 0) PT_STAMP(16 + 16 * j);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      float s[32];
+      tmem_ld32(t_lane + (uint32_t)(b * 64 + hf * 32), s);
+      const int kb0 = j * FE_PAGE + hf * 32;      // key position of s[0]
+      // causal / tail mask: only the diagonal pages (and a ragged tile's dead
+      // rows) need it -- warp-uniform test
+      if (__any_sync(0xffffffffu, !live || kb0 + 31 > pos)) {
+        const int lim = live ? pos - kb0 : -1;
+#pragma unroll
+        for (int i = 0; i < 32; i++) s[i] = i <= lim ? s[i] : -INFINITY;
+      }
+      float mx8[8];
+#pragma unroll
+      for (int e = 0; e < 8; e++) mx8[e] = fmaxf(fmaxf(s[e], s[e + 8]), fmaxf(s[e + 16], s[e + 24]));
+      float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[4]), fmaxf(mx8[2], mx8[6])),
+                       fmaxf(fmaxf(mx8[1], mx8[5]), fmaxf(mx8[3], mx8[7])));
+      // row max over both key halves (double-buffered by page parity)
+      red[((j & 1) * 2 + hf) * 128 + r] = mx;
+      pair_sync(1 + grp);
+      mx = fmaxf(mx, red[((j & 1) * 2 + (hf ^ 1)) * 128 + r]);
+      if (tid == 0) PT_STAMP(16 + 16 * j + 2);
+      // raise the running max only when the new scores would overflow the
+      // headroom (both warps of the pair decide identically)
+      const bool raise = mx > m_used + kRescale;
+      if (__any_sync(0xffffffffu, raise && j > 0)) {
+        // the P V of page j - 1 must have landed in O before O is rescaled
+        mbar_wait(&pv_done[(j - 1) % NS], ((j - 1) / NS) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const float f = raise ? exp2f(m_used - mx) : 1.0f;  // m_used = -inf -> 0 (O is still 0)
 #pragma unroll 1
-      for (int c = 0; c < HD; c += 32) {
-        float o[32];
-        tmem_ld32(t_lane + t_o + c, o);
+        for (int c = hf * 64; c < hf * 64 + 64; c += 32) {  // this half's O columns
+          float o[32];
+          tmem_ld32(t_lane + t_o + c, o);
 #pragma unroll
-        for (int i = 0; i < 32; i++) o[i] *= f;
-        tmem_st32(t_lane + t_o + c, o);
+          for (int i = 0; i < 32; i++) o[i] *= f;
+          tmem_st32(t_lane + t_o + c, o);
+        }
+        if (raise) l *= f;
       }
-      if (raise) l *= f;
+      if (raise) m_used = mx;
+      const float mu = m_used == -INFINITY ? 0.0f : m_used;
+      float sum4[4];
+      unsigned char* pb = sp + b * kP;
+      // P buffer b is free once the P V that read it (page j - 3) completed
+      if (j >= NS) mbar_wait(&pv_done[b], ((j - NS) / NS) & 1);
+      if (tid == 0) PT_STAMP(16 + 16 * j + 3);
+#pragma unroll
+      for (int c = 0; c < 4; c++) {
+        float p[8];
+#pragma unroll
+        for (int e = 0; e < 8; e++) p[e] = ex2_approx(s[8 * c + e] - mu);
+        sum4[c] = ((p[0] + p[4]) + (p[2] + p[6])) + ((p[1] + p[5]) + (p[3] + p[7]));
+        const uint4 v = make_uint4(pack2(p[0], p[1]), pack2(p[2], p[3]), pack2(p[4], p[5]), pack2(p[6], p[7]));
+        const int ch = 4 * hf + c;                // 16-byte chunk of the row's 64 keys
+        *reinterpret_cast<uint4*>(pb + r * 128 + ((ch ^ (r & 7)) << 4)) = v;
+      }
+      l += (sum4[0] + sum4[2]) + (sum4[1] + sum4[3]);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[b]);  // this warp's half of 32 rows of P (and O) are in place
+      if (lane == 0) PT_STAMP(16 + 16 * j + 4 + warp);
     }
-    if (raise) m_used = mx;
-    const float mu = m_used == -INFINITY ? 0.0f : m_used;
-    float sum = 0.0f;
-    unsigned char* pb = sp + st * kP;
-    // P buffer st is free once the P V that read it (page j - 2) completed
-    if (j >= 2) mbar_wait(&pv_done[st], ((j - 2) >> 1) & 1);
+    // O / l -> bf16 attention output; l = both halves' partial sums
+    red[512 + hf * 128 + r] = l;
+    const int jl = n_pages - 1;
+    mbar_wait(&pv_done[jl % NS], (jl / NS) & 1);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    pair_sync(1 + grp);
+    const float lt = red[512 + r] + red[640 + r];
+    const float inv = lt > 0.0f ? 1.0f / lt : 0.0f;
+    // this half's 64 O columns -> bf16 in the (now idle) Q buffer, then
+    // coalesced stores: row r's 16-byte chunk k at r * 256 + ((k ^ (r & 7)) << 4)
+    unsigned char* so = sq;
+#pragma unroll 1
+    for (int c = hf * 64; c < hf * 64 + 64; c += 32) {
+      float o[32];
+      tmem_ld32(t_lane + t_o + c, o);
 #pragma unroll
-    for (int c = 0; c < 8; c++) {
-      float p[8];
-#pragma unroll
-      for (int e = 0; e < 8; e++) {
-        p[e] = exp2f(s[8 * c + e] - mu);
-        sum += p[e];
+      for (int i = 0; i < 32; i += 8) {
+        const int k = (c + i) >> 3;
+        *reinterpret_cast<uint4*>(so + r * 256 + ((k ^ (r & 7)) << 4)) =
+            make_uint4(pack2(o[i] * inv, o[i + 1] * inv), pack2(o[i + 2] * inv, o[i + 3] * inv),
+                       pack2(o[i + 4] * inv, o[i + 5] * inv), pack2(o[i + 6] * inv, o[i + 7] * inv));
       }
-      const uint4 v = make_uint4(pack2(p[0], p[1]), pack2(p[2], p[3]), pack2(p[4], p[5]), pack2(p[6], p[7]));
-      *reinterpret_cast<uint4*>(pb + r * 128 + ((c ^ (r & 7)) << 4)) = v;
     }
-    l += sum;
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();  // every row's P and O rescale are in place
-    if (tid == 0) {
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const unsigned char* vb = skv + (j % NKV) * kKV + 2 * kBox;
-#pragma unroll
-      for (int kk = 0; kk < 4; kk++)  // 16 keys per MMA
-        mma_f16(tmem + t_o, smem_desc(pb) + (uint64_t)((kk * 32) >> 4), smem_desc_mn(vb + kk * 2048, kBox), kIdPV,
-                (j > 0 || kk > 0) ? 1u : 0u);
-      mma_commit(&pv_done[st]);
-      if (j >= 1 && j - 1 + NKV < n_pages) {  // refill page j - 1's stage (its P V is done by now)
-        mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
-        issue_kv(j - 1 + NKV);
-      }
+    __syncwarp();
+#pragma unroll 4
+    for (int i = 0; i < 32; i += 4) {      // four half-rows per instruction, 8 lanes x 16 B each
+      const int row = 32 * grp + i + (lane >> 3), k = 8 * hf + (lane & 7);
+      if (row < n_rows)
+        *reinterpret_cast<uint4*>(out + (size_t)(tile.row0 + row) * d + h * HD + 8 * k) =
+            *reinterpret_cast<const uint4*>(so + row * 256 + ((k ^ (row & 7)) << 4));
     }
   }
-  // O / l -> bf16 attention output
-  const int jl = n_pages - 1;
-  mbar_wait(&pv_done[jl & 1], (jl >> 1) & 1);
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const float inv = l > 0.0f ? 1.0f / l : 0.0f;
-#pragma unroll 1
-  for (int c = 0; c < HD; c += 32) {
-    float o[32];
-    tmem_ld32(t_lane + t_o + c, o);
-    if (live) {
-      __nv_bfloat16* dst = out + (size_t)(tile.row0 + r) * d + h * HD + c;
-#pragma unroll
-      for (int i = 0; i < 32; i += 8)
-        *reinterpret_cast<uint4*>(dst + i) = make_uint4(pack2(o[i] * inv, o[i + 1] * inv),
-                                                         pack2(o[i + 2] * inv, o[i + 3] * inv),
-                                                         pack2(o[i + 4] * inv, o[i + 5] * inv),
-                                                         pack2(o[i + 6] * inv, o[i + 7] * inv));
-    }
-  }
+  if (tid == 0) PT_STAMP(15);
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 0) {
+  if (warp == kIssuer) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols));
   }
@@ -312,15 +413,15 @@ prefill_attn_tc_kernel(const __grid_constant__ CUtensorMap pool_map, const Prefi
 }  // namespace
 
 void launch_prefill_attention_tc(const Fwd& f, const ModelDims& m, const TmaMap& pool_map, const float* q, int layer,
-                                 void* out, cudaStream_t s) {
+                                 void* out, cudaStream_t s, unsigned long long* trace) {
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(prefill_attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     configured = true;
   }
-  launch_k(prefill_attn_tc_kernel, dim3(f.n_ptiles, m.H), dim3(128), (size_t)kSmem, s,
+  launch_k(prefill_attn_tc_kernel, dim3(f.n_ptiles, m.H), dim3(kThreads), (size_t)kSmem, s,
            *reinterpret_cast<const CUtensorMap*>(pool_map.bytes), f.ptiles, f.ptab, q, m.L, layer, m.H, m.d,
-           m.attn_scale * 1.4426950408889634f, (__nv_bfloat16*)out);
+           m.attn_scale * 1.4426950408889634f, (__nv_bfloat16*)out, trace);
 }
 
 }  // namespace fe

@@ -21,6 +21,8 @@ ap.add_argument("rows", nargs="*", type=int, default=[33, 48, 96, 168, 256, 448,
 ap.add_argument("--shapes", default="qkv,o,gate_up,down")
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--out", default=None)
+ap.add_argument("--sk", type=lambda v: [int(x) for x in v.split(",") if x], default=[],
+                help="extra variants with engine option tc_sk = each value")
 ap.add_argument("--force-splits", type=lambda v: [int(x) for x in v.split(",") if x], default=[])
 args = ap.parse_args()
 
@@ -53,11 +55,13 @@ for rows in args.rows:
         torch.cuda.synchronize()
         line = f"rows {rows:5d} {name:8s} N={N:6d} K={K:6d}:"
         rec = {"rows": rows, "shape": name, "N": N, "K": K}
-        variants = [("v1", 0, 0), ("pair_nosplit", 1, 0), ("pair", 1, 1)]
-        variants += [(f"split{k}", 1, k) for k in args.force_splits]
-        for label, pair, split in variants:
+        variants = [("v1", 0, 0, 0), ("pair_nosplit", 1, 0, 0), ("pair", 1, 1, 0)]
+        variants += [(f"split{k}", 1, k, 0) for k in args.force_splits]
+        variants += [(f"sk{k}", 1, 1, k) for k in args.sk]
+        for label, pair, split, sk in variants:
             eng.set_option("tc_pair", pair)
             eng.set_option("tc_split", split)
+            eng.set_option("tc_sk", sk)
             y.fill_(float("nan"))
             us = timed(lambda: eng.op_gemm_tc(x.data_ptr(), w.data_ptr(), rows, N, K, y.data_ptr()), args.reps)
             err = ((y - ref).abs().max() / ref.abs().max()).item()
@@ -67,6 +71,7 @@ for rows in args.rows:
             line += f"  {label}: {us:8.1f}us {tf:6.0f}TF/s"
         eng.set_option("tc_pair", 1)
         eng.set_option("tc_split", 1)
+        eng.set_option("tc_sk", 0)
         print(line, flush=True)
         results.append(rec)
         del w, ref
