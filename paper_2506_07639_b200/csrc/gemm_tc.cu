@@ -533,6 +533,10 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
   cluster_sync_all();  // barriers of both CTAs initialised before any remote arrival
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  // programmatic dependent launch: the prologue above overlapped the previous
+  // kernel's tail; nothing global is touched before it has completed
+  pdl_trigger();
+  pdl_wait();
 
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer (both CTAs)
@@ -1381,8 +1385,8 @@ void launch_gemm_tc(const TmaMap& a_map, const TmaMap& b_map64, const TcLaunch& 
   const int grid = 2 * (p.dp == units ? std::min(units, P) : P);
   const CUtensorMap& am = *reinterpret_cast<const CUtensorMap*>(a_map.bytes);
   const CUtensorMap& bm = *reinterpret_cast<const CUtensorMap*>(b_map64.bytes);
-  if (bn == 256) gemm_pair_kernel<256><<<grid, kPairThreads, pair_smem<256>(), s>>>(am, bm, p);
-  else gemm_pair_kernel<128><<<grid, kPairThreads, pair_smem<128>(), s>>>(am, bm, p);
+  if (bn == 256) launch_k(gemm_pair_kernel<256>, dim3(grid), dim3(kPairThreads), (size_t)pair_smem<256>(), s, am, bm, p);
+  else launch_k(gemm_pair_kernel<128>, dim3(grid), dim3(kPairThreads), (size_t)pair_smem<128>(), s, am, bm, p);
   if (S > 1) {
     const size_t work = l.epi == TC_SWIGLU ? (size_t)l.M * l.F / 4 : l.epi == TC_QKV ? (size_t)l.M * (l.N / 128) * 16
                                                                                    : (size_t)l.M * l.N / 4;
