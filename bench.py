@@ -74,6 +74,8 @@ def parse():
     ap.add_argument("--ref-budget-s", type=float, default=150.0,
                     help="reference arm: stop after this much CPU wall time (at least one timed step)")
     ap.add_argument("--out", default=None, help="also write the JSON line here")
+    ap.add_argument("--engine-opt", action="append", default=[], metavar="KEY=VALUE",
+                    help="engine option (fe_set_option) applied before warm-up; A/B measurements only")
     args = ap.parse_args()
     if args.episodes is None:
         args.episodes = 64 if args.gpus > 1 else 1
@@ -351,6 +353,9 @@ def run_engine(args, rank, world, local):
     backend = EngineBackend(args.config, dtype=args.dtype, seed=0, device=local, profile=make_profile(0),
                             max_rows=args.max_rows, vision=True if args.vision else None)
     eng = backend.engine
+    for kv in args.engine_opt:
+        key, val = kv.split("=", 1)
+        eng.set_option(key, int(val))
     stream = torch.cuda.ExternalStream(eng.stream_handle(), device=local)
     cfg_run = RS.SchedulerConfig(mode=args.mode, slots=8, wall_clock=True)
     if args.episodes > 1:  # config 4: this rank's shard of the episodes, one batch per timestep

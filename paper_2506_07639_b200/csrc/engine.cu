@@ -233,7 +233,8 @@ struct fe_engine {
   unsigned long long* mk_trace = nullptr;  // diagnostics: per-phase barrier timestamps of the last tick
   size_t mk_trace_n = 0;
   bool mk_trace_on = false;
-  bool pattn_trace_on = false;  // diagnostics: prefill attention stamps into mk_trace (option "pattn_trace")
+  bool pattn_trace_on = false;
+  bool fuse_norm = true;  // option "fuse_norm": split-K residual reduces apply the following RMSNorm  // diagnostics: prefill attention stamps into mk_trace (option "pattn_trace")
   int mk_flags = 0;
   int mk_fused = (1 << fe::MK_GU) | (1 << fe::MK_LM);  // option "mk_fused"
   cudaEvent_t mk_ev[kLanes] = {};  // last persistent tick of each lane
@@ -520,13 +521,25 @@ void launch_layers(fe_engine* e, Lane& ln, const fe::Fwd& f, int n, bool decode,
     t.part_keys = ws.part_keys; t.logits = ws.logits; t.V = m.V; t.n_text = m.n_text;
     return t;
   };
+  // a split-K residual GEMM (O, down) can apply the RMSNorm that follows it in
+  // its reduce (launch_gemm_tc returns true); the norm launch is then skipped
+  bool normed = false;
+  auto with_norm = [&](fe::TcLaunch t, const float* w) {
+    if (dt == FE_BF16 && w && e->fuse_norm && !(e->debug_skip & 2)) {
+      t.norm_w = w;
+      t.norm_out = (__nv_bfloat16*)ws.xn;
+      t.norm_eps = m.eps;
+    }
+    return t;
+  };
   for (int l = 0; l < m.L; l++) {
     const fe::Weights::Layer& ly = e->layers[l];
     const auto& mp = e->tc_maps.empty() ? EngineMapsDummy() : e->tc_maps[l];
     const size_t layer_off = (size_t)l * 2 * m.H * FE_PAGE * m.hd;
     const bool skip_norm = e->debug_skip & 2, skip_gemm = e->debug_skip & 4;
     int p;
-    if (!skip_norm) fe::launch_rmsnorm(dt, ws.x, ly.attn_norm, ws.xn, n, m.d, m.d, m.eps, nullptr, st);
+    if (!skip_norm && !normed) fe::launch_rmsnorm(dt, ws.x, ly.attn_norm, ws.xn, n, m.d, m.d, m.eps, nullptr, st);
+    normed = false;
     p = decode ? prof_begin(e, ln, PROF_GEMV) : -1;
     if (skip_gemm) {
     } else if (sk_on(0)) {
@@ -557,11 +570,13 @@ void launch_layers(fe_engine* e, Lane& ln, const fe::Fwd& f, int n, bool decode,
     p = decode ? prof_begin(e, ln, PROF_GEMV) : -1;
     if (skip_gemm) {
     } else if (sk_on(1)) fe::launch_skinny_tc(mp.wo, ln.map_attn16, sk_launch(fe::TC_RESID, m.d, m.d), st);
-    else if (tc_on(1) && e->tc_pair) fe::launch_gemm_tc(ln.map_attn, mp.wo64, tc_launch(fe::TC_RESID, m.d, m.d), st);
+    else if (tc_on(1) && e->tc_pair)
+      normed = fe::launch_gemm_tc(ln.map_attn, mp.wo64, with_norm(tc_launch(fe::TC_RESID, m.d, m.d), ly.ffn_norm), st);
     else if (tc_on(1)) fe::launch_gemm_tc_v1(ln.map_attn, mp.wo, tc_launch(fe::TC_RESID, m.d, m.d), st);
     else fe::launch_resid(dt, f, m.d, m.d, ly.wo, ws.attn, ws.x, st);
     prof_end(e, ln, p, gemv_bytes(m.d, m.d, n));
-    if (!skip_norm) fe::launch_rmsnorm(dt, ws.x, ly.ffn_norm, ws.xn, n, m.d, m.d, m.eps, nullptr, st);
+    if (!skip_norm && !normed) fe::launch_rmsnorm(dt, ws.x, ly.ffn_norm, ws.xn, n, m.d, m.d, m.eps, nullptr, st);
+    normed = false;
     p = decode ? prof_begin(e, ln, PROF_GEMV) : -1;
     if (skip_gemm) {
     } else if (sk_on(2)) fe::launch_skinny_tc(mp.wgu, ln.map_xn16, sk_launch(fe::TC_SWIGLU, 2 * m.F, m.d), st);
@@ -572,7 +587,10 @@ void launch_layers(fe_engine* e, Lane& ln, const fe::Fwd& f, int n, bool decode,
     p = decode ? prof_begin(e, ln, PROF_GEMV) : -1;
     if (skip_gemm) {
     } else if (sk_on(3)) fe::launch_skinny_tc(mp.wdown, ln.map_act16, sk_launch(fe::TC_RESID, m.d, m.F), st);
-    else if (tc_on(3) && e->tc_pair) fe::launch_gemm_tc(ln.map_act, mp.wdown64, tc_launch(fe::TC_RESID, m.d, m.F), st);
+    else if (tc_on(3) && e->tc_pair)
+      normed = fe::launch_gemm_tc(ln.map_act, mp.wdown64,
+                                  with_norm(tc_launch(fe::TC_RESID, m.d, m.F),
+                                            l + 1 < m.L ? e->layers[l + 1].attn_norm : nullptr), st);
     else if (tc_on(3)) fe::launch_gemm_tc_v1(ln.map_act, mp.wdown, tc_launch(fe::TC_RESID, m.d, m.F), st);
     else fe::launch_resid(dt, f, m.d, m.F, ly.wdown, ws.attn, ws.x, st);
     prof_end(e, ln, p, gemv_bytes(m.d, m.F, n));
@@ -1973,6 +1991,9 @@ int fe_set_option(fe_engine* e, const char* key, int64_t value) {
         CK(cudaMemset(e->mk_trace, 0, e->mk_trace_n * 8));
       }
       e->mk_trace_on = value != 0 && e->mk_trace != nullptr;
+      clear_graphs(e);
+    } else if (k == "fuse_norm") {
+      e->fuse_norm = value != 0;
       clear_graphs(e);
     } else if (k == "pattn_trace") {
       if (value && !e->mk_trace) {

@@ -1061,6 +1061,87 @@ skinny_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constan
 }
 
 // Split-K reduction with the fused epilogue (the pair GEMM's split mode):
+// RESID split-K reduce fused with the RMSNorm that follows it: one block per
+// row; x += sum of the splits (split order, as splitk_reduce_kernel), then
+// out = bf16(x * rsqrt(mean x^2 + eps) * w) with rmsnorm_bf16_kernel's thread
+// mapping and summation order, so the result is bit-identical to the two
+// kernels run back to back.
+__global__ void __launch_bounds__(256) splitk_resid_norm_kernel(const float* __restrict__ part, int S, TcArgs a,
+                                                                const float* __restrict__ w,
+                                                                __nv_bfloat16* __restrict__ out, float eps) {
+  pdl_trigger();
+  pdl_wait();
+  __shared__ float red[8];
+  const int row = blockIdx.x, d = a.N;
+  const size_t plane = (size_t)a.M * a.N;
+  float* xr = a.y + (size_t)row * a.ldy;
+  const float* pr = part + (size_t)row * a.N;
+  float ss = 0.0f;
+  // this thread's 16-byte groups: chunk c (k = 8 tid + 2048 c), halves h;
+  // every load of a split is issued before any add (latency, not bandwidth,
+  // bounds a 448-row reduce)
+  constexpr int kMaxChunks = 2;  // d <= 4096 in registers; longer rows loop
+  for (int kc = 8 * threadIdx.x; kc < d; kc += 8 * blockDim.x * kMaxChunks) {
+    float4 v[2 * kMaxChunks];
+    bool on[kMaxChunks];
+#pragma unroll
+    for (int c = 0; c < kMaxChunks; c++) on[c] = kc + c * 8 * blockDim.x < d;
+#pragma unroll
+    for (int c = 0; c < kMaxChunks; c++)
+#pragma unroll
+      for (int h = 0; h < 2; h++)
+        if (on[c]) v[2 * c + h] = __ldcg(reinterpret_cast<const float4*>(pr + kc + c * 8 * blockDim.x + 4 * h));
+    for (int sp = 1; sp < S; sp++) {
+      float4 u[2 * kMaxChunks];
+#pragma unroll
+      for (int c = 0; c < kMaxChunks; c++)
+#pragma unroll
+        for (int h = 0; h < 2; h++)
+          if (on[c]) u[2 * c + h] = __ldcg(reinterpret_cast<const float4*>(pr + sp * plane + kc + c * 8 * blockDim.x + 4 * h));
+#pragma unroll
+      for (int i = 0; i < 2 * kMaxChunks; i++)
+        if (on[i / 2]) { v[i].x += u[i].x; v[i].y += u[i].y; v[i].z += u[i].z; v[i].w += u[i].w; }
+    }
+#pragma unroll
+    for (int c = 0; c < kMaxChunks; c++) {
+      if (!on[c]) continue;
+      float* xk = xr + kc + c * 8 * blockDim.x;
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const float4 o = *reinterpret_cast<const float4*>(xk + 4 * h);
+        float4& acc = v[2 * c + h];
+        acc.x += o.x; acc.y += o.y; acc.z += o.z; acc.w += o.w;
+        *reinterpret_cast<float4*>(xk + 4 * h) = acc;
+      }
+      ss = fmaf(v[2 * c].x, v[2 * c].x, fmaf(v[2 * c].y, v[2 * c].y, fmaf(v[2 * c].z, v[2 * c].z,
+               fmaf(v[2 * c].w, v[2 * c].w, ss))));
+      ss = fmaf(v[2 * c + 1].x, v[2 * c + 1].x, fmaf(v[2 * c + 1].y, v[2 * c + 1].y,
+               fmaf(v[2 * c + 1].z, v[2 * c + 1].z, fmaf(v[2 * c + 1].w, v[2 * c + 1].w, ss))));
+    }
+  }
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  float tot = 0.0f;
+#pragma unroll
+  for (int i = 0; i < 8; i++) tot += red[i];
+  const float r = rsqrtf(tot / (float)d + eps);
+  __nv_bfloat16* o = out + (size_t)row * d;
+  for (int k = 8 * threadIdx.x; k < d; k += 8 * blockDim.x) {  // this thread's own x writes
+    const float4 x0 = *reinterpret_cast<const float4*>(xr + k);
+    const float4 x1 = *reinterpret_cast<const float4*>(xr + k + 4);
+    const float4 wa = *reinterpret_cast<const float4*>(w + k);
+    const float4 wb = *reinterpret_cast<const float4*>(w + k + 4);
+    __nv_bfloat162 y[4];
+    y[0] = __floats2bfloat162_rn(x0.x * r * wa.x, x0.y * r * wa.y);
+    y[1] = __floats2bfloat162_rn(x0.z * r * wa.z, x0.w * r * wa.w);
+    y[2] = __floats2bfloat162_rn(x1.x * r * wb.x, x1.y * r * wb.y);
+    y[3] = __floats2bfloat162_rn(x1.z * r * wb.z, x1.w * r * wb.w);
+    *reinterpret_cast<uint4*>(o + k) = *reinterpret_cast<const uint4*>(y);
+  }
+}
+
 // sums split_out[0 .. S-1][row][col] in split order (deterministic) and
 // applies the GEMM's epilogue -- STORE / RESID (float4 per thread), SwiGLU
 // (gate col j, up col F + j), QKV (RoPE pairs c, c + 64 of a head; q rows or
@@ -1332,7 +1413,7 @@ int pair_tile_n(int M, int N, int epi, int F) {
   return cols % 256 == 0 ? 256 : 128;
 }
 
-void launch_gemm_tc(const TmaMap& a_map, const TmaMap& b_map64, const TcLaunch& l, cudaStream_t s) {
+bool launch_gemm_tc(const TmaMap& a_map, const TmaMap& b_map64, const TcLaunch& l, cudaStream_t s) {
   static bool configured = false;
   static int n_sm = 0;
   if (!configured) {
@@ -1387,12 +1468,18 @@ void launch_gemm_tc(const TmaMap& a_map, const TmaMap& b_map64, const TcLaunch& 
   const CUtensorMap& bm = *reinterpret_cast<const CUtensorMap*>(b_map64.bytes);
   if (bn == 256) launch_k(gemm_pair_kernel<256>, dim3(grid), dim3(kPairThreads), (size_t)pair_smem<256>(), s, am, bm, p);
   else launch_k(gemm_pair_kernel<128>, dim3(grid), dim3(kPairThreads), (size_t)pair_smem<128>(), s, am, bm, p);
+  if (S > 1 && l.epi == TC_RESID && l.norm_w && l.norm_out && l.N % 8 == 0 && l.ldy % 4 == 0) {
+    launch_k(splitk_resid_norm_kernel, dim3(l.M), dim3(256), 0, s, (const float*)l.split_scratch, S, p.t, l.norm_w,
+             l.norm_out, l.norm_eps);
+    return true;
+  }
   if (S > 1) {
     const size_t work = l.epi == TC_SWIGLU ? (size_t)l.M * l.F / 4 : l.epi == TC_QKV ? (size_t)l.M * (l.N / 128) * 16
                                                                                    : (size_t)l.M * l.N / 4;
     const int blocks = (int)std::min<size_t>((work + 255) / 256, (size_t)n_sm * 8);
     launch_k(splitk_reduce_kernel, dim3(blocks), dim3(256), 0, s, (const float*)l.split_scratch, S, p.t);
   }
+  return false;
 }
 
 }  // namespace fe

@@ -33,6 +33,12 @@ struct TcLaunch {
   int* sk_counters;    // pair_sk_counters() ints, zero-initialised
   float* split_scratch;  // split-K partial planes (split_floats floats), or null: no split-K
   size_t split_floats;
+  // RESID only: the RMSNorm that follows (bf16 out = norm(y) * norm_w).  When
+  // the GEMM runs split-K, the reduce applies it too and launch_gemm_tc
+  // returns true (the caller then skips its own norm launch)
+  const float* norm_w;
+  __nv_bfloat16* norm_out;
+  float norm_eps;
 };
 
 // skinny decode GEMM (swap-AB, <= skinny_max_rows() batch rows)
@@ -60,7 +66,7 @@ struct SkLaunch {
 TmaMap make_kmajor_map(const void* base, int rows, int K, int ld_elems, int box_rows);
 int tc_box_rows(int epi);
 // CTA-pair persistent tcgen05 GEMM (B map: 64-row boxes)
-void launch_gemm_tc(const TmaMap& a_map, const TmaMap& b_map64, const TcLaunch& l, cudaStream_t s);
+bool launch_gemm_tc(const TmaMap& a_map, const TmaMap& b_map64, const TcLaunch& l, cudaStream_t s);
 // round-1 1-CTA 128 x 128 tile GEMM (B map: 128-row boxes, SwiGLU 64), kept for A/B (option "tc_pair" 0)
 void launch_gemm_tc_v1(const TmaMap& a_map, const TmaMap& b_map, const TcLaunch& l, cudaStream_t s);
 extern int g_pair_bn;
