@@ -535,6 +535,25 @@ def test_bf16_prefill_tensor_core_attention_matches_cascade(config, plen):
     assert t1[0] == t0[0]
 
 
+def test_bf16_fused_resid_norm_is_bit_identical():
+    """Wide ticks (> 32 rows) run O / down through the CTA-pair GEMM with
+    split-K; its residual reduce then also applies the following RMSNorm
+    (gemm_tc.cu: splitk_resid_norm_kernel, option fuse_norm) in the same
+    summation order as the separate reduce + rmsnorm kernels: logits of a
+    40-branch batch are bit-identical with the fusion on and off."""
+    from oracle.backend import frame
+    ids = frame("7b_2layer", list(range(16)), list(range(300, 600)), "plan")
+    out = {}
+    for fuse in (1, 0):
+        eng = Engine("7b_2layer", dtype="bf16", seed=0, kv_pages=256, max_rows=512)
+        eng.set_option("fuse_norm", fuse)
+        out[fuse] = _branch_batch(eng, ids, 40, 3, 4)
+        eng.close()
+    for (t1, l1), (t0, l0) in zip(out[1], out[0]):
+        assert list(t1) == list(t0)
+        assert np.array_equal(l1, l0)
+
+
 def _branch_batch(eng, ids, n_branches, n_out, stride, capture=True):
     """Trunk prefill + `n_branches` forks (fork points `stride` apart) decoded
     as one continuous batch; returns per-branch (tokens, logits)."""
