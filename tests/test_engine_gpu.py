@@ -554,6 +554,27 @@ def test_bf16_fused_resid_norm_is_bit_identical():
         assert np.array_equal(l1, l0)
 
 
+@pytest.mark.parametrize("config,plen", [("7b_2layer", 2050), ("small", 1500)])
+def test_bf16_long_prefill_tcgen05_attention_matches_mma_sync(config, plen):
+    """Config-5-length trunks (up to 37 KV pages per query tile: every phase
+    of the tcgen05 kernel's K / V rings and triple-buffered S / P wraps many
+    times) through the tcgen05 prefill attention vs the mma.sync kernel
+    (option prefill_tc 0): first decode logits within bf16 tolerance, same
+    greedy tokens."""
+    from oracle.backend import frame
+    ids = frame(config, list(range(16)), [(7 * i + 300) % 30000 for i in range(plen)], "plan")
+    out = {}
+    for tc in (1, 0):
+        eng = Engine(config, dtype="bf16", seed=0, kv_pages=256, max_rows=1024)
+        eng.set_option("prefill_tc", tc)
+        out[tc] = _decode(eng, ids, 4242, 3, capture=True)
+        eng.close()
+    (t1, l1), (t0, l0) = out[1], out[0]
+    rel = np.abs(l1[0] - l0[0]).max() / np.abs(l0[0]).max()
+    assert rel < 2e-2, rel
+    assert list(t1) == list(t0)
+
+
 def _branch_batch(eng, ids, n_branches, n_out, stride, capture=True):
     """Trunk prefill + `n_branches` forks (fork points `stride` apart) decoded
     as one continuous batch; returns per-branch (tokens, logits)."""
