@@ -26,7 +26,7 @@ ap.add_argument("--sk", type=lambda v: [int(x) for x in v.split(",") if x], defa
 ap.add_argument("--force-splits", type=lambda v: [int(x) for x in v.split(",") if x], default=[])
 args = ap.parse_args()
 
-eng = Engine("small", dtype="bf16", seed=0, kv_pages=8, max_rows=64)
+eng = Engine("7b_2layer", dtype="bf16", seed=0, kv_pages=8, max_rows=64)  # 7B-sized split-K planes
 stream = torch.cuda.ExternalStream(eng.stream_handle())
 shapes = {"qkv": (12288, 4096), "o": (4096, 4096), "gate_up": (22016, 4096), "down": (4096, 11008)}
 
