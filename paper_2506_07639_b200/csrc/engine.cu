@@ -2031,6 +2031,9 @@ int fe_set_option(fe_engine* e, const char* key, int64_t value) {
     } else if (k == "tc_split") {
       fe::g_pair_split = (int)value;
       clear_graphs(e);
+    } else if (k == "tc_maxp") {
+      fe::g_pair_maxp = (int)value;
+      clear_graphs(e);
     } else if (k == "tc_sk") {
       fe::g_pair_sk = (int)value;
       clear_graphs(e);

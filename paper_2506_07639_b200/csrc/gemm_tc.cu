@@ -1396,6 +1396,7 @@ void launch_gemm_tc_v1(const TmaMap& a_map, const TmaMap& b_map, const TcLaunch&
 
 int g_pair_bn = 0;  // engine option "tc_bn": force the pair tile width (0: 256 where it divides)
 int g_pair_split = 1;  // engine option "tc_split": split-K for decode-width batches
+int g_pair_maxp = 0;  // engine option "tc_maxp": cap on the pairs of a launch (measurement only)
 int g_pair_sk = 0;  // engine option "tc_sk": stream-K the last waves (measured slower: the 256 x 256 fp32
                     // partials cost more than the wave tail they remove, profiles/r2_gemm_pair_sk.txt)
 
@@ -1434,7 +1435,7 @@ bool launch_gemm_tc(const TmaMap& a_map, const TmaMap& b_map64, const TcLaunch& 
   p.n_tiles = cols / bn;
   p.kblocks = l.K / BK;
   const int tiles = p.m_tiles * p.n_tiles;
-  const int P = std::min(tiles * p.kblocks, std::min(n_sm / 2, kPairMaxPairs));
+  const int P = std::min(tiles * p.kblocks, std::min(g_pair_maxp > 0 ? g_pair_maxp : n_sm / 2, kPairMaxPairs));
   // DP for all but the last one-to-two waves, which are stream-K'd (no wave tail)
   // split-K when the tiles do not fill the pairs (decode-width batches, O and
   // down projections): the split count minimising waves x k-blocks per unit

@@ -71,6 +71,7 @@ bool launch_gemm_tc(const TmaMap& a_map, const TmaMap& b_map64, const TcLaunch& 
 void launch_gemm_tc_v1(const TmaMap& a_map, const TmaMap& b_map, const TcLaunch& l, cudaStream_t s);
 extern int g_pair_bn;
 extern int g_pair_sk;
+extern int g_pair_maxp;
 extern int g_pair_split;
 size_t pair_sk_scratch_floats();
 int pair_sk_counters();
