@@ -124,7 +124,7 @@ constexpr int kThreads = 32 * (kSoftWarps + 1);
 // diagnostics (option "pattn_trace"): clock64 stamps of head 0's CTAs, 512 per tile
 #define PT_STAMP(slot) \
   do {                                                                                   \
-    if (trace && blockIdx.y == 0 && (slot) < 512) trace[blockIdx.x * 512 + (slot)] = clock64(); \
+    if (trace && h == 0 && (slot) < 512) trace[tix * 512 + (slot)] = clock64(); \
   } while (0)
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
@@ -171,7 +171,11 @@ prefill_attn_tc_kernel(const __grid_constant__ CUtensorMap pool_map, const Prefi
 
   pdl_trigger();
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int h = blockIdx.y;
+  // 1-D grid in block-launch order heaviest tile first across all heads:
+  // block b -> tile n_tiles - 1 - b / H, head b % H (a tile's pages grow with
+  // its position, so the blocks left for a second wave are the short ones)
+  const int n_tiles = gridDim.x / H;
+  const int h = blockIdx.x % H, tix = blockIdx.x / H;
   if (warp == kIssuer) {
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(&pool_map) : "memory");
@@ -191,9 +195,7 @@ prefill_attn_tc_kernel(const __grid_constant__ CUtensorMap pool_map, const Prefi
   }
   if (tid == 0) PT_STAMP(0);
   pdl_wait();  // q and the K/V of this forward's rows come from the QKV GEMM
-  // heaviest tiles first: a tile's pages grow with its position, so the CTAs
-  // that spill into a second wave are the short ones
-  const PrefillTile tile = tiles[gridDim.x - 1 - blockIdx.x];
+  const PrefillTile tile = tiles[n_tiles - 1 - tix];
   const int32_t* pages = ptab + tile.pages;
   const int pos0 = tile.pos0, n_rows = tile.n;
   const int n_pages = (pos0 + n_rows - 1) / FE_PAGE + 1;
@@ -419,7 +421,7 @@ void launch_prefill_attention_tc(const Fwd& f, const ModelDims& m, const TmaMap&
     cudaFuncSetAttribute(prefill_attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     configured = true;
   }
-  launch_k(prefill_attn_tc_kernel, dim3(f.n_ptiles, m.H), dim3(kThreads), (size_t)kSmem, s,
+  launch_k(prefill_attn_tc_kernel, dim3(f.n_ptiles * m.H), dim3(kThreads), (size_t)kSmem, s,
            *reinterpret_cast<const CUtensorMap*>(pool_map.bytes), f.ptiles, f.ptab, q, m.L, layer, m.H, m.d,
            m.attn_scale * 1.4426950408889634f, (__nv_bfloat16*)out, trace);
 }
