@@ -4,11 +4,13 @@ JSON outputs).
 
     python tests/golden/make_golden.py            # all fixtures
     python tests/golden/make_golden.py --quick    # skip the 7b_2layer requests
+    python tests/golden/make_golden.py --traces   # traces_tiny.json only
 
 Fixtures:
   traces_tiny.json      golden ECoT traces: the reference's own runners
-                        (SequentialRunner, ParallelSyncRunner, ParallelAsyncRunner;
-                        schedulers.py:363-552) over the CPU oracle model (`tiny`,
+                        (SequentialRunner, ParallelSyncRunner, ParallelAsyncRunner,
+                        KStepRunner, TwoTrackRunner; schedulers.py:363-716) over
+                        the CPU oracle model (`tiny`,
                         fp32), BASELINE config 1: T=10, seed 0, default schema and
                         profile, 8 slots.  Lines are `trace_content_bytes`.
   requests_<cfg>.json   per-request greedy tokens of the oracle model for
@@ -44,7 +46,7 @@ def golden_traces(T: int = 10) -> dict:
     schema = rt.default_schema()
     model = OracleModel("tiny", seed=0)
     out = {"config": "tiny", "seed": 0, "T": T, "slots": 8, "modes": {}}
-    for mode in ("sequential", "parallel_sync", "parallel_async"):
+    for mode in ("sequential", "parallel_sync", "parallel_async", "k_step", "two_track"):
         backend = OracleBackend("tiny", seed=0, model=model)
         cfg = rs.SchedulerConfig(mode=mode, slots=8)
         results, summary = rs.run_episode(cfg, T, backend, schema, seed=0)
@@ -82,9 +84,12 @@ def golden_requests(config: str, n_out: int, cases: int) -> dict:
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--traces", action="store_true")
     args = ap.parse_args()
     (HERE / "traces_tiny.json").write_text(json.dumps(golden_traces()))
     print("traces_tiny.json", file=sys.stderr)
+    if args.traces:
+        return
     (HERE / "requests_small.json").write_text(json.dumps(golden_requests("small", 12, 4)))
     if not args.quick:
         (HERE / "requests_7b_2layer.json").write_text(json.dumps(golden_requests("7b_2layer", 6, 2)))

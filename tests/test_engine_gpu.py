@@ -153,12 +153,14 @@ def test_fork_cow_branch_equals_fresh_sequence(tiny_f32, oracle_tiny):
     assert eng.stats()["pages_used"] == 0
 
 
-@pytest.mark.parametrize("mode", ["sequential", "parallel_sync", "parallel_async"])
+@pytest.mark.parametrize("mode", ["sequential", "parallel_sync", "parallel_async", "k_step", "two_track"])
 def test_traces_byte_identical_to_reference_golden(schema, golden_traces, mode):
     """BASELINE config 1: the reference's own `run_episode` / runners over
     `EngineBackend` (parallel_async through the registered device-engine
-    runner): trace bytes, simulated latency, staleness and accounting equal
-    the reference runners over the CPU oracle."""
+    runner; k_step / two_track are the stock reference runners driving the
+    engine through the GenerationBackend protocol):
+    trace bytes, simulated latency, staleness and accounting equal the
+    reference runners over the CPU oracle."""
     g = golden_traces["modes"][mode]
     be = EngineBackend("tiny", dtype="f32", seed=0, kv_pages=1024)
     try:

@@ -114,7 +114,7 @@ def test_reference_runners_over_oracle_reproduce_golden(schema, golden_traces):
 
     from oracle.backend import OracleBackend, OracleModel
     model = OracleModel("tiny", seed=0)
-    for mode in ("sequential", "parallel_sync", "parallel_async"):
+    for mode in ("sequential", "parallel_sync", "parallel_async", "k_step", "two_track"):
         g = golden_traces["modes"][mode]
         cfg = ecot_sched.SchedulerConfig(mode=mode, slots=8)
         res, _ = ecot_sched.run_episode(cfg, golden_traces["T"], OracleBackend("tiny", seed=0, model=model),
