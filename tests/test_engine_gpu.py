@@ -153,6 +153,60 @@ def test_fork_cow_branch_equals_fresh_sequence(tiny_f32, oracle_tiny):
     assert eng.stats()["pages_used"] == 0
 
 
+@pytest.mark.parametrize("config,dtype", [("tiny", "f32"), ("tiny", "bf16"), ("small", "bf16")])
+def test_kv_exhaustion_mid_decode_is_atomic(oracle_tiny, config, dtype):
+    """A decode tick whose rows cross a page boundary when the pool cannot
+    supply the pages raises EngineError without advancing anything (forward()
+    validates and counts every page before it commits, engine.cu pass 1);
+    once pages are returned, the same requests resume and their tokens equal an
+    uninterrupted decode -- bit-exact vs the CPU oracle in fp32, vs a fresh
+    engine with enough pages in bf16 (`small` bf16 runs the persistent tick
+    kernel)."""
+    from oracle.backend import frame
+    ids = frame(config, list(range(16)), list(range(1000, 1040)), "plan")
+    firsts = (ids[-1], M.TAG_BASE + 3)
+    trunk_len = len(ids) - 1
+    boundary = (trunk_len // 64 + 1) * 64   # both branches need a new page at this position
+    n_out = boundary - trunk_len + 15
+
+    def run(pages, squeeze):
+        eng = Engine(config, dtype=dtype, seed=0, kv_pages=pages)
+        try:
+            trunk = eng.seq_create()
+            eng.prefill(trunk, ids[:-1], 77, M.VIS_ID)
+            branches = [eng.seq_fork(trunk, trunk_len) for _ in firsts]
+            ballast = eng.seq_create()                                    # fills the pool up to one free page
+            k = pages - eng.stats()["pages_used"] - 1 if squeeze else 1
+            eng.prefill(ballast, [M.BOS_ID] + list(range(100, 100 + 64 * k - 1)), 78, M.VIS_ID)
+            reqs = [eng.submit(b, f, n_out, 1) for b, f in zip(branches, firsts)]
+            if squeeze:
+                assert eng.stats()["pages_used"] == pages - 1             # one page free, two needed
+                with pytest.raises(EngineError, match="KV pool exhausted"):
+                    eng.run(-1)
+                assert eng.in_flight() == 2                               # nothing completed, nothing lost
+                for b in branches:
+                    assert eng.seq_len(b) == boundary                     # rolled back to before the failed tick
+                eng.seq_free(ballast)                                     # pages come back
+            eng.run(-1)
+            out = [eng.request_tokens(r, n_out) for r in reqs]
+            for r in reqs:
+                eng.request_release(r)
+            for s in branches + [trunk] + ([] if squeeze else [ballast]):
+                eng.seq_free(s)
+            assert eng.stats()["pages_used"] == 0
+            return out
+        finally:
+            eng.close()
+
+    got = run(12, True)
+    if dtype == "f32":
+        for f, toks in zip(firsts, got):
+            want, _ = oracle_tiny.generate(ids[:-1] + [f], 77, n_out)
+            assert toks == want
+    else:
+        assert got == run(64, False)
+
+
 @pytest.mark.parametrize("mode", ["sequential", "parallel_sync", "parallel_async", "k_step", "two_track"])
 def test_traces_byte_identical_to_reference_golden(schema, golden_traces, mode):
     """BASELINE config 1: the reference's own `run_episode` / runners over
