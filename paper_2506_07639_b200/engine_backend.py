@@ -186,6 +186,7 @@ class EngineBackend:
             raise ValueError(f"async_mode must be 'lockstep' or 'background', got {async_mode!r}")
         self.async_mode = async_mode
         self.request_log = request_log
+        self._owns_engine = engine is None   # a passed-in engine may be shared: close() leaves it open
         self.engine = engine or Engine(self.cfg, dtype=dtype, device=device, seed=seed, **engine_kw)
         self.profile = profile or default_profile(seed)
         self._trunks: list[_Trunk] = []
@@ -570,9 +571,15 @@ class EngineBackend:
         return occupancy
 
     def close(self) -> None:
+        """Stop this backend's async engines; close the device engine if this
+        backend created it.  A shared engine (passed in) stays open for its
+        other users; requests this backend still has in flight on it must be
+        drained by the caller first (`make_async_engine(...).drain()`), since
+        the engine completes requests in batches across backends."""
         for eng in list(self._async_engines):
             eng.close()
-        self.engine.close()
+        if self._owns_engine:
+            self.engine.close()
 
 
 def _device_priority(priority: str) -> int:

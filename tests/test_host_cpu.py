@@ -12,7 +12,7 @@ import time
 
 import numpy as np
 import pytest
-from fake_engine import HashBackend, fake_backend
+from fake_engine import FakeEngine, HashBackend, fake_backend
 
 import ecot_sched
 from ecot_sched import schedulers as RS
@@ -20,7 +20,7 @@ from ecot_sched.batching import LatencyModel
 from ecot_sched.trace import StepSchema, StepSpec, default_schema, trace_content_bytes
 from paper_2506_07639_b200 import BatchedEpisodes, EngineError, runners
 from paper_2506_07639_b200.backends import BackendError, StepProfile, SyntheticProfile, default_profile
-from paper_2506_07639_b200.engine_backend import DeviceTokens
+from paper_2506_07639_b200.engine_backend import DeviceTokens, EngineBackend
 
 HOT_MODES = ("sequential", "parallel_sync", "parallel_async")
 MODEL = LatencyModel(c_iter=10, c_slot=1, c_encode=20, c_decode=5)
@@ -391,3 +391,18 @@ def test_tag_in_prefill_is_exactly_greedy(mode):
         runs[tag] = (lines(res, schema), len(eng.occupancy_log))
     assert runs[True][0] == runs[False][0]
     assert runs[True][1] < runs[False][1]
+
+
+def test_close_leaves_a_shared_engine_open():
+    """A backend built over a passed-in engine does not close it (another
+    backend may share it); a backend that created its engine closes it."""
+    class CountingEngine(FakeEngine):
+        closed = 0
+
+        def close(self):
+            CountingEngine.closed += 1
+
+    eng = CountingEngine()
+    be = EngineBackend("tiny", engine=eng)
+    be.close()
+    assert CountingEngine.closed == 0
