@@ -888,3 +888,40 @@ def test_tag_in_prefill_reproduces_reference_golden(schema, golden_traces, mode)
         assert [trace_content_bytes(r.trace, schema).decode() for r in res] == g["lines"]
     finally:
         be.close()
+
+
+# ------------------------------------------------ full-size properties ----
+def test_7b_tick_decode_is_batch_invariant():
+    """Full 7B shape, bf16, the benchmarked persistent tick kernel: a branch's
+    greedy tokens and fp32 logits do not depend on which other branches share
+    its decode ticks (1 row vs 7 rows vs 16 rows: bit-identical).  Every
+    batch column of the swap-AB MMAs, every attention row and the fixed
+    split-K chunk order are row-independent -- a size-independent property
+    checked at BASELINE config 2's shapes (625-token trunk, 256 VIS rows)."""
+    cfg = M.get_config("7b")
+    ids = [M.BOS_ID] + [M.VIS_ID] * cfg.n_vision + list(range(100, 100 + 625 - 1 - cfg.n_vision))
+    eng = Engine("7b", dtype="bf16", seed=0, kv_pages=256, max_rows=1024)
+    try:
+        trunk = eng.seq_create()
+        eng.prefill(trunk, ids, 7, M.VIS_ID)
+        out = {}
+        for n in (1, 7, 16):
+            seqs, reqs = [], []
+            for j in range(n):
+                b = eng.seq_fork(trunk, len(ids) - 40 * (j % 8))
+                seqs.append(b)
+                r = eng.submit(b, M.TAG_BASE + j, 6, 1)
+                eng.capture_logits(r)
+                reqs.append(r)
+            eng.set_slots(max(8, n))
+            eng.run(-1)
+            out[n] = (eng.request_tokens(reqs[0], 6), eng.request_logits(reqs[0], 6))
+            for r in reqs:
+                eng.request_release(r)
+            for s in seqs:
+                eng.seq_free(s)
+        for n in (7, 16):
+            assert out[n][0] == out[1][0], n
+            assert np.array_equal(out[n][1], out[1][1]), n
+    finally:
+        eng.close()
