@@ -241,6 +241,10 @@ struct fe_engine {
   bool mk_ev_used[kLanes] = {};
   int mk_pf_stages = 0;  // 0 = the whole ring
   int mk_per_cta = 4, mk_nc_cap = 8, mk_nc_cap_o = 0;  // chunk plans (mk_make_plans; swept in tools/mk_sweep.sh)
+  // per-GEMM chunks per tile (options "mk_nc_qkv" ... "mk_nc_lm"; 0 = the per_cta / cap plan).  QKV and
+  // gate/up at 6: measured on the B200 with tools/decode_probe.py (7B, 7 rows: 3.19 -> 3.14-3.16 ms per
+  // tick); lm_head 4 / 7, O 4 and down 7 / 9 measured neutral or slower
+  int mk_nc_force[5] = {6, 0, 6, 0, 0};
   bool graphs_on = true;
   bool lane1_yields = true;
   int lane0_pace = 0;  // option "lane0_pace": lane-0 ticks kept queued (1 or 2; 0: unpaced)
@@ -433,6 +437,13 @@ void mk_make_plans(fe_engine* e) {
   e->mk_plans[fe::MK_GU] = fe::mk_plan(m.F / 64, m.d / 64, G, pc, cap);
   e->mk_plans[fe::MK_DOWN] = fe::mk_plan(m.d / 128, m.F / 64, G, pc, cap);
   e->mk_plans[fe::MK_LM] = fe::mk_plan((m.V + 127) / 128, m.d / 64, G, pc, cap);
+  for (int i = 0; i < 5; i++) {
+    fe::MkPlan& p = e->mk_plans[i];
+    if (e->mk_nc_force[i] > 0) {
+      p.nc = std::max(1, std::min({e->mk_nc_force[i], 16, std::max(1, p.kb_total / 4)}));
+      p.chunks = p.tiles * p.nc;
+    }
+  }
 }
 
 // ---- forward pass -----------------------------------------------------------
@@ -2012,8 +2023,13 @@ int fe_set_option(fe_engine* e, const char* key, int64_t value) {
     } else if (k == "mk_pf") {
       e->mk_pf_stages = (int)value;
       clear_graphs(e);
-    } else if (k == "mk_per_cta" || k == "mk_nc_cap" || k == "mk_nc_cap_o") {
-      (k == "mk_per_cta" ? e->mk_per_cta : k == "mk_nc_cap" ? e->mk_nc_cap : e->mk_nc_cap_o) = (int)value;
+    } else if (k == "mk_per_cta" || k == "mk_nc_cap" || k == "mk_nc_cap_o" || k == "mk_nc_qkv" || k == "mk_nc_o" ||
+               k == "mk_nc_gu" || k == "mk_nc_down" || k == "mk_nc_lm") {
+      int* slot = k == "mk_per_cta" ? &e->mk_per_cta : k == "mk_nc_cap" ? &e->mk_nc_cap
+                  : k == "mk_nc_cap_o" ? &e->mk_nc_cap_o : k == "mk_nc_qkv" ? &e->mk_nc_force[fe::MK_QKV]
+                  : k == "mk_nc_o" ? &e->mk_nc_force[fe::MK_O] : k == "mk_nc_gu" ? &e->mk_nc_force[fe::MK_GU]
+                  : k == "mk_nc_down" ? &e->mk_nc_force[fe::MK_DOWN] : &e->mk_nc_force[fe::MK_LM];
+      *slot = (int)value;
       if (e->mk_on) mk_make_plans(e);
       clear_graphs(e);
     } else if (k == "span_attn") {
