@@ -922,18 +922,18 @@ __device__ __noinline__ void finalize_tile(const Args& a, unsigned char* smem, i
 #pragma unroll
   for (int q4 = 0; q4 < XR / 4; q4++) acc4[q4] = make_float4(0.f, 0.f, 0.f, 0.f);
   const size_t q0 = (size_t)tl * p.nc;
-  if (B <= 8 && p.nc <= 8) {  // every chunk's 2 float4 requested together (straight-line registers)
+  if (B <= 8 && p.nc <= 12) {  // every chunk's 2 float4 requested together (straight-line registers)
     const float4* src = reinterpret_cast<const float4*>(a.partial) + q0 * (XR / 4) * MT + r;
     const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
     const int nc = p.nc;
     const bool two = B > 4;
 #define MK_P(u) const float4 pa##u = u < nc ? __ldcg(src + (size_t)(u) * (XR / 4) * MT) : z; \
           const float4 pb##u = (u < nc && two) ? __ldcg(src + (size_t)(u) * (XR / 4) * MT + MT) : z;
-    MK_P(0) MK_P(1) MK_P(2) MK_P(3) MK_P(4) MK_P(5) MK_P(6) MK_P(7)
+    MK_P(0) MK_P(1) MK_P(2) MK_P(3) MK_P(4) MK_P(5) MK_P(6) MK_P(7) MK_P(8) MK_P(9) MK_P(10) MK_P(11)
 #undef MK_P
 #define MK_S(u) acc4[0].x += pa##u.x; acc4[0].y += pa##u.y; acc4[0].z += pa##u.z; acc4[0].w += pa##u.w; \
           acc4[1].x += pb##u.x; acc4[1].y += pb##u.y; acc4[1].z += pb##u.z; acc4[1].w += pb##u.w;
-    MK_S(0) MK_S(1) MK_S(2) MK_S(3) MK_S(4) MK_S(5) MK_S(6) MK_S(7)
+    MK_S(0) MK_S(1) MK_S(2) MK_S(3) MK_S(4) MK_S(5) MK_S(6) MK_S(7) MK_S(8) MK_S(9) MK_S(10) MK_S(11)
 #undef MK_S
   } else {
     for (int c0 = 0; c0 < p.nc; c0 += 4) {

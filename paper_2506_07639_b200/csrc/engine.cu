@@ -241,10 +241,10 @@ struct fe_engine {
   bool mk_ev_used[kLanes] = {};
   int mk_pf_stages = 0;  // 0 = the whole ring
   int mk_per_cta = 4, mk_nc_cap = 8, mk_nc_cap_o = 0;  // chunk plans (mk_make_plans; swept in tools/mk_sweep.sh)
-  // per-GEMM chunks per tile (options "mk_nc_qkv" ... "mk_nc_lm"; 0 = the per_cta / cap plan).  QKV and
-  // gate/up at 6: measured on the B200 with tools/decode_probe.py (7B, 7 rows: 3.19 -> 3.14-3.16 ms per
-  // tick); lm_head 4 / 7, O 4 and down 7 / 9 measured neutral or slower
-  int mk_nc_force[5] = {6, 0, 6, 0, 0};
+  // per-GEMM chunks per tile (options "mk_nc_qkv" ... "mk_nc_lm"; 0 = the per_cta / cap plan), measured
+  // on the B200 (bench config 2, decode tick): QKV and gate/up at 6 (3.062 -> 2.993 ms), down at 9 with
+  // the 12-partial straight-line reduction (2.993 -> 2.969 ms); O and lm_head keep their plan
+  int mk_nc_force[5] = {6, 0, 6, 9, 0};
   bool graphs_on = true;
   bool lane1_yields = true;
   int lane0_pace = 0;  // option "lane0_pace": lane-0 ticks kept queued (1 or 2; 0: unpaced)
