@@ -57,7 +57,7 @@ def parse():
     ap.add_argument("--episodes", type=int, default=None,
                     help="total episodes (config 4; default 1 on one GPU, 64 on several): sharded over "
                          "ranks, each rank's shard batched per timestep")
-    ap.add_argument("--seq-steps", type=int, default=4)
+    ap.add_argument("--seq-steps", type=int, default=10)
     ap.add_argument("--max-rows", type=int, default=4096,
                     help="engine rows per forward (a batched trunk prefill packs this many rows per GEMM pass)")
     ap.add_argument("--async-steps", type=int, default=50)
